@@ -1,0 +1,135 @@
+/*
+ * pfb.h -- C ABI of libpfb, the sm_100a kernel library behind the pfor
+ * executor.  Plain pointers, sizes and POD descriptors only (no torch types),
+ * so any host (Python ctypes, C++, a cgo/JNI shim) can bind it.
+ *
+ * Boundary replaced (reference /root/reference/pkg/src/pforvec):
+ *   interp.py:161-236  Executor._eval_plain  -- the kind -> kernel dispatch;
+ *   each entry point below replaces the NumPy kernel cited beside it.
+ *
+ * Conventions
+ *   - Every function enqueues work on `stream` (a cudaStream_t, passed as
+ *     void*) and returns immediately; 0 = launched, >0 = PFB_E_* (host-side
+ *     validation failed, nothing launched), <0 = -(cudaError_t) on launch.
+ *   - Outputs are allocated by the caller (the executor knows every shape on
+ *     the host); kernels never allocate, except where a workspace pointer is
+ *     an explicit argument.
+ *   - Inputs may be strided views (stride 0 = broadcast of a loop-invariant
+ *     operand); outputs are dense row-major unless stated.
+ *   - Errors only detectable on the device (index out of bounds, scatter
+ *     collision / incomplete cover) are OR-ed into `*dev_err` (a device int32)
+ *     as PFB_DEV_* bits; the host reads it at its next sync and raises the
+ *     reference's exception class (errors.py IndexOutOfBounds etc.).
+ *   - Float storage is fp32, integers int64, bool one byte (0/1).
+ */
+#ifndef PFB_H_
+#define PFB_H_
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define PFB_MAX_RANK 8
+
+enum pfb_dtype { PFB_F32 = 0, PFB_I64 = 1, PFB_BOOL = 2 };
+
+typedef struct pfb_tensor {
+  void* data;                      /* device pointer to element [0,...,0] */
+  int32_t dtype;                   /* pfb_dtype */
+  int32_t rank;                    /* 0..PFB_MAX_RANK */
+  int64_t shape[PFB_MAX_RANK];
+  int64_t stride[PFB_MAX_RANK];    /* in elements; 0 broadcasts */
+} pfb_tensor;
+
+enum pfb_status {
+  PFB_OK = 0,
+  PFB_E_DTYPE = 1,      /* -> DTypeMismatch */
+  PFB_E_SHAPE = 2,      /* -> IncompatibleShapes */
+  PFB_E_RANK = 3,       /* -> RankError */
+  PFB_E_ARG = 4,        /* -> ValueError (unknown op code, bad attr) */
+  PFB_E_UNSUPPORTED = 5 /* layout the kernel cannot take; caller materialises */
+};
+
+enum pfb_dev_err {
+  PFB_DEV_OOB = 1,        /* -> IndexOutOfBounds */
+  PFB_DEV_COLLISION = 2,  /* -> IndexCollision */
+  PFB_DEV_COVER = 4       /* -> IncompleteCover */
+};
+
+/* op codes: same order as reference tensor.py:124-126 */
+enum pfb_binary_op { PFB_ADD, PFB_SUB, PFB_MUL, PFB_DIV, PFB_MAX, PFB_MIN, PFB_LESS, PFB_EQUAL };
+enum pfb_unary_op { PFB_NEG, PFB_EXP, PFB_LOG, PFB_RELU, PFB_TANH, PFB_SIGMOID, PFB_SQUARE,
+                    PFB_LOGICAL_NOT };
+
+/* library / device info */
+int pfb_version(void);
+int pfb_device_sm_count(void);
+
+/* elementwise (reference tensor.py:140-188): numpy broadcasting via strides */
+int pfb_binary(int32_t op, const pfb_tensor* a, const pfb_tensor* b, pfb_tensor* out,
+               void* stream);
+int pfb_unary(int32_t op, const pfb_tensor* x, pfb_tensor* out, void* stream);
+int pfb_cast(const pfb_tensor* x, pfb_tensor* out, void* stream);
+
+/* fused elementwise program: up to 8 inputs, a register program of binary /
+ * unary / cast steps (see csrc/fused_ew.cu for the encoding); one launch for
+ * a chain the reference runs as separate NumPy calls. */
+int pfb_fused_ew(int32_t n_in, const pfb_tensor* ins, int32_t n_steps, const int32_t* program,
+                 pfb_tensor* out, void* stream);
+
+/* reduce_sum over axes given as a bitmask (reference tensor.py:279-283) */
+int pfb_reduce_sum(const pfb_tensor* x, uint32_t axes_mask, pfb_tensor* out, void* ws,
+                   int64_t ws_bytes, void* stream);
+
+/* strided copy: out (any strides) <- x (any strides, same shape).  Backs
+ * transpose / concat / stack / tile_leading / slice_leading materialisation
+ * (reference tensor.py:286-303, 383-416). */
+int pfb_copy(const pfb_tensor* x, pfb_tensor* out, void* stream);
+int pfb_fill(pfb_tensor* out, double value, void* stream);
+
+/* matmul (reference tensor.py:195-206): rank-2 x rank-2 or batched rank-3;
+ * operands may be strided views.  fp32-accurate: tcgen05 kind::tf32 with a
+ * 3xTF32 split for large shapes, SIMT fp32 for small/odd ones.
+ * `alpha_rows` (nullable, fp32, one per output row) scales each output row in
+ * the epilogue; `accumulate` adds into `out` instead of overwriting. */
+int pfb_matmul(const pfb_tensor* a, const pfb_tensor* b, pfb_tensor* out, void* stream);
+int pfb_matmul_ex(const pfb_tensor* a, const pfb_tensor* b, pfb_tensor* out,
+                  const float* alpha_rows, int32_t accumulate, int32_t force_path, void* stream);
+
+/* conv family (reference tensor.py:209-260), NHWC / HWIO, SAME, stride 1 */
+int pfb_im2col(const pfb_tensor* x, int32_t k1, int32_t k2, pfb_tensor* out, void* stream);
+int pfb_conv2d(const pfb_tensor* x, const pfb_tensor* f, pfb_tensor* out, void* stream);
+int pfb_conv2d_input_grad(const pfb_tensor* gy, const pfb_tensor* f, pfb_tensor* out,
+                          void* stream);
+
+/* indexing (reference tensor.py:306-360, interp.py:210-221) */
+int pfb_gather_rows(const pfb_tensor* x, const pfb_tensor* idx, pfb_tensor* out,
+                    int32_t* dev_err, void* stream);
+int pfb_scatter_rows(int32_t n_parts, const pfb_tensor* index_sets, const pfb_tensor* parts,
+                     int64_t total, pfb_tensor* out, int32_t* ws_count, int32_t* dev_err,
+                     void* stream);
+int pfb_scatter_add_rows(const pfb_tensor* idx, const pfb_tensor* updates, int64_t total,
+                         pfb_tensor* out, int32_t* dev_err, void* stream);
+/* where_true: out has room for n indices; *dev_count receives the count */
+int pfb_where_true(const pfb_tensor* mask, pfb_tensor* out, int64_t* dev_count, void* ws,
+                   int64_t ws_bytes, void* stream);
+/* complement: sorted [0,total) \ idx; out has room for total entries */
+int pfb_complement(const pfb_tensor* idx, int64_t total, pfb_tensor* out, int64_t* dev_count,
+                   void* ws, int64_t ws_bytes, void* stream);
+int pfb_iota(pfb_tensor* out, int64_t start, void* stream);
+
+/* counter-based uniform stream (reference interp.py:52-82), splitmix64 */
+int pfb_rng_uniform(uint64_t seed, uint64_t counter, pfb_tensor* out, void* stream);
+
+/* fused per-example gradient statistics: for rank-1
+ * per-example gradients g_i = a_i (x) b_i of one weight matrix,
+ * sq_norm[i] += |a_i|^2 |b_i|^2 without materialising g. */
+int pfb_outer_sq_norm(const pfb_tensor* a, const pfb_tensor* b, pfb_tensor* sq_norm,
+                      void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* PFB_H_ */

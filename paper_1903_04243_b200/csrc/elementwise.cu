@@ -1,0 +1,476 @@
+// Elementwise family: binary / unary / cast / strided copy / fill / fused
+// programs.  Replaces reference tensor.py:104-188 and the layout copies of
+// tensor.py:286-416.
+//
+// Loop-invariant operands arrive as stride-0 views (no materialised tile),
+// so e.g. [320,32,256] * [32,256] reads the invariant once per row from L2.
+// HBM-bound: 128-bit loads/stores on the inner dim whenever the operand is
+// unit-stride and 16-byte aligned; index math in 32 bits when it fits.
+#include "common.cuh"
+
+namespace pfb {
+
+// ----------------------------------------------------------------------------
+// scalar op semantics (numpy-compatible)
+
+template <int OP>
+__device__ __forceinline__ float bin_f32(float a, float b) {
+  if (OP == PFB_ADD) return a + b;
+  if (OP == PFB_SUB) return a - b;
+  if (OP == PFB_MUL) return a * b;
+  if (OP == PFB_DIV) return a / b;           // IEEE: x/0 -> inf, 0/0 -> nan
+  if (OP == PFB_MAX) return np_max(a, b);
+  if (OP == PFB_MIN) return np_min(a, b);
+  if (OP == PFB_LESS) return a < b ? 1.f : 0.f;
+  return a == b ? 1.f : 0.f;
+}
+
+template <int OP>
+__device__ __forceinline__ int64_t bin_i64(int64_t a, int64_t b) {
+  // two's-complement wraparound like numpy int64
+  uint64_t ua = (uint64_t)a, ub = (uint64_t)b;
+  if (OP == PFB_ADD) return (int64_t)(ua + ub);
+  if (OP == PFB_SUB) return (int64_t)(ua - ub);
+  if (OP == PFB_MUL) return (int64_t)(ua * ub);
+  if (OP == PFB_MAX) return a >= b ? a : b;
+  if (OP == PFB_MIN) return a <= b ? a : b;
+  if (OP == PFB_LESS) return a < b;
+  return a == b;
+}
+
+template <int OP>
+__device__ __forceinline__ float un_f32(float x) {
+  if (OP == PFB_NEG) return -x;
+  if (OP == PFB_EXP) return expf(x);
+  if (OP == PFB_LOG) return logf(x);
+  if (OP == PFB_RELU) return np_max(x, 0.f);
+  if (OP == PFB_TANH) return tanhf(x);
+  if (OP == PFB_SIGMOID) return 1.f / (1.f + expf(-x));
+  if (OP == PFB_SQUARE) return x * x;
+  return x == 0.f ? 1.f : 0.f;  // logical_not on 0/1 floats (fused programs)
+}
+
+template <int OP>
+__device__ __forceinline__ int64_t un_i64(int64_t x) {
+  if (OP == PFB_NEG) return (int64_t)(0ull - (uint64_t)x);
+  if (OP == PFB_RELU) return x > 0 ? x : 0;
+  return (int64_t)((uint64_t)x * (uint64_t)x);  // square
+}
+
+// Functors (Tin -> Tout), one template parameter per op so every op
+// compiles to straight-line code.
+template <int OP, bool CMP> struct BinF32 {
+  __device__ __forceinline__ auto operator()(float a, float b) const {
+    if constexpr (CMP) return (uint8_t)(bin_f32<OP>(a, b) != 0.f);
+    else return bin_f32<OP>(a, b);
+  }
+};
+template <int OP, bool CMP> struct BinI64 {
+  __device__ __forceinline__ auto operator()(int64_t a, int64_t b) const {
+    if constexpr (CMP) return (uint8_t)bin_i64<OP>(a, b);
+    else return bin_i64<OP>(a, b);
+  }
+};
+template <int OP> struct BinBool {
+  __device__ __forceinline__ uint8_t operator()(uint8_t a, uint8_t b) const {
+    return OP == PFB_LESS ? (uint8_t)(a < b) : (uint8_t)(a == b);
+  }
+};
+template <int OP> struct UnF32 {
+  __device__ __forceinline__ float operator()(float x, float) const { return un_f32<OP>(x); }
+};
+template <int OP> struct UnI64 {
+  __device__ __forceinline__ int64_t operator()(int64_t x, int64_t) const { return un_i64<OP>(x); }
+};
+struct NotBool {
+  __device__ __forceinline__ uint8_t operator()(uint8_t x, uint8_t) const { return x ? 0 : 1; }
+};
+template <typename Tin, typename Tout> struct Convert {
+  __device__ __forceinline__ Tout operator()(Tin x, Tin) const {
+    if constexpr (std::is_same<Tout, uint8_t>::value) return (uint8_t)(x != (Tin)0);
+    else if constexpr (std::is_same<Tin, float>::value && std::is_same<Tout, int64_t>::value) {
+      // truncation toward zero; numpy gives INT64_MIN for nan / out of range
+      if (!(x >= -9.2233720368547758e18f && x < 9.2233720368547758e18f)) return INT64_MIN;
+      return (int64_t)x;
+    } else return (Tout)x;
+  }
+};
+template <typename T> struct Identity {
+  __device__ __forceinline__ T operator()(T x, T) const { return x; }
+};
+
+// ----------------------------------------------------------------------------
+// vector helpers: 4 consecutive elements along the inner dim
+
+template <typename T>
+__device__ __forceinline__ void load4(const T* p, int64_t st, bool vec, T* v) {
+  if (st == 0) {
+    T x = __ldg(p);
+    v[0] = v[1] = v[2] = v[3] = x;
+  } else if (vec) {
+    if constexpr (sizeof(T) == 4) {
+      float4 t = __ldg(reinterpret_cast<const float4*>(p));
+      const T* q = reinterpret_cast<const T*>(&t);
+      v[0] = q[0]; v[1] = q[1]; v[2] = q[2]; v[3] = q[3];
+    } else if constexpr (sizeof(T) == 8) {
+      const longlong2* w = reinterpret_cast<const longlong2*>(p);
+      longlong2 t0 = __ldg(w), t1 = __ldg(w + 1);
+      v[0] = (T)t0.x; v[1] = (T)t0.y; v[2] = (T)t1.x; v[3] = (T)t1.y;
+    } else {
+      uchar4 t = __ldg(reinterpret_cast<const uchar4*>(p));
+      v[0] = (T)t.x; v[1] = (T)t.y; v[2] = (T)t.z; v[3] = (T)t.w;
+    }
+  } else {
+#pragma unroll
+    for (int k = 0; k < 4; ++k) v[k] = __ldg(p + k * st);
+  }
+}
+
+template <typename T>
+__device__ __forceinline__ void store4(T* p, int64_t st, bool vec, const T* v) {
+  if (vec) {
+    if constexpr (sizeof(T) == 4) {
+      float4 t;
+      T* q = reinterpret_cast<T*>(&t);
+      q[0] = v[0]; q[1] = v[1]; q[2] = v[2]; q[3] = v[3];
+      *reinterpret_cast<float4*>(p) = t;
+    } else if constexpr (sizeof(T) == 8) {
+      longlong2* w = reinterpret_cast<longlong2*>(p);
+      w[0] = make_longlong2((long long)v[0], (long long)v[1]);
+      w[1] = make_longlong2((long long)v[2], (long long)v[3]);
+    } else {
+      *reinterpret_cast<uchar4*>(p) = make_uchar4(v[0], v[1], v[2], v[3]);
+    }
+  } else {
+#pragma unroll
+    for (int k = 0; k < 4; ++k) p[k * st] = v[k];
+  }
+}
+
+// Grid-stride kernels.  Operand 0 of the layout is the output, 1..NIN inputs.
+template <typename Tin, typename Tout, typename F, typename IdxT, int NIN>
+__global__ void __launch_bounds__(256) ew_vec4_kernel(Layout L, IdxT nchunks, Tout* out,
+                                                      const Tin* a, const Tin* b, F f,
+                                                      unsigned vecmask) {
+  const int last = L.rank - 1;
+  const int64_t so = L.st[0][last], sa = L.st[1][last], sb = NIN > 1 ? L.st[2][last] : 0;
+  for (IdxT c = blockIdx.x * (IdxT)blockDim.x + threadIdx.x; c < nchunks;
+       c += (IdxT)gridDim.x * blockDim.x) {
+    int64_t off[NIN + 1];
+    offsets<IdxT, NIN + 1>(L, c * 4, off);
+    Tin x[4], y[4];
+    load4(a + off[1], sa, vecmask & 2u, x);
+    if (NIN > 1) load4(b + off[2], sb, vecmask & 4u, y);
+    Tout r[4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) r[k] = f(x[k], NIN > 1 ? y[k] : x[k]);
+    store4(out + off[0], so, vecmask & 1u, r);
+  }
+}
+
+template <typename Tin, typename Tout, typename F, typename IdxT, int NIN>
+__global__ void __launch_bounds__(256) ew_scalar_kernel(Layout L, IdxT n, Tout* out,
+                                                        const Tin* a, const Tin* b, F f) {
+  for (IdxT i = blockIdx.x * (IdxT)blockDim.x + threadIdx.x; i < n;
+       i += (IdxT)gridDim.x * blockDim.x) {
+    int64_t off[NIN + 1];
+    offsets<IdxT, NIN + 1>(L, i, off);
+    Tin x = a[off[1]];
+    out[off[0]] = f(x, NIN > 1 ? b[off[2]] : x);
+  }
+}
+
+// Host launcher: `L` over (out, a[, b]); picks the vector path when the inner
+// dim allows it.
+template <typename Tin, typename Tout, int NIN, typename F>
+int launch_ew(const Layout& L, void* out, const void* a, const void* b, F f, cudaStream_t s) {
+  int64_t n = 1;
+  for (int d = 0; d < L.rank; ++d) n *= L.shape[d];
+  if (n == 0) return 0;
+  const int last = L.rank - 1;
+  bool vec_dim = (L.shape[last] % 4) == 0;
+  unsigned vecmask = 0;
+  if (vec_dim) {
+    const void* ptrs[3] = {out, a, b};
+    for (int o = 0; o <= NIN; ++o) {
+      size_t esz = o == 0 ? sizeof(Tout) : sizeof(Tin);
+      bool ok = L.st[o][last] == 1 && ((uintptr_t)ptrs[o] % (4 * esz)) == 0;
+      for (int d = 0; d < last && ok; ++d) ok = (L.st[o][d] % 4) == 0;
+      if (ok) vecmask |= 1u << o;
+    }
+  }
+  const int block = 256;
+  bool small = n < (int64_t)0x7fffffff;
+  if (vec_dim) {
+    int64_t chunks = n / 4;
+    int grid = grid_for(chunks, block);
+    if (small)
+      ew_vec4_kernel<Tin, Tout, F, uint32_t, NIN><<<grid, block, 0, s>>>(
+          L, (uint32_t)chunks, (Tout*)out, (const Tin*)a, (const Tin*)b, f, vecmask);
+    else
+      ew_vec4_kernel<Tin, Tout, F, int64_t, NIN><<<grid, block, 0, s>>>(
+          L, chunks, (Tout*)out, (const Tin*)a, (const Tin*)b, f, vecmask);
+  } else {
+    int grid = grid_for(n, block);
+    if (small)
+      ew_scalar_kernel<Tin, Tout, F, uint32_t, NIN><<<grid, block, 0, s>>>(
+          L, (uint32_t)n, (Tout*)out, (const Tin*)a, (const Tin*)b, f);
+    else
+      ew_scalar_kernel<Tin, Tout, F, int64_t, NIN><<<grid, block, 0, s>>>(
+          L, n, (Tout*)out, (const Tin*)a, (const Tin*)b, f);
+  }
+  return launch_status();
+}
+
+// Build the (out, in...) layout with numpy broadcasting of inputs to out.
+inline int ew_layout(pfb_tensor* out, const pfb_tensor* a, const pfb_tensor* b, Layout* L) {
+  int64_t sa[kMaxRank], sb[kMaxRank];
+  if (!broadcast_strides(a, out->rank, out->shape, sa)) return PFB_E_SHAPE;
+  if (b && !broadcast_strides(b, out->rank, out->shape, sb)) return PFB_E_SHAPE;
+  const int64_t* st[3] = {out->stride, sa, sb};
+  *L = make_layout(out->rank, out->shape, b ? 3 : 2, st);
+  return 0;
+}
+
+template <int OP>
+int binary_dispatch(const pfb_tensor* a, const pfb_tensor* b, pfb_tensor* out, cudaStream_t s) {
+  Layout L;
+  if (int e = ew_layout(out, a, b, &L)) return e;
+  constexpr bool CMP = OP == PFB_LESS || OP == PFB_EQUAL;
+  switch (a->dtype) {
+    case PFB_F32:
+      if (out->dtype != (CMP ? PFB_BOOL : PFB_F32)) return PFB_E_DTYPE;
+      return launch_ew<float, typename std::conditional<CMP, uint8_t, float>::type, 2>(
+          L, out->data, a->data, b->data, BinF32<OP, CMP>{}, s);
+    case PFB_I64:
+      if (OP == PFB_DIV) return PFB_E_DTYPE;
+      if (out->dtype != (CMP ? PFB_BOOL : PFB_I64)) return PFB_E_DTYPE;
+      return launch_ew<int64_t, typename std::conditional<CMP, uint8_t, int64_t>::type, 2>(
+          L, out->data, a->data, b->data, BinI64<OP, CMP>{}, s);
+    default:
+      if (!CMP || out->dtype != PFB_BOOL) return PFB_E_DTYPE;
+      return launch_ew<uint8_t, uint8_t, 2>(L, out->data, a->data, b->data, BinBool<OP>{}, s);
+  }
+}
+
+template <int OP>
+int unary_dispatch(const pfb_tensor* x, pfb_tensor* out, cudaStream_t s) {
+  Layout L;
+  if (int e = ew_layout(out, x, nullptr, &L)) return e;
+  if (x->dtype != out->dtype) return PFB_E_DTYPE;
+  if (OP == PFB_LOGICAL_NOT) {
+    if (x->dtype != PFB_BOOL) return PFB_E_DTYPE;
+    return launch_ew<uint8_t, uint8_t, 1>(L, out->data, x->data, nullptr, NotBool{}, s);
+  }
+  if (x->dtype == PFB_F32)
+    return launch_ew<float, float, 1>(L, out->data, x->data, nullptr, UnF32<OP>{}, s);
+  if (x->dtype == PFB_I64 && (OP == PFB_NEG || OP == PFB_RELU || OP == PFB_SQUARE))
+    return launch_ew<int64_t, int64_t, 1>(L, out->data, x->data, nullptr, UnI64<OP>{}, s);
+  return PFB_E_DTYPE;
+}
+
+template <typename Tin>
+int cast_from(const Layout& L, const pfb_tensor* x, pfb_tensor* out, cudaStream_t s) {
+  switch (out->dtype) {
+    case PFB_F32:
+      return launch_ew<Tin, float, 1>(L, out->data, x->data, nullptr, Convert<Tin, float>{}, s);
+    case PFB_I64:
+      return launch_ew<Tin, int64_t, 1>(L, out->data, x->data, nullptr, Convert<Tin, int64_t>{}, s);
+    default:
+      return launch_ew<Tin, uint8_t, 1>(L, out->data, x->data, nullptr, Convert<Tin, uint8_t>{}, s);
+  }
+}
+
+// ----------------------------------------------------------------------------
+// fused elementwise programs (float registers; bool inputs read as 0/1)
+
+constexpr int kMaxSteps = 48;
+constexpr int kMaxRegs = 16;
+enum FusedOpc { F_LOAD = 64, F_CONST = 65 };
+
+struct FusedProgram {
+  int n_in, n_steps;
+  int in_dtype[8];
+  int code[kMaxSteps][4];  // opcode, dst, src1, src2 (src1 = input / const bits)
+};
+
+__device__ __forceinline__ float run_op(int opc, float x, float y) {
+  switch (opc) {
+    case PFB_ADD: return x + y;
+    case PFB_SUB: return x - y;
+    case PFB_MUL: return x * y;
+    case PFB_DIV: return x / y;
+    case PFB_MAX: return np_max(x, y);
+    case PFB_MIN: return np_min(x, y);
+    case PFB_LESS: return x < y ? 1.f : 0.f;
+    case PFB_EQUAL: return x == y ? 1.f : 0.f;
+    case 16 + PFB_NEG: return -x;
+    case 16 + PFB_EXP: return expf(x);
+    case 16 + PFB_LOG: return logf(x);
+    case 16 + PFB_RELU: return np_max(x, 0.f);
+    case 16 + PFB_TANH: return tanhf(x);
+    case 16 + PFB_SIGMOID: return 1.f / (1.f + expf(-x));
+    case 16 + PFB_SQUARE: return x * x;
+    case 16 + PFB_LOGICAL_NOT: return x == 0.f ? 1.f : 0.f;
+    default: return x;
+  }
+}
+
+template <typename IdxT, typename Tout>
+__global__ void __launch_bounds__(256) fused_kernel(Layout L, IdxT n, FusedProgram P,
+                                                    Tout* out, const void* const* ins_dummy,
+                                                    const float* i0, const float* i1,
+                                                    const float* i2, const float* i3,
+                                                    const float* i4, const float* i5,
+                                                    const float* i6, const float* i7) {
+  const float* ins[8] = {i0, i1, i2, i3, i4, i5, i6, i7};
+  for (IdxT i = blockIdx.x * (IdxT)blockDim.x + threadIdx.x; i < n;
+       i += (IdxT)gridDim.x * blockDim.x) {
+    int64_t off[kMaxOps];
+    offsets<IdxT, kMaxOps>(L, i, off);
+    float r[kMaxRegs];
+    for (int s = 0; s < P.n_steps; ++s) {
+      const int* c = P.code[s];
+      float v;
+      if (c[0] == F_LOAD) {
+        int k = c[2];
+        v = P.in_dtype[k] == PFB_BOOL ? (float)reinterpret_cast<const uint8_t*>(ins[k])[off[k + 1]]
+                                      : ins[k][off[k + 1]];
+      } else if (c[0] == F_CONST) {
+        v = __int_as_float(c[2]);
+      } else {
+        v = run_op(c[0], r[c[2]], r[c[3]]);
+      }
+      r[c[1]] = v;
+    }
+    float res = r[P.code[P.n_steps - 1][1]];
+    if constexpr (std::is_same<Tout, uint8_t>::value) out[off[0]] = (uint8_t)(res != 0.f);
+    else out[off[0]] = res;
+  }
+}
+
+}  // namespace pfb
+
+using namespace pfb;
+
+extern "C" int pfb_binary(int32_t op, const pfb_tensor* a, const pfb_tensor* b, pfb_tensor* out,
+                          void* stream) {
+  cudaStream_t s = as_stream(stream);
+  if (a->dtype != b->dtype) return PFB_E_DTYPE;
+  switch (op) {
+    case PFB_ADD: return binary_dispatch<PFB_ADD>(a, b, out, s);
+    case PFB_SUB: return binary_dispatch<PFB_SUB>(a, b, out, s);
+    case PFB_MUL: return binary_dispatch<PFB_MUL>(a, b, out, s);
+    case PFB_DIV: return binary_dispatch<PFB_DIV>(a, b, out, s);
+    case PFB_MAX: return binary_dispatch<PFB_MAX>(a, b, out, s);
+    case PFB_MIN: return binary_dispatch<PFB_MIN>(a, b, out, s);
+    case PFB_LESS: return binary_dispatch<PFB_LESS>(a, b, out, s);
+    case PFB_EQUAL: return binary_dispatch<PFB_EQUAL>(a, b, out, s);
+    default: return PFB_E_ARG;
+  }
+}
+
+extern "C" int pfb_unary(int32_t op, const pfb_tensor* x, pfb_tensor* out, void* stream) {
+  cudaStream_t s = as_stream(stream);
+  switch (op) {
+    case PFB_NEG: return unary_dispatch<PFB_NEG>(x, out, s);
+    case PFB_EXP: return unary_dispatch<PFB_EXP>(x, out, s);
+    case PFB_LOG: return unary_dispatch<PFB_LOG>(x, out, s);
+    case PFB_RELU: return unary_dispatch<PFB_RELU>(x, out, s);
+    case PFB_TANH: return unary_dispatch<PFB_TANH>(x, out, s);
+    case PFB_SIGMOID: return unary_dispatch<PFB_SIGMOID>(x, out, s);
+    case PFB_SQUARE: return unary_dispatch<PFB_SQUARE>(x, out, s);
+    case PFB_LOGICAL_NOT: return unary_dispatch<PFB_LOGICAL_NOT>(x, out, s);
+    default: return PFB_E_ARG;
+  }
+}
+
+extern "C" int pfb_cast(const pfb_tensor* x, pfb_tensor* out, void* stream) {
+  Layout L;
+  if (int e = ew_layout(out, x, nullptr, &L)) return e;
+  cudaStream_t s = as_stream(stream);
+  switch (x->dtype) {
+    case PFB_F32: return cast_from<float>(L, x, out, s);
+    case PFB_I64: return cast_from<int64_t>(L, x, out, s);
+    default: return cast_from<uint8_t>(L, x, out, s);
+  }
+}
+
+extern "C" int pfb_copy(const pfb_tensor* x, pfb_tensor* out, void* stream) {
+  if (x->dtype != out->dtype) return PFB_E_DTYPE;
+  Layout L;
+  if (int e = ew_layout(out, x, nullptr, &L)) return e;
+  cudaStream_t s = as_stream(stream);
+  switch (x->dtype) {
+    case PFB_F32: return launch_ew<float, float, 1>(L, out->data, x->data, nullptr, Identity<float>{}, s);
+    case PFB_I64:
+      return launch_ew<int64_t, int64_t, 1>(L, out->data, x->data, nullptr, Identity<int64_t>{}, s);
+    default:
+      return launch_ew<uint8_t, uint8_t, 1>(L, out->data, x->data, nullptr, Identity<uint8_t>{}, s);
+  }
+}
+
+namespace pfb {
+template <typename T>
+__global__ void fill_kernel(Layout L, int64_t n, T* out, T v) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    int64_t off[1];
+    offsets<int64_t, 1>(L, i, off);
+    out[off[0]] = v;
+  }
+}
+}  // namespace pfb
+
+extern "C" int pfb_fill(pfb_tensor* out, double value, void* stream) {
+  const int64_t* st[1] = {out->stride};
+  Layout L = make_layout(out->rank, out->shape, 1, st);
+  int64_t n = numel(out);
+  if (n == 0) return 0;
+  cudaStream_t s = as_stream(stream);
+  int grid = grid_for(n, 256);
+  if (out->dtype == PFB_F32) fill_kernel<float><<<grid, 256, 0, s>>>(L, n, (float*)out->data, (float)value);
+  else if (out->dtype == PFB_I64) fill_kernel<int64_t><<<grid, 256, 0, s>>>(L, n, (int64_t*)out->data, (int64_t)value);
+  else fill_kernel<uint8_t><<<grid, 256, 0, s>>>(L, n, (uint8_t*)out->data, (uint8_t)(value != 0.0));
+  return launch_status();
+}
+
+extern "C" int pfb_fused_ew(int32_t n_in, const pfb_tensor* ins, int32_t n_steps,
+                            const int32_t* program, pfb_tensor* out, void* stream) {
+  if (n_in < 1 || n_in > 8 || n_steps < 1 || n_steps > kMaxSteps) return PFB_E_ARG;
+  if (out->dtype != PFB_F32 && out->dtype != PFB_BOOL) return PFB_E_DTYPE;
+  int64_t stb[8][kMaxRank];
+  const int64_t* st[kMaxOps];
+  st[0] = out->stride;
+  FusedProgram P;
+  P.n_in = n_in;
+  P.n_steps = n_steps;
+  for (int k = 0; k < n_in; ++k) {
+    if (ins[k].dtype == PFB_I64) return PFB_E_DTYPE;
+    if (!broadcast_strides(&ins[k], out->rank, out->shape, stb[k])) return PFB_E_SHAPE;
+    st[k + 1] = stb[k];
+    P.in_dtype[k] = ins[k].dtype;
+  }
+  for (int k = n_in; k < 8; ++k) P.in_dtype[k] = PFB_F32;
+  for (int s = 0; s < n_steps; ++s) {
+    for (int j = 0; j < 4; ++j) P.code[s][j] = program[4 * s + j];
+    if (P.code[s][1] < 0 || P.code[s][1] >= kMaxRegs) return PFB_E_ARG;
+  }
+  // pad the layout to kMaxOps operands so the offset loop is fixed-trip
+  int64_t zero[kMaxRank] = {0};
+  for (int k = n_in + 1; k < kMaxOps; ++k) st[k] = zero;
+  Layout L = make_layout(out->rank, out->shape, kMaxOps, st);
+  int64_t n = numel(out);
+  if (n == 0) return 0;
+  const float* p[8];
+  for (int k = 0; k < 8; ++k) p[k] = k < n_in ? (const float*)ins[k].data : nullptr;
+  cudaStream_t s = as_stream(stream);
+  int grid = grid_for(n, 256);
+  if (out->dtype == PFB_F32)
+    fused_kernel<int64_t, float><<<grid, 256, 0, s>>>(L, n, P, (float*)out->data, nullptr, p[0], p[1],
+                                                      p[2], p[3], p[4], p[5], p[6], p[7]);
+  else
+    fused_kernel<int64_t, uint8_t><<<grid, 256, 0, s>>>(L, n, P, (uint8_t*)out->data, nullptr, p[0],
+                                                        p[1], p[2], p[3], p[4], p[5], p[6], p[7]);
+  return launch_status();
+}

@@ -1,0 +1,179 @@
+"""GPU: the sm_100a path against the reference's own outputs (golden fixtures)
+and the oracle.  Bar: fp32 within rtol 1e-4 / atol 1e-5 of the f64 reference;
+integer / index / bool results bit-exact."""
+
+import pathlib
+
+import numpy as np
+import pytest
+
+import kernel_graphs as KG
+from test_oracle_golden import PROGRAM_CASES, build_program
+
+pytestmark = pytest.mark.gpu
+
+RTOL, ATOL = 1e-4, 1e-5
+GOLD = pathlib.Path(__file__).parent / "golden"
+
+
+@pytest.fixture(scope="module")
+def Executor():
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    from paper_1903_04243_b200.executor import Executor
+    return Executor
+
+
+def check(got, want, rtol=RTOL, atol=ATOL):
+    want = np.asarray(want)
+    assert tuple(got.shape) == tuple(want.shape), (got.shape, want.shape)
+    if want.dtype.kind == "f":
+        np.testing.assert_allclose(np.asarray(got.data, np.float64), want, rtol=rtol, atol=atol,
+                                   equal_nan=True)
+    else:
+        np.testing.assert_array_equal(np.asarray(got.data).astype(want.dtype), want)
+
+
+def test_native_library_is_loaded(Executor):
+    from paper_1903_04243_b200 import GraphBuilder
+    b = GraphBuilder()
+    b.graph.set_outputs([b.add(b.f64(np.ones(3)), b.f64(np.ones(3)))])
+    (r,) = Executor(b.graph).run()
+    np.testing.assert_array_equal(r.data, 2 * np.ones(3))
+    maps = pathlib.Path("/proc/self/maps").read_text()
+    assert "libpfb.so" in maps
+
+
+def _kernel_names():
+    return [n for n in KG.case_names(np.load(GOLD / "kernels.npz").files) if n != "rng"]
+
+
+@pytest.mark.parametrize("name", _kernel_names())
+def test_kernel_vs_reference(name, golden, Executor):
+    K = golden["kernels"]
+    g = KG.build_case(name, KG.inputs(K, name))
+    ex = Executor(g)
+    (got,) = ex.run()
+    check(got, K[f"{name}/out"])
+    assert ex.launch_count >= 0
+
+
+def test_rng_vs_reference(golden, Executor):
+    from paper_1903_04243_b200 import GraphBuilder
+    from paper_1903_04243_b200.executor import RngState
+    K = golden["kernels"]
+    b = GraphBuilder()
+    b.graph.set_outputs([b.random_uniform((4, 5))])
+    ex = Executor(b.graph, rng=RngState(int(K["rng/in/seed"]), int(K["rng/in/counter"])))
+    (got,) = ex.run()
+    np.testing.assert_allclose(got.data, K["rng/out"], rtol=1e-7, atol=0)
+
+
+@pytest.mark.parametrize("name", sorted(PROGRAM_CASES))
+def test_program_vs_reference(name, golden, Executor):
+    P = golden["programs"]
+    w = build_program(name)
+    ex = Executor(w.graph)
+    outs = ex.run(feeds=w.feeds)
+    for j, o in enumerate(outs):
+        check(o, P[f"{name}/out/{j}"])
+
+
+@pytest.mark.parametrize("name", sorted(PROGRAM_CASES))
+def test_program_reference_registry_vs_reference(name, golden, Executor):
+    """The unmodified reference formulation (incl. its fallback loops) on device."""
+    from paper_1903_04243_b200 import reference_registry
+    if PROGRAM_CASES[name][0] == "cfg3":
+        pytest.skip("cfg3 takes no registry")
+    P = golden["programs"]
+    w = build_program(name, registry=reference_registry())
+    outs = Executor(w.graph).run(feeds=w.feeds)
+    for j, o in enumerate(outs):
+        check(o, P[f"{name}/out/{j}"])
+
+
+@pytest.mark.parametrize("name", ["pairwise_sum_diff", "gather_identity", "matmul_fold",
+                                  "conv2d_fold", "reduce_sum_renumber", "concat_shift",
+                                  "broadcast_reshape", "cond_example", "while_example"])
+def test_worked_example_parfor_graph(name, golden, Executor):
+    import worked_examples_local as WE
+    g = getattr(WE, name)()  # parfor block: the executor vectorizes it first
+    P = golden["programs"]
+    for j, o in enumerate(Executor(g).run()):
+        check(o, P[f"we_{name}/out/{j}"])
+
+
+def test_gather_out_of_bounds_raises(Executor):
+    from paper_1903_04243_b200 import GraphBuilder, errors
+    b = GraphBuilder()
+    b.graph.set_outputs([b.gather(b.const(np.ones((4, 3))), b.const(np.array([0, 4])))])
+    with pytest.raises(errors.ExecError) as e:
+        Executor(b.graph).run()
+    assert isinstance(e.value.cause, errors.IndexOutOfBounds)
+
+
+@pytest.mark.parametrize("sets,err", [(([0, 1], [1, 2]), "IndexCollision"),
+                                      (([0], [2]), "IncompleteCover")])
+def test_scatter_rows_validation(sets, err, Executor):
+    from paper_1903_04243_b200 import GraphBuilder, errors
+    b = GraphBuilder()
+    i0, i1 = (b.const(np.array(s, dtype=np.int64)) for s in sets)
+    p0 = b.const(np.ones((len(sets[0]), 2)))
+    p1 = b.const(np.ones((len(sets[1]), 2)))
+    b.graph.set_outputs([b.scatter_rows([i0, i1], [p0, p1], b.i64(3))])
+    with pytest.raises(errors.ExecError) as e:
+        Executor(b.graph).run()
+    assert type(e.value.cause).__name__ == err
+
+
+def test_dispatch_count_independent_of_output_size(Executor):
+    from paper_1903_04243_b200 import GraphBuilder, jacobian
+    counts = []
+    for m in (4, 32):
+        r = np.random.default_rng(m)
+        b = GraphBuilder()
+        x = b.const(r.standard_normal((8,)))
+        W = b.const(r.standard_normal((8, m)))
+        y = b.tanh(b.reshape(b.matmul(b.reshape(x, [1, 8]), W), [m]))
+        b.graph.set_outputs([jacobian(b, y, x)])
+        ex = Executor(b.graph)
+        ex.run()
+        counts.append(ex.dispatch_count)
+    assert counts[0] == counts[1]
+
+
+@pytest.mark.parametrize("seed", range(6))
+def test_random_strided_broadcast_binary(seed, Executor):
+    """Transposed / stride-0 views through the elementwise and reduce kernels."""
+    from paper_1903_04243_b200 import GraphBuilder
+    r = np.random.default_rng(seed)
+    a = np.asarray(r.standard_normal((6, 5, 8)), np.float32).astype(np.float64)
+    c = np.asarray(r.standard_normal((5, 1)), np.float32).astype(np.float64)
+    b = GraphBuilder()
+    A = b.transpose(b.const(a), [2, 0, 1])          # [8,6,5] strided view
+    T = b.tile_leading(b.const(c[:, 0]), b.i64(6))  # [6,5] stride-0
+    s = b.mul(A, T)
+    red = b.reduce_sum(s, [seed % 3])
+    b.graph.set_outputs([s, red])
+    got_s, got_r = Executor(b.graph).run()
+    want = np.transpose(a, [2, 0, 1]) * np.broadcast_to(c[:, 0], (6, 5))
+    check(got_s, want)
+    check(got_r, want.sum(axis=seed % 3))
+
+
+@pytest.mark.parametrize("shape", [(1, 1, 1), (7, 33, 65), (2, 130, 257), (1, 512, 1024),
+                                   (3, 64, 2048)])
+def test_matmul_shapes(shape, Executor):
+    from paper_1903_04243_b200 import GraphBuilder
+    bsz, m, k = shape
+    n = (k * 3) // 2 + 1
+    r = np.random.default_rng(k)
+    a = np.asarray(r.standard_normal((bsz, m, k)), np.float32).astype(np.float64)
+    w = np.asarray(r.standard_normal((bsz, k, n)), np.float32).astype(np.float64)
+    b = GraphBuilder()
+    b.graph.set_outputs([b.matmul(b.const(a), b.const(w)),
+                         b.matmul(b.reshape(b.const(a), [bsz * m, k]), b.const(w[0]))])
+    got3, got2 = Executor(b.graph).run()
+    check(got3, a @ w)
+    check(got2, a.reshape(bsz * m, k) @ w[0])
