@@ -1,4 +1,6 @@
 // pfb_matmul: validation + path selection (reference tensor.py:195-206).
+#include <cstdlib>
+
 #include "gemm.cuh"
 
 using namespace pfb;
@@ -52,8 +54,11 @@ extern "C" int pfb_matmul_ex(const pfb_tensor* a, const pfb_tensor* b, pfb_tenso
     zero_f32<<<grid_for(n, 256), 256, 0, s>>>((float*)out->data, n);
     return launch_status();
   }
-  // force_path: 0 = auto, 1 = SIMT, 2 = tcgen05 (error if ineligible)
-  if (force_path == 2 || (force_path == 0 && gemm_tcgen05_eligible(g))) {
+  // force_path: 0 = auto, 1 = SIMT, 2 = tcgen05 (error if ineligible).
+  // PFB_DISABLE_TCGEN05=1 pins auto to SIMT (A/B testing, bring-up).
+  static const bool tc_off = getenv("PFB_DISABLE_TCGEN05") && getenv("PFB_DISABLE_TCGEN05")[0] == '1';
+  if (force_path == 2 || (force_path == 0 && !tc_off && gemm_tcgen05_profitable(g) &&
+                          gemm_tcgen05_eligible(g))) {
     int e = gemm_tcgen05(g, s);
     if (e != PFB_E_UNSUPPORTED || force_path == 2) return e;
   }

@@ -1,8 +1,346 @@
-// tcgen05 / TMEM / TMA GEMM path (3xTF32 for fp32 accuracy) -- placeholder
-// until the kernel lands; the SIMT path serves every shape meanwhile.
+// fp32-accurate GEMM on the 5th-gen tensor cores: tcgen05.mma kind::tf32 with
+// a 3xTF32 split, TMA-fed shared-memory pipeline, accumulator in TMEM.
+//
+//   C = A_hi*B_hi + A_hi*B_lo + A_lo*B_hi,   x_hi = x with the low 13 mantissa
+//   bits cleared (exactly representable in TF32), x_lo = x - x_hi (exact).
+// Single-pass TF32 misses the fp32 parity bar (SURVEY.md §7 "Hard parts"); the
+// dropped lo*lo term is ~2^-22 relative, i.e. fp32-level.
+//
+// CTA = 6 warps, one 128x128 output tile (cta_group::1, UMMA 128x128x8):
+//   warp 0      TMA producer: A/B k-blocks (32 fp32 = one 128B swizzle row)
+//               into a 3-stage ring, completion on `full[s]` (tx bytes);
+//   warp 1      TMEM allocator + single-thread MMA issuer: 4 k-steps x 3
+//               products per stage, tcgen05.commit -> `empty[s]`, and after
+//               the last stage -> `tmem_full`;
+//   warps 2..5  split workers: per stage, rewrite A,B in place as hi and write
+//               lo to the twin buffers (elementwise, so the 128B swizzle is
+//               preserved), fence.proxy.async, arrive `split[s]`; then the
+//               epilogue: tcgen05.ld 32 lanes x 32 cols -> regs -> global
+//               (optional per-row scale / accumulate), warp w owns TMEM lanes
+//               32*(w%4)..+31.
+// Operands must be K-major (unit stride along K) with 16-byte aligned row
+// strides -- the executor's transposed weight views are; others take the
+// SIMT path.  TMA zero-fills out-of-range tiles, so any M/N/K tail works.
+#include <cuda.h>
+#include <cudaTypedefs.h>
+
 #include "gemm.cuh"
 
 namespace pfb {
-bool gemm_tcgen05_eligible(const GemmArgs&) { return false; }
-int gemm_tcgen05(const GemmArgs&, cudaStream_t) { return PFB_E_UNSUPPORTED; }
+namespace tc {
+
+constexpr int BM = 128, BN = 128, BK = 32, STAGES = 3, UMMA_K = 8;
+constexpr int TILE_BYTES = BM * BK * 4;           // 16 KB per operand tile
+constexpr int STAGE_BYTES = 4 * TILE_BYTES;       // A_hi, A_lo, B_hi, B_lo
+constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + 1024 /*align*/ + 256 /*barriers*/;
+constexpr int NUM_THREADS = 192;
+constexpr int TMEM_COLS = 128;
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+               "r"(bytes)
+               : "memory");
+}
+
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  uint32_t addr = smem_u32(bar);
+  asm volatile(
+      "{\n\t"
+      ".reg .pred P1;\n\t"
+      "WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t"
+      "@!P1 bra WAIT_%=;\n\t"
+      "}" ::"r"(addr),
+      "r"(parity)
+      : "memory");
+}
+
+__device__ __forceinline__ void tma_load_3d(const CUtensorMap* map, uint64_t* bar, void* dst,
+                                            int c0, int c1, int c2) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%3, %4, %5}], [%2];" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(bar)), "r"(c0), "r"(c1), "r"(c2)
+      : "memory");
+}
+
+// K-major, 128B-swizzled operand tile: 8-row atoms of 1024 B (SBO), version 1.
+__device__ __forceinline__ uint64_t smem_desc_sw128(uint32_t addr) {
+  uint64_t d = 0;
+  d |= (uint64_t)((addr & 0x3FFFF) >> 4);          // start address
+  d |= (uint64_t)(16 >> 4) << 16;                  // LBO (unused for swizzled K-major)
+  d |= (uint64_t)(1024 >> 4) << 32;                // SBO: stride between 8-row atoms
+  d |= (uint64_t)1 << 46;                          // descriptor version (sm100)
+  d |= (uint64_t)2 << 61;                          // SWIZZLE_128B
+  return d;
+}
+
+// kind::tf32, D=f32, K-major A and B, M=128, N=BN
+constexpr uint32_t kIdesc = (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(BN >> 3) << 17) |
+                            ((uint32_t)(BM >> 4) << 24);
+
+__device__ __forceinline__ void mma_tf32(uint32_t tmem_d, uint64_t da, uint64_t db, uint32_t acc) {
+  asm volatile(
+      "{\n\t"
+      ".reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n\t"
+      "}" ::"r"(tmem_d),
+      "l"(da), "l"(db), "r"(kIdesc), "r"(acc));
+}
+
+__device__ __forceinline__ void mma_commit(uint64_t* bar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+                   smem_u32(bar))
+               : "memory");
+}
+
+__device__ __forceinline__ float hi_part(float x) {
+  return __uint_as_float(__float_as_uint(x) & 0xFFFFE000u);
+}
+
+struct Params {
+  int M, N, K, batch;
+  float* C;
+  int64_t scb, scm, scn;
+  const float* alpha_rows;
+  int accumulate;
+};
+
+__global__ void __launch_bounds__(NUM_THREADS, 1)
+gemm_3xtf32_kernel(const __grid_constant__ CUtensorMap map_a,
+                   const __grid_constant__ CUtensorMap map_b, Params p) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>(
+      (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + STAGES * STAGE_BYTES);
+  uint64_t* full = bars;                 // [STAGES]
+  uint64_t* split = bars + STAGES;       // [STAGES]
+  uint64_t* empty = bars + 2 * STAGES;   // [STAGES]
+  uint64_t* tmem_full = bars + 3 * STAGES;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 3 * STAGES + 1);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int n0 = blockIdx.x * BN, m0 = blockIdx.y * BM, bz = blockIdx.z;
+  const int nk = (p.K + BK - 1) / BK;
+
+  auto tile = [&](int s, int which) { return smem + s * STAGE_BYTES + which * TILE_BYTES; };
+  // which: 0 = A_hi, 1 = A_lo, 2 = B_hi, 3 = B_lo
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < STAGES; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&split[s], 128);
+      mbar_init(&empty[s], 1);
+    }
+    mbar_init(tmem_full, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                     smem_u32(tmem_slot)),
+                 "r"(TMEM_COLS));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;");
+  const uint32_t tmem_base = *tmem_slot;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&map_a)) : "memory");
+      asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&map_b)) : "memory");
+      for (int kb = 0; kb < nk; ++kb) {
+        int s = kb % STAGES;
+        if (kb >= STAGES) mbar_wait(&empty[s], ((kb / STAGES) - 1) & 1);
+        mbar_expect_tx(&full[s], 2 * TILE_BYTES);
+        tma_load_3d(&map_a, &full[s], tile(s, 0), kb * BK, m0, bz);
+        tma_load_3d(&map_b, &full[s], tile(s, 2), kb * BK, n0, bz);
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      for (int kb = 0; kb < nk; ++kb) {
+        int s = kb % STAGES;
+        mbar_wait(&split[s], (kb / STAGES) & 1);
+        asm volatile("tcgen05.fence::after_thread_sync;");
+        uint64_t a_hi = smem_desc_sw128(smem_u32(tile(s, 0)));
+        uint64_t a_lo = smem_desc_sw128(smem_u32(tile(s, 1)));
+        uint64_t b_hi = smem_desc_sw128(smem_u32(tile(s, 2)));
+        uint64_t b_lo = smem_desc_sw128(smem_u32(tile(s, 3)));
+#pragma unroll
+        for (int k = 0; k < BK / UMMA_K; ++k) {
+          const uint64_t adv = (uint64_t)((k * UMMA_K * 4) >> 4);  // +32 B along K
+          uint32_t acc = (kb > 0 || k > 0) ? 1u : 0u;
+          mma_tf32(tmem_base, a_hi + adv, b_hi + adv, acc);
+          mma_tf32(tmem_base, a_hi + adv, b_lo + adv, 1u);
+          mma_tf32(tmem_base, a_lo + adv, b_hi + adv, 1u);
+        }
+        mma_commit(&empty[s]);
+      }
+      mma_commit(tmem_full);
+    }
+    __syncwarp();
+  } else {
+    // ---- split workers (128 threads) ----
+    const int t = threadIdx.x - 64;
+    for (int kb = 0; kb < nk; ++kb) {
+      int s = kb % STAGES;
+      mbar_wait(&full[s], (kb / STAGES) & 1);
+#pragma unroll
+      for (int op = 0; op < 2; ++op) {
+        float4* hi = reinterpret_cast<float4*>(tile(s, 2 * op));
+        float4* lo = reinterpret_cast<float4*>(tile(s, 2 * op + 1));
+#pragma unroll
+        for (int j = 0; j < TILE_BYTES / 16 / 128; ++j) {
+          int idx = t + j * 128;
+          float4 v = hi[idx];
+          float4 h = make_float4(hi_part(v.x), hi_part(v.y), hi_part(v.z), hi_part(v.w));
+          hi[idx] = h;
+          lo[idx] = make_float4(v.x - h.x, v.y - h.y, v.z - h.z, v.w - h.w);
+        }
+      }
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      mbar_arrive(&split[s]);
+    }
+    // ---- epilogue: TMEM -> registers -> global ----
+    mbar_wait(tmem_full, 0);
+    asm volatile("tcgen05.fence::after_thread_sync;");
+    const int quarter = warp & 3;
+    const int row = m0 + quarter * 32 + lane;
+    const float alpha = (p.alpha_rows && row < p.M) ? p.alpha_rows[(int64_t)bz * p.M + row] : 1.f;
+    float* crow = p.C + bz * p.scb + (int64_t)row * p.scm;
+#pragma unroll
+    for (int c = 0; c < BN; c += 32) {
+      uint32_t r[32];
+      const uint32_t taddr = tmem_base + ((uint32_t)(quarter * 32) << 16) + (uint32_t)c;
+      asm volatile(
+          "tcgen05.ld.sync.aligned.32x32b.x32.b32 "
+          "{%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, %15, "
+          "%16, %17, %18, %19, %20, %21, %22, %23, %24, %25, %26, %27, %28, %29, %30, %31}, [%32];"
+          : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
+            "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]),
+            "=r"(r[13]), "=r"(r[14]), "=r"(r[15]), "=r"(r[16]), "=r"(r[17]), "=r"(r[18]),
+            "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]), "=r"(r[24]),
+            "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]),
+            "=r"(r[31])
+          : "r"(taddr));
+      asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+      if (row < p.M) {
+        const int col0 = n0 + c;
+        if (p.scn == 1 && col0 + 32 <= p.N && ((reinterpret_cast<uintptr_t>(crow + col0) & 15) == 0)) {
+          float4* dst = reinterpret_cast<float4*>(crow + col0);
+#pragma unroll
+          for (int j = 0; j < 8; ++j) {
+            float4 v = make_float4(__uint_as_float(r[4 * j]) * alpha, __uint_as_float(r[4 * j + 1]) * alpha,
+                                   __uint_as_float(r[4 * j + 2]) * alpha,
+                                   __uint_as_float(r[4 * j + 3]) * alpha);
+            if (p.accumulate) {
+              float4 o = dst[j];
+              v.x += o.x; v.y += o.y; v.z += o.z; v.w += o.w;
+            }
+            dst[j] = v;
+          }
+        } else {
+#pragma unroll
+          for (int j = 0; j < 32; ++j) {
+            int col = col0 + j;
+            if (col < p.N) {
+              float* q = crow + (int64_t)col * p.scn;
+              float v = __uint_as_float(r[j]) * alpha;
+              *q = p.accumulate ? *q + v : v;
+            }
+          }
+        }
+      }
+    }
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;");
+  __syncthreads();
+  if (warp == 1) {
+    asm volatile("tcgen05.fence::after_thread_sync;");
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base),
+                 "r"(TMEM_COLS));
+  }
+}
+
+// --- host side -------------------------------------------------------------
+
+static PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  static bool tried = false;
+  if (!tried) {
+    tried = true;
+    cudaDriverEntryPointQueryResult q;
+    void* p = nullptr;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+  }
+  return fn;
+}
+
+// K-major operand [batch][rows][K] with row stride `srow`, batch stride `sbat` (elements)
+static bool make_map(CUtensorMap* map, const float* base, int64_t K, int64_t rows, int64_t batch,
+                     int64_t srow, int64_t sbat) {
+  auto fn = encode_fn();
+  if (!fn) return false;
+  cuuint64_t dims[3] = {(cuuint64_t)K, (cuuint64_t)rows, (cuuint64_t)batch};
+  cuuint64_t strides[2] = {(cuuint64_t)(srow * 4), (cuuint64_t)((batch > 1 ? sbat : rows * srow) * 4)};
+  cuuint32_t box[3] = {BK, BM, 1};
+  cuuint32_t estr[3] = {1, 1, 1};
+  CUresult r = fn(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, const_cast<float*>(base), dims, strides,
+                  box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                  CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS;
+}
+
+}  // namespace tc
+
+bool gemm_tcgen05_eligible(const GemmArgs& g) {
+  if (g.sak != 1 || g.sbk != 1) return false;                 // K-major operands only
+  if (g.sam % 4 || g.sbn % 4) return false;                   // 16-byte row strides
+  if (g.batch > 1 && (g.sab % 4 || g.sbb % 4 || g.sab == 0 || g.sbb == 0)) return false;
+  if ((reinterpret_cast<uintptr_t>(g.A) & 15) || (reinterpret_cast<uintptr_t>(g.B) & 15)) return false;
+  if (g.K < 8 || g.M < 1 || g.N < 8) return false;
+  return !(g.M > (1ll << 31) || g.N > (1ll << 31) || g.K > (1ll << 31) || g.batch > 65535);
+}
+
+bool gemm_tcgen05_profitable(const GemmArgs& g) {
+  return g.K >= 32 && g.M >= 64 && g.N >= 64 &&
+         (double)g.batch * g.M * g.N * g.K >= (double)(1 << 22);
+}
+
+int gemm_tcgen05(const GemmArgs& g, cudaStream_t s) {
+  using namespace tc;
+  if (!gemm_tcgen05_eligible(g)) return PFB_E_UNSUPPORTED;
+  CUtensorMap ma, mb;
+  if (!make_map(&ma, g.A, g.K, g.M, g.batch, g.sam, g.sab)) return PFB_E_UNSUPPORTED;
+  if (!make_map(&mb, g.B, g.K, g.N, g.batch, g.sbn, g.sbb)) return PFB_E_UNSUPPORTED;
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(gemm_3xtf32_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES);
+    attr = true;
+  }
+  Params p{(int)g.M, (int)g.N, (int)g.K, (int)g.batch, g.C, g.scb, g.scm, g.scn, g.alpha_rows,
+           g.accumulate};
+  dim3 grid((unsigned)((g.N + BN - 1) / BN), (unsigned)((g.M + BM - 1) / BM), (unsigned)g.batch);
+  if (grid.y > 65535) return PFB_E_UNSUPPORTED;
+  gemm_3xtf32_kernel<<<grid, NUM_THREADS, SMEM_BYTES, s>>>(ma, mb, p);
+  return launch_status();
+}
+
 }  // namespace pfb

@@ -74,8 +74,9 @@ class DArray:
 
     @staticmethod
     def from_numpy(arr, dtype, device):
-        host = np.ascontiguousarray(np.asarray(arr, dtype=dtype.device_np_dtype))
-        buf = torch.from_numpy(host.reshape(-1)).to(device, non_blocking=False)
+        # (np.ascontiguousarray would promote 0-d to 1-d)
+        host = np.require(np.asarray(arr, dtype=dtype.device_np_dtype), requirements="C")
+        buf = torch.from_numpy(host.reshape(-1).copy()).to(device, non_blocking=False)
         return DArray(buf, 0, host.shape, _dense_strides(host.shape), dtype)
 
     @property

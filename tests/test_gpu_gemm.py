@@ -1,0 +1,88 @@
+"""GPU: the tcgen05 3xTF32 GEMM and the SIMT GEMM against f64 numpy, directly
+through the C ABI (pfb_matmul_ex, forced path)."""
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+RTOL, ATOL = 1e-4, 1e-5
+
+
+@pytest.fixture(scope="module")
+def env():
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    from paper_1903_04243_b200 import _native as N
+    from paper_1903_04243_b200.executor import DArray
+    from paper_1903_04243_b200.tensor import DType
+    return torch, N.lib(), DArray, DType
+
+
+def _run(env, a, b, force, transpose_b=False, accumulate_into=None, alpha=None):
+    torch, lib, DArray, DType = env
+    dev = torch.device("cuda")
+    A = DArray.from_numpy(a, DType.F64, dev)
+    if transpose_b:  # K-major B: store B^T densely, pass a transposed view
+        Bt = DArray.from_numpy(np.swapaxes(b, -1, -2).copy(), DType.F64, dev)
+        perm = list(range(b.ndim))
+        perm[-1], perm[-2] = perm[-2], perm[-1]
+        B = Bt.view([Bt.shape[p] for p in perm], [Bt.strides[p] for p in perm])
+    else:
+        B = DArray.from_numpy(b, DType.F64, dev)
+    shape = a.shape[:-1] + (b.shape[-1],)
+    C = (DArray.from_numpy(accumulate_into, DType.F64, dev) if accumulate_into is not None
+         else DArray.empty(shape, DType.F64, dev))
+    al = None
+    if alpha is not None:
+        al_t = torch.as_tensor(alpha.astype(np.float32), device=dev)
+        al = al_t.data_ptr()
+    rc = lib.pfb_matmul_ex(A.desc(), B.desc(), C.desc(), al, int(accumulate_into is not None),
+                           force, torch.cuda.current_stream().cuda_stream)
+    assert rc == 0, rc
+    torch.cuda.synchronize()
+    return C.to_numpy().astype(np.float64)
+
+
+def _f32(r, shape):
+    return np.asarray(r.standard_normal(shape), np.float32).astype(np.float64)
+
+
+@pytest.mark.parametrize("shape", [(128, 128, 32), (256, 384, 256), (200, 300, 100),
+                                   (10240, 784, 256), (513, 129, 1000), (64, 64, 64)])
+@pytest.mark.parametrize("force", [1, 2])
+def test_gemm_2d(env, shape, force):
+    m, n, k = shape
+    r = np.random.default_rng(m + n + k)
+    a, b = _f32(r, (m, k)), _f32(r, (k, n))
+    got = _run(env, a, b, force, transpose_b=True)
+    np.testing.assert_allclose(got, a @ b, rtol=RTOL, atol=ATOL)
+
+
+@pytest.mark.parametrize("force", [1, 2])
+def test_gemm_batched(env, force):
+    r = np.random.default_rng(7)
+    a, b = _f32(r, (3, 160, 96)), _f32(r, (3, 96, 200))
+    got = _run(env, a, b, force, transpose_b=True)
+    np.testing.assert_allclose(got, a @ b, rtol=RTOL, atol=ATOL)
+
+
+def test_gemm_epilogue_alpha_accumulate(env):
+    r = np.random.default_rng(3)
+    a, b = _f32(r, (256, 128)), _f32(r, (128, 256))
+    c0 = _f32(r, (256, 256))
+    alpha = np.asarray(r.standard_normal(256), np.float32).astype(np.float64)
+    for force in (1, 2):
+        got = _run(env, a, b, force, transpose_b=True, accumulate_into=c0, alpha=alpha)
+        np.testing.assert_allclose(got, c0 + alpha[:, None] * (a @ b), rtol=RTOL, atol=ATOL)
+
+
+def test_gemm_tcgen05_is_fp32_accurate_not_tf32(env):
+    """Single-pass TF32 would miss by ~1e-3 relative; 3xTF32 must not."""
+    r = np.random.default_rng(11)
+    a, b = _f32(r, (256, 1024)), _f32(r, (1024, 256))
+    got = _run(env, a, b, 2, transpose_b=True)
+    want = a @ b
+    rel = np.max(np.abs(got - want)) / np.max(np.abs(want))
+    assert rel < 2e-6, rel
