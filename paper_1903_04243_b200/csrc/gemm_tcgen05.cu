@@ -1,10 +1,11 @@
 // fp32-accurate GEMM on the 5th-gen tensor cores: tcgen05.mma kind::tf32 with
 // a 3xTF32 split, TMA-fed shared-memory pipeline, accumulator in TMEM.
 //
-//   C = A_hi*B_hi + A_hi*B_lo + A_lo*B_hi,   x_hi = x with the low 13 mantissa
-//   bits cleared (exactly representable in TF32), x_lo = x - x_hi (exact).
-// Single-pass TF32 misses the fp32 parity bar (SURVEY.md §7 "Hard parts"); the
-// dropped lo*lo term is ~2^-22 relative, i.e. fp32-level.
+//   C = A_hi*B_hi + A_hi*B_lo + A_lo*B_hi,   x_hi = rn_tf32(x), x_lo = rn_tf32(x - x_hi)
+// (both exactly representable in TF32, so the tensor core's own operand
+// rounding never applies).  Single-pass TF32 misses the fp32 parity bar
+// (SURVEY.md §7 "Hard parts"); here the dropped terms (lo*lo and the split
+// remainders) are ~2^-22 relative per product -- a few fp32 ulps.
 //
 // CTA = 6 warps, one 128x128 output tile (cta_group::1, UMMA 128x128x8):
 //   warp 0      TMA producer: A/B k-blocks (32 fp32 = one 128B swizzle row)
@@ -107,8 +108,12 @@ __device__ __forceinline__ void mma_commit(uint64_t* bar) {
                : "memory");
 }
 
-__device__ __forceinline__ float hi_part(float x) {
-  return __uint_as_float(__float_as_uint(x) & 0xFFFFE000u);
+// round-to-nearest to TF32 (10 explicit mantissa bits), result exactly
+// representable, so the tensor core reads it without further rounding
+__device__ __forceinline__ float to_tf32(float x) {
+  uint32_t r;
+  asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"(x));
+  return __uint_as_float(r);
 }
 
 struct Params {
@@ -208,9 +213,10 @@ gemm_3xtf32_kernel(const __grid_constant__ CUtensorMap map_a,
         for (int j = 0; j < TILE_BYTES / 16 / 128; ++j) {
           int idx = t + j * 128;
           float4 v = hi[idx];
-          float4 h = make_float4(hi_part(v.x), hi_part(v.y), hi_part(v.z), hi_part(v.w));
+          float4 h = make_float4(to_tf32(v.x), to_tf32(v.y), to_tf32(v.z), to_tf32(v.w));
           hi[idx] = h;
-          lo[idx] = make_float4(v.x - h.x, v.y - h.y, v.z - h.z, v.w - h.w);
+          lo[idx] = make_float4(to_tf32(v.x - h.x), to_tf32(v.y - h.y), to_tf32(v.z - h.z),
+                                to_tf32(v.w - h.w));
         }
       }
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");

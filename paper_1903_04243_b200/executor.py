@@ -208,8 +208,18 @@ def _block_has_state(block):
 class Executor:
     """Runs a graph on one CUDA device; one stream, values resident in HBM."""
 
-    def __init__(self, graph, store=None, rng=None, budget=None, device=None, check_errors=True):
+    def __init__(self, graph, store=None, rng=None, budget=None, device=None, check_errors=True,
+                 cuda_graph="auto", optimize=True):
+        """`cuda_graph`: "auto" captures pure, block-free graphs (no cond/while,
+        no stateful ops, no data-dependent sizes) into one CUDA graph on the
+        second run with a given feed signature and replays it afterwards --
+        one launch per step instead of one per node.  False = always eager."""
         self._lib = N.lib()
+        self.optimize = optimize
+        self.cuda_graph = cuda_graph
+        self._captures = {}
+        self._capture_ok = {}
+        self._warm = set()
         self.graph = graph
         self.device = torch.device(device if device is not None else "cuda")
         self.store = store if store is not None else VariableStore(graph.variables)
@@ -249,23 +259,104 @@ class Executor:
         return res
 
     def run_device(self, feeds=None, outputs=None):
-        """Execute; return device values (DArray / HostVal) without copying back."""
+        """Execute; return device values (DArray / HostVal) without copying back.
+
+        With CUDA-graph replay active the returned arrays live in the graph's
+        memory pool and are overwritten by the next run."""
+        feeds = feeds or {}
         with torch.cuda.device(self.device):
             g, keys = self._resolve_outputs(outputs)
-            self._begin()
-            env = self._run_graph(g, {}, feeds or {}, roots=keys)
-            return [env[k] for k in keys]
+            if self.cuda_graph and self.kernel_timer is None and self._capturable(g, keys):
+                sig = (tuple(keys), _feed_signature(feeds))
+                cap = self._captures.get(sig)
+                if cap is None and sig in self._warm:
+                    cap = self._capture(g, keys, feeds, sig)
+                if cap is not None:
+                    return self._replay(cap, feeds)
+                self._warm.add(sig)
+            return self._run_eager(g, keys, feeds)
+
+    def _run_eager(self, g, keys, feeds):
+        self._begin()
+        env = self._run_graph(g, {}, feeds, roots=keys)
+        return [env[k] for k in keys]
+
+    # -- CUDA-graph capture of pure block-free graphs --------------------------------
+
+    _NO_CAPTURE = STATEFUL_KINDS | {"where_true", "complement", "cond", "while", "parfor"}
+
+    def _capturable(self, g, keys):
+        key = (id(g), tuple(keys))
+        ok = self._capture_ok.get(key)
+        if ok is None:
+            plan = self._plan(g, keys)
+            ok = not any(n.kind in self._NO_CAPTURE for n in plan.order)
+            self._capture_ok[key] = ok
+        return ok
+
+    def _capture(self, g, keys, feeds, sig):
+        static = {}
+        for name, v in feeds.items():
+            dt = _feed_dtype(g, name)
+            arr = v if isinstance(v, torch.Tensor) else np.asarray(v)
+            static[name] = DArray.empty(tuple(arr.shape), dt, self.device)
+        saved = (self._ws, self._err, self._err_nodes)
+        self._ws, self._err = None, None
+        graph = torch.cuda.CUDAGraph()
+        cap = None
+        try:
+            self._load_feeds(static, feeds)
+            torch.cuda.synchronize(self.device)
+            l0, d0 = self.launch_count, self.dispatch_count
+            with torch.cuda.graph(graph):
+                outs = self._run_eager(g, keys, static)
+            cap = _Captured(graph, static, outs, self._ws, self._err, list(self._err_nodes))
+            cap.launches = self.launch_count - l0
+            cap.dispatches = self.dispatch_count - d0
+            self._captures[sig] = cap
+        except Exception:  # anything the capture cannot take: stay eager for this graph
+            self._capture_ok[(id(g), tuple(keys))] = False
+            torch.cuda.synchronize(self.device)
+        finally:
+            self._ws, self._err, self._err_nodes = saved
+        return cap
+
+    def _load_feeds(self, static, feeds):
+        for name, dst in static.items():
+            v = feeds[name]
+            t = dst.torch_view()
+            if isinstance(v, torch.Tensor):
+                t.copy_(v.reshape(t.shape), non_blocking=True)
+            else:
+                arr = np.asarray(v, dtype=dst.dtype.device_np_dtype)
+                t.copy_(torch.from_numpy(np.require(arr, requirements="C")).reshape(t.shape))
+
+    def _replay(self, cap, feeds):
+        self._load_feeds(cap.inputs, feeds)
+        cap.graph.replay()
+        self.launch_count += cap.launches
+        self.dispatch_count += cap.dispatches
+        self._err, self._err_nodes = cap.err, list(cap.err_nodes)
+        return cap.outputs
 
     # -- setup -------------------------------------------------------------------
 
     def _resolve_outputs(self, outputs):
         if self._exec_graph is None:
-            if _has_parfor_anywhere(self.graph):
-                refmap = {}
-                self._exec_graph, _ = vectorize_graph(self.graph, refmap_out=refmap)
-                self._refmap = {k: (r.nid, r.port) for k, r in refmap.items()}
-            else:
-                self._exec_graph = self.graph
+            g = self.graph
+            refmap = None
+            if _has_parfor_anywhere(g):
+                rm = {}
+                g, _ = vectorize_graph(g, refmap_out=rm)
+                refmap = {k: (r.nid, r.port) for k, r in rm.items()}
+            if self.optimize and not _has_blocks(g):
+                from .passes import optimize as _opt
+                keep = [tuple(o) for o in g.outputs] if refmap is None else \
+                    [refmap[tuple(o)] for o in self.graph.outputs]
+                g2, m2 = _opt(g, keep)
+                refmap = m2 if refmap is None else {k: m2[v] for k, v in refmap.items()}
+                g = g2
+            self._exec_graph, self._refmap = g, refmap
         g = self._exec_graph
         if outputs is None:
             keys = [tuple(o) for o in self.graph.outputs]
@@ -459,6 +550,8 @@ class Executor:
         return h(self, node, ins)
 
     def _feed(self, value, dtype):
+        if isinstance(value, DArray):
+            return value
         if isinstance(value, torch.Tensor):
             t = value.to(self.device, dtype=_TORCH[dtype], non_blocking=True).contiguous()
             return DArray(t.reshape(-1), 0, tuple(t.shape), _dense_strides(t.shape), dtype)
@@ -466,6 +559,37 @@ class Executor:
         if tv.rank == 0 and dtype != DType.F64:
             return HostVal(tv.data, dtype)
         return self._upload(tv)
+
+
+class _Captured:
+    def __init__(self, graph, inputs, outputs, ws, err, err_nodes):
+        self.graph, self.inputs, self.outputs = graph, inputs, outputs
+        self.ws, self.err, self.err_nodes = ws, err, err_nodes
+        self.launches = 0
+        self.dispatches = 0
+
+
+def _feed_signature(feeds):
+    sig = []
+    for k in sorted(feeds):
+        v = feeds[k]
+        if isinstance(v, torch.Tensor):
+            sig.append((k, tuple(v.shape), str(v.dtype), v.device.type))
+        else:
+            a = np.asarray(v)
+            sig.append((k, a.shape, str(a.dtype), "np"))
+    return tuple(sig)
+
+
+def _feed_dtype(g, name):
+    for n in g.nodes.values():
+        if n.kind == "placeholder" and n.attrs["name"] == name:
+            return n.attrs["dtype"]
+    raise E.PforVecError(f"no placeholder named {name!r}")
+
+
+def _has_blocks(g):
+    return any(n.block is not None for n in g.nodes.values())
 
 
 def _has_parfor_anywhere(g):

@@ -1,0 +1,63 @@
+"""CPU: the post-vectorization fusions (passes.py) preserve values.
+
+The rewritten graphs run on the oracle here; on the GPU the same rewrites run
+inside the executor (tests/test_gpu_parity.py compares against goldens)."""
+
+import numpy as np
+import pytest
+
+from oracle import OracleExecutor
+from paper_1903_04243_b200 import workloads as WL
+from paper_1903_04243_b200.passes import optimize
+
+
+def _run_both(w):
+    g = w.graph
+    keys = [tuple(o) for o in g.outputs]
+    g2, m = optimize(g, keys)
+    want = OracleExecutor(g).run(feeds=w.feeds)
+    got = OracleExecutor(g2).run(feeds=w.feeds, outputs=[g2.out(*m[k]) for k in keys])
+    for a, b in zip(got, want):
+        np.testing.assert_allclose(a.data, b.data, rtol=1e-10, atol=1e-12)
+    return g, g2, m
+
+
+def _kinds(g, roots):
+    from paper_1903_04243_b200.executor import _Plan  # noqa: F401  (torch import)
+    live, todo = set(), [r[0] for r in roots]
+    while todo:
+        n = todo.pop()
+        if n in live:
+            continue
+        live.add(n)
+        todo.extend(s for s, _ in g.nodes[n].inputs)
+    return [g.nodes[n] for n in sorted(live)]
+
+
+def test_f1_norm_and_clipped_sum_without_stacked_grads():
+    w = WL.cfg2(WL.this_api(), n=6, model="mlp", d_h=16)
+    g, g2, m = _run_both(w)
+    live = _kinds(g2, [m[tuple(o)] for o in g.outputs])
+    big = [n for n in live if n.kind == "matmul" and len(n.out_shapes[0]) == 3
+           and n.out_shapes[0][1] == 784]
+    assert not big, "the [n,784,16] per-example outer product must not be computed"
+
+
+def test_f1_conv_model():
+    _run_both(WL.cfg2(WL.this_api(), n=3, model="conv"))
+
+
+def test_f2_outer_product_sum_becomes_one_gemm():
+    w = WL.cfg4(WL.this_api(), n=3, steps=5, units=4)
+    g, g2, m = _run_both(w)
+    live = _kinds(g2, [m[tuple(o)] for o in g.outputs])
+    k1 = [n for n in live if n.kind == "matmul" and len(n.out_shapes[0]) == 3
+          and n.out_shapes[0][1:] == (8, 16)]
+    assert len(k1) == 1, [n.out_shapes for n in k1]
+
+
+@pytest.mark.parametrize("cfg,kw", [("cfg1", dict(batch=4, d_in=12, d_h=8, d_out=3)),
+                                    ("cfg3", dict(width=16, out_dim=8)),
+                                    ("cfg5", dict(n=5, max_len=6, units=4))])
+def test_passes_neutral_elsewhere(cfg, kw):
+    _run_both(WL.BUILDERS[cfg](WL.this_api(), **kw))
