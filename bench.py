@@ -263,9 +263,13 @@ def main():
     e2e_s = float(t.item())
     e2e = w.units * world * args.steps / e2e_s
 
-    # roofline of the dominant kernel: instrumented extra steps
+    # roofline of the dominant kernel: instrumented extra (eager) steps.  A
+    # spin kernel first keeps the GPU busy while the host enqueues every launch
+    # and its bracketing events, so event deltas are device time, not host gaps.
     ex.kernel_timer = []
     for _ in range(3):
+        flush.zero_()
+        torch.cuda._sleep(int(50e6))
         step_device()
     torch.cuda.synchronize(dev)
     agg = {}

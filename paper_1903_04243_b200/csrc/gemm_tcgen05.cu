@@ -7,18 +7,20 @@
 // (SURVEY.md §7 "Hard parts"); here the dropped terms (lo*lo and the split
 // remainders) are ~2^-22 relative per product -- a few fp32 ulps.
 //
-// CTA = 6 warps, one 128x128 output tile (cta_group::1, UMMA 128x128x8):
+// CTA = 10 warps, one 128x128 output tile (cta_group::1, UMMA 128x128x8):
 //   warp 0      TMA producer: A/B k-blocks (32 fp32 = one 128B swizzle row)
 //               into a 3-stage ring, completion on `full[s]` (tx bytes);
 //   warp 1      TMEM allocator + single-thread MMA issuer: 4 k-steps x 3
-//               products per stage, tcgen05.commit -> `empty[s]`, and after
-//               the last stage -> `tmem_full`;
+//               products per stage, tcgen05.commit -> `empty[s]`; every
+//               CHUNK_KB stages it switches TMEM buffer and commits
+//               `acc_full[buf]`;
 //   warps 2..5  split workers: per stage, rewrite A,B in place as hi and write
 //               lo to the twin buffers (elementwise, so the 128B swizzle is
-//               preserved), fence.proxy.async, arrive `split[s]`; then the
-//               epilogue: tcgen05.ld 32 lanes x 32 cols -> regs -> global
-//               (optional per-row scale / accumulate), warp w owns TMEM lanes
-//               32*(w%4)..+31.
+//               preserved), fence.proxy.async, arrive `split[s]`;
+//   warps 6..9  accumulators: tcgen05.ld each finished 64-deep chunk
+//               (32 lanes x 32 cols per load; warp w owns TMEM lanes
+//               32*(w%4)..+31), add into fp32 registers (RN), release the
+//               buffer; finally store with optional per-row scale / accumulate.
 // Operands must be K-major (unit stride along K) with 16-byte aligned row
 // strides -- the executor's transposed weight views are; others take the
 // SIMT path.  TMA zero-fills out-of-range tiles, so any M/N/K tail works.
@@ -31,11 +33,12 @@ namespace pfb {
 namespace tc {
 
 constexpr int BM = 128, BN = 128, BK = 32, STAGES = 3, UMMA_K = 8;
+constexpr int CHUNK_KB = 2;                       // k-blocks accumulated in TMEM per chunk
 constexpr int TILE_BYTES = BM * BK * 4;           // 16 KB per operand tile
 constexpr int STAGE_BYTES = 4 * TILE_BYTES;       // A_hi, A_lo, B_hi, B_lo
 constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + 1024 /*align*/ + 256 /*barriers*/;
-constexpr int NUM_THREADS = 192;
-constexpr int TMEM_COLS = 128;
+constexpr int NUM_THREADS = 320;                  // 10 warps
+constexpr int TMEM_COLS = 2 * BN;                 // double-buffered chunk accumulator
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
@@ -116,6 +119,20 @@ __device__ __forceinline__ float to_tf32(float x) {
   return __uint_as_float(r);
 }
 
+__device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t* r) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 "
+      "{%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, %15, "
+      "%16, %17, %18, %19, %20, %21, %22, %23, %24, %25, %26, %27, %28, %29, %30, %31}, [%32];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
+        "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]),
+        "=r"(r[13]), "=r"(r[14]), "=r"(r[15]), "=r"(r[16]), "=r"(r[17]), "=r"(r[18]),
+        "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]), "=r"(r[24]),
+        "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]),
+        "=r"(r[31])
+      : "r"(taddr));
+}
+
 struct Params {
   int M, N, K, batch;
   float* C;
@@ -124,6 +141,12 @@ struct Params {
   int accumulate;
 };
 
+// Warp roles (10 warps): 0 TMA producer | 1 TMEM alloc + MMA issuer |
+// 2..5 hi/lo split of each staged k-block | 6..9 chunk accumulators + epilogue.
+// The tensor core's in-TMEM accumulation truncates (measured: 3xTF32 error grew
+// linearly with K, ~1e-4 relative at K=4096), so TMEM only ever holds a
+// CHUNK_KB*BK = 64-deep partial sum; the accumulator warps drain it into fp32
+// registers with round-to-nearest adds while the MMA fills the other buffer.
 __global__ void __launch_bounds__(NUM_THREADS, 1)
 gemm_3xtf32_kernel(const __grid_constant__ CUtensorMap map_a,
                    const __grid_constant__ CUtensorMap map_b, Params p) {
@@ -131,15 +154,17 @@ gemm_3xtf32_kernel(const __grid_constant__ CUtensorMap map_a,
   uint8_t* smem = reinterpret_cast<uint8_t*>(
       (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + STAGES * STAGE_BYTES);
-  uint64_t* full = bars;                 // [STAGES]
-  uint64_t* split = bars + STAGES;       // [STAGES]
-  uint64_t* empty = bars + 2 * STAGES;   // [STAGES]
-  uint64_t* tmem_full = bars + 3 * STAGES;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 3 * STAGES + 1);
+  uint64_t* full = bars;                   // [STAGES] TMA -> split
+  uint64_t* split = bars + STAGES;         // [STAGES] split -> MMA
+  uint64_t* empty = bars + 2 * STAGES;     // [STAGES] MMA -> TMA
+  uint64_t* acc_full = bars + 3 * STAGES;  // [2] MMA -> accumulators
+  uint64_t* acc_empty = acc_full + 2;      // [2] accumulators -> MMA
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_empty + 2);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int n0 = blockIdx.x * BN, m0 = blockIdx.y * BM, bz = blockIdx.z;
   const int nk = (p.K + BK - 1) / BK;
+  const int nchunks = (nk + CHUNK_KB - 1) / CHUNK_KB;
 
   auto tile = [&](int s, int which) { return smem + s * STAGE_BYTES + which * TILE_BYTES; };
   // which: 0 = A_hi, 1 = A_lo, 2 = B_hi, 3 = B_lo
@@ -150,7 +175,10 @@ gemm_3xtf32_kernel(const __grid_constant__ CUtensorMap map_a,
       mbar_init(&split[s], 128);
       mbar_init(&empty[s], 1);
     }
-    mbar_init(tmem_full, 1);
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(&acc_full[b], 1);
+      mbar_init(&acc_empty[b], 128);
+    }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   if (warp == 1) {
@@ -178,28 +206,35 @@ gemm_3xtf32_kernel(const __grid_constant__ CUtensorMap map_a,
     }
   } else if (warp == 1) {
     if (lane == 0) {
-      for (int kb = 0; kb < nk; ++kb) {
-        int s = kb % STAGES;
-        mbar_wait(&split[s], (kb / STAGES) & 1);
+      for (int c = 0; c < nchunks; ++c) {
+        const int buf = c & 1;
+        if (c >= 2) mbar_wait(&acc_empty[buf], ((c >> 1) - 1) & 1);
         asm volatile("tcgen05.fence::after_thread_sync;");
-        uint64_t a_hi = smem_desc_sw128(smem_u32(tile(s, 0)));
-        uint64_t a_lo = smem_desc_sw128(smem_u32(tile(s, 1)));
-        uint64_t b_hi = smem_desc_sw128(smem_u32(tile(s, 2)));
-        uint64_t b_lo = smem_desc_sw128(smem_u32(tile(s, 3)));
+        const uint32_t tmem_d = tmem_base + (uint32_t)(buf * BN);
+        const int kb_end = min(nk, (c + 1) * CHUNK_KB);
+        for (int kb = c * CHUNK_KB; kb < kb_end; ++kb) {
+          int s = kb % STAGES;
+          mbar_wait(&split[s], (kb / STAGES) & 1);
+          asm volatile("tcgen05.fence::after_thread_sync;");
+          uint64_t a_hi = smem_desc_sw128(smem_u32(tile(s, 0)));
+          uint64_t a_lo = smem_desc_sw128(smem_u32(tile(s, 1)));
+          uint64_t b_hi = smem_desc_sw128(smem_u32(tile(s, 2)));
+          uint64_t b_lo = smem_desc_sw128(smem_u32(tile(s, 3)));
 #pragma unroll
-        for (int k = 0; k < BK / UMMA_K; ++k) {
-          const uint64_t adv = (uint64_t)((k * UMMA_K * 4) >> 4);  // +32 B along K
-          uint32_t acc = (kb > 0 || k > 0) ? 1u : 0u;
-          mma_tf32(tmem_base, a_hi + adv, b_hi + adv, acc);
-          mma_tf32(tmem_base, a_hi + adv, b_lo + adv, 1u);
-          mma_tf32(tmem_base, a_lo + adv, b_hi + adv, 1u);
+          for (int k = 0; k < BK / UMMA_K; ++k) {
+            const uint64_t adv = (uint64_t)((k * UMMA_K * 4) >> 4);  // +32 B along K
+            uint32_t acc = (kb > c * CHUNK_KB || k > 0) ? 1u : 0u;
+            mma_tf32(tmem_d, a_hi + adv, b_hi + adv, acc);
+            mma_tf32(tmem_d, a_hi + adv, b_lo + adv, 1u);
+            mma_tf32(tmem_d, a_lo + adv, b_hi + adv, 1u);
+          }
+          mma_commit(&empty[s]);
         }
-        mma_commit(&empty[s]);
+        mma_commit(&acc_full[buf]);
       }
-      mma_commit(tmem_full);
     }
     __syncwarp();
-  } else {
+  } else if (warp < 6) {
     // ---- split workers (128 threads) ----
     const int t = threadIdx.x - 64;
     for (int kb = 0; kb < nk; ++kb) {
@@ -222,53 +257,53 @@ gemm_3xtf32_kernel(const __grid_constant__ CUtensorMap map_a,
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
       mbar_arrive(&split[s]);
     }
-    // ---- epilogue: TMEM -> registers -> global ----
-    mbar_wait(tmem_full, 0);
-    asm volatile("tcgen05.fence::after_thread_sync;");
+  } else {
+    // ---- chunk accumulators + epilogue (128 threads) ----
     const int quarter = warp & 3;
+    float acc[BN];
+#pragma unroll
+    for (int j = 0; j < BN; ++j) acc[j] = 0.f;
+    for (int c = 0; c < nchunks; ++c) {
+      const int buf = c & 1;
+      mbar_wait(&acc_full[buf], (c >> 1) & 1);
+      asm volatile("tcgen05.fence::after_thread_sync;");
+#pragma unroll
+      for (int cc = 0; cc < BN; cc += 32) {
+        uint32_t r[32];
+        tmem_ld32(tmem_base + ((uint32_t)(quarter * 32) << 16) + (uint32_t)(buf * BN + cc), r);
+        asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+        for (int j = 0; j < 32; ++j) acc[cc + j] += __uint_as_float(r[j]);
+      }
+      asm volatile("tcgen05.fence::before_thread_sync;");
+      mbar_arrive(&acc_empty[buf]);
+    }
     const int row = m0 + quarter * 32 + lane;
-    const float alpha = (p.alpha_rows && row < p.M) ? p.alpha_rows[(int64_t)bz * p.M + row] : 1.f;
-    float* crow = p.C + bz * p.scb + (int64_t)row * p.scm;
+    if (row < p.M) {
+      const float alpha = p.alpha_rows ? p.alpha_rows[(int64_t)bz * p.M + row] : 1.f;
+      float* crow = p.C + bz * p.scb + (int64_t)row * p.scm;
+      const bool vec = p.scn == 1 && n0 + BN <= p.N &&
+                       ((reinterpret_cast<uintptr_t>(crow + n0) & 15) == 0);
+      if (vec) {
+        float4* dst = reinterpret_cast<float4*>(crow + n0);
 #pragma unroll
-    for (int c = 0; c < BN; c += 32) {
-      uint32_t r[32];
-      const uint32_t taddr = tmem_base + ((uint32_t)(quarter * 32) << 16) + (uint32_t)c;
-      asm volatile(
-          "tcgen05.ld.sync.aligned.32x32b.x32.b32 "
-          "{%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, %15, "
-          "%16, %17, %18, %19, %20, %21, %22, %23, %24, %25, %26, %27, %28, %29, %30, %31}, [%32];"
-          : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
-            "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]),
-            "=r"(r[13]), "=r"(r[14]), "=r"(r[15]), "=r"(r[16]), "=r"(r[17]), "=r"(r[18]),
-            "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]), "=r"(r[24]),
-            "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]),
-            "=r"(r[31])
-          : "r"(taddr));
-      asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-      if (row < p.M) {
-        const int col0 = n0 + c;
-        if (p.scn == 1 && col0 + 32 <= p.N && ((reinterpret_cast<uintptr_t>(crow + col0) & 15) == 0)) {
-          float4* dst = reinterpret_cast<float4*>(crow + col0);
-#pragma unroll
-          for (int j = 0; j < 8; ++j) {
-            float4 v = make_float4(__uint_as_float(r[4 * j]) * alpha, __uint_as_float(r[4 * j + 1]) * alpha,
-                                   __uint_as_float(r[4 * j + 2]) * alpha,
-                                   __uint_as_float(r[4 * j + 3]) * alpha);
-            if (p.accumulate) {
-              float4 o = dst[j];
-              v.x += o.x; v.y += o.y; v.z += o.z; v.w += o.w;
-            }
-            dst[j] = v;
+        for (int j = 0; j < BN / 4; ++j) {
+          float4 v = make_float4(acc[4 * j] * alpha, acc[4 * j + 1] * alpha,
+                                 acc[4 * j + 2] * alpha, acc[4 * j + 3] * alpha);
+          if (p.accumulate) {
+            float4 o = dst[j];
+            v.x += o.x; v.y += o.y; v.z += o.z; v.w += o.w;
           }
-        } else {
+          dst[j] = v;
+        }
+      } else {
 #pragma unroll
-          for (int j = 0; j < 32; ++j) {
-            int col = col0 + j;
-            if (col < p.N) {
-              float* q = crow + (int64_t)col * p.scn;
-              float v = __uint_as_float(r[j]) * alpha;
-              *q = p.accumulate ? *q + v : v;
-            }
+        for (int j = 0; j < BN; ++j) {
+          const int col = n0 + j;
+          if (col < p.N) {
+            float* q = crow + (int64_t)col * p.scn;
+            const float v = acc[j] * alpha;
+            *q = p.accumulate ? *q + v : v;
           }
         }
       }

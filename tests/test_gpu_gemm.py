@@ -106,3 +106,14 @@ def test_gemm_tcgen05_matches_simt_error_scale(env, k):
     e_tc = np.max(np.abs(_run(env, a, b, 2, transpose_b=True) - want))
     e_simt = np.max(np.abs(_run(env, a, b, 1, transpose_b=True) - want))
     assert e_tc < 8 * e_simt + 1e-7, (e_tc, e_simt)
+
+
+def test_gemm_tcgen05_no_accumulation_bias(env):
+    """Truncating in-TMEM accumulation would bias results toward zero linearly
+    in K; the chunked RN accumulation must not."""
+    r = np.random.default_rng(5)
+    a, b = _operands(r, (256, 8192), (8192, 256))
+    want = a @ b
+    got = _run(env, a, b, 2, transpose_b=True)
+    bias = np.mean((got - want) * np.sign(want))
+    assert abs(bias) < 5e-7, bias
