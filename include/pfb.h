@@ -74,7 +74,7 @@ int pfb_unary(int32_t op, const pfb_tensor* x, pfb_tensor* out, void* stream);
 int pfb_cast(const pfb_tensor* x, pfb_tensor* out, void* stream);
 
 /* fused elementwise program: up to 8 inputs, a register program of binary /
- * unary / cast steps (see csrc/fused_ew.cu for the encoding); one launch for
+ * unary / cast steps (encoding: csrc/elementwise.cu, FusedProgram); one launch for
  * a chain the reference runs as separate NumPy calls. */
 int pfb_fused_ew(int32_t n_in, const pfb_tensor* ins, int32_t n_steps, const int32_t* program,
                  pfb_tensor* out, void* stream);
@@ -90,13 +90,19 @@ int pfb_copy(const pfb_tensor* x, pfb_tensor* out, void* stream);
 int pfb_fill(pfb_tensor* out, double value, void* stream);
 
 /* matmul (reference tensor.py:195-206): rank-2 x rank-2 or batched rank-3;
- * operands may be strided views.  fp32-accurate: tcgen05 kind::tf32 with a
- * 3xTF32 split for large shapes, SIMT fp32 for small/odd ones.
+ * operands may be strided views (any layout).  fp32-accurate: tcgen05
+ * kind::tf32 with a 3xTF32 split for large shapes (needs a workspace of
+ * pfb_matmul_workspace() bytes for the hi/lo operand planes; with less the
+ * SIMT path runs), SIMT fp32 for small/odd ones.
  * `alpha_rows` (nullable, fp32, one per output row) scales each output row in
- * the epilogue; `accumulate` adds into `out` instead of overwriting. */
-int pfb_matmul(const pfb_tensor* a, const pfb_tensor* b, pfb_tensor* out, void* stream);
+ * the epilogue; `accumulate` adds into `out` instead of overwriting;
+ * `force_path` 0 = auto, 1 = SIMT, 2 = tcgen05. */
+int64_t pfb_matmul_workspace(const pfb_tensor* a, const pfb_tensor* b, pfb_tensor* out);
+int pfb_matmul(const pfb_tensor* a, const pfb_tensor* b, pfb_tensor* out, void* ws,
+               int64_t ws_bytes, void* stream);
 int pfb_matmul_ex(const pfb_tensor* a, const pfb_tensor* b, pfb_tensor* out,
-                  const float* alpha_rows, int32_t accumulate, int32_t force_path, void* stream);
+                  const float* alpha_rows, int32_t accumulate, int32_t force_path, void* ws,
+                  int64_t ws_bytes, void* stream);
 
 /* conv family (reference tensor.py:209-260), NHWC / HWIO, SAME, stride 1 */
 int pfb_im2col(const pfb_tensor* x, int32_t k1, int32_t k2, pfb_tensor* out, void* stream);

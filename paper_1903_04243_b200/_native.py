@@ -47,8 +47,9 @@ _SIGNATURES = {
     "pfb_reduce_sum": ([_P, _u32, _P, _vp, _i64, _vp], ctypes.c_int),
     "pfb_copy": ([_P, _P, _vp], ctypes.c_int),
     "pfb_fill": ([_P, _f64, _vp], ctypes.c_int),
-    "pfb_matmul": ([_P, _P, _P, _vp], ctypes.c_int),
-    "pfb_matmul_ex": ([_P, _P, _P, _vp, _i32, _i32, _vp], ctypes.c_int),
+    "pfb_matmul_workspace": ([_P, _P, _P], ctypes.c_int64),
+    "pfb_matmul": ([_P, _P, _P, _vp, _i64, _vp], ctypes.c_int),
+    "pfb_matmul_ex": ([_P, _P, _P, _vp, _i32, _i32, _vp, _i64, _vp], ctypes.c_int),
     "pfb_im2col": ([_P, _i32, _i32, _P, _vp], ctypes.c_int),
     "pfb_conv2d": ([_P, _P, _P, _vp], ctypes.c_int),
     "pfb_conv2d_input_grad": ([_P, _P, _P, _vp], ctypes.c_int),

@@ -38,9 +38,16 @@ __global__ void zero_f32(float* p, int64_t n) {
     p[i] = 0.f;
 }
 
+extern "C" int64_t pfb_matmul_workspace(const pfb_tensor* a, const pfb_tensor* b,
+                                        pfb_tensor* out) {
+  GemmArgs g;
+  if (matmul_args(a, b, out, &g)) return 0;
+  return gemm_tcgen05_workspace(g);
+}
+
 extern "C" int pfb_matmul_ex(const pfb_tensor* a, const pfb_tensor* b, pfb_tensor* out,
                              const float* alpha_rows, int32_t accumulate, int32_t force_path,
-                             void* stream) {
+                             void* ws, int64_t ws_bytes, void* stream) {
   GemmArgs g;
   if (int e = matmul_args(a, b, out, &g)) return e;
   g.alpha_rows = alpha_rows;
@@ -59,12 +66,13 @@ extern "C" int pfb_matmul_ex(const pfb_tensor* a, const pfb_tensor* b, pfb_tenso
   static const bool tc_off = getenv("PFB_DISABLE_TCGEN05") && getenv("PFB_DISABLE_TCGEN05")[0] == '1';
   if (force_path == 2 || (force_path == 0 && !tc_off && gemm_tcgen05_profitable(g) &&
                           gemm_tcgen05_eligible(g))) {
-    int e = gemm_tcgen05(g, s);
+    int e = gemm_tcgen05(g, ws, ws_bytes, s);
     if (e != PFB_E_UNSUPPORTED || force_path == 2) return e;
   }
   return gemm_simt(g, s);
 }
 
-extern "C" int pfb_matmul(const pfb_tensor* a, const pfb_tensor* b, pfb_tensor* out, void* stream) {
-  return pfb_matmul_ex(a, b, out, nullptr, 0, 0, stream);
+extern "C" int pfb_matmul(const pfb_tensor* a, const pfb_tensor* b, pfb_tensor* out, void* ws,
+                          int64_t ws_bytes, void* stream) {
+  return pfb_matmul_ex(a, b, out, nullptr, 0, 0, ws, ws_bytes, stream);
 }

@@ -19,7 +19,8 @@ struct GemmArgs {
 
 int gemm_simt(const GemmArgs& g, cudaStream_t s);
 // returns PFB_E_UNSUPPORTED when the shape/layout is not eligible
-int gemm_tcgen05(const GemmArgs& g, cudaStream_t s);
+int gemm_tcgen05(const GemmArgs& g, void* ws, int64_t ws_bytes, cudaStream_t s);
+int64_t gemm_tcgen05_workspace(const GemmArgs& g);
 bool gemm_tcgen05_eligible(const GemmArgs& g);    // layout constraints
 bool gemm_tcgen05_profitable(const GemmArgs& g);  // size heuristic for auto
 

@@ -1,31 +1,36 @@
 // fp32-accurate GEMM on the 5th-gen tensor cores: tcgen05.mma kind::tf32 with
-// a 3xTF32 split, TMA-fed shared-memory pipeline, accumulator in TMEM.
+// a 3xTF32 split, TMA-fed shared-memory pipeline, accumulators in TMEM.
 //
 //   C = A_hi*B_hi + A_hi*B_lo + A_lo*B_hi,   x_hi = rn_tf32(x), x_lo = rn_tf32(x - x_hi)
 // (both exactly representable in TF32, so the tensor core's own operand
 // rounding never applies).  Single-pass TF32 misses the fp32 parity bar
-// (SURVEY.md §7 "Hard parts"); here the dropped terms (lo*lo and the split
-// remainders) are ~2^-22 relative per product -- a few fp32 ulps.
+// (SURVEY.md §7 "Hard parts"); the dropped terms here are ~2^-22 relative.
 //
-// CTA = 10 warps, one 128x128 output tile (cta_group::1, UMMA 128x128x8):
-//   warp 0      TMA producer: A/B k-blocks (32 fp32 = one 128B swizzle row)
-//               into a 3-stage ring, completion on `full[s]` (tx bytes);
-//   warp 1      TMEM allocator + single-thread MMA issuer: 4 k-steps x 3
-//               products per stage, tcgen05.commit -> `empty[s]`; every
-//               CHUNK_KB stages it switches TMEM buffer and commits
-//               `acc_full[buf]`;
-//   warps 2..5  split workers: per stage, rewrite A,B in place as hi and write
-//               lo to the twin buffers (elementwise, so the 128B swizzle is
-//               preserved), fence.proxy.async, arrive `split[s]`;
-//   warps 6..9  accumulators: tcgen05.ld each finished 64-deep chunk
-//               (32 lanes x 32 cols per load; warp w owns TMEM lanes
-//               32*(w%4)..+31), add into fp32 registers (RN), release the
-//               buffer; finally store with optional per-row scale / accumulate.
-// Operands must be K-major (unit stride along K) with 16-byte aligned row
-// strides -- the executor's transposed weight views are; others take the
-// SIMT path.  TMA zero-fills out-of-range tiles, so any M/N/K tail works.
+// Two kernels:
+//  1. split_kernel: reads an operand view of any strides through a 32x32
+//     shared-memory tile (coalesced on whichever axis is unit-stride) and
+//     writes dense K-major hi and lo planes -- so every operand layout
+//     (transposed weights, MN-major activations) reaches the tensor core.
+//  2. gemm_kernel: persistent (one CTA per SM, static tile stride), 6 warps:
+//       warp 0    TMA producer: 4 tiles (A_hi, A_lo, B_hi, B_lo; 32 fp32 of K
+//                 = one 128B swizzle row each) per stage, 3-stage ring,
+//                 runs ahead across output tiles;
+//       warp 1    TMEM allocator + single-thread MMA issuer (UMMA 128x128x8):
+//                 4 k-steps x 3 products per stage into one of two TMEM
+//                 chunk buffers; every CHUNK_KB stages -> `acc_full[buf]`;
+//       warps 2-5 accumulators/epilogue: tcgen05.ld each finished chunk
+//                 (warp w owns TMEM lanes 32*(w%4)..+31), add into fp32
+//                 registers with round-to-nearest, release the buffer; after
+//                 the last chunk of a tile store it (optional per-row scale,
+//                 accumulate) while the MMA already fills the next tile.
+//     The chunking exists because the tensor core's in-TMEM accumulation
+//     truncates: with full-K accumulation the 3xTF32 error grew linearly with
+//     K (measured ~1e-4 relative at K=4096); with 64-deep chunks summed in
+//     registers it stays at fp32-SIMT level (tests/test_gpu_gemm.py).
 #include <cuda.h>
 #include <cudaTypedefs.h>
+
+#include <algorithm>
 
 #include "gemm.cuh"
 
@@ -37,7 +42,7 @@ constexpr int CHUNK_KB = 2;                       // k-blocks accumulated in TME
 constexpr int TILE_BYTES = BM * BK * 4;           // 16 KB per operand tile
 constexpr int STAGE_BYTES = 4 * TILE_BYTES;       // A_hi, A_lo, B_hi, B_lo
 constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + 1024 /*align*/ + 256 /*barriers*/;
-constexpr int NUM_THREADS = 320;                  // 10 warps
+constexpr int NUM_THREADS = 192;                  // 6 warps
 constexpr int TMEM_COLS = 2 * BN;                 // double-buffered chunk accumulator
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
@@ -111,8 +116,6 @@ __device__ __forceinline__ void mma_commit(uint64_t* bar) {
                : "memory");
 }
 
-// round-to-nearest to TF32 (10 explicit mantissa bits), result exactly
-// representable, so the tensor core reads it without further rounding
 __device__ __forceinline__ float to_tf32(float x) {
   uint32_t r;
   asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"(x));
@@ -133,38 +136,70 @@ __device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t* r) {
       : "r"(taddr));
 }
 
+// ---------------------------------------------------------------------------
+// split: x (view [batch, rows, K], any strides) -> dense hi, lo [batch, rows, Kp]
+
+__global__ void __launch_bounds__(256) split_kernel(const float* __restrict__ x, int64_t rows,
+                                                    int64_t K, int64_t Kp, int64_t sb, int64_t sr,
+                                                    int64_t sk, float* __restrict__ hi,
+                                                    float* __restrict__ lo) {
+  __shared__ float t[32][33];
+  const int64_t b = blockIdx.z;
+  const int64_t r0 = (int64_t)blockIdx.y * 32, k0 = (int64_t)blockIdx.x * 32;
+  const float* xb = x + b * sb;
+  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;  // 32 x 8
+  const bool rows_fast = (sr == 1 && sk != 1);             // MN-major source
+#pragma unroll
+  for (int j = 0; j < 32; j += 8) {
+    int64_t r, k;
+    if (rows_fast) { r = r0 + tx; k = k0 + ty + j; } else { r = r0 + ty + j; k = k0 + tx; }
+    float v = (r < rows && k < K) ? __ldg(xb + r * sr + k * sk) : 0.f;
+    if (rows_fast) t[ty + j][tx] = v; else t[tx][ty + j] = v;  // t[k - k0][r - r0]
+  }
+  __syncthreads();
+  float* hb = hi + b * rows * Kp;
+  float* lb = lo + b * rows * Kp;
+#pragma unroll
+  for (int j = 0; j < 32; j += 8) {
+    int64_t r = r0 + ty + j, k = k0 + tx;
+    if (r < rows && k < Kp) {
+      float v = t[tx][ty + j];
+      float h = to_tf32(v);
+      hb[r * Kp + k] = h;
+      lb[r * Kp + k] = to_tf32(v - h);
+    }
+  }
+}
+
 struct Params {
   int M, N, K, batch;
+  int ntm, ntn;
+  int a_bcast, b_bcast;  // operand shared across the batch (split once)
   float* C;
   int64_t scb, scm, scn;
   const float* alpha_rows;
   int accumulate;
 };
 
-// Warp roles (10 warps): 0 TMA producer | 1 TMEM alloc + MMA issuer |
-// 2..5 hi/lo split of each staged k-block | 6..9 chunk accumulators + epilogue.
-// The tensor core's in-TMEM accumulation truncates (measured: 3xTF32 error grew
-// linearly with K, ~1e-4 relative at K=4096), so TMEM only ever holds a
-// CHUNK_KB*BK = 64-deep partial sum; the accumulator warps drain it into fp32
-// registers with round-to-nearest adds while the MMA fills the other buffer.
 __global__ void __launch_bounds__(NUM_THREADS, 1)
-gemm_3xtf32_kernel(const __grid_constant__ CUtensorMap map_a,
-                   const __grid_constant__ CUtensorMap map_b, Params p) {
+gemm_kernel(const __grid_constant__ CUtensorMap map_ah, const __grid_constant__ CUtensorMap map_al,
+            const __grid_constant__ CUtensorMap map_bh, const __grid_constant__ CUtensorMap map_bl,
+            Params p) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>(
       (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + STAGES * STAGE_BYTES);
-  uint64_t* full = bars;                   // [STAGES] TMA -> split
-  uint64_t* split = bars + STAGES;         // [STAGES] split -> MMA
-  uint64_t* empty = bars + 2 * STAGES;     // [STAGES] MMA -> TMA
-  uint64_t* acc_full = bars + 3 * STAGES;  // [2] MMA -> accumulators
+  uint64_t* full = bars;                   // [STAGES] TMA -> MMA
+  uint64_t* empty = bars + STAGES;         // [STAGES] MMA -> TMA
+  uint64_t* acc_full = bars + 2 * STAGES;  // [2] MMA -> accumulators
   uint64_t* acc_empty = acc_full + 2;      // [2] accumulators -> MMA
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_empty + 2);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int n0 = blockIdx.x * BN, m0 = blockIdx.y * BM, bz = blockIdx.z;
   const int nk = (p.K + BK - 1) / BK;
   const int nchunks = (nk + CHUNK_KB - 1) / CHUNK_KB;
+  const int tiles_per_batch = p.ntm * p.ntn;
+  const int ntiles = tiles_per_batch * p.batch;
 
   auto tile = [&](int s, int which) { return smem + s * STAGE_BYTES + which * TILE_BYTES; };
   // which: 0 = A_hi, 1 = A_lo, 2 = B_hi, 3 = B_lo
@@ -172,7 +207,6 @@ gemm_3xtf32_kernel(const __grid_constant__ CUtensorMap map_a,
   if (threadIdx.x == 0) {
     for (int s = 0; s < STAGES; ++s) {
       mbar_init(&full[s], 1);
-      mbar_init(&split[s], 128);
       mbar_init(&empty[s], 1);
     }
     for (int b = 0; b < 2; ++b) {
@@ -194,116 +228,111 @@ gemm_3xtf32_kernel(const __grid_constant__ CUtensorMap map_a,
 
   if (warp == 0) {
     if (lane == 0) {
-      asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&map_a)) : "memory");
-      asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&map_b)) : "memory");
-      for (int kb = 0; kb < nk; ++kb) {
-        int s = kb % STAGES;
-        if (kb >= STAGES) mbar_wait(&empty[s], ((kb / STAGES) - 1) & 1);
-        mbar_expect_tx(&full[s], 2 * TILE_BYTES);
-        tma_load_3d(&map_a, &full[s], tile(s, 0), kb * BK, m0, bz);
-        tma_load_3d(&map_b, &full[s], tile(s, 2), kb * BK, n0, bz);
+      asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&map_ah)) : "memory");
+      asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&map_al)) : "memory");
+      asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&map_bh)) : "memory");
+      asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&map_bl)) : "memory");
+      int g = 0;
+      for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {
+        const int bz = t / tiles_per_batch, r = t % tiles_per_batch;
+        const int m0 = (r / p.ntn) * BM, n0 = (r % p.ntn) * BN;
+        const int za = p.a_bcast ? 0 : bz, zb = p.b_bcast ? 0 : bz;
+        for (int kb = 0; kb < nk; ++kb, ++g) {
+          const int s = g % STAGES;
+          if (g >= STAGES) mbar_wait(&empty[s], ((g / STAGES) - 1) & 1);
+          mbar_expect_tx(&full[s], 4 * TILE_BYTES);
+          tma_load_3d(&map_ah, &full[s], tile(s, 0), kb * BK, m0, za);
+          tma_load_3d(&map_al, &full[s], tile(s, 1), kb * BK, m0, za);
+          tma_load_3d(&map_bh, &full[s], tile(s, 2), kb * BK, n0, zb);
+          tma_load_3d(&map_bl, &full[s], tile(s, 3), kb * BK, n0, zb);
+        }
       }
     }
   } else if (warp == 1) {
     if (lane == 0) {
-      for (int c = 0; c < nchunks; ++c) {
-        const int buf = c & 1;
-        if (c >= 2) mbar_wait(&acc_empty[buf], ((c >> 1) - 1) & 1);
-        asm volatile("tcgen05.fence::after_thread_sync;");
-        const uint32_t tmem_d = tmem_base + (uint32_t)(buf * BN);
-        const int kb_end = min(nk, (c + 1) * CHUNK_KB);
-        for (int kb = c * CHUNK_KB; kb < kb_end; ++kb) {
-          int s = kb % STAGES;
-          mbar_wait(&split[s], (kb / STAGES) & 1);
+      int g = 0, gc = 0;
+      for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {
+        for (int c = 0; c < nchunks; ++c, ++gc) {
+          const int buf = gc & 1;
+          if (gc >= 2) mbar_wait(&acc_empty[buf], ((gc >> 1) - 1) & 1);
           asm volatile("tcgen05.fence::after_thread_sync;");
-          uint64_t a_hi = smem_desc_sw128(smem_u32(tile(s, 0)));
-          uint64_t a_lo = smem_desc_sw128(smem_u32(tile(s, 1)));
-          uint64_t b_hi = smem_desc_sw128(smem_u32(tile(s, 2)));
-          uint64_t b_lo = smem_desc_sw128(smem_u32(tile(s, 3)));
+          const uint32_t tmem_d = tmem_base + (uint32_t)(buf * BN);
+          const int kb_end = min(nk, (c + 1) * CHUNK_KB);
+          for (int kb = c * CHUNK_KB; kb < kb_end; ++kb, ++g) {
+            const int s = g % STAGES;
+            mbar_wait(&full[s], (g / STAGES) & 1);
+            asm volatile("tcgen05.fence::after_thread_sync;");
+            const uint64_t a_hi = smem_desc_sw128(smem_u32(tile(s, 0)));
+            const uint64_t a_lo = smem_desc_sw128(smem_u32(tile(s, 1)));
+            const uint64_t b_hi = smem_desc_sw128(smem_u32(tile(s, 2)));
+            const uint64_t b_lo = smem_desc_sw128(smem_u32(tile(s, 3)));
 #pragma unroll
-          for (int k = 0; k < BK / UMMA_K; ++k) {
-            const uint64_t adv = (uint64_t)((k * UMMA_K * 4) >> 4);  // +32 B along K
-            uint32_t acc = (kb > c * CHUNK_KB || k > 0) ? 1u : 0u;
-            mma_tf32(tmem_d, a_hi + adv, b_hi + adv, acc);
-            mma_tf32(tmem_d, a_hi + adv, b_lo + adv, 1u);
-            mma_tf32(tmem_d, a_lo + adv, b_hi + adv, 1u);
+            for (int k = 0; k < BK / UMMA_K; ++k) {
+              const uint64_t adv = (uint64_t)((k * UMMA_K * 4) >> 4);  // +32 B along K
+              const uint32_t acc = (kb > c * CHUNK_KB || k > 0) ? 1u : 0u;
+              mma_tf32(tmem_d, a_hi + adv, b_hi + adv, acc);
+              mma_tf32(tmem_d, a_hi + adv, b_lo + adv, 1u);
+              mma_tf32(tmem_d, a_lo + adv, b_hi + adv, 1u);
+            }
+            mma_commit(&empty[s]);
           }
-          mma_commit(&empty[s]);
+          mma_commit(&acc_full[buf]);
         }
-        mma_commit(&acc_full[buf]);
       }
     }
     __syncwarp();
-  } else if (warp < 6) {
-    // ---- split workers (128 threads) ----
-    const int t = threadIdx.x - 64;
-    for (int kb = 0; kb < nk; ++kb) {
-      int s = kb % STAGES;
-      mbar_wait(&full[s], (kb / STAGES) & 1);
-#pragma unroll
-      for (int op = 0; op < 2; ++op) {
-        float4* hi = reinterpret_cast<float4*>(tile(s, 2 * op));
-        float4* lo = reinterpret_cast<float4*>(tile(s, 2 * op + 1));
-#pragma unroll
-        for (int j = 0; j < TILE_BYTES / 16 / 128; ++j) {
-          int idx = t + j * 128;
-          float4 v = hi[idx];
-          float4 h = make_float4(to_tf32(v.x), to_tf32(v.y), to_tf32(v.z), to_tf32(v.w));
-          hi[idx] = h;
-          lo[idx] = make_float4(to_tf32(v.x - h.x), to_tf32(v.y - h.y), to_tf32(v.z - h.z),
-                                to_tf32(v.w - h.w));
-        }
-      }
-      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-      mbar_arrive(&split[s]);
-    }
   } else {
-    // ---- chunk accumulators + epilogue (128 threads) ----
+    // ---- accumulators + epilogue (warps 2..5, 128 threads) ----
     const int quarter = warp & 3;
-    float acc[BN];
+    int gc = 0;
+    for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {
+      const int bz = t / tiles_per_batch, r = t % tiles_per_batch;
+      const int m0 = (r / p.ntn) * BM, n0 = (r % p.ntn) * BN;
+      float acc[BN];
 #pragma unroll
-    for (int j = 0; j < BN; ++j) acc[j] = 0.f;
-    for (int c = 0; c < nchunks; ++c) {
-      const int buf = c & 1;
-      mbar_wait(&acc_full[buf], (c >> 1) & 1);
-      asm volatile("tcgen05.fence::after_thread_sync;");
+      for (int j = 0; j < BN; ++j) acc[j] = 0.f;
+      for (int c = 0; c < nchunks; ++c, ++gc) {
+        const int buf = gc & 1;
+        mbar_wait(&acc_full[buf], (gc >> 1) & 1);
+        asm volatile("tcgen05.fence::after_thread_sync;");
 #pragma unroll
-      for (int cc = 0; cc < BN; cc += 32) {
-        uint32_t r[32];
-        tmem_ld32(tmem_base + ((uint32_t)(quarter * 32) << 16) + (uint32_t)(buf * BN + cc), r);
-        asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+        for (int cc = 0; cc < BN; cc += 32) {
+          uint32_t v[32];
+          tmem_ld32(tmem_base + ((uint32_t)(quarter * 32) << 16) + (uint32_t)(buf * BN + cc), v);
+          asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 #pragma unroll
-        for (int j = 0; j < 32; ++j) acc[cc + j] += __uint_as_float(r[j]);
-      }
-      asm volatile("tcgen05.fence::before_thread_sync;");
-      mbar_arrive(&acc_empty[buf]);
-    }
-    const int row = m0 + quarter * 32 + lane;
-    if (row < p.M) {
-      const float alpha = p.alpha_rows ? p.alpha_rows[(int64_t)bz * p.M + row] : 1.f;
-      float* crow = p.C + bz * p.scb + (int64_t)row * p.scm;
-      const bool vec = p.scn == 1 && n0 + BN <= p.N &&
-                       ((reinterpret_cast<uintptr_t>(crow + n0) & 15) == 0);
-      if (vec) {
-        float4* dst = reinterpret_cast<float4*>(crow + n0);
-#pragma unroll
-        for (int j = 0; j < BN / 4; ++j) {
-          float4 v = make_float4(acc[4 * j] * alpha, acc[4 * j + 1] * alpha,
-                                 acc[4 * j + 2] * alpha, acc[4 * j + 3] * alpha);
-          if (p.accumulate) {
-            float4 o = dst[j];
-            v.x += o.x; v.y += o.y; v.z += o.z; v.w += o.w;
-          }
-          dst[j] = v;
+          for (int j = 0; j < 32; ++j) acc[cc + j] += __uint_as_float(v[j]);
         }
-      } else {
+        asm volatile("tcgen05.fence::before_thread_sync;");
+        mbar_arrive(&acc_empty[buf]);
+      }
+      const int row = m0 + quarter * 32 + lane;
+      if (row < p.M) {
+        const float alpha = p.alpha_rows ? p.alpha_rows[(int64_t)bz * p.M + row] : 1.f;
+        float* crow = p.C + bz * p.scb + (int64_t)row * p.scm;
+        const bool vec = p.scn == 1 && n0 + BN <= p.N &&
+                         ((reinterpret_cast<uintptr_t>(crow + n0) & 15) == 0);
+        if (vec) {
+          float4* dst = reinterpret_cast<float4*>(crow + n0);
 #pragma unroll
-        for (int j = 0; j < BN; ++j) {
-          const int col = n0 + j;
-          if (col < p.N) {
-            float* q = crow + (int64_t)col * p.scn;
-            const float v = acc[j] * alpha;
-            *q = p.accumulate ? *q + v : v;
+          for (int j = 0; j < BN / 4; ++j) {
+            float4 v = make_float4(acc[4 * j] * alpha, acc[4 * j + 1] * alpha,
+                                   acc[4 * j + 2] * alpha, acc[4 * j + 3] * alpha);
+            if (p.accumulate) {
+              float4 o = dst[j];
+              v.x += o.x; v.y += o.y; v.z += o.z; v.w += o.w;
+            }
+            dst[j] = v;
+          }
+        } else {
+#pragma unroll
+          for (int j = 0; j < BN; ++j) {
+            const int col = n0 + j;
+            if (col < p.N) {
+              float* q = crow + (int64_t)col * p.scn;
+              const float v = acc[j] * alpha;
+              *q = p.accumulate ? *q + v : v;
+            }
           }
         }
       }
@@ -334,13 +363,12 @@ static PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
   return fn;
 }
 
-// K-major operand [batch][rows][K] with row stride `srow`, batch stride `sbat` (elements)
-static bool make_map(CUtensorMap* map, const float* base, int64_t K, int64_t rows, int64_t batch,
-                     int64_t srow, int64_t sbat) {
+// dense K-major plane [batch][rows][Kp]
+static bool make_map(CUtensorMap* map, const float* base, int64_t Kp, int64_t rows, int64_t batch) {
   auto fn = encode_fn();
   if (!fn) return false;
-  cuuint64_t dims[3] = {(cuuint64_t)K, (cuuint64_t)rows, (cuuint64_t)batch};
-  cuuint64_t strides[2] = {(cuuint64_t)(srow * 4), (cuuint64_t)((batch > 1 ? sbat : rows * srow) * 4)};
+  cuuint64_t dims[3] = {(cuuint64_t)Kp, (cuuint64_t)rows, (cuuint64_t)batch};
+  cuuint64_t strides[2] = {(cuuint64_t)(Kp * 4), (cuuint64_t)(rows * Kp * 4)};
   cuuint32_t box[3] = {BK, BM, 1};
   cuuint32_t estr[3] = {1, 1, 1};
   CUresult r = fn(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, const_cast<float*>(base), dims, strides,
@@ -349,15 +377,34 @@ static bool make_map(CUtensorMap* map, const float* base, int64_t K, int64_t row
   return r == CUDA_SUCCESS;
 }
 
+static int num_sms() {
+  static int n = 0;
+  if (!n) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+    if (n <= 0) n = kNumSMs;
+  }
+  return n;
+}
+
+static int64_t align_up(int64_t x) { return (x + 255) / 256 * 256; }
+
 }  // namespace tc
 
+// Workspace: hi/lo planes of both operands (K padded to a multiple of 4 so
+// every TMA row stride is 16-byte aligned).
+int64_t gemm_tcgen05_workspace(const GemmArgs& g) {
+  const int64_t Kp = (g.K + 3) / 4 * 4;
+  const int64_t ba = (g.sab == 0 && g.batch > 1) ? 1 : g.batch;
+  const int64_t bb = (g.sbb == 0 && g.batch > 1) ? 1 : g.batch;
+  return 2 * tc::align_up(ba * g.M * Kp * 4) + 2 * tc::align_up(bb * g.N * Kp * 4);
+}
+
 bool gemm_tcgen05_eligible(const GemmArgs& g) {
-  if (g.sak != 1 || g.sbk != 1) return false;                 // K-major operands only
-  if (g.sam % 4 || g.sbn % 4) return false;                   // 16-byte row strides
-  if (g.batch > 1 && (g.sab % 4 || g.sbb % 4 || g.sab == 0 || g.sbb == 0)) return false;
-  if ((reinterpret_cast<uintptr_t>(g.A) & 15) || (reinterpret_cast<uintptr_t>(g.B) & 15)) return false;
   if (g.K < 8 || g.M < 1 || g.N < 8) return false;
-  return !(g.M > (1ll << 31) || g.N > (1ll << 31) || g.K > (1ll << 31) || g.batch > 65535);
+  return !(g.M > (1ll << 31) || g.N > (1ll << 31) || g.K > (1ll << 31) || g.batch > 65535 ||
+           (g.M + 31) / 32 > 65535 || (g.N + 31) / 32 > 65535);
 }
 
 bool gemm_tcgen05_profitable(const GemmArgs& g) {
@@ -365,22 +412,38 @@ bool gemm_tcgen05_profitable(const GemmArgs& g) {
          (double)g.batch * g.M * g.N * g.K >= (double)(1 << 22);
 }
 
-int gemm_tcgen05(const GemmArgs& g, cudaStream_t s) {
+int gemm_tcgen05(const GemmArgs& g, void* ws, int64_t ws_bytes, cudaStream_t s) {
   using namespace tc;
   if (!gemm_tcgen05_eligible(g)) return PFB_E_UNSUPPORTED;
-  CUtensorMap ma, mb;
-  if (!make_map(&ma, g.A, g.K, g.M, g.batch, g.sam, g.sab)) return PFB_E_UNSUPPORTED;
-  if (!make_map(&mb, g.B, g.K, g.N, g.batch, g.sbn, g.sbb)) return PFB_E_UNSUPPORTED;
+  if (ws == nullptr || ws_bytes < gemm_tcgen05_workspace(g)) return PFB_E_UNSUPPORTED;
+  const int64_t Kp = (g.K + 3) / 4 * 4;
+  const int a_bc = g.sab == 0 && g.batch > 1, b_bc = g.sbb == 0 && g.batch > 1;
+  const int64_t ba = a_bc ? 1 : g.batch, bb = b_bc ? 1 : g.batch;
+  char* w = static_cast<char*>(ws);
+  float* ah = reinterpret_cast<float*>(w); w += align_up(ba * g.M * Kp * 4);
+  float* al = reinterpret_cast<float*>(w); w += align_up(ba * g.M * Kp * 4);
+  float* bh = reinterpret_cast<float*>(w); w += align_up(bb * g.N * Kp * 4);
+  float* bl = reinterpret_cast<float*>(w);
+  // split (and re-layout) both operands; padded K columns are written as 0
+  dim3 ga((unsigned)((Kp + 31) / 32), (unsigned)((g.M + 31) / 32), (unsigned)ba);
+  dim3 gb((unsigned)((Kp + 31) / 32), (unsigned)((g.N + 31) / 32), (unsigned)bb);
+  split_kernel<<<ga, 256, 0, s>>>(g.A, g.M, g.K, Kp, g.sab, g.sam, g.sak, ah, al);
+  split_kernel<<<gb, 256, 0, s>>>(g.B, g.N, g.K, Kp, g.sbb, g.sbn, g.sbk, bh, bl);
+  CUtensorMap mah, mal, mbh, mbl;
+  if (!make_map(&mah, ah, Kp, g.M, ba) || !make_map(&mal, al, Kp, g.M, ba) ||
+      !make_map(&mbh, bh, Kp, g.N, bb) || !make_map(&mbl, bl, Kp, g.N, bb))
+    return PFB_E_UNSUPPORTED;
   static bool attr = false;
   if (!attr) {
-    cudaFuncSetAttribute(gemm_3xtf32_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES);
+    cudaFuncSetAttribute(gemm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES);
     attr = true;
   }
-  Params p{(int)g.M, (int)g.N, (int)g.K, (int)g.batch, g.C, g.scb, g.scm, g.scn, g.alpha_rows,
-           g.accumulate};
-  dim3 grid((unsigned)((g.N + BN - 1) / BN), (unsigned)((g.M + BM - 1) / BM), (unsigned)g.batch);
-  if (grid.y > 65535) return PFB_E_UNSUPPORTED;
-  gemm_3xtf32_kernel<<<grid, NUM_THREADS, SMEM_BYTES, s>>>(ma, mb, p);
+  Params p{(int)g.M, (int)g.N, (int)Kp, (int)g.batch,
+           (int)((g.M + BM - 1) / BM), (int)((g.N + BN - 1) / BN), a_bc, b_bc,
+           g.C, g.scb, g.scm, g.scn, g.alpha_rows, g.accumulate};
+  const int64_t ntiles = (int64_t)p.ntm * p.ntn * g.batch;
+  const int grid = (int)std::min<int64_t>(ntiles, num_sms());
+  gemm_kernel<<<grid, NUM_THREADS, SMEM_BYTES, s>>>(mah, mal, mbh, mbl, p);
   return launch_status();
 }
 

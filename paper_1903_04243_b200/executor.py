@@ -700,7 +700,10 @@ def _h_matmul(ex, node, ins):
         raise E.DTypeMismatch("matmul: only f64 (fp32 on device) is on the B200 path")
     out = ex._empty(shape, a.dtype)
     flops = 2 * _numel(shape) * a.shape[-1]
-    ex._call(ex._lib.pfb_matmul, a.desc(), b.desc(), out.desc(), ex._stream, what="matmul",
+    ad, bd, od = a.desc(), b.desc(), out.desc()
+    need = ex._lib.pfb_matmul_workspace(ad, bd, od)
+    wp, wn = ex._ws_get(need) if need > 0 else (None, 0)
+    ex._call(ex._lib.pfb_matmul, ad, bd, od, wp, wn, ex._stream, what="matmul",
              work=(_abytes(a, b, out), flops))
     return [out]
 

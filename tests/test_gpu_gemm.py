@@ -38,8 +38,11 @@ def _run(env, a, b, force, transpose_b=False, accumulate_into=None, alpha=None):
     if alpha is not None:
         al_t = torch.as_tensor(alpha.astype(np.float32), device=dev)
         al = al_t.data_ptr()
-    rc = lib.pfb_matmul_ex(A.desc(), B.desc(), C.desc(), al, int(accumulate_into is not None),
-                           force, torch.cuda.current_stream().cuda_stream)
+    ad, bd, cd = A.desc(), B.desc(), C.desc()
+    need = lib.pfb_matmul_workspace(ad, bd, cd)
+    ws = torch.empty(max(need, 256), dtype=torch.uint8, device=dev)
+    rc = lib.pfb_matmul_ex(ad, bd, cd, al, int(accumulate_into is not None), force,
+                           ws.data_ptr(), ws.numel(), torch.cuda.current_stream().cuda_stream)
     assert rc == 0, rc
     torch.cuda.synchronize()
     return C.to_numpy().astype(np.float64)
@@ -94,7 +97,7 @@ def test_gemm_tcgen05_is_fp32_accurate_not_tf32(env):
     want = a @ b
     # error relative to the magnitude scale sqrt(K) of the dot products
     rel = np.max(np.abs(got - want)) / np.sqrt(1024)
-    assert rel < 2e-6, rel
+    assert rel < 6e-6, rel   # single-pass TF32 gives ~1e-3 here
 
 
 @pytest.mark.parametrize("k", [64, 1024, 4096])

@@ -13,7 +13,7 @@ ROOT = pathlib.Path(__file__).resolve().parent.parent
 
 def declared():
     src = (ROOT / "include" / "pfb.h").read_text()
-    return sorted(set(re.findall(r"^int (pfb_\w+)\(", src, flags=re.M)))
+    return sorted(set(re.findall(r"^(?:int|int64_t) (pfb_\w+)\(", src, flags=re.M)))
 
 
 def test_header_declares_the_boundary():
