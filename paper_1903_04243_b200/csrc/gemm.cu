@@ -1,4 +1,5 @@
 // pfb_matmul: validation + path selection (reference tensor.py:195-206).
+#include <algorithm>
 #include <cstdlib>
 
 #include "gemm.cuh"
@@ -42,7 +43,7 @@ extern "C" int64_t pfb_matmul_workspace(const pfb_tensor* a, const pfb_tensor* b
                                         pfb_tensor* out) {
   GemmArgs g;
   if (matmul_args(a, b, out, &g)) return 0;
-  return gemm_tcgen05_workspace(g);
+  return std::max(gemm_tcgen05_workspace(g), gemm_simt_workspace(g));
 }
 
 extern "C" int pfb_matmul_ex(const pfb_tensor* a, const pfb_tensor* b, pfb_tensor* out,
@@ -69,7 +70,7 @@ extern "C" int pfb_matmul_ex(const pfb_tensor* a, const pfb_tensor* b, pfb_tenso
     int e = gemm_tcgen05(g, ws, ws_bytes, s);
     if (e != PFB_E_UNSUPPORTED || force_path == 2) return e;
   }
-  return gemm_simt(g, s);
+  return gemm_simt(g, ws, ws_bytes, s);
 }
 
 extern "C" int pfb_matmul(const pfb_tensor* a, const pfb_tensor* b, pfb_tensor* out, void* ws,

@@ -17,7 +17,8 @@ struct GemmArgs {
   int accumulate;           // C += result
 };
 
-int gemm_simt(const GemmArgs& g, cudaStream_t s);
+int gemm_simt(const GemmArgs& g, void* ws, int64_t ws_bytes, cudaStream_t s);
+int64_t gemm_simt_workspace(const GemmArgs& g);
 // returns PFB_E_UNSUPPORTED when the shape/layout is not eligible
 int gemm_tcgen05(const GemmArgs& g, void* ws, int64_t ws_bytes, cudaStream_t s);
 int64_t gemm_tcgen05_workspace(const GemmArgs& g);

@@ -1,36 +1,71 @@
-// SIMT fp32 GEMM for shapes the tensor-core path does not take: tiny M/N/K
-// (per-example conv filter grads 9x8, K=1 outer products, K=10 cotangents),
-// odd strides and ragged batches.  64x64x16 tiles, 256 threads, 4x4 register
-// micro-tile; operands staged through shared memory with the global read
-// mapped onto whichever of their two strides is unit (coalesced for both
-// normal and transposed views).  Exact fp32 FMA accumulation.
+// SIMT fp32 GEMM for shapes the tensor-core path does not take: tiny K
+// (K=1 outer products, K=10 cotangents), skinny M (batch-32 forward passes),
+// tiny per-example conv filter grads (9x8) and odd strides.
+//
+//  * tile kernel: 64x64x16 tiles, 256 threads, 4x4 register micro-tile;
+//    operands staged through shared memory with the global read mapped onto
+//    whichever of their two strides is unit (coalesced for normal and
+//    transposed views); 128-bit stores of 4 consecutive output columns.
+//    Split-K (grid.z = batch x splits) when there are too few tiles to fill
+//    148 SMs: per-split partials go to the workspace and a second pass sums
+//    them in split order (deterministic), applying the epilogue.
+//  * small-K kernel (K <= 16): store-bound; each thread produces 4 consecutive
+//    columns of one row (one 128-bit store), operands read through L1.
+// Exact fp32 FMA accumulation in both.
+#include <algorithm>
+
 #include "gemm.cuh"
 
 namespace pfb {
 
 constexpr int BM = 64, BN = 64, BK = 16;
 
-__global__ void __launch_bounds__(256) gemm_simt_kernel(GemmArgs g) {
+__device__ __forceinline__ void store_row4(const GemmArgs& g, int64_t b, int64_t m, int64_t n,
+                                           const float* v, float alpha) {
+  if (m >= g.M) return;
+  float* p = g.C + b * g.scb + m * g.scm + n * g.scn;
+  if (g.scn == 1 && n + 3 < g.N && ((reinterpret_cast<uintptr_t>(p) & 15) == 0)) {
+    float4 o = make_float4(v[0] * alpha, v[1] * alpha, v[2] * alpha, v[3] * alpha);
+    if (g.accumulate) {
+      float4 c = *reinterpret_cast<float4*>(p);
+      o.x += c.x; o.y += c.y; o.z += c.z; o.w += c.w;
+    }
+    *reinterpret_cast<float4*>(p) = o;
+    return;
+  }
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    if (n + j >= g.N) break;
+    float* q = p + j * g.scn;
+    const float x = v[j] * alpha;
+    *q = g.accumulate ? *q + x : x;
+  }
+}
+
+// partials: nullptr -> epilogue straight to C; else ws[split][b][M][N]
+__global__ void __launch_bounds__(256) gemm_simt_kernel(GemmArgs g, int splits, int64_t kchunk,
+                                                        float* partials) {
   __shared__ float As[BK][BM + 4];
   __shared__ float Bs[BK][BN + 4];
-  const int64_t b = blockIdx.z;
+  const int64_t bz = blockIdx.z / splits;
+  const int split = blockIdx.z % splits;
   const int64_t m0 = (int64_t)blockIdx.y * BM, n0 = (int64_t)blockIdx.x * BN;
-  const float* A = g.A + b * g.sab;
-  const float* B = g.B + b * g.sbb;
+  const int64_t kbeg = split * kchunk, kend = std::min<int64_t>(g.K, kbeg + kchunk);
+  const float* A = g.A + bz * g.sab;
+  const float* B = g.B + bz * g.sbb;
   const int tid = threadIdx.x;
   const int tm = (tid / 16) * 4, tn = (tid % 16) * 4;
   float acc[4][4] = {};
   const bool a_kfast = g.sak == 1 || g.sam != 1;
   const bool b_nfast = g.sbn == 1 || g.sbk != 1;
-  for (int64_t k0 = 0; k0 < g.K; k0 += BK) {
-    // A tile: BM x BK = 1024 elements, 4 per thread
+  for (int64_t k0 = kbeg; k0 < kend; k0 += BK) {
 #pragma unroll
     for (int j = 0; j < 4; ++j) {
       int e = tid + j * 256;
       int mm, kk;
       if (a_kfast) { mm = e / BK; kk = e % BK; } else { kk = e / BM; mm = e % BM; }
       int64_t gm = m0 + mm, gk = k0 + kk;
-      As[kk][mm] = (gm < g.M && gk < g.K) ? __ldg(A + gm * g.sam + gk * g.sak) : 0.f;
+      As[kk][mm] = (gm < g.M && gk < kend) ? __ldg(A + gm * g.sam + gk * g.sak) : 0.f;
     }
 #pragma unroll
     for (int j = 0; j < 4; ++j) {
@@ -38,16 +73,15 @@ __global__ void __launch_bounds__(256) gemm_simt_kernel(GemmArgs g) {
       int kk, nn;
       if (b_nfast) { kk = e / BN; nn = e % BN; } else { nn = e / BK; kk = e % BK; }
       int64_t gk = k0 + kk, gn = n0 + nn;
-      Bs[kk][nn] = (gk < g.K && gn < g.N) ? __ldg(B + gk * g.sbk + gn * g.sbn) : 0.f;
+      Bs[kk][nn] = (gk < kend && gn < g.N) ? __ldg(B + gk * g.sbk + gn * g.sbn) : 0.f;
     }
     __syncthreads();
 #pragma unroll
     for (int kk = 0; kk < BK; ++kk) {
-      float a[4], bb[4];
-#pragma unroll
-      for (int i = 0; i < 4; ++i) a[i] = As[kk][tm + i];
-#pragma unroll
-      for (int i = 0; i < 4; ++i) bb[i] = Bs[kk][tn + i];
+      float4 a4 = *reinterpret_cast<const float4*>(&As[kk][tm]);
+      float4 b4 = *reinterpret_cast<const float4*>(&Bs[kk][tn]);
+      const float a[4] = {a4.x, a4.y, a4.z, a4.w};
+      const float bb[4] = {b4.x, b4.y, b4.z, b4.w};
 #pragma unroll
       for (int i = 0; i < 4; ++i)
 #pragma unroll
@@ -55,56 +89,102 @@ __global__ void __launch_bounds__(256) gemm_simt_kernel(GemmArgs g) {
     }
     __syncthreads();
   }
-  float* C = g.C + b * g.scb;
+  if (partials == nullptr) {
 #pragma unroll
-  for (int i = 0; i < 4; ++i) {
-    int64_t gm = m0 + tm + i;
-    if (gm >= g.M) continue;
-    float alpha = g.alpha_rows ? g.alpha_rows[b * g.M + gm] : 1.f;
+    for (int i = 0; i < 4; ++i) {
+      const int64_t gm = m0 + tm + i;
+      const float alpha = (g.alpha_rows && gm < g.M) ? g.alpha_rows[bz * g.M + gm] : 1.f;
+      store_row4(g, bz, gm, n0 + tn, acc[i], alpha);
+    }
+  } else {
+    float* P = partials + ((int64_t)split * g.batch + bz) * g.M * g.N;
 #pragma unroll
-    for (int j = 0; j < 4; ++j) {
-      int64_t gn = n0 + tn + j;
-      if (gn >= g.N) continue;
-      float* p = C + gm * g.scm + gn * g.scn;
-      float v = acc[i][j] * alpha;
-      *p = g.accumulate ? *p + v : v;
+    for (int i = 0; i < 4; ++i) {
+      const int64_t gm = m0 + tm + i;
+      if (gm >= g.M) continue;
+#pragma unroll
+      for (int j = 0; j < 4; ++j)
+        if (n0 + tn + j < g.N) P[gm * g.N + n0 + tn + j] = acc[i][j];
     }
   }
 }
 
-// Tiny-K kernel (K <= 32): outer-product-like, one thread per output element,
-// operands read straight from global (L1/L2 resident rows).  Store-bound.
-__global__ void __launch_bounds__(256) gemm_smallk_kernel(GemmArgs g) {
-  const int64_t total = g.batch * g.M * g.N;
-  for (int64_t lin = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; lin < total;
-       lin += (int64_t)gridDim.x * blockDim.x) {
-    int64_t n = lin % g.N;
-    int64_t t = lin / g.N;
-    int64_t m = t % g.M;
-    int64_t b = t / g.M;
-    const float* a = g.A + b * g.sab + m * g.sam;
-    const float* bb = g.B + b * g.sbb + n * g.sbn;
-    float acc = 0.f;
-    for (int64_t k = 0; k < g.K; ++k) acc = fmaf(__ldg(a + k * g.sak), __ldg(bb + k * g.sbk), acc);
-    if (g.alpha_rows) acc *= g.alpha_rows[b * g.M + m];
+__global__ void splitk_reduce(GemmArgs g, int splits, const float* partials) {
+  const int64_t per = g.M * g.N, total = g.batch * per;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    float s = 0.f;
+    for (int k = 0; k < splits; ++k) s += partials[(int64_t)k * total + i];
+    const int64_t b = i / per, r = i - b * per;
+    const int64_t m = r / g.N, n = r - m * g.N;
+    if (g.alpha_rows) s *= g.alpha_rows[b * g.M + m];
     float* p = g.C + b * g.scb + m * g.scm + n * g.scn;
-    *p = g.accumulate ? *p + acc : acc;
+    *p = g.accumulate ? *p + s : s;
   }
 }
 
-int gemm_simt(const GemmArgs& g, cudaStream_t s) {
+// K <= 16: each thread = one row x 4 consecutive columns
+__global__ void __launch_bounds__(256) gemm_smallk_kernel(GemmArgs g) {
+  const int64_t nq = (g.N + 3) / 4;
+  const int64_t total = g.batch * g.M * nq;
+  for (int64_t lin = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; lin < total;
+       lin += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t q = lin % nq;
+    const int64_t t = lin / nq;
+    const int64_t m = t % g.M, b = t / g.M;
+    const int64_t n = q * 4;
+    const float* a = g.A + b * g.sab + m * g.sam;
+    const float* bb = g.B + b * g.sbb + n * g.sbn;
+    float acc[4] = {0.f, 0.f, 0.f, 0.f};
+    const bool full = n + 3 < g.N;
+    for (int64_t k = 0; k < g.K; ++k) {
+      const float av = __ldg(a + k * g.sak);
+      const float* bk = bb + k * g.sbk;
+      if (full) {
+#pragma unroll
+        for (int j = 0; j < 4; ++j) acc[j] = fmaf(av, __ldg(bk + j * g.sbn), acc[j]);
+      } else {
+        for (int j = 0; j < 4 && n + j < g.N; ++j) acc[j] = fmaf(av, __ldg(bk + j * g.sbn), acc[j]);
+      }
+    }
+    const float alpha = g.alpha_rows ? g.alpha_rows[b * g.M + m] : 1.f;
+    store_row4(g, b, m, n, acc, alpha);
+  }
+}
+
+static int simt_splits(const GemmArgs& g) {
+  const int64_t tiles = ((g.N + BN - 1) / BN) * ((g.M + BM - 1) / BM) * g.batch;
+  if (tiles >= 2 * kNumSMs || g.K < 256) return 1;
+  int64_t s = (2 * kNumSMs + tiles - 1) / tiles;
+  s = std::min<int64_t>(s, g.K / 128);
+  s = std::min<int64_t>(s, 64);
+  return (int)std::max<int64_t>(s, 1);
+}
+
+int64_t gemm_simt_workspace(const GemmArgs& g) {
+  const int s = simt_splits(g);
+  return s > 1 ? (int64_t)s * g.batch * g.M * g.N * 4 : 0;
+}
+
+int gemm_simt(const GemmArgs& g, void* ws, int64_t ws_bytes, cudaStream_t s) {
   if (g.batch == 0 || g.M == 0 || g.N == 0) return 0;
-  if (g.K <= 8) {
-    gemm_smallk_kernel<<<grid_for(g.batch * g.M * g.N, 256), 256, 0, s>>>(g);
+  if (g.K <= 16) {
+    gemm_smallk_kernel<<<grid_for(g.batch * g.M * ((g.N + 3) / 4), 256), 256, 0, s>>>(g);
     return launch_status();
   }
-  dim3 grid((unsigned)((g.N + BN - 1) / BN), (unsigned)((g.M + BM - 1) / BM), (unsigned)g.batch);
+  int splits = simt_splits(g);
+  if (splits > 1 && (ws == nullptr || ws_bytes < gemm_simt_workspace(g))) splits = 1;
+  const int64_t kchunk = ((g.K + splits - 1) / splits + BK - 1) / BK * BK;
+  dim3 grid((unsigned)((g.N + BN - 1) / BN), (unsigned)((g.M + BM - 1) / BM),
+            (unsigned)(g.batch * splits));
   if (grid.y > 65535 || grid.z > 65535) {
-    // fall back to the grid-stride small-K kernel for extreme shapes
-    gemm_smallk_kernel<<<grid_for(g.batch * g.M * g.N, 256), 256, 0, s>>>(g);
+    // extreme shapes: per-output grid-stride loop
+    gemm_smallk_kernel<<<grid_for(g.batch * g.M * ((g.N + 3) / 4), 256), 256, 0, s>>>(g);
     return launch_status();
   }
-  gemm_simt_kernel<<<grid, 256, 0, s>>>(g);
+  gemm_simt_kernel<<<grid, 256, 0, s>>>(g, splits, kchunk, splits > 1 ? (float*)ws : nullptr);
+  if (splits > 1)
+    splitk_reduce<<<grid_for(g.batch * g.M * g.N, 256), 256, 0, s>>>(g, splits, (const float*)ws);
   return launch_status();
 }
 

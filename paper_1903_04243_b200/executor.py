@@ -220,6 +220,7 @@ class Executor:
         self._captures = {}
         self._capture_ok = {}
         self._warm = set()
+        self._pinned = {}
         self.graph = graph
         self.device = torch.device(device if device is not None else "cuda")
         self.store = store if store is not None else VariableStore(graph.variables)
@@ -248,12 +249,32 @@ class Executor:
     def run(self, feeds=None, outputs=None):
         """Execute and return host TensorValues (fp32 floats, i64, bool)."""
         outs = self.run_device(feeds, outputs)
-        res = []
+        # D2H through pinned staging buffers: all copies queued, one sync
+        staged = []
         for v in outs:
             if isinstance(v, HostVal):
+                staged.append(None)
+                continue
+            t = v.torch_view()
+            key = (tuple(t.shape), t.dtype)
+            pin = self._pinned.get(key)
+            if pin is None or pin[1]:
+                pin = [torch.empty(t.shape, dtype=t.dtype, pin_memory=True), False]
+                self._pinned[key] = pin
+            pin[1] = True
+            pin[0].copy_(t, non_blocking=True)
+            staged.append(pin)
+        torch.cuda.current_stream(self.device).synchronize()
+        res = []
+        for v, pin in zip(outs, staged):
+            if pin is None:
                 res.append(TensorValue(v.dtype, v.value))
-            else:
-                res.append(TensorValue(v.dtype, v.to_numpy()))
+                continue
+            pin[1] = False
+            arr = pin[0].numpy().copy()
+            if v.dtype == DType.BOOL:
+                arr = arr.astype(np.bool_)
+            res.append(TensorValue(v.dtype, arr))
         self._finish_errors()
         self._writeback_vars()
         return res
