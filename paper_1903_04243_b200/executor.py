@@ -251,17 +251,16 @@ class Executor:
         outs = self.run_device(feeds, outputs)
         # D2H through pinned staging buffers: all copies queued, one sync
         staged = []
-        for v in outs:
+        for i, v in enumerate(outs):
             if isinstance(v, HostVal):
                 staged.append(None)
                 continue
             t = v.torch_view()
-            key = (tuple(t.shape), t.dtype)
+            key = (i, tuple(t.shape), t.dtype)
             pin = self._pinned.get(key)
-            if pin is None or pin[1]:
-                pin = [torch.empty(t.shape, dtype=t.dtype, pin_memory=True), False]
-                self._pinned[key] = pin
-            pin[1] = True
+            if pin is None:
+                pin = self._pinned[key] = [torch.empty(t.shape, dtype=t.dtype, pin_memory=True),
+                                           False]
             pin[0].copy_(t, non_blocking=True)
             staged.append(pin)
         torch.cuda.current_stream(self.device).synchronize()
@@ -270,7 +269,6 @@ class Executor:
             if pin is None:
                 res.append(TensorValue(v.dtype, v.value))
                 continue
-            pin[1] = False
             arr = pin[0].numpy().copy()
             if v.dtype == DType.BOOL:
                 arr = arr.astype(np.bool_)
