@@ -9,8 +9,8 @@
 //    Split-K (grid.z = batch x splits) when there are too few tiles to fill
 //    148 SMs: per-split partials go to the workspace and a second pass sums
 //    them in split order (deterministic), applying the epilogue.
-//  * small-K kernel (K <= 16): store-bound; each thread produces 4 consecutive
-//    columns of one row (one 128-bit store), operands read through L1.
+//  * small-K kernel (K <= 16): store-bound; a CTA per output row, each thread
+//    4 consecutive columns per 128-bit store, the row's lhs in registers.
 // Exact fp32 FMA accumulation in both.
 #include <algorithm>
 
@@ -123,33 +123,63 @@ __global__ void splitk_reduce(GemmArgs g, int splits, const float* partials) {
   }
 }
 
-// K <= 16: each thread = one row x 4 consecutive columns
+// K <= 16 (outer products, K=1 weight jacobians): store-bound.  One CTA per
+// output row at a time (grid-stride over rows); the row's K lhs values are
+// read once into registers, every thread then produces 4 consecutive columns
+// per iteration with one 128-bit store -- a warp writes 512 contiguous bytes.
+template <bool VEC>
 __global__ void __launch_bounds__(256) gemm_smallk_kernel(GemmArgs g) {
+  const int64_t rows = g.batch * g.M;
   const int64_t nq = (g.N + 3) / 4;
-  const int64_t total = g.batch * g.M * nq;
-  for (int64_t lin = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; lin < total;
-       lin += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t q = lin % nq;
-    const int64_t t = lin / nq;
-    const int64_t m = t % g.M, b = t / g.M;
-    const int64_t n = q * 4;
+  for (int64_t row = blockIdx.x; row < rows; row += gridDim.x) {
+    const int64_t b = row / g.M, m = row - b * g.M;
+    float av[16];
     const float* a = g.A + b * g.sab + m * g.sam;
-    const float* bb = g.B + b * g.sbb + n * g.sbn;
-    float acc[4] = {0.f, 0.f, 0.f, 0.f};
-    const bool full = n + 3 < g.N;
-    for (int64_t k = 0; k < g.K; ++k) {
-      const float av = __ldg(a + k * g.sak);
-      const float* bk = bb + k * g.sbk;
-      if (full) {
 #pragma unroll
-        for (int j = 0; j < 4; ++j) acc[j] = fmaf(av, __ldg(bk + j * g.sbn), acc[j]);
+    for (int k = 0; k < 16; ++k) av[k] = k < g.K ? __ldg(a + k * g.sak) : 0.f;
+    const float alpha = g.alpha_rows ? g.alpha_rows[row] : 1.f;
+    const float* bb = g.B + b * g.sbb;
+    float* crow = g.C + b * g.scb + m * g.scm;
+    for (int64_t q = threadIdx.x; q < nq; q += blockDim.x) {
+      const int64_t n = q * 4;
+      float acc[4] = {0.f, 0.f, 0.f, 0.f};
+      if (VEC) {
+#pragma unroll 4
+        for (int k = 0; k < g.K; ++k) {
+          const float4 v = __ldg(reinterpret_cast<const float4*>(bb + k * g.sbk + n));
+          acc[0] = fmaf(av[k], v.x, acc[0]); acc[1] = fmaf(av[k], v.y, acc[1]);
+          acc[2] = fmaf(av[k], v.z, acc[2]); acc[3] = fmaf(av[k], v.w, acc[3]);
+        }
+        float4 o = make_float4(acc[0] * alpha, acc[1] * alpha, acc[2] * alpha, acc[3] * alpha);
+        float4* dst = reinterpret_cast<float4*>(crow + n);
+        if (g.accumulate) {
+          const float4 c = *dst;
+          o.x += c.x; o.y += c.y; o.z += c.z; o.w += c.w;
+        }
+        *dst = o;
       } else {
-        for (int j = 0; j < 4 && n + j < g.N; ++j) acc[j] = fmaf(av, __ldg(bk + j * g.sbn), acc[j]);
+        for (int k = 0; k < g.K; ++k) {
+          const float* bk = bb + k * g.sbk + n * g.sbn;
+#pragma unroll
+          for (int j = 0; j < 4; ++j)
+            if (n + j < g.N) acc[j] = fmaf(av[k], __ldg(bk + j * g.sbn), acc[j]);
+        }
+        store_row4(g, b, m, n, acc, alpha);
       }
     }
-    const float alpha = g.alpha_rows ? g.alpha_rows[b * g.M + m] : 1.f;
-    store_row4(g, b, m, n, acc, alpha);
   }
+}
+
+static int smallk_launch(const GemmArgs& g, cudaStream_t s) {
+  const bool vec = g.K <= 16 && g.sbn == 1 && g.scn == 1 && g.N % 4 == 0 && g.sbk % 4 == 0 &&
+                   g.sbb % 4 == 0 && g.scm % 4 == 0 && g.scb % 4 == 0 &&
+                   (reinterpret_cast<uintptr_t>(g.B) & 15) == 0 &&
+                   (reinterpret_cast<uintptr_t>(g.C) & 15) == 0;
+  const int64_t rows = g.batch * g.M;
+  const int grid = (int)std::min<int64_t>(rows, (int64_t)kNumSMs * 8);
+  if (vec) gemm_smallk_kernel<true><<<grid, 256, 0, s>>>(g);
+  else gemm_smallk_kernel<false><<<grid, 256, 0, s>>>(g);
+  return launch_status();
 }
 
 static int simt_splits(const GemmArgs& g) {
@@ -168,20 +198,13 @@ int64_t gemm_simt_workspace(const GemmArgs& g) {
 
 int gemm_simt(const GemmArgs& g, void* ws, int64_t ws_bytes, cudaStream_t s) {
   if (g.batch == 0 || g.M == 0 || g.N == 0) return 0;
-  if (g.K <= 16) {
-    gemm_smallk_kernel<<<grid_for(g.batch * g.M * ((g.N + 3) / 4), 256), 256, 0, s>>>(g);
-    return launch_status();
-  }
+  if (g.K <= 16) return smallk_launch(g, s);
   int splits = simt_splits(g);
   if (splits > 1 && (ws == nullptr || ws_bytes < gemm_simt_workspace(g))) splits = 1;
   const int64_t kchunk = ((g.K + splits - 1) / splits + BK - 1) / BK * BK;
   dim3 grid((unsigned)((g.N + BN - 1) / BN), (unsigned)((g.M + BM - 1) / BM),
             (unsigned)(g.batch * splits));
-  if (grid.y > 65535 || grid.z > 65535) {
-    // extreme shapes: per-output grid-stride loop
-    gemm_smallk_kernel<<<grid_for(g.batch * g.M * ((g.N + 3) / 4), 256), 256, 0, s>>>(g);
-    return launch_status();
-  }
+  if (grid.y > 65535 || grid.z > 65535) return PFB_E_UNSUPPORTED;
   gemm_simt_kernel<<<grid, 256, 0, s>>>(g, splits, kchunk, splits > 1 ? (float*)ws : nullptr);
   if (splits > 1)
     splitk_reduce<<<grid_for(g.batch * g.M * g.N, 256), 256, 0, s>>>(g, splits, (const float*)ws);

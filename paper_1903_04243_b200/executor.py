@@ -467,7 +467,7 @@ class Executor:
         _raise_status(fn(*args), what)
         en.record()
         nbytes, flops = work if work is not None else (0, 0)
-        self.kernel_timer.append((what, nbytes, flops, st, en))
+        self.kernel_timer.append((what, nbytes, flops, st, en, fn, args))
 
     def _dense(self, x):
         if x.is_dense():
