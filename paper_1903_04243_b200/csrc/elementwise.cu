@@ -312,30 +312,31 @@ __device__ __forceinline__ float run_op(int opc, float x, float y) {
     case 16 + PFB_SIGMOID: return 1.f / (1.f + expf(-x));
     case 16 + PFB_SQUARE: return x * x;
     case 16 + PFB_LOGICAL_NOT: return x == 0.f ? 1.f : 0.f;
-    default: return x;
+    case 66: return x != 0.f ? 1.f : 0.f;  // cast f32 -> bool
+    default: return x;                     // 67: move (cast bool -> f32)
   }
 }
 
-template <typename IdxT, typename Tout>
-__global__ void __launch_bounds__(256) fused_kernel(Layout L, IdxT n, FusedProgram P,
-                                                    Tout* out, const void* const* ins_dummy,
-                                                    const float* i0, const float* i1,
-                                                    const float* i2, const float* i3,
-                                                    const float* i4, const float* i5,
-                                                    const float* i6, const float* i7) {
-  const float* ins[8] = {i0, i1, i2, i3, i4, i5, i6, i7};
+template <typename IdxT, typename Tout, int NIN>
+__global__ void __launch_bounds__(256) fused_kernel(Layout L, IdxT n, FusedProgram P, Tout* out,
+                                                    const void* i0, const void* i1,
+                                                    const void* i2, const void* i3,
+                                                    const void* i4, const void* i5,
+                                                    const void* i6, const void* i7) {
+  const void* ins[8] = {i0, i1, i2, i3, i4, i5, i6, i7};
   for (IdxT i = blockIdx.x * (IdxT)blockDim.x + threadIdx.x; i < n;
        i += (IdxT)gridDim.x * blockDim.x) {
-    int64_t off[kMaxOps];
-    offsets<IdxT, kMaxOps>(L, i, off);
+    int64_t off[NIN + 1];
+    offsets<IdxT, NIN + 1>(L, i, off);
     float r[kMaxRegs];
     for (int s = 0; s < P.n_steps; ++s) {
       const int* c = P.code[s];
       float v;
       if (c[0] == F_LOAD) {
-        int k = c[2];
-        v = P.in_dtype[k] == PFB_BOOL ? (float)reinterpret_cast<const uint8_t*>(ins[k])[off[k + 1]]
-                                      : ins[k][off[k + 1]];
+        const int k = c[2];
+        v = P.in_dtype[k] == PFB_BOOL
+                ? (float)__ldg(reinterpret_cast<const uint8_t*>(ins[k]) + off[k + 1])
+                : __ldg(reinterpret_cast<const float*>(ins[k]) + off[k + 1]);
       } else if (c[0] == F_CONST) {
         v = __int_as_float(c[2]);
       } else {
@@ -343,10 +344,26 @@ __global__ void __launch_bounds__(256) fused_kernel(Layout L, IdxT n, FusedProgr
       }
       r[c[1]] = v;
     }
-    float res = r[P.code[P.n_steps - 1][1]];
+    const float res = r[P.code[P.n_steps - 1][1]];
     if constexpr (std::is_same<Tout, uint8_t>::value) out[off[0]] = (uint8_t)(res != 0.f);
     else out[off[0]] = res;
   }
+}
+
+template <typename IdxT, typename Tout>
+void launch_fused(int n_in, const Layout& L, IdxT n, const FusedProgram& P, Tout* out,
+                  const void* const* p, cudaStream_t s) {
+  const int grid = grid_for((int64_t)n, 256);
+#define PFB_FUSED_CASE(K)                                                                    \
+  case K:                                                                                    \
+    fused_kernel<IdxT, Tout, K><<<grid, 256, 0, s>>>(L, n, P, out, p[0], p[1], p[2], p[3],  \
+                                                     p[4], p[5], p[6], p[7]);                \
+    break;
+  switch (n_in) {
+    PFB_FUSED_CASE(1) PFB_FUSED_CASE(2) PFB_FUSED_CASE(3) PFB_FUSED_CASE(4)
+    PFB_FUSED_CASE(5) PFB_FUSED_CASE(6) PFB_FUSED_CASE(7) PFB_FUSED_CASE(8)
+  }
+#undef PFB_FUSED_CASE
 }
 
 }  // namespace pfb
@@ -456,21 +473,19 @@ extern "C" int pfb_fused_ew(int32_t n_in, const pfb_tensor* ins, int32_t n_steps
     for (int j = 0; j < 4; ++j) P.code[s][j] = program[4 * s + j];
     if (P.code[s][1] < 0 || P.code[s][1] >= kMaxRegs) return PFB_E_ARG;
   }
-  // pad the layout to kMaxOps operands so the offset loop is fixed-trip
-  int64_t zero[kMaxRank] = {0};
-  for (int k = n_in + 1; k < kMaxOps; ++k) st[k] = zero;
-  Layout L = make_layout(out->rank, out->shape, kMaxOps, st);
+  Layout L = make_layout(out->rank, out->shape, n_in + 1, st);
   int64_t n = numel(out);
   if (n == 0) return 0;
-  const float* p[8];
-  for (int k = 0; k < 8; ++k) p[k] = k < n_in ? (const float*)ins[k].data : nullptr;
+  const void* p[8];
+  for (int k = 0; k < 8; ++k) p[k] = k < n_in ? ins[k].data : nullptr;
   cudaStream_t s = as_stream(stream);
-  int grid = grid_for(n, 256);
-  if (out->dtype == PFB_F32)
-    fused_kernel<int64_t, float><<<grid, 256, 0, s>>>(L, n, P, (float*)out->data, nullptr, p[0], p[1],
-                                                      p[2], p[3], p[4], p[5], p[6], p[7]);
-  else
-    fused_kernel<int64_t, uint8_t><<<grid, 256, 0, s>>>(L, n, P, (uint8_t*)out->data, nullptr, p[0],
-                                                        p[1], p[2], p[3], p[4], p[5], p[6], p[7]);
+  const bool small = n < (int64_t)0x7fffffff;
+  if (out->dtype == PFB_F32) {
+    if (small) launch_fused<uint32_t, float>(n_in, L, (uint32_t)n, P, (float*)out->data, p, s);
+    else launch_fused<int64_t, float>(n_in, L, n, P, (float*)out->data, p, s);
+  } else {
+    if (small) launch_fused<uint32_t, uint8_t>(n_in, L, (uint32_t)n, P, (uint8_t*)out->data, p, s);
+    else launch_fused<int64_t, uint8_t>(n_in, L, n, P, (uint8_t*)out->data, p, s);
+  }
   return launch_status();
 }

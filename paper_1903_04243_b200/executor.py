@@ -22,6 +22,7 @@ What differs from the reference, by design (all value-neutral):
 
 from __future__ import annotations
 
+import ctypes
 import os
 
 import numpy as np
@@ -221,6 +222,7 @@ class Executor:
         self._capture_ok = {}
         self._warm = set()
         self._pinned = {}
+        self._programs = {}
         self.graph = graph
         self.device = torch.device(device if device is not None else "cuda")
         self.store = store if store is not None else VariableStore(graph.variables)
@@ -980,6 +982,25 @@ def _h_range_vec(ex, node, ins):
     return [out]
 
 
+def _h_fused(ex, node, ins):
+    """fused_ew (passes.fuse_elementwise): one launch for a chain of elementwise
+    ops; the program rides in the node attrs."""
+    arrs = [ex._dev(v) for v in ins]
+    shape = ()
+    for a in arrs:
+        shape = broadcast_shapes(shape, a.shape)
+    out = ex._empty(shape, node.attrs["out_dtype"])
+    prog = ex._programs.get(id(node))
+    if prog is None:
+        flat = [int(x) for step in node.attrs["program"] for x in step]
+        prog = ex._programs[id(node)] = ((ctypes.c_int32 * len(flat))(*flat),
+                                         len(node.attrs["program"]))
+    descs = (N.PfbTensor * len(arrs))(*[a.desc() for a in arrs])
+    ex._call(ex._lib.pfb_fused_ew, len(arrs), descs, prog[1], prog[0], out.desc(), ex._stream,
+             what="fused_ew", work=(_abytes(*arrs, out), 0))
+    return [out]
+
+
 def _h_read_variable(ex, node, ins):
     name = node.attrs["name"]
     if name not in ex._dvars:
@@ -1030,7 +1051,7 @@ _HANDLERS.update({
     "slice_leading": _h_slice_leading, "tile_leading": _h_tile_leading,
     "where_true": _h_where_true, "complement": _h_complement, "dim0": _h_dim0,
     "range_vec": _h_range_vec, "read_variable": _h_read_variable, "assign": _h_assign,
-    "assign_add": _h_assign, "random_uniform": _h_random_uniform,
+    "assign_add": _h_assign, "random_uniform": _h_random_uniform, "fused_ew": _h_fused,
 })
 
 

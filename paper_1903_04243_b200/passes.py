@@ -12,6 +12,9 @@ F1b  reduce_sum((a (x) b) * s, (0,))            ->  A^T diag(s) B   (one K=n GEM
 F2   (a_1 (x) b_1) + ... + (a_T (x) b_T)        ->  [a_1..a_T] [b_1..b_T]^T
                                                     (one batched K=T GEMM; B laid
                                                     out K-major for tcgen05)
+F3   chains of elementwise ops (binary / unary / f32<->bool cast) whose interior
+     values have no other consumer  ->  one `fused_ew` launch running a small
+     register program (the same fp32 ops in the same order: bit-identical).
 
 Each rewrite adds nodes to a private copy of the graph and redirects the
 consumers; the now-unread outer products are removed by the executor's
@@ -172,12 +175,169 @@ def _f2(rw, node):
     return 1
 
 
-def optimize(g, keep_keys):
+def optimize(g, keep_keys, elementwise=True):
     """Copy `g`, apply the rewrites, return (graph, key map old->new)."""
     dst, mapping = copy_with_map(g)
     keep = [mapping[k] for k in keep_keys]
     _, moved = fuse_outer_products(dst, keep)
+    keep2 = [moved.get(k, k) for k in keep]
+    moved2 = {}
+    if elementwise:
+        _, moved2 = fuse_elementwise(dst, keep2)
     final = {}
     for k, v in mapping.items():
-        final[k] = moved.get(v, v)
+        v = moved.get(v, v)
+        final[k] = moved2.get(v, v)
     return dst, final
+
+
+# ----------------------------------------------------------------------------
+# F3: elementwise chains -> one fused_ew launch
+
+_BIN_CODE = {"add": 0, "sub": 1, "mul": 2, "div": 3, "max": 4, "min": 5, "less": 6, "equal": 7}
+_UN_CODE = {"neg": 0, "exp": 1, "log": 2, "relu": 3, "tanh": 4, "sigmoid": 5, "square": 6,
+            "logical_not": 7}
+OP_LOAD, OP_CONST, OP_TOBOOL, OP_MOV = 64, 65, 66, 67
+MAX_INPUTS, MAX_STEPS, MAX_REGS = 8, 48, 16
+
+
+def _ew_eligible(g, node):
+    from .tensor import DType
+    k = node.kind
+    if k not in _BIN_CODE and k not in _UN_CODE and k != "cast":
+        return False
+    if node.output_arity != 1 or node.out_dtypes[0] not in (DType.F64, DType.BOOL):
+        return False
+    sh = node.out_shapes[0]
+    if sh is None or any(d is None for d in sh):
+        return False
+    for src in node.inputs:
+        if g.ref_dtype(src) not in (DType.F64, DType.BOOL):
+            return False
+    return True
+
+
+def _const_scalar_f(g, key):
+    import numpy as np
+    from .tensor import DType
+    n = g.nodes[key[0]]
+    if n.kind == "constant" and key[1] == 0:
+        v = n.attrs["value"]
+        if v.rank == 0 and v.dtype == DType.F64:
+            return float(np.float32(v.item()))
+    return None
+
+
+def _program(g, order, root, externals):
+    """Register program for the group `order` (topo order, root last)."""
+    import struct
+    from .tensor import DType
+    ext_index = {k: i for i, k in enumerate(externals)}
+    last_use = {}
+    for i, n in enumerate(order):
+        for src in n.inputs:
+            last_use[src] = i
+    free = list(range(MAX_REGS - 1, -1, -1))
+    reg = {}
+    steps = []
+
+    def operand(src):
+        if src in reg:
+            return reg[src]
+        if not free:
+            raise OverflowError
+        r = free.pop()
+        c = _const_scalar_f(g, src)
+        if c is not None:
+            bits = struct.unpack("<i", struct.pack("<f", c))[0]
+            steps.append((OP_CONST, r, bits, 0))
+        else:
+            steps.append((OP_LOAD, r, ext_index[src], 0))
+        reg[src] = r
+        return r
+
+    for i, n in enumerate(order):
+        ops = [operand(src) for src in n.inputs]
+        for src in set(n.inputs):
+            if last_use.get(src) == i and src in reg:
+                free.append(reg.pop(src))
+        if not free:
+            raise OverflowError
+        dst = free.pop()
+        k = n.kind
+        if k in _BIN_CODE:
+            steps.append((_BIN_CODE[k], dst, ops[0], ops[1]))
+        elif k in _UN_CODE:
+            steps.append((16 + _UN_CODE[k], dst, ops[0], ops[0]))
+        else:  # cast between f64 (fp32) and bool
+            to = n.attrs["dtype"]
+            frm = g.ref_dtype(n.inputs[0])
+            op = OP_TOBOOL if (to == DType.BOOL and frm != DType.BOOL) else OP_MOV
+            steps.append((op, dst, ops[0], ops[0]))
+        reg[(n.id, 0)] = dst
+    if len(steps) > MAX_STEPS:
+        raise OverflowError
+    return tuple(steps)
+
+
+def fuse_elementwise(g, keep=()):
+    """Replace single-output elementwise chains (same output shape, interior
+    values used only inside the chain) by `fused_ew` nodes.  Returns the
+    number of groups fused and the moved requested outputs."""
+    keep = set(keep)
+    topo = g.topo_order()
+    pos = {n.id: i for i, n in enumerate(topo)}
+    users = {}
+    for n in topo:
+        for src in n.inputs:
+            users.setdefault(src, set()).add(n.id)
+    assigned = set()
+    moved = {}
+    fused = 0
+    for root in reversed(topo):
+        if root.id in assigned or not _ew_eligible(g, root):
+            continue
+        shape = root.out_shapes[0]
+        group = {root.id}
+        changed = True
+        while changed:
+            changed = False
+            for nid in list(group):
+                for src in g.nodes[nid].inputs:
+                    p = g.nodes[src[0]]
+                    if p.id in group or p.id in assigned or src in keep:
+                        continue
+                    if not _ew_eligible(g, p) or p.out_shapes[0] != shape:
+                        continue
+                    if not users.get(src, set()) <= group:
+                        continue
+                    if len(group) + 1 > MAX_STEPS // 2:
+                        continue
+                    group.add(p.id)
+                    changed = True
+        if len(group) < 2:
+            continue
+        order = sorted((g.nodes[i] for i in group), key=lambda n: pos[n.id])
+        externals = []
+        for n in order:
+            for src in n.inputs:
+                if src[0] not in group and src not in externals and _const_scalar_f(g, src) is None:
+                    externals.append(src)
+        if len(externals) > MAX_INPUTS:
+            continue
+        try:
+            prog = _program(g, order, root, externals)
+        except OverflowError:
+            continue
+        new = g.add_node("fused_ew", externals,
+                         {"program": prog, "out_dtype": root.out_dtypes[0]})
+        key = (root.id, 0)
+        for u in users.get(key, ()):
+            un = g.nodes[u]
+            un.inputs = [(new.id, 0) if s == key else s for s in un.inputs]
+        if key in keep:
+            moved[key] = (new.id, 0)
+        assigned |= group
+        fused += 1
+    g._topo_cache = None
+    return fused, moved

@@ -192,3 +192,22 @@ def test_cuda_graph_replay_tracks_feeds(Executor):
     for g, want in zip(got, [want1, want2, want1, want2]):
         for a, b in zip(g, want):
             np.testing.assert_allclose(a.data, b.data, rtol=1e-6, atol=1e-7)
+
+
+@pytest.mark.parametrize("name", ["cfg2_mlp", "cfg2_conv", "cfg4_mid", "cfg1_full"])
+def test_program_unoptimized_vs_reference(name, golden, Executor):
+    """The executor with its fusion passes off (one kernel per reference op)."""
+    P = golden["programs"]
+    w = build_program(name)
+    outs = Executor(w.graph, optimize=False, cuda_graph=False).run(feeds=w.feeds)
+    for j, o in enumerate(outs):
+        check(o, P[f"{name}/out/{j}"])
+
+
+def test_fusion_reduces_launches(Executor):
+    w = build_program("cfg4_mid")
+    fused, plain = Executor(w.graph, cuda_graph=False), Executor(w.graph, optimize=False,
+                                                                  cuda_graph=False)
+    fused.run(feeds=w.feeds)
+    plain.run(feeds=w.feeds)
+    assert fused.launch_count < 0.7 * plain.launch_count, (fused.launch_count, plain.launch_count)
