@@ -31,6 +31,7 @@
 #include <cudaTypedefs.h>
 
 #include <algorithm>
+#include <cmath>
 
 #include "gemm.cuh"
 
@@ -41,7 +42,9 @@ constexpr int BM = 128, BN = 128, BK = 32, STAGES = 3, UMMA_K = 8;
 constexpr int CHUNK_KB = 2;                       // k-blocks accumulated in TMEM per chunk
 constexpr int TILE_BYTES = BM * BK * 4;           // 16 KB per operand tile
 constexpr int STAGE_BYTES = 4 * TILE_BYTES;       // A_hi, A_lo, B_hi, B_lo
-constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + 1024 /*align*/ + 256 /*barriers*/;
+constexpr int EPI_STAGE_FLOATS = 32 * 33;         // per epilogue warp: 32x32 transpose tile
+constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + 1024 /*align*/ + 256 /*barriers*/ +
+                           4 * EPI_STAGE_FLOATS * 4;
 constexpr int NUM_THREADS = 192;                  // 6 warps
 constexpr int TMEM_COLS = 2 * BN;                 // double-buffered chunk accumulator
 
@@ -306,35 +309,29 @@ gemm_kernel(const __grid_constant__ CUtensorMap map_ah, const __grid_constant__ 
         asm volatile("tcgen05.fence::before_thread_sync;");
         mbar_arrive(&acc_empty[buf]);
       }
-      const int row = m0 + quarter * 32 + lane;
-      if (row < p.M) {
-        const float alpha = p.alpha_rows ? p.alpha_rows[(int64_t)bz * p.M + row] : 1.f;
-        float* crow = p.C + bz * p.scb + (int64_t)row * p.scm;
-        const bool vec = p.scn == 1 && n0 + BN <= p.N &&
-                         ((reinterpret_cast<uintptr_t>(crow + n0) & 15) == 0);
-        if (vec) {
-          float4* dst = reinterpret_cast<float4*>(crow + n0);
+      // store through a per-warp 32x32 smem transpose so that every store
+      // instruction writes 32 consecutive columns of one row (128 B, coalesced)
+      float* stage = reinterpret_cast<float*>(smem + STAGES * STAGE_BYTES + 256) +
+                     (warp - 2) * EPI_STAGE_FLOATS;
+      const int row0 = m0 + quarter * 32;
+      float* cbase = p.C + bz * p.scb;
 #pragma unroll
-          for (int j = 0; j < BN / 4; ++j) {
-            float4 v = make_float4(acc[4 * j] * alpha, acc[4 * j + 1] * alpha,
-                                   acc[4 * j + 2] * alpha, acc[4 * j + 3] * alpha);
-            if (p.accumulate) {
-              float4 o = dst[j];
-              v.x += o.x; v.y += o.y; v.z += o.z; v.w += o.w;
-            }
-            dst[j] = v;
-          }
-        } else {
+      for (int cc = 0; cc < BN; cc += 32) {
 #pragma unroll
-          for (int j = 0; j < BN; ++j) {
-            const int col = n0 + j;
-            if (col < p.N) {
-              float* q = crow + (int64_t)col * p.scn;
-              const float v = acc[j] * alpha;
-              *q = p.accumulate ? *q + v : v;
-            }
+        for (int j = 0; j < 32; ++j) stage[lane * 33 + j] = acc[cc + j];
+        __syncwarp();
+        const int col = n0 + cc + lane;
+        for (int i = 0; i < 32; ++i) {
+          const int row = row0 + i;
+          if (row >= p.M) break;
+          const float alpha = p.alpha_rows ? __ldg(p.alpha_rows + (int64_t)bz * p.M + row) : 1.f;
+          if (col < p.N) {
+            float* q = cbase + (int64_t)row * p.scm + (int64_t)col * p.scn;
+            const float v = stage[i * 33 + lane] * alpha;
+            *q = p.accumulate ? *q + v : v;
           }
         }
+        __syncwarp();
       }
     }
   }
@@ -407,9 +404,18 @@ bool gemm_tcgen05_eligible(const GemmArgs& g) {
            (g.M + 31) / 32 > 65535 || (g.N + 31) / 32 > 65535);
 }
 
+// Dispatch model (microseconds), calibrated on B200 (tools/gemm_probe.py):
+// tensor path ~0.45 us per 32-deep k-block per 128x128 tile per wave plus
+// fixed split/launch costs; SIMT fp32 ~15 TFLOP/s.  Skinny problems with few
+// tiles (batch-128 forward passes) go SIMT with split-K.
 bool gemm_tcgen05_profitable(const GemmArgs& g) {
-  return g.K >= 32 && g.M >= 64 && g.N >= 64 &&
-         (double)g.batch * g.M * g.N * g.K >= (double)(1 << 22);
+  if (g.K < 16 || g.M < 16 || g.N < 16) return false;
+  const double tiles = (double)((g.M + 127) / 128) * ((g.N + 127) / 128) * g.batch;
+  const double nk = (double)((g.K + 31) / 32);
+  const double waves = std::ceil(tiles / tc::num_sms());
+  const double t_tc = waves * (nk * 0.45 + 1.5) + 6.0;
+  const double t_simt = 2.0 * g.M * g.N * g.K * g.batch / 15e6 + 3.0;
+  return t_tc < t_simt;
 }
 
 int gemm_tcgen05(const GemmArgs& g, void* ws, int64_t ws_bytes, cudaStream_t s) {
