@@ -216,6 +216,11 @@ class Executor:
         second run with a given feed signature and replays it afterwards --
         one launch per step instead of one per node.  False = always eager."""
         self._lib = N.lib()
+        from .interop import import_graph, is_native
+        self._foreign = None
+        if not is_native(graph):  # a reference `pforvec` graph: translate once
+            self._foreign = graph
+            graph = import_graph(graph)
         self.optimize = optimize
         self.cuda_graph = cuda_graph
         self._captures = {}
@@ -381,6 +386,9 @@ class Executor:
         g = self._exec_graph
         if outputs is None:
             keys = [tuple(o) for o in self.graph.outputs]
+        elif self._foreign is not None:
+            from .interop import translate_ref
+            keys = [translate_ref(self._foreign, self.graph, o) for o in outputs]
         else:
             keys = [self.graph._resolve(o) for o in outputs]
         if self._refmap is not None:
