@@ -48,7 +48,8 @@ CONFIGS = {
     "cfg1_full": ("cfg1", dict(batch=32, variant="full"), "jacobian rows/s"),
     "cfg3": ("cfg3", dict(width=4096, out_dim=1024, rows=8), "jacobian rows/s"),
     "cfg4": ("cfg4", dict(n=256, steps=64, units=512), "per-example grads/s"),
-    "cfg5": ("cfg5", dict(n=1024, max_len=100, units=256), "examples/s"),
+    "cfg5": ("cfg5", dict(n=1024, max_len=100, units=256, masked=True, unroll=4), "examples/s"),
+    "cfg5_compact": ("cfg5", dict(n=1024, max_len=100, units=256), "examples/s"),
 }
 # bounded CPU samples of the same workload (reference formulation, f64)
 CPU_SAMPLE = {
@@ -59,6 +60,7 @@ CPU_SAMPLE = {
     "cfg3": dict(width=1024, out_dim=1024, rows=4),
     "cfg4": dict(n=4, steps=64, units=128),
     "cfg5": dict(n=128, max_len=100, units=256),
+    "cfg5_compact": dict(n=128, max_len=100, units=256),
 }
 
 

@@ -79,6 +79,11 @@ int pfb_cast(const pfb_tensor* x, pfb_tensor* out, void* stream);
 int pfb_fused_ew(int32_t n_in, const pfb_tensor* ins, int32_t n_steps, const int32_t* program,
                  pfb_tensor* out, void* stream);
 
+/* select(mask, a, b) = mask ? a : b with broadcasting (predicated cond /
+ * while bodies; numpy.where semantics); any dtype, mask is bool. */
+int pfb_select(const pfb_tensor* mask, const pfb_tensor* a, const pfb_tensor* b, pfb_tensor* out,
+               void* stream);
+
 /* reduce_sum over axes given as a bitmask (reference tensor.py:279-283) */
 int pfb_reduce_sum(const pfb_tensor* x, uint32_t axes_mask, pfb_tensor* out, void* ws,
                    int64_t ws_bytes, void* stream);

@@ -489,3 +489,54 @@ extern "C" int pfb_fused_ew(int32_t n_in, const pfb_tensor* ins, int32_t n_steps
   }
   return launch_status();
 }
+
+// ---------------------------------------------------------------------------
+// select(mask, a, b) = mask ? a : b  (predicated control flow; numpy.where)
+
+namespace pfb {
+template <typename T, typename IdxT>
+__global__ void __launch_bounds__(256) select_kernel(Layout L, IdxT n, T* out, const uint8_t* m,
+                                                     const T* a, const T* b) {
+  for (IdxT i = blockIdx.x * (IdxT)blockDim.x + threadIdx.x; i < n;
+       i += (IdxT)gridDim.x * blockDim.x) {
+    int64_t off[4];
+    offsets<IdxT, 4>(L, i, off);
+    out[off[0]] = __ldg(m + off[1]) ? __ldg(a + off[2]) : __ldg(b + off[3]);
+  }
+}
+
+template <typename T>
+int select_run(const Layout& L, int64_t n, pfb_tensor* out, const pfb_tensor* m,
+               const pfb_tensor* a, const pfb_tensor* b, cudaStream_t s) {
+  const int grid = grid_for(n, 256);
+  if (n < (int64_t)0x7fffffff)
+    select_kernel<T, uint32_t><<<grid, 256, 0, s>>>(L, (uint32_t)n, (T*)out->data,
+                                                    (const uint8_t*)m->data, (const T*)a->data,
+                                                    (const T*)b->data);
+  else
+    select_kernel<T, int64_t><<<grid, 256, 0, s>>>(L, n, (T*)out->data, (const uint8_t*)m->data,
+                                                   (const T*)a->data, (const T*)b->data);
+  return launch_status();
+}
+}  // namespace pfb
+
+extern "C" int pfb_select(const pfb_tensor* mask, const pfb_tensor* a, const pfb_tensor* b,
+                          pfb_tensor* out, void* stream) {
+  using namespace pfb;
+  if (mask->dtype != PFB_BOOL || a->dtype != b->dtype || a->dtype != out->dtype) return PFB_E_DTYPE;
+  int64_t sm[kMaxRank], sa[kMaxRank], sb[kMaxRank];
+  if (!broadcast_strides(mask, out->rank, out->shape, sm) ||
+      !broadcast_strides(a, out->rank, out->shape, sa) ||
+      !broadcast_strides(b, out->rank, out->shape, sb))
+    return PFB_E_SHAPE;
+  const int64_t* st[4] = {out->stride, sm, sa, sb};
+  Layout L = make_layout(out->rank, out->shape, 4, st);
+  int64_t n = numel(out);
+  if (n == 0) return 0;
+  cudaStream_t s = as_stream(stream);
+  switch (a->dtype) {
+    case PFB_F32: return select_run<float>(L, n, out, mask, a, b, s);
+    case PFB_I64: return select_run<int64_t>(L, n, out, mask, a, b, s);
+    default: return select_run<uint8_t>(L, n, out, mask, a, b, s);
+  }
+}

@@ -226,6 +226,9 @@ class Executor:
         self._captures = {}
         self._capture_ok = {}
         self._warm = set()
+        self._sub_captures = {}
+        self._sub_warm = set()
+        self._used_caps = {}
         self._pinned = {}
         self._programs = {}
         self.graph = graph
@@ -347,6 +350,78 @@ class Executor:
             self._ws, self._err, self._err_nodes = saved
         return cap
 
+    # -- CUDA-graph capture of pure loop-body sub-graphs --------------------------
+
+    def _dense_copy(self, v):
+        out = self._empty(v.shape, v.dtype)
+        if v.size:
+            self._call(self._lib.pfb_copy, v.desc(), out.desc(), self._stream, what="copy")
+        return out
+
+    def _run_sub(self, sub, bind, feeds):
+        """Run a block sub-graph; pure block-free bodies with device-resident,
+        fixed-shape inputs are captured on their second execution and replayed
+        afterwards (carried values copied into static inputs, captures read in
+        place).  Predicated while loops (vectorize Policy(masked_control))
+        produce exactly such bodies."""
+        vals = list(bind.get("capture", [])) + list(bind.get("carried", []))
+        if not (self.cuda_graph and self.kernel_timer is None
+                and all(isinstance(v, DArray) for v in vals)
+                and self._capturable(sub, [tuple(o) for o in sub.outputs])):
+            return self._run_graph(sub, bind, feeds)
+        caps, car = bind.get("capture", []), bind.get("carried", [])
+        sig = (id(sub), tuple((v.ptr, v.shape, v.strides, v.dtype) for v in caps),
+               tuple((v.shape, v.dtype) for v in car))
+        cap = self._sub_captures.get(sig)
+        if cap is None:
+            if sig not in self._sub_warm:
+                self._sub_warm.add(sig)
+                return self._run_graph(sub, bind, feeds)
+            cap = self._capture_sub(sub, caps, car, feeds, sig)
+            if cap is None:
+                return self._run_graph(sub, bind, feeds)
+        for src, dst in zip(car, cap.inputs):
+            if src.size:
+                self._call(self._lib.pfb_copy, src.desc(), dst.desc(), self._stream, what="copy")
+        cap.graph.replay()
+        self.launch_count += cap.launches
+        self.dispatch_count += cap.dispatches
+        if cap.err_nodes:
+            self._used_caps[id(cap)] = cap
+        env = {tuple(o): v for o, v in zip(sub.outputs, cap.outputs)}
+        env["__replayed__"] = True
+        return env
+
+    def _capture_sub(self, sub, caps, car, feeds, sig):
+        static = [DArray.empty(v.shape, v.dtype, self.device) for v in car]
+        for src, dst in zip(car, static):
+            if src.size:
+                self._call(self._lib.pfb_copy, src.desc(), dst.desc(), self._stream, what="copy")
+        saved = (self._ws, self._err, self._err_nodes, self._stream)
+        self._ws = None
+        self._err = torch.zeros(_ERR_SLOTS, dtype=torch.int32, device=self.device)
+        self._err_nodes = []
+        graph = torch.cuda.CUDAGraph()
+        cap = None
+        try:
+            torch.cuda.synchronize(self.device)
+            l0, d0 = self.launch_count, self.dispatch_count
+            with torch.cuda.graph(graph):
+                self._stream = torch.cuda.current_stream(self.device).cuda_stream
+                env = self._run_graph(sub, {"capture": list(caps), "carried": static}, feeds)
+            outs = [env[tuple(o)] for o in sub.outputs]
+            if all(isinstance(v, DArray) for v in outs):
+                cap = _Captured(graph, static, outs, self._ws, self._err, list(self._err_nodes))
+                cap.launches = self.launch_count - l0
+                cap.dispatches = self.dispatch_count - d0
+                self._sub_captures[sig] = cap
+        except Exception:  # uncapturable: stay eager for this body
+            self._capture_ok[(id(sub), tuple(tuple(o) for o in sub.outputs))] = False
+            torch.cuda.synchronize(self.device)
+        finally:
+            self._ws, self._err, self._err_nodes, self._stream = saved
+        return cap
+
     def _load_feeds(self, static, feeds):
         for name, dst in static.items():
             v = feeds[name]
@@ -418,17 +493,26 @@ class Executor:
         return self._err.data_ptr() + 4 * k
 
     def _finish_errors(self):
-        if not (self.check_errors and self._err_nodes):
+        used = list(self._used_caps.values())
+        self._used_caps = {}
+        if not self.check_errors:
             return
-        n = min(len(self._err_nodes), _ERR_SLOTS)
-        bits = self._err[:n].cpu().numpy()
-        self.sync_count += 1
-        for k in np.nonzero(bits)[0]:
-            b = int(bits[k])
-            cause = (E.IndexOutOfBounds("index out of range") if b & N.DEV_OOB else
-                     E.IndexCollision("scatter_rows: overlapping index sets") if b & N.DEV_COLLISION
-                     else E.IncompleteCover("scatter_rows: rows uncovered"))
-            raise E.ExecError(self._err_nodes[k], cause)
+        sources = [(self._err, self._err_nodes)] + [(c.err, c.err_nodes) for c in used]
+        for buf, nodes in sources:
+            if not nodes:
+                continue
+            n = min(len(nodes), _ERR_SLOTS)
+            bits = buf[:n].cpu().numpy()
+            self.sync_count += 1
+            if buf is not self._err:
+                buf.zero_()
+            for k in np.nonzero(bits)[0]:
+                b = int(bits[k])
+                cause = (E.IndexOutOfBounds("index out of range") if b & N.DEV_OOB else
+                         E.IndexCollision("scatter_rows: overlapping index sets")
+                         if b & N.DEV_COLLISION else
+                         E.IncompleteCover("scatter_rows: rows uncovered"))
+                raise E.ExecError(nodes[k], cause)
 
     def _writeback_vars(self):
         for name, dv in self._dvars.items():
@@ -539,12 +623,16 @@ class Executor:
             car = [env[r] for r in node.inputs[:nc]]
             caps = [env[r] for r in node.inputs[nc:]]
             cg, bg = node.block.subgraphs["cond"], node.block.subgraphs["body"]
+            replayed = False
             while True:
                 bind = {"capture": caps, "carried": car}
-                cenv = self._run_graph(cg, bind, feeds)
+                cenv = self._run_sub(cg, bind, feeds)
                 if not self._host_bool(cenv[tuple(cg.outputs[0])]):
+                    if replayed:  # detach the results from the body graph's memory pool
+                        car = [self._dense_copy(v) if isinstance(v, DArray) else v for v in car]
                     return car
-                benv = self._run_graph(bg, bind, feeds)
+                benv = self._run_sub(bg, bind, feeds)
+                replayed = replayed or benv.get("__replayed__", False)
                 car = [benv[tuple(o)] for o in bg.outputs]
         self._tick(node)
         ins = [env[r] for r in node.inputs]
@@ -1009,6 +1097,18 @@ def _h_fused(ex, node, ins):
     return [out]
 
 
+def _h_select(ex, node, ins):
+    m, a, b = (ex._dev(v) for v in ins)
+    if m.dtype != DType.BOOL:
+        raise E.DTypeMismatch("select: mask must be bool")
+    if a.dtype != b.dtype:
+        raise E.DTypeMismatch(f"select: {a.dtype.value} vs {b.dtype.value}")
+    out = ex._empty(broadcast_shapes(broadcast_shapes(m.shape, a.shape), b.shape), a.dtype)
+    ex._call(ex._lib.pfb_select, m.desc(), a.desc(), b.desc(), out.desc(), ex._stream,
+             what="select", work=(_abytes(m, a, b, out), 0))
+    return [out]
+
+
 def _h_read_variable(ex, node, ins):
     name = node.attrs["name"]
     if name not in ex._dvars:
@@ -1060,6 +1160,7 @@ _HANDLERS.update({
     "where_true": _h_where_true, "complement": _h_complement, "dim0": _h_dim0,
     "range_vec": _h_range_vec, "read_variable": _h_read_variable, "assign": _h_assign,
     "assign_add": _h_assign, "random_uniform": _h_random_uniform, "fused_ew": _h_fused,
+    "select": _h_select,
 })
 
 

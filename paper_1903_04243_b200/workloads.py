@@ -285,7 +285,11 @@ def cfg4(api, n=256, steps=64, units=512, shard=None, registry=None):
 # ----------------------------------------------------------------------------
 # cfg5: auto-batched variable-length RNN (per-example while + cond)
 
-def cfg5(api, n=1024, max_len=100, units=256, shard=None, registry=None):
+def cfg5(api, n=1024, max_len=100, units=256, shard=None, registry=None, masked=False,
+         unroll=1):
+    """`masked=True` converts the per-example while/cond with predication
+    (Policy(masked_control=True)) instead of the reference's compaction:
+    same values, fixed shapes (CUDA-graph capturable loop body)."""
     r = np.random.default_rng(0)
     X0 = _f32(r.standard_normal((n, max_len, units)))
     L0 = r.integers(1, max_len + 1, n).astype(np.int64)
@@ -316,6 +320,9 @@ def cfg5(api, n=1024, max_len=100, units=256, shard=None, registry=None):
         return [bb.reshape(hf, [units])]
 
     kw = {} if registry is None else {"registry": registry}
+    if masked:
+        from .vectorize import Policy
+        kw["policy"] = Policy(masked_control=True, unroll=unroll)
     (H,) = _pfor(api, b, body, n, shard, **kw)
     b.graph.set_outputs([H])
     sel = slice(None) if shard is None else slice(shard[0], shard[1])

@@ -211,3 +211,19 @@ def test_fusion_reduces_launches(Executor):
     fused.run(feeds=w.feeds)
     plain.run(feeds=w.feeds)
     assert fused.launch_count < 0.7 * plain.launch_count, (fused.launch_count, plain.launch_count)
+
+
+@pytest.mark.parametrize("unroll", [1, 4])
+@pytest.mark.parametrize("name", ["cfg5", "cfg5_mid"])
+def test_masked_control_flow_vs_reference(name, unroll, golden, Executor):
+    """Predicated while/cond (fixed shapes) on device: reference values, and the
+    loop body is captured as a CUDA graph and replayed per trip."""
+    from paper_1903_04243_b200 import workloads as WL
+    _, kw = PROGRAM_CASES[name]
+    w = WL.cfg5(WL.this_api(), masked=True, unroll=unroll, **kw)
+    ex = Executor(w.graph)
+    for _ in range(3):
+        outs = ex.run(feeds=w.feeds)
+        for j, o in enumerate(outs):
+            check(o, golden["programs"][f"{name}/out/{j}"])
+    assert ex._sub_captures, "the predicated loop body should have been captured"
