@@ -11,18 +11,20 @@
 //     shared-memory tile (coalesced on whichever axis is unit-stride) and
 //     writes dense K-major hi and lo planes -- so every operand layout
 //     (transposed weights, MN-major activations) reaches the tensor core.
-//  2. gemm_kernel: persistent (one CTA per SM, static tile stride), 6 warps:
+//  2. gemm_kernel: persistent (one CTA per SM, static tile stride), 10 warps:
 //       warp 0    TMA producer: 4 tiles (A_hi, A_lo, B_hi, B_lo; 32 fp32 of K
 //                 = one 128B swizzle row each) per stage, 3-stage ring,
 //                 runs ahead across output tiles;
 //       warp 1    TMEM allocator + single-thread MMA issuer (UMMA 128x128x8):
 //                 4 k-steps x 3 products per stage into one of two TMEM
 //                 chunk buffers; every CHUNK_KB stages -> `acc_full[buf]`;
-//       warps 2-5 accumulators/epilogue: tcgen05.ld each finished chunk
-//                 (warp w owns TMEM lanes 32*(w%4)..+31), add into fp32
-//                 registers with round-to-nearest, release the buffer; after
-//                 the last chunk of a tile store it (optional per-row scale,
-//                 accumulate) while the MMA already fills the next tile.
+//       warps 2-9 accumulators/epilogue: tcgen05.ld each finished chunk
+//                 (warp w owns TMEM lanes 32*(w%4)..+31 and 64 of the 128
+//                 columns), add into fp32 registers with round-to-nearest,
+//                 release the buffer; after the last chunk of a tile store it
+//                 through a conflict-free smem transpose as 4-row x 128-byte
+//                 float4 stores (optional per-row scale, accumulate) while the
+//                 MMA already fills the next tile.
 //     The chunking exists because the tensor core's in-TMEM accumulation
 //     truncates: with full-K accumulation the 3xTF32 error grew linearly with
 //     K (measured ~1e-4 relative at K=4096); with 64-deep chunks summed in
@@ -42,10 +44,13 @@ constexpr int BM = 128, BN = 128, BK = 32, STAGES = 3, UMMA_K = 8;
 constexpr int CHUNK_KB = 2;                       // k-blocks accumulated in TMEM per chunk
 constexpr int TILE_BYTES = BM * BK * 4;           // 16 KB per operand tile
 constexpr int STAGE_BYTES = 4 * TILE_BYTES;       // A_hi, A_lo, B_hi, B_lo
-constexpr int EPI_STAGE_FLOATS = 32 * 33;         // per epilogue warp: 32x32 transpose tile
+constexpr int EPI_WARPS = 8;                      // 2 per TMEM lane quarter, 64 columns each
+constexpr int EPI_COLS = BN / 2;
+constexpr int EPI_STAGE_FLOATS = 32 * 32;         // per epilogue warp: one 32x32 block,
+                                                  // 16B chunks XOR-swizzled by row
 constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + 1024 /*align*/ + 256 /*barriers*/ +
-                           4 * EPI_STAGE_FLOATS * 4;
-constexpr int NUM_THREADS = 192;                  // 6 warps
+                           EPI_WARPS * EPI_STAGE_FLOATS * 4;
+constexpr int NUM_THREADS = 64 + 32 * EPI_WARPS;  // TMA, MMA, 8 epilogue warps
 constexpr int TMEM_COLS = 2 * BN;                 // double-buffered chunk accumulator
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
@@ -214,7 +219,7 @@ gemm_kernel(const __grid_constant__ CUtensorMap map_ah, const __grid_constant__ 
     }
     for (int b = 0; b < 2; ++b) {
       mbar_init(&acc_full[b], 1);
-      mbar_init(&acc_empty[b], 128);
+      mbar_init(&acc_empty[b], 32 * EPI_WARPS);
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
@@ -285,23 +290,28 @@ gemm_kernel(const __grid_constant__ CUtensorMap map_ah, const __grid_constant__ 
     }
     __syncwarp();
   } else {
-    // ---- accumulators + epilogue (warps 2..5, 128 threads) ----
+    // ---- accumulators + epilogue (warps 2..9): warp w owns TMEM lanes
+    // 32*(w%4)..+31 (its rows) and columns [half*64, half*64+64) ----
     const int quarter = warp & 3;
+    const int half = (warp - 2) >> 2;
+    float* stage = reinterpret_cast<float*>(smem + STAGES * STAGE_BYTES + 256) +
+                   (warp - 2) * EPI_STAGE_FLOATS;
     int gc = 0;
     for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {
       const int bz = t / tiles_per_batch, r = t % tiles_per_batch;
       const int m0 = (r / p.ntn) * BM, n0 = (r % p.ntn) * BN;
-      float acc[BN];
+      float acc[EPI_COLS];
 #pragma unroll
-      for (int j = 0; j < BN; ++j) acc[j] = 0.f;
+      for (int j = 0; j < EPI_COLS; ++j) acc[j] = 0.f;
       for (int c = 0; c < nchunks; ++c, ++gc) {
         const int buf = gc & 1;
         mbar_wait(&acc_full[buf], (gc >> 1) & 1);
         asm volatile("tcgen05.fence::after_thread_sync;");
 #pragma unroll
-        for (int cc = 0; cc < BN; cc += 32) {
+        for (int cc = 0; cc < EPI_COLS; cc += 32) {
           uint32_t v[32];
-          tmem_ld32(tmem_base + ((uint32_t)(quarter * 32) << 16) + (uint32_t)(buf * BN + cc), v);
+          tmem_ld32(tmem_base + ((uint32_t)(quarter * 32) << 16) +
+                        (uint32_t)(buf * BN + half * EPI_COLS + cc), v);
           asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 #pragma unroll
           for (int j = 0; j < 32; ++j) acc[cc + j] += __uint_as_float(v[j]);
@@ -309,26 +319,47 @@ gemm_kernel(const __grid_constant__ CUtensorMap map_ah, const __grid_constant__ 
         asm volatile("tcgen05.fence::before_thread_sync;");
         mbar_arrive(&acc_empty[buf]);
       }
-      // store through a per-warp 32x32 smem transpose so that every store
-      // instruction writes 32 consecutive columns of one row (128 B, coalesced)
-      float* stage = reinterpret_cast<float*>(smem + STAGES * STAGE_BYTES + 256) +
-                     (warp - 2) * EPI_STAGE_FLOATS;
+      // 32x32 blocks through smem: each lane writes its row as float4s, then
+      // every store instruction covers 4 rows x 128 contiguous bytes
       const int row0 = m0 + quarter * 32;
       float* cbase = p.C + bz * p.scb;
+      const int sub_r = lane >> 3, sub_c = (lane & 7) * 4;
 #pragma unroll
-      for (int cc = 0; cc < BN; cc += 32) {
+      for (int cc = 0; cc < EPI_COLS; cc += 32) {
 #pragma unroll
-        for (int j = 0; j < 32; ++j) stage[lane * 33 + j] = acc[cc + j];
+        for (int q = 0; q < 8; ++q)
+          *reinterpret_cast<float4*>(stage + lane * 32 + 4 * (q ^ (lane & 7))) =
+              make_float4(acc[cc + 4 * q], acc[cc + 4 * q + 1], acc[cc + 4 * q + 2],
+                          acc[cc + 4 * q + 3]);
         __syncwarp();
-        const int col = n0 + cc + lane;
-        for (int i = 0; i < 32; ++i) {
-          const int row = row0 + i;
-          if (row >= p.M) break;
-          const float alpha = p.alpha_rows ? __ldg(p.alpha_rows + (int64_t)bz * p.M + row) : 1.f;
-          if (col < p.N) {
+        const int col = n0 + half * EPI_COLS + cc + sub_c;
+#pragma unroll 4
+        for (int i = 0; i < 32; i += 4) {
+          const int row = row0 + i + sub_r;
+          if (row < p.M) {
+            const float alpha =
+                p.alpha_rows ? __ldg(p.alpha_rows + (int64_t)bz * p.M + row) : 1.f;
+            const int srow = i + sub_r;
+            float4 v = *reinterpret_cast<const float4*>(
+                stage + srow * 32 + 4 * ((sub_c >> 2) ^ (srow & 7)));
+            v.x *= alpha; v.y *= alpha; v.z *= alpha; v.w *= alpha;
             float* q = cbase + (int64_t)row * p.scm + (int64_t)col * p.scn;
-            const float v = stage[i * 33 + lane] * alpha;
-            *q = p.accumulate ? *q + v : v;
+            if (p.scn == 1 && col + 3 < p.N && ((reinterpret_cast<uintptr_t>(q) & 15) == 0)) {
+              if (p.accumulate) {
+                const float4 o = *reinterpret_cast<const float4*>(q);
+                v.x += o.x; v.y += o.y; v.z += o.z; v.w += o.w;
+              }
+              *reinterpret_cast<float4*>(q) = v;
+            } else {
+              const float e[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+              for (int j = 0; j < 4; ++j) {
+                if (col + j < p.N) {
+                  float* qq = q + (int64_t)j * p.scn;
+                  *qq = p.accumulate ? *qq + e[j] : e[j];
+                }
+              }
+            }
           }
         }
         __syncwarp();
