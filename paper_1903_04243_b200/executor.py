@@ -227,6 +227,7 @@ class Executor:
         self._capture_ok = {}
         self._warm = set()
         self._sub_captures = {}
+        self.capture_failures = []
         self._sub_warm = set()
         self._used_caps = {}
         self._pinned = {}
@@ -343,7 +344,8 @@ class Executor:
             cap.launches = self.launch_count - l0
             cap.dispatches = self.dispatch_count - d0
             self._captures[sig] = cap
-        except Exception:  # anything the capture cannot take: stay eager for this graph
+        except Exception as e:  # anything the capture cannot take: stay eager for this graph
+            self.capture_failures.append(f"graph: {type(e).__name__}: {e}")
             self._capture_ok[(id(g), tuple(keys))] = False
             torch.cuda.synchronize(self.device)
         finally:
@@ -415,7 +417,8 @@ class Executor:
                 cap.launches = self.launch_count - l0
                 cap.dispatches = self.dispatch_count - d0
                 self._sub_captures[sig] = cap
-        except Exception:  # uncapturable: stay eager for this body
+        except Exception as e:  # uncapturable: stay eager for this body
+            self.capture_failures.append(f"sub-graph: {type(e).__name__}: {e}")
             self._capture_ok[(id(sub), tuple(tuple(o) for o in sub.outputs))] = False
             torch.cuda.synchronize(self.device)
         finally:

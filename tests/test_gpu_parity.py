@@ -226,4 +226,4 @@ def test_masked_control_flow_vs_reference(name, unroll, golden, Executor):
         outs = ex.run(feeds=w.feeds)
         for j, o in enumerate(outs):
             check(o, golden["programs"][f"{name}/out/{j}"])
-    assert ex._sub_captures, "the predicated loop body should have been captured"
+    assert ex._sub_captures, f"loop body not captured: {ex.capture_failures}"
