@@ -366,13 +366,16 @@ class Executor:
         afterwards (carried values copied into static inputs, captures read in
         place).  Predicated while loops (vectorize Policy(masked_control))
         produce exactly such bodies."""
-        vals = list(bind.get("capture", [])) + list(bind.get("carried", []))
+        caps, car = bind.get("capture", []), bind.get("carried", [])
         if not (self.cuda_graph and self.kernel_timer is None
-                and all(isinstance(v, DArray) for v in vals)
+                and all(isinstance(v, DArray) for v in car)
+                and all(isinstance(v, (DArray, HostVal)) for v in caps)
                 and self._capturable(sub, [tuple(o) for o in sub.outputs])):
             return self._run_graph(sub, bind, feeds)
-        caps, car = bind.get("capture", []), bind.get("carried", [])
-        sig = (id(sub), tuple((v.ptr, v.shape, v.strides, v.dtype) for v in caps),
+        # captures are read in place (device) or baked in (host scalars)
+        sig = (id(sub),
+               tuple((v.ptr, v.shape, v.strides, v.dtype) if isinstance(v, DArray)
+                     else ("host", id(v), v.value.tobytes(), v.dtype) for v in caps),
                tuple((v.shape, v.dtype) for v in car))
         cap = self._sub_captures.get(sig)
         if cap is None:
