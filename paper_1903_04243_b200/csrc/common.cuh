@@ -3,6 +3,9 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 #include <math.h>
+#include <stdlib.h>
+
+#include <utility>
 
 #include "../../include/pfb.h"
 
@@ -120,6 +123,40 @@ __device__ __forceinline__ void offsets(const Layout& L, IdxT lin, int64_t* off)
 #pragma unroll
     for (int o = 0; o < NOPS; ++o) off[o] += (int64_t)c * L.st[o][d];
   }
+}
+
+// Programmatic dependent launch: every kernel waits for its predecessor's
+// memory at entry (griddepcontrol.wait) and immediately lets its successor
+// start launching (launch_dependents), so back-to-back small kernels overlap
+// their launch latency -- they are captured as programmatic edges in the CUDA
+// graphs the executor replays.  Both are no-ops without the launch attribute.
+__device__ __forceinline__ void pdl_enter() {
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  asm volatile("griddepcontrol.launch_dependents;" :::);
+}
+
+inline bool pdl_enabled() {
+  static const int on = [] {
+    const char* e = getenv("PFB_DISABLE_PDL");
+    return (e && e[0] == '1') ? 0 : 1;
+  }();
+  return on;
+}
+
+template <typename... KArgs, typename... Args>
+inline void launch(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s,
+                   Args&&... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = pdl_enabled() ? 1 : 0;
+  cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...);
 }
 
 __device__ __forceinline__ void set_err(int32_t* err, int32_t bits) {

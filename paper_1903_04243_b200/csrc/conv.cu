@@ -17,6 +17,7 @@ struct ConvDims {
 // x/out/f must be dense (executor materialises views first)
 __global__ void conv2d_direct(ConvDims d, const float* __restrict__ x, const float* __restrict__ f,
                               float* __restrict__ out) {
+  pdl_enter();
   const int64_t total = d.b * d.h * d.w * d.c2;
   for (int64_t lin = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; lin < total;
        lin += (int64_t)gridDim.x * blockDim.x) {
@@ -43,6 +44,7 @@ __global__ void conv2d_direct(ConvDims d, const float* __restrict__ x, const flo
 
 __global__ void conv2d_input_grad_direct(ConvDims d, const float* __restrict__ gy,
                                          const float* __restrict__ f, float* __restrict__ dx) {
+  pdl_enter();
   const int64_t total = d.b * d.h * d.w * d.c1;
   for (int64_t lin = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; lin < total;
        lin += (int64_t)gridDim.x * blockDim.x) {
@@ -69,6 +71,7 @@ __global__ void conv2d_input_grad_direct(ConvDims d, const float* __restrict__ g
 }
 
 __global__ void im2col_kernel(ConvDims d, const float* __restrict__ x, float* __restrict__ cols) {
+  pdl_enter();
   const int64_t kc = (int64_t)d.k1 * d.k2 * d.c1;
   const int64_t total = d.b * d.h * d.w * kc;
   for (int64_t lin = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; lin < total;
@@ -104,7 +107,7 @@ extern "C" int pfb_im2col(const pfb_tensor* x, int32_t k1, int32_t k2, pfb_tenso
   same_pad(k2, &d.p2);
   int64_t n = d.b * d.h * d.w * k1 * k2 * d.c1;
   if (n == 0) return 0;
-  im2col_kernel<<<grid_for(n, 256), 256, 0, as_stream(stream)>>>(d, (const float*)x->data,
+  launch(im2col_kernel, grid_for(n, 256), 256, 0, as_stream(stream), d, (const float*)x->data,
                                                                  (float*)out->data);
   return launch_status();
 }
@@ -120,7 +123,7 @@ extern "C" int pfb_conv2d(const pfb_tensor* x, const pfb_tensor* f, pfb_tensor* 
   same_pad(d.k2, &d.p2);
   int64_t n = d.b * d.h * d.w * d.c2;
   if (n == 0) return 0;
-  conv2d_direct<<<grid_for(n, 256), 256, 0, as_stream(stream)>>>(d, (const float*)x->data,
+  launch(conv2d_direct, grid_for(n, 256), 256, 0, as_stream(stream), d, (const float*)x->data,
                                                                  (const float*)f->data,
                                                                  (float*)out->data);
   return launch_status();
@@ -138,7 +141,7 @@ extern "C" int pfb_conv2d_input_grad(const pfb_tensor* gy, const pfb_tensor* f, 
   same_pad(d.k2, &d.p2);
   int64_t n = d.b * d.h * d.w * d.c1;
   if (n == 0) return 0;
-  conv2d_input_grad_direct<<<grid_for(n, 256), 256, 0, as_stream(stream)>>>(
+  launch(conv2d_input_grad_direct, grid_for(n, 256), 256, 0, as_stream(stream), 
       d, (const float*)gy->data, (const float*)f->data, (float*)out->data);
   return launch_status();
 }

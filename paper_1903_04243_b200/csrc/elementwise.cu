@@ -152,6 +152,7 @@ template <typename Tin, typename Tout, typename F, typename IdxT, int NIN>
 __global__ void __launch_bounds__(256) ew_vec4_kernel(Layout L, IdxT nchunks, Tout* out,
                                                       const Tin* a, const Tin* b, F f,
                                                       unsigned vecmask) {
+  pdl_enter();
   const int last = L.rank - 1;
   const int64_t so = L.st[0][last], sa = L.st[1][last], sb = NIN > 1 ? L.st[2][last] : 0;
   for (IdxT c = blockIdx.x * (IdxT)blockDim.x + threadIdx.x; c < nchunks;
@@ -171,6 +172,7 @@ __global__ void __launch_bounds__(256) ew_vec4_kernel(Layout L, IdxT nchunks, To
 template <typename Tin, typename Tout, typename F, typename IdxT, int NIN>
 __global__ void __launch_bounds__(256) ew_scalar_kernel(Layout L, IdxT n, Tout* out,
                                                         const Tin* a, const Tin* b, F f) {
+  pdl_enter();
   for (IdxT i = blockIdx.x * (IdxT)blockDim.x + threadIdx.x; i < n;
        i += (IdxT)gridDim.x * blockDim.x) {
     int64_t off[NIN + 1];
@@ -205,18 +207,18 @@ int launch_ew(const Layout& L, void* out, const void* a, const void* b, F f, cud
     int64_t chunks = n / 4;
     int grid = grid_for(chunks, block);
     if (small)
-      ew_vec4_kernel<Tin, Tout, F, uint32_t, NIN><<<grid, block, 0, s>>>(
+      launch(ew_vec4_kernel<Tin, Tout, F, uint32_t, NIN>, grid, block, 0, s, 
           L, (uint32_t)chunks, (Tout*)out, (const Tin*)a, (const Tin*)b, f, vecmask);
     else
-      ew_vec4_kernel<Tin, Tout, F, int64_t, NIN><<<grid, block, 0, s>>>(
+      launch(ew_vec4_kernel<Tin, Tout, F, int64_t, NIN>, grid, block, 0, s, 
           L, chunks, (Tout*)out, (const Tin*)a, (const Tin*)b, f, vecmask);
   } else {
     int grid = grid_for(n, block);
     if (small)
-      ew_scalar_kernel<Tin, Tout, F, uint32_t, NIN><<<grid, block, 0, s>>>(
+      launch(ew_scalar_kernel<Tin, Tout, F, uint32_t, NIN>, grid, block, 0, s, 
           L, (uint32_t)n, (Tout*)out, (const Tin*)a, (const Tin*)b, f);
     else
-      ew_scalar_kernel<Tin, Tout, F, int64_t, NIN><<<grid, block, 0, s>>>(
+      launch(ew_scalar_kernel<Tin, Tout, F, int64_t, NIN>, grid, block, 0, s, 
           L, n, (Tout*)out, (const Tin*)a, (const Tin*)b, f);
   }
   return launch_status();
@@ -323,6 +325,7 @@ __global__ void __launch_bounds__(256) fused_kernel(Layout L, IdxT n, FusedProgr
                                                     const void* i2, const void* i3,
                                                     const void* i4, const void* i5,
                                                     const void* i6, const void* i7) {
+  pdl_enter();
   const void* ins[8] = {i0, i1, i2, i3, i4, i5, i6, i7};
   for (IdxT i = blockIdx.x * (IdxT)blockDim.x + threadIdx.x; i < n;
        i += (IdxT)gridDim.x * blockDim.x) {
@@ -356,7 +359,7 @@ void launch_fused(int n_in, const Layout& L, IdxT n, const FusedProgram& P, Tout
   const int grid = grid_for((int64_t)n, 256);
 #define PFB_FUSED_CASE(K)                                                                    \
   case K:                                                                                    \
-    fused_kernel<IdxT, Tout, K><<<grid, 256, 0, s>>>(L, n, P, out, p[0], p[1], p[2], p[3],  \
+    launch(fused_kernel<IdxT, Tout, K>, grid, 256, 0, s, L, n, P, out, p[0], p[1], p[2], p[3],  \
                                                      p[4], p[5], p[6], p[7]);                \
     break;
   switch (n_in) {
@@ -430,6 +433,7 @@ extern "C" int pfb_copy(const pfb_tensor* x, pfb_tensor* out, void* stream) {
 namespace pfb {
 template <typename T>
 __global__ void fill_kernel(Layout L, int64_t n, T* out, T v) {
+  pdl_enter();
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
        i += (int64_t)gridDim.x * blockDim.x) {
     int64_t off[1];
@@ -446,9 +450,9 @@ extern "C" int pfb_fill(pfb_tensor* out, double value, void* stream) {
   if (n == 0) return 0;
   cudaStream_t s = as_stream(stream);
   int grid = grid_for(n, 256);
-  if (out->dtype == PFB_F32) fill_kernel<float><<<grid, 256, 0, s>>>(L, n, (float*)out->data, (float)value);
-  else if (out->dtype == PFB_I64) fill_kernel<int64_t><<<grid, 256, 0, s>>>(L, n, (int64_t*)out->data, (int64_t)value);
-  else fill_kernel<uint8_t><<<grid, 256, 0, s>>>(L, n, (uint8_t*)out->data, (uint8_t)(value != 0.0));
+  if (out->dtype == PFB_F32) launch(fill_kernel<float>, grid, 256, 0, s, L, n, (float*)out->data, (float)value);
+  else if (out->dtype == PFB_I64) launch(fill_kernel<int64_t>, grid, 256, 0, s, L, n, (int64_t*)out->data, (int64_t)value);
+  else launch(fill_kernel<uint8_t>, grid, 256, 0, s, L, n, (uint8_t*)out->data, (uint8_t)(value != 0.0));
   return launch_status();
 }
 
@@ -497,6 +501,7 @@ namespace pfb {
 template <typename T, typename IdxT>
 __global__ void __launch_bounds__(256) select_kernel(Layout L, IdxT n, T* out, const uint8_t* m,
                                                      const T* a, const T* b) {
+  pdl_enter();
   for (IdxT i = blockIdx.x * (IdxT)blockDim.x + threadIdx.x; i < n;
        i += (IdxT)gridDim.x * blockDim.x) {
     int64_t off[4];
@@ -510,11 +515,11 @@ int select_run(const Layout& L, int64_t n, pfb_tensor* out, const pfb_tensor* m,
                const pfb_tensor* a, const pfb_tensor* b, cudaStream_t s) {
   const int grid = grid_for(n, 256);
   if (n < (int64_t)0x7fffffff)
-    select_kernel<T, uint32_t><<<grid, 256, 0, s>>>(L, (uint32_t)n, (T*)out->data,
+    launch(select_kernel<T, uint32_t>, grid, 256, 0, s, L, (uint32_t)n, (T*)out->data,
                                                     (const uint8_t*)m->data, (const T*)a->data,
                                                     (const T*)b->data);
   else
-    select_kernel<T, int64_t><<<grid, 256, 0, s>>>(L, n, (T*)out->data, (const uint8_t*)m->data,
+    launch(select_kernel<T, int64_t>, grid, 256, 0, s, L, n, (T*)out->data, (const uint8_t*)m->data,
                                                    (const T*)a->data, (const T*)b->data);
   return launch_status();
 }

@@ -34,6 +34,7 @@ static int matmul_args(const pfb_tensor* a, const pfb_tensor* b, pfb_tensor* out
 }
 
 __global__ void zero_f32(float* p, int64_t n) {
+  pdl_enter();
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
        i += (int64_t)gridDim.x * blockDim.x)
     p[i] = 0.f;
@@ -59,7 +60,7 @@ extern "C" int pfb_matmul_ex(const pfb_tensor* a, const pfb_tensor* b, pfb_tenso
     if (accumulate) return 0;
     if (!is_dense(out)) return PFB_E_UNSUPPORTED;
     int64_t n = numel(out);
-    zero_f32<<<grid_for(n, 256), 256, 0, s>>>((float*)out->data, n);
+    launch(zero_f32, grid_for(n, 256), 256, 0, s, (float*)out->data, n);
     return launch_status();
   }
   // force_path: 0 = auto, 1 = SIMT, 2 = tcgen05 (error if ineligible).

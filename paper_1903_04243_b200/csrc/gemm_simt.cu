@@ -45,6 +45,7 @@ __device__ __forceinline__ void store_row4(const GemmArgs& g, int64_t b, int64_t
 // partials: nullptr -> epilogue straight to C; else ws[split][b][M][N]
 __global__ void __launch_bounds__(256) gemm_simt_kernel(GemmArgs g, int splits, int64_t kchunk,
                                                         float* partials) {
+  pdl_enter();
   __shared__ float As[BK][BM + 4];
   __shared__ float Bs[BK][BN + 4];
   const int64_t bz = blockIdx.z / splits;
@@ -110,6 +111,7 @@ __global__ void __launch_bounds__(256) gemm_simt_kernel(GemmArgs g, int splits, 
 }
 
 __global__ void splitk_reduce(GemmArgs g, int splits, const float* partials) {
+  pdl_enter();
   const int64_t per = g.M * g.N, total = g.batch * per;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
        i += (int64_t)gridDim.x * blockDim.x) {
@@ -129,6 +131,7 @@ __global__ void splitk_reduce(GemmArgs g, int splits, const float* partials) {
 // per iteration with one 128-bit store -- a warp writes 512 contiguous bytes.
 template <bool VEC>
 __global__ void __launch_bounds__(256) gemm_smallk_kernel(GemmArgs g) {
+  pdl_enter();
   const int64_t rows = g.batch * g.M;
   const int64_t nq = (g.N + 3) / 4;
   for (int64_t row = blockIdx.x; row < rows; row += gridDim.x) {
@@ -177,8 +180,8 @@ static int smallk_launch(const GemmArgs& g, cudaStream_t s) {
                    (reinterpret_cast<uintptr_t>(g.C) & 15) == 0;
   const int64_t rows = g.batch * g.M;
   const int grid = (int)std::min<int64_t>(rows, (int64_t)kNumSMs * 8);
-  if (vec) gemm_smallk_kernel<true><<<grid, 256, 0, s>>>(g);
-  else gemm_smallk_kernel<false><<<grid, 256, 0, s>>>(g);
+  if (vec) launch(gemm_smallk_kernel<true>, grid, 256, 0, s, g);
+  else launch(gemm_smallk_kernel<false>, grid, 256, 0, s, g);
   return launch_status();
 }
 
@@ -205,9 +208,9 @@ int gemm_simt(const GemmArgs& g, void* ws, int64_t ws_bytes, cudaStream_t s) {
   dim3 grid((unsigned)((g.N + BN - 1) / BN), (unsigned)((g.M + BM - 1) / BM),
             (unsigned)(g.batch * splits));
   if (grid.y > 65535 || grid.z > 65535) return PFB_E_UNSUPPORTED;
-  gemm_simt_kernel<<<grid, 256, 0, s>>>(g, splits, kchunk, splits > 1 ? (float*)ws : nullptr);
+  launch(gemm_simt_kernel, grid, 256, 0, s, g, splits, kchunk, splits > 1 ? (float*)ws : nullptr);
   if (splits > 1)
-    splitk_reduce<<<grid_for(g.batch * g.M * g.N, 256), 256, 0, s>>>(g, splits, (const float*)ws);
+    launch(splitk_reduce, grid_for(g.batch * g.M * g.N, 256), 256, 0, s, g, splits, (const float*)ws);
   return launch_status();
 }
 

@@ -151,6 +151,7 @@ __global__ void __launch_bounds__(256) split_kernel(const float* __restrict__ x,
                                                     int64_t K, int64_t Kp, int64_t sb, int64_t sr,
                                                     int64_t sk, float* __restrict__ hi,
                                                     float* __restrict__ lo) {
+  pdl_enter();
   __shared__ float t[32][33];
   const int64_t b = blockIdx.z;
   const int64_t r0 = (int64_t)blockIdx.y * 32, k0 = (int64_t)blockIdx.x * 32;
@@ -193,6 +194,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
 gemm_kernel(const __grid_constant__ CUtensorMap map_ah, const __grid_constant__ CUtensorMap map_al,
             const __grid_constant__ CUtensorMap map_bh, const __grid_constant__ CUtensorMap map_bl,
             Params p) {
+  pdl_enter();
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>(
       (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -464,8 +466,8 @@ int gemm_tcgen05(const GemmArgs& g, void* ws, int64_t ws_bytes, cudaStream_t s) 
   // split (and re-layout) both operands; padded K columns are written as 0
   dim3 ga((unsigned)((Kp + 31) / 32), (unsigned)((g.M + 31) / 32), (unsigned)ba);
   dim3 gb((unsigned)((Kp + 31) / 32), (unsigned)((g.N + 31) / 32), (unsigned)bb);
-  split_kernel<<<ga, 256, 0, s>>>(g.A, g.M, g.K, Kp, g.sab, g.sam, g.sak, ah, al);
-  split_kernel<<<gb, 256, 0, s>>>(g.B, g.N, g.K, Kp, g.sbb, g.sbn, g.sbk, bh, bl);
+  launch(split_kernel, ga, 256, 0, s, g.A, g.M, g.K, Kp, g.sab, g.sam, g.sak, ah, al);
+  launch(split_kernel, gb, 256, 0, s, g.B, g.N, g.K, Kp, g.sbb, g.sbn, g.sbk, bh, bl);
   CUtensorMap mah, mal, mbh, mbl;
   if (!make_map(&mah, ah, Kp, g.M, ba) || !make_map(&mal, al, Kp, g.M, ba) ||
       !make_map(&mbh, bh, Kp, g.N, bb) || !make_map(&mbl, bl, Kp, g.N, bb))
@@ -480,7 +482,7 @@ int gemm_tcgen05(const GemmArgs& g, void* ws, int64_t ws_bytes, cudaStream_t s) 
            g.C, g.scb, g.scm, g.scn, g.alpha_rows, g.accumulate};
   const int64_t ntiles = (int64_t)p.ntm * p.ntn * g.batch;
   const int grid = (int)std::min<int64_t>(ntiles, num_sms());
-  gemm_kernel<<<grid, NUM_THREADS, SMEM_BYTES, s>>>(mah, mal, mbh, mbl, p);
+  launch(gemm_kernel, grid, NUM_THREADS, SMEM_BYTES, s, mah, mal, mbh, mbl, p);
   return launch_status();
 }
 

@@ -14,6 +14,7 @@ __global__ void __launch_bounds__(256) gather_kernel(Layout Lt, int64_t k, int64
                                                      const T* x, int64_t xrow, int64_t nrows,
                                                      const int64_t* idx, int64_t idx_st, T* out,
                                                      int64_t orow, int32_t* err) {
+  pdl_enter();
   const int64_t per = VEC ? D / 4 : D;
   const int64_t total = k * per;
   for (int64_t lin = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; lin < total;
@@ -59,11 +60,11 @@ int gather_run(const pfb_tensor* x, const pfb_tensor* idx, pfb_tensor* out, int3
   int64_t work = k * (vec ? D / 4 : D);
   int grid = grid_for(work, 256);
   if (vec)
-    gather_kernel<T, true><<<grid, 256, 0, s>>>(Lt, k, D, (const T*)x->data, x->stride[0],
+    launch(gather_kernel<T, true>, grid, 256, 0, s, Lt, k, D, (const T*)x->data, x->stride[0],
                                                  x->shape[0], (const int64_t*)idx->data, idx_st,
                                                  (T*)out->data, orow, err);
   else
-    gather_kernel<T, false><<<grid, 256, 0, s>>>(Lt, k, D, (const T*)x->data, x->stride[0],
+    launch(gather_kernel<T, false>, grid, 256, 0, s, Lt, k, D, (const T*)x->data, x->stride[0],
                                                   x->shape[0], (const int64_t*)idx->data, idx_st,
                                                   (T*)out->data, orow, err);
   return launch_status();
@@ -74,6 +75,7 @@ int gather_run(const pfb_tensor* x, const pfb_tensor* idx, pfb_tensor* out, int3
 
 __global__ void count_rows(const int64_t* idx, int64_t st, int64_t k, int64_t total,
                            int32_t* cnt, int32_t* err) {
+  pdl_enter();
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < k;
        i += (int64_t)gridDim.x * blockDim.x) {
     int64_t r = idx[i * st];
@@ -83,6 +85,7 @@ __global__ void count_rows(const int64_t* idx, int64_t st, int64_t k, int64_t to
 }
 
 __global__ void check_cover(const int32_t* cnt, int64_t total, int32_t* err) {
+  pdl_enter();
   int32_t bits = 0;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
        i += (int64_t)gridDim.x * blockDim.x) {
@@ -99,6 +102,7 @@ __global__ void __launch_bounds__(256) scatter_kernel(Layout Lt, int64_t k, int6
                                                       const int64_t* idx, int64_t idx_st,
                                                       int64_t total, const T* src, int64_t srow,
                                                       T* out, int64_t orow) {
+  pdl_enter();
   const int64_t n = k * D;
   for (int64_t lin = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; lin < n;
        lin += (int64_t)gridDim.x * blockDim.x) {
@@ -121,6 +125,7 @@ __global__ void __launch_bounds__(256) scatter_kernel(Layout Lt, int64_t k, int6
 }
 
 __global__ void check_bounds(const int64_t* idx, int64_t st, int64_t k, int64_t total, int32_t* err) {
+  pdl_enter();
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < k;
        i += (int64_t)gridDim.x * blockDim.x) {
     int64_t r = idx[i * st];
@@ -146,7 +151,7 @@ int scatter_part(const pfb_tensor* idx, const pfb_tensor* src, int64_t total, pf
   const int64_t* st[2] = {out->stride + 1, src->stride + s0};
   Layout Lt = make_layout(tail_rank, out->shape + 1, 2, st);
   int64_t srow = s0 ? src->stride[0] : 0;
-  scatter_kernel<T, ADD><<<grid_for(k * D, 256), 256, 0, s>>>(
+  launch(scatter_kernel<T, ADD>, grid_for(k * D, 256), 256, 0, s, 
       Lt, k, D, (const int64_t*)idx->data, idx_st, total, (const T*)src->data, srow,
       (T*)out->data, out->stride[0]);
   return launch_status();
@@ -200,6 +205,7 @@ __device__ __forceinline__ int block_exclusive_scan(int v, int* smem, int* total
 // phase 1: per-tile counts
 __global__ void __launch_bounds__(kScanThreads) tile_counts(const uint8_t* m, int64_t st, int64_t n,
                                                             int64_t* counts) {
+  pdl_enter();
   __shared__ int smem[32];
   int64_t t0 = blockIdx.x * (int64_t)kTile + threadIdx.x * kScanPer;
   int c = 0;
@@ -213,6 +219,7 @@ __global__ void __launch_bounds__(kScanThreads) tile_counts(const uint8_t* m, in
 // phase 2: exclusive scan of tile counts (single block, loops)
 __global__ void __launch_bounds__(kScanThreads) scan_counts(int64_t* counts, int64_t nt,
                                                             int64_t* dev_count) {
+  pdl_enter();
   __shared__ int smem[32];
   int64_t carry = 0;
   for (int64_t b = 0; b < nt; b += kScanThreads) {
@@ -230,6 +237,7 @@ __global__ void __launch_bounds__(kScanThreads) scan_counts(int64_t* counts, int
 __global__ void __launch_bounds__(kScanThreads) tile_write(const uint8_t* m, int64_t st, int64_t n,
                                                            const int64_t* offs, int64_t* out,
                                                            int64_t* dev_count, int single) {
+  pdl_enter();
   __shared__ int smem[32];
   int64_t t0 = blockIdx.x * (int64_t)kTile + threadIdx.x * kScanPer;
   uint8_t f[kScanPer];
@@ -255,18 +263,19 @@ int where_true_u8(const uint8_t* m, int64_t st, int64_t n, int64_t* out, int64_t
   }
   int64_t nt = (n + kTile - 1) / kTile;
   if (nt == 1) {
-    tile_write<<<1, kScanThreads, 0, s>>>(m, st, n, nullptr, out, dev_count, 1);
+    launch(tile_write, 1, kScanThreads, 0, s, m, st, n, nullptr, out, dev_count, 1);
     return launch_status();
   }
   if (ws == nullptr || ws_bytes < nt * (int64_t)sizeof(int64_t)) return PFB_E_ARG;
   int64_t* counts = (int64_t*)ws;
-  tile_counts<<<(unsigned)nt, kScanThreads, 0, s>>>(m, st, n, counts);
-  scan_counts<<<1, kScanThreads, 0, s>>>(counts, nt, dev_count);
-  tile_write<<<(unsigned)nt, kScanThreads, 0, s>>>(m, st, n, counts, out, dev_count, 0);
+  launch(tile_counts, (unsigned)nt, kScanThreads, 0, s, m, st, n, counts);
+  launch(scan_counts, 1, kScanThreads, 0, s, counts, nt, dev_count);
+  launch(tile_write, (unsigned)nt, kScanThreads, 0, s, m, st, n, counts, out, dev_count, 0);
   return launch_status();
 }
 
 __global__ void mark_kernel(uint8_t* mark, int64_t total, const int64_t* idx, int64_t st, int64_t k) {
+  pdl_enter();
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < k;
        i += (int64_t)gridDim.x * blockDim.x) {
     int64_t r = idx[i * st];
@@ -275,6 +284,7 @@ __global__ void mark_kernel(uint8_t* mark, int64_t total, const int64_t* idx, in
 }
 
 __global__ void iota_kernel(int64_t* out, int64_t n, int64_t start) {
+  pdl_enter();
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
        i += (int64_t)gridDim.x * blockDim.x)
     out[i] = start + i;
@@ -294,6 +304,7 @@ __host__ __device__ __forceinline__ uint64_t mix64(uint64_t x) {
 }
 
 __global__ void rng_kernel(float* out, int64_t n, uint64_t dctr) {
+  pdl_enter();
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
        i += (int64_t)gridDim.x * blockDim.x) {
     uint64_t bits = mix64(dctr ^ (uint64_t)i);
@@ -329,16 +340,16 @@ extern "C" int pfb_scatter_rows(int32_t n_parts, const pfb_tensor* index_sets,
       const pfb_tensor* ix = &index_sets[p];
       int64_t k = ix->rank == 0 ? 1 : ix->shape[0];
       if (k == 0) continue;
-      count_rows<<<grid_for(k, 256), 256, 0, s>>>((const int64_t*)ix->data,
+      launch(count_rows, grid_for(k, 256), 256, 0, s, (const int64_t*)ix->data,
                                                  ix->rank ? ix->stride[0] : 0, k, total,
                                                  ws_count, dev_err);
     }
-    check_cover<<<grid_for(total, 256), 256, 0, s>>>(ws_count, total, dev_err);
+    launch(check_cover, grid_for(total, 256), 256, 0, s, ws_count, total, dev_err);
   } else {
     for (int p = 0; p < n_parts; ++p) {
       const pfb_tensor* ix = &index_sets[p];
       int64_t k = ix->rank == 0 ? 1 : ix->shape[0];
-      if (k) check_bounds<<<grid_for(k, 256), 256, 0, s>>>((const int64_t*)ix->data,
+      if (k) launch(check_bounds, grid_for(k, 256), 256, 0, s, (const int64_t*)ix->data,
                                                            ix->rank ? ix->stride[0] : 0, k, total,
                                                            dev_err);
     }
@@ -357,7 +368,7 @@ extern "C" int pfb_scatter_add_rows(const pfb_tensor* idx, const pfb_tensor* upd
   int64_t n = numel(out);
   if (n) cudaMemsetAsync(out->data, 0, n * dtype_size(out->dtype), s);
   int64_t k = idx->rank == 0 ? 1 : idx->shape[0];
-  if (k) check_bounds<<<grid_for(k, 256), 256, 0, s>>>((const int64_t*)idx->data,
+  if (k) launch(check_bounds, grid_for(k, 256), 256, 0, s, (const int64_t*)idx->data,
                                                        idx->rank ? idx->stride[0] : 0, k, total,
                                                        dev_err);
   if (int e = scatter_dispatch<true>(idx, updates, total, out, s)) return e;
@@ -385,7 +396,7 @@ extern "C" int pfb_complement(const pfb_tensor* idx, int64_t total, pfb_tensor* 
   uint8_t* mark = (uint8_t*)ws;
   cudaMemsetAsync(mark, 1, total, s);
   int64_t k = idx->rank == 0 ? 1 : idx->shape[0];
-  if (k) mark_kernel<<<grid_for(k, 256), 256, 0, s>>>(mark, total, (const int64_t*)idx->data,
+  if (k) launch(mark_kernel, grid_for(k, 256), 256, 0, s, mark, total, (const int64_t*)idx->data,
                                                       idx->rank ? idx->stride[0] : 0, k);
   return where_true_u8(mark, 1, total, (int64_t*)out->data, dev_count, (char*)ws + mark_bytes,
                        ws_bytes - mark_bytes, s);
@@ -395,7 +406,7 @@ extern "C" int pfb_iota(pfb_tensor* out, int64_t start, void* stream) {
   if (out->dtype != PFB_I64 || !is_dense(out)) return PFB_E_DTYPE;
   int64_t n = numel(out);
   if (n == 0) return 0;
-  iota_kernel<<<grid_for(n, 256), 256, 0, as_stream(stream)>>>((int64_t*)out->data, n, start);
+  launch(iota_kernel, grid_for(n, 256), 256, 0, as_stream(stream), (int64_t*)out->data, n, start);
   return launch_status();
 }
 
@@ -404,6 +415,6 @@ extern "C" int pfb_rng_uniform(uint64_t seed, uint64_t counter, pfb_tensor* out,
   int64_t n = numel(out);
   if (n == 0) return 0;
   uint64_t dctr = mix64(mix64(seed) ^ counter);
-  rng_kernel<<<grid_for(n, 256), 256, 0, as_stream(stream)>>>((float*)out->data, n, dctr);
+  launch(rng_kernel, grid_for(n, 256), 256, 0, as_stream(stream), (float*)out->data, n, dctr);
   return launch_status();
 }

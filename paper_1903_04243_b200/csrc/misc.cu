@@ -17,6 +17,7 @@ namespace pfb {
 __global__ void outer_sq_norm_kernel(int64_t n, int64_t da, int64_t db, const float* a,
                                      int64_t sa0, int64_t sa1, const float* b, int64_t sb0,
                                      int64_t sb1, float* out) {
+  pdl_enter();
   __shared__ float red[2][8];
   int64_t i = blockIdx.x;
   float sa = 0.f, sb = 0.f;
@@ -52,7 +53,7 @@ extern "C" int pfb_outer_sq_norm(const pfb_tensor* a, const pfb_tensor* b, pfb_t
   if (sq_norm->rank != 1 || sq_norm->shape[0] != a->shape[0] || !is_dense(sq_norm)) return PFB_E_SHAPE;
   int64_t n = a->shape[0];
   if (n == 0) return 0;
-  outer_sq_norm_kernel<<<(unsigned)n, 256, 0, as_stream(stream)>>>(
+  launch(outer_sq_norm_kernel, (unsigned)n, 256, 0, as_stream(stream), 
       n, a->shape[1], b->shape[1], (const float*)a->data, a->stride[0], a->stride[1],
       (const float*)b->data, b->stride[0], b->stride[1], (float*)sq_norm->data);
   return launch_status();

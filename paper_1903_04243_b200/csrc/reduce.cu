@@ -64,6 +64,7 @@ __device__ __forceinline__ T warp_sum(T v) {
 template <typename T>
 __global__ void __launch_bounds__(256) reduce_inner_warp(RedDesc D, int64_t K, int64_t R,
                                                          const T* x, T* out) {
+  pdl_enter();
   int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   for (int64_t k = blockIdx.x * 8ll + warp; k < K; k += gridDim.x * 8ll) {
     int64_t base = decode(D.kr, D.kshape, D.kst, k);
@@ -78,6 +79,7 @@ __global__ void __launch_bounds__(256) reduce_inner_warp(RedDesc D, int64_t K, i
 template <typename T>
 __global__ void __launch_bounds__(256) reduce_inner_block(RedDesc D, int64_t K, int64_t R,
                                                           int nsplit, const T* x, T* dst) {
+  pdl_enter();
   __shared__ T red[8];
   int64_t k = blockIdx.x / nsplit;
   int split = blockIdx.x % nsplit;
@@ -106,6 +108,7 @@ __global__ void __launch_bounds__(256) reduce_inner_block(RedDesc D, int64_t K, 
 template <typename T>
 __global__ void __launch_bounds__(256) reduce_outer(RedDesc D, int64_t K, int64_t R, int nsplit,
                                                     const T* x, T* dst) {
+  pdl_enter();
   int split = blockIdx.y;
   int64_t chunk = (R + nsplit - 1) / nsplit;
   int64_t r0 = split * chunk, r1 = min(R, r0 + chunk);
@@ -126,6 +129,7 @@ __global__ void __launch_bounds__(256) reduce_outer(RedDesc D, int64_t K, int64_
 
 template <typename T>
 __global__ void sum_partials(int64_t K, int nsplit, bool k_major, const T* ws, T* out) {
+  pdl_enter();
   for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < K;
        k += (int64_t)gridDim.x * blockDim.x) {
     Acc<T> acc;
@@ -136,6 +140,7 @@ __global__ void sum_partials(int64_t K, int nsplit, bool k_major, const T* ws, T
 
 template <typename T>
 __global__ void fill_zero(int64_t n, T* out) {
+  pdl_enter();
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
        i += (int64_t)gridDim.x * blockDim.x)
     out[i] = (T)0;
@@ -176,7 +181,7 @@ int reduce_run(const pfb_tensor* x, uint32_t mask, pfb_tensor* out, void* ws, in
   if (K == 0) return 0;
   T* o = (T*)out->data;
   if (R == 0) {
-    fill_zero<T><<<grid_for(K, 256), 256, 0, s>>>(K, o);
+    launch(fill_zero<T>, grid_for(K, 256), 256, 0, s, K, o);
     return launch_status();
   }
   int64_t kinner = 0, rinner = 0;  // smallest non-trivial stride on each side
@@ -188,7 +193,7 @@ int reduce_run(const pfb_tensor* x, uint32_t mask, pfb_tensor* out, void* ws, in
   bool inner = (K == 1) || (rinner != 0 && (kinner == 0 || rinner < kinner));
   if (inner) {
     if (R <= 2048 && K > 1) {
-      reduce_inner_warp<T><<<grid_for(K, 8, 64), 256, 0, s>>>(D, K, R, xp, o);
+      launch(reduce_inner_warp<T>, grid_for(K, 8, 64), 256, 0, s, D, K, R, xp, o);
       return launch_status();
     }
     int nsplit = 1;
@@ -196,9 +201,9 @@ int reduce_run(const pfb_tensor* x, uint32_t mask, pfb_tensor* out, void* ws, in
       nsplit = (int)std::min<int64_t>((4 * kNumSMs + K - 1) / K, R / 8192 + 1);
       if ((int64_t)nsplit * K * (int64_t)sizeof(T) > ws_bytes || ws == nullptr) nsplit = 1;
     }
-    reduce_inner_block<T><<<(unsigned)(K * nsplit), 256, 0, s>>>(D, K, R, nsplit, xp,
+    launch(reduce_inner_block<T>, (unsigned)(K * nsplit), 256, 0, s, D, K, R, nsplit, xp,
                                                                   nsplit == 1 ? o : (T*)ws);
-    if (nsplit > 1) sum_partials<T><<<grid_for(K, 256), 256, 0, s>>>(K, nsplit, true, (const T*)ws, o);
+    if (nsplit > 1) launch(sum_partials<T>, grid_for(K, 256), 256, 0, s, K, nsplit, true, (const T*)ws, o);
     return launch_status();
   }
   int gx = grid_for(K, 256, 8);
@@ -209,8 +214,8 @@ int reduce_run(const pfb_tensor* x, uint32_t mask, pfb_tensor* out, void* ws, in
     if ((int64_t)nsplit * K * (int64_t)sizeof(T) > ws_bytes || ws == nullptr) nsplit = 1;
   }
   dim3 grid(gx, nsplit);
-  reduce_outer<T><<<grid, 256, 0, s>>>(D, K, R, nsplit, xp, nsplit == 1 ? o : (T*)ws);
-  if (nsplit > 1) sum_partials<T><<<grid_for(K, 256), 256, 0, s>>>(K, nsplit, false, (const T*)ws, o);
+  launch(reduce_outer<T>, grid, 256, 0, s, D, K, R, nsplit, xp, nsplit == 1 ? o : (T*)ws);
+  if (nsplit > 1) launch(sum_partials<T>, grid_for(K, 256), 256, 0, s, K, nsplit, false, (const T*)ws, o);
   return launch_status();
 }
 
