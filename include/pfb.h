@@ -88,6 +88,10 @@ int pfb_select(const pfb_tensor* mask, const pfb_tensor* a, const pfb_tensor* b,
 int pfb_reduce_sum(const pfb_tensor* x, uint32_t axes_mask, pfb_tensor* out, void* ws,
                    int64_t ws_bytes, void* stream);
 
+/* sum over axes of x*y, y broadcast to x (fused square / scaled reductions) */
+int pfb_reduce_dot(const pfb_tensor* x, const pfb_tensor* y, uint32_t axes_mask, pfb_tensor* out,
+                   void* ws, int64_t ws_bytes, void* stream);
+
 /* strided copy: out (any strides) <- x (any strides, same shape).  Backs
  * transpose / concat / stack / tile_leading / slice_leading materialisation
  * (reference tensor.py:286-303, 383-416). */

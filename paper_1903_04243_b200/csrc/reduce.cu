@@ -19,9 +19,26 @@ namespace pfb {
 
 struct RedDesc {
   int kr, rr;
-  int64_t kshape[kMaxRank], kst[kMaxRank];
-  int64_t rshape[kMaxRank], rst[kMaxRank];
+  int64_t kshape[kMaxRank], kst[kMaxRank], kst_y[kMaxRank];
+  int64_t rshape[kMaxRank], rst[kMaxRank], rst_y[kMaxRank];
 };
+
+// offsets of one (kept or reduced) index for x and y at once
+__device__ __forceinline__ void decode2(int rank, const int64_t* shape, const int64_t* st,
+                                        const int64_t* sty, int64_t lin, int64_t* ox,
+                                        int64_t* oy) {
+  if (rank == 1) { *ox = lin * st[0]; *oy = lin * sty[0]; return; }
+  int64_t a = 0, b = 0;
+  for (int d = rank - 1; d >= 0; --d) {
+    int64_t q = lin / shape[d];
+    int64_t c = lin - q * shape[d];
+    a += c * st[d];
+    b += c * sty[d];
+    lin = q;
+  }
+  *ox = a;
+  *oy = b;
+}
 
 __device__ __forceinline__ int64_t decode(int rank, const int64_t* shape, const int64_t* st,
                                           int64_t lin) {
@@ -60,39 +77,52 @@ __device__ __forceinline__ T warp_sum(T v) {
   return v;
 }
 
+// x[i] (PROD: x[i] * y[i])
+template <typename T, bool PROD>
+__device__ __forceinline__ T elem(const RedDesc& D, const T* x, const T* y, int64_t kx,
+                                  int64_t ky, int64_t r) {
+  if (!PROD) return x[kx + decode(D.rr, D.rshape, D.rst, r)];
+  int64_t ox, oy;
+  decode2(D.rr, D.rshape, D.rst, D.rst_y, r, &ox, &oy);
+  return x[kx + ox] * y[ky + oy];
+}
+
 // one warp per output; R small
-template <typename T>
+template <typename T, bool PROD>
 __global__ void __launch_bounds__(256) reduce_inner_warp(RedDesc D, int64_t K, int64_t R,
-                                                         const T* x, T* out) {
+                                                         const T* x, const T* y, T* out) {
   pdl_enter();
   int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   for (int64_t k = blockIdx.x * 8ll + warp; k < K; k += gridDim.x * 8ll) {
-    int64_t base = decode(D.kr, D.kshape, D.kst, k);
+    int64_t base, basey;
+    decode2(D.kr, D.kshape, D.kst, D.kst_y, k, &base, &basey);
     Acc<T> acc;
-    for (int64_t r = lane; r < R; r += 32) acc.add(x[base + decode(D.rr, D.rshape, D.rst, r)]);
+    for (int64_t r = lane; r < R; r += 32) acc.add(elem<T, PROD>(D, x, y, base, basey, r));
     T v = warp_sum(acc.s);
     if (lane == 0) out[k] = v;
   }
 }
 
 // block per (output, split); partial -> out[k] (nsplit==1) or ws[k*nsplit+split]
-template <typename T>
+template <typename T, bool PROD>
 __global__ void __launch_bounds__(256) reduce_inner_block(RedDesc D, int64_t K, int64_t R,
-                                                          int nsplit, const T* x, T* dst) {
+                                                          int nsplit, const T* x, const T* y,
+                                                          T* dst) {
   pdl_enter();
   __shared__ T red[8];
   int64_t k = blockIdx.x / nsplit;
   int split = blockIdx.x % nsplit;
   int64_t chunk = (R + nsplit - 1) / nsplit;
   int64_t r0 = split * chunk, r1 = min(R, r0 + chunk);
-  int64_t base = decode(D.kr, D.kshape, D.kst, k);
+  int64_t base, basey;
+  decode2(D.kr, D.kshape, D.kst, D.kst_y, k, &base, &basey);
   Acc<T> acc;
-  if (D.rr == 1 && D.rst[0] == 1) {
+  if (!PROD && D.rr == 1 && D.rst[0] == 1) {
     const T* p = x + base;
     for (int64_t r = r0 + threadIdx.x; r < r1; r += blockDim.x) acc.add(__ldg(p + r));
   } else {
     for (int64_t r = r0 + threadIdx.x; r < r1; r += blockDim.x)
-      acc.add(x[base + decode(D.rr, D.rshape, D.rst, r)]);
+      acc.add(elem<T, PROD>(D, x, y, base, basey, r));
   }
   T v = warp_sum(acc.s);
   if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = v;
@@ -105,23 +135,30 @@ __global__ void __launch_bounds__(256) reduce_inner_block(RedDesc D, int64_t K, 
 }
 
 // thread per output, loop over an R chunk (blockIdx.y = split)
-template <typename T>
+template <typename T, bool PROD>
 __global__ void __launch_bounds__(256) reduce_outer(RedDesc D, int64_t K, int64_t R, int nsplit,
-                                                    const T* x, T* dst) {
+                                                    const T* x, const T* y, T* dst) {
   pdl_enter();
   int split = blockIdx.y;
   int64_t chunk = (R + nsplit - 1) / nsplit;
   int64_t r0 = split * chunk, r1 = min(R, r0 + chunk);
   for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < K;
        k += (int64_t)gridDim.x * blockDim.x) {
-    int64_t base = decode(D.kr, D.kshape, D.kst, k);
+    int64_t base, basey;
+    decode2(D.kr, D.kshape, D.kst, D.kst_y, k, &base, &basey);
     Acc<T> acc;
     if (D.rr == 1) {
       const T* p = x + base;
-      int64_t s = D.rst[0];
-      for (int64_t r = r0; r < r1; ++r) acc.add(__ldg(p + r * s));
+      const int64_t s = D.rst[0];
+      if (PROD) {
+        const T* q = y + basey;
+        const int64_t sy = D.rst_y[0];
+        for (int64_t r = r0; r < r1; ++r) acc.add(__ldg(p + r * s) * __ldg(q + r * sy));
+      } else {
+        for (int64_t r = r0; r < r1; ++r) acc.add(__ldg(p + r * s));
+      }
     } else {
-      for (int64_t r = r0; r < r1; ++r) acc.add(x[base + decode(D.rr, D.rshape, D.rst, r)]);
+      for (int64_t r = r0; r < r1; ++r) acc.add(elem<T, PROD>(D, x, y, base, basey, r));
     }
     dst[nsplit == 1 ? k : split * K + k] = acc.s;
   }
@@ -146,34 +183,39 @@ __global__ void fill_zero(int64_t n, T* out) {
     out[i] = (T)0;
 }
 
-static int collapse(int n, int64_t* shape, int64_t* st) {
+static int collapse(int n, int64_t* shape, int64_t* st, int64_t* sty) {
   int w = 0;
   for (int d = 0; d < n; ++d) {
     if (shape[d] == 1) continue;
-    if (w > 0 && st[w - 1] == st[d] * shape[d]) {
+    if (w > 0 && st[w - 1] == st[d] * shape[d] && sty[w - 1] == sty[d] * shape[d]) {
       shape[w - 1] *= shape[d];
       st[w - 1] = st[d];
+      sty[w - 1] = sty[d];
       continue;
     }
     shape[w] = shape[d];
     st[w] = st[d];
+    sty[w] = sty[d];
     ++w;
   }
-  if (w == 0) { shape[0] = 1; st[0] = 0; w = 1; }
+  if (w == 0) { shape[0] = 1; st[0] = 0; sty[0] = 0; w = 1; }
   return w;
 }
 
-template <typename T>
-int reduce_run(const pfb_tensor* x, uint32_t mask, pfb_tensor* out, void* ws, int64_t ws_bytes,
-               cudaStream_t s) {
+template <typename T, bool PROD>
+int reduce_run(const pfb_tensor* x, const int64_t* ystride, const T* yp, uint32_t mask,
+               pfb_tensor* out, void* ws, int64_t ws_bytes, cudaStream_t s) {
   RedDesc D;
   int nk = 0, nr = 0;
   int64_t K = 1, R = 1;
   for (int d = 0; d < x->rank; ++d) {
+    const int64_t sy = PROD ? ystride[d] : 0;
     if (mask & (1u << d)) {
-      D.rshape[nr] = x->shape[d]; D.rst[nr] = x->stride[d]; ++nr; R *= x->shape[d];
+      D.rshape[nr] = x->shape[d]; D.rst[nr] = x->stride[d]; D.rst_y[nr] = sy; ++nr;
+      R *= x->shape[d];
     } else {
-      D.kshape[nk] = x->shape[d]; D.kst[nk] = x->stride[d]; ++nk; K *= x->shape[d];
+      D.kshape[nk] = x->shape[d]; D.kst[nk] = x->stride[d]; D.kst_y[nk] = sy; ++nk;
+      K *= x->shape[d];
     }
   }
   if (numel(out) != K) return PFB_E_SHAPE;
@@ -187,13 +229,13 @@ int reduce_run(const pfb_tensor* x, uint32_t mask, pfb_tensor* out, void* ws, in
   int64_t kinner = 0, rinner = 0;  // smallest non-trivial stride on each side
   for (int d = 0; d < nk; ++d) if (D.kshape[d] > 1 && (kinner == 0 || llabs(D.kst[d]) < kinner)) kinner = llabs(D.kst[d]);
   for (int d = 0; d < nr; ++d) if (D.rshape[d] > 1 && (rinner == 0 || llabs(D.rst[d]) < rinner)) rinner = llabs(D.rst[d]);
-  D.kr = collapse(nk, D.kshape, D.kst);
-  D.rr = collapse(nr, D.rshape, D.rst);
+  D.kr = collapse(nk, D.kshape, D.kst, D.kst_y);
+  D.rr = collapse(nr, D.rshape, D.rst, D.rst_y);
   const T* xp = (const T*)x->data;
   bool inner = (K == 1) || (rinner != 0 && (kinner == 0 || rinner < kinner));
   if (inner) {
     if (R <= 2048 && K > 1) {
-      launch(reduce_inner_warp<T>, grid_for(K, 8, 64), 256, 0, s, D, K, R, xp, o);
+      launch(reduce_inner_warp<T, PROD>, grid_for(K, 8, 64), 256, 0, s, D, K, R, xp, yp, o);
       return launch_status();
     }
     int nsplit = 1;
@@ -201,7 +243,7 @@ int reduce_run(const pfb_tensor* x, uint32_t mask, pfb_tensor* out, void* ws, in
       nsplit = (int)std::min<int64_t>((4 * kNumSMs + K - 1) / K, R / 8192 + 1);
       if ((int64_t)nsplit * K * (int64_t)sizeof(T) > ws_bytes || ws == nullptr) nsplit = 1;
     }
-    launch(reduce_inner_block<T>, (unsigned)(K * nsplit), 256, 0, s, D, K, R, nsplit, xp,
+    launch(reduce_inner_block<T, PROD>, (unsigned)(K * nsplit), 256, 0, s, D, K, R, nsplit, xp, yp,
                                                                   nsplit == 1 ? o : (T*)ws);
     if (nsplit > 1) launch(sum_partials<T>, grid_for(K, 256), 256, 0, s, K, nsplit, true, (const T*)ws, o);
     return launch_status();
@@ -214,7 +256,7 @@ int reduce_run(const pfb_tensor* x, uint32_t mask, pfb_tensor* out, void* ws, in
     if ((int64_t)nsplit * K * (int64_t)sizeof(T) > ws_bytes || ws == nullptr) nsplit = 1;
   }
   dim3 grid(gx, nsplit);
-  launch(reduce_outer<T>, grid, 256, 0, s, D, K, R, nsplit, xp, nsplit == 1 ? o : (T*)ws);
+  launch(reduce_outer<T, PROD>, grid, 256, 0, s, D, K, R, nsplit, xp, yp, nsplit == 1 ? o : (T*)ws);
   if (nsplit > 1) launch(sum_partials<T>, grid_for(K, 256), 256, 0, s, K, nsplit, false, (const T*)ws, o);
   return launch_status();
 }
@@ -226,7 +268,21 @@ extern "C" int pfb_reduce_sum(const pfb_tensor* x, uint32_t axes_mask, pfb_tenso
   using namespace pfb;
   if (x->dtype != out->dtype) return PFB_E_DTYPE;
   cudaStream_t s = as_stream(stream);
-  if (x->dtype == PFB_F32) return reduce_run<float>(x, axes_mask, out, ws, ws_bytes, s);
-  if (x->dtype == PFB_I64) return reduce_run<int64_t>(x, axes_mask, out, ws, ws_bytes, s);
-  return PFB_E_DTYPE;  // bool sums are rejected by graph inference too (np.sum(bool) -> int)
+  if (x->dtype == PFB_F32)
+    return reduce_run<float, false>(x, nullptr, nullptr, axes_mask, out, ws, ws_bytes, s);
+  if (x->dtype == PFB_I64)
+    return reduce_run<int64_t, false>(x, nullptr, nullptr, axes_mask, out, ws, ws_bytes, s);
+  return PFB_E_DTYPE;  // bools are cast to i64 by the executor first
+}
+
+// sum over axes of x * y (y broadcast to x's shape): fused square / scaled
+// reductions (passes.py F4) -- the product is never written to HBM.
+extern "C" int pfb_reduce_dot(const pfb_tensor* x, const pfb_tensor* y, uint32_t axes_mask,
+                              pfb_tensor* out, void* ws, int64_t ws_bytes, void* stream) {
+  using namespace pfb;
+  if (x->dtype != PFB_F32 || y->dtype != PFB_F32 || out->dtype != PFB_F32) return PFB_E_DTYPE;
+  int64_t sy[kMaxRank];
+  if (!broadcast_strides(y, x->rank, x->shape, sy)) return PFB_E_SHAPE;
+  return reduce_run<float, true>(x, sy, (const float*)y->data, axes_mask, out, ws, ws_bytes,
+                                 as_stream(stream));
 }

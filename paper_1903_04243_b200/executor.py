@@ -196,6 +196,19 @@ class _Plan:
         for n in self.order:
             for key in n.inputs:
                 self.uses[key] = self.uses.get(key, 0) + 1
+        # constant-derived nodes (all inputs, transitively, are constants): the
+        # executor evaluates them once and reuses the device values
+        self.const_nodes = set()
+        for n in self.order:
+            if n.kind == "constant":
+                self.const_nodes.add(n.id)
+            elif (n.kind not in _NO_HOIST and n.block is None and n.inputs
+                  and all(src in self.const_nodes for src, _ in n.inputs)):
+                self.const_nodes.add(n.id)
+
+
+_NO_HOIST = STATEFUL_KINDS | {"placeholder", "capture", "carried", "loop_var", "where_true",
+                              "complement"}
 
 
 def _block_has_state(block):
@@ -227,6 +240,7 @@ class Executor:
         self._capture_ok = {}
         self._warm = set()
         self._sub_captures = {}
+        self._hoisted = {}
         self.capture_failures = []
         self._sub_warm = set()
         self._used_caps = {}
@@ -598,12 +612,17 @@ class Executor:
             remaining[r] = remaining.get(r, 0) + 1
         env = {}
         for node in plan.order:
-            try:
-                outs = self._eval_node(g, node, env, binder, feeds)
-            except E.PforVecError as e:
-                if isinstance(e, (E.ExecError, E.BudgetExceeded)):
-                    raise
-                raise E.ExecError(node.id, e) from e
+            hoist = node.id in plan.const_nodes and node.kind != "constant"
+            outs = self._hoisted.get((id(g), node.id)) if hoist else None
+            if outs is None:
+                try:
+                    outs = self._eval_node(g, node, env, binder, feeds)
+                except E.PforVecError as e:
+                    if isinstance(e, (E.ExecError, E.BudgetExceeded)):
+                        raise
+                    raise E.ExecError(node.id, e) from e
+                if hoist and not torch.cuda.is_current_stream_capturing():
+                    self._hoisted[(id(g), node.id)] = outs
             for p, v in enumerate(outs):
                 env[(node.id, p)] = v
             for key in node.inputs:
@@ -1103,6 +1122,20 @@ def _h_fused(ex, node, ins):
     return [out]
 
 
+def _h_reduce_dot(ex, node, ins):
+    x, y = (ex._dev(v) for v in ins)
+    axes = normalize_axes(node.attrs["axes"], x.rank)
+    shape = tuple(d for i, d in enumerate(x.shape) if i not in axes)
+    mask = 0
+    for ax in axes:
+        mask |= 1 << ax
+    out = ex._empty(shape, x.dtype)
+    wp, wn = ex._ws_get(min(8 * max(1, _numel(shape)) * 1024, 1 << 26))
+    ex._call(ex._lib.pfb_reduce_dot, x.desc(), y.desc(), mask, out.desc(), wp, wn, ex._stream,
+             what="reduce_dot", work=(_abytes(x, y, out), 0))
+    return [out]
+
+
 def _h_select(ex, node, ins):
     m, a, b = (ex._dev(v) for v in ins)
     if m.dtype != DType.BOOL:
@@ -1167,6 +1200,7 @@ _HANDLERS.update({
     "range_vec": _h_range_vec, "read_variable": _h_read_variable, "assign": _h_assign,
     "assign_add": _h_assign, "random_uniform": _h_random_uniform, "fused_ew": _h_fused,
     "select": _h_select,
+    "reduce_dot": _h_reduce_dot,
 })
 
 

@@ -13,8 +13,10 @@ F2   (a_1 (x) b_1) + ... + (a_T (x) b_T)        ->  [a_1..a_T] [b_1..b_T]^T
                                                     (one batched K=T GEMM; B laid
                                                     out K-major for tcgen05)
 F3   chains of elementwise ops (binary / unary / f32<->bool cast) whose interior
-     values have no other consumer  ->  one `fused_ew` launch running a small
-     register program (the same fp32 ops in the same order: bit-identical).
+     values have no other live consumer  ->  one `fused_ew` launch running a
+     small register program (the same fp32 ops in the same order).
+F4   reduce_sum(square(x)) / reduce_sum(x * y)  ->  reduce_dot(x, y): the
+     product is formed in registers inside the reduction.
 
 Each rewrite adds nodes to a private copy of the graph and redirects the
 consumers; the now-unread outer products are removed by the executor's
@@ -175,19 +177,85 @@ def _f2(rw, node):
     return 1
 
 
+def live_set(g, keep):
+    """Nodes the requested outputs depend on (plus stateful nodes and control
+    deps) -- what the executor will actually run."""
+    from .graph import STATEFUL_KINDS
+    live = set()
+    todo = [k[0] for k in keep] + [n.id for n in g.nodes.values()
+                                   if n.kind in STATEFUL_KINDS or n.block is not None]
+    while todo:
+        nid = todo.pop()
+        if nid in live:
+            continue
+        live.add(nid)
+        node = g.nodes[nid]
+        todo.extend(src for src, _ in node.inputs)
+        todo.extend(node.control_deps)
+    return live
+
+
+def fuse_reductions(g, keep=()):
+    """F4: reduce_sum(square(x)) and reduce_sum(mul(x, y)) (y broadcast to x)
+    -> reduce_dot(x, y): the product is never written to HBM."""
+    keep = set(keep)
+    live = live_set(g, keep)
+    users = {}
+    for n in g.nodes.values():
+        if n.id in live:
+            for src in n.inputs:
+                users.setdefault(src, []).append(n)
+    moved = {}
+    count = 0
+    from .tensor import DType
+    for node in list(g.topo_order()):
+        if node.kind != "reduce_sum" or node.id not in live:
+            continue
+        src = node.inputs[0]
+        inner = g.nodes[src[0]]
+        if len(users.get(src, [])) != 1 or src in keep or inner.out_dtypes[0] != DType.F64:
+            continue
+        if inner.kind == "square":
+            x = y = inner.inputs[0]
+        elif inner.kind == "mul":
+            a, b = inner.inputs
+            out_sh = inner.out_shapes[0]
+            if g.ref_shape(a) == out_sh:
+                x, y = a, b
+            elif g.ref_shape(b) == out_sh:
+                x, y = b, a
+            else:
+                continue
+        else:
+            continue
+        new = g.add_node("reduce_dot", [x, y], {"axes": tuple(node.attrs["axes"])})
+        for u in users.get((node.id, 0), []):
+            u.inputs = [(new.id, 0) if s_ == (node.id, 0) else s_ for s_ in u.inputs]
+        if (node.id, 0) in keep:
+            moved[(node.id, 0)] = (new.id, 0)
+            keep.discard((node.id, 0))
+            keep.add((new.id, 0))
+        count += 1
+    g._topo_cache = None
+    return count, moved
+
+
 def optimize(g, keep_keys, elementwise=True):
     """Copy `g`, apply the rewrites, return (graph, key map old->new)."""
     dst, mapping = copy_with_map(g)
     keep = [mapping[k] for k in keep_keys]
     _, moved = fuse_outer_products(dst, keep)
-    keep2 = [moved.get(k, k) for k in keep]
-    moved2 = {}
+    keep = [moved.get(k, k) for k in keep]
+    _, moved4 = fuse_reductions(dst, keep)
+    keep = [moved4.get(k, k) for k in keep]
+    moved3 = {}
     if elementwise:
-        _, moved2 = fuse_elementwise(dst, keep2)
+        _, moved3 = fuse_elementwise(dst, keep)
     final = {}
     for k, v in mapping.items():
         v = moved.get(v, v)
-        final[k] = moved2.get(v, v)
+        v = moved4.get(v, v)
+        final[k] = moved3.get(v, v)
     return dst, final
 
 
@@ -286,16 +354,19 @@ def fuse_elementwise(g, keep=()):
     number of groups fused and the moved requested outputs."""
     keep = set(keep)
     topo = g.topo_order()
+    live = live_set(g, keep)
     pos = {n.id: i for i, n in enumerate(topo)}
     users = {}
     for n in topo:
+        if n.id not in live:
+            continue
         for src in n.inputs:
             users.setdefault(src, set()).add(n.id)
     assigned = set()
     moved = {}
     fused = 0
     for root in reversed(topo):
-        if root.id in assigned or not _ew_eligible(g, root):
+        if root.id in assigned or root.id not in live or not _ew_eligible(g, root):
             continue
         shape = root.out_shapes[0]
         group = {root.id}
@@ -331,10 +402,15 @@ def fuse_elementwise(g, keep=()):
             continue
         new = g.add_node("fused_ew", externals,
                          {"program": prog, "out_dtype": root.out_dtypes[0]})
+        live.add(new.id)
+        for src in externals:  # the fused node now reads these (later groups redirect it)
+            users.setdefault(src, set()).add(new.id)
+            users[src] -= group
         key = (root.id, 0)
         for u in users.get(key, ()):
             un = g.nodes[u]
             un.inputs = [(new.id, 0) if s == key else s for s in un.inputs]
+        users[(new.id, 0)] = set(users.get(key, ()))
         if key in keep:
             moved[key] = (new.id, 0)
         assigned |= group
