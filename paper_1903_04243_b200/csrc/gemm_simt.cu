@@ -42,7 +42,9 @@ __device__ __forceinline__ void store_row4(const GemmArgs& g, int64_t b, int64_t
   }
 }
 
-// partials: nullptr -> epilogue straight to C; else ws[split][b][M][N]
+// partials: nullptr -> epilogue straight to C; else ws[split][b][M][N].
+// Register-staged double buffering: the next k-tile's global loads are issued
+// before the current tile's FMAs, so the loop is not load-latency bound.
 __global__ void __launch_bounds__(256) gemm_simt_kernel(GemmArgs g, int splits, int64_t kchunk,
                                                         float* partials) {
   pdl_enter();
@@ -59,24 +61,32 @@ __global__ void __launch_bounds__(256) gemm_simt_kernel(GemmArgs g, int splits, 
   float acc[4][4] = {};
   const bool a_kfast = g.sak == 1 || g.sam != 1;
   const bool b_nfast = g.sbn == 1 || g.sbk != 1;
+  int am[4], ak[4], bk[4], bn[4];
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    const int e = tid + j * 256;
+    if (a_kfast) { am[j] = e / BK; ak[j] = e % BK; } else { ak[j] = e / BM; am[j] = e % BM; }
+    if (b_nfast) { bk[j] = e / BN; bn[j] = e % BN; } else { bn[j] = e / BK; bk[j] = e % BK; }
+  }
+  float ra[4], rb[4];
+  auto load = [&](int64_t k0) {
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const int64_t gm = m0 + am[j], gk = k0 + ak[j];
+      ra[j] = (gm < g.M && gk < kend) ? __ldg(A + gm * g.sam + gk * g.sak) : 0.f;
+      const int64_t gk2 = k0 + bk[j], gn = n0 + bn[j];
+      rb[j] = (gk2 < kend && gn < g.N) ? __ldg(B + gk2 * g.sbk + gn * g.sbn) : 0.f;
+    }
+  };
+  if (kbeg < kend) load(kbeg);
   for (int64_t k0 = kbeg; k0 < kend; k0 += BK) {
 #pragma unroll
     for (int j = 0; j < 4; ++j) {
-      int e = tid + j * 256;
-      int mm, kk;
-      if (a_kfast) { mm = e / BK; kk = e % BK; } else { kk = e / BM; mm = e % BM; }
-      int64_t gm = m0 + mm, gk = k0 + kk;
-      As[kk][mm] = (gm < g.M && gk < kend) ? __ldg(A + gm * g.sam + gk * g.sak) : 0.f;
-    }
-#pragma unroll
-    for (int j = 0; j < 4; ++j) {
-      int e = tid + j * 256;
-      int kk, nn;
-      if (b_nfast) { kk = e / BN; nn = e % BN; } else { nn = e / BK; kk = e % BK; }
-      int64_t gk = k0 + kk, gn = n0 + nn;
-      Bs[kk][nn] = (gk < kend && gn < g.N) ? __ldg(B + gk * g.sbk + gn * g.sbn) : 0.f;
+      As[ak[j]][am[j]] = ra[j];
+      Bs[bk[j]][bn[j]] = rb[j];
     }
     __syncthreads();
+    if (k0 + BK < kend) load(k0 + BK);
 #pragma unroll
     for (int kk = 0; kk < BK; ++kk) {
       float4 a4 = *reinterpret_cast<const float4*>(&As[kk][tm]);
@@ -187,9 +197,10 @@ static int smallk_launch(const GemmArgs& g, cudaStream_t s) {
 
 static int simt_splits(const GemmArgs& g) {
   const int64_t tiles = ((g.N + BN - 1) / BN) * ((g.M + BM - 1) / BM) * g.batch;
-  if (tiles >= 2 * kNumSMs || g.K < 256) return 1;
-  int64_t s = (2 * kNumSMs + tiles - 1) / tiles;
-  s = std::min<int64_t>(s, g.K / 128);
+  if (tiles >= kNumSMs || g.K < 64) return 1;
+  // aim for >= 148 CTAs with >= 2 k-tiles (32) each
+  int64_t s = (kNumSMs + tiles - 1) / tiles;
+  s = std::min<int64_t>(s, g.K / 32);
   s = std::min<int64_t>(s, 64);
   return (int)std::max<int64_t>(s, 1);
 }

@@ -97,7 +97,19 @@ __global__ void __launch_bounds__(256) reduce_inner_warp(RedDesc D, int64_t K, i
     int64_t base, basey;
     decode2(D.kr, D.kshape, D.kst, D.kst_y, k, &base, &basey);
     Acc<T> acc;
-    for (int64_t r = lane; r < R; r += 32) acc.add(elem<T, PROD>(D, x, y, base, basey, r));
+    if (D.rr == 1) {  // single collapsed reduced dim: no index decode per element
+      const T* p = x + base;
+      const int64_t s = D.rst[0];
+      if (PROD) {
+        const T* q = y + basey;
+        const int64_t sy = D.rst_y[0];
+        for (int64_t r = lane; r < R; r += 32) acc.add(__ldg(p + r * s) * __ldg(q + r * sy));
+      } else {
+        for (int64_t r = lane; r < R; r += 32) acc.add(__ldg(p + r * s));
+      }
+    } else {
+      for (int64_t r = lane; r < R; r += 32) acc.add(elem<T, PROD>(D, x, y, base, basey, r));
+    }
     T v = warp_sum(acc.s);
     if (lane == 0) out[k] = v;
   }
