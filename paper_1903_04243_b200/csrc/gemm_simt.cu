@@ -46,7 +46,7 @@ __device__ __forceinline__ void store_row4(const GemmArgs& g, int64_t b, int64_t
 // Register-staged double buffering: the next k-tile's global loads are issued
 // before the current tile's FMAs, so the loop is not load-latency bound.
 __global__ void __launch_bounds__(256) gemm_simt_kernel(GemmArgs g, int splits, int64_t kchunk,
-                                                        float* partials, int* tile_count) {
+                                                        float* partials) {
   pdl_enter();
   __shared__ float As[BK][BM + 4];
   __shared__ float Bs[BK][BN + 4];
@@ -116,35 +116,6 @@ __global__ void __launch_bounds__(256) gemm_simt_kernel(GemmArgs g, int splits, 
 #pragma unroll
       for (int j = 0; j < 4; ++j)
         if (n0 + tn + j < g.N) P[gm * g.N + n0 + tn + j] = acc[i][j];
-    }
-    if (tile_count == nullptr) return;
-    // the last split CTA of this tile sums all partials (fixed split order:
-    // deterministic) and applies the epilogue; counters reset themselves
-    __shared__ int last;
-    __threadfence();
-    __syncthreads();
-    if (tid == 0) {
-      int* ctr = tile_count + (bz * gridDim.y + blockIdx.y) * gridDim.x + blockIdx.x;
-      last = atomicAdd(ctr, 1) == splits - 1;
-      if (last) *ctr = 0;
-    }
-    __syncthreads();
-    if (!last) return;
-    __threadfence();
-    const int64_t plane = g.batch * g.M * g.N;
-    const float* P0 = partials + bz * g.M * g.N;
-#pragma unroll
-    for (int i = 0; i < 4; ++i) {
-      const int64_t gm = m0 + tm + i;
-      if (gm >= g.M) continue;
-      float v[4] = {0.f, 0.f, 0.f, 0.f};
-      for (int sp = 0; sp < splits; ++sp) {
-#pragma unroll
-        for (int j = 0; j < 4; ++j)
-          if (n0 + tn + j < g.N) v[j] += __ldcg(P0 + sp * plane + gm * g.N + n0 + tn + j);
-      }
-      const float alpha = g.alpha_rows ? g.alpha_rows[bz * g.M + gm] : 1.f;
-      store_row4(g, bz, gm, n0 + tn, v, alpha);
     }
   }
 }
@@ -239,28 +210,6 @@ int64_t gemm_simt_workspace(const GemmArgs& g) {
   return s > 1 ? (int64_t)s * g.batch * g.M * g.N * 4 : 0;
 }
 
-// Persistent per-tile arrival counters for the fused split-K reduction
-// (zeroed once; each use leaves them at zero).  Allocated on first use
-// outside stream capture; during capture without them the separate
-// reduction kernel runs instead.
-static int* tile_counters(int64_t need, cudaStream_t s) {
-  static int* buf = nullptr;
-  static int64_t cap = 0;
-  if (need <= cap) return buf;
-  cudaStreamCaptureStatus st = cudaStreamCaptureStatusNone;
-  cudaStreamIsCapturing(s, &st);
-  if (st != cudaStreamCaptureStatusNone) return nullptr;
-  int64_t want = std::max<int64_t>(need, 1 << 16);
-  int* nb = nullptr;
-  if (cudaMalloc(&nb, want * sizeof(int)) != cudaSuccess) { cudaGetLastError(); return nullptr; }
-  cudaMemset(nb, 0, want * sizeof(int));
-  cudaStreamSynchronize(s);  // old counters may still be in use by queued work
-  if (buf) cudaFree(buf);
-  buf = nb;
-  cap = want;
-  return buf;
-}
-
 int gemm_simt(const GemmArgs& g, void* ws, int64_t ws_bytes, cudaStream_t s) {
   if (g.batch == 0 || g.M == 0 || g.N == 0) return 0;
   if (g.K <= 16) return smallk_launch(g, s);
@@ -270,10 +219,8 @@ int gemm_simt(const GemmArgs& g, void* ws, int64_t ws_bytes, cudaStream_t s) {
   dim3 grid((unsigned)((g.N + BN - 1) / BN), (unsigned)((g.M + BM - 1) / BM),
             (unsigned)(g.batch * splits));
   if (grid.y > 65535 || grid.z > 65535) return PFB_E_UNSUPPORTED;
-  int* ctr = splits > 1 ? tile_counters((int64_t)grid.x * grid.y * g.batch, s) : nullptr;
-  launch(gemm_simt_kernel, grid, 256, 0, s, g, splits, kchunk, splits > 1 ? (float*)ws : nullptr,
-         ctr);
-  if (splits > 1 && ctr == nullptr)
+  launch(gemm_simt_kernel, grid, 256, 0, s, g, splits, kchunk, splits > 1 ? (float*)ws : nullptr);
+  if (splits > 1)
     launch(splitk_reduce, grid_for(g.batch * g.M * g.N, 256), 256, 0, s, g, splits, (const float*)ws);
   return launch_status();
 }
