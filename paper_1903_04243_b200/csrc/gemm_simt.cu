@@ -120,16 +120,19 @@ __global__ void __launch_bounds__(256) gemm_simt_kernel(GemmArgs g, int splits, 
   }
 }
 
-__global__ void splitk_reduce(GemmArgs g, int splits, const float* partials) {
+// sum split partials in split order (deterministic); 32-bit indexing, the
+// split loop unrolled so its loads are in flight together
+__global__ void __launch_bounds__(256) splitk_reduce(GemmArgs g, int splits, const float* partials) {
   pdl_enter();
-  const int64_t per = g.M * g.N, total = g.batch * per;
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
-       i += (int64_t)gridDim.x * blockDim.x) {
+  const uint32_t N = (uint32_t)g.N, per = (uint32_t)(g.M * g.N);
+  const uint32_t total = (uint32_t)(g.batch * g.M * g.N);
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < total; i += gridDim.x * blockDim.x) {
     float s = 0.f;
-    for (int k = 0; k < splits; ++k) s += partials[(int64_t)k * total + i];
-    const int64_t b = i / per, r = i - b * per;
-    const int64_t m = r / g.N, n = r - m * g.N;
-    if (g.alpha_rows) s *= g.alpha_rows[b * g.M + m];
+#pragma unroll 8
+    for (int k = 0; k < splits; ++k) s += __ldg(partials + (size_t)k * total + i);
+    const uint32_t b = i / per, r = i - b * per;
+    const uint32_t m = r / N, n = r - m * N;
+    if (g.alpha_rows) s *= g.alpha_rows[(size_t)b * g.M + m];
     float* p = g.C + b * g.scb + m * g.scm + n * g.scn;
     *p = g.accumulate ? *p + s : s;
   }
@@ -168,8 +171,10 @@ __global__ void __launch_bounds__(256) gemm_smallk_kernel(GemmArgs g) {
         if (g.accumulate) {
           const float4 c = *dst;
           o.x += c.x; o.y += c.y; o.z += c.z; o.w += c.w;
+          *dst = o;
+        } else {
+          __stcs(dst, o);  // write-once output (jacobian rows): streaming store
         }
-        *dst = o;
       } else {
         for (int k = 0; k < g.K; ++k) {
           const float* bk = bb + k * g.sbk + n * g.sbn;
@@ -196,6 +201,7 @@ static int smallk_launch(const GemmArgs& g, cudaStream_t s) {
 }
 
 static int simt_splits(const GemmArgs& g) {
+  if ((int64_t)g.batch * g.M * g.N >= 0x7fffffff) return 1;  // 32-bit reduction indexing
   const int64_t tiles = ((g.N + BN - 1) / BN) * ((g.M + BM - 1) / BM) * g.batch;
   if (tiles >= kNumSMs || g.K < 64) return 1;
   // aim for >= 148 CTAs with >= 2 k-tiles (32) each

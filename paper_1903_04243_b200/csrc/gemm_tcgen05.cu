@@ -188,6 +188,9 @@ struct Params {
   int64_t scb, scm, scn;
   const float* alpha_rows;
   int accumulate;
+  int ksplit;            // >1: work unit = (tile, k-range); partial tiles -> `partials`
+  int kb_per_split;      // k-blocks per split (multiple of CHUNK_KB)
+  float* partials;       // [ksplit][batch][M][N] when ksplit > 1
 };
 
 __global__ void __launch_bounds__(NUM_THREADS, 1)
@@ -207,9 +210,8 @@ gemm_kernel(const __grid_constant__ CUtensorMap map_ah, const __grid_constant__ 
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int nk = (p.K + BK - 1) / BK;
-  const int nchunks = (nk + CHUNK_KB - 1) / CHUNK_KB;
   const int tiles_per_batch = p.ntm * p.ntn;
-  const int ntiles = tiles_per_batch * p.batch;
+  const int ntiles = tiles_per_batch * p.batch * p.ksplit;  // work units
 
   auto tile = [&](int s, int which) { return smem + s * STAGE_BYTES + which * TILE_BYTES; };
   // which: 0 = A_hi, 1 = A_lo, 2 = B_hi, 3 = B_lo
@@ -243,11 +245,13 @@ gemm_kernel(const __grid_constant__ CUtensorMap map_ah, const __grid_constant__ 
       asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&map_bh)) : "memory");
       asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&map_bl)) : "memory");
       int g = 0;
-      for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {
+      for (int u = blockIdx.x; u < ntiles; u += gridDim.x) {
+        const int t = u / p.ksplit, ks = u % p.ksplit;
         const int bz = t / tiles_per_batch, r = t % tiles_per_batch;
         const int m0 = (r / p.ntn) * BM, n0 = (r % p.ntn) * BN;
         const int za = p.a_bcast ? 0 : bz, zb = p.b_bcast ? 0 : bz;
-        for (int kb = 0; kb < nk; ++kb, ++g) {
+        const int kb0 = ks * p.kb_per_split, kb1 = min(nk, kb0 + p.kb_per_split);
+        for (int kb = kb0; kb < kb1; ++kb, ++g) {
           const int s = g % STAGES;
           if (g >= STAGES) mbar_wait(&empty[s], ((g / STAGES) - 1) & 1);
           mbar_expect_tx(&full[s], 4 * TILE_BYTES);
@@ -261,14 +265,18 @@ gemm_kernel(const __grid_constant__ CUtensorMap map_ah, const __grid_constant__ 
   } else if (warp == 1) {
     if (lane == 0) {
       int g = 0, gc = 0;
-      for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {
-        for (int c = 0; c < nchunks; ++c, ++gc) {
+      for (int u = blockIdx.x; u < ntiles; u += gridDim.x) {
+        const int ks = u % p.ksplit;
+        const int kb0 = ks * p.kb_per_split, kb1 = min(nk, kb0 + p.kb_per_split);
+        const int uchunks = (kb1 - kb0 + CHUNK_KB - 1) / CHUNK_KB;
+        for (int c = 0; c < uchunks; ++c, ++gc) {
           const int buf = gc & 1;
           if (gc >= 2) mbar_wait(&acc_empty[buf], ((gc >> 1) - 1) & 1);
           asm volatile("tcgen05.fence::after_thread_sync;");
           const uint32_t tmem_d = tmem_base + (uint32_t)(buf * BN);
-          const int kb_end = min(nk, (c + 1) * CHUNK_KB);
-          for (int kb = c * CHUNK_KB; kb < kb_end; ++kb, ++g) {
+          const int kb_beg = kb0 + c * CHUNK_KB;
+          const int kb_end = min(kb1, kb_beg + CHUNK_KB);
+          for (int kb = kb_beg; kb < kb_end; ++kb, ++g) {
             const int s = g % STAGES;
             mbar_wait(&full[s], (g / STAGES) & 1);
             asm volatile("tcgen05.fence::after_thread_sync;");
@@ -279,7 +287,7 @@ gemm_kernel(const __grid_constant__ CUtensorMap map_ah, const __grid_constant__ 
 #pragma unroll
             for (int k = 0; k < BK / UMMA_K; ++k) {
               const uint64_t adv = (uint64_t)((k * UMMA_K * 4) >> 4);  // +32 B along K
-              const uint32_t acc = (kb > c * CHUNK_KB || k > 0) ? 1u : 0u;
+              const uint32_t acc = (kb > kb_beg || k > 0) ? 1u : 0u;
               mma_tf32(tmem_d, a_hi + adv, b_hi + adv, acc);
               mma_tf32(tmem_d, a_hi + adv, b_lo + adv, 1u);
               mma_tf32(tmem_d, a_lo + adv, b_hi + adv, 1u);
@@ -299,13 +307,16 @@ gemm_kernel(const __grid_constant__ CUtensorMap map_ah, const __grid_constant__ 
     float* stage = reinterpret_cast<float*>(smem + STAGES * STAGE_BYTES + 256) +
                    (warp - 2) * EPI_STAGE_FLOATS;
     int gc = 0;
-    for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {
+    for (int u = blockIdx.x; u < ntiles; u += gridDim.x) {
+      const int t = u / p.ksplit, ks = u % p.ksplit;
       const int bz = t / tiles_per_batch, r = t % tiles_per_batch;
       const int m0 = (r / p.ntn) * BM, n0 = (r % p.ntn) * BN;
+      const int kb0 = ks * p.kb_per_split, kb1 = min(nk, kb0 + p.kb_per_split);
+      const int uchunks = (kb1 - kb0 + CHUNK_KB - 1) / CHUNK_KB;
       float acc[EPI_COLS];
 #pragma unroll
       for (int j = 0; j < EPI_COLS; ++j) acc[j] = 0.f;
-      for (int c = 0; c < nchunks; ++c, ++gc) {
+      for (int c = 0; c < uchunks; ++c, ++gc) {
         const int buf = gc & 1;
         mbar_wait(&acc_full[buf], (gc >> 1) & 1);
         asm volatile("tcgen05.fence::after_thread_sync;");
@@ -324,7 +335,10 @@ gemm_kernel(const __grid_constant__ CUtensorMap map_ah, const __grid_constant__ 
       // 32x32 blocks through smem: each lane writes its row as float4s, then
       // every store instruction covers 4 rows x 128 contiguous bytes
       const int row0 = m0 + quarter * 32;
-      float* cbase = p.C + bz * p.scb;
+      const bool partial = p.ksplit > 1;  // dense partial tile, epilogue in the reduction
+      float* cbase = partial ? p.partials + ((int64_t)ks * p.batch + bz) * p.M * p.N
+                             : p.C + bz * p.scb;
+      const int64_t ldm = partial ? p.N : p.scm, ldn = partial ? 1 : p.scn;
       const int sub_r = lane >> 3, sub_c = (lane & 7) * 4;
 #pragma unroll
       for (int cc = 0; cc < EPI_COLS; cc += 32) {
@@ -339,15 +353,15 @@ gemm_kernel(const __grid_constant__ CUtensorMap map_ah, const __grid_constant__ 
         for (int i = 0; i < 32; i += 4) {
           const int row = row0 + i + sub_r;
           if (row < p.M) {
-            const float alpha =
-                p.alpha_rows ? __ldg(p.alpha_rows + (int64_t)bz * p.M + row) : 1.f;
+            const float alpha = (!partial && p.alpha_rows)
+                                    ? __ldg(p.alpha_rows + (int64_t)bz * p.M + row) : 1.f;
             const int srow = i + sub_r;
             float4 v = *reinterpret_cast<const float4*>(
                 stage + srow * 32 + 4 * ((sub_c >> 2) ^ (srow & 7)));
             v.x *= alpha; v.y *= alpha; v.z *= alpha; v.w *= alpha;
-            float* q = cbase + (int64_t)row * p.scm + (int64_t)col * p.scn;
-            if (p.scn == 1 && col + 3 < p.N && ((reinterpret_cast<uintptr_t>(q) & 15) == 0)) {
-              if (p.accumulate) {
+            float* q = cbase + (int64_t)row * ldm + (int64_t)col * ldn;
+            if (ldn == 1 && col + 3 < p.N && ((reinterpret_cast<uintptr_t>(q) & 15) == 0)) {
+              if (p.accumulate && !partial) {
                 const float4 o = *reinterpret_cast<const float4*>(q);
                 v.x += o.x; v.y += o.y; v.z += o.z; v.w += o.w;
               }
@@ -357,8 +371,8 @@ gemm_kernel(const __grid_constant__ CUtensorMap map_ah, const __grid_constant__ 
 #pragma unroll
               for (int j = 0; j < 4; ++j) {
                 if (col + j < p.N) {
-                  float* qq = q + (int64_t)j * p.scn;
-                  *qq = p.accumulate ? *qq + e[j] : e[j];
+                  float* qq = q + (int64_t)j * ldn;
+                  *qq = (p.accumulate && !partial) ? *qq + e[j] : e[j];
                 }
               }
             }
@@ -420,6 +434,42 @@ static int num_sms() {
 
 static int64_t align_up(int64_t x) { return (x + 255) / 256 * 256; }
 
+// K-splits so that (tiles x splits) covers the SMs, >= 2 chunks per split
+static void choose_split(const GemmArgs& g, int* ksplit, int* kb_per) {
+  const int64_t tiles = ((g.M + BM - 1) / BM) * ((g.N + BN - 1) / BN) * g.batch;
+  const int64_t Kp = (g.K + 3) / 4 * 4;
+  const int nk = (int)((Kp + BK - 1) / BK);
+  int s = 1;
+  if (tiles < num_sms() && nk >= 4 * CHUNK_KB) {
+    s = (int)std::min<int64_t>((num_sms() + tiles - 1) / tiles, nk / (2 * CHUNK_KB));
+    s = std::max(1, std::min(s, 32));
+  }
+  int per = (nk + s - 1) / s;
+  per = (per + CHUNK_KB - 1) / CHUNK_KB * CHUNK_KB;
+  s = (nk + per - 1) / per;
+  *ksplit = s;
+  *kb_per = per;
+}
+
+__global__ void __launch_bounds__(256) splitk_sum(int64_t M, int64_t N, int64_t batch, int ksplit,
+                                                  const float* __restrict__ part, float* C,
+                                                  int64_t scb, int64_t scm, int64_t scn,
+                                                  const float* alpha_rows, int accumulate) {
+  pdl_enter();
+  const int64_t plane = batch * M * N;
+  const int64_t total = plane;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    float s = 0.f;
+    for (int k = 0; k < ksplit; ++k) s += __ldg(part + k * plane + i);
+    const int64_t b = i / (M * N), rem = i - b * M * N;
+    const int64_t m = rem / N, n = rem - m * N;
+    if (alpha_rows) s *= alpha_rows[b * M + m];
+    float* q = C + b * scb + m * scm + n * scn;
+    *q = accumulate ? *q + s : s;
+  }
+}
+
 }  // namespace tc
 
 // Workspace: hi/lo planes of both operands (K padded to a multiple of 4 so
@@ -428,7 +478,10 @@ int64_t gemm_tcgen05_workspace(const GemmArgs& g) {
   const int64_t Kp = (g.K + 3) / 4 * 4;
   const int64_t ba = (g.sab == 0 && g.batch > 1) ? 1 : g.batch;
   const int64_t bb = (g.sbb == 0 && g.batch > 1) ? 1 : g.batch;
-  return 2 * tc::align_up(ba * g.M * Kp * 4) + 2 * tc::align_up(bb * g.N * Kp * 4);
+  int ks, per;
+  tc::choose_split(g, &ks, &per);
+  const int64_t part = ks > 1 ? tc::align_up((int64_t)ks * g.batch * g.M * g.N * 4) : 0;
+  return 2 * tc::align_up(ba * g.M * Kp * 4) + 2 * tc::align_up(bb * g.N * Kp * 4) + part;
 }
 
 bool gemm_tcgen05_eligible(const GemmArgs& g) {
@@ -444,9 +497,11 @@ bool gemm_tcgen05_eligible(const GemmArgs& g) {
 bool gemm_tcgen05_profitable(const GemmArgs& g) {
   if (g.K < 16 || g.M < 16 || g.N < 16) return false;
   const double tiles = (double)((g.M + 127) / 128) * ((g.N + 127) / 128) * g.batch;
-  const double nk = (double)((g.K + 31) / 32);
-  const double waves = std::ceil(tiles / tc::num_sms());
-  const double t_tc = waves * (nk * 0.45 + 1.5) + 6.0;
+  int ks, per;
+  tc::choose_split(g, &ks, &per);
+  const double nk = (double)per;
+  const double waves = std::ceil(tiles * ks / tc::num_sms());
+  const double t_tc = waves * (nk * 0.6 + 1.5) + 6.0 + (ks > 1 ? 3.0 : 0.0);
   const double t_simt = 2.0 * g.M * g.N * g.K * g.batch / 15e6 + 3.0;
   return t_tc < t_simt;
 }
@@ -462,7 +517,10 @@ int gemm_tcgen05(const GemmArgs& g, void* ws, int64_t ws_bytes, cudaStream_t s) 
   float* ah = reinterpret_cast<float*>(w); w += align_up(ba * g.M * Kp * 4);
   float* al = reinterpret_cast<float*>(w); w += align_up(ba * g.M * Kp * 4);
   float* bh = reinterpret_cast<float*>(w); w += align_up(bb * g.N * Kp * 4);
-  float* bl = reinterpret_cast<float*>(w);
+  float* bl = reinterpret_cast<float*>(w); w += align_up(bb * g.N * Kp * 4);
+  int ksplit, kb_per;
+  choose_split(g, &ksplit, &kb_per);
+  float* partials = ksplit > 1 ? reinterpret_cast<float*>(w) : nullptr;
   // split (and re-layout) both operands; padded K columns are written as 0
   dim3 ga((unsigned)((Kp + 31) / 32), (unsigned)((g.M + 31) / 32), (unsigned)ba);
   dim3 gb((unsigned)((Kp + 31) / 32), (unsigned)((g.N + 31) / 32), (unsigned)bb);
@@ -479,10 +537,13 @@ int gemm_tcgen05(const GemmArgs& g, void* ws, int64_t ws_bytes, cudaStream_t s) 
   }
   Params p{(int)g.M, (int)g.N, (int)Kp, (int)g.batch,
            (int)((g.M + BM - 1) / BM), (int)((g.N + BN - 1) / BN), a_bc, b_bc,
-           g.C, g.scb, g.scm, g.scn, g.alpha_rows, g.accumulate};
-  const int64_t ntiles = (int64_t)p.ntm * p.ntn * g.batch;
-  const int grid = (int)std::min<int64_t>(ntiles, num_sms());
+           g.C, g.scb, g.scm, g.scn, g.alpha_rows, g.accumulate, ksplit, kb_per, partials};
+  const int64_t units = (int64_t)p.ntm * p.ntn * g.batch * ksplit;
+  const int grid = (int)std::min<int64_t>(units, num_sms());
   launch(gemm_kernel, grid, NUM_THREADS, SMEM_BYTES, s, mah, mal, mbh, mbl, p);
+  if (ksplit > 1)
+    launch(splitk_sum, grid_for(g.batch * g.M * g.N, 256), 256, 0, s, g.M, g.N, g.batch, ksplit,
+           (const float*)partials, g.C, g.scb, g.scm, g.scn, g.alpha_rows, g.accumulate);
   return launch_status();
 }
 
