@@ -288,7 +288,7 @@ int cast_from(const Layout& L, const pfb_tensor* x, pfb_tensor* out, cudaStream_
 
 constexpr int kMaxSteps = 48;
 constexpr int kMaxRegs = 16;
-enum FusedOpc { F_LOAD = 64, F_CONST = 65 };
+enum FusedOpc { F_LOAD = 64, F_CONST = 65, F_SELECT = 68 };
 
 struct FusedProgram {
   int n_in, n_steps;
@@ -342,6 +342,8 @@ __global__ void __launch_bounds__(256) fused_kernel(Layout L, IdxT n, FusedProgr
                 : __ldg(reinterpret_cast<const float*>(ins[k]) + off[k + 1]);
       } else if (c[0] == F_CONST) {
         v = __int_as_float(c[2]);
+      } else if (c[0] == F_SELECT) {
+        v = r[c[2]] != 0.f ? r[c[3]] : r[c[1]];
       } else {
         v = run_op(c[0], r[c[2]], r[c[3]]);
       }

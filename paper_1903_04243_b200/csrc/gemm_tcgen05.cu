@@ -439,16 +439,28 @@ static void choose_split(const GemmArgs& g, int* ksplit, int* kb_per) {
   const int64_t tiles = ((g.M + BM - 1) / BM) * ((g.N + BN - 1) / BN) * g.batch;
   const int64_t Kp = (g.K + 3) / 4 * 4;
   const int nk = (int)((Kp + BK - 1) / BK);
-  int s = 1;
-  if (tiles < num_sms() && nk >= 4 * CHUNK_KB) {
-    s = (int)std::min<int64_t>((num_sms() + tiles - 1) / tiles, nk / (2 * CHUNK_KB));
-    s = std::max(1, std::min(s, 32));
+  // time model (us): waves x (k-blocks per unit x 0.6 + 1.5), +4 for the reduction
+  auto cost = [&](int s, int* per_out) {
+    int per = (nk + s - 1) / s;
+    per = (per + CHUNK_KB - 1) / CHUNK_KB * CHUNK_KB;
+    const int real = (nk + per - 1) / per;
+    *per_out = per;
+    const double waves = std::ceil((double)tiles * real / num_sms());
+    return waves * (per * 0.6 + 1.5) + (real > 1 ? 4.0 : 0.0);
+  };
+  int best_per = 0;
+  double best = cost(1, &best_per);
+  int s_max = 1;
+  if (tiles < num_sms() && nk >= 4 * CHUNK_KB)
+    s_max = (int)std::max<int64_t>(1, std::min<int64_t>(
+        std::min<int64_t>((num_sms() + tiles - 1) / tiles, nk / (2 * CHUNK_KB)), 32));
+  for (int s = 2; s <= s_max; ++s) {
+    int per;
+    const double c = cost(s, &per);
+    if (c < best) { best = c; best_per = per; }
   }
-  int per = (nk + s - 1) / s;
-  per = (per + CHUNK_KB - 1) / CHUNK_KB * CHUNK_KB;
-  s = (nk + per - 1) / per;
-  *ksplit = s;
-  *kb_per = per;
+  *kb_per = best_per;
+  *ksplit = (nk + best_per - 1) / best_per;
 }
 
 __global__ void __launch_bounds__(256) splitk_sum(int64_t M, int64_t N, int64_t batch, int ksplit,
@@ -501,7 +513,7 @@ bool gemm_tcgen05_profitable(const GemmArgs& g) {
   tc::choose_split(g, &ks, &per);
   const double nk = (double)per;
   const double waves = std::ceil(tiles * ks / tc::num_sms());
-  const double t_tc = waves * (nk * 0.6 + 1.5) + 6.0 + (ks > 1 ? 3.0 : 0.0);
+  const double t_tc = waves * (nk * 0.6 + 1.5) + 6.0 + (ks > 1 ? 4.0 : 0.0);
   const double t_simt = 2.0 * g.M * g.N * g.K * g.batch / 15e6 + 3.0;
   return t_tc < t_simt;
 }

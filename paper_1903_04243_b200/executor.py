@@ -470,7 +470,7 @@ class Executor:
                 rm = {}
                 g, _ = vectorize_graph(g, refmap_out=rm)
                 refmap = {k: (r.nid, r.port) for k, r in rm.items()}
-            if self.optimize and not _has_blocks(g):
+            if self.optimize:
                 from .passes import optimize as _opt
                 keep = [tuple(o) for o in g.outputs] if refmap is None else \
                     [refmap[tuple(o)] for o in self.graph.outputs]

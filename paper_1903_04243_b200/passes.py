@@ -240,9 +240,31 @@ def fuse_reductions(g, keep=()):
     return count, moved
 
 
+def _optimize_in_place(g, keep, elementwise=True):
+    _, moved = fuse_outer_products(g, keep)
+    keep = [moved.get(k, k) for k in keep]
+    _, moved4 = fuse_reductions(g, keep)
+    keep = [moved4.get(k, k) for k in keep]
+    moved3 = {}
+    if elementwise:
+        _, moved3 = fuse_elementwise(g, keep)
+    return [moved3.get(k, k) for k in keep]
+
+
+def _optimize_blocks(g, elementwise=True):
+    """Apply the rewrites inside every cond / while sub-graph (outputs kept)."""
+    for node in list(g.nodes.values()):
+        if node.block is None:
+            continue
+        for sg in node.block.subgraphs.values():
+            _optimize_blocks(sg, elementwise)
+            sg.set_outputs(_optimize_in_place(sg, [tuple(o) for o in sg.outputs], elementwise))
+
+
 def optimize(g, keep_keys, elementwise=True):
     """Copy `g`, apply the rewrites, return (graph, key map old->new)."""
     dst, mapping = copy_with_map(g)
+    _optimize_blocks(dst, elementwise)
     keep = [mapping[k] for k in keep_keys]
     _, moved = fuse_outer_products(dst, keep)
     keep = [moved.get(k, k) for k in keep]
@@ -265,14 +287,14 @@ def optimize(g, keep_keys, elementwise=True):
 _BIN_CODE = {"add": 0, "sub": 1, "mul": 2, "div": 3, "max": 4, "min": 5, "less": 6, "equal": 7}
 _UN_CODE = {"neg": 0, "exp": 1, "log": 2, "relu": 3, "tanh": 4, "sigmoid": 5, "square": 6,
             "logical_not": 7}
-OP_LOAD, OP_CONST, OP_TOBOOL, OP_MOV = 64, 65, 66, 67
+OP_LOAD, OP_CONST, OP_TOBOOL, OP_MOV, OP_SELECT = 64, 65, 66, 67, 68
 MAX_INPUTS, MAX_STEPS, MAX_REGS = 8, 48, 16
 
 
 def _ew_eligible(g, node):
     from .tensor import DType
     k = node.kind
-    if k not in _BIN_CODE and k not in _UN_CODE and k != "cast":
+    if k not in _BIN_CODE and k not in _UN_CODE and k not in ("cast", "select"):
         return False
     if node.output_arity != 1 or node.out_dtypes[0] not in (DType.F64, DType.BOOL):
         return False
@@ -282,6 +304,8 @@ def _ew_eligible(g, node):
     for src in node.inputs:
         if g.ref_dtype(src) not in (DType.F64, DType.BOOL):
             return False
+    if k == "select" and g.ref_dtype(node.inputs[0]) != DType.BOOL:
+        return False
     return True
 
 
@@ -326,13 +350,24 @@ def _program(g, order, root, externals):
 
     for i, n in enumerate(order):
         ops = [operand(src) for src in n.inputs]
+        k = n.kind
+        if k == "select":  # r[dst] = m ? a : b; dst must not alias m or a
+            if not free:
+                raise OverflowError
+            dst = free.pop()
+            steps.append((OP_MOV, dst, ops[2], ops[2]))
+            steps.append((OP_SELECT, dst, ops[0], ops[1]))
+            for src in set(n.inputs):
+                if last_use.get(src) == i and src in reg:
+                    free.append(reg.pop(src))
+            reg[(n.id, 0)] = dst
+            continue
         for src in set(n.inputs):
             if last_use.get(src) == i and src in reg:
                 free.append(reg.pop(src))
         if not free:
             raise OverflowError
         dst = free.pop()
-        k = n.kind
         if k in _BIN_CODE:
             steps.append((_BIN_CODE[k], dst, ops[0], ops[1]))
         elif k in _UN_CODE:

@@ -96,3 +96,19 @@ def test_masked_nested_matches_compaction_and_loop():
     manual = [sum((2 * v if v > 0 else -v) for v in X[i, :L[i]]) for i in range(6)]
     np.testing.assert_allclose(got, manual, rtol=0, atol=1e-12)
     del g
+
+
+def test_passes_inside_loop_bodies_preserve_values(golden):
+    """optimize() also fuses inside cond / while sub-graphs (predicated cfg5 body)."""
+    from paper_1903_04243_b200.passes import optimize
+    _, kw = PROGRAM_CASES["cfg5_mid"]
+    w = WL.cfg5(WL.this_api(), masked=True, unroll=2, **kw)
+    keys = [tuple(o) for o in w.graph.outputs]
+    g2, m = optimize(w.graph, keys)
+    fused = [n for n in g2.nodes.values() if n.block is not None
+             for sg in n.block.subgraphs.values() for x in sg.nodes.values()
+             if x.kind == "fused_ew"]
+    assert fused
+    got = OracleExecutor(g2).run(feeds=w.feeds, outputs=[g2.out(*m[k]) for k in keys])
+    np.testing.assert_allclose(got[0].data, golden["programs"]["cfg5_mid/out/0"], rtol=0,
+                               atol=1e-12)
