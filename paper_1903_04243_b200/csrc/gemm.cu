@@ -1,6 +1,9 @@
 // pfb_matmul: validation + path selection (reference tensor.py:195-206).
 #include <algorithm>
 #include <cstdlib>
+#include <map>
+#include <mutex>
+#include <tuple>
 
 #include "gemm.cuh"
 
@@ -40,6 +43,47 @@ __global__ void zero_f32(float* p, int64_t n) {
     p[i] = 0.f;
 }
 
+// Per-shape autotuning of the tcgen05-vs-SIMT choice: on the first call of a
+// shape (outside stream capture, not accumulating) both paths run twice and
+// the faster second run wins; later calls -- including the ones captured into
+// CUDA graphs -- reuse the cached choice.  PFB_GEMM_AUTOTUNE=0 uses the model.
+namespace {
+using ShapeKey = std::tuple<int64_t, int64_t, int64_t, int64_t, int, int, int, int, int>;
+std::map<ShapeKey, int> g_choice;  // 1 = SIMT, 2 = tcgen05
+std::mutex g_mu;
+
+ShapeKey key_of(const GemmArgs& g) {
+  return ShapeKey(g.batch, g.M, g.N, g.K, g.sak == 1, g.sam == 1, g.sbk == 1, g.sbn == 1,
+                  g.sab == 0 ? 1 : (g.sbb == 0 ? 2 : 0));
+}
+
+bool autotune_enabled() {
+  static const bool on = [] {
+    const char* e = getenv("PFB_GEMM_AUTOTUNE");
+    return !(e && e[0] == '0');
+  }();
+  return on;
+}
+
+float time_path(const GemmArgs& g, int path, void* ws, int64_t ws_bytes, cudaStream_t s) {
+  cudaEvent_t e0, e1;
+  cudaEventCreate(&e0);
+  cudaEventCreate(&e1);
+  float ms = 1e30f;
+  for (int rep = 0; rep < 2; ++rep) {
+    cudaEventRecord(e0, s);
+    int rc = path == 2 ? gemm_tcgen05(g, ws, ws_bytes, s) : gemm_simt(g, ws, ws_bytes, s);
+    cudaEventRecord(e1, s);
+    cudaEventSynchronize(e1);
+    if (rc != 0) { ms = 1e30f; break; }
+    cudaEventElapsedTime(&ms, e0, e1);
+  }
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  return ms;
+}
+}  // namespace
+
 extern "C" int64_t pfb_matmul_workspace(const pfb_tensor* a, const pfb_tensor* b,
                                         pfb_tensor* out) {
   GemmArgs g;
@@ -66,10 +110,35 @@ extern "C" int pfb_matmul_ex(const pfb_tensor* a, const pfb_tensor* b, pfb_tenso
   // force_path: 0 = auto, 1 = SIMT, 2 = tcgen05 (error if ineligible).
   // PFB_DISABLE_TCGEN05=1 pins auto to SIMT (A/B testing, bring-up).
   static const bool tc_off = getenv("PFB_DISABLE_TCGEN05") && getenv("PFB_DISABLE_TCGEN05")[0] == '1';
-  if (force_path == 2 || (force_path == 0 && !tc_off && gemm_tcgen05_profitable(g) &&
-                          gemm_tcgen05_eligible(g))) {
+  if (force_path == 1) return gemm_simt(g, ws, ws_bytes, s);
+  if (force_path == 2) return gemm_tcgen05(g, ws, ws_bytes, s);
+  const bool tc_ok = !tc_off && gemm_tcgen05_eligible(g) &&
+                     ws_bytes >= gemm_tcgen05_workspace(g) && ws != nullptr &&
+                     (double)g.batch * g.M * g.N * g.K >= (double)(1 << 20);
+  if (!tc_ok) return gemm_simt(g, ws, ws_bytes, s);
+  int path = 0;
+  {
+    std::lock_guard<std::mutex> lk(g_mu);
+    auto it = g_choice.find(key_of(g));
+    if (it != g_choice.end()) path = it->second;
+  }
+  if (path == 0) {
+    cudaStreamCaptureStatus st = cudaStreamCaptureStatusNone;
+    cudaStreamIsCapturing(s, &st);
+    if (autotune_enabled() && !accumulate && st == cudaStreamCaptureStatusNone) {
+      const float t_simt = time_path(g, 1, ws, ws_bytes, s);
+      const float t_tc = time_path(g, 2, ws, ws_bytes, s);  // leaves C computed
+      path = t_tc < t_simt ? 2 : 1;
+      std::lock_guard<std::mutex> lk(g_mu);
+      g_choice[key_of(g)] = path;
+      if (path == 2) return launch_status();  // C already holds the tcgen05 result
+      return gemm_simt(g, ws, ws_bytes, s);
+    }
+    path = gemm_tcgen05_profitable(g) ? 2 : 1;
+  }
+  if (path == 2) {
     int e = gemm_tcgen05(g, ws, ws_bytes, s);
-    if (e != PFB_E_UNSUPPORTED || force_path == 2) return e;
+    if (e != PFB_E_UNSUPPORTED) return e;
   }
   return gemm_simt(g, ws, ws_bytes, s);
 }
