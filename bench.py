@@ -64,6 +64,45 @@ CPU_SAMPLE = {
 }
 
 
+SWEEPS = {"cfg2_mlp": ("n", [1024, 8192]), "cfg1_batch": ("batch", [256, 2048])}
+
+
+def device_throughput(builder, kw, dev, steps=10, warmup=3):
+    """Device-timed units/s for one extra workload size (sweep entries)."""
+    import torch
+    from paper_1903_04243_b200 import workloads as WL
+    from paper_1903_04243_b200.executor import Executor
+    w = WL.BUILDERS[builder](WL.this_api(), **kw)
+    ex = Executor(w.graph, device=dev, check_errors=False)
+    feeds = {k: torch.as_tensor(np.asarray(v, np.float32 if np.asarray(v).dtype == np.float64
+                                           else np.asarray(v).dtype)).to(dev)
+             for k, v in w.feeds.items()}
+    for _ in range(warmup):
+        ex.run_device(feeds)
+    torch.cuda.synchronize(dev)
+    st, en = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    st.record()
+    for _ in range(steps):
+        ex.run_device(feeds)
+    en.record()
+    torch.cuda.synchronize(dev)
+    return w.units * steps / (st.elapsed_time(en) / 1e3)
+
+
+def load_traffic(cfg_name):
+    """DRAM bytes per launch of the dominant kernel from the committed ncu
+    `--set full` capture (profiles/<round>/full_<cfg>.json), if present."""
+    rounds = sorted((ROOT / "profiles").glob("r*/full_%s.json" % cfg_name))
+    if not rounds:
+        return None, None
+    try:
+        recs = json.loads(rounds[-1].read_text())
+        r = recs[0]
+        return r.get("dram_read", 0) + r.get("dram_write", 0), f"{rounds[-1].parent.name}: {r['kernel'][:60]}"
+    except Exception:
+        return None, None
+
+
 def load_peaks():
     p = ROOT / "MEASURED_PEAKS.json"
     if p.exists():
@@ -178,6 +217,7 @@ def main():
     ap.add_argument("--config", default="cfg2_mlp", choices=sorted(CONFIGS))
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-sweep", action="store_true")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     if args.impl == "reference":
@@ -309,6 +349,19 @@ def main():
                          "launches_of_kind_per_step": len(same),
                          "launches_per_step": len(recs)})
 
+    if roofline is not None:
+        traffic, src_k = load_traffic(args.config)
+        roofline["traffic"] = traffic
+        roofline["traffic_source"] = src_k
+    sweep = None
+    if args.config in SWEEPS and world == 1 and not args.no_sweep:
+        key, sizes = SWEEPS[args.config]
+        sweep = {"scaling": "batch sweep (device-timed, same program, larger pfor)"}
+        for n in sizes:
+            kw2 = dict(kw)
+            kw2[key] = n
+            sweep[f"{key}={n}"] = device_throughput(builder, kw2, dev)
+
     line = {"metric": METRIC, "value": value, "unit": unit, "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
@@ -319,6 +372,8 @@ def main():
             "e2e": {"value": e2e, "unit": unit, "h2d_bytes_per_step": h2d,
                     "d2h_bytes_per_step": d2h},
             "gpu_launches": launches, "roofline": roofline, "clocks": clocks.summary()}
+    if sweep is not None:
+        line["sweep"] = sweep
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         cb = cpu_baseline(args.config)
         line["cpu_baseline"] = {"value": cb["value"], "unit": unit, "cores": cb["cores"],
