@@ -46,7 +46,7 @@ CONFIGS = {
     "cfg2_conv": ("cfg2", dict(n=128, model="conv"), "per-example grads/s"),
     "cfg1_batch": ("cfg1", dict(batch=32, variant="batch"), "jacobian rows/s"),
     "cfg1_full": ("cfg1", dict(batch=32, variant="full"), "jacobian rows/s"),
-    "cfg3": ("cfg3", dict(width=4096, out_dim=1024, rows=8), "jacobian rows/s"),
+    "cfg3": ("cfg3", dict(width=4096, out_dim=1024, rows=32), "jacobian rows/s"),
     "cfg4": ("cfg4", dict(n=256, steps=64, units=512), "per-example grads/s"),
     "cfg5": ("cfg5", dict(n=1024, max_len=100, units=256, masked=True, unroll=4), "examples/s"),
     "cfg5_compact": ("cfg5", dict(n=1024, max_len=100, units=256), "examples/s"),

@@ -188,12 +188,56 @@ __global__ void __launch_bounds__(256) gemm_smallk_kernel(GemmArgs g) {
   }
 }
 
+// K = 1, rhs unit-stride: C[b, m, :] = a[b, m] * B[b, 0, :].  Each thread owns
+// 4 consecutive columns (kept in registers) and streams a block of rows with
+// 128-bit streaming stores -- the cfg3 weight-jacobian writer (store-bound).
+__global__ void __launch_bounds__(256) outer1_kernel(GemmArgs g, int64_t rows_per_cta) {
+  pdl_enter();
+  const int64_t nq = g.N / 4;
+  const int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (q >= nq) return;
+  const int64_t rows = g.batch * g.M;
+  const int64_t r0 = (int64_t)blockIdx.y * rows_per_cta;
+  const int64_t r1 = r0 + rows_per_cta < rows ? r0 + rows_per_cta : rows;
+  int64_t b = r0 / g.M, m = r0 - b * g.M;
+  float4 bv = __ldg(reinterpret_cast<const float4*>(g.B + b * g.sbb) + q);
+  for (int64_t r = r0; r < r1; ++r) {
+    const float av = __ldg(g.A + b * g.sab + m * g.sam) *
+                     (g.alpha_rows ? g.alpha_rows[r] : 1.f);
+    float4* dst = reinterpret_cast<float4*>(g.C + b * g.scb + m * g.scm) + q;
+    float4 o = make_float4(av * bv.x, av * bv.y, av * bv.z, av * bv.w);
+    if (g.accumulate) {
+      const float4 c = *dst;
+      o.x += c.x; o.y += c.y; o.z += c.z; o.w += c.w;
+      *dst = o;
+    } else {
+      __stcs(dst, o);
+    }
+    if (++m == g.M) {
+      m = 0;
+      ++b;
+      if (r + 1 < r1) bv = __ldg(reinterpret_cast<const float4*>(g.B + b * g.sbb) + q);
+    }
+  }
+}
+
 static int smallk_launch(const GemmArgs& g, cudaStream_t s) {
   const bool vec = g.K <= 16 && g.sbn == 1 && g.scn == 1 && g.N % 4 == 0 && g.sbk % 4 == 0 &&
                    g.sbb % 4 == 0 && g.scm % 4 == 0 && g.scb % 4 == 0 &&
                    (reinterpret_cast<uintptr_t>(g.B) & 15) == 0 &&
                    (reinterpret_cast<uintptr_t>(g.C) & 15) == 0;
   const int64_t rows = g.batch * g.M;
+  if (vec && g.K == 1 && g.N >= 512) {
+    const int64_t nq = g.N / 4;
+    const unsigned gx = (unsigned)((nq + 255) / 256);
+    // enough CTAs for ~8 per SM, at least 16 rows each
+    int64_t rpc = std::max<int64_t>(16, rows * gx / ((int64_t)kNumSMs * 8));
+    const int64_t gy = (rows + rpc - 1) / rpc;
+    if (gy <= 65535) {
+      launch(outer1_kernel, dim3(gx, (unsigned)gy), 256, 0, s, g, rpc);
+      return launch_status();
+    }
+  }
   const int grid = (int)std::min<int64_t>(rows, (int64_t)kNumSMs * 8);
   if (vec) launch(gemm_smallk_kernel<true>, grid, 256, 0, s, g);
   else launch(gemm_smallk_kernel<false>, grid, 256, 0, s, g);

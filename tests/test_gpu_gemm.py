@@ -120,3 +120,14 @@ def test_gemm_tcgen05_no_accumulation_bias(env):
     got = _run(env, a, b, 2, transpose_b=True)
     bias = np.mean((got - want) * np.sign(want))
     assert abs(bias) < 5e-7, bias
+
+
+@pytest.mark.parametrize("shape", [(4096, 1, 4096, 1), (300, 1, 1024, 3), (64, 2, 520, 1)])
+def test_small_k_outer_products(env, shape):
+    """K<=16 writer paths (cfg3 weight jacobians): exact fp32 products."""
+    m, k, n, bsz = shape
+    r = np.random.default_rng(m + n)
+    a = _f32(r, (bsz, m, k) if bsz > 1 else (m, k))
+    b = _f32(r, (bsz, k, n) if bsz > 1 else (k, n))
+    got = _run(env, a, b, 0)
+    np.testing.assert_allclose(got, a @ b, rtol=1e-6, atol=1e-6)
