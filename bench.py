@@ -343,9 +343,14 @@ def main():
             ach = nbytes / dur / 1e9
             roofline = {"bound": "hbm", "achieved": ach, "peak": hbm, "unit": "GB/s",
                         "frac": ach / hbm, "peak_source": f"{src} hbm_gbs"}
+        # share of the eager instrumented step spent in launches of this kind
+        # (per-launch events; comparable with the ncu launch list's shares)
+        ev_ms = [r[3].elapsed_time(r[4]) for r in recs]
+        kind_share = sum(t for t, r in zip(ev_ms, recs) if r[0] == what) / max(sum(ev_ms), 1e-9)
         roofline.update({"traffic": None, "kernel": what, "algorithmic_bytes": nbytes,
                          "algorithmic_flops": flops, "launch_us": dur * 1e6,
-                         "share_of_step": dur * len(same) / (ms_per_step / 1e3),
+                         "share_of_step": dur / (ms_per_step / 1e3),
+                         "kind_share_eager": kind_share,
                          "launches_of_kind_per_step": len(same),
                          "launches_per_step": len(recs)})
 
