@@ -97,6 +97,9 @@ int pfb_reduce_dot(const pfb_tensor* x, const pfb_tensor* y, uint32_t axes_mask,
  * (reference tensor.py:286-303, 383-416). */
 int pfb_copy(const pfb_tensor* x, pfb_tensor* out, void* stream);
 int pfb_fill(pfb_tensor* out, double value, void* stream);
+/* concat of n same-dtype inputs (any strides) along `axis` into out, in one
+ * launch per 24 inputs (reference tensor.concat, tensor.py:383-393). */
+int pfb_concat(int32_t n, const pfb_tensor* xs, int32_t axis, pfb_tensor* out, void* stream);
 
 /* matmul (reference tensor.py:195-206): rank-2 x rank-2 or batched rank-3;
  * operands may be strided views (any layout).  fp32-accurate: tcgen05
@@ -112,6 +115,29 @@ int pfb_matmul(const pfb_tensor* a, const pfb_tensor* b, pfb_tensor* out, void* 
 int pfb_matmul_ex(const pfb_tensor* a, const pfb_tensor* b, pfb_tensor* out,
                   const float* alpha_rows, int32_t accumulate, int32_t force_path, void* ws,
                   int64_t ws_bytes, void* stream);
+
+/* n (<= 8) independent row-dots in one launch (passes.fuse_row_dots):
+ * outs[j][i] = sum_k xs[j][i,k] * ys[j][i,k], xs/ys rank-2 [rows, inner_j]
+ * views with unit inner stride (any row stride), outs rank-1 [rows].  The
+ * per-parameter-block squared norms of per-example gradients (reference
+ * reduce_sum(square(g), axes) per block, tensor.py:279-283). */
+int pfb_row_dots(int32_t n, const pfb_tensor* xs, const pfb_tensor* ys, pfb_tensor* outs,
+                 void* stream);
+
+/* matmul with a fused prologue/epilogue (post-vectorization rewrite
+ * passes.fuse_matmul_epilogues; SURVEY.md §8a F3 "GEMM epilogues: bias add,
+ * activation, broadcast scale"):
+ *   out = act(alpha_rows * (a @ diag(kscale) @ b) [+ out] + bias)
+ * `kscale` (nullable) is broadcast to [batch, K] and scales b's rows (the
+ * per-example clip factors of a clipped-sum contraction); `bias` (nullable) is
+ * broadcast to out's shape (right-aligned; stride 0 = broadcast); `act` is a
+ * PFB_ACT_* code.  Replaces the reference's matmul -> mul / add / tanh chain
+ * (tensor.py:140-206). */
+enum pfb_act { PFB_ACT_NONE = 0, PFB_ACT_TANH = 1, PFB_ACT_SIGMOID = 2, PFB_ACT_RELU = 3 };
+int pfb_matmul_fused(const pfb_tensor* a, const pfb_tensor* b, pfb_tensor* out,
+                     const pfb_tensor* kscale, const pfb_tensor* bias, int32_t act,
+                     const float* alpha_rows, int32_t accumulate, int32_t force_path, void* ws,
+                     int64_t ws_bytes, void* stream);
 
 /* conv family (reference tensor.py:209-260), NHWC / HWIO, SAME, stride 1 */
 int pfb_im2col(const pfb_tensor* x, int32_t k1, int32_t k2, pfb_tensor* out, void* stream);

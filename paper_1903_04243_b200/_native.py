@@ -52,6 +52,9 @@ _SIGNATURES = {
     "pfb_matmul_workspace": ([_P, _P, _P], ctypes.c_int64),
     "pfb_matmul": ([_P, _P, _P, _vp, _i64, _vp], ctypes.c_int),
     "pfb_matmul_ex": ([_P, _P, _P, _vp, _i32, _i32, _vp, _i64, _vp], ctypes.c_int),
+    "pfb_concat": ([_i32, _P, _i32, _P, _vp], ctypes.c_int),
+    "pfb_row_dots": ([_i32, _P, _P, _P, _vp], ctypes.c_int),
+    "pfb_matmul_fused": ([_P, _P, _P, _P, _P, _i32, _vp, _i32, _i32, _vp, _i64, _vp], ctypes.c_int),
     "pfb_im2col": ([_P, _i32, _i32, _P, _vp], ctypes.c_int),
     "pfb_conv2d": ([_P, _P, _P, _vp], ctypes.c_int),
     "pfb_conv2d_input_grad": ([_P, _P, _P, _vp], ctypes.c_int),

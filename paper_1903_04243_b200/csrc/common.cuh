@@ -135,6 +135,11 @@ __device__ __forceinline__ void pdl_enter() {
   asm volatile("griddepcontrol.launch_dependents;" :::);
 }
 
+inline bool getenv_flag(const char* name) {
+  const char* e = getenv(name);
+  return e && e[0] == '1';
+}
+
 inline bool pdl_enabled() {
   static const int on = [] {
     const char* e = getenv("PFB_DISABLE_PDL");

@@ -8,6 +8,8 @@
 // unit-stride and 16-byte aligned; index math in 32 bits when it fits.
 #include "common.cuh"
 
+#include <algorithm>
+
 namespace pfb {
 
 // ----------------------------------------------------------------------------
@@ -296,73 +298,162 @@ struct FusedProgram {
   int code[kMaxSteps][4];  // opcode, dst, src1, src2 (src1 = input / const bits)
 };
 
-__device__ __forceinline__ float run_op(int opc, float x, float y) {
-  switch (opc) {
-    case PFB_ADD: return x + y;
-    case PFB_SUB: return x - y;
-    case PFB_MUL: return x * y;
-    case PFB_DIV: return x / y;
-    case PFB_MAX: return np_max(x, y);
-    case PFB_MIN: return np_min(x, y);
-    case PFB_LESS: return x < y ? 1.f : 0.f;
-    case PFB_EQUAL: return x == y ? 1.f : 0.f;
-    case 16 + PFB_NEG: return -x;
-    case 16 + PFB_EXP: return expf(x);
-    case 16 + PFB_LOG: return logf(x);
-    case 16 + PFB_RELU: return np_max(x, 0.f);
-    case 16 + PFB_TANH: return tanhf(x);
-    case 16 + PFB_SIGMOID: return 1.f / (1.f + expf(-x));
-    case 16 + PFB_SQUARE: return x * x;
-    case 16 + PFB_LOGICAL_NOT: return x == 0.f ? 1.f : 0.f;
-    case 66: return x != 0.f ? 1.f : 0.f;  // cast f32 -> bool
-    default: return x;                     // 67: move (cast bool -> f32)
+// One templated kernel for both widths: V = 4 runs the program on 4
+// consecutive elements of the innermost dim per thread (extent a multiple of
+// 4; contiguous operands move as 128-bit accesses), V = 1 on single elements.
+// The program is staged in shared memory once per CTA; each step is one
+// warp-uniform switch whose cases apply the op to all V lanes, so dispatch,
+// offset arithmetic and register-file traffic are paid once per V elements.
+// Operand feed modes (2 bits per operand, operand 0 = output): 0 = contiguous
+// + aligned vector, 1 = inner-dim broadcast, 2 = strided.
+template <int V>
+struct alignas(4 * V) Vec {
+  float v[V];
+};
+
+template <int V, typename T>
+__device__ __forceinline__ Vec<V> load_v(const void* base, int64_t off, int64_t inner, int mode) {
+  Vec<V> r;
+  const T* p = reinterpret_cast<const T*>(base) + off;
+  if (V == 4 && mode == 0) {
+    if constexpr (std::is_same<T, float>::value) {
+      const float4 f = __ldg(reinterpret_cast<const float4*>(p));
+      r.v[0] = f.x; r.v[1] = f.y; r.v[2] = f.z; r.v[3] = f.w;
+    } else {
+      const uchar4 u = __ldg(reinterpret_cast<const uchar4*>(p));
+      r.v[0] = u.x; r.v[1] = u.y; r.v[2] = u.z; r.v[3] = u.w;
+    }
+    return r;
   }
+  if (mode == 1) {
+    const float x = (float)__ldg(p);
+#pragma unroll
+    for (int j = 0; j < V; ++j) r.v[j] = x;
+    return r;
+  }
+#pragma unroll
+  for (int j = 0; j < V; ++j) r.v[j] = (float)__ldg(p + j * inner);
+  return r;
 }
 
-template <typename IdxT, typename Tout, int NIN>
-__global__ void __launch_bounds__(256) fused_kernel(Layout L, IdxT n, FusedProgram P, Tout* out,
+#define PFB_EW1(EXPR)                                     \
+  {                                                       \
+    _Pragma("unroll") for (int j = 0; j < V; ++j) {       \
+      const float x = a.v[j];                             \
+      (void)x;                                            \
+      o.v[j] = (EXPR);                                    \
+    }                                                     \
+  }                                                       \
+  break;
+#define PFB_EW2(EXPR)                                     \
+  {                                                       \
+    _Pragma("unroll") for (int j = 0; j < V; ++j) {       \
+      const float x = a.v[j], y = b.v[j];                 \
+      o.v[j] = (EXPR);                                    \
+    }                                                     \
+  }                                                       \
+  break;
+
+template <typename IdxT, typename Tout, int NIN, int V>
+__global__ void __launch_bounds__(256) fused_kernel(Layout L, IdxT ngroups, FusedProgram P,
+                                                    uint32_t modes, Tout* out,
                                                     const void* i0, const void* i1,
                                                     const void* i2, const void* i3,
                                                     const void* i4, const void* i5,
                                                     const void* i6, const void* i7) {
   pdl_enter();
-  const void* ins[8] = {i0, i1, i2, i3, i4, i5, i6, i7};
-  for (IdxT i = blockIdx.x * (IdxT)blockDim.x + threadIdx.x; i < n;
-       i += (IdxT)gridDim.x * blockDim.x) {
+  __shared__ int4 prog[kMaxSteps];
+  for (int s = threadIdx.x; s < P.n_steps; s += blockDim.x)
+    prog[s] = make_int4(P.code[s][0], P.code[s][1], P.code[s][2], P.code[s][3]);
+  __syncthreads();
+  const int nsteps = P.n_steps;
+  const int ir = L.rank - 1;
+  const int res_reg = P.code[P.n_steps - 1][1];
+  for (IdxT g = blockIdx.x * (IdxT)blockDim.x + threadIdx.x; g < ngroups;
+       g += (IdxT)gridDim.x * blockDim.x) {
     int64_t off[NIN + 1];
-    offsets<IdxT, NIN + 1>(L, i, off);
-    float r[kMaxRegs];
-    for (int s = 0; s < P.n_steps; ++s) {
-      const int* c = P.code[s];
-      float v;
-      if (c[0] == F_LOAD) {
-        const int k = c[2];
-        v = P.in_dtype[k] == PFB_BOOL
-                ? (float)__ldg(reinterpret_cast<const uint8_t*>(ins[k]) + off[k + 1])
-                : __ldg(reinterpret_cast<const float*>(ins[k]) + off[k + 1]);
-      } else if (c[0] == F_CONST) {
-        v = __int_as_float(c[2]);
-      } else if (c[0] == F_SELECT) {
-        v = r[c[2]] != 0.f ? r[c[3]] : r[c[1]];
+    offsets<IdxT, NIN + 1>(L, g * V, off);
+    Vec<V> r[kMaxRegs];
+    for (int s = 0; s < nsteps; ++s) {
+      const int4 c = prog[s];
+      Vec<V> o;
+      if (c.x == F_LOAD) {
+        switch (c.z) {
+#define PFB_LD(K)                                                                          \
+  case K:                                                                                  \
+    if (K < NIN) {                                                                         \
+      const int md = (modes >> (2 * (K + 1))) & 3;                                         \
+      o = P.in_dtype[K] == PFB_BOOL ? load_v<V, uint8_t>(i##K, off[K < NIN ? K + 1 : 0],   \
+                                                         L.st[K + 1][ir], md)              \
+                                    : load_v<V, float>(i##K, off[K < NIN ? K + 1 : 0],     \
+                                                       L.st[K + 1][ir], md);               \
+    }                                                                                      \
+    break;
+          PFB_LD(0) PFB_LD(1) PFB_LD(2) PFB_LD(3) PFB_LD(4) PFB_LD(5) PFB_LD(6) PFB_LD(7)
+#undef PFB_LD
+        }
+      } else if (c.x == F_CONST) {
+        const float x = __int_as_float(c.z);
+#pragma unroll
+        for (int j = 0; j < V; ++j) o.v[j] = x;
+      } else if (c.x == F_SELECT) {
+        const Vec<V> pr = r[c.z], t = r[c.w], e = r[c.y];
+#pragma unroll
+        for (int j = 0; j < V; ++j) o.v[j] = pr.v[j] != 0.f ? t.v[j] : e.v[j];
       } else {
-        v = run_op(c[0], r[c[2]], r[c[3]]);
+        const Vec<V> a = r[c.z];
+        const Vec<V> b = r[c.w];
+        switch (c.x) {
+          case PFB_ADD: PFB_EW2(x + y)
+          case PFB_SUB: PFB_EW2(x - y)
+          case PFB_MUL: PFB_EW2(x * y)
+          case PFB_DIV: PFB_EW2(x / y)
+          case PFB_MAX: PFB_EW2(np_max(x, y))
+          case PFB_MIN: PFB_EW2(np_min(x, y))
+          case PFB_LESS: PFB_EW2(x < y ? 1.f : 0.f)
+          case PFB_EQUAL: PFB_EW2(x == y ? 1.f : 0.f)
+          case 16 + PFB_NEG: PFB_EW1(-x)
+          case 16 + PFB_EXP: PFB_EW1(expf(x))
+          case 16 + PFB_LOG: PFB_EW1(logf(x))
+          case 16 + PFB_RELU: PFB_EW1(np_max(x, 0.f))
+          case 16 + PFB_TANH: PFB_EW1(tanhf(x))
+          case 16 + PFB_SIGMOID: PFB_EW1(1.f / (1.f + expf(-x)))
+          case 16 + PFB_SQUARE: PFB_EW1(x * x)
+          case 16 + PFB_LOGICAL_NOT: PFB_EW1(x == 0.f ? 1.f : 0.f)
+          case 66: PFB_EW1(x != 0.f ? 1.f : 0.f)  // cast f32 -> bool
+          default: o = a; break;                  // 67: move (cast bool -> f32)
+        }
       }
-      r[c[1]] = v;
+      r[c.y] = o;
     }
-    const float res = r[P.code[P.n_steps - 1][1]];
-    if constexpr (std::is_same<Tout, uint8_t>::value) out[off[0]] = (uint8_t)(res != 0.f);
-    else out[off[0]] = res;
+    const Vec<V> res = r[res_reg];
+    Tout* q = out + off[0];
+    if (V == 4 && (modes & 3) == 0) {
+      if constexpr (std::is_same<Tout, uint8_t>::value)
+        *reinterpret_cast<uchar4*>(q) = make_uchar4(res.v[0] != 0.f, res.v[1] != 0.f,
+                                                    res.v[2] != 0.f, res.v[3] != 0.f);
+      else *reinterpret_cast<float4*>(q) = make_float4(res.v[0], res.v[1], res.v[2], res.v[3]);
+    } else {
+      const int64_t in = L.st[0][ir];
+#pragma unroll
+      for (int j = 0; j < V; ++j) {
+        if constexpr (std::is_same<Tout, uint8_t>::value) q[j * in] = (uint8_t)(res.v[j] != 0.f);
+        else q[j * in] = res.v[j];
+      }
+    }
   }
 }
+#undef PFB_EW1
+#undef PFB_EW2
 
-template <typename IdxT, typename Tout>
-void launch_fused(int n_in, const Layout& L, IdxT n, const FusedProgram& P, Tout* out,
-                  const void* const* p, cudaStream_t s) {
-  const int grid = grid_for((int64_t)n, 256);
-#define PFB_FUSED_CASE(K)                                                                    \
-  case K:                                                                                    \
-    launch(fused_kernel<IdxT, Tout, K>, grid, 256, 0, s, L, n, P, out, p[0], p[1], p[2], p[3],  \
-                                                     p[4], p[5], p[6], p[7]);                \
+template <int V, typename IdxT, typename Tout>
+void launch_fused(int n_in, const Layout& L, IdxT ngroups, const FusedProgram& P, uint32_t modes,
+                  Tout* out, const void* const* p, cudaStream_t s) {
+  const int grid = grid_for((int64_t)ngroups, 256);
+#define PFB_FUSED_CASE(K)                                                                      \
+  case K:                                                                                      \
+    launch(fused_kernel<IdxT, Tout, K, V>, grid, 256, 0, s, L, ngroups, P, modes, out, p[0],   \
+           p[1], p[2], p[3], p[4], p[5], p[6], p[7]);                                          \
     break;
   switch (n_in) {
     PFB_FUSED_CASE(1) PFB_FUSED_CASE(2) PFB_FUSED_CASE(3) PFB_FUSED_CASE(4)
@@ -486,13 +577,24 @@ extern "C" int pfb_fused_ew(int32_t n_in, const pfb_tensor* ins, int32_t n_steps
   for (int k = 0; k < 8; ++k) p[k] = k < n_in ? ins[k].data : nullptr;
   cudaStream_t s = as_stream(stream);
   const bool small = n < (int64_t)0x7fffffff;
-  if (out->dtype == PFB_F32) {
-    if (small) launch_fused<uint32_t, float>(n_in, L, (uint32_t)n, P, (float*)out->data, p, s);
-    else launch_fused<int64_t, float>(n_in, L, n, P, (float*)out->data, p, s);
-  } else {
-    if (small) launch_fused<uint32_t, uint8_t>(n_in, L, (uint32_t)n, P, (uint8_t*)out->data, p, s);
-    else launch_fused<int64_t, uint8_t>(n_in, L, n, P, (uint8_t*)out->data, p, s);
+  const int ir = L.rank - 1;
+  static const bool scalar_only = getenv_flag("PFB_FUSED_SCALAR");
+  const bool v4 = L.shape[ir] % 4 == 0 && !scalar_only;
+  // per-operand feed mode
+  uint32_t modes = 0;
+  for (int o = 0; o <= n_in; ++o) {
+    const void* base = o == 0 ? out->data : ins[o - 1].data;
+    const int dt = o == 0 ? out->dtype : ins[o - 1].dtype;
+    const int64_t esz = dt == PFB_F32 ? 4 : 1;
+    bool vec = v4 && L.st[o][ir] == 1 && (reinterpret_cast<uintptr_t>(base) % (4 * esz)) == 0;
+    for (int d = 0; d < ir && vec; ++d) vec = (L.st[o][d] % 4) == 0;
+    const uint32_t m = (L.st[o][ir] == 0 && o > 0) ? 1u : (vec ? 0u : 2u);
+    modes |= m << (2 * o);
   }
+  const int64_t ng = v4 ? n / 4 : n;
+#define PFB_GO(VV)                                                                                if (out->dtype == PFB_F32) {                                                                      if (small) launch_fused<VV, uint32_t, float>(n_in, L, (uint32_t)ng, P, modes, (float*)out->data, p, s);     else launch_fused<VV, int64_t, float>(n_in, L, ng, P, modes, (float*)out->data, p, s);       } else {                                                                                          if (small) launch_fused<VV, uint32_t, uint8_t>(n_in, L, (uint32_t)ng, P, modes, (uint8_t*)out->data, p, s);     else launch_fused<VV, int64_t, uint8_t>(n_in, L, ng, P, modes, (uint8_t*)out->data, p, s);   }
+  if (v4) { PFB_GO(4) } else { PFB_GO(1) }
+#undef PFB_GO
   return launch_status();
 }
 
@@ -546,4 +648,86 @@ extern "C" int pfb_select(const pfb_tensor* mask, const pfb_tensor* a, const pfb
     case PFB_I64: return select_run<int64_t>(L, n, out, mask, a, b, s);
     default: return select_run<uint8_t>(L, n, out, mask, a, b, s);
   }
+}
+
+// ---------------------------------------------------------------------------
+// concat of up to kMaxCat same-dtype inputs along one axis in one launch
+// (reference tensor.concat, tensor.py:383-393): blockIdx.y picks the input,
+// threads stride over its elements; each input may be any strided view.
+
+namespace pfb {
+constexpr int kMaxCat = 24;
+struct CatDesc {
+  int rank, ax, n;
+  int64_t shape[kMaxRank];      // common shape (axis extent per input below)
+  int64_t ost[kMaxRank];        // output strides
+  const void* x[kMaxCat];
+  int64_t ext[kMaxCat], off[kMaxCat];
+  int64_t xst[kMaxCat][kMaxRank];
+};
+
+template <typename T>
+__global__ void __launch_bounds__(256) concat_kernel(CatDesc d, T* out) {
+  pdl_enter();
+  const int j = blockIdx.y;
+  int64_t numel = 1;
+  for (int i = 0; i < d.rank; ++i) numel *= (i == d.ax ? d.ext[j] : d.shape[i]);
+  const T* x = reinterpret_cast<const T*>(d.x[j]);
+  for (int64_t lin = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; lin < numel;
+       lin += (int64_t)gridDim.x * blockDim.x) {
+    int64_t r = lin, xo = 0, oo = d.off[j] * d.ost[d.ax];
+    for (int i = d.rank - 1; i >= 0; --i) {
+      const int64_t e = (i == d.ax ? d.ext[j] : d.shape[i]);
+      const int64_t q = r / e, c = r - q * e;
+      xo += c * d.xst[j][i];
+      oo += c * d.ost[i];
+      r = q;
+    }
+    out[oo] = __ldg(x + xo);
+  }
+}
+}  // namespace pfb
+
+extern "C" int pfb_concat(int32_t n, const pfb_tensor* xs, int32_t axis, pfb_tensor* out,
+                          void* stream) {
+  using namespace pfb;
+  if (n < 1) return PFB_E_ARG;
+  const int rank = out->rank;
+  if (axis < 0 || axis >= rank) return PFB_E_ARG;
+  cudaStream_t s = as_stream(stream);
+  int64_t off = 0;
+  for (int base = 0; base < n; base += kMaxCat) {
+    CatDesc d;
+    d.rank = rank;
+    d.ax = axis;
+    d.n = std::min(kMaxCat, n - base);
+    int64_t maxel = 0;
+    for (int i = 0; i < rank; ++i) {
+      d.shape[i] = out->shape[i];
+      d.ost[i] = out->stride[i];
+    }
+    for (int j = 0; j < d.n; ++j) {
+      const pfb_tensor* x = &xs[base + j];
+      if (x->dtype != out->dtype) return PFB_E_DTYPE;
+      if (x->rank != rank) return PFB_E_RANK;
+      for (int i = 0; i < rank; ++i)
+        if (i != axis && x->shape[i] != out->shape[i]) return PFB_E_SHAPE;
+      d.x[j] = x->data;
+      d.ext[j] = x->shape[axis];
+      d.off[j] = off;
+      off += x->shape[axis];
+      for (int i = 0; i < rank; ++i) d.xst[j][i] = x->stride[i];
+      maxel = std::max(maxel, numel(x));
+    }
+    if (off > out->shape[axis]) return PFB_E_SHAPE;
+    if (maxel == 0) continue;
+    dim3 grid((unsigned)grid_for(maxel, 256, 4), (unsigned)d.n);
+    switch (out->dtype) {
+      case PFB_F32: launch(concat_kernel<float>, grid, 256, 0, s, d, (float*)out->data); break;
+      case PFB_I64: launch(concat_kernel<int64_t>, grid, 256, 0, s, d, (int64_t*)out->data); break;
+      default: launch(concat_kernel<uint8_t>, grid, 256, 0, s, d, (uint8_t*)out->data); break;
+    }
+  }
+  if (off != out->shape[axis]) return PFB_E_SHAPE;
+  return launch_status();
 }

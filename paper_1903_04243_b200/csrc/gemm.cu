@@ -1,5 +1,6 @@
 // pfb_matmul: validation + path selection (reference tensor.py:195-206).
 #include <algorithm>
+#include <cstdio>
 #include <cstdlib>
 #include <map>
 #include <mutex>
@@ -49,12 +50,47 @@ __global__ void zero_f32(float* p, int64_t n) {
 // CUDA graphs -- reuse the cached choice.  PFB_GEMM_AUTOTUNE=0 uses the model.
 namespace {
 using ShapeKey = std::tuple<int64_t, int64_t, int64_t, int64_t, int, int, int, int, int>;
-std::map<ShapeKey, int> g_choice;  // 1 = SIMT, 2 = tcgen05
+std::map<ShapeKey, int> g_choice;  // 1 = SIMT, 3 = tcgen05 pre-split, 4 = tcgen05 raw feed
 std::mutex g_mu;
 
 ShapeKey key_of(const GemmArgs& g) {
   return ShapeKey(g.batch, g.M, g.N, g.K, g.sak == 1, g.sam == 1, g.sbk == 1, g.sbn == 1,
-                  g.sab == 0 ? 1 : (g.sbb == 0 ? 2 : 0));
+                  (g.sab == 0 ? 1 : (g.sbb == 0 ? 2 : 0)) + 4 * gemm_tcgen05_raw_possible(g));
+}
+
+// PFB_GEMM_TUNE_FILE: persist choices across processes (a profiling run under
+// ncu replays the choices of an unprofiled run instead of re-timing under the
+// profiler).  One line per shape: the 9 key fields and the path.
+const char* tune_file() {
+  static const char* f = getenv("PFB_GEMM_TUNE_FILE");
+  return (f && f[0]) ? f : nullptr;
+}
+
+void load_tune_file() {
+  static bool done = false;
+  if (done) return;
+  done = true;
+  const char* fn = tune_file();
+  if (!fn) return;
+  FILE* f = fopen(fn, "r");
+  if (!f) return;
+  long long v[10];
+  while (fscanf(f, "%lld %lld %lld %lld %lld %lld %lld %lld %lld %lld", &v[0], &v[1], &v[2],
+                &v[3], &v[4], &v[5], &v[6], &v[7], &v[8], &v[9]) == 10)
+    g_choice[ShapeKey(v[0], v[1], v[2], v[3], (int)v[4], (int)v[5], (int)v[6], (int)v[7],
+                      (int)v[8])] = (int)v[9];
+  fclose(f);
+}
+
+void save_choice(const ShapeKey& k, int path) {
+  const char* fn = tune_file();
+  if (!fn) return;
+  FILE* f = fopen(fn, "a");
+  if (!f) return;
+  fprintf(f, "%lld %lld %lld %lld %d %d %d %d %d %d\n", (long long)std::get<0>(k),
+          (long long)std::get<1>(k), (long long)std::get<2>(k), (long long)std::get<3>(k),
+          std::get<4>(k), std::get<5>(k), std::get<6>(k), std::get<7>(k), std::get<8>(k), path);
+  fclose(f);
 }
 
 bool autotune_enabled() {
@@ -65,6 +101,15 @@ bool autotune_enabled() {
   return on;
 }
 
+int run_path(const GemmArgs& g, int path, void* ws, int64_t ws_bytes, cudaStream_t s) {
+  switch (path) {
+    case 1: return gemm_simt(g, ws, ws_bytes, s);
+    case 3: return gemm_tcgen05(g, ws, ws_bytes, s, 1);
+    case 4: return gemm_tcgen05(g, ws, ws_bytes, s, 2);
+    default: return gemm_tcgen05(g, ws, ws_bytes, s, 0);
+  }
+}
+
 float time_path(const GemmArgs& g, int path, void* ws, int64_t ws_bytes, cudaStream_t s) {
   cudaEvent_t e0, e1;
   cudaEventCreate(&e0);
@@ -72,7 +117,7 @@ float time_path(const GemmArgs& g, int path, void* ws, int64_t ws_bytes, cudaStr
   float ms = 1e30f;
   for (int rep = 0; rep < 2; ++rep) {
     cudaEventRecord(e0, s);
-    int rc = path == 2 ? gemm_tcgen05(g, ws, ws_bytes, s) : gemm_simt(g, ws, ws_bytes, s);
+    int rc = run_path(g, path, ws, ws_bytes, s);
     cudaEventRecord(e1, s);
     cudaEventSynchronize(e1);
     if (rc != 0) { ms = 1e30f; break; }
@@ -91,13 +136,55 @@ extern "C" int64_t pfb_matmul_workspace(const pfb_tensor* a, const pfb_tensor* b
   return std::max(gemm_tcgen05_workspace(g), gemm_simt_workspace(g));
 }
 
+static int matmul_impl(GemmArgs& g, pfb_tensor* out, int32_t force_path, void* ws,
+                       int64_t ws_bytes, void* stream);
+
 extern "C" int pfb_matmul_ex(const pfb_tensor* a, const pfb_tensor* b, pfb_tensor* out,
                              const float* alpha_rows, int32_t accumulate, int32_t force_path,
                              void* ws, int64_t ws_bytes, void* stream) {
+  return pfb_matmul_fused(a, b, out, nullptr, nullptr, PFB_ACT_NONE, alpha_rows, accumulate,
+                          force_path, ws, ws_bytes, stream);
+}
+
+extern "C" int pfb_matmul_fused(const pfb_tensor* a, const pfb_tensor* b, pfb_tensor* out,
+                                const pfb_tensor* kscale, const pfb_tensor* bias, int32_t act,
+                                const float* alpha_rows, int32_t accumulate, int32_t force_path,
+                                void* ws, int64_t ws_bytes, void* stream) {
   GemmArgs g;
   if (int e = matmul_args(a, b, out, &g)) return e;
   g.alpha_rows = alpha_rows;
   g.accumulate = accumulate;
+  if (act < PFB_ACT_NONE || act > PFB_ACT_RELU) return PFB_E_ARG;
+  g.act = act;
+  const bool batched = a->rank == 3;
+  if (bias) {
+    if (bias->dtype != PFB_F32) return PFB_E_DTYPE;
+    int64_t st[3];
+    if (!broadcast_strides(bias, out->rank, out->shape, st)) return PFB_E_SHAPE;
+    g.bias = (const float*)bias->data;
+    if (batched) { g.sxb = st[0]; g.sxm = st[1]; g.sxn = st[2]; }
+    else { g.sxb = 0; g.sxm = st[0]; g.sxn = st[1]; }
+  }
+  if (kscale) {
+    if (kscale->dtype != PFB_F32) return PFB_E_DTYPE;
+    const int64_t shp[2] = {g.batch, g.K};
+    int64_t st[2];
+    if (batched) {
+      if (!broadcast_strides(kscale, 2, shp, st)) return PFB_E_SHAPE;
+      g.skb = st[0]; g.skk = st[1];
+    } else {
+      if (!broadcast_strides(kscale, 1, shp + 1, st)) return PFB_E_SHAPE;
+      g.skb = 0; g.skk = st[0];
+    }
+    g.kscale = (const float*)kscale->data;
+  }
+  if (g.K == 0 && (g.has_epi() || g.kscale)) return PFB_E_UNSUPPORTED;
+  return matmul_impl(g, out, force_path, ws, ws_bytes, stream);
+}
+
+static int matmul_impl(GemmArgs& g, pfb_tensor* out, int32_t force_path, void* ws,
+                       int64_t ws_bytes, void* stream) {
+  const int accumulate = g.accumulate;
   cudaStream_t s = as_stream(stream);
   if (g.batch == 0 || g.M == 0 || g.N == 0) return 0;
   if (g.K == 0) {
@@ -107,11 +194,11 @@ extern "C" int pfb_matmul_ex(const pfb_tensor* a, const pfb_tensor* b, pfb_tenso
     launch(zero_f32, grid_for(n, 256), 256, 0, s, (float*)out->data, n);
     return launch_status();
   }
-  // force_path: 0 = auto, 1 = SIMT, 2 = tcgen05 (error if ineligible).
+  // force_path: 0 = auto, 1 = SIMT, 2 = tcgen05 (error if ineligible),
+  // 3 = tcgen05 with pre-split operands, 4 = tcgen05 with the raw TMA feed.
   // PFB_DISABLE_TCGEN05=1 pins auto to SIMT (A/B testing, bring-up).
   static const bool tc_off = getenv("PFB_DISABLE_TCGEN05") && getenv("PFB_DISABLE_TCGEN05")[0] == '1';
-  if (force_path == 1) return gemm_simt(g, ws, ws_bytes, s);
-  if (force_path == 2) return gemm_tcgen05(g, ws, ws_bytes, s);
+  if (force_path >= 1 && force_path <= 4) return run_path(g, force_path, ws, ws_bytes, s);
   const bool tc_ok = !tc_off && gemm_tcgen05_eligible(g) &&
                      ws_bytes >= gemm_tcgen05_workspace(g) && ws != nullptr &&
                      (double)g.batch * g.M * g.N * g.K >= (double)(1 << 20);
@@ -119,6 +206,7 @@ extern "C" int pfb_matmul_ex(const pfb_tensor* a, const pfb_tensor* b, pfb_tenso
   int path = 0;
   {
     std::lock_guard<std::mutex> lk(g_mu);
+    load_tune_file();
     auto it = g_choice.find(key_of(g));
     if (it != g_choice.end()) path = it->second;
   }
@@ -126,18 +214,26 @@ extern "C" int pfb_matmul_ex(const pfb_tensor* a, const pfb_tensor* b, pfb_tenso
     cudaStreamCaptureStatus st = cudaStreamCaptureStatusNone;
     cudaStreamIsCapturing(s, &st);
     if (autotune_enabled() && !accumulate && st == cudaStreamCaptureStatusNone) {
-      const float t_simt = time_path(g, 1, ws, ws_bytes, s);
-      const float t_tc = time_path(g, 2, ws, ws_bytes, s);  // leaves C computed
-      path = t_tc < t_simt ? 2 : 1;
-      std::lock_guard<std::mutex> lk(g_mu);
-      g_choice[key_of(g)] = path;
-      if (path == 2) return launch_status();  // C already holds the tcgen05 result
-      return gemm_simt(g, ws, ws_bytes, s);
+      // every candidate runs twice; the last one timed leaves C computed
+      int cand[3] = {1, 3, 4};
+      const int ncand = gemm_tcgen05_raw_possible(g) ? 3 : 2;
+      float best = 1e30f;
+      for (int i = 0; i < ncand; ++i) {
+        const float t = time_path(g, cand[i], ws, ws_bytes, s);
+        if (t < best) { best = t; path = cand[i]; }
+      }
+      {
+        std::lock_guard<std::mutex> lk(g_mu);
+        g_choice[key_of(g)] = path;
+        save_choice(key_of(g), path);
+      }
+      if (path == cand[ncand - 1]) return launch_status();
+      return run_path(g, path, ws, ws_bytes, s);
     }
     path = gemm_tcgen05_profitable(g) ? 2 : 1;
   }
-  if (path == 2) {
-    int e = gemm_tcgen05(g, ws, ws_bytes, s);
+  if (path != 1) {
+    int e = run_path(g, path, ws, ws_bytes, s);
     if (e != PFB_E_UNSUPPORTED) return e;
   }
   return gemm_simt(g, ws, ws_bytes, s);

@@ -15,14 +15,45 @@ struct GemmArgs {
   int64_t scb, scm, scn;
   const float* alpha_rows;  // nullable: C[m, :] *= alpha_rows[b*M + m]
   int accumulate;           // C += result
+  // fused prologue / epilogue (passes.fuse_matmul_epilogues):
+  //   C = act(alpha * (A diag(kscale) B) [+ C] + bias)
+  const float* kscale = nullptr;  // nullable, per (batch, k): scales B's rows
+  int64_t skb = 0, skk = 0;
+  const float* bias = nullptr;    // nullable, broadcast to (batch, M, N) by strides
+  int64_t sxb = 0, sxm = 0, sxn = 0;
+  int act = 0;                    // PFB_ACT_*
+  __host__ __device__ bool has_epi() const { return bias != nullptr || act != 0; }
 };
+
+__device__ __forceinline__ float apply_act(int act, float v) {
+  switch (act) {
+    case PFB_ACT_TANH: return tanhf(v);
+    case PFB_ACT_SIGMOID: return 1.f / (1.f + expf(-v));
+    case PFB_ACT_RELU: return v != v ? v : (v >= 0.f ? v : 0.f);
+    default: return v;
+  }
+}
+
+// bias + activation on a finished output value
+__device__ __forceinline__ float epi_value(const GemmArgs& g, int64_t b, int64_t m, int64_t n,
+                                           float v) {
+  if (g.bias) v += __ldg(g.bias + b * g.sxb + m * g.sxm + n * g.sxn);
+  return apply_act(g.act, v);
+}
+
+__device__ __forceinline__ float kscale_at(const GemmArgs& g, int64_t b, int64_t k) {
+  return g.kscale ? __ldg(g.kscale + b * g.skb + k * g.skk) : 1.f;
+}
 
 int gemm_simt(const GemmArgs& g, void* ws, int64_t ws_bytes, cudaStream_t s);
 int64_t gemm_simt_workspace(const GemmArgs& g);
 // returns PFB_E_UNSUPPORTED when the shape/layout is not eligible
-int gemm_tcgen05(const GemmArgs& g, void* ws, int64_t ws_bytes, cudaStream_t s);
+// variant: 0 = auto, 1 = operands pre-split by split_kernel, 2 = raw operands
+// fed by TMA and split in shared memory wherever the layout allows it
+int gemm_tcgen05(const GemmArgs& g, void* ws, int64_t ws_bytes, cudaStream_t s, int variant = 0);
 int64_t gemm_tcgen05_workspace(const GemmArgs& g);
 bool gemm_tcgen05_eligible(const GemmArgs& g);    // layout constraints
+bool gemm_tcgen05_raw_possible(const GemmArgs& g);
 bool gemm_tcgen05_profitable(const GemmArgs& g);  // size heuristic for auto
 
 }  // namespace pfb

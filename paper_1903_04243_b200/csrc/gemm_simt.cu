@@ -30,6 +30,10 @@ __device__ __forceinline__ void store_row4(const GemmArgs& g, int64_t b, int64_t
       float4 c = *reinterpret_cast<float4*>(p);
       o.x += c.x; o.y += c.y; o.z += c.z; o.w += c.w;
     }
+    if (g.has_epi()) {
+      o.x = epi_value(g, b, m, n, o.x); o.y = epi_value(g, b, m, n + 1, o.y);
+      o.z = epi_value(g, b, m, n + 2, o.z); o.w = epi_value(g, b, m, n + 3, o.w);
+    }
     *reinterpret_cast<float4*>(p) = o;
     return;
   }
@@ -37,14 +41,16 @@ __device__ __forceinline__ void store_row4(const GemmArgs& g, int64_t b, int64_t
   for (int j = 0; j < 4; ++j) {
     if (n + j >= g.N) break;
     float* q = p + j * g.scn;
-    const float x = v[j] * alpha;
-    *q = g.accumulate ? *q + x : x;
+    float x = v[j] * alpha;
+    if (g.accumulate) x += *q;
+    *q = epi_value(g, b, m, n + j, x);
   }
 }
 
 // partials: nullptr -> epilogue straight to C; else ws[split][b][M][N].
 // Register-staged double buffering: the next k-tile's global loads are issued
 // before the current tile's FMAs, so the loop is not load-latency bound.
+template <bool KS>
 __global__ void __launch_bounds__(256) gemm_simt_kernel(GemmArgs g, int splits, int64_t kchunk,
                                                         float* partials) {
   pdl_enter();
@@ -76,6 +82,7 @@ __global__ void __launch_bounds__(256) gemm_simt_kernel(GemmArgs g, int splits, 
       ra[j] = (gm < g.M && gk < kend) ? __ldg(A + gm * g.sam + gk * g.sak) : 0.f;
       const int64_t gk2 = k0 + bk[j], gn = n0 + bn[j];
       rb[j] = (gk2 < kend && gn < g.N) ? __ldg(B + gk2 * g.sbk + gn * g.sbn) : 0.f;
+      if (KS && gk2 < kend) rb[j] *= __ldg(g.kscale + bz * g.skb + gk2 * g.skk);
     }
   };
   if (kbeg < kend) load(kbeg);
@@ -134,7 +141,8 @@ __global__ void __launch_bounds__(256) splitk_reduce(GemmArgs g, int splits, con
     const uint32_t m = r / N, n = r - m * N;
     if (g.alpha_rows) s *= g.alpha_rows[(size_t)b * g.M + m];
     float* p = g.C + b * g.scb + m * g.scm + n * g.scn;
-    *p = g.accumulate ? *p + s : s;
+    if (g.accumulate) s += *p;
+    *p = epi_value(g, b, m, n, s);
   }
 }
 
@@ -152,7 +160,7 @@ __global__ void __launch_bounds__(256) gemm_smallk_kernel(GemmArgs g) {
     float av[16];
     const float* a = g.A + b * g.sab + m * g.sam;
 #pragma unroll
-    for (int k = 0; k < 16; ++k) av[k] = k < g.K ? __ldg(a + k * g.sak) : 0.f;
+    for (int k = 0; k < 16; ++k) av[k] = k < g.K ? __ldg(a + k * g.sak) * kscale_at(g, b, k) : 0.f;
     const float alpha = g.alpha_rows ? g.alpha_rows[row] : 1.f;
     const float* bb = g.B + b * g.sbb;
     float* crow = g.C + b * g.scb + m * g.scm;
@@ -171,10 +179,13 @@ __global__ void __launch_bounds__(256) gemm_smallk_kernel(GemmArgs g) {
         if (g.accumulate) {
           const float4 c = *dst;
           o.x += c.x; o.y += c.y; o.z += c.z; o.w += c.w;
-          *dst = o;
-        } else {
-          __stcs(dst, o);  // write-once output (jacobian rows): streaming store
         }
+        if (g.has_epi()) {
+          o.x = epi_value(g, b, m, n, o.x); o.y = epi_value(g, b, m, n + 1, o.y);
+          o.z = epi_value(g, b, m, n + 2, o.z); o.w = epi_value(g, b, m, n + 3, o.w);
+        }
+        if (g.accumulate) *dst = o;
+        else __stcs(dst, o);  // write-once output (jacobian rows): streaming store
       } else {
         for (int k = 0; k < g.K; ++k) {
           const float* bk = bb + k * g.sbk + n * g.sbn;
@@ -202,17 +213,22 @@ __global__ void __launch_bounds__(256) outer1_kernel(GemmArgs g, int64_t rows_pe
   int64_t b = r0 / g.M, m = r0 - b * g.M;
   float4 bv = __ldg(reinterpret_cast<const float4*>(g.B + b * g.sbb) + q);
   for (int64_t r = r0; r < r1; ++r) {
-    const float av = __ldg(g.A + b * g.sab + m * g.sam) *
-                     (g.alpha_rows ? g.alpha_rows[r] : 1.f);
+    const float av = __ldg(g.A + b * g.sab + m * g.sam) * kscale_at(g, b, 0);
+    const float alpha = g.alpha_rows ? g.alpha_rows[r] : 1.f;
     float4* dst = reinterpret_cast<float4*>(g.C + b * g.scb + m * g.scm) + q;
-    float4 o = make_float4(av * bv.x, av * bv.y, av * bv.z, av * bv.w);
+    float4 o = make_float4(av * bv.x * alpha, av * bv.y * alpha, av * bv.z * alpha,
+                           av * bv.w * alpha);
     if (g.accumulate) {
       const float4 c = *dst;
       o.x += c.x; o.y += c.y; o.z += c.z; o.w += c.w;
-      *dst = o;
-    } else {
-      __stcs(dst, o);
     }
+    if (g.has_epi()) {
+      const int64_t n = 4 * q;
+      o.x = epi_value(g, b, m, n, o.x); o.y = epi_value(g, b, m, n + 1, o.y);
+      o.z = epi_value(g, b, m, n + 2, o.z); o.w = epi_value(g, b, m, n + 3, o.w);
+    }
+    if (g.accumulate) *dst = o;
+    else __stcs(dst, o);
     if (++m == g.M) {
       m = 0;
       ++b;
@@ -269,7 +285,10 @@ int gemm_simt(const GemmArgs& g, void* ws, int64_t ws_bytes, cudaStream_t s) {
   dim3 grid((unsigned)((g.N + BN - 1) / BN), (unsigned)((g.M + BM - 1) / BM),
             (unsigned)(g.batch * splits));
   if (grid.y > 65535 || grid.z > 65535) return PFB_E_UNSUPPORTED;
-  launch(gemm_simt_kernel, grid, 256, 0, s, g, splits, kchunk, splits > 1 ? (float*)ws : nullptr);
+  if (g.kscale)
+    launch(gemm_simt_kernel<true>, grid, 256, 0, s, g, splits, kchunk, splits > 1 ? (float*)ws : nullptr);
+  else
+    launch(gemm_simt_kernel<false>, grid, 256, 0, s, g, splits, kchunk, splits > 1 ? (float*)ws : nullptr);
   if (splits > 1)
     launch(splitk_reduce, grid_for(g.batch * g.M * g.N, 256), 256, 0, s, g, splits, (const float*)ws);
   return launch_status();

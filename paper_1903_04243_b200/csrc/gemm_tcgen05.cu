@@ -104,18 +104,19 @@ __device__ __forceinline__ uint64_t smem_desc_sw128(uint32_t addr) {
   return d;
 }
 
-// kind::tf32, D=f32, K-major A and B, M=128, N=BN
+// kind::tf32, D=f32, M=128, N=BN; bit 15/16 = A/B MN-major (set per call)
 constexpr uint32_t kIdesc = (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(BN >> 3) << 17) |
                             ((uint32_t)(BM >> 4) << 24);
 
-__device__ __forceinline__ void mma_tf32(uint32_t tmem_d, uint64_t da, uint64_t db, uint32_t acc) {
+__device__ __forceinline__ void mma_tf32(uint32_t tmem_d, uint64_t da, uint64_t db, uint32_t idesc,
+                                         uint32_t acc) {
   asm volatile(
       "{\n\t"
       ".reg .pred p;\n\t"
       "setp.ne.b32 p, %4, 0;\n\t"
       "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n\t"
       "}" ::"r"(tmem_d),
-      "l"(da), "l"(db), "r"(kIdesc), "r"(acc));
+      "l"(da), "l"(db), "r"(idesc), "r"(acc));
 }
 
 __device__ __forceinline__ void mma_commit(uint64_t* bar) {
@@ -150,7 +151,9 @@ __device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t* r) {
 __global__ void __launch_bounds__(256) split_kernel(const float* __restrict__ x, int64_t rows,
                                                     int64_t K, int64_t Kp, int64_t sb, int64_t sr,
                                                     int64_t sk, float* __restrict__ hi,
-                                                    float* __restrict__ lo) {
+                                                    float* __restrict__ lo,
+                                                    const float* __restrict__ kscale,
+                                                    int64_t skb, int64_t skk) {
   pdl_enter();
   __shared__ float t[32][33];
   const int64_t b = blockIdx.z;
@@ -163,6 +166,7 @@ __global__ void __launch_bounds__(256) split_kernel(const float* __restrict__ x,
     int64_t r, k;
     if (rows_fast) { r = r0 + tx; k = k0 + ty + j; } else { r = r0 + ty + j; k = k0 + tx; }
     float v = (r < rows && k < K) ? __ldg(xb + r * sr + k * sk) : 0.f;
+    if (kscale && k < K) v *= __ldg(kscale + b * skb + k * skk);
     if (rows_fast) t[ty + j][tx] = v; else t[tx][ty + j] = v;  // t[k - k0][r - r0]
   }
   __syncthreads();
@@ -180,18 +184,110 @@ __global__ void __launch_bounds__(256) split_kernel(const float* __restrict__ x,
   }
 }
 
+// Operand feed modes (per operand, chosen on the host):
+//   kPreSplit: dense K-major hi/lo planes written by split_kernel (any view)
+//   kRawK:     the operand itself, K contiguous -- one TMA box per stage
+//   kRawMN:    the operand itself, M/N contiguous -- four 32-wide TMA boxes,
+//              consumed by the MMA as an MN-major smem operand
+// Raw tiles are split in shared memory by the accumulator warps (hi written
+// in place, lo beside it), so small GEMMs need no extra launches.
+enum { kPreSplit = 0, kRawK = 1, kRawMN = 2 };
+
 struct Params {
   int M, N, K, batch;
   int ntm, ntn;
-  int a_bcast, b_bcast;  // operand shared across the batch (split once)
+  int a_bcast, b_bcast;  // operand shared across the batch
+  int a_mode, b_mode;
+  uint32_t idesc;
   float* C;
   int64_t scb, scm, scn;
   const float* alpha_rows;
   int accumulate;
-  int ksplit;            // >1: work unit = (tile, k-range); partial tiles -> `partials`
+  int ksplit;            // >1: a cluster of `ksplit` CTAs per tile, DSMEM reduction
   int kb_per_split;      // k-blocks per split (multiple of CHUNK_KB)
-  float* partials;       // [ksplit][batch][M][N] when ksplit > 1
+  const float* bias;     // fused epilogue: + bias (broadcast strides), activation
+  int64_t sxb, sxm, sxn;
+  int act;
+  uint32_t mn_lbo, mn_sbo;  // MN-major descriptor strides (4 KB, 512 B)
 };
+
+__device__ __forceinline__ void epi4(const Params& p, int bz, int row, int col, float4& v) {
+  if (p.bias == nullptr && p.act == 0) return;
+  float e[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    if (p.bias && col + j < p.N)
+      e[j] += __ldg(p.bias + (int64_t)bz * p.sxb + (int64_t)row * p.sxm + (int64_t)(col + j) * p.sxn);
+    e[j] = apply_act(p.act, e[j]);
+  }
+  v = make_float4(e[0], e[1], e[2], e[3]);
+}
+
+__device__ __forceinline__ uint32_t cluster_rank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+
+__device__ __forceinline__ void cluster_sync_all() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::
+                   : "memory");
+}
+
+__device__ __forceinline__ float4 ld_dsmem_f4(uint32_t local_addr, uint32_t rank) {
+  uint32_t remote;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(remote) : "r"(local_addr), "r"(rank));
+  float4 v;
+  asm volatile("ld.shared::cluster.v4.f32 {%0, %1, %2, %3}, [%4];"
+               : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w)
+               : "r"(remote)
+               : "memory");
+  return v;
+}
+
+// MN-major tf32 operand: the UMMA only takes the 128B swizzle with 32-byte
+// atomicity for MN-major 32-bit types (layout type 1, "128B_BASE32B"; TMA
+// CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B).  Tile = 32-wide MN groups (LBO =
+// 4 KB apart) of 32 K rows x 128 B; swizzle atoms of 4 K rows (SBO = 512 B).
+// One UMMA k-step (8 of K) = two atoms = +1 KB.
+__device__ __forceinline__ uint64_t smem_desc_mn_sw128(uint32_t addr, uint32_t lbo = 4096,
+                                                      uint32_t sbo = 512) {
+  uint64_t d = 0;
+  d |= (uint64_t)((addr & 0x3FFFF) >> 4);
+  d |= (uint64_t)(lbo >> 4) << 16;                 // LBO: next 32-wide MN group
+  d |= (uint64_t)(sbo >> 4) << 32;                 // SBO: next 4-row K atom
+  d |= (uint64_t)1 << 46;
+  d |= (uint64_t)1 << 61;                          // SWIZZLE_128B_BASE32B
+  return d;
+}
+
+__device__ __forceinline__ void tma_load_operand(const CUtensorMap* mh, const CUtensorMap* ml,
+                                                 int mode, uint64_t* bar, uint8_t* dst_hi,
+                                                 uint8_t* dst_lo, int kb, int row0, int z) {
+  if (mode == kRawMN) {
+#pragma unroll
+    for (int j = 0; j < BM / 32; ++j) tma_load_3d(mh, bar, dst_hi + j * 4096, row0 + 32 * j, kb * BK, z);
+  } else {
+    tma_load_3d(mh, bar, dst_hi, kb * BK, row0, z);
+    if (mode == kPreSplit) tma_load_3d(ml, bar, dst_lo, kb * BK, row0, z);
+  }
+}
+
+// hi = rn_tf32(x) in place, lo = rn_tf32(x - hi); elementwise, so the TMA
+// swizzle is preserved.  256 threads, 16 KB tile: 4 float4 per thread.
+__device__ __forceinline__ void split_tile_smem(uint8_t* hi, uint8_t* lo, int t) {
+  float4* h4 = reinterpret_cast<float4*>(hi);
+  float4* l4 = reinterpret_cast<float4*>(lo);
+#pragma unroll
+  for (int i = 0; i < TILE_BYTES / 16 / (32 * EPI_WARPS); ++i) {
+    const int idx = t + i * 32 * EPI_WARPS;
+    float4 v = h4[idx];
+    float4 h = make_float4(to_tf32(v.x), to_tf32(v.y), to_tf32(v.z), to_tf32(v.w));
+    l4[idx] = make_float4(to_tf32(v.x - h.x), to_tf32(v.y - h.y), to_tf32(v.z - h.z),
+                          to_tf32(v.w - h.w));
+    h4[idx] = h;
+  }
+}
 
 __global__ void __launch_bounds__(NUM_THREADS, 1)
 gemm_kernel(const __grid_constant__ CUtensorMap map_ah, const __grid_constant__ CUtensorMap map_al,
@@ -202,16 +298,21 @@ gemm_kernel(const __grid_constant__ CUtensorMap map_ah, const __grid_constant__ 
   uint8_t* smem = reinterpret_cast<uint8_t*>(
       (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + STAGES * STAGE_BYTES);
-  uint64_t* full = bars;                   // [STAGES] TMA -> MMA
+  uint64_t* full = bars;                   // [STAGES] TMA -> (split) -> MMA
   uint64_t* empty = bars + STAGES;         // [STAGES] MMA -> TMA
-  uint64_t* acc_full = bars + 2 * STAGES;  // [2] MMA -> accumulators
+  uint64_t* ready = bars + 2 * STAGES;     // [STAGES] smem split -> MMA
+  uint64_t* acc_full = bars + 3 * STAGES;  // [2] MMA -> accumulators
   uint64_t* acc_empty = acc_full + 2;      // [2] accumulators -> MMA
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_empty + 2);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int nk = (p.K + BK - 1) / BK;
   const int tiles_per_batch = p.ntm * p.ntn;
-  const int ntiles = tiles_per_batch * p.batch * p.ksplit;  // work units
+  const bool clustered = p.ksplit > 1;
+  // clustered: exactly one work unit per CTA (cluster rank = k-split index)
+  const int ntiles = clustered ? (int)blockIdx.x + 1 : tiles_per_batch * p.batch * p.ksplit;
+  const int ustride = clustered ? 1 : (int)gridDim.x;
+  const bool split_smem = p.a_mode != kPreSplit || p.b_mode != kPreSplit;
 
   auto tile = [&](int s, int which) { return smem + s * STAGE_BYTES + which * TILE_BYTES; };
   // which: 0 = A_hi, 1 = A_lo, 2 = B_hi, 3 = B_lo
@@ -220,6 +321,7 @@ gemm_kernel(const __grid_constant__ CUtensorMap map_ah, const __grid_constant__ 
     for (int s = 0; s < STAGES; ++s) {
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], 1);
+      mbar_init(&ready[s], EPI_WARPS);
     }
     for (int b = 0; b < 2; ++b) {
       mbar_init(&acc_full[b], 1);
@@ -238,6 +340,9 @@ gemm_kernel(const __grid_constant__ CUtensorMap map_ah, const __grid_constant__ 
   asm volatile("tcgen05.fence::after_thread_sync;");
   const uint32_t tmem_base = *tmem_slot;
 
+  const int bytes_a = (p.a_mode == kPreSplit ? 2 : 1) * TILE_BYTES;
+  const int bytes_b = (p.b_mode == kPreSplit ? 2 : 1) * TILE_BYTES;
+
   if (warp == 0) {
     if (lane == 0) {
       asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&map_ah)) : "memory");
@@ -245,7 +350,7 @@ gemm_kernel(const __grid_constant__ CUtensorMap map_ah, const __grid_constant__ 
       asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&map_bh)) : "memory");
       asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&map_bl)) : "memory");
       int g = 0;
-      for (int u = blockIdx.x; u < ntiles; u += gridDim.x) {
+      for (int u = blockIdx.x; u < ntiles; u += ustride) {
         const int t = u / p.ksplit, ks = u % p.ksplit;
         const int bz = t / tiles_per_batch, r = t % tiles_per_batch;
         const int m0 = (r / p.ntn) * BM, n0 = (r % p.ntn) * BN;
@@ -254,18 +359,16 @@ gemm_kernel(const __grid_constant__ CUtensorMap map_ah, const __grid_constant__ 
         for (int kb = kb0; kb < kb1; ++kb, ++g) {
           const int s = g % STAGES;
           if (g >= STAGES) mbar_wait(&empty[s], ((g / STAGES) - 1) & 1);
-          mbar_expect_tx(&full[s], 4 * TILE_BYTES);
-          tma_load_3d(&map_ah, &full[s], tile(s, 0), kb * BK, m0, za);
-          tma_load_3d(&map_al, &full[s], tile(s, 1), kb * BK, m0, za);
-          tma_load_3d(&map_bh, &full[s], tile(s, 2), kb * BK, n0, zb);
-          tma_load_3d(&map_bl, &full[s], tile(s, 3), kb * BK, n0, zb);
+          mbar_expect_tx(&full[s], bytes_a + bytes_b);
+          tma_load_operand(&map_ah, &map_al, p.a_mode, &full[s], tile(s, 0), tile(s, 1), kb, m0, za);
+          tma_load_operand(&map_bh, &map_bl, p.b_mode, &full[s], tile(s, 2), tile(s, 3), kb, n0, zb);
         }
       }
     }
   } else if (warp == 1) {
     if (lane == 0) {
       int g = 0, gc = 0;
-      for (int u = blockIdx.x; u < ntiles; u += gridDim.x) {
+      for (int u = blockIdx.x; u < ntiles; u += ustride) {
         const int ks = u % p.ksplit;
         const int kb0 = ks * p.kb_per_split, kb1 = min(nk, kb0 + p.kb_per_split);
         const int uchunks = (kb1 - kb0 + CHUNK_KB - 1) / CHUNK_KB;
@@ -278,19 +381,26 @@ gemm_kernel(const __grid_constant__ CUtensorMap map_ah, const __grid_constant__ 
           const int kb_end = min(kb1, kb_beg + CHUNK_KB);
           for (int kb = kb_beg; kb < kb_end; ++kb, ++g) {
             const int s = g % STAGES;
-            mbar_wait(&full[s], (g / STAGES) & 1);
+            mbar_wait(split_smem ? &ready[s] : &full[s], (g / STAGES) & 1);
             asm volatile("tcgen05.fence::after_thread_sync;");
-            const uint64_t a_hi = smem_desc_sw128(smem_u32(tile(s, 0)));
-            const uint64_t a_lo = smem_desc_sw128(smem_u32(tile(s, 1)));
-            const uint64_t b_hi = smem_desc_sw128(smem_u32(tile(s, 2)));
-            const uint64_t b_lo = smem_desc_sw128(smem_u32(tile(s, 3)));
+            const uint32_t a0 = smem_u32(tile(s, 0)), a1 = smem_u32(tile(s, 1));
+            const uint32_t b0 = smem_u32(tile(s, 2)), b1 = smem_u32(tile(s, 3));
+            const bool amn = p.a_mode == kRawMN, bmn = p.b_mode == kRawMN;
+            const uint64_t a_hi = amn ? smem_desc_mn_sw128(a0, p.mn_lbo, p.mn_sbo) : smem_desc_sw128(a0);
+            const uint64_t a_lo = amn ? smem_desc_mn_sw128(a1, p.mn_lbo, p.mn_sbo) : smem_desc_sw128(a1);
+            const uint64_t b_hi = bmn ? smem_desc_mn_sw128(b0, p.mn_lbo, p.mn_sbo) : smem_desc_sw128(b0);
+            const uint64_t b_lo = bmn ? smem_desc_mn_sw128(b1, p.mn_lbo, p.mn_sbo) : smem_desc_sw128(b1);
+            // k-step advance: +32 B inside the swizzle row (K-major) or one
+            // 1 KB atom (MN-major)
+            const uint64_t astep = amn ? (1024 >> 4) : ((UMMA_K * 4) >> 4);
+            const uint64_t bstep = bmn ? (1024 >> 4) : ((UMMA_K * 4) >> 4);
 #pragma unroll
             for (int k = 0; k < BK / UMMA_K; ++k) {
-              const uint64_t adv = (uint64_t)((k * UMMA_K * 4) >> 4);  // +32 B along K
+              const uint64_t da = astep * k, db = bstep * k;
               const uint32_t acc = (kb > kb_beg || k > 0) ? 1u : 0u;
-              mma_tf32(tmem_d, a_hi + adv, b_hi + adv, acc);
-              mma_tf32(tmem_d, a_hi + adv, b_lo + adv, 1u);
-              mma_tf32(tmem_d, a_lo + adv, b_hi + adv, 1u);
+              mma_tf32(tmem_d, a_hi + da, b_hi + db, p.idesc, acc);
+              mma_tf32(tmem_d, a_hi + da, b_lo + db, p.idesc, 1u);
+              mma_tf32(tmem_d, a_lo + da, b_hi + db, p.idesc, 1u);
             }
             mma_commit(&empty[s]);
           }
@@ -300,45 +410,78 @@ gemm_kernel(const __grid_constant__ CUtensorMap map_ah, const __grid_constant__ 
     }
     __syncwarp();
   } else {
-    // ---- accumulators + epilogue (warps 2..9): warp w owns TMEM lanes
-    // 32*(w%4)..+31 (its rows) and columns [half*64, half*64+64) ----
+    // ---- split + accumulators + epilogue (warps 2..9): warp w owns TMEM
+    // lanes 32*(w%4)..+31 (its rows) and columns [half*64, half*64+64) ----
     const int quarter = warp & 3;
     const int half = (warp - 2) >> 2;
+    const int et = threadIdx.x - 64;  // 0..255
     float* stage = reinterpret_cast<float*>(smem + STAGES * STAGE_BYTES + 256) +
                    (warp - 2) * EPI_STAGE_FLOATS;
-    int gc = 0;
-    for (int u = blockIdx.x; u < ntiles; u += gridDim.x) {
+    int gc = 0, gs = 0;
+    auto split_stage = [&]() {
+      const int s = gs % STAGES;
+      mbar_wait(&full[s], (gs / STAGES) & 1);
+      if (p.a_mode != kPreSplit) split_tile_smem(tile(s, 0), tile(s, 1), et);
+      if (p.b_mode != kPreSplit) split_tile_smem(tile(s, 2), tile(s, 3), et);
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&ready[s]);
+      ++gs;
+    };
+    float acc[EPI_COLS];
+    auto drain = [&]() {
+      const int buf = gc & 1;
+      mbar_wait(&acc_full[buf], (gc >> 1) & 1);
+      asm volatile("tcgen05.fence::after_thread_sync;");
+#pragma unroll
+      for (int cc = 0; cc < EPI_COLS; cc += 32) {
+        uint32_t v[32];
+        tmem_ld32(tmem_base + ((uint32_t)(quarter * 32) << 16) +
+                      (uint32_t)(buf * BN + half * EPI_COLS + cc), v);
+        asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+        for (int j = 0; j < 32; ++j) acc[cc + j] += __uint_as_float(v[j]);
+      }
+      asm volatile("tcgen05.fence::before_thread_sync;");
+      mbar_arrive(&acc_empty[buf]);
+      ++gc;
+    };
+    for (int u = blockIdx.x; u < ntiles; u += ustride) {
       const int t = u / p.ksplit, ks = u % p.ksplit;
       const int bz = t / tiles_per_batch, r = t % tiles_per_batch;
       const int m0 = (r / p.ntn) * BM, n0 = (r % p.ntn) * BN;
       const int kb0 = ks * p.kb_per_split, kb1 = min(nk, kb0 + p.kb_per_split);
       const int uchunks = (kb1 - kb0 + CHUNK_KB - 1) / CHUNK_KB;
-      float acc[EPI_COLS];
 #pragma unroll
       for (int j = 0; j < EPI_COLS; ++j) acc[j] = 0.f;
-      for (int c = 0; c < uchunks; ++c, ++gc) {
-        const int buf = gc & 1;
-        mbar_wait(&acc_full[buf], (gc >> 1) & 1);
-        asm volatile("tcgen05.fence::after_thread_sync;");
-#pragma unroll
-        for (int cc = 0; cc < EPI_COLS; cc += 32) {
-          uint32_t v[32];
-          tmem_ld32(tmem_base + ((uint32_t)(quarter * 32) << 16) +
-                        (uint32_t)(buf * BN + half * EPI_COLS + cc), v);
-          asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-#pragma unroll
-          for (int j = 0; j < 32; ++j) acc[cc + j] += __uint_as_float(v[j]);
+      // split chunk c's stages, then drain chunk c-1 (the MMA works on
+      // chunk c-1 while the stages of chunk c are being split)
+      for (int c = 0; c < uchunks; ++c) {
+        if (split_smem) {
+          const int kb_beg = kb0 + c * CHUNK_KB, kb_end = min(kb1, kb_beg + CHUNK_KB);
+          for (int kb = kb_beg; kb < kb_end; ++kb) split_stage();
         }
-        asm volatile("tcgen05.fence::before_thread_sync;");
-        mbar_arrive(&acc_empty[buf]);
+        if (c > 0) drain();
+      }
+      drain();
+      if (clustered) {
+        // partial tile -> own smem (stage area is idle: every MMA of this
+        // CTA's only unit has completed), rows x 32 float4, XOR-swizzled
+        float* red = reinterpret_cast<float*>(smem);
+        const int row = quarter * 32 + lane;
+#pragma unroll
+        for (int j = 0; j < EPI_COLS / 4; ++j) {
+          const int ch = half * (EPI_COLS / 4) + j;
+          *reinterpret_cast<float4*>(red + row * BN + 4 * (ch ^ (row & 7))) =
+              make_float4(acc[4 * j], acc[4 * j + 1], acc[4 * j + 2], acc[4 * j + 3]);
+        }
+        continue;
       }
       // 32x32 blocks through smem: each lane writes its row as float4s, then
       // every store instruction covers 4 rows x 128 contiguous bytes
       const int row0 = m0 + quarter * 32;
-      const bool partial = p.ksplit > 1;  // dense partial tile, epilogue in the reduction
-      float* cbase = partial ? p.partials + ((int64_t)ks * p.batch + bz) * p.M * p.N
-                             : p.C + bz * p.scb;
-      const int64_t ldm = partial ? p.N : p.scm, ldn = partial ? 1 : p.scn;
+      float* cbase = p.C + bz * p.scb;
+      const int64_t ldm = p.scm, ldn = p.scn;
       const int sub_r = lane >> 3, sub_c = (lane & 7) * 4;
 #pragma unroll
       for (int cc = 0; cc < EPI_COLS; cc += 32) {
@@ -353,28 +496,32 @@ gemm_kernel(const __grid_constant__ CUtensorMap map_ah, const __grid_constant__ 
         for (int i = 0; i < 32; i += 4) {
           const int row = row0 + i + sub_r;
           if (row < p.M) {
-            const float alpha = (!partial && p.alpha_rows)
-                                    ? __ldg(p.alpha_rows + (int64_t)bz * p.M + row) : 1.f;
+            const float alpha = p.alpha_rows ? __ldg(p.alpha_rows + (int64_t)bz * p.M + row) : 1.f;
             const int srow = i + sub_r;
             float4 v = *reinterpret_cast<const float4*>(
                 stage + srow * 32 + 4 * ((sub_c >> 2) ^ (srow & 7)));
             v.x *= alpha; v.y *= alpha; v.z *= alpha; v.w *= alpha;
             float* q = cbase + (int64_t)row * ldm + (int64_t)col * ldn;
             if (ldn == 1 && col + 3 < p.N && ((reinterpret_cast<uintptr_t>(q) & 15) == 0)) {
-              if (p.accumulate && !partial) {
+              if (p.accumulate) {
                 const float4 o = *reinterpret_cast<const float4*>(q);
                 v.x += o.x; v.y += o.y; v.z += o.z; v.w += o.w;
               }
+              epi4(p, bz, row, col, v);
               *reinterpret_cast<float4*>(q) = v;
             } else {
+              if (p.accumulate) {
+                const float* qq = q;
+                if (col < p.N) v.x += qq[0];
+                if (col + 1 < p.N) v.y += qq[ldn];
+                if (col + 2 < p.N) v.z += qq[2 * ldn];
+                if (col + 3 < p.N) v.w += qq[3 * ldn];
+              }
+              epi4(p, bz, row, col, v);
               const float e[4] = {v.x, v.y, v.z, v.w};
 #pragma unroll
-              for (int j = 0; j < 4; ++j) {
-                if (col + j < p.N) {
-                  float* qq = q + (int64_t)j * ldn;
-                  *qq = (p.accumulate && !partial) ? *qq + e[j] : e[j];
-                }
-              }
+              for (int j = 0; j < 4; ++j)
+                if (col + j < p.N) q[(int64_t)j * ldn] = e[j];
             }
           }
         }
@@ -384,6 +531,53 @@ gemm_kernel(const __grid_constant__ CUtensorMap map_ah, const __grid_constant__ 
   }
   asm volatile("tcgen05.fence::before_thread_sync;");
   __syncthreads();
+  if (clustered) {
+    // deterministic split-K reduction over DSMEM: CTA `rank` of the cluster
+    // sums rows [rank*rows_per, ...) of all partial tiles in rank order
+    cluster_sync_all();
+    const int t = blockIdx.x / p.ksplit;
+    const int bz = t / tiles_per_batch, r = t % tiles_per_batch;
+    const int m0 = (r / p.ntn) * BM, n0 = (r % p.ntn) * BN;
+    const int rank = (int)cluster_rank();
+    const int rows_per = (BM + p.ksplit - 1) / p.ksplit;
+    const int rb = rank * rows_per, re = min(BM, rb + rows_per);
+    const uint32_t red = smem_u32(smem);
+    float* cbase = p.C + bz * p.scb;
+    for (int idx = threadIdx.x; idx < (re - rb) * (BN / 4); idx += NUM_THREADS) {
+      const int row = rb + idx / (BN / 4), ch = idx % (BN / 4);
+      const uint32_t off = (uint32_t)(row * BN + 4 * (ch ^ (row & 7))) * 4u;
+      float4 v = ld_dsmem_f4(red + off, 0);
+      for (int q = 1; q < p.ksplit; ++q) {
+        const float4 w = ld_dsmem_f4(red + off, (uint32_t)q);
+        v.x += w.x; v.y += w.y; v.z += w.z; v.w += w.w;
+      }
+      const int grow = m0 + row, col = n0 + 4 * ch;
+      if (grow >= p.M) continue;
+      const float alpha = p.alpha_rows ? __ldg(p.alpha_rows + (int64_t)bz * p.M + grow) : 1.f;
+      v.x *= alpha; v.y *= alpha; v.z *= alpha; v.w *= alpha;
+      float* q = cbase + (int64_t)grow * p.scm + (int64_t)col * p.scn;
+      if (p.scn == 1 && col + 3 < p.N && ((reinterpret_cast<uintptr_t>(q) & 15) == 0)) {
+        if (p.accumulate) {
+          const float4 o = *reinterpret_cast<const float4*>(q);
+          v.x += o.x; v.y += o.y; v.z += o.z; v.w += o.w;
+        }
+        epi4(p, bz, grow, col, v);
+        *reinterpret_cast<float4*>(q) = v;
+      } else {
+        if (p.accumulate) {
+          if (col < p.N) v.x += q[0];
+          if (col + 1 < p.N) v.y += q[p.scn];
+          if (col + 2 < p.N) v.z += q[2 * p.scn];
+          if (col + 3 < p.N) v.w += q[3 * p.scn];
+        }
+        epi4(p, bz, grow, col, v);
+        const float e[4] = {v.x, v.y, v.z, v.w};
+        for (int j = 0; j < 4; ++j)
+          if (col + j < p.N) q[(int64_t)j * p.scn] = e[j];
+      }
+    }
+    cluster_sync_all();  // peers' smem stays live until every CTA has read it
+  }
   if (warp == 1) {
     asm volatile("tcgen05.fence::after_thread_sync;");
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base),
@@ -407,18 +601,51 @@ static PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
   return fn;
 }
 
-// dense K-major plane [batch][rows][Kp]
-static bool make_map(CUtensorMap* map, const float* base, int64_t Kp, int64_t rows, int64_t batch) {
+static bool encode(CUtensorMap* map, const float* base, const cuuint64_t* dims,
+                   const cuuint64_t* strides, const cuuint32_t* box,
+                   CUtensorMapSwizzle swz = CU_TENSOR_MAP_SWIZZLE_128B) {
   auto fn = encode_fn();
   if (!fn) return false;
+  cuuint32_t estr[3] = {1, 1, 1};
+  CUresult r = fn(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, const_cast<float*>(base), dims, strides,
+                  box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, swz,
+                  CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS;
+}
+
+// dense K-major plane [batch][rows][Kp]
+static bool make_map(CUtensorMap* map, const float* base, int64_t Kp, int64_t rows, int64_t batch) {
   cuuint64_t dims[3] = {(cuuint64_t)Kp, (cuuint64_t)rows, (cuuint64_t)batch};
   cuuint64_t strides[2] = {(cuuint64_t)(Kp * 4), (cuuint64_t)(rows * Kp * 4)};
   cuuint32_t box[3] = {BK, BM, 1};
-  cuuint32_t estr[3] = {1, 1, 1};
-  CUresult r = fn(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, const_cast<float*>(base), dims, strides,
-                  box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
-                  CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-  return r == CUDA_SUCCESS;
+  return encode(map, base, dims, strides, box);
+}
+
+// Can the operand view (rows x K per batch, strides in elements) be read by
+// TMA directly?  Returns kRawK / kRawMN, or kPreSplit when it cannot.
+static int raw_mode(const float* base, int64_t rows, int64_t K, int64_t nb, int64_t sb, int64_t sr,
+                    int64_t sk) {
+  if ((reinterpret_cast<uintptr_t>(base) & 15) != 0) return kPreSplit;
+  const bool b_ok = nb == 1 || ((sb * 4) % 16 == 0 && sb > 0);
+  if (!b_ok) return kPreSplit;
+  if (sk == 1 && (rows == 1 || ((sr * 4) % 16 == 0 && sr >= K))) return kRawK;
+  if (sr == 1 && rows > 1 && (sk * 4) % 16 == 0 && sk >= rows) return kRawMN;
+  return kPreSplit;
+}
+
+static bool make_raw_map(CUtensorMap* map, int mode, const float* base, int64_t rows, int64_t K,
+                         int64_t nb, int64_t sb, int64_t sr, int64_t sk) {
+  if (mode == kRawK) {
+    const int64_t ld = rows == 1 ? (K + 3) / 4 * 4 : sr;
+    cuuint64_t dims[3] = {(cuuint64_t)K, (cuuint64_t)rows, (cuuint64_t)nb};
+    cuuint64_t strides[2] = {(cuuint64_t)(ld * 4), (cuuint64_t)((nb == 1 ? ld * rows : sb) * 4)};
+    cuuint32_t box[3] = {BK, BM, 1};
+    return encode(map, base, dims, strides, box);
+  }
+  cuuint64_t dims[3] = {(cuuint64_t)rows, (cuuint64_t)K, (cuuint64_t)nb};
+  cuuint64_t strides[2] = {(cuuint64_t)(sk * 4), (cuuint64_t)((nb == 1 ? sk * K : sb) * 4)};
+  cuuint32_t box[3] = {32, BK, 1};
+  return encode(map, base, dims, strides, box, CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B);
 }
 
 static int num_sms() {
@@ -434,7 +661,9 @@ static int num_sms() {
 
 static int64_t align_up(int64_t x) { return (x + 255) / 256 * 256; }
 
-// K-splits so that (tiles x splits) covers the SMs, >= 2 chunks per split
+// K-splits so that (tiles x splits) covers the SMs, >= 2 chunks per split;
+// the splits of one tile form a thread-block cluster (<= 8, portable size)
+constexpr int kMaxCluster = 8;
 static void choose_split(const GemmArgs& g, int* ksplit, int* kb_per) {
   const int64_t tiles = ((g.M + BM - 1) / BM) * ((g.N + BN - 1) / BN) * g.batch;
   const int64_t Kp = (g.K + 3) / 4 * 4;
@@ -446,14 +675,14 @@ static void choose_split(const GemmArgs& g, int* ksplit, int* kb_per) {
     const int real = (nk + per - 1) / per;
     *per_out = per;
     const double waves = std::ceil((double)tiles * real / num_sms());
-    return waves * (per * 0.6 + 1.5) + (real > 1 ? 4.0 : 0.0);
+    return waves * (per * 0.6 + 1.5) + (real > 1 ? 1.0 : 0.0);
   };
   int best_per = 0;
   double best = cost(1, &best_per);
   int s_max = 1;
   if (tiles < num_sms() && nk >= 4 * CHUNK_KB)
     s_max = (int)std::max<int64_t>(1, std::min<int64_t>(
-        std::min<int64_t>((num_sms() + tiles - 1) / tiles, nk / (2 * CHUNK_KB)), 32));
+        std::min<int64_t>((num_sms() + tiles - 1) / tiles, nk / (2 * CHUNK_KB)), kMaxCluster));
   for (int s = 2; s <= s_max; ++s) {
     int per;
     const double c = cost(s, &per);
@@ -463,37 +692,16 @@ static void choose_split(const GemmArgs& g, int* ksplit, int* kb_per) {
   *ksplit = (nk + best_per - 1) / best_per;
 }
 
-__global__ void __launch_bounds__(256) splitk_sum(int64_t M, int64_t N, int64_t batch, int ksplit,
-                                                  const float* __restrict__ part, float* C,
-                                                  int64_t scb, int64_t scm, int64_t scn,
-                                                  const float* alpha_rows, int accumulate) {
-  pdl_enter();
-  const int64_t plane = batch * M * N;
-  const int64_t total = plane;
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
-       i += (int64_t)gridDim.x * blockDim.x) {
-    float s = 0.f;
-    for (int k = 0; k < ksplit; ++k) s += __ldg(part + k * plane + i);
-    const int64_t b = i / (M * N), rem = i - b * M * N;
-    const int64_t m = rem / N, n = rem - m * N;
-    if (alpha_rows) s *= alpha_rows[b * M + m];
-    float* q = C + b * scb + m * scm + n * scn;
-    *q = accumulate ? *q + s : s;
-  }
-}
-
 }  // namespace tc
 
-// Workspace: hi/lo planes of both operands (K padded to a multiple of 4 so
-// every TMA row stride is 16-byte aligned).
+// Workspace: hi/lo planes of both operands for the pre-split feed (K padded
+// to a multiple of 4 so every TMA row stride is 16-byte aligned); raw-fed
+// operands use none of it.
 int64_t gemm_tcgen05_workspace(const GemmArgs& g) {
   const int64_t Kp = (g.K + 3) / 4 * 4;
   const int64_t ba = (g.sab == 0 && g.batch > 1) ? 1 : g.batch;
   const int64_t bb = (g.sbb == 0 && g.batch > 1) ? 1 : g.batch;
-  int ks, per;
-  tc::choose_split(g, &ks, &per);
-  const int64_t part = ks > 1 ? tc::align_up((int64_t)ks * g.batch * g.M * g.N * 4) : 0;
-  return 2 * tc::align_up(ba * g.M * Kp * 4) + 2 * tc::align_up(bb * g.N * Kp * 4) + part;
+  return 2 * tc::align_up(ba * g.M * Kp * 4) + 2 * tc::align_up(bb * g.N * Kp * 4);
 }
 
 bool gemm_tcgen05_eligible(const GemmArgs& g) {
@@ -502,9 +710,18 @@ bool gemm_tcgen05_eligible(const GemmArgs& g) {
            (g.M + 31) / 32 > 65535 || (g.N + 31) / 32 > 65535);
 }
 
+// Does the raw (in-smem split) feed apply to at least one operand?
+bool gemm_tcgen05_raw_possible(const GemmArgs& g) {
+  using namespace tc;
+  const int64_t ba = (g.sab == 0 && g.batch > 1) ? 1 : g.batch;
+  const int64_t bb = (g.sbb == 0 && g.batch > 1) ? 1 : g.batch;
+  return raw_mode(g.A, g.M, g.K, ba, g.sab, g.sam, g.sak) != kPreSplit ||
+         raw_mode(g.B, g.N, g.K, bb, g.sbb, g.sbn, g.sbk) != kPreSplit;
+}
+
 // Dispatch model (microseconds), calibrated on B200 (tools/gemm_probe.py):
-// tensor path ~0.45 us per 32-deep k-block per 128x128 tile per wave plus
-// fixed split/launch costs; SIMT fp32 ~15 TFLOP/s.  Skinny problems with few
+// tensor path ~0.6 us per 32-deep k-block per 128x128 tile per wave plus
+// fixed launch costs; SIMT fp32 ~15 TFLOP/s.  Skinny problems with few
 // tiles (batch-128 forward passes) go SIMT with split-K.
 bool gemm_tcgen05_profitable(const GemmArgs& g) {
   if (g.K < 16 || g.M < 16 || g.N < 16) return false;
@@ -513,49 +730,89 @@ bool gemm_tcgen05_profitable(const GemmArgs& g) {
   tc::choose_split(g, &ks, &per);
   const double nk = (double)per;
   const double waves = std::ceil(tiles * ks / tc::num_sms());
-  const double t_tc = waves * (nk * 0.6 + 1.5) + 6.0 + (ks > 1 ? 4.0 : 0.0);
+  const double t_tc = waves * (nk * 0.6 + 1.5) + 3.0 + (ks > 1 ? 1.0 : 0.0);
   const double t_simt = 2.0 * g.M * g.N * g.K * g.batch / 15e6 + 3.0;
   return t_tc < t_simt;
 }
 
-int gemm_tcgen05(const GemmArgs& g, void* ws, int64_t ws_bytes, cudaStream_t s) {
+// variant: 0 = auto (raw feed for small problems), 1 = pre-split both
+// operands, 2 = raw feed wherever the operand layout allows it
+int gemm_tcgen05(const GemmArgs& g, void* ws, int64_t ws_bytes, cudaStream_t s, int variant) {
   using namespace tc;
   if (!gemm_tcgen05_eligible(g)) return PFB_E_UNSUPPORTED;
-  if (ws == nullptr || ws_bytes < gemm_tcgen05_workspace(g)) return PFB_E_UNSUPPORTED;
   const int64_t Kp = (g.K + 3) / 4 * 4;
-  const int a_bc = g.sab == 0 && g.batch > 1, b_bc = g.sbb == 0 && g.batch > 1;
+  const int a_bc = g.sab == 0 && g.batch > 1;
+  // a per-batch kscale makes B's planes differ per batch even for a shared B
+  const int b_bc = g.sbb == 0 && g.batch > 1 && !(g.kscale && g.skb != 0);
   const int64_t ba = a_bc ? 1 : g.batch, bb = b_bc ? 1 : g.batch;
+  if (variant == 0)
+    variant = (2.0 * g.M * g.N * g.K * g.batch < 4e9) ? 2 : 1;
+  int am = kPreSplit, bm = kPreSplit;
+  if (variant == 2) {
+    am = raw_mode(g.A, g.M, g.K, ba, g.sab, g.sam, g.sak);
+    bm = g.kscale ? kPreSplit : raw_mode(g.B, g.N, g.K, bb, g.sbb, g.sbn, g.sbk);
+  }
+  const int64_t need = (am == kPreSplit ? 2 * align_up(ba * g.M * Kp * 4) : 0) +
+                       (bm == kPreSplit ? 2 * align_up(bb * g.N * Kp * 4) : 0);
+  if (need > 0 && (ws == nullptr || ws_bytes < need)) return PFB_E_UNSUPPORTED;
   char* w = static_cast<char*>(ws);
-  float* ah = reinterpret_cast<float*>(w); w += align_up(ba * g.M * Kp * 4);
-  float* al = reinterpret_cast<float*>(w); w += align_up(ba * g.M * Kp * 4);
-  float* bh = reinterpret_cast<float*>(w); w += align_up(bb * g.N * Kp * 4);
-  float* bl = reinterpret_cast<float*>(w); w += align_up(bb * g.N * Kp * 4);
-  int ksplit, kb_per;
-  choose_split(g, &ksplit, &kb_per);
-  float* partials = ksplit > 1 ? reinterpret_cast<float*>(w) : nullptr;
-  // split (and re-layout) both operands; padded K columns are written as 0
-  dim3 ga((unsigned)((Kp + 31) / 32), (unsigned)((g.M + 31) / 32), (unsigned)ba);
-  dim3 gb((unsigned)((Kp + 31) / 32), (unsigned)((g.N + 31) / 32), (unsigned)bb);
-  launch(split_kernel, ga, 256, 0, s, g.A, g.M, g.K, Kp, g.sab, g.sam, g.sak, ah, al);
-  launch(split_kernel, gb, 256, 0, s, g.B, g.N, g.K, Kp, g.sbb, g.sbn, g.sbk, bh, bl);
   CUtensorMap mah, mal, mbh, mbl;
-  if (!make_map(&mah, ah, Kp, g.M, ba) || !make_map(&mal, al, Kp, g.M, ba) ||
-      !make_map(&mbh, bh, Kp, g.N, bb) || !make_map(&mbl, bl, Kp, g.N, bb))
-    return PFB_E_UNSUPPORTED;
+  if (am == kPreSplit) {
+    float* ah = reinterpret_cast<float*>(w); w += align_up(ba * g.M * Kp * 4);
+    float* al = reinterpret_cast<float*>(w); w += align_up(ba * g.M * Kp * 4);
+    dim3 ga((unsigned)((Kp + 31) / 32), (unsigned)((g.M + 31) / 32), (unsigned)ba);
+    launch(split_kernel, ga, 256, 0, s, g.A, g.M, g.K, Kp, g.sab, g.sam, g.sak, ah, al,
+           (const float*)nullptr, (int64_t)0, (int64_t)0);
+    if (!make_map(&mah, ah, Kp, g.M, ba) || !make_map(&mal, al, Kp, g.M, ba)) return PFB_E_UNSUPPORTED;
+  } else {
+    if (!make_raw_map(&mah, am, g.A, g.M, g.K, ba, g.sab, g.sam, g.sak)) return PFB_E_UNSUPPORTED;
+    mal = mah;
+  }
+  if (bm == kPreSplit) {
+    float* bh = reinterpret_cast<float*>(w); w += align_up(bb * g.N * Kp * 4);
+    float* bl = reinterpret_cast<float*>(w); w += align_up(bb * g.N * Kp * 4);
+    dim3 gb((unsigned)((Kp + 31) / 32), (unsigned)((g.N + 31) / 32), (unsigned)bb);
+    launch(split_kernel, gb, 256, 0, s, g.B, g.N, g.K, Kp, g.sbb, g.sbn, g.sbk, bh, bl, g.kscale,
+           g.skb, g.skk);
+    if (!make_map(&mbh, bh, Kp, g.N, bb) || !make_map(&mbl, bl, Kp, g.N, bb)) return PFB_E_UNSUPPORTED;
+  } else {
+    if (!make_raw_map(&mbh, bm, g.B, g.N, g.K, bb, g.sbb, g.sbn, g.sbk)) return PFB_E_UNSUPPORTED;
+    mbl = mbh;
+  }
   static bool attr = false;
   if (!attr) {
     cudaFuncSetAttribute(gemm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES);
     attr = true;
   }
+  int ksplit, kb_per;
+  choose_split(g, &ksplit, &kb_per);
+  const uint32_t idesc = kIdesc | ((uint32_t)(am == kRawMN) << 15) | ((uint32_t)(bm == kRawMN) << 16);
   Params p{(int)g.M, (int)g.N, (int)Kp, (int)g.batch,
-           (int)((g.M + BM - 1) / BM), (int)((g.N + BN - 1) / BN), a_bc, b_bc,
-           g.C, g.scb, g.scm, g.scn, g.alpha_rows, g.accumulate, ksplit, kb_per, partials};
+           (int)((g.M + BM - 1) / BM), (int)((g.N + BN - 1) / BN), a_bc, b_bc, am, bm, idesc,
+           g.C, g.scb, g.scm, g.scn, g.alpha_rows, g.accumulate, ksplit, kb_per,
+           g.bias, g.sxb, g.sxm, g.sxn, g.act, 4096u, 512u};
   const int64_t units = (int64_t)p.ntm * p.ntn * g.batch * ksplit;
-  const int grid = (int)std::min<int64_t>(units, num_sms());
-  launch(gemm_kernel, grid, NUM_THREADS, SMEM_BYTES, s, mah, mal, mbh, mbl, p);
-  if (ksplit > 1)
-    launch(splitk_sum, grid_for(g.batch * g.M * g.N, 256), 256, 0, s, g.M, g.N, g.batch, ksplit,
-           (const float*)partials, g.C, g.scb, g.scm, g.scn, g.alpha_rows, g.accumulate);
+  if (ksplit > 1) {
+    // one CTA per (tile, k-split); the k-splits of a tile are one cluster
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3((unsigned)units);
+    cfg.blockDim = dim3(NUM_THREADS);
+    cfg.dynamicSmemBytes = SMEM_BYTES;
+    cfg.stream = s;
+    cudaLaunchAttribute at[2];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = (unsigned)ksplit;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    at[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[1].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = pdl_enabled() ? 2 : 1;
+    cudaLaunchKernelEx(&cfg, gemm_kernel, mah, mal, mbh, mbl, p);
+  } else {
+    const int grid = (int)std::min<int64_t>(units, num_sms());
+    launch(gemm_kernel, grid, NUM_THREADS, SMEM_BYTES, s, mah, mal, mbh, mbl, p);
+  }
   return launch_status();
 }
 

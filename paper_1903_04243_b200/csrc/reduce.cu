@@ -298,3 +298,88 @@ extern "C" int pfb_reduce_dot(const pfb_tensor* x, const pfb_tensor* y, uint32_t
   return reduce_run<float, true>(x, sy, (const float*)y->data, axes_mask, out, ws, ws_bytes,
                                  as_stream(stream));
 }
+
+// ---------------------------------------------------------------------------
+// Several row-dots in one launch (passes.fuse_row_dots): for pair j,
+// out_j[i] = sum_k x_j[i, k] * y_j[i, k] over the dense trailing part of
+// rank-2 views [rows, inner_j] (row stride arbitrary, unit inner stride).
+// The per-example gradient norms of a network (one |g|^2 per parameter
+// block) are independent reductions of the same length-n leading dim; one
+// launch replaces one per block.  One CTA per (row, pair); Kahan per thread,
+// warp-shuffle + smem tree across the CTA: deterministic.
+
+namespace pfb {
+constexpr int kMaxDots = 8;
+struct RowDots {
+  int n;
+  int64_t rows;
+  const float* x[kMaxDots];
+  const float* y[kMaxDots];
+  int64_t inner[kMaxDots], sx[kMaxDots], sy[kMaxDots];
+  float* out[kMaxDots];
+  int64_t so[kMaxDots];
+  int vec[kMaxDots];  // x and y rows 16-byte aligned with inner % 4 == 0
+};
+
+__global__ void __launch_bounds__(256) row_dots_kernel(RowDots d) {
+  pdl_enter();
+  const int j = blockIdx.y;
+  const int64_t i = blockIdx.x;
+  const float* x = d.x[j] + i * d.sx[j];
+  const float* y = d.y[j] + i * d.sy[j];
+  const int64_t inner = d.inner[j];
+  Acc<float> acc;
+  if (d.vec[j]) {
+    const float4* x4 = reinterpret_cast<const float4*>(x);
+    const float4* y4 = reinterpret_cast<const float4*>(y);
+    for (int64_t k = threadIdx.x; k < inner / 4; k += blockDim.x) {
+      const float4 a = __ldg(x4 + k), b = __ldg(y4 + k);
+      acc.add(a.x * b.x + a.y * b.y + (a.z * b.z + a.w * b.w));
+    }
+  } else {
+    for (int64_t k = threadIdx.x; k < inner; k += blockDim.x) acc.add(__ldg(x + k) * __ldg(y + k));
+  }
+  __shared__ float red[8];
+  float v = warp_sum(acc.s);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = v;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    float t = 0.f;
+    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) t += red[w];
+    d.out[j][i * d.so[j]] = t;
+  }
+}
+}  // namespace pfb
+
+extern "C" int pfb_row_dots(int32_t n, const pfb_tensor* xs, const pfb_tensor* ys,
+                            pfb_tensor* outs, void* stream) {
+  using namespace pfb;
+  if (n < 1 || n > kMaxDots) return PFB_E_ARG;
+  RowDots d;
+  d.n = n;
+  d.rows = xs[0].shape[0];
+  for (int j = 0; j < n; ++j) {
+    const pfb_tensor *x = &xs[j], *y = &ys[j], *o = &outs[j];
+    if (x->dtype != PFB_F32 || y->dtype != PFB_F32 || o->dtype != PFB_F32) return PFB_E_DTYPE;
+    if (x->rank != 2 || y->rank != 2 || o->rank != 1) return PFB_E_RANK;
+    if (x->shape[0] != d.rows || y->shape[0] != d.rows || o->shape[0] != d.rows ||
+        x->shape[1] != y->shape[1])
+      return PFB_E_SHAPE;
+    if ((x->shape[1] > 1 && x->stride[1] != 1) || (y->shape[1] > 1 && y->stride[1] != 1))
+      return PFB_E_UNSUPPORTED;
+    d.x[j] = (const float*)x->data;
+    d.y[j] = (const float*)y->data;
+    d.inner[j] = x->shape[1];
+    d.sx[j] = x->stride[0];
+    d.sy[j] = y->stride[0];
+    d.out[j] = (float*)o->data;
+    d.so[j] = o->stride[0];
+    d.vec[j] = (x->shape[1] % 4 == 0) && (d.sx[j] % 4 == 0) && (d.sy[j] % 4 == 0) &&
+               (reinterpret_cast<uintptr_t>(x->data) % 16 == 0) &&
+               (reinterpret_cast<uintptr_t>(y->data) % 16 == 0);
+  }
+  if (d.rows == 0) return 0;
+  if (d.rows > 0x7fffffff) return PFB_E_UNSUPPORTED;
+  launch(row_dots_kernel, dim3((unsigned)d.rows, (unsigned)n), 256, 0, as_stream(stream), d);
+  return launch_status();
+}

@@ -59,7 +59,7 @@ def _numel(shape):
 class DArray:
     """A device tensor view: flat typed torch buffer + element offset/shape/strides."""
 
-    __slots__ = ("buf", "offset", "shape", "strides", "dtype")
+    __slots__ = ("buf", "offset", "shape", "strides", "dtype", "host")
 
     def __init__(self, buf, offset, shape, strides, dtype):
         self.buf = buf
@@ -67,6 +67,7 @@ class DArray:
         self.shape = tuple(int(d) for d in shape)
         self.strides = tuple(int(s) for s in strides)
         self.dtype = dtype
+        self.host = None  # host copy of a small constant index vector (view gathers)
 
     @staticmethod
     def empty(shape, dtype, device):
@@ -541,7 +542,10 @@ class Executor:
     # -- value helpers -------------------------------------------------------------
 
     def _upload(self, tv):
-        return DArray.from_numpy(tv.data, tv.dtype, self.device)
+        d = DArray.from_numpy(tv.data, tv.dtype, self.device)
+        if tv.dtype == DType.I64 and tv.rank == 1 and tv.data.size <= 1 << 16:
+            d.host = np.asarray(tv.data, dtype=np.int64)
+        return d
 
     def _dev(self, v):
         if isinstance(v, HostVal):
@@ -850,6 +854,86 @@ def _h_matmul(ex, node, ins):
     return [out]
 
 
+_ACT_CODE = {None: 0, "tanh": 1, "sigmoid": 2, "relu": 3}
+
+
+def _rows_view(x):
+    """x [lead, ...] as a [lead, inner] view with a unit inner stride, or None."""
+    inner = _numel(x.shape[1:])
+    exp = 1
+    for d, st in zip(reversed(x.shape[1:]), reversed(x.strides[1:])):
+        if d != 1 and st != exp:
+            return None
+        exp *= d
+    return x.view((x.shape[0], inner), (x.strides[0], 1))
+
+
+def _h_row_dots(ex, node, ins):
+    """row_dots (passes.fuse_row_dots): n independent per-row dot products in
+    one launch (pfb_row_dots); pairs without a unit-stride row view go through
+    pfb_reduce_dot individually."""
+    n = node.attrs["n"]
+    vals = [ex._dev(v) for v in ins]
+    outs, xs, ys, os_ = [], [], [], []
+    nbytes = 0
+    for j in range(n):
+        x, y = vals[2 * j], vals[2 * j + 1]
+        out = ex._empty((x.shape[0],), x.dtype)
+        outs.append(out)
+        xv, yv = _rows_view(x), _rows_view(y)
+        if xv is None or yv is None:
+            mask = sum(1 << a for a in range(1, x.rank))
+            wp, wn = ex._ws_get(min(8 * max(1, x.shape[0]) * 1024, 1 << 26))
+            ex._call(ex._lib.pfb_reduce_dot, x.desc(), y.desc(), mask, out.desc(), wp, wn,
+                     ex._stream, what="reduce_dot", work=(_abytes(x, y, out), 0))
+            continue
+        xs.append(xv)
+        ys.append(yv)
+        os_.append(out)
+        nbytes += _abytes(x, y, out) if x.buf is not y.buf or x.offset != y.offset else _abytes(x, out)
+    if xs:
+        m = len(xs)
+        XA, YA, OA = N.PfbTensor * m, N.PfbTensor * m, N.PfbTensor * m
+        xa, ya, oa = XA(*[v.desc() for v in xs]), YA(*[v.desc() for v in ys]), OA(*[v.desc() for v in os_])
+        ex._call(ex._lib.pfb_row_dots, m, xa, ya, oa, ex._stream, what="row_dots",
+                 work=(nbytes, 0))
+    return outs
+
+
+def _h_matmul_ep(ex, node, ins):
+    """matmul_ep (passes.fuse_matmul_epilogues): one GEMM launch computing
+    act(a @ diag(kscale) @ b + bias) -- prologue scale and epilogue in the
+    kernel (pfb_matmul_fused)."""
+    import ctypes
+    at = node.attrs
+    vals = [ex._dev(v) for v in ins]
+    a, b = vals[0], vals[1]
+    k = 2
+    ks = bias = None
+    if at.get("has_kscale"):
+        ks = vals[k]
+        k += 1
+    if at.get("has_bias"):
+        bias = vals[k]
+    if a.rank == 2:
+        shape = (a.shape[0], b.shape[1])
+    else:
+        shape = (a.shape[0], a.shape[1], b.shape[2])
+    out = ex._empty(shape, a.dtype)
+    flops = 2 * _numel(shape) * a.shape[-1]
+    ad, bd, od = a.desc(), b.desc(), out.desc()
+    kd = ks.desc() if ks is not None else None
+    xd = bias.desc() if bias is not None else None
+    need = ex._lib.pfb_matmul_workspace(ad, bd, od)
+    wp, wn = ex._ws_get(need) if need > 0 else (None, 0)
+    ex._call(ex._lib.pfb_matmul_fused, ad, bd, od,
+             ctypes.byref(kd) if kd is not None else None,
+             ctypes.byref(xd) if xd is not None else None, _ACT_CODE[at.get("act")],
+             None, 0, 0, wp, wn, ex._stream, what="matmul",
+             work=(_abytes(*[v for v in vals] + [out]), flops))
+    return [out]
+
+
 def _h_conv(ex, node, ins):
     x, f = (ex._dense(ex._dev(v)) for v in ins)
     k = node.kind
@@ -884,6 +968,8 @@ def _h_reduce_sum(ex, node, ins):
     if not axes:
         return [ins[0]]
     shape = tuple(d for i, d in enumerate(x.shape) if i not in axes)
+    if all(x.shape[ax] == 1 for ax in axes):  # sum over extent-1 axes: a view
+        return [x.view(shape, tuple(st for i, st in enumerate(x.strides) if i not in axes))]
     mask = 0
     for ax in axes:
         mask |= 1 << ax
@@ -930,12 +1016,12 @@ def _h_concat(ex, node, ins):
     shape = list(xs[0].shape)
     shape[ax] = sum(x.shape[ax] for x in xs)
     out = ex._empty(shape, dt)
-    off = 0
-    for x in xs:
-        if x.size:
-            ex._call(ex._lib.pfb_copy, x.desc(), _slice_view(out, ax, off, x.shape[ax]).desc(),
-                     ex._stream, what="concat")
-        off += x.shape[ax]
+    if out.size == 0:
+        return [out]
+    parts = [x for x in xs if x.shape[ax] > 0]
+    arr = (N.PfbTensor * len(parts))(*[x.desc() for x in parts])
+    ex._call(ex._lib.pfb_concat, len(parts), arr, ax, out.desc(), ex._stream, what="concat",
+             work=(_abytes(*parts) * 2, 0))
     return [out]
 
 
@@ -970,6 +1056,19 @@ def _h_gather(ex, node, ins):
         if not 0 <= r < x.shape[0]:
             raise E.IndexOutOfBounds(f"gather_rows: index {r} out of range [0, {x.shape[0]})")
         return [x.view(x.shape[1:], x.strides[1:], r * x.strides[0])]
+    h = getattr(idx, "host", None)
+    if h is not None and h.size >= 1:
+        # constant index = arithmetic progression (a slice, or a broadcast when
+        # the step is 0): a strided view, no kernel.  Bounds as the kernel's.
+        step = int(h[1] - h[0]) if h.size > 1 else 0
+        if step >= 0 and (h.size == 1 or np.array_equal(h, h[0] + step * np.arange(h.size, dtype=np.int64))):
+            lo, hi = int(h.min()), int(h.max())
+            if lo < 0 or hi >= x.shape[0]:
+                bad = lo if lo < 0 else hi
+                raise E.IndexOutOfBounds(
+                    f"gather_rows: index {bad} out of range [0, {x.shape[0]})")
+            return [x.view((h.size,) + x.shape[1:], (step * x.strides[0],) + x.strides[1:],
+                           int(h[0]) * x.strides[0])]
     out = ex._empty(tuple(idx.shape) + x.shape[1:], x.dtype)
     ex._call(ex._lib.pfb_gather_rows, x.desc(), idx.desc(), out.desc(), ex._err_slot(node),
              ex._stream, what="gather_rows")
@@ -1126,6 +1225,8 @@ def _h_reduce_dot(ex, node, ins):
     x, y = (ex._dev(v) for v in ins)
     axes = normalize_axes(node.attrs["axes"], x.rank)
     shape = tuple(d for i, d in enumerate(x.shape) if i not in axes)
+    if all(x.shape[ax] == 1 for ax in axes):  # sum over extent-1 axes: a view
+        return [x.view(shape, tuple(st for i, st in enumerate(x.strides) if i not in axes))]
     mask = 0
     for ax in axes:
         mask |= 1 << ax
@@ -1193,6 +1294,8 @@ _HANDLERS.update({k: _h_unary for k in UNARY_KINDS})
 _HANDLERS.update({
     "cast": _h_cast, "matmul": _h_matmul, "conv2d": _h_conv, "conv2d_input_grad": _h_conv,
     "im2col": _h_im2col, "reduce_sum": _h_reduce_sum, "concat": _h_concat, "stack": _h_stack,
+    "matmul_ep": _h_matmul_ep,
+    "row_dots": _h_row_dots,
     "gather_rows": _h_gather, "scatter_rows": _h_scatter_rows,
     "scatter_add_rows": _h_scatter_add, "reshape": _h_reshape, "transpose": _h_transpose,
     "slice_leading": _h_slice_leading, "tile_leading": _h_tile_leading,

@@ -17,6 +17,13 @@ F3   chains of elementwise ops (binary / unary / f32<->bool cast) whose interior
      small register program (the same fp32 ops in the same order).
 F4   reduce_sum(square(x)) / reduce_sum(x * y)  ->  reduce_dot(x, y): the
      product is formed in registers inside the reduction.
+F6   independent reduce_dot row-reductions over the same leading dim (the
+     per-parameter-block |g_i|^2 of per-example norms)  ->  one
+     `row_dots` launch with one output per reduction.
+F5   GEMM prologue / epilogue (SURVEY.md §8a F3 "GEMM epilogues"):
+     matmul(A, B * s[K,1]) -> [reshape] -> add(., bias[N]) -> [reshape] ->
+     tanh | sigmoid | relu   ->  one `matmul_ep` launch (kscale scales B's
+     rows as the operand is read; bias + activation in the store epilogue).
 
 Each rewrite adds nodes to a private copy of the graph and redirects the
 consumers; the now-unread outer products are removed by the executor's
@@ -240,11 +247,184 @@ def fuse_reductions(g, keep=()):
     return count, moved
 
 
+_ACT_KINDS = ("tanh", "sigmoid", "relu")
+
+
+def fuse_matmul_epilogues(g, keep=()):
+    """F5 in place on `g` (a private copy).  Returns (count, moved outputs)."""
+    from .tensor import DType
+    rw = _Rewriter(g, keep)
+    rw.replaced = {}
+    count = 0
+    for node in list(g.topo_order()):
+        if node.id not in g.nodes or node.kind != "matmul":
+            continue
+        if node.out_dtypes[0] != DType.F64:
+            continue
+        count += _f5(rw, node)
+    return count, rw.replaced
+
+
+def _strip_units(shape):
+    return tuple(d for d in shape if d != 1)
+
+
+def _f5(rw, node):
+    import math
+    g, b = rw.g, rw.b
+    sm = g.ref_shape((node.id, 0))
+    sa, sbb = g.ref_shape(node.inputs[0]), g.ref_shape(node.inputs[1])
+    if None in (sm, sa, sbb) or None in sm or None in sa or None in sbb or sa[-1] == 0:
+        return 0
+    A, B = Ref(g, *node.inputs[0]), Ref(g, *node.inputs[1])
+    kscale = None
+    bn = rw.node(node.inputs[1])
+    if bn.kind == "mul" and node.inputs[1][1] == 0 and rw.single_use(node.inputs[1]):
+        for j in (0, 1):
+            s_key, b0_key = bn.inputs[1 - j], bn.inputs[j]
+            ss, s0 = g.ref_shape(s_key), g.ref_shape(b0_key)
+            if (ss is not None and s0 is not None and tuple(s0) == tuple(sbb)
+                    and len(ss) == len(s0) and ss[-1] == 1 and tuple(ss[:-1]) == tuple(s0[:-1])
+                    and g.ref_dtype(s_key) == g.ref_dtype(b0_key)):
+                kscale = b.reshape(Ref(g, *s_key), list(ss[:-1]))
+                B = Ref(g, *b0_key)
+                break
+    n_cols = sm[-1]
+    key = (node.id, 0)
+    end = key
+    bias = act = None
+    while True:
+        us = rw.users().get(key, [])
+        if len(us) != 1 or key in rw.keep:
+            break
+        un, idx = us[0]
+        osh = g.ref_shape((un.id, 0))
+        if osh is None or None in osh:
+            break
+        if un.kind == "reshape":
+            if _strip_units(osh) != _strip_units(sm) or not osh or osh[-1] != n_cols:
+                break
+            key = (un.id, 0)
+            continue
+        if un.kind == "add" and bias is None and act is None:
+            other = un.inputs[1 - idx]
+            bsh = g.ref_shape(other)
+            if (bsh is None or None in bsh or tuple(osh) != tuple(g.ref_shape(key))
+                    or g.ref_dtype(other) != g.ref_dtype(key)):
+                break
+            nb = math.prod(bsh)
+            if not (nb == 1 or (nb == n_cols and bsh and bsh[-1] == n_cols)):
+                break
+            bias = b.reshape(Ref(g, *other), [nb])
+            key = end = (un.id, 0)
+            continue
+        if un.kind in _ACT_KINDS and act is None:
+            act = un.kind
+            key = end = (un.id, 0)
+            continue
+        break
+    if kscale is None and bias is None and act is None:
+        return 0
+    ins = [A, B] + ([kscale] if kscale is not None else []) + ([bias] if bias is not None else [])
+    new = g.add_node("matmul_ep", [(r.nid, r.port) for r in ins],
+                     {"act": act, "has_kscale": kscale is not None, "has_bias": bias is not None})
+    out = Ref(g, new.id, 0)
+    esh = g.ref_shape(end)
+    if tuple(esh) != tuple(sm):
+        out = b.reshape(out, list(esh))
+    rw.redirect(end, out)
+    return 1
+
+
+MAX_ROW_DOTS = 8
+
+
+def fuse_row_dots(g, keep=()):
+    """F6 in place on `g`: group reduce_dot nodes that reduce every
+    non-leading axis of same-shape operands and share the leading extent into
+    `row_dots` nodes (<= 8 each).  A node joins a group only if no member is
+    its ancestor or descendant, so the grouped node cannot create a cycle."""
+    from .tensor import DType
+    keep = set(keep)
+    live = live_set(g, keep)
+    cands = []
+    for node in g.topo_order():
+        if node.kind != "reduce_dot" or node.id not in live:
+            continue
+        x, y = node.inputs
+        sx, sy = g.ref_shape(x), g.ref_shape(y)
+        if sx is None or None in sx or len(sx) < 2 or tuple(sx) != tuple(sy):
+            continue
+        if node.out_dtypes[0] != DType.F64:
+            continue
+        from .tensor import normalize_axes
+        if tuple(sorted(normalize_axes(node.attrs["axes"], len(sx)))) != tuple(range(1, len(sx))):
+            continue
+        cands.append(node)
+    if len(cands) < 2:
+        return 0, {}
+    anc_memo = {}
+
+    def ancestors(nid):
+        if nid in anc_memo:
+            return anc_memo[nid]
+        out, todo = set(), [nid]
+        while todo:
+            k = todo.pop()
+            for src, _ in g.nodes[k].inputs:
+                if src not in out:
+                    out.add(src)
+                    todo.append(src)
+        anc_memo[nid] = out
+        return out
+
+    groups = []
+    for node in cands:
+        lead = g.ref_shape(node.inputs[0])[0]
+        anc = ancestors(node.id)
+        placed = False
+        for grp in groups:
+            if grp["lead"] != lead or len(grp["nodes"]) >= MAX_ROW_DOTS:
+                continue
+            if any(m.id in anc or node.id in ancestors(m.id) for m in grp["nodes"]):
+                continue
+            grp["nodes"].append(node)
+            placed = True
+            break
+        if not placed:
+            groups.append({"lead": lead, "nodes": [node]})
+    users = {}
+    for n in g.nodes.values():
+        for i, src in enumerate(n.inputs):
+            users.setdefault(src, []).append((n, i))
+    moved, count = {}, 0
+    for grp in groups:
+        members = grp["nodes"]
+        if len(members) < 2:
+            continue
+        ins = []
+        for m in members:
+            ins.extend(m.inputs)
+        new = g.add_node("row_dots", ins, {"n": len(members)})
+        for j, m in enumerate(members):
+            for u, i in users.get((m.id, 0), []):
+                u.inputs[i] = (new.id, j)
+            if (m.id, 0) in keep:
+                moved[(m.id, 0)] = (new.id, j)
+        count += 1
+    g._topo_cache = None
+    return count, moved
+
+
 def _optimize_in_place(g, keep, elementwise=True):
     _, moved = fuse_outer_products(g, keep)
     keep = [moved.get(k, k) for k in keep]
     _, moved4 = fuse_reductions(g, keep)
     keep = [moved4.get(k, k) for k in keep]
+    _, moved6 = fuse_row_dots(g, keep)
+    keep = [moved6.get(k, k) for k in keep]
+    _, moved5 = fuse_matmul_epilogues(g, keep)
+    keep = [moved5.get(k, k) for k in keep]
     moved3 = {}
     if elementwise:
         _, moved3 = fuse_elementwise(g, keep)
@@ -270,6 +450,10 @@ def optimize(g, keep_keys, elementwise=True):
     keep = [moved.get(k, k) for k in keep]
     _, moved4 = fuse_reductions(dst, keep)
     keep = [moved4.get(k, k) for k in keep]
+    _, moved6 = fuse_row_dots(dst, keep)
+    keep = [moved6.get(k, k) for k in keep]
+    _, moved5 = fuse_matmul_epilogues(dst, keep)
+    keep = [moved5.get(k, k) for k in keep]
     moved3 = {}
     if elementwise:
         _, moved3 = fuse_elementwise(dst, keep)
@@ -277,6 +461,8 @@ def optimize(g, keep_keys, elementwise=True):
     for k, v in mapping.items():
         v = moved.get(v, v)
         v = moved4.get(v, v)
+        v = moved6.get(v, v)
+        v = moved5.get(v, v)
         final[k] = moved3.get(v, v)
     return dst, final
 

@@ -20,11 +20,27 @@ def env():
     return torch, N.lib(), DArray, DType
 
 
-def _run(env, a, b, force, transpose_b=False, accumulate_into=None, alpha=None):
+def _tview(DArray, DType, dev, x):
+    """x as a transposed view of a dense copy of x^T (last two axes swapped)."""
+    xt = DArray.from_numpy(np.swapaxes(x, -1, -2).copy(), DType.F64, dev)
+    perm = list(range(x.ndim))
+    perm[-1], perm[-2] = perm[-2], perm[-1]
+    return xt.view([xt.shape[p] for p in perm], [xt.strides[p] for p in perm])
+
+
+def _run(env, a, b, force, transpose_b=False, accumulate_into=None, alpha=None, a_mn=False,
+         b_bcast=False):
     torch, lib, DArray, DType = env
     dev = torch.device("cuda")
-    A = DArray.from_numpy(a, DType.F64, dev)
-    if transpose_b:  # K-major B: store B^T densely, pass a transposed view
+    A = _tview(DArray, DType, dev, a) if a_mn else DArray.from_numpy(a, DType.F64, dev)
+    if b_bcast:  # one [K,N] matrix shared by the batch: batch stride 0
+        B1 = (_tview(DArray, DType, dev, b[0]) if transpose_b
+              else DArray.from_numpy(b[0].copy(), DType.F64, dev))
+        B = B1.view((a.shape[0],) + tuple(B1.shape), (0,) + tuple(B1.strides))
+        transpose_b = None
+    if transpose_b is None:
+        pass
+    elif transpose_b:  # K-major B: store B^T densely, pass a transposed view
         Bt = DArray.from_numpy(np.swapaxes(b, -1, -2).copy(), DType.F64, dev)
         perm = list(range(b.ndim))
         perm[-1], perm[-2] = perm[-2], perm[-1]
@@ -131,3 +147,111 @@ def test_small_k_outer_products(env, shape):
     b = _f32(r, (bsz, k, n) if bsz > 1 else (k, n))
     got = _run(env, a, b, 0)
     np.testing.assert_allclose(got, a @ b, rtol=1e-6, atol=1e-6)
+
+
+# tcgen05 operand feeds: 3 = both operands pre-split by split_kernel, 4 = raw
+# TMA feed split in shared memory (K-major or MN-major smem operands), with the
+# k-splits of a tile reduced across a thread-block cluster through DSMEM.
+FEED_SHAPES = [(256, 2048, 1024), (200, 300, 100), (513, 129, 1000), (128, 256, 36),
+               (96, 160, 37), (256, 1024, 2048), (64, 512, 4096)]
+
+
+@pytest.mark.parametrize("shape", FEED_SHAPES)
+@pytest.mark.parametrize("layout", ["a_k/b_mn", "a_k/b_k", "a_mn/b_mn", "a_mn/b_k"])
+@pytest.mark.parametrize("force", [3, 4])
+def test_gemm_tcgen05_feeds(env, shape, layout, force):
+    m, n, k = shape
+    r = np.random.default_rng(m * 7 + n + k)
+    a, b = _operands(r, (m, k), (k, n))
+    got = _run(env, a, b, force, transpose_b=layout.endswith("b_k"), a_mn=layout.startswith("a_mn"))
+    np.testing.assert_allclose(got, a @ b, rtol=RTOL, atol=ATOL)
+
+
+@pytest.mark.parametrize("force", [3, 4])
+@pytest.mark.parametrize("bcast", [False, True])
+def test_gemm_tcgen05_feeds_batched(env, force, bcast):
+    r = np.random.default_rng(17)
+    a, b = _operands(r, (3, 160, 96), (3, 96, 200))
+    if bcast:
+        b = np.broadcast_to(b[:1], b.shape).copy()
+    got = _run(env, a, b, force, b_bcast=bcast)
+    np.testing.assert_allclose(got, a @ b, rtol=RTOL, atol=ATOL)
+
+
+@pytest.mark.parametrize("force", [3, 4])
+def test_gemm_tcgen05_cluster_splitk_epilogue(env, force):
+    """alpha rows + accumulate applied once, in the cluster reduction."""
+    r = np.random.default_rng(23)
+    a, b = _operands(r, (256, 2048), (2048, 512))
+    c0 = _f32(r, (256, 512))
+    alpha = np.asarray(r.standard_normal(256), np.float32).astype(np.float64)
+    got = _run(env, a, b, force, accumulate_into=c0, alpha=alpha)
+    np.testing.assert_allclose(got, c0 + alpha[:, None] * (a @ b), rtol=RTOL, atol=ATOL)
+
+
+def test_gemm_tcgen05_cluster_splitk_deterministic(env):
+    r = np.random.default_rng(29)
+    a, b = _operands(r, (256, 4096), (4096, 256))
+    x = _run(env, a, b, 4)
+    y = _run(env, a, b, 4)
+    assert np.array_equal(x, y)
+
+
+def _run_fused(env, a, b, force, bias=None, act=0, kscale=None):
+    torch, lib, DArray, DType = env
+    dev = torch.device("cuda")
+    A = DArray.from_numpy(a, DType.F64, dev)
+    B = DArray.from_numpy(b, DType.F64, dev)
+    C = DArray.empty(a.shape[:-1] + (b.shape[-1],), DType.F64, dev)
+    bd = DArray.from_numpy(bias, DType.F64, dev).desc() if bias is not None else None
+    kd = DArray.from_numpy(kscale, DType.F64, dev).desc() if kscale is not None else None
+    ad, bdd, cd = A.desc(), B.desc(), C.desc()
+    need = lib.pfb_matmul_workspace(ad, bdd, cd)
+    ws = torch.empty(max(need, 256), dtype=torch.uint8, device=dev)
+    import ctypes
+    rc = lib.pfb_matmul_fused(ad, bdd, cd, ctypes.byref(kd) if kd is not None else None,
+                              ctypes.byref(bd) if bd is not None else None, act, None, 0, force,
+                              ws.data_ptr(), ws.numel(), torch.cuda.current_stream().cuda_stream)
+    assert rc == 0, rc
+    torch.cuda.synchronize()
+    return C.to_numpy().astype(np.float64)
+
+
+_ACTS = {0: lambda v: v, 1: np.tanh, 2: lambda v: 1 / (1 + np.exp(-v)), 3: lambda v: np.maximum(v, 0)}
+
+
+@pytest.mark.parametrize("force", [1, 3, 4])
+@pytest.mark.parametrize("shape", [(128, 256, 784), (256, 2048, 1024), (64, 10, 256), (300, 4096, 1)])
+@pytest.mark.parametrize("act", [0, 1, 2, 3])
+def test_gemm_fused_bias_act(env, force, shape, act):
+    m, n, k = shape
+    if k < 8 and force != 1:
+        pytest.skip("tcgen05 path needs K >= 8")
+    r = np.random.default_rng(m + n + k + act)
+    a, b = _operands(r, (m, k), (k, n))
+    bias = _f32(r, (n,), 0.1)
+    got = _run_fused(env, a, b, force, bias=bias, act=act)
+    np.testing.assert_allclose(got, _ACTS[act](a @ b + bias), rtol=RTOL, atol=ATOL)
+
+
+@pytest.mark.parametrize("force", [1, 3, 4])
+@pytest.mark.parametrize("shape", [(784, 256, 128), (256, 10, 128), (1024, 2048, 64)])
+def test_gemm_fused_kscale(env, force, shape):
+    """clipped-sum contraction X^T diag(s) D (cfg2 F1) with the scale fused."""
+    m, n, k = shape
+    r = np.random.default_rng(m * n + k)
+    a, b = _operands(r, (m, k), (k, n))
+    s = np.asarray(r.uniform(0.1, 1.0, k), np.float32).astype(np.float64)
+    got = _run_fused(env, a, b, force, kscale=s)
+    np.testing.assert_allclose(got, a @ (s[:, None] * b), rtol=RTOL, atol=ATOL)
+
+
+def test_gemm_fused_batched_bias_kscale(env):
+    r = np.random.default_rng(41)
+    a, b = _operands(r, (4, 96, 130), (4, 130, 72))
+    bias = _f32(r, (4, 1, 72), 0.1)
+    s = np.asarray(r.uniform(0.1, 1.0, (4, 130)), np.float32).astype(np.float64)
+    for force in (1, 3, 4):
+        got = _run_fused(env, a, b, force, bias=bias, act=1, kscale=s)
+        np.testing.assert_allclose(got, np.tanh(a @ (s[:, :, None] * b) + bias), rtol=RTOL,
+                                   atol=ATOL)

@@ -113,6 +113,32 @@ def test_gather_out_of_bounds_raises(Executor):
     assert isinstance(e.value.cause, errors.IndexOutOfBounds)
 
 
+@pytest.mark.parametrize("idx", [[0, 5, 1], [1, 2, 3, 4]])
+def test_gather_out_of_bounds_raises_kernel_and_view(idx, Executor):
+    """[0,5,1] goes through the gather kernel (device error word), the
+    arithmetic progression through the view path (host check)."""
+    from paper_1903_04243_b200 import GraphBuilder, errors
+    b = GraphBuilder()
+    b.graph.set_outputs([b.gather(b.const(np.ones((4, 3))), b.const(np.array(idx)))])
+    with pytest.raises(errors.ExecError) as e:
+        Executor(b.graph).run()
+    assert isinstance(e.value.cause, errors.IndexOutOfBounds)
+
+
+@pytest.mark.parametrize("idx", [[2], [0, 1, 2], [1, 3, 5], [4, 4, 4], [5, 3, 0]])
+def test_gather_constant_index_values(idx, Executor):
+    """Constant progressions become strided views; values as the reference."""
+    from paper_1903_04243_b200 import GraphBuilder
+    x = np.arange(6 * 5, dtype=np.float64).reshape(6, 5)
+    b = GraphBuilder()
+    xc = b.const(x)
+    g1 = b.gather(xc, b.const(np.array(idx)))
+    b.graph.set_outputs([g1, b.mul(g1, b.f64(2.0))])
+    got, got2 = Executor(b.graph).run()
+    check(got, x[idx])
+    check(got2, 2 * x[idx])
+
+
 @pytest.mark.parametrize("sets,err", [(([0, 1], [1, 2]), "IndexCollision"),
                                       (([0], [2]), "IncompleteCover")])
 def test_scatter_rows_validation(sets, err, Executor):

@@ -61,3 +61,42 @@ def test_f2_outer_product_sum_becomes_one_gemm():
                                     ("cfg5", dict(n=5, max_len=6, units=4))])
 def test_passes_neutral_elsewhere(cfg, kw):
     _run_both(WL.BUILDERS[cfg](WL.this_api(), **kw))
+
+
+def test_f5_matmul_epilogues_and_f6_row_dots():
+    """cfg2 MLP: forward GEMMs carry bias(+tanh) epilogues, the clipped-sum
+    GEMMs the clip-factor kscale, and the six per-block |g_i|^2 reductions
+    run as one row_dots node -- values unchanged (oracle)."""
+    w = WL.cfg2(WL.this_api(), n=6, model="mlp", d_h=16)
+    g, g2, m = _run_both(w)
+    live = _kinds(g2, [m[tuple(o)] for o in g.outputs])
+    eps = [n for n in live if n.kind == "matmul_ep"]
+    assert any(n.attrs["act"] == "tanh" and n.attrs["has_bias"] for n in eps)
+    assert sum(n.attrs["has_kscale"] for n in eps) == 2
+    rd = [n for n in live if n.kind == "row_dots"]
+    assert len(rd) == 1 and rd[0].attrs["n"] == 6
+    assert not [n for n in live if n.kind == "reduce_dot" and len(n.out_shapes[0]) == 1
+                and n.out_shapes[0][0] == 6 and len(g2.ref_shape(n.inputs[0])) > 1
+                and n.attrs["axes"] != (0,)]
+
+
+def test_f5_respects_multi_use_preactivation():
+    """z = xW + b used twice (tanh and an output): only the bias is fused."""
+    from paper_1903_04243_b200 import GraphBuilder
+    from oracle import OracleExecutor as OE
+    r = np.random.default_rng(0)
+    b = GraphBuilder()
+    x = b.const(r.standard_normal((5, 7)))
+    W = b.const(r.standard_normal((7, 3)))
+    bias = b.const(r.standard_normal((3,)))
+    z = b.add(b.matmul(x, W), bias)
+    y = b.tanh(z)
+    b.graph.set_outputs([y, b.mul(z, z)])
+    keys = [tuple(o) for o in b.graph.outputs]
+    g2, mp = optimize(b.graph, keys)
+    want = OE(b.graph).run()
+    got = OE(g2).run(outputs=[g2.out(*mp[k]) for k in keys])
+    for a_, b_ in zip(got, want):
+        np.testing.assert_allclose(a_.data, b_.data, rtol=1e-12)
+    eps = [n for n in g2.nodes.values() if n.kind == "matmul_ep"]
+    assert len(eps) == 1 and eps[0].attrs["act"] is None and eps[0].attrs["has_bias"]
