@@ -334,7 +334,8 @@ def main():
             durs.append(s_ev.elapsed_time(e_ev) / 1e3)
         dur = float(np.median(durs))
         same = [r for r in recs if r[0] == what]
-        if flops and flops / max(nbytes, 1) > 8:
+        # the bound is whichever roofline time is larger for this launch
+        if flops and flops / (tc_peak * 1e12) >= nbytes / (hbm * 1e9):
             ach = flops / dur / 1e12
             roofline = {"bound": "tensor", "achieved": ach, "peak": tc_peak, "unit": "TFLOP/s",
                         "frac": ach / tc_peak,

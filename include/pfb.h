@@ -78,6 +78,14 @@ int pfb_cast(const pfb_tensor* x, pfb_tensor* out, void* stream);
  * a chain the reference runs as separate NumPy calls. */
 int pfb_fused_ew(int32_t n_in, const pfb_tensor* ins, int32_t n_steps, const int32_t* program,
                  pfb_tensor* out, void* stream);
+/* multi-output form: the registers out_regs[0..n_out) are
+ * stored to outs[k] after the program (n_out <= 8); all outputs share one shape and one
+ * stride layout (f32 or u8-bool each).  Lets an elementwise group whose
+ * interior values have consumers outside it (the LSTM gate activations kept
+ * for the backward pass) run as one launch. */
+int pfb_fused_ew_multi(int32_t n_in, const pfb_tensor* ins, int32_t n_steps,
+                       const int32_t* program, int32_t n_out, const int32_t* out_regs,
+                       pfb_tensor* outs, void* stream);
 
 /* select(mask, a, b) = mask ? a : b with broadcasting (predicated cond /
  * while bodies; numpy.where semantics); any dtype, mask is bool. */

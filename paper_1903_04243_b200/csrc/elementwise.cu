@@ -292,10 +292,18 @@ constexpr int kMaxSteps = 48;
 constexpr int kMaxRegs = 16;
 enum FusedOpc { F_LOAD = 64, F_CONST = 65, F_SELECT = 68 };
 
+constexpr int kMaxOuts = 8;
 struct FusedProgram {
   int n_in, n_steps;
   int in_dtype[8];
   int code[kMaxSteps][4];  // opcode, dst, src1, src2 (src1 = input / const bits)
+  int n_out;               // outputs: registers stored after the program
+  int out_reg[kMaxOuts];
+  int out_dt[kMaxOuts];    // PFB_F32 or PFB_BOOL
+};
+
+struct FusedOuts {
+  void* p[kMaxOuts];
 };
 
 // One templated kernel for both widths: V = 4 runs the program on 4
@@ -354,9 +362,34 @@ __device__ __forceinline__ Vec<V> load_v(const void* base, int64_t off, int64_t 
   }                                                       \
   break;
 
-template <typename IdxT, typename Tout, int NIN, int V>
+template <int V>
+__device__ __forceinline__ void store_v(void* base, int dt, int64_t off, int64_t inner, bool vec,
+                                        const Vec<V>& res) {
+  if (dt == PFB_BOOL) {
+    uint8_t* q = reinterpret_cast<uint8_t*>(base) + off;
+    if (V == 4 && vec) {
+      *reinterpret_cast<uchar4*>(q) = make_uchar4(res.v[0] != 0.f, res.v[1] != 0.f,
+                                                  res.v[V > 2 ? 2 : 0] != 0.f,
+                                                  res.v[V > 3 ? 3 : 0] != 0.f);
+      return;
+    }
+#pragma unroll
+    for (int j = 0; j < V; ++j) q[j * inner] = (uint8_t)(res.v[j] != 0.f);
+  } else {
+    float* q = reinterpret_cast<float*>(base) + off;
+    if (V == 4 && vec) {
+      *reinterpret_cast<float4*>(q) = make_float4(res.v[0], res.v[V > 1 ? 1 : 0],
+                                                  res.v[V > 2 ? 2 : 0], res.v[V > 3 ? 3 : 0]);
+      return;
+    }
+#pragma unroll
+    for (int j = 0; j < V; ++j) q[j * inner] = res.v[j];
+  }
+}
+
+template <typename IdxT, int NIN, int V>
 __global__ void __launch_bounds__(256) fused_kernel(Layout L, IdxT ngroups, FusedProgram P,
-                                                    uint32_t modes, Tout* out,
+                                                    uint32_t modes, FusedOuts outs,
                                                     const void* i0, const void* i1,
                                                     const void* i2, const void* i3,
                                                     const void* i4, const void* i5,
@@ -368,7 +401,6 @@ __global__ void __launch_bounds__(256) fused_kernel(Layout L, IdxT ngroups, Fuse
   __syncthreads();
   const int nsteps = P.n_steps;
   const int ir = L.rank - 1;
-  const int res_reg = P.code[P.n_steps - 1][1];
   for (IdxT g = blockIdx.x * (IdxT)blockDim.x + threadIdx.x; g < ngroups;
        g += (IdxT)gridDim.x * blockDim.x) {
     int64_t off[NIN + 1];
@@ -426,34 +458,23 @@ __global__ void __launch_bounds__(256) fused_kernel(Layout L, IdxT ngroups, Fuse
       }
       r[c.y] = o;
     }
-    const Vec<V> res = r[res_reg];
-    Tout* q = out + off[0];
-    if (V == 4 && (modes & 3) == 0) {
-      if constexpr (std::is_same<Tout, uint8_t>::value)
-        *reinterpret_cast<uchar4*>(q) = make_uchar4(res.v[0] != 0.f, res.v[1] != 0.f,
-                                                    res.v[2] != 0.f, res.v[3] != 0.f);
-      else *reinterpret_cast<float4*>(q) = make_float4(res.v[0], res.v[1], res.v[2], res.v[3]);
-    } else {
-      const int64_t in = L.st[0][ir];
-#pragma unroll
-      for (int j = 0; j < V; ++j) {
-        if constexpr (std::is_same<Tout, uint8_t>::value) q[j * in] = (uint8_t)(res.v[j] != 0.f);
-        else q[j * in] = res.v[j];
-      }
-    }
+    // outputs share one dense layout: operand 0's offsets
+    const bool vec = (modes & 3) == 0;
+    for (int k = 0; k < P.n_out; ++k)
+      store_v<V>(outs.p[k], P.out_dt[k], off[0], L.st[0][ir], vec, r[P.out_reg[k]]);
   }
 }
 #undef PFB_EW1
 #undef PFB_EW2
 
-template <int V, typename IdxT, typename Tout>
+template <int V, typename IdxT>
 void launch_fused(int n_in, const Layout& L, IdxT ngroups, const FusedProgram& P, uint32_t modes,
-                  Tout* out, const void* const* p, cudaStream_t s) {
+                  const FusedOuts& outs, const void* const* p, cudaStream_t s) {
   const int grid = grid_for((int64_t)ngroups, 256);
 #define PFB_FUSED_CASE(K)                                                                      \
   case K:                                                                                      \
-    launch(fused_kernel<IdxT, Tout, K, V>, grid, 256, 0, s, L, ngroups, P, modes, out, p[0],   \
-           p[1], p[2], p[3], p[4], p[5], p[6], p[7]);                                          \
+    launch(fused_kernel<IdxT, K, V>, grid, 256, 0, s, L, ngroups, P, modes, outs, p[0], p[1],  \
+           p[2], p[3], p[4], p[5], p[6], p[7]);                                                \
     break;
   switch (n_in) {
     PFB_FUSED_CASE(1) PFB_FUSED_CASE(2) PFB_FUSED_CASE(3) PFB_FUSED_CASE(4)
@@ -549,10 +570,20 @@ extern "C" int pfb_fill(pfb_tensor* out, double value, void* stream) {
   return launch_status();
 }
 
-extern "C" int pfb_fused_ew(int32_t n_in, const pfb_tensor* ins, int32_t n_steps,
-                            const int32_t* program, pfb_tensor* out, void* stream) {
+static int fused_impl(int32_t n_in, const pfb_tensor* ins, int32_t n_steps,
+                      const int32_t* program, int32_t n_out, const int32_t* out_regs,
+                      pfb_tensor* outs, void* stream) {
   if (n_in < 1 || n_in > 8 || n_steps < 1 || n_steps > kMaxSteps) return PFB_E_ARG;
-  if (out->dtype != PFB_F32 && out->dtype != PFB_BOOL) return PFB_E_DTYPE;
+  if (n_out < 1 || n_out > kMaxOuts) return PFB_E_ARG;
+  const pfb_tensor* out = &outs[0];
+  for (int k = 0; k < n_out; ++k) {
+    if (outs[k].dtype != PFB_F32 && outs[k].dtype != PFB_BOOL) return PFB_E_DTYPE;
+    if (outs[k].rank != out->rank) return PFB_E_SHAPE;
+    for (int d = 0; d < out->rank; ++d)
+      if (outs[k].shape[d] != out->shape[d] || (out->shape[d] > 1 && outs[k].stride[d] != out->stride[d]))
+        return PFB_E_SHAPE;
+    if (out_regs[k] < 0 || out_regs[k] >= kMaxRegs) return PFB_E_ARG;
+  }
   int64_t stb[8][kMaxRank];
   const int64_t* st[kMaxOps];
   st[0] = out->stride;
@@ -570,6 +601,13 @@ extern "C" int pfb_fused_ew(int32_t n_in, const pfb_tensor* ins, int32_t n_steps
     for (int j = 0; j < 4; ++j) P.code[s][j] = program[4 * s + j];
     if (P.code[s][1] < 0 || P.code[s][1] >= kMaxRegs) return PFB_E_ARG;
   }
+  FusedOuts fo;
+  P.n_out = n_out;
+  for (int k = 0; k < kMaxOuts; ++k) {
+    fo.p[k] = k < n_out ? outs[k].data : nullptr;
+    P.out_reg[k] = k < n_out ? out_regs[k] : 0;
+    P.out_dt[k] = k < n_out ? outs[k].dtype : PFB_F32;
+  }
   Layout L = make_layout(out->rank, out->shape, n_in + 1, st);
   int64_t n = numel(out);
   if (n == 0) return 0;
@@ -580,22 +618,45 @@ extern "C" int pfb_fused_ew(int32_t n_in, const pfb_tensor* ins, int32_t n_steps
   const int ir = L.rank - 1;
   static const bool scalar_only = getenv_flag("PFB_FUSED_SCALAR");
   const bool v4 = L.shape[ir] % 4 == 0 && !scalar_only;
-  // per-operand feed mode
+  // per-operand feed mode; the outputs share operand 0's (all must be aligned)
   uint32_t modes = 0;
   for (int o = 0; o <= n_in; ++o) {
-    const void* base = o == 0 ? out->data : ins[o - 1].data;
-    const int dt = o == 0 ? out->dtype : ins[o - 1].dtype;
-    const int64_t esz = dt == PFB_F32 ? 4 : 1;
-    bool vec = v4 && L.st[o][ir] == 1 && (reinterpret_cast<uintptr_t>(base) % (4 * esz)) == 0;
+    bool vec = v4 && L.st[o][ir] == 1;
+    if (o == 0) {
+      for (int k = 0; k < n_out && vec; ++k) {
+        const int64_t esz = outs[k].dtype == PFB_F32 ? 4 : 1;
+        vec = (reinterpret_cast<uintptr_t>(outs[k].data) % (4 * esz)) == 0;
+      }
+    } else {
+      const int64_t esz = ins[o - 1].dtype == PFB_F32 ? 4 : 1;
+      vec = vec && (reinterpret_cast<uintptr_t>(ins[o - 1].data) % (4 * esz)) == 0;
+    }
     for (int d = 0; d < ir && vec; ++d) vec = (L.st[o][d] % 4) == 0;
     const uint32_t m = (L.st[o][ir] == 0 && o > 0) ? 1u : (vec ? 0u : 2u);
     modes |= m << (2 * o);
   }
   const int64_t ng = v4 ? n / 4 : n;
-#define PFB_GO(VV)                                                                                if (out->dtype == PFB_F32) {                                                                      if (small) launch_fused<VV, uint32_t, float>(n_in, L, (uint32_t)ng, P, modes, (float*)out->data, p, s);     else launch_fused<VV, int64_t, float>(n_in, L, ng, P, modes, (float*)out->data, p, s);       } else {                                                                                          if (small) launch_fused<VV, uint32_t, uint8_t>(n_in, L, (uint32_t)ng, P, modes, (uint8_t*)out->data, p, s);     else launch_fused<VV, int64_t, uint8_t>(n_in, L, ng, P, modes, (uint8_t*)out->data, p, s);   }
-  if (v4) { PFB_GO(4) } else { PFB_GO(1) }
-#undef PFB_GO
+  if (v4) {
+    if (small) launch_fused<4, uint32_t>(n_in, L, (uint32_t)ng, P, modes, fo, p, s);
+    else launch_fused<4, int64_t>(n_in, L, ng, P, modes, fo, p, s);
+  } else {
+    if (small) launch_fused<1, uint32_t>(n_in, L, (uint32_t)ng, P, modes, fo, p, s);
+    else launch_fused<1, int64_t>(n_in, L, ng, P, modes, fo, p, s);
+  }
   return launch_status();
+}
+
+extern "C" int pfb_fused_ew(int32_t n_in, const pfb_tensor* ins, int32_t n_steps,
+                            const int32_t* program, pfb_tensor* out, void* stream) {
+  if (n_steps < 1 || n_steps > kMaxSteps) return PFB_E_ARG;
+  const int32_t last = program[4 * (n_steps - 1) + 1];
+  return fused_impl(n_in, ins, n_steps, program, 1, &last, out, stream);
+}
+
+extern "C" int pfb_fused_ew_multi(int32_t n_in, const pfb_tensor* ins, int32_t n_steps,
+                                  const int32_t* program, int32_t n_out, const int32_t* out_regs,
+                                  pfb_tensor* outs, void* stream) {
+  return fused_impl(n_in, ins, n_steps, program, n_out, out_regs, outs, stream);
 }
 
 // ---------------------------------------------------------------------------

@@ -48,6 +48,7 @@ constexpr int EPI_WARPS = 8;                      // 2 per TMEM lane quarter, 64
 constexpr int EPI_COLS = BN / 2;
 constexpr int EPI_STAGE_FLOATS = 32 * 32;         // per epilogue warp: one 32x32 block,
                                                   // 16B chunks XOR-swizzled by row
+// layout: [stages][epilogue staging, 4 KB per warp, 1 KB aligned for TMA][barriers]
 constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + 1024 /*align*/ + 256 /*barriers*/ +
                            EPI_WARPS * EPI_STAGE_FLOATS * 4;
 constexpr int NUM_THREADS = 64 + 32 * EPI_WARPS;  // TMA, MMA, 8 epilogue warps
@@ -81,6 +82,15 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
       "@!P1 bra WAIT_%=;\n\t"
       "}" ::"r"(addr),
       "r"(parity)
+      : "memory");
+}
+
+__device__ __forceinline__ void tma_store_3d(const CUtensorMap* map, const void* src, int c0,
+                                             int c1, int c2) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.global.shared::cta.bulk_group [%0, {%2, %3, %4}], [%1];" ::"l"(
+          reinterpret_cast<uint64_t>(map)),
+      "r"(smem_u32(src)), "r"(c0), "r"(c1), "r"(c2)
       : "memory");
 }
 
@@ -209,6 +219,7 @@ struct Params {
   int64_t sxb, sxm, sxn;
   int act;
   uint32_t mn_lbo, mn_sbo;  // MN-major descriptor strides (4 KB, 512 B)
+  int tma_store;            // epilogue stores 32x32 blocks with TMA (map_c)
 };
 
 __device__ __forceinline__ void epi4(const Params& p, int bz, int row, int col, float4& v) {
@@ -292,12 +303,13 @@ __device__ __forceinline__ void split_tile_smem(uint8_t* hi, uint8_t* lo, int t)
 __global__ void __launch_bounds__(NUM_THREADS, 1)
 gemm_kernel(const __grid_constant__ CUtensorMap map_ah, const __grid_constant__ CUtensorMap map_al,
             const __grid_constant__ CUtensorMap map_bh, const __grid_constant__ CUtensorMap map_bl,
-            Params p) {
+            const __grid_constant__ CUtensorMap map_c, Params p) {
   pdl_enter();
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>(
       (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + STAGES * STAGE_BYTES);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + STAGES * STAGE_BYTES +
+                                               EPI_WARPS * EPI_STAGE_FLOATS * 4);
   uint64_t* full = bars;                   // [STAGES] TMA -> (split) -> MMA
   uint64_t* empty = bars + STAGES;         // [STAGES] MMA -> TMA
   uint64_t* ready = bars + 2 * STAGES;     // [STAGES] smem split -> MMA
@@ -415,7 +427,7 @@ gemm_kernel(const __grid_constant__ CUtensorMap map_ah, const __grid_constant__ 
     const int quarter = warp & 3;
     const int half = (warp - 2) >> 2;
     const int et = threadIdx.x - 64;  // 0..255
-    float* stage = reinterpret_cast<float*>(smem + STAGES * STAGE_BYTES + 256) +
+    float* stage = reinterpret_cast<float*>(smem + STAGES * STAGE_BYTES) +
                    (warp - 2) * EPI_STAGE_FLOATS;
     int gc = 0, gs = 0;
     auto split_stage = [&]() {
@@ -477,9 +489,37 @@ gemm_kernel(const __grid_constant__ CUtensorMap map_ah, const __grid_constant__ 
         }
         continue;
       }
+      const int row0 = m0 + quarter * 32;
+      if (p.tma_store) {
+        // the staging block's XOR layout is TMA's SWIZZLE_128B: write the
+        // finished 32x32 block, one bulk tensor store per block (bounds
+        // clipped by the map), staging reuse gated on the bulk read
+        const int grow = row0 + lane;
+        const float alpha =
+            (p.alpha_rows && grow < p.M) ? __ldg(p.alpha_rows + (int64_t)bz * p.M + grow) : 1.f;
+#pragma unroll
+        for (int cc = 0; cc < EPI_COLS; cc += 32) {
+          if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+          __syncwarp();
+          const int col0 = n0 + half * EPI_COLS + cc;
+#pragma unroll
+          for (int q = 0; q < 8; ++q) {
+            float4 v = make_float4(acc[cc + 4 * q] * alpha, acc[cc + 4 * q + 1] * alpha,
+                                   acc[cc + 4 * q + 2] * alpha, acc[cc + 4 * q + 3] * alpha);
+            if (grow < p.M) epi4(p, bz, grow, col0 + 4 * q, v);
+            *reinterpret_cast<float4*>(stage + lane * 32 + 4 * (q ^ (lane & 7))) = v;
+          }
+          asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+          __syncwarp();
+          if (lane == 0) {
+            tma_store_3d(&map_c, stage, col0, row0, bz);
+            asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+          }
+        }
+        continue;
+      }
       // 32x32 blocks through smem: each lane writes its row as float4s, then
       // every store instruction covers 4 rows x 128 contiguous bytes
-      const int row0 = m0 + quarter * 32;
       float* cbase = p.C + bz * p.scb;
       const int64_t ldm = p.scm, ldn = p.scn;
       const int sub_r = lane >> 3, sub_c = (lane & 7) * 4;
@@ -529,6 +569,8 @@ gemm_kernel(const __grid_constant__ CUtensorMap map_ah, const __grid_constant__ 
       }
     }
   }
+  if (p.tma_store && warp >= 2 && lane == 0)
+    asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
   asm volatile("tcgen05.fence::before_thread_sync;");
   __syncthreads();
   if (clustered) {
@@ -786,11 +828,24 @@ int gemm_tcgen05(const GemmArgs& g, void* ws, int64_t ws_bytes, cudaStream_t s, 
   }
   int ksplit, kb_per;
   choose_split(g, &ksplit, &kb_per);
+  // TMA-store epilogue: C row-major with 16-byte aligned rows, overwrite
+  CUtensorMap mc = mah;
+  int tma_store = 0;
+  if (ksplit == 1 && !g.accumulate && g.scn == 1 && (g.N == 1 || (g.scm * 4) % 16 == 0) &&
+      (g.batch == 1 || (g.scb * 4) % 16 == 0) &&
+      (reinterpret_cast<uintptr_t>(g.C) & 15) == 0 && !getenv_flag("PFB_NO_TMA_STORE")) {
+    const int64_t ldc = g.M == 1 ? (g.N + 3) / 4 * 4 : g.scm;
+    cuuint64_t dims[3] = {(cuuint64_t)g.N, (cuuint64_t)g.M, (cuuint64_t)g.batch};
+    cuuint64_t strides[2] = {(cuuint64_t)(ldc * 4),
+                             (cuuint64_t)((g.batch == 1 ? ldc * g.M : g.scb) * 4)};
+    cuuint32_t box[3] = {32, 32, 1};
+    tma_store = encode(&mc, g.C, dims, strides, box) ? 1 : 0;
+  }
   const uint32_t idesc = kIdesc | ((uint32_t)(am == kRawMN) << 15) | ((uint32_t)(bm == kRawMN) << 16);
   Params p{(int)g.M, (int)g.N, (int)Kp, (int)g.batch,
            (int)((g.M + BM - 1) / BM), (int)((g.N + BN - 1) / BN), a_bc, b_bc, am, bm, idesc,
            g.C, g.scb, g.scm, g.scn, g.alpha_rows, g.accumulate, ksplit, kb_per,
-           g.bias, g.sxb, g.sxm, g.sxn, g.act, 4096u, 512u};
+           g.bias, g.sxb, g.sxm, g.sxn, g.act, 4096u, 512u, tma_store};
   const int64_t units = (int64_t)p.ntm * p.ntn * g.batch * ksplit;
   if (ksplit > 1) {
     // one CTA per (tile, k-split); the k-splits of a tile are one cluster
@@ -808,10 +863,10 @@ int gemm_tcgen05(const GemmArgs& g, void* ws, int64_t ws_bytes, cudaStream_t s, 
     at[1].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = at;
     cfg.numAttrs = pdl_enabled() ? 2 : 1;
-    cudaLaunchKernelEx(&cfg, gemm_kernel, mah, mal, mbh, mbl, p);
+    cudaLaunchKernelEx(&cfg, gemm_kernel, mah, mal, mbh, mbl, mc, p);
   } else {
     const int grid = (int)std::min<int64_t>(units, num_sms());
-    launch(gemm_kernel, grid, NUM_THREADS, SMEM_BYTES, s, mah, mal, mbh, mbl, p);
+    launch(gemm_kernel, grid, NUM_THREADS, SMEM_BYTES, s, mah, mal, mbh, mbl, mc, p);
   }
   return launch_status();
 }

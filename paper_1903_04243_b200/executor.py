@@ -1221,6 +1221,28 @@ def _h_fused(ex, node, ins):
     return [out]
 
 
+def _h_fused_multi(ex, node, ins):
+    """fused_ewm (passes.fuse_elementwise, multi-output groups): one launch,
+    several same-shape outputs (pfb_fused_ew_multi)."""
+    arrs = [ex._dev(v) for v in ins]
+    shape = ()
+    for a in arrs:
+        shape = broadcast_shapes(shape, a.shape)
+    outs = [ex._empty(shape, dt) for dt in node.attrs["out_dtypes"]]
+    prog = ex._programs.get(id(node))
+    if prog is None:
+        flat = [int(x) for step in node.attrs["program"] for x in step]
+        regs = [int(r) for r in node.attrs["out_regs"]]
+        prog = ex._programs[id(node)] = ((ctypes.c_int32 * len(flat))(*flat),
+                                         len(node.attrs["program"]),
+                                         (ctypes.c_int32 * len(regs))(*regs), len(regs))
+    descs = (N.PfbTensor * len(arrs))(*[a.desc() for a in arrs])
+    odescs = (N.PfbTensor * len(outs))(*[o.desc() for o in outs])
+    ex._call(ex._lib.pfb_fused_ew_multi, len(arrs), descs, prog[1], prog[0], prog[3], prog[2],
+             odescs, ex._stream, what="fused_ew", work=(_abytes(*arrs, *outs), 0))
+    return outs
+
+
 def _h_reduce_dot(ex, node, ins):
     x, y = (ex._dev(v) for v in ins)
     axes = normalize_axes(node.attrs["axes"], x.rank)
@@ -1296,6 +1318,7 @@ _HANDLERS.update({
     "im2col": _h_im2col, "reduce_sum": _h_reduce_sum, "concat": _h_concat, "stack": _h_stack,
     "matmul_ep": _h_matmul_ep,
     "row_dots": _h_row_dots,
+    "fused_ewm": _h_fused_multi,
     "gather_rows": _h_gather, "scatter_rows": _h_scatter_rows,
     "scatter_add_rows": _h_scatter_add, "reshape": _h_reshape, "transpose": _h_transpose,
     "slice_leading": _h_slice_leading, "tile_leading": _h_tile_leading,

@@ -506,8 +506,9 @@ def _const_scalar_f(g, key):
     return None
 
 
-def _program(g, order, root, externals):
-    """Register program for the group `order` (topo order, root last)."""
+def _program(g, order, root, externals, outputs=()):
+    """Register program for the group `order` (topo order, root last).
+    Registers of `outputs` (node ids) are kept to the end of the program."""
     import struct
     from .tensor import DType
     ext_index = {k: i for i, k in enumerate(externals)}
@@ -518,6 +519,7 @@ def _program(g, order, root, externals):
     free = list(range(MAX_REGS - 1, -1, -1))
     reg = {}
     steps = []
+    pinned = {(i, 0) for i in outputs}
 
     def operand(src):
         if src in reg:
@@ -544,12 +546,12 @@ def _program(g, order, root, externals):
             steps.append((OP_MOV, dst, ops[2], ops[2]))
             steps.append((OP_SELECT, dst, ops[0], ops[1]))
             for src in set(n.inputs):
-                if last_use.get(src) == i and src in reg:
+                if last_use.get(src) == i and src in reg and src not in pinned:
                     free.append(reg.pop(src))
             reg[(n.id, 0)] = dst
             continue
         for src in set(n.inputs):
-            if last_use.get(src) == i and src in reg:
+            if last_use.get(src) == i and src in reg and src not in pinned:
                 free.append(reg.pop(src))
         if not free:
             raise OverflowError
@@ -566,13 +568,23 @@ def _program(g, order, root, externals):
         reg[(n.id, 0)] = dst
     if len(steps) > MAX_STEPS:
         raise OverflowError
+    if outputs:
+        return tuple(steps), tuple(reg[(i, 0)] for i in outputs)
     return tuple(steps)
 
 
+MAX_OUTPUTS = 8
+
+
 def fuse_elementwise(g, keep=()):
-    """Replace single-output elementwise chains (same output shape, interior
-    values used only inside the chain) by `fused_ew` nodes.  Returns the
-    number of groups fused and the moved requested outputs."""
+    """Replace elementwise groups (same output shape) by `fused_ew` nodes.
+    A producer whose value is also read outside the group is absorbed when
+    every such outside reader comes after the group's root in topological
+    order (so the fused node cannot be on a cycle); it then becomes an extra
+    output of a multi-output `fused_ewm` node.  Groups whose register program
+    does not fit fall back to the single-output rule (interior values read
+    only inside the group).  Returns the number of groups fused and the moved
+    requested outputs."""
     keep = set(keep)
     topo = g.topo_order()
     live = live_set(g, keep)
@@ -586,10 +598,10 @@ def fuse_elementwise(g, keep=()):
     assigned = set()
     moved = {}
     fused = 0
-    for root in reversed(topo):
-        if root.id in assigned or root.id not in live or not _ew_eligible(g, root):
-            continue
+
+    def grow(root, multi):
         shape = root.out_shapes[0]
+        rpos = pos[root.id]
         group = {root.id}
         changed = True
         while changed:
@@ -597,18 +609,30 @@ def fuse_elementwise(g, keep=()):
             for nid in list(group):
                 for src in g.nodes[nid].inputs:
                     p = g.nodes[src[0]]
-                    if p.id in group or p.id in assigned or src in keep:
+                    if p.id in group or p.id in assigned or src[1] != 0:
                         continue
                     if not _ew_eligible(g, p) or p.out_shapes[0] != shape:
                         continue
-                    if not users.get(src, set()) <= group:
+                    outside = users.get(src, set()) - group
+                    if multi:
+                        if any(pos[u] <= rpos for u in outside):
+                            continue
+                        n_out = 1 + sum(1 for m in group if m != root.id and _is_out(m, group))
+                        if (outside or src in keep) and n_out + 1 > MAX_OUTPUTS:
+                            continue
+                    elif outside or src in keep:
                         continue
                     if len(group) + 1 > MAX_STEPS // 2:
                         continue
                     group.add(p.id)
                     changed = True
-        if len(group) < 2:
-            continue
+        return group
+
+    def _is_out(nid, group):
+        key = (nid, 0)
+        return key in keep or bool(users.get(key, set()) - group)
+
+    def build(root, group):
         order = sorted((g.nodes[i] for i in group), key=lambda n: pos[n.id])
         externals = []
         for n in order:
@@ -616,24 +640,51 @@ def fuse_elementwise(g, keep=()):
                 if src[0] not in group and src not in externals and _const_scalar_f(g, src) is None:
                     externals.append(src)
         if len(externals) > MAX_INPUTS:
-            continue
+            return None
+        extra = [n.id for n in order if n.id != root.id and _is_out(n.id, group)]
         try:
-            prog = _program(g, order, root, externals)
+            if not extra:
+                return order, externals, [root.id], _program(g, order, root, externals), None
+            outs = [root.id] + extra
+            prog, regs = _program(g, order, root, externals, outs)
+            return order, externals, outs, prog, regs
         except OverflowError:
+            return None
+
+    for root in reversed(topo):
+        if root.id in assigned or root.id not in live or not _ew_eligible(g, root):
             continue
-        new = g.add_node("fused_ew", externals,
-                         {"program": prog, "out_dtype": root.out_dtypes[0]})
+        group = grow(root, True)
+        built = build(root, group) if len(group) >= 2 else None
+        if built is None:
+            group = grow(root, False)
+            if len(group) < 2:
+                continue
+            built = build(root, group)
+            if built is None:
+                continue
+        order, externals, outs, prog, regs = built
+        if regs is None:
+            new = g.add_node("fused_ew", externals,
+                             {"program": prog, "out_dtype": root.out_dtypes[0]})
+        else:
+            new = g.add_node("fused_ewm", externals,
+                             {"program": prog, "out_regs": regs,
+                              "out_dtypes": tuple(g.nodes[i].out_dtypes[0] for i in outs)})
         live.add(new.id)
+        pos[new.id] = pos[root.id]
         for src in externals:  # the fused node now reads these (later groups redirect it)
             users.setdefault(src, set()).add(new.id)
             users[src] -= group
-        key = (root.id, 0)
-        for u in users.get(key, ()):
-            un = g.nodes[u]
-            un.inputs = [(new.id, 0) if s == key else s for s in un.inputs]
-        users[(new.id, 0)] = set(users.get(key, ()))
-        if key in keep:
-            moved[key] = (new.id, 0)
+        for k, nid in enumerate(outs):
+            key = (nid, 0)
+            ext = users.get(key, set()) - group
+            for u in ext:
+                un = g.nodes[u]
+                un.inputs = [(new.id, k) if s_ == key else s_ for s_ in un.inputs]
+            users[(new.id, k)] = set(ext)
+            if key in keep:
+                moved[key] = (new.id, k)
         assigned |= group
         fused += 1
     g._topo_cache = None

@@ -203,8 +203,11 @@ def _run_fused(env, a, b, force, bias=None, act=0, kscale=None):
     A = DArray.from_numpy(a, DType.F64, dev)
     B = DArray.from_numpy(b, DType.F64, dev)
     C = DArray.empty(a.shape[:-1] + (b.shape[-1],), DType.F64, dev)
-    bd = DArray.from_numpy(bias, DType.F64, dev).desc() if bias is not None else None
-    kd = DArray.from_numpy(kscale, DType.F64, dev).desc() if kscale is not None else None
+    # keep the device arrays alive until the kernel has run (a desc holds a raw pointer)
+    bias_d = DArray.from_numpy(bias, DType.F64, dev) if bias is not None else None
+    ks_d = DArray.from_numpy(kscale, DType.F64, dev) if kscale is not None else None
+    bd = bias_d.desc() if bias_d is not None else None
+    kd = ks_d.desc() if ks_d is not None else None
     ad, bdd, cd = A.desc(), B.desc(), C.desc()
     need = lib.pfb_matmul_workspace(ad, bdd, cd)
     ws = torch.empty(max(need, 256), dtype=torch.uint8, device=dev)
