@@ -147,6 +147,18 @@ int pfb_matmul_fused(const pfb_tensor* a, const pfb_tensor* b, pfb_tensor* out,
                      const float* alpha_rows, int32_t accumulate, int32_t force_path, void* ws,
                      int64_t ws_bytes, void* stream);
 
+/* device-resident while loops (csrc/loop.cu; reference interp.py:133-154 runs
+ * the loop on the host): a CUDA graph with a conditional WHILE node.  The
+ * caller captures a `head` graph (condition -> pfb_set_condition) and an
+ * `iter` graph (body, carried-state update, condition -> pfb_set_condition)
+ * using the handle from pfb_loop_create, then pfb_loop_finalize assembles
+ * head -> WHILE { iter } and each pfb_loop_launch runs the whole loop. */
+int pfb_loop_create(void** loop, uint64_t* handle);
+int pfb_set_condition(uint64_t handle, const void* flag, void* counter, void* stream);
+int pfb_loop_finalize(void* loop, void* head_graph, void* iter_graph);
+int pfb_loop_launch(void* loop, void* stream);
+int pfb_loop_destroy(void* loop);
+
 /* conv family (reference tensor.py:209-260), NHWC / HWIO, SAME, stride 1 */
 int pfb_im2col(const pfb_tensor* x, int32_t k1, int32_t k2, pfb_tensor* out, void* stream);
 int pfb_conv2d(const pfb_tensor* x, const pfb_tensor* f, pfb_tensor* out, void* stream);

@@ -55,6 +55,12 @@ _SIGNATURES = {
     "pfb_matmul": ([_P, _P, _P, _vp, _i64, _vp], ctypes.c_int),
     "pfb_matmul_ex": ([_P, _P, _P, _vp, _i32, _i32, _vp, _i64, _vp], ctypes.c_int),
     "pfb_concat": ([_i32, _P, _i32, _P, _vp], ctypes.c_int),
+    "pfb_loop_create": ([ctypes.POINTER(ctypes.c_void_p), ctypes.POINTER(ctypes.c_uint64)],
+                        ctypes.c_int),
+    "pfb_set_condition": ([ctypes.c_uint64, _vp, _vp, _vp], ctypes.c_int),
+    "pfb_loop_finalize": ([_vp, _vp, _vp], ctypes.c_int),
+    "pfb_loop_launch": ([_vp, _vp], ctypes.c_int),
+    "pfb_loop_destroy": ([_vp], ctypes.c_int),
     "pfb_row_dots": ([_i32, _P, _P, _P, _vp], ctypes.c_int),
     "pfb_matmul_fused": ([_P, _P, _P, _P, _P, _i32, _vp, _i32, _i32, _vp, _i64, _vp], ctypes.c_int),
     "pfb_im2col": ([_P, _i32, _i32, _P, _vp], ctypes.c_int),

@@ -258,7 +258,10 @@ class Executor:
         self.budget = budget
         self.check_errors = check_errors
         self.dispatch_count = 0
-        self.launch_count = 0
+        self._launches = 0
+        self._loops = {}
+        self._loop_warm = set()
+        self._loop_pending = []
         self.sync_count = 0
         self._exec_graph = None
         self._refmap = None
@@ -443,6 +446,110 @@ class Executor:
             self._ws, self._err, self._err_nodes, self._stream = saved
         return cap
 
+    # -- device-resident while loops (CUDA graph conditional WHILE node) -----------
+
+    def _device_loop(self, node, cg, bg, car, caps, feeds):
+        """Run a `while` entirely on the device: from its second execution on,
+        a capturable (pure, fixed-shape) cond/body pair becomes one CUDA graph
+        whose conditional WHILE node re-runs the captured body while the
+        captured condition (read on the device) holds -- no host round trip
+        per trip (csrc/loop.cu).  Returns the carried results, or None when
+        the loop must run on the host."""
+        if not (self.cuda_graph and self.kernel_timer is None and _DEVICE_LOOPS
+                and not torch.cuda.is_current_stream_capturing()
+                and all(isinstance(v, DArray) for v in car)
+                and all(isinstance(v, (DArray, HostVal)) for v in caps)
+                and self._capturable(cg, [tuple(o) for o in cg.outputs])
+                and self._capturable(bg, [tuple(o) for o in bg.outputs])):
+            return None
+        sig = (id(node),
+               tuple((v.ptr, v.shape, v.strides, v.dtype) if isinstance(v, DArray)
+                     else ("host", id(v), v.value.tobytes(), v.dtype) for v in caps),
+               tuple((v.shape, v.dtype) for v in car))
+        lp = self._loops.get(sig)
+        if lp is None:
+            if sig not in self._loop_warm:
+                self._loop_warm.add(sig)
+                return None
+            lp = self._build_loop(cg, bg, car, caps, feeds, sig)
+            if lp is None:
+                return None
+        for src, dst in zip(car, lp.state):
+            if src.size:
+                self._call(self._lib.pfb_copy, src.desc(), dst.desc(), self._stream, what="copy")
+        _raise_status(self._lib.pfb_loop_launch(lp.ptr, self._stream), "while")
+        self._loop_pending.append(lp)
+        if lp.err_nodes:
+            self._used_caps[id(lp)] = lp
+        # detach the results from the loop's static state (rewritten next run)
+        return [self._dense_copy(v) for v in lp.state]
+
+    def _build_loop(self, cg, bg, car, caps, feeds, sig):
+        import ctypes
+        state = [DArray.empty(v.shape, v.dtype, self.device) for v in car]
+        loop, handle = ctypes.c_void_p(), ctypes.c_uint64()
+        if self._lib.pfb_loop_create(ctypes.byref(loop), ctypes.byref(handle)) != 0:
+            return None
+        counter = torch.zeros(1, dtype=torch.int64, device=self.device)
+        saved = (self._ws, self._err, self._err_nodes, self._stream)
+        self._ws = None
+        self._err = torch.zeros(_ERR_SLOTS, dtype=torch.int32, device=self.device)
+        self._err_nodes = []
+        head = torch.cuda.CUDAGraph(keep_graph=True)
+        it = torch.cuda.CUDAGraph(keep_graph=True)
+        lp = None
+        l0 = self.launch_count  # captured launches are not executions: restored below
+        try:
+            for src, dst in zip(car, state):
+                if src.size:
+                    self._call(self._lib.pfb_copy, src.desc(), dst.desc(), self._stream,
+                               what="copy")
+            torch.cuda.synchronize(self.device)
+            bind = {"capture": list(caps), "carried": state}
+
+            def cond_to_handle():
+                cenv = self._run_graph(cg, bind, feeds)
+                flag = cenv[tuple(cg.outputs[0])]
+                if not isinstance(flag, DArray) or flag.dtype != DType.BOOL or flag.size != 1:
+                    raise RuntimeError("loop condition is not a device bool scalar")
+                _raise_status(self._lib.pfb_set_condition(handle.value, flag.ptr,
+                                                          counter.data_ptr(), self._stream),
+                              "while")
+
+            with torch.cuda.graph(head):
+                self._stream = torch.cuda.current_stream(self.device).cuda_stream
+                cond_to_handle()
+            l1 = self.launch_count
+            with torch.cuda.graph(it, pool=head.pool()):
+                self._stream = torch.cuda.current_stream(self.device).cuda_stream
+                benv = self._run_graph(bg, bind, feeds)
+                outs = [benv[tuple(o)] for o in bg.outputs]
+                if not all(isinstance(v, DArray) for v in outs):
+                    raise RuntimeError("loop body result is not on the device")
+                for src, dst in zip(outs, state):
+                    if src.size and (src.ptr != dst.ptr or src.strides != dst.strides):
+                        self._call(self._lib.pfb_copy, src.desc(), dst.desc(), self._stream,
+                                   what="copy")
+                cond_to_handle()
+            l2 = self.launch_count
+            rc = self._lib.pfb_loop_finalize(loop, ctypes.c_void_p(head.raw_cuda_graph()),
+                                             ctypes.c_void_p(it.raw_cuda_graph()))
+            if rc != 0:
+                raise RuntimeError(f"pfb_loop_finalize failed ({rc})")
+            lp = _DeviceLoop(loop.value, state, counter, (head, it), self._ws, self._err,
+                             list(self._err_nodes))
+            lp.head_launches, lp.iter_launches = l1 - l0 + 1, l2 - l1 + 1
+            self._launches = l0
+            self._loops[sig] = lp
+        except Exception as e:  # the loop stays on the host
+            self.capture_failures.append(f"device loop: {type(e).__name__}: {e}")
+            self._launches = l0
+            self._lib.pfb_loop_destroy(loop)
+            torch.cuda.synchronize(self.device)
+        finally:
+            self._ws, self._err, self._err_nodes, self._stream = saved
+        return lp
+
     def _load_feeds(self, static, feeds):
         for name, dst in static.items():
             v = feeds[name]
@@ -501,6 +608,24 @@ class Executor:
         for name, tv in self.store.values.items():
             if name not in self._dvars:
                 self._dvars[name] = self._upload(tv)
+
+    @property
+    def launch_count(self):
+        """Kernels launched so far.  Device-resident loops run an unknown
+        number of trips; their invocation counters are folded in here (one
+        small device read, only when this is queried)."""
+        if self._loop_pending:
+            pend, self._loop_pending = self._loop_pending, []
+            for lp in set(pend):
+                runs = pend.count(lp)
+                now = int(lp.counter.item())
+                calls, lp.counter_seen = now - lp.counter_seen, now
+                self._launches += runs * lp.head_launches + (calls - runs) * lp.iter_launches
+        return self._launches
+
+    @launch_count.setter
+    def launch_count(self, v):
+        self._launches = v
 
     def _ws_get(self, nbytes):
         nbytes = max(int(nbytes), 256)
@@ -652,6 +777,9 @@ class Executor:
             car = [env[r] for r in node.inputs[:nc]]
             caps = [env[r] for r in node.inputs[nc:]]
             cg, bg = node.block.subgraphs["cond"], node.block.subgraphs["body"]
+            res = self._device_loop(node, cg, bg, car, caps, feeds)
+            if res is not None:
+                return res
             replayed = False
             while True:
                 bind = {"capture": caps, "carried": car}
@@ -705,6 +833,21 @@ class Executor:
         if tv.rank == 0 and dtype != DType.F64:
             return HostVal(tv.data, dtype)
         return self._upload(tv)
+
+
+class _DeviceLoop:
+    """A built device-resident loop: native handle, static carried state, the
+    captured head/iter graphs (kept alive: their memory pool holds the
+    loop's intermediates) and the invocation counter."""
+
+    def __init__(self, ptr, state, counter, graphs, ws, err, err_nodes):
+        self.ptr, self.state, self.counter, self.graphs = ptr, state, counter, graphs
+        self.ws, self.err, self.err_nodes = ws, err, err_nodes
+        self.counter_seen = 0
+        self.head_launches = self.iter_launches = 0
+
+
+_DEVICE_LOOPS = os.environ.get("PFB_DEVICE_LOOPS", "1") != "0"
 
 
 class _Captured:

@@ -242,14 +242,41 @@ def test_fusion_reduces_launches(Executor):
 @pytest.mark.parametrize("unroll", [1, 4])
 @pytest.mark.parametrize("name", ["cfg5", "cfg5_mid"])
 def test_masked_control_flow_vs_reference(name, unroll, golden, Executor):
-    """Predicated while/cond (fixed shapes) on device: reference values, and the
-    loop body is captured as a CUDA graph and replayed per trip."""
+    """Predicated while/cond (fixed shapes) on device: reference values; run 1
+    is host-driven (its body captured and replayed per trip from trip 2), runs
+    2+ execute the whole loop as one CUDA graph with a conditional WHILE node."""
     from paper_1903_04243_b200 import workloads as WL
     _, kw = PROGRAM_CASES[name]
     w = WL.cfg5(WL.this_api(), masked=True, unroll=unroll, **kw)
     ex = Executor(w.graph)
-    for _ in range(3):
+    counts = []
+    for _ in range(4):
+        c0 = ex.launch_count
         outs = ex.run(feeds=w.feeds)
+        counts.append(ex.launch_count - c0)
         for j, o in enumerate(outs):
             check(o, golden["programs"][f"{name}/out/{j}"])
     assert ex._sub_captures, f"loop body not captured: {ex.capture_failures}"
+    assert ex._loops, f"device loop not built: {ex.capture_failures}"
+    # the device loop's launch accounting matches the host-driven run's
+    assert counts[2] == counts[3] and counts[2] > 0, counts
+
+
+def test_device_loop_host_loop_agree(Executor):
+    """Same program with device loops disabled (host-driven trips): identical
+    results, bit for bit (same kernels, same order)."""
+    from paper_1903_04243_b200 import executor as X
+    from paper_1903_04243_b200 import workloads as WL
+    w = WL.cfg5(WL.this_api(), masked=True, unroll=2, n=64, max_len=20, units=32)
+    ex = Executor(w.graph)
+    for _ in range(3):
+        dev = ex.run(feeds=w.feeds)
+    assert ex._loops, ex.capture_failures
+    saved = X._DEVICE_LOOPS
+    try:
+        X._DEVICE_LOOPS = False
+        host = Executor(w.graph).run(feeds=w.feeds)
+    finally:
+        X._DEVICE_LOOPS = saved
+    for a, b in zip(dev, host):
+        np.testing.assert_array_equal(np.asarray(a.data), np.asarray(b.data))

@@ -17,6 +17,10 @@ WANT = {
     "gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed": "dram_pct",
     "sm__throughput.avg.pct_of_peak_sustained_elapsed": "sm_pct",
     "sm__pipe_tensor_cycles_active_realtime.avg.pct_of_peak_sustained_elapsed": "tensor_pct_rt",
+    "sm__pipe_tensor_subpipe_hmma_cycles_active_realtime.avg": "tensor_hmma_cycles",
+    "sm__mem_tensor_cycles_active.avg.pct_of_peak_sustained_elapsed": "tensor_mem_pct",
+    "sm__cycles_elapsed.avg": "cycles_elapsed",
+    "l1tex__data_pipe_tc_wavefronts_mem_shared.sum.pct_of_peak_sustained_elapsed": "tc_smem_pct",
     "sm__inst_executed_pipe_tensor_op_hmma.avg.pct_of_peak_sustained_active": "hmma_pct",
     "sm__warps_active.avg.pct_of_peak_sustained_active": "occupancy_pct",
     "launch__registers_per_thread": "registers",
@@ -35,6 +39,7 @@ def main(path, json_out=None):
     for r in rows[2:]:
         rec = {"kernel": r[hdr.index("Kernel Name")][:90]}
         for i, h in enumerate(hdr):
+            h = h.split(".", 2)[-1] if h.startswith(("TPC.", "SM_C.", "GPC.")) else h
             if h in WANT:
                 try:
                     v = float(r[i].replace(",", ""))
