@@ -218,6 +218,8 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-sweep", action="store_true")
+    ap.add_argument("--minimal", action="store_true",
+                    help="timed steps only (profiling runs under ncu): no e2e / roofline / sweep")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     if args.impl == "reference":
@@ -285,6 +287,12 @@ def main():
     dev_ms = float(t.item())
     ms_per_step = dev_ms / args.steps
     value = w.units * world * args.steps / (dev_ms / 1e3)
+
+    if args.minimal:
+        if rank == 0:
+            print(json.dumps({"metric": METRIC, "value": value, "ms_per_step": ms_per_step,
+                              "config": {"workload": args.config}, "minimal": True}))
+        return
 
     # end to end through the public API: pinned host feeds -> H2D -> run -> D2H
     h2d = sum(int(v.numel() * v.element_size()) for v in feeds_pinned.values())

@@ -262,6 +262,7 @@ class Executor:
         self._loops = {}
         self._loop_warm = set()
         self._loop_pending = []
+        self._feed_bufs = {}
         self.sync_count = 0
         self._exec_graph = None
         self._refmap = None
@@ -811,7 +812,7 @@ class Executor:
         if k == "placeholder":
             if a["name"] not in feeds:
                 raise E.PforVecError(f"missing feed for placeholder {a['name']!r}")
-            return [self._feed(feeds[a["name"]], a["dtype"])]
+            return [self._feed(a["name"], feeds[a["name"]], a["dtype"])]
         if k == "loop_var":
             return [binder["loop_var"]]
         if k == "capture":
@@ -823,16 +824,32 @@ class Executor:
             raise E.PforVecError(f"no evaluation rule for kind {k!r}")
         return h(self, node, ins)
 
-    def _feed(self, value, dtype):
+    def _feed(self, name, value, dtype):
+        """Placeholder value on the device.  Host feeds are copied into one
+        persistent buffer per placeholder (same address every run), so
+        captured loop bodies / device loops that read them stay valid."""
         if isinstance(value, DArray):
             return value
         if isinstance(value, torch.Tensor):
-            t = value.to(self.device, dtype=_TORCH[dtype], non_blocking=True).contiguous()
-            return DArray(t.reshape(-1), 0, tuple(t.shape), _dense_strides(t.shape), dtype)
-        tv = to_tensor(value, dtype)
-        if tv.rank == 0 and dtype != DType.F64:
-            return HostVal(tv.data, dtype)
-        return self._upload(tv)
+            if (value.device == self.device and value.dtype == _TORCH[dtype]
+                    and value.is_contiguous()):
+                # already resident: read in place (the caller owns its lifetime)
+                return DArray(value.reshape(-1), 0, tuple(value.shape),
+                              _dense_strides(value.shape), dtype)
+            src = value
+        else:
+            tv = to_tensor(value, dtype)
+            if tv.rank == 0 and dtype != DType.F64:
+                return HostVal(tv.data, dtype)
+            src = torch.from_numpy(np.require(np.asarray(tv.data, dtype=dtype.device_np_dtype),
+                                              requirements="C"))
+        shape = tuple(src.shape)
+        buf = self._feed_bufs.get(name)
+        if buf is None or buf.shape != shape or buf.dtype != dtype:
+            buf = self._feed_bufs[name] = DArray.empty(shape, dtype, self.device)
+        if buf.size:
+            buf.torch_view().copy_(src, non_blocking=True)
+        return buf
 
 
 class _DeviceLoop:
