@@ -93,6 +93,11 @@ void save_choice(const ShapeKey& k, int path) {
   fclose(f);
 }
 
+bool tc_pair_off() {
+  static const bool off = getenv_flag("PFB_DISABLE_PAIR");
+  return off;
+}
+
 bool autotune_enabled() {
   static const bool on = [] {
     const char* e = getenv("PFB_GEMM_AUTOTUNE");
@@ -106,6 +111,8 @@ int run_path(const GemmArgs& g, int path, void* ws, int64_t ws_bytes, cudaStream
     case 1: return gemm_simt(g, ws, ws_bytes, s);
     case 3: return gemm_tcgen05(g, ws, ws_bytes, s, 1);
     case 4: return gemm_tcgen05(g, ws, ws_bytes, s, 2);
+    case 5: return gemm_tcgen05_pair(g, ws, ws_bytes, s, 1);
+    case 6: return gemm_tcgen05_pair(g, ws, ws_bytes, s, 2);
     default: return gemm_tcgen05(g, ws, ws_bytes, s, 0);
   }
 }
@@ -195,10 +202,11 @@ static int matmul_impl(GemmArgs& g, pfb_tensor* out, int32_t force_path, void* w
     return launch_status();
   }
   // force_path: 0 = auto, 1 = SIMT, 2 = tcgen05 (error if ineligible),
-  // 3 = tcgen05 with pre-split operands, 4 = tcgen05 with the raw TMA feed.
+  // 3 = tcgen05 with pre-split operands, 4 = tcgen05 with the raw TMA feed,
+  // 5 / 6 = CTA-pair tcgen05 (cta_group::2) with pre-split / raw operands.
   // PFB_DISABLE_TCGEN05=1 pins auto to SIMT (A/B testing, bring-up).
   static const bool tc_off = getenv("PFB_DISABLE_TCGEN05") && getenv("PFB_DISABLE_TCGEN05")[0] == '1';
-  if (force_path >= 1 && force_path <= 4) return run_path(g, force_path, ws, ws_bytes, s);
+  if (force_path >= 1 && force_path <= 6) return run_path(g, force_path, ws, ws_bytes, s);
   const bool tc_ok = !tc_off && gemm_tcgen05_eligible(g) &&
                      ws_bytes >= gemm_tcgen05_workspace(g) && ws != nullptr &&
                      (double)g.batch * g.M * g.N * g.K >= (double)(1 << 20);
@@ -215,8 +223,15 @@ static int matmul_impl(GemmArgs& g, pfb_tensor* out, int32_t force_path, void* w
     cudaStreamIsCapturing(s, &st);
     if (autotune_enabled() && !accumulate && st == cudaStreamCaptureStatusNone) {
       // every candidate runs twice; the last one timed leaves C computed
-      int cand[3] = {1, 3, 4};
-      const int ncand = gemm_tcgen05_raw_possible(g) ? 3 : 2;
+      int cand[5];
+      int ncand = 0;
+      cand[ncand++] = 1;
+      cand[ncand++] = 3;
+      if (gemm_tcgen05_raw_possible(g)) cand[ncand++] = 4;
+      if (g.M > 128 && !tc_pair_off()) {
+        cand[ncand++] = 5;
+        if (gemm_tcgen05_raw_possible(g)) cand[ncand++] = 6;
+      }
       float best = 1e30f;
       for (int i = 0; i < ncand; ++i) {
         const float t = time_path(g, cand[i], ws, ws_bytes, s);

@@ -55,5 +55,12 @@ int64_t gemm_tcgen05_workspace(const GemmArgs& g);
 bool gemm_tcgen05_eligible(const GemmArgs& g);    // layout constraints
 bool gemm_tcgen05_raw_possible(const GemmArgs& g);
 bool gemm_tcgen05_profitable(const GemmArgs& g);  // size heuristic for auto
+// CTA-pair (cta_group::2) kernel: 256-row pair tiles, N tile 128 or 256;
+// variant 1 = pre-split planes, 2 = raw TMA feed where the layout allows it
+int gemm_tcgen05_pair(const GemmArgs& g, void* ws, int64_t ws_bytes, cudaStream_t s, int variant);
+// dense K-major hi/lo tf32 planes [batch][rows][Kp] of an operand view
+void tc_split_launch(const float* x, int64_t batch, int64_t rows, int64_t K, int64_t Kp, int64_t sb,
+                     int64_t sr, int64_t sk, float* hi, float* lo, const float* kscale,
+                     int64_t skb, int64_t skk, cudaStream_t s);
 
 }  // namespace pfb

@@ -36,6 +36,7 @@
 #include <cmath>
 
 #include "gemm.cuh"
+#include "tc_ptx.cuh"
 
 namespace pfb {
 namespace tc {
@@ -54,106 +55,9 @@ constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + 1024 /*align*/ + 256 /*barrier
 constexpr int NUM_THREADS = 64 + 32 * EPI_WARPS;  // TMA, MMA, 8 epilogue warps
 constexpr int TMEM_COLS = 2 * BN;                 // double-buffered chunk accumulator
 
-__device__ __forceinline__ uint32_t smem_u32(const void* p) {
-  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
-}
-
-__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
-  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
-}
-
-__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
-  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
-               "r"(bytes)
-               : "memory");
-}
-
-__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
-  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
-}
-
-__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
-  uint32_t addr = smem_u32(bar);
-  asm volatile(
-      "{\n\t"
-      ".reg .pred P1;\n\t"
-      "WAIT_%=:\n\t"
-      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t"
-      "@!P1 bra WAIT_%=;\n\t"
-      "}" ::"r"(addr),
-      "r"(parity)
-      : "memory");
-}
-
-__device__ __forceinline__ void tma_store_3d(const CUtensorMap* map, const void* src, int c0,
-                                             int c1, int c2) {
-  asm volatile(
-      "cp.async.bulk.tensor.3d.global.shared::cta.bulk_group [%0, {%2, %3, %4}], [%1];" ::"l"(
-          reinterpret_cast<uint64_t>(map)),
-      "r"(smem_u32(src)), "r"(c0), "r"(c1), "r"(c2)
-      : "memory");
-}
-
-__device__ __forceinline__ void tma_load_3d(const CUtensorMap* map, uint64_t* bar, void* dst,
-                                            int c0, int c1, int c2) {
-  asm volatile(
-      "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes"
-      " [%0], [%1, {%3, %4, %5}], [%2];" ::"r"(smem_u32(dst)),
-      "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(bar)), "r"(c0), "r"(c1), "r"(c2)
-      : "memory");
-}
-
-// K-major, 128B-swizzled operand tile: 8-row atoms of 1024 B (SBO), version 1.
-__device__ __forceinline__ uint64_t smem_desc_sw128(uint32_t addr) {
-  uint64_t d = 0;
-  d |= (uint64_t)((addr & 0x3FFFF) >> 4);          // start address
-  d |= (uint64_t)(16 >> 4) << 16;                  // LBO (unused for swizzled K-major)
-  d |= (uint64_t)(1024 >> 4) << 32;                // SBO: stride between 8-row atoms
-  d |= (uint64_t)1 << 46;                          // descriptor version (sm100)
-  d |= (uint64_t)2 << 61;                          // SWIZZLE_128B
-  return d;
-}
-
 // kind::tf32, D=f32, M=128, N=BN; bit 15/16 = A/B MN-major (set per call)
 constexpr uint32_t kIdesc = (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(BN >> 3) << 17) |
                             ((uint32_t)(BM >> 4) << 24);
-
-__device__ __forceinline__ void mma_tf32(uint32_t tmem_d, uint64_t da, uint64_t db, uint32_t idesc,
-                                         uint32_t acc) {
-  asm volatile(
-      "{\n\t"
-      ".reg .pred p;\n\t"
-      "setp.ne.b32 p, %4, 0;\n\t"
-      "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n\t"
-      "}" ::"r"(tmem_d),
-      "l"(da), "l"(db), "r"(idesc), "r"(acc));
-}
-
-__device__ __forceinline__ void mma_commit(uint64_t* bar) {
-  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
-                   smem_u32(bar))
-               : "memory");
-}
-
-__device__ __forceinline__ float to_tf32(float x) {
-  uint32_t r;
-  asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"(x));
-  return __uint_as_float(r);
-}
-
-__device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t* r) {
-  asm volatile(
-      "tcgen05.ld.sync.aligned.32x32b.x32.b32 "
-      "{%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, %15, "
-      "%16, %17, %18, %19, %20, %21, %22, %23, %24, %25, %26, %27, %28, %29, %30, %31}, [%32];"
-      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
-        "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]),
-        "=r"(r[13]), "=r"(r[14]), "=r"(r[15]), "=r"(r[16]), "=r"(r[17]), "=r"(r[18]),
-        "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]), "=r"(r[24]),
-        "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]),
-        "=r"(r[31])
-      : "r"(taddr));
-}
 
 // ---------------------------------------------------------------------------
 // split: x (view [batch, rows, K], any strides) -> dense hi, lo [batch, rows, Kp]
@@ -234,44 +138,6 @@ __device__ __forceinline__ void epi4(const Params& p, int bz, int row, int col, 
   v = make_float4(e[0], e[1], e[2], e[3]);
 }
 
-__device__ __forceinline__ uint32_t cluster_rank() {
-  uint32_t r;
-  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
-  return r;
-}
-
-__device__ __forceinline__ void cluster_sync_all() {
-  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::
-                   : "memory");
-}
-
-__device__ __forceinline__ float4 ld_dsmem_f4(uint32_t local_addr, uint32_t rank) {
-  uint32_t remote;
-  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(remote) : "r"(local_addr), "r"(rank));
-  float4 v;
-  asm volatile("ld.shared::cluster.v4.f32 {%0, %1, %2, %3}, [%4];"
-               : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w)
-               : "r"(remote)
-               : "memory");
-  return v;
-}
-
-// MN-major tf32 operand: the UMMA only takes the 128B swizzle with 32-byte
-// atomicity for MN-major 32-bit types (layout type 1, "128B_BASE32B"; TMA
-// CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B).  Tile = 32-wide MN groups (LBO =
-// 4 KB apart) of 32 K rows x 128 B; swizzle atoms of 4 K rows (SBO = 512 B).
-// One UMMA k-step (8 of K) = two atoms = +1 KB.
-__device__ __forceinline__ uint64_t smem_desc_mn_sw128(uint32_t addr, uint32_t lbo = 4096,
-                                                      uint32_t sbo = 512) {
-  uint64_t d = 0;
-  d |= (uint64_t)((addr & 0x3FFFF) >> 4);
-  d |= (uint64_t)(lbo >> 4) << 16;                 // LBO: next 32-wide MN group
-  d |= (uint64_t)(sbo >> 4) << 32;                 // SBO: next 4-row K atom
-  d |= (uint64_t)1 << 46;
-  d |= (uint64_t)1 << 61;                          // SWIZZLE_128B_BASE32B
-  return d;
-}
-
 __device__ __forceinline__ void tma_load_operand(const CUtensorMap* mh, const CUtensorMap* ml,
                                                  int mode, uint64_t* bar, uint8_t* dst_hi,
                                                  uint8_t* dst_lo, int kb, int row0, int z) {
@@ -284,20 +150,9 @@ __device__ __forceinline__ void tma_load_operand(const CUtensorMap* mh, const CU
   }
 }
 
-// hi = rn_tf32(x) in place, lo = rn_tf32(x - hi); elementwise, so the TMA
-// swizzle is preserved.  256 threads, 16 KB tile: 4 float4 per thread.
+// raw tiles split in place (tc_ptx.cuh), 256 accumulator threads
 __device__ __forceinline__ void split_tile_smem(uint8_t* hi, uint8_t* lo, int t) {
-  float4* h4 = reinterpret_cast<float4*>(hi);
-  float4* l4 = reinterpret_cast<float4*>(lo);
-#pragma unroll
-  for (int i = 0; i < TILE_BYTES / 16 / (32 * EPI_WARPS); ++i) {
-    const int idx = t + i * 32 * EPI_WARPS;
-    float4 v = h4[idx];
-    float4 h = make_float4(to_tf32(v.x), to_tf32(v.y), to_tf32(v.z), to_tf32(v.w));
-    l4[idx] = make_float4(to_tf32(v.x - h.x), to_tf32(v.y - h.y), to_tf32(v.z - h.z),
-                          to_tf32(v.w - h.w));
-    h4[idx] = h;
-  }
+  split_tf32_smem(smem_u32(hi), smem_u32(lo), TILE_BYTES / 16, t, 32 * EPI_WARPS);
 }
 
 __global__ void __launch_bounds__(NUM_THREADS, 1)
@@ -629,32 +484,6 @@ gemm_kernel(const __grid_constant__ CUtensorMap map_ah, const __grid_constant__ 
 
 // --- host side -------------------------------------------------------------
 
-static PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
-  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
-  static bool tried = false;
-  if (!tried) {
-    tried = true;
-    cudaDriverEntryPointQueryResult q;
-    void* p = nullptr;
-    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
-        q == cudaDriverEntryPointSuccess)
-      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
-  }
-  return fn;
-}
-
-static bool encode(CUtensorMap* map, const float* base, const cuuint64_t* dims,
-                   const cuuint64_t* strides, const cuuint32_t* box,
-                   CUtensorMapSwizzle swz = CU_TENSOR_MAP_SWIZZLE_128B) {
-  auto fn = encode_fn();
-  if (!fn) return false;
-  cuuint32_t estr[3] = {1, 1, 1};
-  CUresult r = fn(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, const_cast<float*>(base), dims, strides,
-                  box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, swz,
-                  CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-  return r == CUDA_SUCCESS;
-}
-
 // dense K-major plane [batch][rows][Kp]
 static bool make_map(CUtensorMap* map, const float* base, int64_t Kp, int64_t rows, int64_t batch) {
   cuuint64_t dims[3] = {(cuuint64_t)Kp, (cuuint64_t)rows, (cuuint64_t)batch};
@@ -735,6 +564,13 @@ static void choose_split(const GemmArgs& g, int* ksplit, int* kb_per) {
 }
 
 }  // namespace tc
+
+void tc_split_launch(const float* x, int64_t batch, int64_t rows, int64_t K, int64_t Kp, int64_t sb,
+                     int64_t sr, int64_t sk, float* hi, float* lo, const float* kscale,
+                     int64_t skb, int64_t skk, cudaStream_t s) {
+  dim3 grid((unsigned)((Kp + 31) / 32), (unsigned)((rows + 31) / 32), (unsigned)batch);
+  launch(tc::split_kernel, grid, 256, 0, s, x, rows, K, Kp, sb, sr, sk, hi, lo, kscale, skb, skk);
+}
 
 // Workspace: hi/lo planes of both operands for the pre-split feed (K padded
 // to a multiple of 4 so every TMA row stride is 16-byte aligned); raw-fed

@@ -35,7 +35,9 @@ def run(lib, m, n, k, bsz, force, iters):
     ws = torch.empty(max(need, 256), dtype=torch.uint8, device=dev)
     wp, wn = ws.data_ptr(), ws.numel()
     for _ in range(3):
-        assert lib.pfb_matmul_ex(ad, bd, cd, None, 0, force, wp, wn, s) == 0
+        rc = lib.pfb_matmul_ex(ad, bd, cd, None, 0, force, wp, wn, s)
+        if rc != 0:
+            raise RuntimeError(f"pfb_matmul_ex returned {rc}")
     torch.cuda.synchronize()
     st, en = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     torch.cuda._sleep(int(20e6))
