@@ -105,6 +105,10 @@ int pfb_reduce_dot(const pfb_tensor* x, const pfb_tensor* y, uint32_t axes_mask,
  * (reference tensor.py:286-303, 383-416). */
 int pfb_copy(const pfb_tensor* x, pfb_tensor* out, void* stream);
 int pfb_fill(pfb_tensor* out, double value, void* stream);
+/* pack n dense tensors into one byte buffer at dst + dst_offsets[i] (one
+ * launch per 16): the executor's single D2H of a run's outputs and device
+ * error words (reference Executor.run returns host values, interp.py:109-125). */
+int pfb_pack(int32_t n, const pfb_tensor* xs, void* dst, const int64_t* dst_offsets, void* stream);
 /* concat of n same-dtype inputs (any strides) along `axis` into out, in one
  * launch per 24 inputs (reference tensor.concat, tensor.py:383-393). */
 int pfb_concat(int32_t n, const pfb_tensor* xs, int32_t axis, pfb_tensor* out, void* stream);

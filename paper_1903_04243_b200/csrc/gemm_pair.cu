@@ -139,7 +139,6 @@ pair_kernel(const __grid_constant__ CUtensorMap map_ah, const __grid_constant__ 
             const __grid_constant__ CUtensorMap map_c, PParams p) {
   using C = Cfg<BN>;
   constexpr int STAGES = C::STAGES, BNH = C::BNH, EPI_COLS = C::EPI_COLS;
-  pdl_enter();
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>(
       (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -176,6 +175,8 @@ pair_kernel(const __grid_constant__ CUtensorMap map_ah, const __grid_constant__ 
       mbar_init(&acc_empty[b], 2);
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&map_ah)) : "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&map_bh)) : "memory");
   }
   if (warp == 1) {
     asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
@@ -188,14 +189,13 @@ pair_kernel(const __grid_constant__ CUtensorMap map_ah, const __grid_constant__ 
   cluster_sync_all();  // peers' barriers are initialised before any remote arrive
   asm volatile("tcgen05.fence::after_thread_sync;");
   const uint32_t tmem_base = *tmem_slot;
+  pdl_enter();  // prologue above overlaps the previous kernel (PDL)
 
   const int bytes_a = (p.a_mode == kPreSplit ? 2 : 1) * A_BYTES;
   const int bytes_b = (p.b_mode == kPreSplit ? 2 : 1) * C::B_BYTES;
 
   if (warp == 0) {
     if (lane == 0) {
-      asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&map_ah)) : "memory");
-      asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&map_bh)) : "memory");
       int g = 0;
       for (int u = pair; u < units; u += npairs) {
         const int bz = u / tiles_per_batch, r = u % tiles_per_batch;

@@ -93,7 +93,7 @@ __global__ void __launch_bounds__(256) split_kernel(const float* __restrict__ x,
       float v = t[tx][ty + j];
       float h = to_tf32(v);
       hb[r * Kp + k] = h;
-      lb[r * Kp + k] = to_tf32(v - h);
+      lb[r * Kp + k] = tf32_lo(v, h);
     }
   }
 }
@@ -124,7 +124,16 @@ struct Params {
   int act;
   uint32_t mn_lbo, mn_sbo;  // MN-major descriptor strides (4 KB, 512 B)
   int tma_store;            // epilogue stores 32x32 blocks with TMA (map_c)
+  unsigned long long* trace;  // PFB_TC_TRACE: globaltimer stamps of CTA 0 (bring-up)
 };
+
+__device__ __forceinline__ void stamp(const Params& p, int i) {
+  if (p.trace != nullptr && blockIdx.x == 0) {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    p.trace[i] = t;
+  }
+}
 
 __device__ __forceinline__ void epi4(const Params& p, int bz, int row, int col, float4& v) {
   if (p.bias == nullptr && p.act == 0) return;
@@ -159,7 +168,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
 gemm_kernel(const __grid_constant__ CUtensorMap map_ah, const __grid_constant__ CUtensorMap map_al,
             const __grid_constant__ CUtensorMap map_bh, const __grid_constant__ CUtensorMap map_bl,
             const __grid_constant__ CUtensorMap map_c, Params p) {
-  pdl_enter();
+  stamp(p, 0);
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>(
       (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -195,6 +204,10 @@ gemm_kernel(const __grid_constant__ CUtensorMap map_ah, const __grid_constant__ 
       mbar_init(&acc_empty[b], 32 * EPI_WARPS);
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&map_ah)) : "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&map_al)) : "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&map_bh)) : "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&map_bl)) : "memory");
   }
   if (warp == 1) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
@@ -206,16 +219,18 @@ gemm_kernel(const __grid_constant__ CUtensorMap map_ah, const __grid_constant__ 
   __syncthreads();
   asm volatile("tcgen05.fence::after_thread_sync;");
   const uint32_t tmem_base = *tmem_slot;
+  // the prologue above (barriers, TMEM, descriptor prefetch) overlaps the
+  // previous kernel's tail under programmatic dependent launch; operands are
+  // only read after this wait
+  if (threadIdx.x == 0) stamp(p, 1);
+  pdl_enter();
+  if (threadIdx.x == 0) stamp(p, 2);
 
   const int bytes_a = (p.a_mode == kPreSplit ? 2 : 1) * TILE_BYTES;
   const int bytes_b = (p.b_mode == kPreSplit ? 2 : 1) * TILE_BYTES;
 
   if (warp == 0) {
     if (lane == 0) {
-      asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&map_ah)) : "memory");
-      asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&map_al)) : "memory");
-      asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&map_bh)) : "memory");
-      asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&map_bl)) : "memory");
       int g = 0;
       for (int u = blockIdx.x; u < ntiles; u += ustride) {
         const int t = u / p.ksplit, ks = u % p.ksplit;
@@ -229,6 +244,7 @@ gemm_kernel(const __grid_constant__ CUtensorMap map_ah, const __grid_constant__ 
           mbar_expect_tx(&full[s], bytes_a + bytes_b);
           tma_load_operand(&map_ah, &map_al, p.a_mode, &full[s], tile(s, 0), tile(s, 1), kb, m0, za);
           tma_load_operand(&map_bh, &map_bl, p.b_mode, &full[s], tile(s, 2), tile(s, 3), kb, n0, zb);
+          if (g == 0) stamp(p, 3);
         }
       }
     }
@@ -249,6 +265,7 @@ gemm_kernel(const __grid_constant__ CUtensorMap map_ah, const __grid_constant__ 
           for (int kb = kb_beg; kb < kb_end; ++kb, ++g) {
             const int s = g % STAGES;
             mbar_wait(split_smem ? &ready[s] : &full[s], (g / STAGES) & 1);
+            if (g == 0) stamp(p, 5);
             asm volatile("tcgen05.fence::after_thread_sync;");
             const uint32_t a0 = smem_u32(tile(s, 0)), a1 = smem_u32(tile(s, 1));
             const uint32_t b0 = smem_u32(tile(s, 2)), b1 = smem_u32(tile(s, 3));
@@ -274,6 +291,7 @@ gemm_kernel(const __grid_constant__ CUtensorMap map_ah, const __grid_constant__ 
           mma_commit(&acc_full[buf]);
         }
       }
+      stamp(p, 6);
     }
     __syncwarp();
   } else {
@@ -288,6 +306,7 @@ gemm_kernel(const __grid_constant__ CUtensorMap map_ah, const __grid_constant__ 
     auto split_stage = [&]() {
       const int s = gs % STAGES;
       mbar_wait(&full[s], (gs / STAGES) & 1);
+      if (gs == 0 && et == 0) stamp(p, 4);
       if (p.a_mode != kPreSplit) split_tile_smem(tile(s, 0), tile(s, 1), et);
       if (p.b_mode != kPreSplit) split_tile_smem(tile(s, 2), tile(s, 3), et);
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
@@ -299,6 +318,7 @@ gemm_kernel(const __grid_constant__ CUtensorMap map_ah, const __grid_constant__ 
     auto drain = [&]() {
       const int buf = gc & 1;
       mbar_wait(&acc_full[buf], (gc >> 1) & 1);
+      if (gc == 0 && et == 0) stamp(p, 7);
       asm volatile("tcgen05.fence::after_thread_sync;");
 #pragma unroll
       for (int cc = 0; cc < EPI_COLS; cc += 32) {
@@ -424,10 +444,12 @@ gemm_kernel(const __grid_constant__ CUtensorMap map_ah, const __grid_constant__ 
       }
     }
   }
+  if (threadIdx.x == 64) stamp(p, 8);
   if (p.tma_store && warp >= 2 && lane == 0)
-    asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+    asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
   asm volatile("tcgen05.fence::before_thread_sync;");
   __syncthreads();
+  if (threadIdx.x == 0) stamp(p, 9);
   if (clustered) {
     // deterministic split-K reduction over DSMEM: CTA `rank` of the cluster
     // sums rows [rank*rows_per, ...) of all partial tiles in rank order
@@ -479,6 +501,7 @@ gemm_kernel(const __grid_constant__ CUtensorMap map_ah, const __grid_constant__ 
     asm volatile("tcgen05.fence::after_thread_sync;");
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base),
                  "r"(TMEM_COLS));
+    if (lane == 0) stamp(p, 10);
   }
 }
 
@@ -570,6 +593,20 @@ void tc_split_launch(const float* x, int64_t batch, int64_t rows, int64_t K, int
                      int64_t skb, int64_t skk, cudaStream_t s) {
   dim3 grid((unsigned)((Kp + 31) / 32), (unsigned)((rows + 31) / 32), (unsigned)batch);
   launch(tc::split_kernel, grid, 256, 0, s, x, rows, K, Kp, sb, sr, sk, hi, lo, kscale, skb, skk);
+}
+
+// PFB_TC_TRACE=1: CTA 0 of every tcgen05 GEMM launch writes globaltimer
+// stamps (entry, after PDL wait, after prologue, first TMA issued, first
+// stage landed, first MMA issued, last commit, first accumulator ready,
+// epilogue done, CTA done, TMEM freed) -- read with pfb_debug_tc_trace().
+static unsigned long long* g_trace = nullptr;
+unsigned long long* tc_trace_buffer() {
+  static const bool on = getenv_flag("PFB_TC_TRACE");
+  if (on && g_trace == nullptr) {
+    cudaMalloc(&g_trace, 16 * sizeof(unsigned long long));
+    cudaMemset(g_trace, 0, 16 * sizeof(unsigned long long));
+  }
+  return on ? g_trace : nullptr;
 }
 
 // Workspace: hi/lo planes of both operands for the pre-split feed (K padded
@@ -664,6 +701,12 @@ int gemm_tcgen05(const GemmArgs& g, void* ws, int64_t ws_bytes, cudaStream_t s, 
   }
   int ksplit, kb_per;
   choose_split(g, &ksplit, &kb_per);
+  if (const char* e = getenv("PFB_TC_KSPLIT")) {  // bring-up / tuning override
+    const int nk = (int)((Kp + BK - 1) / BK);
+    const int want = std::max(1, std::min(atoi(e), kMaxCluster));
+    kb_per = (nk + want - 1) / want;
+    ksplit = (nk + kb_per - 1) / kb_per;
+  }
   // TMA-store epilogue: C row-major with 16-byte aligned rows, overwrite
   CUtensorMap mc = mah;
   int tma_store = 0;
@@ -681,7 +724,7 @@ int gemm_tcgen05(const GemmArgs& g, void* ws, int64_t ws_bytes, cudaStream_t s, 
   Params p{(int)g.M, (int)g.N, (int)Kp, (int)g.batch,
            (int)((g.M + BM - 1) / BM), (int)((g.N + BN - 1) / BN), a_bc, b_bc, am, bm, idesc,
            g.C, g.scb, g.scm, g.scn, g.alpha_rows, g.accumulate, ksplit, kb_per,
-           g.bias, g.sxb, g.sxm, g.sxn, g.act, 4096u, 512u, tma_store};
+           g.bias, g.sxb, g.sxm, g.sxn, g.act, 4096u, 512u, tma_store, tc_trace_buffer()};
   const int64_t units = (int64_t)p.ntm * p.ntn * g.batch * ksplit;
   if (ksplit > 1) {
     // one CTA per (tile, k-split); the k-splits of a tile are one cluster
@@ -708,3 +751,10 @@ int gemm_tcgen05(const GemmArgs& g, void* ws, int64_t ws_bytes, cudaStream_t s, 
 }
 
 }  // namespace pfb
+
+extern "C" int pfb_debug_tc_trace(unsigned long long* out16) {
+  if (pfb::g_trace == nullptr) return PFB_E_UNSUPPORTED;
+  cudaDeviceSynchronize();
+  return cudaMemcpy(out16, pfb::g_trace, 16 * sizeof(unsigned long long), cudaMemcpyDeviceToHost) ==
+                 cudaSuccess ? 0 : PFB_E_ARG;
+}

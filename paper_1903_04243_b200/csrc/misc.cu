@@ -58,3 +58,56 @@ extern "C" int pfb_outer_sq_norm(const pfb_tensor* a, const pfb_tensor* b, pfb_t
       (const float*)b->data, b->stride[0], b->stride[1], (float*)sq_norm->data);
   return launch_status();
 }
+
+// ---------------------------------------------------------------------------
+// pack: several dense tensors -> one byte buffer (one launch), so a run's
+// outputs (and its device error words) come back in a single D2H copy.
+
+namespace pfb {
+constexpr int kMaxPack = 16;
+struct PackDesc {
+  const uint8_t* src[kMaxPack];
+  int64_t off[kMaxPack];
+  int64_t bytes[kMaxPack];
+};
+
+__global__ void __launch_bounds__(256) pack_kernel(PackDesc d, uint8_t* dst) {
+  pdl_enter();
+  const int t = blockIdx.y;
+  const uint8_t* s = d.src[t];
+  uint8_t* o = dst + d.off[t];
+  const int64_t nb = d.bytes[t];
+  const bool vec = ((reinterpret_cast<uintptr_t>(s) | reinterpret_cast<uintptr_t>(o)) & 15) == 0;
+  const int64_t n16 = vec ? nb / 16 : 0;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n16; i += stride)
+    reinterpret_cast<int4*>(o)[i] = __ldg(reinterpret_cast<const int4*>(s) + i);
+  for (int64_t i = 16 * n16 + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < nb; i += stride)
+    o[i] = s[i];
+}
+}  // namespace pfb
+
+extern "C" int pfb_pack(int32_t n, const pfb_tensor* xs, void* dst, const int64_t* dst_offsets,
+                        void* stream) {
+  if (n < 0) return PFB_E_ARG;
+  cudaStream_t s = as_stream(stream);
+  for (int base = 0; base < n; base += kMaxPack) {
+    PackDesc d = {};
+    const int m = n - base < kMaxPack ? n - base : kMaxPack;
+    int64_t most = 0;
+    for (int j = 0; j < m; ++j) {
+      const pfb_tensor* x = &xs[base + j];
+      if (!is_dense(x)) return PFB_E_UNSUPPORTED;
+      d.src[j] = static_cast<const uint8_t*>(x->data);
+      d.off[j] = dst_offsets[base + j];
+      d.bytes[j] = numel(x) * dtype_size(x->dtype);
+      if (d.bytes[j] > most) most = d.bytes[j];
+    }
+    if (most == 0) continue;
+    const int gx = grid_for((most + 15) / 16, 256, 2);
+    launch(pack_kernel, dim3((unsigned)gx, (unsigned)m), 256, 0, s, d,
+           static_cast<uint8_t*>(dst));
+    if (int e = launch_status()) return e;
+  }
+  return 0;
+}

@@ -24,6 +24,7 @@ from __future__ import annotations
 
 import ctypes
 import os
+import sys
 
 import numpy as np
 import torch
@@ -246,6 +247,7 @@ class Executor:
         self._sub_warm = set()
         self._used_caps = {}
         self._pinned = {}
+        self._last_replay = None
         self._programs = {}
         self.graph = graph
         self.device = torch.device(device if device is not None else "cuda")
@@ -279,6 +281,9 @@ class Executor:
     def run(self, feeds=None, outputs=None):
         """Execute and return host TensorValues (fp32 floats, i64, bool)."""
         outs = self.run_device(feeds, outputs)
+        cap = self._last_replay
+        if cap is not None and cap.host_pack is not None:
+            return self._unpack(cap, outs)
         # D2H through pinned staging buffers: all copies queued, one sync
         staged = []
         for i, v in enumerate(outs):
@@ -307,12 +312,55 @@ class Executor:
         self._writeback_vars()
         return res
 
+    def _unpack(self, cap, outs):
+        """Results of a replayed capture: replay its pack + D2H graph into a
+        free pinned slot, one sync, numpy views per output (no host copy)."""
+        plan = cap.host_pack
+        sl, copy_out = self._io_slot(plan)
+        sl["graph"].replay()
+        self.launch_count += (plan["n"] + 15) // 16
+        torch.cuda.current_stream(self.device).synchronize()
+        host = np.frombuffer(sl["raw"], dtype=np.uint8)
+        if copy_out:
+            host = host.copy()
+        res = []
+        for v, ent in zip(outs, plan["layout"]):
+            if ent is None:
+                res.append(TensorValue(v.dtype, v.value))
+                continue
+            off, nbytes, npdt, shape = ent
+            arr = host[off:off + nbytes].view(npdt).reshape(shape)
+            if v.dtype == DType.BOOL:
+                arr = arr.view(np.bool_)
+            res.append(TensorValue(v.dtype, arr))
+        if self._used_caps:  # error words of captured loop bodies: the general path
+            saved, self._err_nodes = self._err_nodes, []
+            try:
+                self._finish_errors()
+            finally:
+                self._err_nodes = saved
+        err_slice = plan["err"]
+        if self.check_errors and err_slice is not None:
+            off, n = err_slice
+            bits = host[off:off + 4 * n].view(np.int32)
+            for k in np.nonzero(bits)[0]:
+                b = int(bits[k])
+                cause = (E.IndexOutOfBounds("index out of range") if b & N.DEV_OOB else
+                         E.IndexCollision("scatter_rows: overlapping index sets")
+                         if b & N.DEV_COLLISION else
+                         E.IncompleteCover("scatter_rows: rows uncovered"))
+                cap.err.zero_()
+                raise E.ExecError(cap.err_nodes[k], cause)
+        self._writeback_vars()
+        return res
+
     def run_device(self, feeds=None, outputs=None):
         """Execute; return device values (DArray / HostVal) without copying back.
 
         With CUDA-graph replay active the returned arrays live in the graph's
         memory pool and are overwritten by the next run."""
         feeds = feeds or {}
+        self._last_replay = None
         with torch.cuda.device(self.device):
             g, keys = self._resolve_outputs(outputs)
             if self.cuda_graph and self.kernel_timer is None and self._capturable(g, keys):
@@ -360,6 +408,7 @@ class Executor:
             with torch.cuda.graph(graph):
                 outs = self._run_eager(g, keys, static)
             cap = _Captured(graph, static, outs, self._ws, self._err, list(self._err_nodes))
+            cap.host_pack = self._pack_plan(outs, cap)
             cap.launches = self.launch_count - l0
             cap.dispatches = self.dispatch_count - d0
             self._captures[sig] = cap
@@ -370,6 +419,69 @@ class Executor:
         finally:
             self._ws, self._err, self._err_nodes = saved
         return cap
+
+    def _pack_plan(self, outs, cap):
+        """Layout of a captured graph's results in one byte buffer: every dense
+        device output plus the used device error words.  `run()` replays a
+        small second graph (one pack kernel + one D2H copy into pinned memory)
+        after the compute graph, so a run's results come back in a single
+        copy and `run_device` (the compute graph alone) stays free of D2H.
+        Returns (layout, err_slice, descs, offsets, total) or None when an
+        output is not dense (then the per-output copy path is used)."""
+        srcs, layout, off = [], [], 0
+        for v in outs:
+            if isinstance(v, HostVal):
+                layout.append(None)
+                continue
+            if not v.is_dense():
+                return None
+            nbytes = v.size * v.buf.element_size()
+            layout.append((off, nbytes, np.dtype(v.dtype.device_np_dtype), tuple(v.shape)))
+            if nbytes:
+                srcs.append((v.desc(), off))
+            off += (nbytes + 15) // 16 * 16
+        err_slice = None
+        if cap.err_nodes:
+            n = min(len(cap.err_nodes), _ERR_SLOTS)
+            d = N.PfbTensor()  # the int32 error words as bytes
+            d.data, d.dtype, d.rank = cap.err.data_ptr(), N.BOOL, 1
+            d.shape[0], d.stride[0] = 4 * n, 1
+            err_slice = (off, n)
+            srcs.append((d, off))
+            off += (4 * n + 15) // 16 * 16
+        total = max(off, 16)
+        descs = (N.PfbTensor * max(len(srcs), 1))(*[d for d, _ in srcs])
+        offs = (ctypes.c_int64 * max(len(srcs), 1))(*[o for _, o in srcs])
+        return {"layout": layout, "err": err_slice, "descs": descs, "offs": offs,
+                "n": len(srcs), "total": total,
+                "dev": torch.empty(total, dtype=torch.uint8, device=self.device), "slots": []}
+
+    _IO_SLOTS = 4
+
+    def _io_slot(self, plan):
+        """A pinned result buffer no live result still views (zero-copy
+        results).  The pool (slot 0 + _IO_SLOTS) and each slot's pack + D2H
+        graph are built on first use; slot 0's contents are copied out when
+        every pooled slot is still referenced by results the caller holds."""
+        slots = plan["slots"]
+        if not slots:
+            torch.cuda.synchronize(self.device)
+            for _ in range(self._IO_SLOTS + 1):
+                pinned = torch.empty(plan["total"], dtype=torch.uint8, pin_memory=True)
+                raw = (ctypes.c_uint8 * plan["total"]).from_address(pinned.data_ptr())
+                graph = torch.cuda.CUDAGraph()
+                with torch.cuda.graph(graph):
+                    st = torch.cuda.current_stream(self.device).cuda_stream
+                    if plan["n"]:
+                        _raise_status(self._lib.pfb_pack(plan["n"], plan["descs"],
+                                                         plan["dev"].data_ptr(), plan["offs"], st),
+                                      "pack")
+                    pinned.copy_(plan["dev"], non_blocking=True)
+                slots.append({"graph": graph, "pinned": pinned, "raw": raw})
+        for sl in slots[1:]:
+            if sys.getrefcount(sl["raw"]) <= 2:  # only the slot dict (+ this call's argument)
+                return sl, False
+        return slots[0], True
 
     # -- CUDA-graph capture of pure loop-body sub-graphs --------------------------
 
@@ -564,6 +676,7 @@ class Executor:
     def _replay(self, cap, feeds):
         self._load_feeds(cap.inputs, feeds)
         cap.graph.replay()
+        self._last_replay = cap
         self.launch_count += cap.launches
         self.dispatch_count += cap.dispatches
         self._err, self._err_nodes = cap.err, list(cap.err_nodes)
@@ -871,6 +984,7 @@ class _Captured:
     def __init__(self, graph, inputs, outputs, ws, err, err_nodes):
         self.graph, self.inputs, self.outputs = graph, inputs, outputs
         self.ws, self.err, self.err_nodes = ws, err, err_nodes
+        self.host_pack = None
         self.launches = 0
         self.dispatches = 0
 

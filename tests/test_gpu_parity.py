@@ -280,3 +280,32 @@ def test_device_loop_host_loop_agree(Executor):
         X._DEVICE_LOOPS = saved
     for a, b in zip(dev, host):
         np.testing.assert_array_equal(np.asarray(a.data), np.asarray(b.data))
+
+
+def test_replayed_results_stay_valid(Executor):
+    """run() of a captured graph returns zero-copy views of pooled pinned
+    buffers: results the caller still holds must never be overwritten by
+    later runs (pool exhaustion falls back to copies), released buffers are
+    reused, and errors words still travel with the packed results."""
+    import gc
+    w = build_program("cfg2_mlp")
+    feeds = [{k: (np.asarray(v) * (0.25 * (i + 1)) if np.asarray(v).dtype.kind == "f" else v)
+              for k, v in w.feeds.items()} for i in range(3)]
+    eager = Executor(w.graph, cuda_graph=False)
+    want = [eager.run(f) for f in feeds]
+    ex = Executor(w.graph)
+    held = [ex.run(feeds[i % 3]) for i in range(10)]
+    assert ex._captures
+    for i, res in enumerate(held):
+        for a, b in zip(res, want[i % 3]):
+            np.testing.assert_allclose(a.data, b.data, rtol=1e-6, atol=1e-7)
+    cap = next(iter(ex._captures.values()))
+    n_slots = len(cap.host_pack["slots"])
+    assert n_slots <= ex._IO_SLOTS + 1
+    del held, res, a, b
+    gc.collect()
+    for i in range(6):
+        res = ex.run(feeds[i % 3])
+        for a, b in zip(res, want[i % 3]):
+            np.testing.assert_allclose(a.data, b.data, rtol=1e-6, atol=1e-7)
+    assert len(cap.host_pack["slots"]) == n_slots == ex._IO_SLOTS + 1

@@ -14,6 +14,7 @@ from paper_1903_04243_b200 import _native as N  # noqa: E402
 from paper_1903_04243_b200.executor import DArray  # noqa: E402
 from paper_1903_04243_b200.tensor import DType  # noqa: E402
 
+GRAPH = False
 SHAPES = [(10240, 784, 256, 1), (256, 1024, 2048, 1), (256, 2048, 1024, 1),
           (4096, 4096, 4096, 1), (1024, 2048, 64, 64)]
 
@@ -40,6 +41,25 @@ def run(lib, m, n, k, bsz, force, iters):
             raise RuntimeError(f"pfb_matmul_ex returned {rc}")
     torch.cuda.synchronize()
     st, en = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    if GRAPH:
+        # device time without host launch overhead: replay a captured graph
+        g = torch.cuda.CUDAGraph()
+        cs = torch.cuda.Stream()
+        with torch.cuda.stream(cs):
+            with torch.cuda.graph(g, stream=cs):
+                for _ in range(iters):
+                    lib.pfb_matmul_ex(ad, bd, cd, None, 0, force, wp, wn, cs.cuda_stream)
+        g.replay()
+        torch.cuda.synchronize()
+        st.record()
+        g.replay()
+        en.record()
+        torch.cuda.synchronize()
+        ms = st.elapsed_time(en) / iters
+        flops = 2.0 * bsz * m * n * k
+        ref = (a.double() @ bt.double().transpose(-1, -2))
+        err = (c.double() - ref).abs().max().item()
+        return ms, flops / ms / 1e9, err
     torch.cuda._sleep(int(20e6))
     st.record()
     for _ in range(iters):
@@ -58,7 +78,10 @@ def main():
     ap.add_argument("--force", type=int, default=2)
     ap.add_argument("--shape", type=int, nargs="+")
     ap.add_argument("--iters", type=int, default=20)
+    ap.add_argument("--graph", action="store_true", help="time a replayed CUDA graph")
     args = ap.parse_args()
+    global GRAPH
+    GRAPH = args.graph
     lib = N.lib()
     shapes = [tuple(args.shape) + ((1,) if len(args.shape) == 3 else ())] if args.shape else SHAPES
     for shp in shapes:
