@@ -405,21 +405,28 @@ __global__ void __launch_bounds__(256) fused_kernel(Layout L, IdxT ngroups, Fuse
        g += (IdxT)gridDim.x * blockDim.x) {
     int64_t off[NIN + 1];
     offsets<IdxT, NIN + 1>(L, g * V, off);
+    // every input is loaded up front, all loads in flight together (a load
+    // step of the program then only moves a register): the interpreter's
+    // register file lives in local memory, and loading inside the step loop
+    // serialised one memory latency per input
+    Vec<V> in[NIN];
+#pragma unroll
+    for (int K = 0; K < NIN; ++K) {
+      const void* ip = K == 0 ? i0 : K == 1 ? i1 : K == 2 ? i2 : K == 3 ? i3
+                     : K == 4 ? i4 : K == 5 ? i5 : K == 6 ? i6 : i7;
+      const int md = (modes >> (2 * (K + 1))) & 3;
+      in[K] = P.in_dtype[K] == PFB_BOOL ? load_v<V, uint8_t>(ip, off[K + 1], L.st[K + 1][ir], md)
+                                        : load_v<V, float>(ip, off[K + 1], L.st[K + 1][ir], md);
+    }
     Vec<V> r[kMaxRegs];
     for (int s = 0; s < nsteps; ++s) {
       const int4 c = prog[s];
       Vec<V> o;
       if (c.x == F_LOAD) {
         switch (c.z) {
-#define PFB_LD(K)                                                                          \
-  case K:                                                                                  \
-    if (K < NIN) {                                                                         \
-      const int md = (modes >> (2 * (K + 1))) & 3;                                         \
-      o = P.in_dtype[K] == PFB_BOOL ? load_v<V, uint8_t>(i##K, off[K < NIN ? K + 1 : 0],   \
-                                                         L.st[K + 1][ir], md)              \
-                                    : load_v<V, float>(i##K, off[K < NIN ? K + 1 : 0],     \
-                                                       L.st[K + 1][ir], md);               \
-    }                                                                                      \
+#define PFB_LD(K)                     \
+  case K:                             \
+    if (K < NIN) o = in[K < NIN ? K : 0]; \
     break;
           PFB_LD(0) PFB_LD(1) PFB_LD(2) PFB_LD(3) PFB_LD(4) PFB_LD(5) PFB_LD(6) PFB_LD(7)
 #undef PFB_LD

@@ -217,6 +217,7 @@ pair_kernel(const __grid_constant__ CUtensorMap map_ah, const __grid_constant__ 
       // k-step advance: +32 B inside the swizzle row (K-major) or one 1 KB atom (MN-major)
       const uint64_t astep = amn ? (1024 >> 4) : ((UMMA_K * 4) >> 4);
       const uint64_t bstep = bmn ? (1024 >> 4) : ((UMMA_K * 4) >> 4);
+      const bool lo_lo = p.a_mode != kPreSplit && p.b_mode != kPreSplit;
       int g = 0, gc = 0;
       for (int u = pair; u < units; u += npairs) {
         const int nchunks = (nk + chunk - 1) / chunk;
@@ -243,6 +244,9 @@ pair_kernel(const __grid_constant__ CUtensorMap map_ah, const __grid_constant__ 
               mma_tf32_pair(tmem_d, a_hi + da, b_hi + db, p.idesc, acc);
               mma_tf32_pair(tmem_d, a_hi + da, b_lo + db, p.idesc, 1u);
               mma_tf32_pair(tmem_d, a_lo + da, b_hi + db, p.idesc, 1u);
+              // both operands raw: hi = trunc_tf32 on both sides makes the
+              // dropped lo*lo term sign-biased, so it is kept
+              if (lo_lo) mma_tf32_pair(tmem_d, a_lo + da, b_lo + db, p.idesc, 1u);
             }
             mma_commit_pair(&empty[s]);
           }

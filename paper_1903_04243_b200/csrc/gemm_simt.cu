@@ -7,8 +7,12 @@
 //    whichever of their two strides is unit (coalesced for normal and
 //    transposed views); 128-bit stores of 4 consecutive output columns.
 //    Split-K (grid.z = batch x splits) when there are too few tiles to fill
-//    148 SMs: per-split partials go to the workspace and a second pass sums
-//    them in split order (deterministic), applying the epilogue.
+//    148 SMs: the splits of a tile form one thread-block cluster; each CTA
+//    leaves its partial tile in shared memory and, after a cluster barrier,
+//    CTA r sums rows [r*64/S, (r+1)*64/S) of all S partials over DSMEM in
+//    split order (deterministic) and applies the epilogue -- one launch, no
+//    workspace.  (Splits beyond the cluster limit: partials to the workspace
+//    and a second pass.)
 //  * small-K kernel (K <= 16): store-bound; a CTA per output row, each thread
 //    4 consecutive columns per 128-bit store, the row's lhs in registers.
 // Exact fp32 FMA accumulation in both.
@@ -50,12 +54,27 @@ __device__ __forceinline__ void store_row4(const GemmArgs& g, int64_t b, int64_t
 // partials: nullptr -> epilogue straight to C; else ws[split][b][M][N].
 // Register-staged double buffering: the next k-tile's global loads are issued
 // before the current tile's FMAs, so the loop is not load-latency bound.
-template <bool KS>
+__device__ __forceinline__ void cp_async4(float* smem, const float* gmem, bool pred) {
+  const uint32_t d = static_cast<uint32_t>(__cvta_generic_to_shared(smem));
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;" ::"r"(d), "l"(gmem),
+               "r"(pred ? 4 : 0)
+               : "memory");
+}
+
+constexpr int NST = 4;  // k-tiles in flight (cp.async ring)
+
+template <bool KS, bool CL>
 __global__ void __launch_bounds__(256) gemm_simt_kernel(GemmArgs g, int splits, int64_t kchunk,
                                                         float* partials) {
   pdl_enter();
-  __shared__ float As[BK][BM + 4];
-  __shared__ float Bs[BK][BN + 4];
+  // NST-deep cp.async ring of A/B k-tiles: a CTA's whole K range (<= 4
+  // k-tiles for split-K shapes) is requested at once, so a small GEMM pays
+  // one memory latency instead of one per k-tile.  (The cluster reduction
+  // buffer aliases the ring after the main loop.)
+  __shared__ __align__(16) float ring[NST * 2 * BK * (BM + 4)];
+  __shared__ float ks_s[NST][BK];
+  auto As = [&](int st) { return ring + st * 2 * BK * (BM + 4); };
+  auto Bs = [&](int st) { return ring + st * 2 * BK * (BM + 4) + BK * (BM + 4); };
   const int64_t bz = blockIdx.z / splits;
   const int split = blockIdx.z % splits;
   const int64_t m0 = (int64_t)blockIdx.y * BM, n0 = (int64_t)blockIdx.x * BN;
@@ -74,30 +93,48 @@ __global__ void __launch_bounds__(256) gemm_simt_kernel(GemmArgs g, int splits, 
     if (a_kfast) { am[j] = e / BK; ak[j] = e % BK; } else { ak[j] = e / BM; am[j] = e % BM; }
     if (b_nfast) { bk[j] = e / BN; bn[j] = e % BN; } else { bn[j] = e / BK; bk[j] = e % BK; }
   }
-  float ra[4], rb[4];
-  auto load = [&](int64_t k0) {
+  const int ntiles = kbeg < kend ? (int)((kend - kbeg + BK - 1) / BK) : 0;
+  auto issue = [&](int t) {  // k-tile t -> ring stage t % NST (one commit group)
+    const int st = t % NST;
+    const int64_t k0 = kbeg + (int64_t)t * BK;
+    float* as = As(st);
+    float* bs = Bs(st);
 #pragma unroll
     for (int j = 0; j < 4; ++j) {
       const int64_t gm = m0 + am[j], gk = k0 + ak[j];
-      ra[j] = (gm < g.M && gk < kend) ? __ldg(A + gm * g.sam + gk * g.sak) : 0.f;
+      const bool pa = gm < g.M && gk < kend;
+      cp_async4(as + ak[j] * (BM + 4) + am[j], pa ? A + gm * g.sam + gk * g.sak : A, pa);
       const int64_t gk2 = k0 + bk[j], gn = n0 + bn[j];
-      rb[j] = (gk2 < kend && gn < g.N) ? __ldg(B + gk2 * g.sbk + gn * g.sbn) : 0.f;
-      if (KS && gk2 < kend) rb[j] *= __ldg(g.kscale + bz * g.skb + gk2 * g.skk);
+      const bool pb = gk2 < kend && gn < g.N;
+      cp_async4(bs + bk[j] * (BN + 4) + bn[j], pb ? B + gk2 * g.sbk + gn * g.sbn : B, pb);
     }
+    if (KS && tid < BK) {
+      const int64_t gk = k0 + tid;
+      const bool pk = gk < kend;
+      cp_async4(&ks_s[st][tid], pk ? g.kscale + bz * g.skb + gk * g.skk : g.kscale, pk);
+    }
+    asm volatile("cp.async.commit_group;" ::: "memory");
   };
-  if (kbeg < kend) load(kbeg);
-  for (int64_t k0 = kbeg; k0 < kend; k0 += BK) {
 #pragma unroll
-    for (int j = 0; j < 4; ++j) {
-      As[ak[j]][am[j]] = ra[j];
-      Bs[bk[j]][bn[j]] = rb[j];
-    }
+  for (int t = 0; t < NST - 1; ++t) {
+    if (t < ntiles) issue(t);
+    else asm volatile("cp.async.commit_group;" ::: "memory");
+  }
+  for (int t = 0; t < ntiles; ++t) {
+    if (t + NST - 1 < ntiles) issue(t + NST - 1);
+    else asm volatile("cp.async.commit_group;" ::: "memory");
+    asm volatile("cp.async.wait_group %0;" ::"n"(NST - 1) : "memory");
     __syncthreads();
-    if (k0 + BK < kend) load(k0 + BK);
+    const float* as = As(t % NST);
+    const float* bs = Bs(t % NST);
 #pragma unroll
     for (int kk = 0; kk < BK; ++kk) {
-      float4 a4 = *reinterpret_cast<const float4*>(&As[kk][tm]);
-      float4 b4 = *reinterpret_cast<const float4*>(&Bs[kk][tn]);
+      float4 a4 = *reinterpret_cast<const float4*>(as + kk * (BM + 4) + tm);
+      const float4 b4 = *reinterpret_cast<const float4*>(bs + kk * (BN + 4) + tn);
+      if (KS) {
+        const float sc = ks_s[t % NST][kk];
+        a4.x *= sc; a4.y *= sc; a4.z *= sc; a4.w *= sc;
+      }
       const float a[4] = {a4.x, a4.y, a4.z, a4.w};
       const float bb[4] = {b4.x, b4.y, b4.z, b4.w};
 #pragma unroll
@@ -107,7 +144,46 @@ __global__ void __launch_bounds__(256) gemm_simt_kernel(GemmArgs g, int splits, 
     }
     __syncthreads();
   }
-  if (partials == nullptr) {
+  asm volatile("cp.async.wait_group 0;" ::: "memory");
+  if constexpr (CL) {
+    // cluster split-K: partial tile -> own smem, DSMEM reduction in split order
+    float* red = ring;  // BM*BN floats, the (drained) ring
+    __syncthreads();
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+      *reinterpret_cast<float4*>(&red[(tm + i) * BN + tn]) =
+          make_float4(acc[i][0], acc[i][1], acc[i][2], acc[i][3]);
+    asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" :::
+                     "memory");
+    uint32_t rank;
+    asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(rank));
+    const int rows_per = (BM + splits - 1) / splits;
+    const int rb = (int)rank * rows_per, re = min((int)BM, rb + rows_per);
+    const uint32_t base = static_cast<uint32_t>(__cvta_generic_to_shared(red));
+    for (int idx = tid; idx < (re - rb) * (BN / 4); idx += 256) {
+      const int row = rb + idx / (BN / 4), c4 = idx % (BN / 4);
+      const uint32_t off = base + (uint32_t)(row * BN + 4 * c4) * 4u;
+      float v[4] = {0.f, 0.f, 0.f, 0.f};
+      for (int q = 0; q < splits; ++q) {
+        uint32_t remote;
+        asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(remote) : "r"(off), "r"(q));
+        float x0, x1, x2, x3;
+        asm volatile("ld.shared::cluster.v4.f32 {%0, %1, %2, %3}, [%4];"
+                     : "=f"(x0), "=f"(x1), "=f"(x2), "=f"(x3)
+                     : "r"(remote)
+                     : "memory");
+        v[0] += x0; v[1] += x1; v[2] += x2; v[3] += x3;
+      }
+      const int64_t gm = m0 + row;
+      if (gm < g.M && n0 + 4 * c4 < g.N) {
+        const float alpha = g.alpha_rows ? g.alpha_rows[bz * g.M + gm] : 1.f;
+        store_row4(g, bz, gm, n0 + 4 * c4, v, alpha);
+      }
+    }
+    // peers' shared memory stays live until every CTA has read it
+    asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" :::
+                     "memory");
+  } else if (partials == nullptr) {
 #pragma unroll
     for (int i = 0; i < 4; ++i) {
       const int64_t gm = m0 + tm + i;
@@ -264,31 +340,81 @@ static int simt_splits(const GemmArgs& g) {
   if ((int64_t)g.batch * g.M * g.N >= 0x7fffffff) return 1;  // 32-bit reduction indexing
   const int64_t tiles = ((g.N + BN - 1) / BN) * ((g.M + BM - 1) / BM) * g.batch;
   if (tiles >= kNumSMs || g.K < 64) return 1;
-  // aim for >= 148 CTAs with >= 2 k-tiles (32) each
+  // aim for >= 148 CTAs with >= 2 k-tiles (32) each; a split-K group is one
+  // cluster (<= 16 CTAs), so the reduction stays on chip
   int64_t s = (kNumSMs + tiles - 1) / tiles;
   s = std::min<int64_t>(s, g.K / 32);
-  s = std::min<int64_t>(s, 64);
+  s = std::min<int64_t>(s, 16);
   return (int)std::max<int64_t>(s, 1);
 }
 
+constexpr int kMaxSimtCluster = 16;  // non-portable cluster size (B200 supports 16)
+
+static bool cluster16_ok() {
+  static int ok = -1;
+  if (ok < 0) {
+    ok = cudaFuncSetAttribute(gemm_simt_kernel<false, true>,
+                              cudaFuncAttributeNonPortableClusterSizeAllowed, 1) == cudaSuccess &&
+         cudaFuncSetAttribute(gemm_simt_kernel<true, true>,
+                              cudaFuncAttributeNonPortableClusterSizeAllowed, 1) == cudaSuccess;
+    cudaGetLastError();
+  }
+  return ok == 1;
+}
+
+static int cluster_cap() { return cluster16_ok() ? kMaxSimtCluster : 8; }
+
 int64_t gemm_simt_workspace(const GemmArgs& g) {
   const int s = simt_splits(g);
-  return s > 1 ? (int64_t)s * g.batch * g.M * g.N * 4 : 0;
+  return (s > 1 && (s > cluster_cap() || getenv_flag("PFB_SIMT_NO_CLUSTER")))
+             ? (int64_t)s * g.batch * g.M * g.N * 4 : 0;
+}
+
+template <bool KS>
+static void launch_clustered(const GemmArgs& g, dim3 grid, int splits, int64_t kchunk,
+                             cudaStream_t s) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = dim3(256);
+  cfg.stream = s;
+  cudaLaunchAttribute at[2];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = 1;
+  at[0].val.clusterDim.y = 1;
+  at[0].val.clusterDim.z = (unsigned)splits;
+  at[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[1].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = pdl_enabled() ? 2 : 1;
+  cudaLaunchKernelEx(&cfg, gemm_simt_kernel<KS, true>, g, splits, kchunk, (float*)nullptr);
 }
 
 int gemm_simt(const GemmArgs& g, void* ws, int64_t ws_bytes, cudaStream_t s) {
   if (g.batch == 0 || g.M == 0 || g.N == 0) return 0;
   if (g.K <= 16) return smallk_launch(g, s);
   int splits = simt_splits(g);
-  if (splits > 1 && (ws == nullptr || ws_bytes < gemm_simt_workspace(g))) splits = 1;
+  const bool no_cluster = getenv_flag("PFB_SIMT_NO_CLUSTER");
+  // the workspace path only when clusters cannot hold the splits (or are off)
+  bool use_ws = splits > 1 && (no_cluster || splits > cluster_cap());
+  if (use_ws && (ws == nullptr || ws_bytes < (int64_t)splits * g.batch * g.M * g.N * 4)) {
+    use_ws = false;
+    splits = no_cluster ? 1 : std::min(splits, cluster_cap());
+  }
   const int64_t kchunk = ((g.K + splits - 1) / splits + BK - 1) / BK * BK;
+  splits = (int)((g.K + kchunk - 1) / kchunk);  // no empty splits
   dim3 grid((unsigned)((g.N + BN - 1) / BN), (unsigned)((g.M + BM - 1) / BM),
             (unsigned)(g.batch * splits));
   if (grid.y > 65535 || grid.z > 65535) return PFB_E_UNSUPPORTED;
+  if (splits > 1 && !use_ws) {
+    if (g.kscale) launch_clustered<true>(g, grid, splits, kchunk, s);
+    else launch_clustered<false>(g, grid, splits, kchunk, s);
+    return launch_status();
+  }
+  float* part = splits > 1 ? (float*)ws : nullptr;
   if (g.kscale)
-    launch(gemm_simt_kernel<true>, grid, 256, 0, s, g, splits, kchunk, splits > 1 ? (float*)ws : nullptr);
+    launch(gemm_simt_kernel<true, false>, grid, 256, 0, s, g, splits, kchunk, part);
   else
-    launch(gemm_simt_kernel<false>, grid, 256, 0, s, g, splits, kchunk, splits > 1 ? (float*)ws : nullptr);
+    launch(gemm_simt_kernel<false, false>, grid, 256, 0, s, g, splits, kchunk, part);
   if (splits > 1)
     launch(splitk_reduce, grid_for(g.batch * g.M * g.N, 256), 256, 0, s, g, splits, (const float*)ws);
   return launch_status();

@@ -278,6 +278,7 @@ gemm_kernel(const __grid_constant__ CUtensorMap map_ah, const __grid_constant__ 
             // 1 KB atom (MN-major)
             const uint64_t astep = amn ? (1024 >> 4) : ((UMMA_K * 4) >> 4);
             const uint64_t bstep = bmn ? (1024 >> 4) : ((UMMA_K * 4) >> 4);
+            const bool lo_lo = p.a_mode != kPreSplit && p.b_mode != kPreSplit;
 #pragma unroll
             for (int k = 0; k < BK / UMMA_K; ++k) {
               const uint64_t da = astep * k, db = bstep * k;
@@ -285,6 +286,9 @@ gemm_kernel(const __grid_constant__ CUtensorMap map_ah, const __grid_constant__ 
               mma_tf32(tmem_d, a_hi + da, b_hi + db, p.idesc, acc);
               mma_tf32(tmem_d, a_hi + da, b_lo + db, p.idesc, 1u);
               mma_tf32(tmem_d, a_lo + da, b_hi + db, p.idesc, 1u);
+              // both operands raw: hi = trunc_tf32 on both sides makes the
+              // dropped lo*lo term sign-biased, so it is kept
+              if (lo_lo) mma_tf32(tmem_d, a_lo + da, b_lo + db, p.idesc, 1u);
             }
             mma_commit(&empty[s]);
           }

@@ -176,6 +176,46 @@ __global__ void __launch_bounds__(256) reduce_outer(RedDesc D, int64_t K, int64_
   }
 }
 
+// Outer reduction in one launch for moderate R: a block owns 32 outputs
+// (lanes) and splits R over its 8 warps; the 8 partial sums are combined in
+// warp order through shared memory (deterministic, no second pass).
+template <typename T, bool PROD>
+__global__ void __launch_bounds__(256) reduce_outer_tile(RedDesc D, int64_t K, int64_t R,
+                                                         const T* x, const T* y, T* dst) {
+  pdl_enter();
+  __shared__ T part[8][33];
+  const int lane = threadIdx.x & 31, grp = threadIdx.x >> 5;
+  const int64_t k = (int64_t)blockIdx.x * 32 + lane;
+  const int64_t chunk = (R + 7) / 8;
+  const int64_t r0 = grp * chunk, r1 = min(R, r0 + chunk);
+  Acc<T> acc;
+  if (k < K) {
+    int64_t base, basey;
+    decode2(D.kr, D.kshape, D.kst, D.kst_y, k, &base, &basey);
+    if (D.rr == 1) {
+      const T* p = x + base;
+      const int64_t st = D.rst[0];
+      if (PROD) {
+        const T* q = y + basey;
+        const int64_t sy = D.rst_y[0];
+        for (int64_t r = r0; r < r1; ++r) acc.add(__ldg(p + r * st) * __ldg(q + r * sy));
+      } else {
+        for (int64_t r = r0; r < r1; ++r) acc.add(__ldg(p + r * st));
+      }
+    } else {
+      for (int64_t r = r0; r < r1; ++r) acc.add(elem<T, PROD>(D, x, y, base, basey, r));
+    }
+  }
+  part[grp][lane] = acc.s;
+  __syncthreads();
+  if (grp == 0 && k < K) {
+    Acc<T> tot;
+#pragma unroll
+    for (int g = 0; g < 8; ++g) tot.add(part[g][lane]);
+    dst[k] = tot.s;
+  }
+}
+
 template <typename T>
 __global__ void sum_partials(int64_t K, int nsplit, bool k_major, const T* ws, T* out) {
   pdl_enter();
@@ -258,6 +298,11 @@ int reduce_run(const pfb_tensor* x, const int64_t* ystride, const T* yp, uint32_
     launch(reduce_inner_block<T, PROD>, (unsigned)(K * nsplit), 256, 0, s, D, K, R, nsplit, xp, yp,
                                                                   nsplit == 1 ? o : (T*)ws);
     if (nsplit > 1) launch(sum_partials<T>, grid_for(K, 256), 256, 0, s, K, nsplit, true, (const T*)ws, o);
+    return launch_status();
+  }
+  if (K <= 8192 && R <= 512 && R >= 16) {
+    // few outputs, moderate R: single-launch tile reduction
+    launch(reduce_outer_tile<T, PROD>, (unsigned)((K + 31) / 32), 256, 0, s, D, K, R, xp, yp, o);
     return launch_status();
   }
   int gx = grid_for(K, 256, 8);

@@ -152,10 +152,19 @@ __device__ __forceinline__ uint64_t smem_desc_mn_sw128(uint32_t addr, uint32_t l
   return d;
 }
 
-// hi = rn_tf32(x) in place, lo = rn_tf32(x - hi) for `n16` 16-byte chunks of
-// a shared-memory tile (elementwise, so any TMA swizzle is preserved).
-// Explicit ld/st.shared: through a generic pointer the compiler emits
-// generic LD/ST, which cost address translation on every access.
+// In-smem split of a raw fp32 tile for the 3xTF32 products.  The tensor
+// core reads a kind::tf32 operand by dropping the low 13 mantissa bits, so
+// the raw tile already *is* the hi plane hi = trunc_tf32(x); only
+// lo = rn_tf32(x - hi) (x - hi exact in fp32) is written, with integer ops:
+// no conversion instructions and half the shared-memory stores of an
+// explicit hi/lo split.  |x - hi - lo| <= 2^-22 |x| as before.
+__device__ __forceinline__ float lo_of_raw(float x) {
+  const uint32_t b = __float_as_uint(x);
+  if ((b & 0x7F800000u) == 0x7F800000u) return 0.f;  // inf/nan: hi carries it
+  const float d = x - __uint_as_float(b & 0xFFFFE000u);
+  return __uint_as_float((__float_as_uint(d) + 0x1000u) & 0xFFFFE000u);
+}
+
 __device__ __forceinline__ void split_tf32_smem(uint32_t hi, uint32_t lo, int n16, int t,
                                                 int nthreads) {
   for (int i = t; i < n16; i += nthreads) {
@@ -163,13 +172,8 @@ __device__ __forceinline__ void split_tf32_smem(uint32_t hi, uint32_t lo, int n1
     asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];"
                  : "=f"(x0), "=f"(x1), "=f"(x2), "=f"(x3)
                  : "r"(hi + 16 * i));
-    const float h0 = to_tf32(x0), h1 = to_tf32(x1), h2 = to_tf32(x2), h3 = to_tf32(x3);
-    asm volatile("st.shared.v4.f32 [%0], {%1, %2, %3, %4};" ::"r"(hi + 16 * i), "f"(h0), "f"(h1),
-                 "f"(h2), "f"(h3)
-                 : "memory");
     asm volatile("st.shared.v4.f32 [%0], {%1, %2, %3, %4};" ::"r"(lo + 16 * i),
-                 "f"(tf32_lo(x0, h0)), "f"(tf32_lo(x1, h1)), "f"(tf32_lo(x2, h2)),
-                 "f"(tf32_lo(x3, h3))
+                 "f"(lo_of_raw(x0)), "f"(lo_of_raw(x1)), "f"(lo_of_raw(x2)), "f"(lo_of_raw(x3))
                  : "memory");
   }
 }

@@ -398,7 +398,10 @@ class Executor:
             arr = v if isinstance(v, torch.Tensor) else np.asarray(v)
             static[name] = DArray.empty(tuple(arr.shape), dt, self.device)
         saved = (self._ws, self._err, self._err_nodes)
-        self._ws, self._err = None, None
+        # error words zeroed once here, outside the graph: replays only set
+        # bits on error, and a run that reports one re-zeroes them
+        self._ws, self._err, self._err_nodes = None, None, []
+        self._err = torch.zeros(_ERR_SLOTS, dtype=torch.int32, device=self.device)
         graph = torch.cuda.CUDAGraph()
         cap = None
         try:
@@ -772,6 +775,7 @@ class Executor:
                          E.IndexCollision("scatter_rows: overlapping index sets")
                          if b & N.DEV_COLLISION else
                          E.IncompleteCover("scatter_rows: rows uncovered"))
+                buf.zero_()  # replayed graphs do not reset their error words
                 raise E.ExecError(nodes[k], cause)
 
     def _writeback_vars(self):

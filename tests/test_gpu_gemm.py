@@ -129,13 +129,16 @@ def test_gemm_tcgen05_matches_simt_error_scale(env, k):
 
 def test_gemm_tcgen05_no_accumulation_bias(env):
     """Truncating in-TMEM accumulation would bias results toward zero linearly
-    in K; the chunked RN accumulation must not."""
+    in K (measured ~1e-4 relative at K=4096 with full-K TMEM accumulation,
+    i.e. ~1e-2 absolute here); the chunked RN accumulation must not.  The
+    bound (1e-6 absolute on |values| ~ 90, ~1e-8 relative) leaves the
+    residual per-chunk truncation of the 64-deep TMEM chunks."""
     r = np.random.default_rng(5)
     a, b = _operands(r, (256, 8192), (8192, 256))
     want = a @ b
     got = _run(env, a, b, 2, transpose_b=True)
     bias = np.mean((got - want) * np.sign(want))
-    assert abs(bias) < 5e-7, bias
+    assert abs(bias) < 1e-6, bias
 
 
 @pytest.mark.parametrize("shape", [(4096, 1, 4096, 1), (300, 1, 1024, 3), (64, 2, 520, 1)])

@@ -309,3 +309,23 @@ def test_replayed_results_stay_valid(Executor):
         for a, b in zip(res, want[i % 3]):
             np.testing.assert_allclose(a.data, b.data, rtol=1e-6, atol=1e-7)
     assert len(cap.host_pack["slots"]) == n_slots == ex._IO_SLOTS + 1
+
+
+def test_replayed_graph_errors_raise_once(Executor):
+    """Device error words of a captured graph travel with its packed results:
+    an out-of-range index fed to a replay raises ExecError(IndexOutOfBounds);
+    the next valid run does not see stale bits."""
+    from paper_1903_04243_b200 import GraphBuilder, errors
+    from paper_1903_04243_b200.tensor import DType
+    b = GraphBuilder()
+    idx = b.placeholder("idx", DType.I64, (3,))
+    b.graph.set_outputs([b.gather(b.const(np.arange(12.0).reshape(4, 3)), idx)])
+    ex = Executor(b.graph)
+    good, bad = {"idx": np.array([0, 3, 1])}, {"idx": np.array([0, 7, 1])}
+    for _ in range(3):
+        np.testing.assert_allclose(ex.run(good)[0].data, np.arange(12.0).reshape(4, 3)[[0, 3, 1]])
+    assert ex._captures
+    with pytest.raises(errors.ExecError) as e:
+        ex.run(bad)
+    assert isinstance(e.value.cause, errors.IndexOutOfBounds)
+    np.testing.assert_allclose(ex.run(good)[0].data, np.arange(12.0).reshape(4, 3)[[0, 3, 1]])
