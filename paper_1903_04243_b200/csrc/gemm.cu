@@ -111,6 +111,9 @@ int run_path(const GemmArgs& g, int path, void* ws, int64_t ws_bytes, cudaStream
     case 1: return gemm_simt(g, ws, ws_bytes, s);
     case 3: return gemm_tcgen05(g, ws, ws_bytes, s, 1);
     case 4: return gemm_tcgen05(g, ws, ws_bytes, s, 2);
+    case 7: return gemm_tcgen05(g, ws, ws_bytes, s, 2, 2);  // raw feed, 2 / 4 k-splits
+    case 8: return gemm_tcgen05(g, ws, ws_bytes, s, 2, 4);
+    case 9: return gemm_tcgen05(g, ws, ws_bytes, s, 1, 4);  // pre-split, 4 k-splits
     case 5: return gemm_tcgen05_pair(g, ws, ws_bytes, s, 1);
     case 6: return gemm_tcgen05_pair(g, ws, ws_bytes, s, 2);
     default: return gemm_tcgen05(g, ws, ws_bytes, s, 0);
@@ -206,7 +209,7 @@ static int matmul_impl(GemmArgs& g, pfb_tensor* out, int32_t force_path, void* w
   // 5 / 6 = CTA-pair tcgen05 (cta_group::2) with pre-split / raw operands.
   // PFB_DISABLE_TCGEN05=1 pins auto to SIMT (A/B testing, bring-up).
   static const bool tc_off = getenv("PFB_DISABLE_TCGEN05") && getenv("PFB_DISABLE_TCGEN05")[0] == '1';
-  if (force_path >= 1 && force_path <= 6) return run_path(g, force_path, ws, ws_bytes, s);
+  if (force_path >= 1 && force_path <= 9) return run_path(g, force_path, ws, ws_bytes, s);
   const bool tc_ok = !tc_off && gemm_tcgen05_eligible(g) &&
                      ws_bytes >= gemm_tcgen05_workspace(g) && ws != nullptr &&
                      (double)g.batch * g.M * g.N * g.K >= (double)(1 << 20);
@@ -223,11 +226,19 @@ static int matmul_impl(GemmArgs& g, pfb_tensor* out, int32_t force_path, void* w
     cudaStreamIsCapturing(s, &st);
     if (autotune_enabled() && !accumulate && st == cudaStreamCaptureStatusNone) {
       // every candidate runs twice; the last one timed leaves C computed
-      int cand[5];
+      int cand[9];
       int ncand = 0;
       cand[ncand++] = 1;
       cand[ncand++] = 3;
-      if (gemm_tcgen05_raw_possible(g)) cand[ncand++] = 4;
+      // forced k-splits only where tiles leave SMs idle (the model's split
+      // choice is a heuristic; the timing decides)
+      const int64_t tiles128 = ((g.M + 127) / 128) * ((g.N + 127) / 128) * g.batch;
+      const bool few_tiles = tiles128 < 148 && g.K >= 256;
+      if (few_tiles) cand[ncand++] = 9;
+      if (gemm_tcgen05_raw_possible(g)) {
+        cand[ncand++] = 4;
+        if (few_tiles) { cand[ncand++] = 7; cand[ncand++] = 8; }
+      }
       if (g.M > 128 && !tc_pair_off()) {
         cand[ncand++] = 5;
         if (gemm_tcgen05_raw_possible(g)) cand[ncand++] = 6;

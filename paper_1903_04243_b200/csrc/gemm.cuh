@@ -50,7 +50,9 @@ int64_t gemm_simt_workspace(const GemmArgs& g);
 // returns PFB_E_UNSUPPORTED when the shape/layout is not eligible
 // variant: 0 = auto, 1 = operands pre-split by split_kernel, 2 = raw operands
 // fed by TMA and split in shared memory wherever the layout allows it
-int gemm_tcgen05(const GemmArgs& g, void* ws, int64_t ws_bytes, cudaStream_t s, int variant = 0);
+// ksplit_want > 0 forces that many k-splits (autotune candidates), 0 = model
+int gemm_tcgen05(const GemmArgs& g, void* ws, int64_t ws_bytes, cudaStream_t s, int variant = 0,
+                 int ksplit_want = 0);
 int64_t gemm_tcgen05_workspace(const GemmArgs& g);
 bool gemm_tcgen05_eligible(const GemmArgs& g);    // layout constraints
 bool gemm_tcgen05_raw_possible(const GemmArgs& g);

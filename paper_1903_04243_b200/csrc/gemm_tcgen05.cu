@@ -656,7 +656,8 @@ bool gemm_tcgen05_profitable(const GemmArgs& g) {
 
 // variant: 0 = auto (raw feed for small problems), 1 = pre-split both
 // operands, 2 = raw feed wherever the operand layout allows it
-int gemm_tcgen05(const GemmArgs& g, void* ws, int64_t ws_bytes, cudaStream_t s, int variant) {
+int gemm_tcgen05(const GemmArgs& g, void* ws, int64_t ws_bytes, cudaStream_t s, int variant,
+                 int ksplit_want) {
   using namespace tc;
   if (!gemm_tcgen05_eligible(g)) return PFB_E_UNSUPPORTED;
   const int64_t Kp = (g.K + 3) / 4 * 4;
@@ -705,9 +706,10 @@ int gemm_tcgen05(const GemmArgs& g, void* ws, int64_t ws_bytes, cudaStream_t s, 
   }
   int ksplit, kb_per;
   choose_split(g, &ksplit, &kb_per);
-  if (const char* e = getenv("PFB_TC_KSPLIT")) {  // bring-up / tuning override
+  if (const char* e = getenv("PFB_TC_KSPLIT")) ksplit_want = atoi(e);  // bring-up override
+  if (ksplit_want > 0) {  // autotuner candidate / override: this many k-splits
     const int nk = (int)((Kp + BK - 1) / BK);
-    const int want = std::max(1, std::min(atoi(e), kMaxCluster));
+    const int want = std::max(1, std::min(ksplit_want, kMaxCluster));
     kb_per = (nk + want - 1) / want;
     ksplit = (nk + kb_per - 1) / kb_per;
   }
