@@ -128,6 +128,17 @@ int pfb_matmul_ex(const pfb_tensor* a, const pfb_tensor* b, pfb_tensor* out,
                   const float* alpha_rows, int32_t accumulate, int32_t force_path, void* ws,
                   int64_t ws_bytes, void* stream);
 
+/* out = act(a1 @ b1 + a2 @ b2 + bias): two operand pairs, one output
+ * (passes.fuse_dual_matmuls -- matmul of a K-concat, or a sum of matmuls;
+ * reference tensor.py:195-206 + binary add).  tcgen05 path: both K ranges
+ * accumulate in one launch.  force_path 0 = auto (timed once per shape),
+ * 1 = two launches, 2 = tcgen05 raw feed, 3 = tcgen05 pre-split. */
+int64_t pfb_matmul_dual_workspace(const pfb_tensor* a1, const pfb_tensor* b1,
+                                  const pfb_tensor* a2, const pfb_tensor* b2, pfb_tensor* out);
+int pfb_matmul_dual(const pfb_tensor* a1, const pfb_tensor* b1, const pfb_tensor* a2,
+                    const pfb_tensor* b2, pfb_tensor* out, const pfb_tensor* bias, int32_t act,
+                    int32_t force_path, void* ws, int64_t ws_bytes, void* stream);
+
 /* n (<= 8) independent row-dots in one launch (passes.fuse_row_dots):
  * outs[j][i] = sum_k xs[j][i,k] * ys[j][i,k], xs/ys rank-2 [rows, inner_j]
  * views with unit inner stride (any row stride), outs rank-1 [rows].  The

@@ -269,3 +269,108 @@ extern "C" int pfb_matmul(const pfb_tensor* a, const pfb_tensor* b, pfb_tensor* 
                           int64_t ws_bytes, void* stream) {
   return pfb_matmul_ex(a, b, out, nullptr, 0, 0, ws, ws_bytes, stream);
 }
+
+// ---------------------------------------------------------------------------
+// Two operand pairs into one output (passes.fuse_dual_matmuls):
+//   out = act(a1 @ b1 + a2 @ b2 + bias)
+// -- matmul(concat([a1, a2], -1), b) with b split at K1, or the sum of two
+// matmuls.  The tcgen05 path accumulates both K ranges in one launch; the
+// fallback is two GEMM launches, the second accumulating with the epilogue.
+
+namespace {
+std::map<std::tuple<ShapeKey, int64_t, int>, int> g_dual_choice;  // 1 two launches, 2 raw, 3 pre-split
+
+int dual_path(const GemmArgs& g1, const GemmArgs& g2, int path, pfb_tensor* out, void* ws,
+              int64_t ws_bytes, cudaStream_t s) {
+  if (path == 2 || path == 3)
+    return gemm_tcgen05_dual(g1, g2, ws, ws_bytes, s, path == 2 ? 2 : 1);
+  GemmArgs h1 = g1, h2 = g2;
+  h1.bias = nullptr;
+  h1.act = 0;
+  h2.accumulate = 1;
+  h2.bias = g1.bias;
+  h2.sxb = g1.sxb; h2.sxm = g1.sxm; h2.sxn = g1.sxn;
+  h2.act = g1.act;
+  if (int e = matmul_impl(h1, out, 0, ws, ws_bytes, s)) return e;
+  return matmul_impl(h2, out, 0, ws, ws_bytes, s);
+}
+
+float time_dual(const GemmArgs& g1, const GemmArgs& g2, int path, pfb_tensor* out, void* ws,
+                int64_t ws_bytes, cudaStream_t s) {
+  cudaEvent_t e0, e1;
+  cudaEventCreate(&e0);
+  cudaEventCreate(&e1);
+  float ms = 1e30f;
+  for (int rep = 0; rep < 2; ++rep) {
+    cudaEventRecord(e0, s);
+    int rc = dual_path(g1, g2, path, out, ws, ws_bytes, s);
+    cudaEventRecord(e1, s);
+    cudaEventSynchronize(e1);
+    if (rc != 0) { ms = 1e30f; break; }
+    cudaEventElapsedTime(&ms, e0, e1);
+  }
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  return ms;
+}
+}  // namespace
+
+extern "C" int64_t pfb_matmul_dual_workspace(const pfb_tensor* a1, const pfb_tensor* b1,
+                                             const pfb_tensor* a2, const pfb_tensor* b2,
+                                             pfb_tensor* out) {
+  GemmArgs g1, g2;
+  if (matmul_args(a1, b1, out, &g1) || matmul_args(a2, b2, out, &g2)) return 0;
+  return std::max({gemm_tcgen05_dual_workspace(g1, g2), gemm_tcgen05_workspace(g1),
+                   gemm_tcgen05_workspace(g2), gemm_simt_workspace(g1), gemm_simt_workspace(g2)});
+}
+
+extern "C" int pfb_matmul_dual(const pfb_tensor* a1, const pfb_tensor* b1, const pfb_tensor* a2,
+                               const pfb_tensor* b2, pfb_tensor* out, const pfb_tensor* bias,
+                               int32_t act, int32_t force_path, void* ws, int64_t ws_bytes,
+                               void* stream) {
+  GemmArgs g1, g2;
+  if (int e = matmul_args(a1, b1, out, &g1)) return e;
+  if (int e = matmul_args(a2, b2, out, &g2)) return e;
+  if (act < PFB_ACT_NONE || act > PFB_ACT_RELU) return PFB_E_ARG;
+  g1.act = act;
+  if (bias) {
+    if (bias->dtype != PFB_F32) return PFB_E_DTYPE;
+    int64_t st[3];
+    if (!broadcast_strides(bias, out->rank, out->shape, st)) return PFB_E_SHAPE;
+    g1.bias = (const float*)bias->data;
+    if (a1->rank == 3) { g1.sxb = st[0]; g1.sxm = st[1]; g1.sxn = st[2]; }
+    else { g1.sxb = 0; g1.sxm = st[0]; g1.sxn = st[1]; }
+  }
+  cudaStream_t s = as_stream(stream);
+  if (g1.batch == 0 || g1.M == 0 || g1.N == 0) return 0;
+  static const bool tc_off = getenv_flag("PFB_DISABLE_TCGEN05") || getenv_flag("PFB_DISABLE_DUAL");
+  if (force_path >= 1 && force_path <= 3) return dual_path(g1, g2, force_path, out, ws, ws_bytes, s);
+  const bool tc_ok = !tc_off && g1.K > 0 && g2.K > 0 && gemm_tcgen05_eligible(g1) &&
+                     gemm_tcgen05_eligible(g2) && ws != nullptr &&
+                     ws_bytes >= gemm_tcgen05_dual_workspace(g1, g2) &&
+                     (double)g1.batch * g1.M * g1.N * (g1.K + g2.K) >= (double)(1 << 20);
+  if (!tc_ok) return dual_path(g1, g2, 1, out, ws, ws_bytes, s);
+  const auto key = std::make_tuple(key_of(g1), g2.K, (int)(g2.sak == 1) + 2 * (int)(g2.sbk == 1));
+  int path = 0;
+  {
+    std::lock_guard<std::mutex> lk(g_mu);
+    auto it = g_dual_choice.find(key);
+    if (it != g_dual_choice.end()) path = it->second;
+  }
+  if (path == 0) {
+    cudaStreamCaptureStatus st = cudaStreamCaptureStatusNone;
+    cudaStreamIsCapturing(s, &st);
+    if (!autotune_enabled() || st != cudaStreamCaptureStatusNone)
+      return dual_path(g1, g2, 2, out, ws, ws_bytes, s);
+    float best = 1e30f;
+    for (int cand : {1, 3, 2}) {
+      const float t = time_dual(g1, g2, cand, out, ws, ws_bytes, s);
+      if (t < best) { best = t; path = cand; }
+    }
+    std::lock_guard<std::mutex> lk(g_mu);
+    g_dual_choice[key] = path;
+  }
+  const int e = dual_path(g1, g2, path, out, ws, ws_bytes, s);
+  if (e == PFB_E_UNSUPPORTED && path != 1) return dual_path(g1, g2, 1, out, ws, ws_bytes, s);
+  return e;
+}

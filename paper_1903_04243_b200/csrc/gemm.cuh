@@ -54,6 +54,11 @@ int64_t gemm_simt_workspace(const GemmArgs& g);
 int gemm_tcgen05(const GemmArgs& g, void* ws, int64_t ws_bytes, cudaStream_t s, int variant = 0,
                  int ksplit_want = 0);
 int64_t gemm_tcgen05_workspace(const GemmArgs& g);
+// C = epi(A1 B1 + A2 B2) in one tcgen05 launch (consecutive K ranges of one
+// accumulation); g1 carries C and the epilogue, g2 only its operands
+int gemm_tcgen05_dual(const GemmArgs& g1, const GemmArgs& g2, void* ws, int64_t ws_bytes,
+                      cudaStream_t s, int variant = 0, int ksplit_want = 0);
+int64_t gemm_tcgen05_dual_workspace(const GemmArgs& g1, const GemmArgs& g2);
 bool gemm_tcgen05_eligible(const GemmArgs& g);    // layout constraints
 bool gemm_tcgen05_raw_possible(const GemmArgs& g);
 bool gemm_tcgen05_profitable(const GemmArgs& g);  // size heuristic for auto

@@ -125,6 +125,11 @@ struct Params {
   uint32_t mn_lbo, mn_sbo;  // MN-major descriptor strides (4 KB, 512 B)
   int tma_store;            // epilogue stores 32x32 blocks with TMA (map_c)
   unsigned long long* trace;  // PFB_TC_TRACE: globaltimer stamps of CTA 0 (bring-up)
+  // second operand pair (C = A B + A2 B2, one accumulation): k-blocks
+  // [nk1, nk) come from map_*2 with their own feed modes and broadcast flags
+  int nk1;
+  int a_mode2, b_mode2, a_bcast2, b_bcast2;
+  uint32_t idesc2;
 };
 
 __device__ __forceinline__ void stamp(const Params& p, int i) {
@@ -167,7 +172,9 @@ __device__ __forceinline__ void split_tile_smem(uint8_t* hi, uint8_t* lo, int t)
 __global__ void __launch_bounds__(NUM_THREADS, 1)
 gemm_kernel(const __grid_constant__ CUtensorMap map_ah, const __grid_constant__ CUtensorMap map_al,
             const __grid_constant__ CUtensorMap map_bh, const __grid_constant__ CUtensorMap map_bl,
-            const __grid_constant__ CUtensorMap map_c, Params p) {
+            const __grid_constant__ CUtensorMap map_c, const __grid_constant__ CUtensorMap map_ah2,
+            const __grid_constant__ CUtensorMap map_al2, const __grid_constant__ CUtensorMap map_bh2,
+            const __grid_constant__ CUtensorMap map_bl2, Params p) {
   stamp(p, 0);
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>(
@@ -188,7 +195,9 @@ gemm_kernel(const __grid_constant__ CUtensorMap map_ah, const __grid_constant__ 
   // clustered: exactly one work unit per CTA (cluster rank = k-split index)
   const int ntiles = clustered ? (int)blockIdx.x + 1 : tiles_per_batch * p.batch * p.ksplit;
   const int ustride = clustered ? 1 : (int)gridDim.x;
-  const bool split_smem = p.a_mode != kPreSplit || p.b_mode != kPreSplit;
+  const bool dual = p.nk1 < (p.K + BK - 1) / BK;
+  const bool split_smem = p.a_mode != kPreSplit || p.b_mode != kPreSplit ||
+                          (dual && (p.a_mode2 != kPreSplit || p.b_mode2 != kPreSplit));
 
   auto tile = [&](int s, int which) { return smem + s * STAGE_BYTES + which * TILE_BYTES; };
   // which: 0 = A_hi, 1 = A_lo, 2 = B_hi, 3 = B_lo
@@ -208,6 +217,10 @@ gemm_kernel(const __grid_constant__ CUtensorMap map_ah, const __grid_constant__ 
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&map_al)) : "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&map_bh)) : "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&map_bl)) : "memory");
+    if (dual) {
+      asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&map_ah2)) : "memory");
+      asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&map_bh2)) : "memory");
+    }
   }
   if (warp == 1) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
@@ -226,8 +239,7 @@ gemm_kernel(const __grid_constant__ CUtensorMap map_ah, const __grid_constant__ 
   pdl_enter();
   if (threadIdx.x == 0) stamp(p, 2);
 
-  const int bytes_a = (p.a_mode == kPreSplit ? 2 : 1) * TILE_BYTES;
-  const int bytes_b = (p.b_mode == kPreSplit ? 2 : 1) * TILE_BYTES;
+  auto tile_bytes = [&](int mode) { return (mode == kPreSplit ? 2 : 1) * TILE_BYTES; };
 
   if (warp == 0) {
     if (lane == 0) {
@@ -236,14 +248,21 @@ gemm_kernel(const __grid_constant__ CUtensorMap map_ah, const __grid_constant__ 
         const int t = u / p.ksplit, ks = u % p.ksplit;
         const int bz = t / tiles_per_batch, r = t % tiles_per_batch;
         const int m0 = (r / p.ntn) * BM, n0 = (r % p.ntn) * BN;
-        const int za = p.a_bcast ? 0 : bz, zb = p.b_bcast ? 0 : bz;
         const int kb0 = ks * p.kb_per_split, kb1 = min(nk, kb0 + p.kb_per_split);
         for (int kb = kb0; kb < kb1; ++kb, ++g) {
           const int s = g % STAGES;
           if (g >= STAGES) mbar_wait(&empty[s], ((g / STAGES) - 1) & 1);
-          mbar_expect_tx(&full[s], bytes_a + bytes_b);
-          tma_load_operand(&map_ah, &map_al, p.a_mode, &full[s], tile(s, 0), tile(s, 1), kb, m0, za);
-          tma_load_operand(&map_bh, &map_bl, p.b_mode, &full[s], tile(s, 2), tile(s, 3), kb, n0, zb);
+          if (kb < p.nk1) {
+            const int za = p.a_bcast ? 0 : bz, zb = p.b_bcast ? 0 : bz;
+            mbar_expect_tx(&full[s], tile_bytes(p.a_mode) + tile_bytes(p.b_mode));
+            tma_load_operand(&map_ah, &map_al, p.a_mode, &full[s], tile(s, 0), tile(s, 1), kb, m0, za);
+            tma_load_operand(&map_bh, &map_bl, p.b_mode, &full[s], tile(s, 2), tile(s, 3), kb, n0, zb);
+          } else {
+            const int za = p.a_bcast2 ? 0 : bz, zb = p.b_bcast2 ? 0 : bz, k2 = kb - p.nk1;
+            mbar_expect_tx(&full[s], tile_bytes(p.a_mode2) + tile_bytes(p.b_mode2));
+            tma_load_operand(&map_ah2, &map_al2, p.a_mode2, &full[s], tile(s, 0), tile(s, 1), k2, m0, za);
+            tma_load_operand(&map_bh2, &map_bl2, p.b_mode2, &full[s], tile(s, 2), tile(s, 3), k2, n0, zb);
+          }
           if (g == 0) stamp(p, 3);
         }
       }
@@ -269,7 +288,10 @@ gemm_kernel(const __grid_constant__ CUtensorMap map_ah, const __grid_constant__ 
             asm volatile("tcgen05.fence::after_thread_sync;");
             const uint32_t a0 = smem_u32(tile(s, 0)), a1 = smem_u32(tile(s, 1));
             const uint32_t b0 = smem_u32(tile(s, 2)), b1 = smem_u32(tile(s, 3));
-            const bool amn = p.a_mode == kRawMN, bmn = p.b_mode == kRawMN;
+            const bool second = kb >= p.nk1;
+            const int am_ = second ? p.a_mode2 : p.a_mode, bm_ = second ? p.b_mode2 : p.b_mode;
+            const uint32_t idesc = second ? p.idesc2 : p.idesc;
+            const bool amn = am_ == kRawMN, bmn = bm_ == kRawMN;
             const uint64_t a_hi = amn ? smem_desc_mn_sw128(a0, p.mn_lbo, p.mn_sbo) : smem_desc_sw128(a0);
             const uint64_t a_lo = amn ? smem_desc_mn_sw128(a1, p.mn_lbo, p.mn_sbo) : smem_desc_sw128(a1);
             const uint64_t b_hi = bmn ? smem_desc_mn_sw128(b0, p.mn_lbo, p.mn_sbo) : smem_desc_sw128(b0);
@@ -278,17 +300,17 @@ gemm_kernel(const __grid_constant__ CUtensorMap map_ah, const __grid_constant__ 
             // 1 KB atom (MN-major)
             const uint64_t astep = amn ? (1024 >> 4) : ((UMMA_K * 4) >> 4);
             const uint64_t bstep = bmn ? (1024 >> 4) : ((UMMA_K * 4) >> 4);
-            const bool lo_lo = p.a_mode != kPreSplit && p.b_mode != kPreSplit;
+            const bool lo_lo = am_ != kPreSplit && bm_ != kPreSplit;
 #pragma unroll
             for (int k = 0; k < BK / UMMA_K; ++k) {
               const uint64_t da = astep * k, db = bstep * k;
               const uint32_t acc = (kb > kb_beg || k > 0) ? 1u : 0u;
-              mma_tf32(tmem_d, a_hi + da, b_hi + db, p.idesc, acc);
-              mma_tf32(tmem_d, a_hi + da, b_lo + db, p.idesc, 1u);
-              mma_tf32(tmem_d, a_lo + da, b_hi + db, p.idesc, 1u);
+              mma_tf32(tmem_d, a_hi + da, b_hi + db, idesc, acc);
+              mma_tf32(tmem_d, a_hi + da, b_lo + db, idesc, 1u);
+              mma_tf32(tmem_d, a_lo + da, b_hi + db, idesc, 1u);
               // both operands raw: hi = trunc_tf32 on both sides makes the
               // dropped lo*lo term sign-biased, so it is kept
-              if (lo_lo) mma_tf32(tmem_d, a_lo + da, b_lo + db, p.idesc, 1u);
+              if (lo_lo) mma_tf32(tmem_d, a_lo + da, b_lo + db, idesc, 1u);
             }
             mma_commit(&empty[s]);
           }
@@ -307,12 +329,13 @@ gemm_kernel(const __grid_constant__ CUtensorMap map_ah, const __grid_constant__ 
     float* stage = reinterpret_cast<float*>(smem + STAGES * STAGE_BYTES) +
                    (warp - 2) * EPI_STAGE_FLOATS;
     int gc = 0, gs = 0;
-    auto split_stage = [&]() {
+    auto split_stage = [&](int kb) {
       const int s = gs % STAGES;
       mbar_wait(&full[s], (gs / STAGES) & 1);
       if (gs == 0 && et == 0) stamp(p, 4);
-      if (p.a_mode != kPreSplit) split_tile_smem(tile(s, 0), tile(s, 1), et);
-      if (p.b_mode != kPreSplit) split_tile_smem(tile(s, 2), tile(s, 3), et);
+      const bool second = kb >= p.nk1;
+      if ((second ? p.a_mode2 : p.a_mode) != kPreSplit) split_tile_smem(tile(s, 0), tile(s, 1), et);
+      if ((second ? p.b_mode2 : p.b_mode) != kPreSplit) split_tile_smem(tile(s, 2), tile(s, 3), et);
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
       __syncwarp();
       if (lane == 0) mbar_arrive(&ready[s]);
@@ -350,7 +373,7 @@ gemm_kernel(const __grid_constant__ CUtensorMap map_ah, const __grid_constant__ 
       for (int c = 0; c < uchunks; ++c) {
         if (split_smem) {
           const int kb_beg = kb0 + c * CHUNK_KB, kb_end = min(kb1, kb_beg + CHUNK_KB);
-          for (int kb = kb_beg; kb < kb_end; ++kb) split_stage();
+          for (int kb = kb_beg; kb < kb_end; ++kb) split_stage(kb);
         }
         if (c > 0) drain();
       }
@@ -656,65 +679,88 @@ bool gemm_tcgen05_profitable(const GemmArgs& g) {
 
 // variant: 0 = auto (raw feed for small problems), 1 = pre-split both
 // operands, 2 = raw feed wherever the operand layout allows it
-int gemm_tcgen05(const GemmArgs& g, void* ws, int64_t ws_bytes, cudaStream_t s, int variant,
-                 int ksplit_want) {
-  using namespace tc;
-  if (!gemm_tcgen05_eligible(g)) return PFB_E_UNSUPPORTED;
+namespace tc {
+
+// One operand pair's TMA feed: raw maps (split in smem) or pre-split hi/lo
+// planes written into the workspace at `w` (advanced past what it uses).
+struct PairFeed {
+  CUtensorMap ah, al, bh, bl;
+  int am = kPreSplit, bm = kPreSplit, a_bc = 0, b_bc = 0;
+  int64_t Kp = 0;
+};
+
+static int64_t pair_need(const GemmArgs& g, int variant, int* am_out, int* bm_out) {
   const int64_t Kp = (g.K + 3) / 4 * 4;
   const int a_bc = g.sab == 0 && g.batch > 1;
-  // a per-batch kscale makes B's planes differ per batch even for a shared B
   const int b_bc = g.sbb == 0 && g.batch > 1 && !(g.kscale && g.skb != 0);
   const int64_t ba = a_bc ? 1 : g.batch, bb = b_bc ? 1 : g.batch;
-  if (variant == 0)
-    variant = (2.0 * g.M * g.N * g.K * g.batch < 4e9) ? 2 : 1;
   int am = kPreSplit, bm = kPreSplit;
   if (variant == 2) {
     am = raw_mode(g.A, g.M, g.K, ba, g.sab, g.sam, g.sak);
     bm = g.kscale ? kPreSplit : raw_mode(g.B, g.N, g.K, bb, g.sbb, g.sbn, g.sbk);
   }
-  const int64_t need = (am == kPreSplit ? 2 * align_up(ba * g.M * Kp * 4) : 0) +
-                       (bm == kPreSplit ? 2 * align_up(bb * g.N * Kp * 4) : 0);
-  if (need > 0 && (ws == nullptr || ws_bytes < need)) return PFB_E_UNSUPPORTED;
-  char* w = static_cast<char*>(ws);
-  CUtensorMap mah, mal, mbh, mbl;
-  if (am == kPreSplit) {
+  *am_out = am;
+  *bm_out = bm;
+  return (am == kPreSplit ? 2 * align_up(ba * g.M * Kp * 4) : 0) +
+         (bm == kPreSplit ? 2 * align_up(bb * g.N * Kp * 4) : 0);
+}
+
+static int prep_pair(const GemmArgs& g, int variant, char*& w, cudaStream_t s, PairFeed* f) {
+  f->Kp = (g.K + 3) / 4 * 4;
+  const int64_t Kp = f->Kp;
+  // a per-batch kscale makes B's planes differ per batch even for a shared B
+  f->a_bc = g.sab == 0 && g.batch > 1;
+  f->b_bc = g.sbb == 0 && g.batch > 1 && !(g.kscale && g.skb != 0);
+  const int64_t ba = f->a_bc ? 1 : g.batch, bb = f->b_bc ? 1 : g.batch;
+  pair_need(g, variant, &f->am, &f->bm);
+  if (f->am == kPreSplit) {
     float* ah = reinterpret_cast<float*>(w); w += align_up(ba * g.M * Kp * 4);
     float* al = reinterpret_cast<float*>(w); w += align_up(ba * g.M * Kp * 4);
     dim3 ga((unsigned)((Kp + 31) / 32), (unsigned)((g.M + 31) / 32), (unsigned)ba);
     launch(split_kernel, ga, 256, 0, s, g.A, g.M, g.K, Kp, g.sab, g.sam, g.sak, ah, al,
            (const float*)nullptr, (int64_t)0, (int64_t)0);
-    if (!make_map(&mah, ah, Kp, g.M, ba) || !make_map(&mal, al, Kp, g.M, ba)) return PFB_E_UNSUPPORTED;
+    if (!make_map(&f->ah, ah, Kp, g.M, ba) || !make_map(&f->al, al, Kp, g.M, ba)) return PFB_E_UNSUPPORTED;
   } else {
-    if (!make_raw_map(&mah, am, g.A, g.M, g.K, ba, g.sab, g.sam, g.sak)) return PFB_E_UNSUPPORTED;
-    mal = mah;
+    if (!make_raw_map(&f->ah, f->am, g.A, g.M, g.K, ba, g.sab, g.sam, g.sak)) return PFB_E_UNSUPPORTED;
+    f->al = f->ah;
   }
-  if (bm == kPreSplit) {
+  if (f->bm == kPreSplit) {
     float* bh = reinterpret_cast<float*>(w); w += align_up(bb * g.N * Kp * 4);
     float* bl = reinterpret_cast<float*>(w); w += align_up(bb * g.N * Kp * 4);
     dim3 gb((unsigned)((Kp + 31) / 32), (unsigned)((g.N + 31) / 32), (unsigned)bb);
     launch(split_kernel, gb, 256, 0, s, g.B, g.N, g.K, Kp, g.sbb, g.sbn, g.sbk, bh, bl, g.kscale,
            g.skb, g.skk);
-    if (!make_map(&mbh, bh, Kp, g.N, bb) || !make_map(&mbl, bl, Kp, g.N, bb)) return PFB_E_UNSUPPORTED;
+    if (!make_map(&f->bh, bh, Kp, g.N, bb) || !make_map(&f->bl, bl, Kp, g.N, bb)) return PFB_E_UNSUPPORTED;
   } else {
-    if (!make_raw_map(&mbh, bm, g.B, g.N, g.K, bb, g.sbb, g.sbn, g.sbk)) return PFB_E_UNSUPPORTED;
-    mbl = mbh;
+    if (!make_raw_map(&f->bh, f->bm, g.B, g.N, g.K, bb, g.sbb, g.sbn, g.sbk)) return PFB_E_UNSUPPORTED;
+    f->bl = f->bh;
   }
+  return 0;
+}
+
+// g carries the output, epilogue and (for the split model) the total K;
+// f2 == nullptr: one operand pair
+static int launch_gemm(const GemmArgs& g, const PairFeed& f1, const PairFeed* f2, cudaStream_t s,
+                       int ksplit_want) {
   static bool attr = false;
   if (!attr) {
     cudaFuncSetAttribute(gemm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES);
     attr = true;
   }
+  const int nk1 = (int)((f1.Kp + BK - 1) / BK);
+  const int nk = nk1 + (f2 ? (int)((f2->Kp + BK - 1) / BK) : 0);
+  GemmArgs gm = g;
+  gm.K = (int64_t)nk * BK;
   int ksplit, kb_per;
-  choose_split(g, &ksplit, &kb_per);
+  choose_split(gm, &ksplit, &kb_per);
   if (const char* e = getenv("PFB_TC_KSPLIT")) ksplit_want = atoi(e);  // bring-up override
   if (ksplit_want > 0) {  // autotuner candidate / override: this many k-splits
-    const int nk = (int)((Kp + BK - 1) / BK);
     const int want = std::max(1, std::min(ksplit_want, kMaxCluster));
     kb_per = (nk + want - 1) / want;
     ksplit = (nk + kb_per - 1) / kb_per;
   }
   // TMA-store epilogue: C row-major with 16-byte aligned rows, overwrite
-  CUtensorMap mc = mah;
+  CUtensorMap mc = f1.ah;
   int tma_store = 0;
   if (ksplit == 1 && !g.accumulate && g.scn == 1 && (g.N == 1 || (g.scm * 4) % 16 == 0) &&
       (g.batch == 1 || (g.scb * 4) % 16 == 0) &&
@@ -726,11 +772,15 @@ int gemm_tcgen05(const GemmArgs& g, void* ws, int64_t ws_bytes, cudaStream_t s, 
     cuuint32_t box[3] = {32, 32, 1};
     tma_store = encode(&mc, g.C, dims, strides, box) ? 1 : 0;
   }
-  const uint32_t idesc = kIdesc | ((uint32_t)(am == kRawMN) << 15) | ((uint32_t)(bm == kRawMN) << 16);
-  Params p{(int)g.M, (int)g.N, (int)Kp, (int)g.batch,
-           (int)((g.M + BM - 1) / BM), (int)((g.N + BN - 1) / BN), a_bc, b_bc, am, bm, idesc,
-           g.C, g.scb, g.scm, g.scn, g.alpha_rows, g.accumulate, ksplit, kb_per,
-           g.bias, g.sxb, g.sxm, g.sxn, g.act, 4096u, 512u, tma_store, tc_trace_buffer()};
+  auto idesc_of = [](const PairFeed& f) {
+    return kIdesc | ((uint32_t)(f.am == kRawMN) << 15) | ((uint32_t)(f.bm == kRawMN) << 16);
+  };
+  const PairFeed& q = f2 ? *f2 : f1;
+  Params p{(int)g.M, (int)g.N, nk * BK, (int)g.batch,
+           (int)((g.M + BM - 1) / BM), (int)((g.N + BN - 1) / BN), f1.a_bc, f1.b_bc, f1.am, f1.bm,
+           idesc_of(f1), g.C, g.scb, g.scm, g.scn, g.alpha_rows, g.accumulate, ksplit, kb_per,
+           g.bias, g.sxb, g.sxm, g.sxn, g.act, 4096u, 512u, tma_store, tc_trace_buffer(),
+           nk1, q.am, q.bm, q.a_bc, q.b_bc, idesc_of(q)};
   const int64_t units = (int64_t)p.ntm * p.ntn * g.batch * ksplit;
   if (ksplit > 1) {
     // one CTA per (tile, k-split); the k-splits of a tile are one cluster
@@ -748,12 +798,51 @@ int gemm_tcgen05(const GemmArgs& g, void* ws, int64_t ws_bytes, cudaStream_t s, 
     at[1].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = at;
     cfg.numAttrs = pdl_enabled() ? 2 : 1;
-    cudaLaunchKernelEx(&cfg, gemm_kernel, mah, mal, mbh, mbl, mc, p);
+    cudaLaunchKernelEx(&cfg, gemm_kernel, f1.ah, f1.al, f1.bh, f1.bl, mc, q.ah, q.al, q.bh, q.bl, p);
   } else {
     const int grid = (int)std::min<int64_t>(units, num_sms());
-    launch(gemm_kernel, grid, NUM_THREADS, SMEM_BYTES, s, mah, mal, mbh, mbl, mc, p);
+    launch(gemm_kernel, grid, NUM_THREADS, SMEM_BYTES, s, f1.ah, f1.al, f1.bh, f1.bl, mc, q.ah,
+           q.al, q.bh, q.bl, p);
   }
   return launch_status();
+}
+
+}  // namespace tc
+
+int gemm_tcgen05(const GemmArgs& g, void* ws, int64_t ws_bytes, cudaStream_t s, int variant,
+                 int ksplit_want) {
+  using namespace tc;
+  if (!gemm_tcgen05_eligible(g)) return PFB_E_UNSUPPORTED;
+  if (variant == 0) variant = (2.0 * g.M * g.N * g.K * g.batch < 4e9) ? 2 : 1;
+  int am, bm;
+  const int64_t need = pair_need(g, variant, &am, &bm);
+  if (need > 0 && (ws == nullptr || ws_bytes < need)) return PFB_E_UNSUPPORTED;
+  char* w = static_cast<char*>(ws);
+  PairFeed f;
+  if (int e = prep_pair(g, variant, w, s, &f)) return e;
+  return launch_gemm(g, f, nullptr, s, ksplit_want);
+}
+
+int64_t gemm_tcgen05_dual_workspace(const GemmArgs& g1, const GemmArgs& g2) {
+  return gemm_tcgen05_workspace(g1) + gemm_tcgen05_workspace(g2);
+}
+
+// C = epi(A1 B1 + A2 B2): both pairs accumulate into one TMEM tile (the
+// K ranges are consecutive k-blocks of one launch); g1 carries C/epilogue.
+int gemm_tcgen05_dual(const GemmArgs& g1, const GemmArgs& g2, void* ws, int64_t ws_bytes,
+                      cudaStream_t s, int variant, int ksplit_want) {
+  using namespace tc;
+  if (!gemm_tcgen05_eligible(g1) || !gemm_tcgen05_eligible(g2)) return PFB_E_UNSUPPORTED;
+  if (g1.M != g2.M || g1.N != g2.N || g1.batch != g2.batch || g2.kscale) return PFB_E_UNSUPPORTED;
+  if (variant == 0) variant = (2.0 * g1.M * g1.N * (g1.K + g2.K) * g1.batch < 4e9) ? 2 : 1;
+  int a1, b1, a2, b2;
+  const int64_t need = pair_need(g1, variant, &a1, &b1) + pair_need(g2, variant, &a2, &b2);
+  if (need > 0 && (ws == nullptr || ws_bytes < need)) return PFB_E_UNSUPPORTED;
+  char* w = static_cast<char*>(ws);
+  PairFeed f1, f2;
+  if (int e = prep_pair(g1, variant, w, s, &f1)) return e;
+  if (int e = prep_pair(g2, variant, w, s, &f2)) return e;
+  return launch_gemm(g1, f1, &f2, s, ksplit_want);
 }
 
 }  // namespace pfb

@@ -1212,6 +1212,37 @@ def _h_matmul_ep(ex, node, ins):
     return [out]
 
 
+def _h_matmul2(ex, node, ins):
+    """matmul2 (passes.fuse_dual_matmuls): act(a1 @ b1 + a2 @ b2 + bias) in one
+    dual-operand GEMM (pfb_matmul_dual: both K ranges in one accumulation)."""
+    import ctypes
+    at = node.attrs
+    vals = [ex._dev(v) for v in ins]
+    a1, b1, a2, b2 = vals[:4]
+    bias = vals[4] if at.get("has_bias") else None
+    for x in vals:
+        if x.dtype != DType.F64:
+            raise E.DTypeMismatch("matmul2: only f64 (fp32 on device) is on the B200 path")
+    if a1.rank != 2 or b1.rank != 2 or a2.rank != 2 or b2.rank != 2:
+        raise E.RankError("matmul2: rank-2 operands expected")
+    if a1.shape[1] != b1.shape[0] or a2.shape[1] != b2.shape[0]:
+        raise E.IncompatibleShapes(f"matmul2: {a1.shape}x{b1.shape} + {a2.shape}x{b2.shape}")
+    shape = (a1.shape[0], b1.shape[1])
+    if (a2.shape[0], b2.shape[1]) != shape:
+        raise E.IncompatibleShapes(f"matmul2: {shape} vs {(a2.shape[0], b2.shape[1])}")
+    out = ex._empty(shape, a1.dtype)
+    flops = 2 * _numel(shape) * (a1.shape[1] + a2.shape[1])
+    d = [x.desc() for x in (a1, b1, a2, b2)]
+    od = out.desc()
+    xd = bias.desc() if bias is not None else None
+    need = ex._lib.pfb_matmul_dual_workspace(d[0], d[1], d[2], d[3], od)
+    wp, wn = ex._ws_get(need) if need > 0 else (None, 0)
+    ex._call(ex._lib.pfb_matmul_dual, d[0], d[1], d[2], d[3], od,
+             ctypes.byref(xd) if xd is not None else None, _ACT_CODE[at.get("act")], 0,
+             wp, wn, ex._stream, what="matmul", work=(_abytes(*vals, out), flops))
+    return [out]
+
+
 def _h_conv(ex, node, ins):
     x, f = (ex._dense(ex._dev(v)) for v in ins)
     k = node.kind
@@ -1597,6 +1628,7 @@ _HANDLERS.update({
     "matmul_ep": _h_matmul_ep,
     "row_dots": _h_row_dots,
     "fused_ewm": _h_fused_multi,
+    "matmul2": _h_matmul2,
     "gather_rows": _h_gather, "scatter_rows": _h_scatter_rows,
     "scatter_add_rows": _h_scatter_add, "reshape": _h_reshape, "transpose": _h_transpose,
     "slice_leading": _h_slice_leading, "tile_leading": _h_tile_leading,

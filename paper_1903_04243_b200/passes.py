@@ -33,6 +33,8 @@ rounding (tests/test_passes.py checks against the oracle).
 
 from __future__ import annotations
 
+import numpy as np
+
 from .builder import GraphBuilder
 from .graph import Ref
 
@@ -257,9 +259,11 @@ def fuse_matmul_epilogues(g, keep=()):
     rw.replaced = {}
     count = 0
     for node in list(g.topo_order()):
-        if node.id not in g.nodes or node.kind != "matmul":
+        if node.id not in g.nodes or node.kind not in ("matmul", "matmul2"):
             continue
         if node.out_dtypes[0] != DType.F64:
+            continue
+        if node.kind == "matmul2" and node.attrs.get("has_bias"):
             continue
         count += _f5(rw, node)
     return count, rw.replaced
@@ -278,8 +282,10 @@ def _f5(rw, node):
         return 0
     A, B = Ref(g, *node.inputs[0]), Ref(g, *node.inputs[1])
     kscale = None
+    dual = node.kind == "matmul2"
     bn = rw.node(node.inputs[1])
-    if bn.kind == "mul" and node.inputs[1][1] == 0 and rw.single_use(node.inputs[1]):
+    if (not dual and bn.kind == "mul" and node.inputs[1][1] == 0
+            and rw.single_use(node.inputs[1])):
         for j in (0, 1):
             s_key, b0_key = bn.inputs[1 - j], bn.inputs[j]
             ss, s0 = g.ref_shape(s_key), g.ref_shape(b0_key)
@@ -325,14 +331,127 @@ def _f5(rw, node):
         break
     if kscale is None and bias is None and act is None:
         return 0
-    ins = [A, B] + ([kscale] if kscale is not None else []) + ([bias] if bias is not None else [])
-    new = g.add_node("matmul_ep", [(r.nid, r.port) for r in ins],
-                     {"act": act, "has_kscale": kscale is not None, "has_bias": bias is not None})
+    if dual:
+        ins = [A, B, Ref(g, *node.inputs[2]), Ref(g, *node.inputs[3])] + (
+            [bias] if bias is not None else [])
+        new = g.add_node("matmul2", [(r.nid, r.port) for r in ins],
+                         {"act": act, "has_bias": bias is not None})
+    else:
+        ins = [A, B] + ([kscale] if kscale is not None else []) + (
+            [bias] if bias is not None else [])
+        new = g.add_node("matmul_ep", [(r.nid, r.port) for r in ins],
+                         {"act": act, "has_kscale": kscale is not None,
+                          "has_bias": bias is not None})
     out = Ref(g, new.id, 0)
     esh = g.ref_shape(end)
     if tuple(esh) != tuple(sm):
         out = b.reshape(out, list(esh))
     rw.redirect(end, out)
+    return 1
+
+
+# ----------------------------------------------------------------------------
+# F7: two GEMMs into one output -> one dual-operand GEMM launch
+
+def fuse_dual_matmuls(g, keep=()):
+    """F7 in place on `g` (a private copy).  Two patterns become one
+    `matmul2(a1, b1, a2, b2)` node (out = a1 @ b1 + a2 @ b2, one launch that
+    accumulates both K ranges):
+      * add(M1, M2) of two single-use rank-2 matmuls (through reshapes) with
+        the same output shape -- e.g. the RNN cell z = x_t Wx + h Wh (cfg5);
+      * matmul(reshape(concat([a1, a2], -1)), B) with a single-use concat:
+        B's rows split at K1 (zero-cost view gathers), no concat copy.
+    Returns (count, moved outputs)."""
+    rw = _Rewriter(g, keep)
+    rw.replaced = {}
+    count = 0
+    for node in list(g.topo_order()):
+        if node.id not in g.nodes:
+            continue
+        if node.kind == "add":
+            count += _f7_sum(rw, node)
+        elif node.kind == "matmul":
+            count += _f7_cat(rw, node)
+    return count, rw.replaced
+
+
+def _through_reshapes(rw, key):
+    """Follow single-use reshapes upward from `key`; the first non-reshape key."""
+    while True:
+        n = rw.node(key)
+        if n.kind != "reshape" or not rw.single_use(key):
+            return key
+        key = n.inputs[0]
+
+
+def _f7_sum(rw, node):
+    from .tensor import DType
+    g, b = rw.g, rw.b
+    osh = g.ref_shape((node.id, 0))
+    if osh is None or None in osh:
+        return 0
+    if any(g.ref_shape(i) is None or tuple(g.ref_shape(i)) != tuple(osh) for i in node.inputs):
+        return 0
+    mms = []
+    for i in node.inputs:
+        k = _through_reshapes(rw, i)
+        n = rw.node(k)
+        if n.kind != "matmul" or k[1] != 0 or not rw.single_use(k) or n.out_dtypes[0] != DType.F64:
+            return 0
+        sa, sb = g.ref_shape(n.inputs[0]), g.ref_shape(n.inputs[1])
+        if sa is None or sb is None or len(sa) != 2 or len(sb) != 2 or None in sa or None in sb:
+            return 0
+        if sa[1] == 0:
+            return 0
+        mms.append(n)
+    m1, m2 = mms
+    if tuple(g.ref_shape((m1.id, 0))) != tuple(g.ref_shape((m2.id, 0))):
+        return 0
+    new = g.add_node("matmul2", [m1.inputs[0], m1.inputs[1], m2.inputs[0], m2.inputs[1]],
+                     {"act": None, "has_bias": False})
+    out = Ref(g, new.id, 0)
+    if tuple(g.ref_shape((new.id, 0))) != tuple(osh):
+        out = b.reshape(out, list(osh))
+    rw.redirect((node.id, 0), out)
+    return 1
+
+
+def _f7_cat(rw, node):
+    from .tensor import DType
+    g, b = rw.g, rw.b
+    if node.out_dtypes[0] != DType.F64:
+        return 0
+    sa, sb = g.ref_shape(node.inputs[0]), g.ref_shape(node.inputs[1])
+    if sa is None or sb is None or len(sa) != 2 or len(sb) != 2 or None in sa or None in sb:
+        return 0
+    ck = _through_reshapes(rw, node.inputs[0])
+    cn = rw.node(ck)
+    if cn.kind != "concat" or len(cn.inputs) != 2 or not rw.single_use(ck):
+        return 0
+    csh = g.ref_shape(ck)
+    if csh is None or None in csh or not csh:
+        return 0
+    ax = cn.attrs["axis"]
+    if ax < 0:
+        ax += len(csh)
+    if ax != len(csh) - 1 or csh[-1] != sa[1]:
+        return 0
+    parts = []
+    for i in cn.inputs:
+        ps = g.ref_shape(i)
+        if ps is None or None in ps or ps[-1] == 0 or g.ref_dtype(i) != DType.F64:
+            return 0
+        parts.append((Ref(g, *i), ps[-1]))
+    k1 = parts[0][1]
+    rows = sa[0]
+    a1 = b.reshape(parts[0][0], [rows, k1])
+    a2 = b.reshape(parts[1][0], [rows, sa[1] - k1])
+    B = Ref(g, *node.inputs[1])
+    b1 = b.gather(B, b.const(np.arange(0, k1, dtype=np.int64)))
+    b2 = b.gather(B, b.const(np.arange(k1, sa[1], dtype=np.int64)))
+    new = g.add_node("matmul2", [(a1.nid, a1.port), (b1.nid, b1.port), (a2.nid, a2.port),
+                                 (b2.nid, b2.port)], {"act": None, "has_bias": False})
+    rw.redirect((node.id, 0), Ref(g, new.id, 0))
     return 1
 
 
@@ -423,6 +542,8 @@ def _optimize_in_place(g, keep, elementwise=True):
     keep = [moved4.get(k, k) for k in keep]
     _, moved6 = fuse_row_dots(g, keep)
     keep = [moved6.get(k, k) for k in keep]
+    _, moved7 = fuse_dual_matmuls(g, keep)
+    keep = [moved7.get(k, k) for k in keep]
     _, moved5 = fuse_matmul_epilogues(g, keep)
     keep = [moved5.get(k, k) for k in keep]
     moved3 = {}
@@ -452,6 +573,8 @@ def optimize(g, keep_keys, elementwise=True):
     keep = [moved4.get(k, k) for k in keep]
     _, moved6 = fuse_row_dots(dst, keep)
     keep = [moved6.get(k, k) for k in keep]
+    _, moved7 = fuse_dual_matmuls(dst, keep)
+    keep = [moved7.get(k, k) for k in keep]
     _, moved5 = fuse_matmul_epilogues(dst, keep)
     keep = [moved5.get(k, k) for k in keep]
     moved3 = {}
@@ -462,6 +585,7 @@ def optimize(g, keep_keys, elementwise=True):
         v = moved.get(v, v)
         v = moved4.get(v, v)
         v = moved6.get(v, v)
+        v = moved7.get(v, v)
         v = moved5.get(v, v)
         final[k] = moved3.get(v, v)
     return dst, final

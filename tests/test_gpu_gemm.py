@@ -261,3 +261,33 @@ def test_gemm_fused_batched_bias_kscale(env):
         got = _run_fused(env, a, b, force, bias=bias, act=1, kscale=s)
         np.testing.assert_allclose(got, np.tanh(a @ (s[:, :, None] * b) + bias), rtol=RTOL,
                                    atol=ATOL)
+
+
+@pytest.mark.parametrize("force", [0, 1, 2, 3])
+@pytest.mark.parametrize("shape", [(1024, 256, 256, 256), (200, 300, 100, 37), (256, 2048, 512, 512)])
+def test_matmul_dual(env, force, shape):
+    """pfb_matmul_dual: act(a1 b1 + a2 b2 + bias) -- one tcgen05 accumulation
+    over both K ranges (force 2 raw, 3 pre-split), two launches (1), auto (0)."""
+    import ctypes
+    torch, lib, DArray, DType = env
+    dev = torch.device("cuda")
+    m, n, k1, k2 = shape
+    r = np.random.default_rng(m + k2)
+    a1, b1 = _operands(r, (m, k1), (k1, n))
+    a2, b2 = _operands(r, (m, k2), (k2, n))
+    bias = _f32(r, (n,))
+    want = np.tanh(a1 @ b1 + a2 @ b2 + bias)
+    A1, A2 = DArray.from_numpy(a1, DType.F64, dev), DArray.from_numpy(a2, DType.F64, dev)
+    B1 = _tview(DArray, DType, dev, b1)  # K-major view
+    B2 = DArray.from_numpy(b2, DType.F64, dev)  # MN-major
+    X = DArray.from_numpy(bias, DType.F64, dev)
+    C = DArray.empty((m, n), DType.F64, dev)
+    d = [v.desc() for v in (A1, B1, A2, B2, C)]
+    xd = X.desc()
+    need = lib.pfb_matmul_dual_workspace(*d)
+    ws = torch.empty(max(need, 256), dtype=torch.uint8, device=dev)
+    rc = lib.pfb_matmul_dual(d[0], d[1], d[2], d[3], d[4], ctypes.byref(xd), 1, force,
+                             ws.data_ptr(), ws.numel(), torch.cuda.current_stream().cuda_stream)
+    assert rc == 0, rc
+    torch.cuda.synchronize()
+    np.testing.assert_allclose(C.to_numpy().astype(np.float64), want, rtol=RTOL, atol=ATOL)

@@ -100,3 +100,36 @@ def test_f5_respects_multi_use_preactivation():
         np.testing.assert_allclose(a_.data, b_.data, rtol=1e-12)
     eps = [n for n in g2.nodes.values() if n.kind == "matmul_ep"]
     assert len(eps) == 1 and eps[0].attrs["act"] is None and eps[0].attrs["has_bias"]
+
+
+def test_f7_dual_matmul_sum_and_concat():
+    """F7: z = x Wx + h Wh (cfg5's cell, inside the while body) becomes one
+    matmul2; matmul(concat([a1, a2], -1), W) becomes matmul2 over row-split W
+    views -- values unchanged (oracle)."""
+    from paper_1903_04243_b200 import GraphBuilder
+    from oracle import OracleExecutor as OE
+    w = WL.cfg5(WL.this_api(), n=6, max_len=5, units=8, masked=True)
+    _, g2, _ = _run_both(w)
+
+    def count(gr):
+        c = 0
+        for n in gr.nodes.values():
+            c += n.kind == "matmul2"
+            if n.block is not None:
+                c += sum(count(sg) for sg in n.block.subgraphs.values())
+        return c
+    assert count(g2) >= 1
+    r = np.random.default_rng(1)
+    b = GraphBuilder()
+    a1, a2 = b.const(r.standard_normal((5, 3))), b.const(r.standard_normal((5, 4)))
+    W, bias = b.const(r.standard_normal((7, 6))), b.const(r.standard_normal((6,)))
+    b.graph.set_outputs([b.tanh(b.add(b.matmul(b.concat([a1, a2], 1), W), bias))])
+    keys = [tuple(o) for o in b.graph.outputs]
+    g3, mp = optimize(b.graph, keys)
+    live = _kinds(g3, [mp[k] for k in keys])
+    m2 = [n for n in live if n.kind == "matmul2"]
+    assert len(m2) == 1 and m2[0].attrs["act"] == "tanh" and m2[0].attrs["has_bias"]
+    assert not [n for n in live if n.kind == "concat"]
+    want = OE(b.graph).run()
+    got = OE(g3).run(outputs=[g3.out(*mp[k]) for k in keys])
+    np.testing.assert_allclose(got[0].data, want[0].data, rtol=1e-12)
