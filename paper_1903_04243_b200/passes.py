@@ -351,6 +351,92 @@ def _f5(rw, node):
 
 
 # ----------------------------------------------------------------------------
+# F8: loop-invariant code motion out of while bodies
+
+_NO_LICM = frozenset({"read_variable", "assign", "assign_add", "random_uniform", "placeholder",
+                      "loop_var", "carried", "capture", "constant"})
+
+
+def hoist_loop_invariants(g):
+    """F8 in place on `g` (a private copy), nested blocks first: every pure
+    node of a `while` body whose inputs are all captures, constants or other
+    such nodes is evaluated once in the enclosing graph and reaches the body
+    as a new capture (the reference re-evaluates it every trip, e.g. the
+    row-index iota of the per-example gathers in cfg5's body).  Values are
+    unchanged.  Returns the number of nodes moved."""
+    moved_total = 0
+    for node in list(g.topo_order()):
+        if node.block is None:
+            continue
+        for sg in node.block.subgraphs.values():
+            moved_total += hoist_loop_invariants(sg)
+        if node.block.kind != "while":
+            continue
+        moved_total += _licm_while(g, node)
+    return moved_total
+
+
+def _licm_while(g, wnode):
+    body = wnode.block.subgraphs["body"]
+    nc = wnode.block.num_carried
+    inv = set()
+    movable = []
+    for n in body.topo_order():
+        if n.kind in ("capture", "constant"):
+            inv.add(n.id)
+        elif (n.kind not in _NO_LICM and n.block is None and n.inputs and not n.control_deps
+              and all(src in inv for src, _ in n.inputs)):
+            inv.add(n.id)
+            movable.append(n)
+    if not movable:
+        return 0
+    users = {}
+    for n in body.nodes.values():
+        for src in n.inputs:
+            users.setdefault(tuple(src), []).append(n)
+    outs = {tuple(o) for o in body.outputs}
+    pmap = {}  # body (nid, port) -> parent (nid, port)
+
+    def parent_ref(src):
+        sn = body.nodes[src[0]]
+        if sn.kind == "capture":
+            return tuple(wnode.inputs[nc + sn.attrs["index"]])
+        if sn.kind == "constant":
+            if src not in pmap:
+                c = g.add_node("constant", [], dict(sn.attrs))
+                pmap[src] = (c.id, 0)
+            return pmap[src]
+        return pmap[src]
+
+    moved_ids = {n.id for n in movable}
+    for n in movable:
+        pn = g.add_node(n.kind, [parent_ref(tuple(s_)) for s_ in n.inputs], dict(n.attrs))
+        for p in range(n.output_arity):
+            pmap[(n.id, p)] = (pn.id, p)
+    count = 0
+    for n in movable:
+        for p in range(n.output_arity):
+            key = (n.id, p)
+            ext = [u for u in users.get(key, []) if u.id not in moved_ids]
+            if not ext and key not in outs:
+                continue
+            idx = len(wnode.inputs) - nc
+            pref = pmap[key]
+            pnode = g.nodes[pref[0]]
+            cap = body.add_node("capture", [], {"index": idx, "dtype": pnode.out_dtypes[p],
+                                                "shape": pnode.out_shapes[p]})
+            wnode.inputs.append(pref)
+            for u in ext:
+                u.inputs = [(cap.id, 0) if tuple(s_) == key else s_ for s_ in u.inputs]
+            if key in outs:
+                body.outputs = [(cap.id, 0) if tuple(o) == key else o for o in body.outputs]
+            count += 1
+    body._topo_cache = None
+    g._topo_cache = None
+    return len(movable)
+
+
+# ----------------------------------------------------------------------------
 # F7: two GEMMs into one output -> one dual-operand GEMM launch
 
 def fuse_dual_matmuls(g, keep=()):
@@ -565,6 +651,7 @@ def _optimize_blocks(g, elementwise=True):
 def optimize(g, keep_keys, elementwise=True):
     """Copy `g`, apply the rewrites, return (graph, key map old->new)."""
     dst, mapping = copy_with_map(g)
+    hoist_loop_invariants(dst)
     _optimize_blocks(dst, elementwise)
     keep = [mapping[k] for k in keep_keys]
     _, moved = fuse_outer_products(dst, keep)

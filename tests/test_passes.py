@@ -133,3 +133,22 @@ def test_f7_dual_matmul_sum_and_concat():
     want = OE(b.graph).run()
     got = OE(g3).run(outputs=[g3.out(*mp[k]) for k in keys])
     np.testing.assert_allclose(got[0].data, want[0].data, rtol=1e-12)
+
+
+@pytest.mark.parametrize("kw", [dict(masked=True, unroll=4), dict(masked=True, unroll=1), dict()])
+def test_f8_loop_invariants_leave_the_while_body(kw):
+    """F8: the per-trip row-index iota (range_vec of a captured size) and its
+    products move out of cfg5's while body as new captures -- values unchanged."""
+    w = WL.cfg5(WL.this_api(), n=6, max_len=5, units=8, **kw)
+    g, g2, _ = _run_both(w)
+
+    def body_kinds(gr):
+        (wn,) = [n for n in gr.nodes.values() if n.kind == "while"]
+        body = wn.block.subgraphs["body"]
+        return wn, [n.kind for n in body.nodes.values()
+                    if n.id in __import__("paper_1903_04243_b200.passes", fromlist=["x"]).live_set(
+                        body, [tuple(o) for o in body.outputs])]
+    w0, k0 = body_kinds(g)
+    w1, k1 = body_kinds(g2)
+    assert "range_vec" not in k1
+    assert len(w1.inputs) > len(w0.inputs)  # hoisted values arrive as captures
