@@ -754,6 +754,93 @@ __global__ void __launch_bounds__(256) concat_kernel(CatDesc d, T* out) {
     out[oo] = __ldg(x + xo);
   }
 }
+// Concat of many width-1 inputs along a contiguous innermost axis (cfg4's F2
+// operands: 64 [n,1024,1] columns -> [n,1024,64]).  The generic kernel walks
+// each input and writes one float per 256-byte output row; here a 32x32 tile
+// is transposed through shared memory: every input column is read as 128
+// contiguous bytes and every output row segment written as 128 bytes.
+constexpr int kThinCat = 128;
+struct ThinCat {
+  int n;
+  int64_t R, ost_row, off;
+  const void* x[kThinCat];
+  int64_t rs[kThinCat];  // row stride of each input (collapsed leading dims)
+};
+
+template <typename T>
+__global__ void __launch_bounds__(256) concat_thin_kernel(ThinCat d, T* out) {
+  pdl_enter();
+  __shared__ T tile[32][33];
+  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
+  const int64_t r0 = (int64_t)blockIdx.x * 32;
+  const int c0 = blockIdx.y * 32;
+#pragma unroll
+  for (int i = ty; i < 32; i += 8) {
+    const int c = c0 + i;
+    const int64_t r = r0 + tx;
+    if (c < d.n && r < d.R) tile[i][tx] = __ldg(reinterpret_cast<const T*>(d.x[c]) + r * d.rs[c]);
+  }
+  __syncthreads();
+#pragma unroll
+  for (int i = ty; i < 32; i += 8) {
+    const int64_t r = r0 + i;
+    const int c = c0 + tx;
+    if (c < d.n && r < d.R) out[r * d.ost_row + d.off + c] = tile[tx][i];
+  }
+}
+
+// leading dims [0, rank-1) of a view collapsed into one stride, or -1
+static int64_t collapse_rows(const pfb_tensor* t, int rank) {
+  int64_t st = -1, expect = -1;
+  for (int i = rank - 2; i >= 0; --i) {
+    if (t->shape[i] == 1) continue;
+    if (st < 0) { st = t->stride[i]; expect = st * t->shape[i]; continue; }
+    if (t->stride[i] != expect) return -1;
+    expect *= t->shape[i];
+  }
+  return st < 0 ? 0 : st;
+}
+
+static bool concat_thin(int32_t n, const pfb_tensor* xs, int32_t axis, pfb_tensor* out,
+                        cudaStream_t s) {
+  const int rank = out->rank;
+  if (axis != rank - 1 || rank < 2 || out->stride[axis] != 1 || n < 8) return false;
+  ThinCat d;
+  d.R = 1;
+  for (int i = 0; i < rank - 1; ++i) d.R *= out->shape[i];
+  d.ost_row = collapse_rows(out, rank);
+  if (d.ost_row < 0 || d.R == 0) return false;
+  for (int base = 0; base < n; base += kThinCat) {
+    d.n = std::min(kThinCat, n - base);
+    d.off = base;
+    for (int j = 0; j < d.n; ++j) {
+      const pfb_tensor* x = &xs[base + j];
+      if (x->rank != rank || x->shape[axis] != 1 || x->dtype != out->dtype) return false;
+      for (int i = 0; i < rank - 1; ++i)
+        if (x->shape[i] != out->shape[i]) return false;
+      const int64_t rs = collapse_rows(x, rank);
+      if (rs < 0) return false;
+      d.x[j] = x->data;
+      d.rs[j] = rs;
+    }
+  }
+  if (out->shape[axis] != n) return false;
+  for (int base = 0; base < n; base += kThinCat) {
+    d.n = std::min(kThinCat, n - base);
+    d.off = base;
+    for (int j = 0; j < d.n; ++j) {
+      d.x[j] = xs[base + j].data;
+      d.rs[j] = collapse_rows(&xs[base + j], rank);
+    }
+    dim3 grid((unsigned)((d.R + 31) / 32), (unsigned)((d.n + 31) / 32));
+    switch (out->dtype) {
+      case PFB_F32: launch(concat_thin_kernel<float>, grid, 256, 0, s, d, (float*)out->data); break;
+      case PFB_I64: launch(concat_thin_kernel<int64_t>, grid, 256, 0, s, d, (int64_t*)out->data); break;
+      default: launch(concat_thin_kernel<uint8_t>, grid, 256, 0, s, d, (uint8_t*)out->data); break;
+    }
+  }
+  return true;
+}
 }  // namespace pfb
 
 extern "C" int pfb_concat(int32_t n, const pfb_tensor* xs, int32_t axis, pfb_tensor* out,
@@ -763,6 +850,7 @@ extern "C" int pfb_concat(int32_t n, const pfb_tensor* xs, int32_t axis, pfb_ten
   const int rank = out->rank;
   if (axis < 0 || axis >= rank) return PFB_E_ARG;
   cudaStream_t s = as_stream(stream);
+  if (concat_thin(n, xs, axis, out, s)) return launch_status();
   int64_t off = 0;
   for (int base = 0; base < n; base += kMaxCat) {
     CatDesc d;

@@ -329,3 +329,18 @@ def test_replayed_graph_errors_raise_once(Executor):
         ex.run(bad)
     assert isinstance(e.value.cause, errors.IndexOutOfBounds)
     np.testing.assert_allclose(ex.run(good)[0].data, np.arange(12.0).reshape(4, 3)[[0, 3, 1]])
+
+
+@pytest.mark.parametrize("n_in", [8, 70, 200])
+def test_concat_many_thin_inputs(n_in, Executor):
+    """concat of many width-1 columns along the last axis (cfg4's F2 operand
+    path: tiled transpose kernel), inputs as transposed views."""
+    from paper_1903_04243_b200 import GraphBuilder
+    r = np.random.default_rng(n_in)
+    cols = [r.standard_normal((3, 1, 37)) for _ in range(n_in)]
+    b = GraphBuilder()
+    parts = [b.transpose(b.const(c), [0, 2, 1]) for c in cols]  # [3, 37, 1] views
+    b.graph.set_outputs([b.concat(parts, 2)])
+    got = Executor(b.graph, cuda_graph=False).run()[0].data
+    want = np.concatenate([np.transpose(c, (0, 2, 1)) for c in cols], axis=2)
+    np.testing.assert_allclose(np.asarray(got, np.float64), want, rtol=1e-6, atol=1e-7)
