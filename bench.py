@@ -232,10 +232,18 @@ def main():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
-    torch.cuda.set_device(local)
-    dev = torch.device("cuda", local)
+    # PFB_BENCH_BACKEND=gloo: smoke-test the multi-rank code path with several
+    # ranks sharing the visible GPU(s) (NCCL refuses two ranks on one device)
+    backend = os.environ.get("PFB_BENCH_BACKEND", "nccl")
+    ndev = torch.cuda.device_count()
+    local_dev = local if backend == "nccl" else local % max(ndev, 1)
+    torch.cuda.set_device(local_dev)
+    dev = torch.device("cuda", local_dev)
     if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=dev)
+        else:
+            dist.init_process_group(backend)
 
     from paper_1903_04243_b200 import workloads as WL
     from paper_1903_04243_b200.executor import Executor
@@ -268,7 +276,7 @@ def main():
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize(dev)
-    with ClockSampler(local) as clocks:
+    with ClockSampler(local_dev) as clocks:
         for _ in range(args.steps):
             flush.zero_()
             s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)

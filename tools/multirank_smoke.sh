@@ -1,0 +1,8 @@
+# multi-rank code path of bench.py on one GPU (gloo; ranks share the device)
+export PFB_BENCH_BACKEND=gloo
+for c in cfg2_mlp cfg3; do
+  timeout 600 python -m torch.distributed.run --nnodes=1 --nproc-per-node 2 --master-addr 127.0.0.1 --master-port 29512 \
+    bench.py --gpus 2 --steps 3 --warmup 3 --config $c --no-cpu-baseline 2>&1 | grep -E '^\{|Error|error' | cut -c1-400
+done
+timeout 600 python -m torch.distributed.run --nnodes=1 --nproc-per-node 2 --master-addr 127.0.0.1 --master-port 29513 \
+  bench.py --impl reference --gpus 2 --steps 1 --warmup 1 2>&1 | grep -E '^\{|Error' | cut -c1-300
