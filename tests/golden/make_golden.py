@@ -13,7 +13,12 @@ It imports the reference `pforvec` package read-only from
                    and the reference's worked examples, executed by the
                    reference Executor;
 * structure.json -- the op-kind sequence of each reference vectorized graph
-                   (the drop-in frontend must emit the same kernels).
+                   (the drop-in frontend must emit the same kernels);
+* pfg/*.pfg      -- the reference's `.pfg` text (its own serializer) of each
+                   worked example's source graph (`src_*`) and vectorized
+                   graph (`vec_*`), and of small BASELINE programs (`prog_*`):
+                   the interchange-format fixtures (`--pfg-only` rewrites
+                   just these).
 
 The GPU box has no /root/reference: tests there read only these files.
 """
@@ -214,5 +219,27 @@ def main():
           f"programs: {len(PROGRAM_CASES)} + worked examples")
 
 
+def write_pfg():
+    ser = sys.modules["pforvec.serialize"] if "pforvec.serialize" in sys.modules else None
+    if ser is None:
+        import pforvec.serialize as ser  # noqa: F811
+    out = HERE / "pfg"
+    out.mkdir(exist_ok=True)
+    for name, fn in list(W.GOLDEN_EXAMPLES.items()) + [("cond_example", W.cond_example),
+                                                       ("while_example", W.while_example)]:
+        g = fn()
+        (out / f"src_{name}.pfg").write_text(ser.dumps(g))
+        g2, _ = pforvec.vectorize_graph(g)
+        (out / f"vec_{name}.pfg").write_text(ser.dumps(g2))
+    ref_api = WL.reference_api(pforvec)
+    for name in ("cfg1_full", "cfg2_mlp", "cfg5"):
+        cfg, kw = PROGRAM_CASES[name]
+        w = WL.BUILDERS[cfg](ref_api, **kw)
+        (out / f"prog_{name}.pfg").write_text(ser.dumps(w.graph))
+    print(f"pfg fixtures: {len(list(out.glob('*.pfg')))}")
+
+
 if __name__ == "__main__":
-    main()
+    if "--pfg-only" not in sys.argv:
+        main()
+    write_pfg()

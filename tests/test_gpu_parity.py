@@ -344,3 +344,30 @@ def test_concat_many_thin_inputs(n_in, Executor):
     got = Executor(b.graph, cuda_graph=False).run()[0].data
     want = np.concatenate([np.transpose(c, (0, 2, 1)) for c in cols], axis=2)
     np.testing.assert_allclose(np.asarray(got, np.float64), want, rtol=1e-6, atol=1e-7)
+
+
+_PFG = pathlib.Path(__file__).parent / "golden" / "pfg"
+
+
+@pytest.mark.parametrize("name", sorted(p.name for p in _PFG.glob("vec_*.pfg")))
+def test_reference_pfg_graph_on_device(name, golden, Executor):
+    """The reference's own vectorized graphs (its `.pfg` text, loaded by
+    paper_1903_04243_b200.pfg) execute on the B200 to the reference outputs."""
+    from paper_1903_04243_b200 import pfg
+    P = golden["programs"]
+    got = Executor(pfg.load(_PFG / name)).run()
+    case = "we_" + name[4:-4]
+    for j, o in enumerate(got):
+        check(o, P[f"{case}/out/{j}"])
+
+
+@pytest.mark.parametrize("fname,case", [("prog_cfg1_full.pfg", "cfg1_full"),
+                                        ("prog_cfg2_mlp.pfg", "cfg2_mlp"),
+                                        ("prog_cfg5.pfg", "cfg5")])
+def test_reference_pfg_program_on_device(fname, case, golden, Executor):
+    from paper_1903_04243_b200 import pfg
+    P = golden["programs"]
+    feeds = {k.split("/")[-1]: P[k] for k in P if k.startswith(f"{case}/feed/")}
+    got = Executor(pfg.load(_PFG / fname)).run(feeds=feeds)
+    for j, o in enumerate(got):
+        check(o, P[f"{case}/out/{j}"])
