@@ -225,11 +225,16 @@ class Executor:
     """Runs a graph on one CUDA device; one stream, values resident in HBM."""
 
     def __init__(self, graph, store=None, rng=None, budget=None, device=None, check_errors=True,
-                 cuda_graph="auto", optimize=True):
+                 cuda_graph="auto", optimize=True, hoist_constants=True):
         """`cuda_graph`: "auto" captures pure, block-free graphs (no cond/while,
         no stateful ops, no data-dependent sizes) into one CUDA graph on the
         second run with a given feed signature and replays it afterwards --
-        one launch per step instead of one per node.  False = always eager."""
+        one launch per step instead of one per node.  False = always eager.
+        `hoist_constants`: nodes computed only from constants are evaluated
+        once and reused across runs (False re-evaluates them every run, as
+        the reference executor does -- used by the bench harness, whose
+        models are built from constants)."""
+        self.hoist_constants = hoist_constants
         self._lib = N.lib()
         from .interop import import_graph, is_native
         self._foreign = None
@@ -859,7 +864,8 @@ class Executor:
             remaining[r] = remaining.get(r, 0) + 1
         env = {}
         for node in plan.order:
-            hoist = node.id in plan.const_nodes and node.kind != "constant"
+            hoist = (self.hoist_constants and node.id in plan.const_nodes
+                     and node.kind != "constant")
             outs = self._hoisted.get((id(g), node.id)) if hoist else None
             if outs is None:
                 try:
