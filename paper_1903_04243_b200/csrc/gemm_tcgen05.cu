@@ -42,7 +42,10 @@ namespace pfb {
 namespace tc {
 
 constexpr int BM = 128, BN = 128, BK = 32, STAGES = 3, UMMA_K = 8;
-constexpr int CHUNK_KB = 2;                       // k-blocks accumulated in TMEM per chunk
+#ifndef PFB_CHUNK_KB
+#define PFB_CHUNK_KB 2
+#endif
+constexpr int CHUNK_KB = PFB_CHUNK_KB;            // k-blocks accumulated in TMEM per chunk
 constexpr int TILE_BYTES = BM * BK * 4;           // 16 KB per operand tile
 constexpr int STAGE_BYTES = 4 * TILE_BYTES;       // A_hi, A_lo, B_hi, B_lo
 constexpr int EPI_WARPS = 8;                      // 2 per TMEM lane quarter, 64 columns each
