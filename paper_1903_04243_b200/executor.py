@@ -419,6 +419,8 @@ class Executor:
             cap.host_pack = self._pack_plan(outs, cap)
             cap.launches = self.launch_count - l0
             cap.dispatches = self.dispatch_count - d0
+            # recording is not an execution: the replay that follows counts it
+            self.launch_count, self.dispatch_count = l0, d0
             self._captures[sig] = cap
         except Exception as e:  # anything the capture cannot take: stay eager for this graph
             self.capture_failures.append(f"graph: {type(e).__name__}: {e}")

@@ -850,7 +850,9 @@ def fuse_elementwise(g, keep=()):
             for src in n.inputs:
                 if src[0] not in group and src not in externals and _const_scalar_f(g, src) is None:
                     externals.append(src)
-        if len(externals) > MAX_INPUTS:
+        if len(externals) > MAX_INPUTS or not externals:
+            # (no tensor input: a constant-only group -- left to the
+            # executor's constant hoisting; the kernel needs >= 1 operand)
             return None
         extra = [n.id for n in order if n.id != root.id and _is_out(n.id, group)]
         try:

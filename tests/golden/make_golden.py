@@ -18,7 +18,11 @@ It imports the reference `pforvec` package read-only from
                    worked example's source graph (`src_*`) and vectorized
                    graph (`vec_*`), and of small BASELINE programs (`prog_*`):
                    the interchange-format fixtures (`--pfg-only` rewrites
-                   just these).
+                   just these);
+* corpus.json.gz -- the reference's randomized differential-testing corpus
+                   (randgen.generate_case, seeds 42..141 x n in {0,1,3,7}):
+                   source + vectorized `.pfg`, reference outputs and variable
+                   values (`--corpus-only`).
 
 The GPU box has no /root/reference: tests there read only these files.
 """
@@ -219,6 +223,40 @@ def main():
           f"programs: {len(PROGRAM_CASES)} + worked examples")
 
 
+def write_corpus(seeds=range(42, 142), ns=(0, 1, 3, 7)):
+    """Differential-testing corpus (reference randgen.py / test_acceptance.py
+    criterion 1): random parfor bodies from the reference's own generator; per
+    case the source graph and the reference's vectorized graph as `.pfg`
+    text, the reference Executor's outputs / final variable values on the
+    source graph (RngState(seed)), and which of them depend on random draws
+    (compared by shape/dtype only, as the reference does)."""
+    import gzip
+    rg = sys.modules.get("pforvec.randgen") or __import__("pforvec.randgen", fromlist=["x"])
+    ser = sys.modules.get("pforvec.serialize") or __import__("pforvec.serialize", fromlist=["x"])
+    cases = {}
+    for seed in seeds:
+        for n in ns:
+            case = rg.generate_case(seed, max_depth=8, n=n)
+            g = case.graph
+            ex = interp.Executor(g, store=interp.VariableStore(g.variables),
+                                 rng=interp.RngState(seed))
+            try:
+                outs = ex.run()
+            except pforvec.PforVecError as e:  # noqa: F841  (not in the corpus)
+                continue
+            g2, _ = pforvec.vectorize_graph(g, policy=pforvec.Policy(stateful_assign_fallback=True))
+            enc = lambda v: {"dtype": v.dtype.value, "shape": list(v.shape),  # noqa: E731
+                             "data": np.asarray(v.data, np.float64).reshape(-1).tolist()}
+            cases[f"{seed}_{n}"] = {
+                "seed": seed, "n": n, "src": ser.dumps(g), "vec": ser.dumps(g2),
+                "outs": [enc(o) for o in outs], "tainted": list(map(bool, case.tainted)),
+                "vars": {k: enc(v) for k, v in ex.store.values.items()},
+                "var_tainted": {k: bool(t) for k, t in case.var_tainted.items()}}
+    with gzip.open(HERE / "corpus.json.gz", "wt") as fh:
+        json.dump(cases, fh)
+    print(f"corpus: {len(cases)} cases")
+
+
 def write_pfg():
     ser = sys.modules["pforvec.serialize"] if "pforvec.serialize" in sys.modules else None
     if ser is None:
@@ -240,6 +278,8 @@ def write_pfg():
 
 
 if __name__ == "__main__":
-    if "--pfg-only" not in sys.argv:
+    if "--pfg-only" not in sys.argv and "--corpus-only" not in sys.argv:
         main()
-    write_pfg()
+    if "--corpus-only" not in sys.argv:
+        write_pfg()
+    write_corpus()

@@ -371,3 +371,47 @@ def test_reference_pfg_program_on_device(fname, case, golden, Executor):
     got = Executor(pfg.load(_PFG / fname)).run(feeds=feeds)
     for j, o in enumerate(got):
         check(o, P[f"{case}/out/{j}"])
+
+
+def test_reference_random_corpus_on_device(Executor):
+    """The reference's 400-case randomized corpus (randgen.py, criterion 1 of
+    its acceptance tests), its own vectorized graphs loaded from `.pfg`,
+    executed on the B200 (variables, random draws, nested cond/while):
+    outputs and final variables against the reference's (random-draw
+    dependent ones by shape/dtype, as the reference compares them)."""
+    import gzip
+    import json
+    from paper_1903_04243_b200 import pfg
+    from paper_1903_04243_b200.executor import RngState, VariableStore
+    corpus = json.load(gzip.open(GOLD / "corpus.json.gz", "rt"))
+
+    def cmp(got, want, tainted):
+        if tuple(got.shape) != tuple(want["shape"]) or got.dtype.value != want["dtype"]:
+            return f"{got.dtype.value}{list(got.shape)} vs {want['dtype']}{want['shape']}"
+        if tainted or not got.data.size:
+            return None
+        g = np.asarray(got.data, np.float64)
+        w = np.asarray(want["data"], np.float64).reshape(want["shape"])
+        if want["dtype"] == "f64":
+            ok = np.allclose(g, w, rtol=RTOL, atol=ATOL, equal_nan=True)
+        else:
+            ok = np.array_equal(g, w)
+        return None if ok else f"max abs delta {np.max(np.abs(g - w)):.3e}"
+    bad = []
+    for key, c in corpus.items():
+        g = pfg.loads(c["vec"])
+        ex = Executor(g, store=VariableStore(g.variables), rng=RngState(c["seed"]))
+        try:
+            outs = ex.run()
+        except Exception as e:  # noqa: BLE001
+            bad.append(f"{key}: {type(e).__name__}: {e}")
+            continue
+        for j, (o, w) in enumerate(zip(outs, c["outs"])):
+            msg = cmp(o, w, c["tainted"][j])
+            if msg:
+                bad.append(f"{key} out {j}: {msg}")
+        for name, w in c["vars"].items():
+            msg = cmp(ex.store.values[name], w, c["var_tainted"].get(name, False))
+            if msg:
+                bad.append(f"{key} var {name}: {msg}")
+    assert not bad, f"{len(bad)} mismatches: {bad[:8]}"

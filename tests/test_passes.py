@@ -153,3 +153,34 @@ def test_f8_loop_invariants_leave_the_while_body(kw):
     assert "range_vec" not in k1
     if kw:  # masked conversion: the hoisted values arrive as new captures
         assert len(w1.inputs) > len(w0.inputs)
+
+
+def test_f3_leaves_constant_only_groups_alone():
+    """A chain whose only inputs are scalar constants (reference randgen
+    corpus case 123) is not turned into an input-less fused kernel."""
+    import gzip
+    import json
+    import pathlib
+    from paper_1903_04243_b200 import pfg
+    from oracle import OracleExecutor as OE
+    c = json.load(gzip.open(pathlib.Path(__file__).parent / "golden" / "corpus.json.gz",
+                            "rt"))["123_1"]
+    g = pfg.loads(c["vec"])
+    keys = [tuple(o) for o in g.outputs]
+    g2, mp = optimize(g, keys)
+
+    def walk(gr):
+        for n in gr.nodes.values():
+            if n.kind in ("fused_ew", "fused_ewm"):
+                assert n.inputs, n
+            if n.block is not None:
+                for sg in n.block.subgraphs.values():
+                    walk(sg)
+    walk(g2)
+    from oracle import RngState, VariableStore
+    want = OE(g, store=VariableStore(g.variables), rng=RngState(123)).run()
+    got = OE(g2, store=VariableStore(g2.variables), rng=RngState(123)).run(
+        outputs=[g2.out(*mp[k]) for k in keys])
+    for a, b in zip(got, want):
+        if a.data.size and not c["tainted"][0]:
+            np.testing.assert_allclose(a.data, b.data, rtol=1e-12)
