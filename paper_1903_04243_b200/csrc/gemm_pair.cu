@@ -132,8 +132,8 @@ __device__ __forceinline__ void epi4(const PParams& p, int bz, int row, int col,
   v = make_float4(e[0], e[1], e[2], e[3]);
 }
 
-template <int BN>
-__global__ void __maxnreg__(192)
+template <int BN, bool SINGLE>
+__global__ void __maxnreg__(168)
 pair_kernel(const __grid_constant__ CUtensorMap map_ah, const __grid_constant__ CUtensorMap map_al,
             const __grid_constant__ CUtensorMap map_bh, const __grid_constant__ CUtensorMap map_bl,
             const __grid_constant__ CUtensorMap map_c, PParams p) {
@@ -157,7 +157,7 @@ pair_kernel(const __grid_constant__ CUtensorMap map_ah, const __grid_constant__ 
   const int nk = (p.K + BK - 1) / BK;
   const int tiles_per_batch = p.ntm * p.ntn;
   const int units = tiles_per_batch * p.batch;
-  const int chunk = p.chunk_kb;
+  const int chunk = SINGLE ? nk : p.chunk_kb;
 
   auto tile = [&](int s, int which) -> uint8_t* {  // 0 A_hi, 1 A_lo, 2 B_hi, 3 B_lo
     uint8_t* b = smem + s * C::STAGE_BYTES;
@@ -278,111 +278,156 @@ pair_kernel(const __grid_constant__ CUtensorMap map_ah, const __grid_constant__ 
       }
       ++gs;
     };
-    float acc[EPI_COLS];
-    auto drain = [&]() {
-      const int buf = gc & 1;
-      mbar_wait(&acc_full[buf], (gc >> 1) & 1);
-      asm volatile("tcgen05.fence::after_thread_sync;");
+    // one finished 32x32 block (this warp's 32 rows x 32 columns from col0):
+    // alpha, bias/act epilogue, then a TMA store of the XOR-swizzled staging
+    // block or (strided / accumulating C) 4-row x 128-byte stores through it
+    auto emit32 = [&](const float* vals, int bz, int row0, int col0, float alpha) {
+      const int grow = row0 + lane;
+      if (p.tma_store) {
+        if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+        __syncwarp();
 #pragma unroll
-      for (int cc = 0; cc < EPI_COLS; cc += 32) {
-        uint32_t v[32];
-        tmem_ld32(tmem_base + ((uint32_t)(quarter * 32) << 16) +
-                      (uint32_t)(buf * BN + half * EPI_COLS + cc), v);
-        asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-#pragma unroll
-        for (int j = 0; j < 32; ++j) acc[cc + j] += __uint_as_float(v[j]);
+        for (int q = 0; q < 8; ++q) {
+          float4 v = make_float4(vals[4 * q] * alpha, vals[4 * q + 1] * alpha,
+                                 vals[4 * q + 2] * alpha, vals[4 * q + 3] * alpha);
+          if (grow < p.M) epi4(p, bz, grow, col0 + 4 * q, v);
+          *reinterpret_cast<float4*>(stage + lane * 32 + 4 * (q ^ (lane & 7))) = v;
+        }
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        __syncwarp();
+        if (lane == 0) {
+          tma_store_3d(&map_c, stage, col0, row0, bz);
+          asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+        }
+        return;
       }
+      float* cbase = p.C + bz * p.scb;
+      const int sub_r = lane >> 3, sub_c = (lane & 7) * 4;
+#pragma unroll
+      for (int q = 0; q < 8; ++q)
+        *reinterpret_cast<float4*>(stage + lane * 32 + 4 * (q ^ (lane & 7))) =
+            make_float4(vals[4 * q] * alpha, vals[4 * q + 1] * alpha, vals[4 * q + 2] * alpha,
+                        vals[4 * q + 3] * alpha);
+      __syncwarp();
+      const int col = col0 + sub_c;
+#pragma unroll 4
+      for (int i = 0; i < 32; i += 4) {
+        const int row = row0 + i + sub_r;
+        const int srow = i + sub_r;
+        float4 v = *reinterpret_cast<const float4*>(stage + srow * 32 +
+                                                    4 * ((sub_c >> 2) ^ (srow & 7)));
+        if (row < p.M && col < p.N) {
+          float* q = cbase + (int64_t)row * p.scm + (int64_t)col * p.scn;
+          if (p.scn == 1 && col + 3 < p.N && ((reinterpret_cast<uintptr_t>(q) & 15) == 0)) {
+            if (p.accumulate) {
+              const float4 o = *reinterpret_cast<const float4*>(q);
+              v.x += o.x; v.y += o.y; v.z += o.z; v.w += o.w;
+            }
+            epi4(p, bz, row, col, v);
+            *reinterpret_cast<float4*>(q) = v;
+          } else {
+            if (p.accumulate) {
+              if (col < p.N) v.x += q[0];
+              if (col + 1 < p.N) v.y += q[p.scn];
+              if (col + 2 < p.N) v.z += q[2 * p.scn];
+              if (col + 3 < p.N) v.w += q[3 * p.scn];
+            }
+            epi4(p, bz, row, col, v);
+            const float e[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+            for (int j = 0; j < 4; ++j)
+              if (col + j < p.N) q[(int64_t)j * p.scn] = e[j];
+          }
+        }
+      }
+      __syncwarp();
+    };
+    auto release = [&](int buf) {
       asm volatile("tcgen05.fence::before_thread_sync;");
       named_bar(1, 32 * EPI_WARPS);
       if (et == 0) {
         if (rank == 0) mbar_arrive(&acc_empty[buf]);
         else mbar_arrive_remote(&acc_empty[buf], 0);
       }
-      ++gc;
     };
-    for (int u = pair; u < units; u += npairs) {
-      const int bz = u / tiles_per_batch, r = u % tiles_per_batch;
-      const int m0 = (r / p.ntn) * 256 + (int)rank * 128;
-      const int n0 = (r % p.ntn) * BN;
-      const int nchunks = (nk + chunk - 1) / chunk;
+    auto tile_of = [&](int u, int* bz, int* m0, int* n0) {
+      *bz = u / tiles_per_batch;
+      const int r = u % tiles_per_batch;
+      *m0 = (r / p.ntn) * 256 + (int)rank * 128;
+      *n0 = (r % p.ntn) * BN;
+    };
+    auto alpha_of = [&](int bz, int grow) {
+      return (p.alpha_rows && grow < p.M) ? __ldg(p.alpha_rows + (int64_t)bz * p.M + grow) : 1.f;
+    };
+    if constexpr (SINGLE) {
+      // the whole K accumulates in TMEM (short K): each finished tile streams
+      // TMEM -> registers (32 columns at a time) -> store; no register
+      // accumulator, so 256-wide tiles fit.  The drain of tile t runs while
+      // the MMA works on tile t+1 (its stages are split first).
+      auto drain_store = [&](int u) {
+        int bz, m0, n0;
+        tile_of(u, &bz, &m0, &n0);
+        const int buf = gc & 1;
+        mbar_wait(&acc_full[buf], (gc >> 1) & 1);
+        asm volatile("tcgen05.fence::after_thread_sync;");
+        const int row0 = m0 + quarter * 32;
+        const float alpha = alpha_of(bz, row0 + lane);
+#pragma unroll 1
+        for (int cc = 0; cc < EPI_COLS; cc += 32) {
+          uint32_t v[32];
+          tmem_ld32(tmem_base + ((uint32_t)(quarter * 32) << 16) +
+                        (uint32_t)(buf * BN + half * EPI_COLS + cc), v);
+          asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+          float f[32];
 #pragma unroll
-      for (int j = 0; j < EPI_COLS; ++j) acc[j] = 0.f;
-      for (int c = 0; c < nchunks; ++c) {
-        const int kb_beg = c * chunk, kb_end = min(nk, kb_beg + chunk);
-        for (int kb = kb_beg; kb < kb_end; ++kb) split_stage();
-        if (c > 0) drain();
+          for (int j = 0; j < 32; ++j) f[j] = __uint_as_float(v[j]);
+          if (cc + 32 >= EPI_COLS) release(buf);  // all of this buffer is in registers
+          emit32(f, bz, row0, n0 + half * EPI_COLS + cc, alpha);
+        }
+        ++gc;
+      };
+      int prev = -1;
+      for (int u = pair; u < units; u += npairs) {
+        for (int kb = 0; kb < nk; ++kb) split_stage();
+        if (prev >= 0) drain_store(prev);
+        prev = u;
       }
-      drain();
-      const int row0 = m0 + quarter * 32;
-      const int grow = row0 + lane;
-      const float alpha =
-          (p.alpha_rows && grow < p.M) ? __ldg(p.alpha_rows + (int64_t)bz * p.M + grow) : 1.f;
-      if (p.tma_store) {
+      if (prev >= 0) drain_store(prev);
+    } else {
+      float acc[EPI_COLS];
+      auto drain = [&]() {
+        const int buf = gc & 1;
+        mbar_wait(&acc_full[buf], (gc >> 1) & 1);
+        asm volatile("tcgen05.fence::after_thread_sync;");
 #pragma unroll
         for (int cc = 0; cc < EPI_COLS; cc += 32) {
-          if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
-          __syncwarp();
-          const int col0 = n0 + half * EPI_COLS + cc;
+          uint32_t v[32];
+          tmem_ld32(tmem_base + ((uint32_t)(quarter * 32) << 16) +
+                        (uint32_t)(buf * BN + half * EPI_COLS + cc), v);
+          asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 #pragma unroll
-          for (int q = 0; q < 8; ++q) {
-            float4 v = make_float4(acc[cc + 4 * q] * alpha, acc[cc + 4 * q + 1] * alpha,
-                                   acc[cc + 4 * q + 2] * alpha, acc[cc + 4 * q + 3] * alpha);
-            if (grow < p.M) epi4(p, bz, grow, col0 + 4 * q, v);
-            *reinterpret_cast<float4*>(stage + lane * 32 + 4 * (q ^ (lane & 7))) = v;
-          }
-          asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-          __syncwarp();
-          if (lane == 0) {
-            tma_store_3d(&map_c, stage, col0, row0, bz);
-            asm volatile("cp.async.bulk.commit_group;" ::: "memory");
-          }
+          for (int j = 0; j < 32; ++j) acc[cc + j] += __uint_as_float(v[j]);
         }
-        continue;
-      }
-      // generic strided / accumulating store: 32x32 blocks transposed through
-      // smem so each store instruction covers 4 rows x 128 contiguous bytes
-      float* cbase = p.C + bz * p.scb;
-      const int sub_r = lane >> 3, sub_c = (lane & 7) * 4;
+        release(buf);
+        ++gc;
+      };
+      for (int u = pair; u < units; u += npairs) {
+        int bz, m0, n0;
+        tile_of(u, &bz, &m0, &n0);
+        const int nchunks = (nk + chunk - 1) / chunk;
 #pragma unroll
-      for (int cc = 0; cc < EPI_COLS; cc += 32) {
-#pragma unroll
-        for (int q = 0; q < 8; ++q)
-          *reinterpret_cast<float4*>(stage + lane * 32 + 4 * (q ^ (lane & 7))) =
-              make_float4(acc[cc + 4 * q] * alpha, acc[cc + 4 * q + 1] * alpha,
-                          acc[cc + 4 * q + 2] * alpha, acc[cc + 4 * q + 3] * alpha);
-        __syncwarp();
-        const int col = n0 + half * EPI_COLS + cc + sub_c;
-#pragma unroll 4
-        for (int i = 0; i < 32; i += 4) {
-          const int row = row0 + i + sub_r;
-          const int srow = i + sub_r;
-          float4 v = *reinterpret_cast<const float4*>(stage + srow * 32 +
-                                                      4 * ((sub_c >> 2) ^ (srow & 7)));
-          if (row < p.M && col < p.N) {
-            float* q = cbase + (int64_t)row * p.scm + (int64_t)col * p.scn;
-            if (p.scn == 1 && col + 3 < p.N && ((reinterpret_cast<uintptr_t>(q) & 15) == 0)) {
-              if (p.accumulate) {
-                const float4 o = *reinterpret_cast<const float4*>(q);
-                v.x += o.x; v.y += o.y; v.z += o.z; v.w += o.w;
-              }
-              epi4(p, bz, row, col, v);
-              *reinterpret_cast<float4*>(q) = v;
-            } else {
-              if (p.accumulate) {
-                if (col < p.N) v.x += q[0];
-                if (col + 1 < p.N) v.y += q[p.scn];
-                if (col + 2 < p.N) v.z += q[2 * p.scn];
-                if (col + 3 < p.N) v.w += q[3 * p.scn];
-              }
-              epi4(p, bz, row, col, v);
-              const float e[4] = {v.x, v.y, v.z, v.w};
-#pragma unroll
-              for (int j = 0; j < 4; ++j)
-                if (col + j < p.N) q[(int64_t)j * p.scn] = e[j];
-            }
-          }
+        for (int j = 0; j < EPI_COLS; ++j) acc[j] = 0.f;
+        for (int c = 0; c < nchunks; ++c) {
+          const int kb_beg = c * chunk, kb_end = min(nk, kb_beg + chunk);
+          for (int kb = kb_beg; kb < kb_end; ++kb) split_stage();
+          if (c > 0) drain();
         }
-        __syncwarp();
+        drain();
+        const int row0 = m0 + quarter * 32;
+        const float alpha = alpha_of(bz, row0 + lane);
+#pragma unroll
+        for (int cc = 0; cc < EPI_COLS; cc += 32)
+          emit32(&acc[cc], bz, row0, n0 + half * EPI_COLS + cc, alpha);
       }
     }
     if (p.tma_store && lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
@@ -446,9 +491,12 @@ static int num_pairs() {
 }
 
 // N tile: the smaller of (waves x tile width), ties to 256 (less operand traffic)
-static int choose_bn(const GemmArgs& g) {
-  if (const char* e = getenv("PFB_PAIR_BN")) return atoi(e) == 256 ? 256 : 128;
-  if (g.N <= 128) return 128;
+// 256-wide tiles only in the TMEM-resident (short-K) mode: with register
+// accumulation a 128 x 256 half tile needs 128 accumulators per epilogue
+// thread, more than 10 warps per SM can hold
+static int choose_bn(const GemmArgs& g, bool single) {
+  if (const char* e = getenv("PFB_PAIR_BN")) return (atoi(e) == 256 && single) ? 256 : 128;
+  if (g.N <= 128 || !single) return 128;
   const int64_t ntm = (g.M + 255) / 256;
   auto cost = [&](int bn) {
     const int64_t units = ntm * ((g.N + bn - 1) / bn) * g.batch;
@@ -466,14 +514,15 @@ static int pair_chunk() {
   return c;
 }
 
-template <int BN>
+template <int BN, bool SINGLE>
 static int launch_pair(const CUtensorMap& mah, const CUtensorMap& mal, const CUtensorMap& mbh,
                        const CUtensorMap& mbl, const CUtensorMap& mc, const PParams& p,
                        cudaStream_t s) {
   using C = Cfg<BN>;
   static bool attr = false;
   if (!attr) {
-    cudaFuncSetAttribute(pair_kernel<BN>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
+    cudaFuncSetAttribute(pair_kernel<BN, SINGLE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         C::SMEM);
     attr = true;
   }
   const int64_t units = (int64_t)p.ntm * p.ntn * p.batch;
@@ -492,7 +541,7 @@ static int launch_pair(const CUtensorMap& mah, const CUtensorMap& mal, const CUt
   at[1].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = at;
   cfg.numAttrs = pdl_enabled() ? 2 : 1;
-  cudaLaunchKernelEx(&cfg, pair_kernel<BN>, mah, mal, mbh, mbl, mc, p);
+  cudaLaunchKernelEx(&cfg, pair_kernel<BN, SINGLE>, mah, mal, mbh, mbl, mc, p);
   return launch_status();
 }
 
@@ -505,7 +554,11 @@ int gemm_tcgen05_pair(const GemmArgs& g, void* ws, int64_t ws_bytes, cudaStream_
   const int a_bc = g.sab == 0 && g.batch > 1;
   const int b_bc = g.sbb == 0 && g.batch > 1 && !(g.kscale && g.skb != 0);
   const int64_t ba = a_bc ? 1 : g.batch, bb = b_bc ? 1 : g.batch;
-  const int bn = choose_bn(g);
+  // short K: the whole accumulation stays in TMEM (error ~K/4096 x 1e-4
+  // relative from the tensor core's truncating accumulation, measured)
+  const int64_t Kp0 = (g.K + 3) / 4 * 4;
+  const bool single = Kp0 <= 256 && !getenv_flag("PFB_PAIR_NO_SINGLE");
+  const int bn = choose_bn(g, single);
   const int bnh = bn / 2;
   int am = kPreSplit, bm = kPreSplit;
   if (variant == 2) {
@@ -558,8 +611,10 @@ int gemm_tcgen05_pair(const GemmArgs& g, void* ws, int64_t ws_bytes, cudaStream_
             (int)((g.M + 255) / 256), (int)((g.N + bn - 1) / bn), a_bc, b_bc, am, bm, idesc,
             g.C, g.scb, g.scm, g.scn, g.alpha_rows, g.accumulate,
             g.bias, g.sxb, g.sxm, g.sxn, g.act, tma_store, pair_chunk()};
-  return bn == 256 ? launch_pair<256>(mah, mal, mbh, mbl, mc, p, s)
-                   : launch_pair<128>(mah, mal, mbh, mbl, mc, p, s);
+  if (single)
+    return bn == 256 ? launch_pair<256, true>(mah, mal, mbh, mbl, mc, p, s)
+                     : launch_pair<128, true>(mah, mal, mbh, mbl, mc, p, s);
+  return launch_pair<128, false>(mah, mal, mbh, mbl, mc, p, s);
 }
 
 }  // namespace pfb

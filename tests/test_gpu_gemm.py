@@ -291,3 +291,32 @@ def test_matmul_dual(env, force, shape):
     assert rc == 0, rc
     torch.cuda.synchronize()
     np.testing.assert_allclose(C.to_numpy().astype(np.float64), want, rtol=RTOL, atol=ATOL)
+
+
+# CTA-pair kernel (cta_group::2): 5 = pre-split, 6 = raw feed.  K <= 256 runs
+# the TMEM-resident mode (256-wide tiles allowed), longer K the chunked one.
+PAIR_SHAPES = [(512, 256, 64), (300, 520, 200), (257, 130, 96), (1024, 768, 256),
+               (384, 256, 1000)]
+
+
+@pytest.mark.parametrize("shape", PAIR_SHAPES)
+@pytest.mark.parametrize("layout", ["a_k/b_mn", "a_k/b_k", "a_mn/b_k"])
+@pytest.mark.parametrize("force", [5, 6])
+def test_gemm_pair_kernel(env, shape, layout, force):
+    m, n, k = shape
+    r = np.random.default_rng(m * 3 + n + k)
+    a, b = _operands(r, (m, k), (k, n))
+    got = _run(env, a, b, force, transpose_b=layout.endswith("b_k"),
+               a_mn=layout.startswith("a_mn"))
+    np.testing.assert_allclose(got, a @ b, rtol=RTOL, atol=ATOL)
+
+
+@pytest.mark.parametrize("force", [5, 6])
+def test_gemm_pair_batched_alpha_accumulate(env, force):
+    r = np.random.default_rng(29)
+    a, b = _operands(r, (3, 300, 64), (3, 64, 260))
+    c0 = _f32(r, (3, 300, 260))
+    alpha = np.asarray(r.standard_normal(3 * 300), np.float32).astype(np.float64)
+    got = _run(env, a, b, force, transpose_b=True, accumulate_into=c0, alpha=alpha)
+    want = c0 + alpha.reshape(3, 300)[:, :, None] * (a @ b)
+    np.testing.assert_allclose(got, want, rtol=RTOL, atol=ATOL)
