@@ -36,6 +36,11 @@ using namespace tc;
 
 constexpr int BK = 32, UMMA_K = 8, EPI_WARPS = 8;
 constexpr int NUM_THREADS = 64 + 32 * EPI_WARPS;
+// TMEM-resident mode: 4 more warps split the raw stages, so splitting the
+// next tile never waits behind the drain + store of the previous one
+constexpr int SPLIT_WARPS = 4;
+template <bool SINGLE>
+constexpr int threads_of() { return NUM_THREADS + (SINGLE ? 32 * SPLIT_WARPS : 0); }
 constexpr int A_BYTES = 128 * BK * 4;  // 16 KB: this CTA's 128 rows of A
 enum { kPreSplit = 0, kRawK = 1, kRawMN = 2 };
 
@@ -133,7 +138,7 @@ __device__ __forceinline__ void epi4(const PParams& p, int bz, int row, int col,
 }
 
 template <int BN, bool SINGLE>
-__global__ void __maxnreg__(168)
+__global__ void __launch_bounds__(threads_of<SINGLE>(), 1)
 pair_kernel(const __grid_constant__ CUtensorMap map_ah, const __grid_constant__ CUtensorMap map_al,
             const __grid_constant__ CUtensorMap map_bh, const __grid_constant__ CUtensorMap map_bl,
             const __grid_constant__ CUtensorMap map_c, PParams p) {
@@ -255,6 +260,30 @@ pair_kernel(const __grid_constant__ CUtensorMap map_ah, const __grid_constant__ 
       }
     }
     __syncwarp();
+  } else if (SINGLE && warp >= 2 + EPI_WARPS) {
+    // ---- split warps (TMEM-resident mode): raw stages -> lo planes, then
+    // one `ready` arrival per CTA on the leader
+    const int st_ = threadIdx.x - 32 * (2 + EPI_WARPS);
+    const bool split_a = p.a_mode != kPreSplit, split_b = p.b_mode != kPreSplit;
+    int g = 0;
+    for (int u = pair; u < units; u += npairs) {
+      for (int kb = 0; kb < nk; ++kb, ++g) {
+        const int s = g % STAGES;
+        mbar_wait(&full[s], (g / STAGES) & 1);
+        if (split_a)
+          split_tf32_smem(smem_u32(tile(s, 0)), smem_u32(tile(s, 1)), A_BYTES / 16, st_,
+                          32 * SPLIT_WARPS);
+        if (split_b)
+          split_tf32_smem(smem_u32(tile(s, 2)), smem_u32(tile(s, 3)), C::B_BYTES / 16, st_,
+                          32 * SPLIT_WARPS);
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        named_bar(2, 32 * SPLIT_WARPS);
+        if (st_ == 0) {
+          if (rank == 0) mbar_arrive(&ready[s]);
+          else mbar_arrive_remote(&ready[s], 0);
+        }
+      }
+    }
   } else {
     const int quarter = warp & 3;
     const int half = (warp - 2) >> 2;
@@ -386,13 +415,7 @@ pair_kernel(const __grid_constant__ CUtensorMap map_ah, const __grid_constant__ 
         }
         ++gc;
       };
-      int prev = -1;
-      for (int u = pair; u < units; u += npairs) {
-        for (int kb = 0; kb < nk; ++kb) split_stage();
-        if (prev >= 0) drain_store(prev);
-        prev = u;
-      }
-      if (prev >= 0) drain_store(prev);
+      for (int u = pair; u < units; u += npairs) drain_store(u);
     } else {
       float acc[EPI_COLS];
       auto drain = [&]() {
@@ -529,7 +552,7 @@ static int launch_pair(const CUtensorMap& mah, const CUtensorMap& mal, const CUt
   const int pairs = (int)std::min<int64_t>(units, num_pairs());
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3((unsigned)(2 * pairs));
-  cfg.blockDim = dim3(NUM_THREADS);
+  cfg.blockDim = dim3(threads_of<SINGLE>());
   cfg.dynamicSmemBytes = C::SMEM;
   cfg.stream = s;
   cudaLaunchAttribute at[2];

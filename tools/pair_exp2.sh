@@ -1,0 +1,4 @@
+timeout 900 python -m pytest tests/test_gpu_gemm.py -q -k pair 2>&1 | tail -1
+for s in "1024 2048 64 256" "8192 256 784" "1024 256 256" "2048 2048 256" "320 784 256" "10240 784 256"; do
+  for f in 5 6; do timeout 60 python tools/gemm_probe.py --graph --force $f --shape $s --iters 10 2>&1 | tail -1; done
+done
