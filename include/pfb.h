@@ -89,6 +89,12 @@ int pfb_fused_ew_multi(int32_t n_in, const pfb_tensor* ins, int32_t n_steps,
 
 /* select(mask, a, b) = mask ? a : b with broadcasting (predicated cond /
  * while bodies; numpy.where semantics); any dtype, mask is bool. */
+/* integer-domain fused elementwise program (i64 / bool registers, int32
+ * immediates; same encoding as pfb_fused_ew_multi): loop counters, index
+ * arithmetic and masks of converted control flow (reference tensor.py:104-188
+ * on i64/bool values), bit-exact with numpy int64 wraparound. */
+int pfb_fused_int(int32_t n_in, const pfb_tensor* ins, int32_t n_steps, const int32_t* program,
+                  int32_t n_out, const int32_t* out_regs, pfb_tensor* outs, void* stream);
 int pfb_select(const pfb_tensor* mask, const pfb_tensor* a, const pfb_tensor* b, pfb_tensor* out,
                void* stream);
 

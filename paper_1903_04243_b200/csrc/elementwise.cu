@@ -490,9 +490,146 @@ void launch_fused(int n_in, const Layout& L, IdxT ngroups, const FusedProgram& P
 #undef PFB_FUSED_CASE
 }
 
+// ---------------------------------------------------------------------------
+// Integer-domain fused programs (F3 over i64 / bool: loop counters, index
+// arithmetic, masks of predicated control flow).  Same program encoding as
+// the float interpreter; registers are int64 (bool = 0/1), i64 wraps like
+// numpy; constants are int32 immediates.  One element per thread (these
+// tensors are [n]-sized bookkeeping values).
+template <typename IdxT, int NIN>
+__global__ void __launch_bounds__(256) fused_int_kernel(Layout L, IdxT n, FusedProgram P,
+                                                        FusedOuts outs, const void* i0,
+                                                        const void* i1, const void* i2,
+                                                        const void* i3, const void* i4,
+                                                        const void* i5, const void* i6,
+                                                        const void* i7) {
+  pdl_enter();
+  __shared__ int4 prog[kMaxSteps];
+  for (int s = threadIdx.x; s < P.n_steps; s += blockDim.x)
+    prog[s] = make_int4(P.code[s][0], P.code[s][1], P.code[s][2], P.code[s][3]);
+  __syncthreads();
+  for (IdxT e = blockIdx.x * (IdxT)blockDim.x + threadIdx.x; e < n;
+       e += (IdxT)gridDim.x * blockDim.x) {
+    int64_t off[NIN + 1];
+    offsets<IdxT, NIN + 1>(L, e, off);
+    int64_t in[NIN];
+#pragma unroll
+    for (int K = 0; K < NIN; ++K) {
+      const void* ip = K == 0 ? i0 : K == 1 ? i1 : K == 2 ? i2 : K == 3 ? i3
+                     : K == 4 ? i4 : K == 5 ? i5 : K == 6 ? i6 : i7;
+      in[K] = P.in_dtype[K] == PFB_BOOL
+                  ? (int64_t)__ldg(reinterpret_cast<const uint8_t*>(ip) + off[K + 1])
+                  : __ldg(reinterpret_cast<const long long*>(ip) + off[K + 1]);
+    }
+    int64_t r[kMaxRegs];
+    for (int s = 0; s < P.n_steps; ++s) {
+      const int4 c = prog[s];
+      int64_t o = 0;
+      if (c.x == F_LOAD) {
+        switch (c.z) {
+#define PFB_LDI(K) case K: if (K < NIN) o = in[K < NIN ? K : 0]; break;
+          PFB_LDI(0) PFB_LDI(1) PFB_LDI(2) PFB_LDI(3) PFB_LDI(4) PFB_LDI(5) PFB_LDI(6) PFB_LDI(7)
+#undef PFB_LDI
+        }
+      } else if (c.x == F_CONST) {
+        o = (int64_t)c.z;
+      } else if (c.x == F_SELECT) {
+        o = r[c.z] != 0 ? r[c.w] : r[c.y];
+      } else {
+        const int64_t a = r[c.z], b = r[c.w];
+        const uint64_t ua = (uint64_t)a, ub = (uint64_t)b;
+        switch (c.x) {
+          case PFB_ADD: o = (int64_t)(ua + ub); break;
+          case PFB_SUB: o = (int64_t)(ua - ub); break;
+          case PFB_MUL: o = (int64_t)(ua * ub); break;
+          case PFB_MAX: o = a >= b ? a : b; break;
+          case PFB_MIN: o = a <= b ? a : b; break;
+          case PFB_LESS: o = a < b; break;
+          case PFB_EQUAL: o = a == b; break;
+          case 16 + PFB_NEG: o = (int64_t)(0 - ua); break;
+          case 16 + PFB_SQUARE: o = (int64_t)(ua * ua); break;
+          case 16 + PFB_LOGICAL_NOT: o = a == 0; break;
+          case 66: o = a != 0; break;  // to bool
+          default: o = a; break;        // 67: move
+        }
+      }
+      r[c.y] = o;
+    }
+    for (int k = 0; k < P.n_out; ++k) {
+      const int64_t v = r[P.out_reg[k]];
+      if (P.out_dt[k] == PFB_BOOL)
+        reinterpret_cast<uint8_t*>(outs.p[k])[off[0]] = (uint8_t)(v != 0);
+      else
+        reinterpret_cast<long long*>(outs.p[k])[off[0]] = v;
+    }
+  }
+}
 }  // namespace pfb
 
 using namespace pfb;
+
+extern "C" int pfb_fused_int(int32_t n_in, const pfb_tensor* ins, int32_t n_steps,
+                             const int32_t* program, int32_t n_out, const int32_t* out_regs,
+                             pfb_tensor* outs, void* stream) {
+  if (n_in < 1 || n_in > 8 || n_steps < 1 || n_steps > kMaxSteps) return PFB_E_ARG;
+  if (n_out < 1 || n_out > kMaxOuts) return PFB_E_ARG;
+  const pfb_tensor* out = &outs[0];
+  for (int k = 0; k < n_out; ++k) {
+    if (outs[k].dtype != PFB_I64 && outs[k].dtype != PFB_BOOL) return PFB_E_DTYPE;
+    if (outs[k].rank != out->rank) return PFB_E_SHAPE;
+    for (int d = 0; d < out->rank; ++d)
+      if (outs[k].shape[d] != out->shape[d] ||
+          (out->shape[d] > 1 && outs[k].stride[d] != out->stride[d]))
+        return PFB_E_SHAPE;
+    if (out_regs[k] < 0 || out_regs[k] >= kMaxRegs) return PFB_E_ARG;
+  }
+  int64_t stb[8][kMaxRank];
+  const int64_t* st[kMaxOps];
+  st[0] = out->stride;
+  FusedProgram P;
+  P.n_in = n_in;
+  P.n_steps = n_steps;
+  for (int k = 0; k < n_in; ++k) {
+    if (ins[k].dtype != PFB_I64 && ins[k].dtype != PFB_BOOL) return PFB_E_DTYPE;
+    if (!broadcast_strides(&ins[k], out->rank, out->shape, stb[k])) return PFB_E_SHAPE;
+    st[k + 1] = stb[k];
+    P.in_dtype[k] = ins[k].dtype;
+  }
+  for (int k = n_in; k < 8; ++k) P.in_dtype[k] = PFB_I64;
+  for (int s = 0; s < n_steps; ++s) {
+    for (int j = 0; j < 4; ++j) P.code[s][j] = program[4 * s + j];
+    if (P.code[s][1] < 0 || P.code[s][1] >= kMaxRegs) return PFB_E_ARG;
+  }
+  FusedOuts fo;
+  P.n_out = n_out;
+  for (int k = 0; k < kMaxOuts; ++k) {
+    fo.p[k] = k < n_out ? outs[k].data : nullptr;
+    P.out_reg[k] = k < n_out ? out_regs[k] : 0;
+    P.out_dt[k] = k < n_out ? outs[k].dtype : PFB_I64;
+  }
+  Layout L = make_layout(out->rank, out->shape, n_in + 1, st);
+  const int64_t n = numel(out);
+  if (n == 0) return 0;
+  const void* p[8];
+  for (int k = 0; k < 8; ++k) p[k] = k < n_in ? ins[k].data : nullptr;
+  cudaStream_t s = as_stream(stream);
+  const int grid = grid_for(n, 256);
+#define PFB_FI_CASE(K)                                                                         \
+  case K:                                                                                      \
+    if (n < (int64_t)0x7fffffff)                                                               \
+      launch(fused_int_kernel<uint32_t, K>, grid, 256, 0, s, L, (uint32_t)n, P, fo, p[0], p[1], \
+             p[2], p[3], p[4], p[5], p[6], p[7]);                                              \
+    else                                                                                       \
+      launch(fused_int_kernel<int64_t, K>, grid, 256, 0, s, L, n, P, fo, p[0], p[1], p[2],     \
+             p[3], p[4], p[5], p[6], p[7]);                                                    \
+    break;
+  switch (n_in) {
+    PFB_FI_CASE(1) PFB_FI_CASE(2) PFB_FI_CASE(3) PFB_FI_CASE(4)
+    PFB_FI_CASE(5) PFB_FI_CASE(6) PFB_FI_CASE(7) PFB_FI_CASE(8)
+  }
+#undef PFB_FI_CASE
+  return launch_status();
+}
 
 extern "C" int pfb_binary(int32_t op, const pfb_tensor* a, const pfb_tensor* b, pfb_tensor* out,
                           void* stream) {

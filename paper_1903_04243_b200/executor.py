@@ -1560,6 +1560,29 @@ def _h_fused_multi(ex, node, ins):
     return outs
 
 
+def _h_fused_int(ex, node, ins):
+    """fused_int (passes.fuse_elementwise, i64/bool domain): counter, index
+    and mask arithmetic of converted control flow in one launch
+    (pfb_fused_int)."""
+    arrs = [ex._dev(v) for v in ins]
+    shape = ()
+    for a in arrs:
+        shape = broadcast_shapes(shape, a.shape)
+    outs = [ex._empty(shape, dt) for dt in node.attrs["out_dtypes"]]
+    prog = ex._programs.get(id(node))
+    if prog is None:
+        flat = [int(x) for step in node.attrs["program"] for x in step]
+        regs = [int(r) for r in node.attrs["out_regs"]]
+        prog = ex._programs[id(node)] = ((ctypes.c_int32 * len(flat))(*flat),
+                                         len(node.attrs["program"]),
+                                         (ctypes.c_int32 * len(regs))(*regs), len(regs))
+    descs = (N.PfbTensor * len(arrs))(*[a.desc() for a in arrs])
+    odescs = (N.PfbTensor * len(outs))(*[o.desc() for o in outs])
+    ex._call(ex._lib.pfb_fused_int, len(arrs), descs, prog[1], prog[0], prog[3], prog[2],
+             odescs, ex._stream, what="fused_int", work=(_abytes(*arrs, *outs), 0))
+    return outs
+
+
 def _h_reduce_dot(ex, node, ins):
     x, y = (ex._dev(v) for v in ins)
     axes = normalize_axes(node.attrs["axes"], x.rank)
@@ -1637,6 +1660,7 @@ _HANDLERS.update({
     "row_dots": _h_row_dots,
     "fused_ewm": _h_fused_multi,
     "matmul2": _h_matmul2,
+    "fused_int": _h_fused_int,
     "gather_rows": _h_gather, "scatter_rows": _h_scatter_rows,
     "scatter_add_rows": _h_scatter_add, "reshape": _h_reshape, "transpose": _h_transpose,
     "slice_leading": _h_slice_leading, "tile_leading": _h_tile_leading,

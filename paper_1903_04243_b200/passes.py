@@ -688,22 +688,59 @@ OP_LOAD, OP_CONST, OP_TOBOOL, OP_MOV, OP_SELECT = 64, 65, 66, 67, 68
 MAX_INPUTS, MAX_STEPS, MAX_REGS = 8, 48, 16
 
 
-def _ew_eligible(g, node):
+_INT_BIN = frozenset({"add", "sub", "mul", "max", "min", "less", "equal"})
+_INT_UN = frozenset({"neg", "square", "logical_not"})
+
+
+def _ew_eligible(g, node, domain="float"):
+    """Can `node` join an elementwise group of `domain`: "float" (fp32 / bool
+    registers, `fused_ew[m]`) or "int" (int64 / bool registers, `fused_int`:
+    loop counters, index arithmetic, masks)."""
     from .tensor import DType
     k = node.kind
-    if k not in _BIN_CODE and k not in _UN_CODE and k not in ("cast", "select"):
+    allowed = (DType.F64, DType.BOOL) if domain == "float" else (DType.I64, DType.BOOL)
+    if domain == "float":
+        if k not in _BIN_CODE and k not in _UN_CODE and k not in ("cast", "select"):
+            return False
+    elif k not in _INT_BIN and k not in _INT_UN and k not in ("cast", "select"):
         return False
-    if node.output_arity != 1 or node.out_dtypes[0] not in (DType.F64, DType.BOOL):
+    if node.output_arity != 1 or node.out_dtypes[0] not in allowed:
         return False
     sh = node.out_shapes[0]
     if sh is None or any(d is None for d in sh):
         return False
     for src in node.inputs:
-        if g.ref_dtype(src) not in (DType.F64, DType.BOOL):
+        if g.ref_dtype(src) not in allowed:
             return False
     if k == "select" and g.ref_dtype(node.inputs[0]) != DType.BOOL:
         return False
     return True
+
+
+def _domains(g, node):
+    """Domains a group rooted at `node` can use (bool-only roots: both)."""
+    from .tensor import DType
+    if node.output_arity != 1:
+        return ()
+    dts = [node.out_dtypes[0]] + [g.ref_dtype(s_) for s_ in node.inputs]
+    if any(d == DType.I64 for d in dts):
+        return ("int",)
+    if any(d == DType.F64 for d in dts):
+        return ("float",)
+    return ("int", "float")
+
+
+def _const_scalar_i(g, key):
+    import numpy as np
+    from .tensor import DType
+    n = g.nodes[key[0]]
+    if n.kind == "constant" and key[1] == 0:
+        v = n.attrs["value"]
+        if v.rank == 0 and v.dtype in (DType.I64, DType.BOOL):
+            x = int(np.asarray(v.data).item())
+            if -2 ** 31 <= x < 2 ** 31:
+                return x
+    return None
 
 
 def _const_scalar_f(g, key):
@@ -717,9 +754,10 @@ def _const_scalar_f(g, key):
     return None
 
 
-def _program(g, order, root, externals, outputs=()):
+def _program(g, order, root, externals, outputs=(), domain="float"):
     """Register program for the group `order` (topo order, root last).
-    Registers of `outputs` (node ids) are kept to the end of the program."""
+    Registers of `outputs` (node ids) are kept to the end of the program.
+    domain "int": constants are int32 immediates, casts bool<->i64."""
     import struct
     from .tensor import DType
     ext_index = {k: i for i, k in enumerate(externals)}
@@ -738,9 +776,9 @@ def _program(g, order, root, externals, outputs=()):
         if not free:
             raise OverflowError
         r = free.pop()
-        c = _const_scalar_f(g, src)
+        c = _const_scalar_f(g, src) if domain == "float" else _const_scalar_i(g, src)
         if c is not None:
-            bits = struct.unpack("<i", struct.pack("<f", c))[0]
+            bits = struct.unpack("<i", struct.pack("<f", c))[0] if domain == "float" else c
             steps.append((OP_CONST, r, bits, 0))
         else:
             steps.append((OP_LOAD, r, ext_index[src], 0))
@@ -771,7 +809,7 @@ def _program(g, order, root, externals, outputs=()):
             steps.append((_BIN_CODE[k], dst, ops[0], ops[1]))
         elif k in _UN_CODE:
             steps.append((16 + _UN_CODE[k], dst, ops[0], ops[0]))
-        else:  # cast between f64 (fp32) and bool
+        else:  # cast between f64 (fp32) / i64 and bool
             to = n.attrs["dtype"]
             frm = g.ref_dtype(n.inputs[0])
             op = OP_TOBOOL if (to == DType.BOOL and frm != DType.BOOL) else OP_MOV
@@ -810,7 +848,7 @@ def fuse_elementwise(g, keep=()):
     moved = {}
     fused = 0
 
-    def grow(root, multi):
+    def grow(root, multi, domain="float"):
         shape = root.out_shapes[0]
         rpos = pos[root.id]
         group = {root.id}
@@ -822,7 +860,7 @@ def fuse_elementwise(g, keep=()):
                     p = g.nodes[src[0]]
                     if p.id in group or p.id in assigned or src[1] != 0:
                         continue
-                    if not _ew_eligible(g, p) or p.out_shapes[0] != shape:
+                    if not _ew_eligible(g, p, domain) or p.out_shapes[0] != shape:
                         continue
                     outside = users.get(src, set()) - group
                     if multi:
@@ -843,12 +881,13 @@ def fuse_elementwise(g, keep=()):
         key = (nid, 0)
         return key in keep or bool(users.get(key, set()) - group)
 
-    def build(root, group):
+    def build(root, group, domain="float"):
         order = sorted((g.nodes[i] for i in group), key=lambda n: pos[n.id])
+        const_of = _const_scalar_f if domain == "float" else _const_scalar_i
         externals = []
         for n in order:
             for src in n.inputs:
-                if src[0] not in group and src not in externals and _const_scalar_f(g, src) is None:
+                if src[0] not in group and src not in externals and const_of(g, src) is None:
                     externals.append(src)
         if len(externals) > MAX_INPUTS or not externals:
             # (no tensor input: a constant-only group -- left to the
@@ -856,28 +895,38 @@ def fuse_elementwise(g, keep=()):
             return None
         extra = [n.id for n in order if n.id != root.id and _is_out(n.id, group)]
         try:
-            if not extra:
+            if not extra and domain == "float":
                 return order, externals, [root.id], _program(g, order, root, externals), None
             outs = [root.id] + extra
-            prog, regs = _program(g, order, root, externals, outs)
+            prog, regs = _program(g, order, root, externals, outs, domain)
             return order, externals, outs, prog, regs
         except OverflowError:
             return None
 
-    for root in reversed(topo):
-        if root.id in assigned or root.id not in live or not _ew_eligible(g, root):
-            continue
-        group = grow(root, True)
-        built = build(root, group) if len(group) >= 2 else None
+    def best_group(root, domain):
+        group = grow(root, True, domain)
+        built = build(root, group, domain) if len(group) >= 2 else None
         if built is None:
-            group = grow(root, False)
+            group = grow(root, False, domain)
             if len(group) < 2:
-                continue
-            built = build(root, group)
-            if built is None:
-                continue
+                return None
+            built = build(root, group, domain)
+        return None if built is None else (group, built)
+
+    for root in reversed(topo):
+        if root.id in assigned or root.id not in live:
+            continue
+        cands = [(d, best_group(root, d)) for d in _domains(g, root) if _ew_eligible(g, root, d)]
+        cands = [(d, r) for d, r in cands if r is not None]
+        if not cands:
+            continue
+        domain, (group, built) = max(cands, key=lambda c: len(c[1][0]))
         order, externals, outs, prog, regs = built
-        if regs is None:
+        if domain == "int":
+            new = g.add_node("fused_int", externals,
+                             {"program": prog, "out_regs": regs,
+                              "out_dtypes": tuple(g.nodes[i].out_dtypes[0] for i in outs)})
+        elif regs is None:
             new = g.add_node("fused_ew", externals,
                              {"program": prog, "out_dtype": root.out_dtypes[0]})
         else:

@@ -184,3 +184,21 @@ def test_f3_leaves_constant_only_groups_alone():
     for a, b in zip(got, want):
         if a.data.size and not c["tainted"][0]:
             np.testing.assert_allclose(a.data, b.data, rtol=1e-12)
+
+
+def test_f3_integer_domain_groups():
+    """cfg5's masked loop body: the per-example counter / index / mask
+    arithmetic (i64 and bool) fuses into `fused_int` programs -- values
+    unchanged (oracle), integer results exact."""
+    w = WL.cfg5(WL.this_api(), n=7, max_len=6, units=4, masked=True, unroll=2)
+    _, g2, _ = _run_both(w)
+
+    def kinds(gr):
+        out = []
+        for n in gr.nodes.values():
+            out.append(n.kind)
+            if n.block is not None:
+                for sg in n.block.subgraphs.values():
+                    out.extend(kinds(sg))
+        return out
+    assert "fused_int" in kinds(g2)
