@@ -21,6 +21,16 @@ last = max(i for i, (_, k, _) in enumerate(seq) if "FillFunctor<unsigned char>" 
 step = seq[last + 1:]
 tot = sum(t for _, _, t in step)
 print(f"{c}: {len(step)} launches in the last step, sum {tot/1e3:.1f} us (units ns->us)")
+import collections
+agg = collections.defaultdict(lambda: [0.0, 0])
 for i, k, t in step:
-    print(f"  {t/1e3:8.2f} us  {k[:90]}")
+    a = agg[k[:80]]
+    a[0] += t
+    a[1] += 1
+if len(step) > 40:
+    for k, (t, n) in sorted(agg.items(), key=lambda kv: -kv[1][0])[:25]:
+        print(f"  {t/1e3:9.1f} us  n={n:4d}  mean={t/n/1e3:6.2f} us  {k}")
+else:
+    for i, k, t in step:
+        print(f"  {t/1e3:8.2f} us  {k[:90]}")
 PY
