@@ -313,6 +313,76 @@ __global__ void __launch_bounds__(256) outer1_kernel(GemmArgs g, int64_t rows_pe
   }
 }
 
+// N <= 16 (logits layers, class-dimension cotangents: cfg2's h W2 and
+// h^T diag(s) dlogits): one warp per output row, lanes stride over K with
+// all N accumulators in registers, then a fixed-order shuffle reduction per
+// column -- a 64x64 tile would leave 84% of its lanes idle and still need
+// split-K for parallelism.
+template <int NMAX, bool KS>
+__global__ void __launch_bounds__(256) gemm_narrow_kernel(GemmArgs g) {
+  pdl_enter();
+  const int lane = threadIdx.x & 31;
+  const int64_t rows = g.batch * g.M;
+  const int64_t row = (int64_t)blockIdx.x * 8 + (threadIdx.x >> 5);
+  if (row >= rows) return;
+  const int64_t b = row / g.M, m = row - b * g.M;
+  const float* A = g.A + b * g.sab + m * g.sam;
+  const float* B = g.B + b * g.sbb;
+  float acc[NMAX];
+#pragma unroll
+  for (int j = 0; j < NMAX; ++j) acc[j] = 0.f;
+  // 4 k per lane per trip: all their loads are in flight together
+  int64_t k = lane;
+  for (; k + 96 < g.K; k += 128) {
+    float a[4];
+    float bv[4][NMAX];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int64_t ku = k + 32 * u;
+      a[u] = __ldg(A + ku * g.sak);
+      if (KS) a[u] *= __ldg(g.kscale + b * g.skb + ku * g.skk);
+#pragma unroll
+      for (int j = 0; j < NMAX; ++j) bv[u][j] = j < g.N ? __ldg(B + ku * g.sbk + j * g.sbn) : 0.f;
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u)
+#pragma unroll
+      for (int j = 0; j < NMAX; ++j) acc[j] = fmaf(a[u], bv[u][j], acc[j]);
+  }
+  for (; k < g.K; k += 32) {
+    float a = __ldg(A + k * g.sak);
+    if (KS) a *= __ldg(g.kscale + b * g.skb + k * g.skk);
+    const float* bk = B + k * g.sbk;
+#pragma unroll
+    for (int j = 0; j < NMAX; ++j)
+      if (j < g.N) acc[j] = fmaf(a, __ldg(bk + j * g.sbn), acc[j]);
+  }
+#pragma unroll
+  for (int j = 0; j < NMAX; ++j) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) acc[j] += __shfl_xor_sync(0xffffffffu, acc[j], o);
+  }
+  float v = 0.f;
+#pragma unroll
+  for (int j = 0; j < NMAX; ++j)
+    if (lane == j) v = acc[j];
+  if (lane < g.N) {
+    float* p = g.C + b * g.scb + m * g.scm + lane * g.scn;
+    float x = v * (g.alpha_rows ? g.alpha_rows[row] : 1.f);
+    if (g.accumulate) x += *p;
+    *p = epi_value(g, b, m, lane, x);
+  }
+}
+
+static int narrow_launch(const GemmArgs& g, cudaStream_t s) {
+  const int64_t rows = g.batch * g.M;
+  const int64_t blocks = (rows + 7) / 8;
+  if (blocks > 0x7fffffff) return PFB_E_UNSUPPORTED;
+  if (g.kscale) launch(gemm_narrow_kernel<16, true>, (unsigned)blocks, 256, 0, s, g);
+  else launch(gemm_narrow_kernel<16, false>, (unsigned)blocks, 256, 0, s, g);
+  return launch_status();
+}
+
 static int smallk_launch(const GemmArgs& g, cudaStream_t s) {
   const bool vec = g.K <= 16 && g.sbn == 1 && g.scn == 1 && g.N % 4 == 0 && g.sbk % 4 == 0 &&
                    g.sbb % 4 == 0 && g.scm % 4 == 0 && g.scb % 4 == 0 &&
@@ -392,6 +462,11 @@ static void launch_clustered(const GemmArgs& g, dim3 grid, int splits, int64_t k
 int gemm_simt(const GemmArgs& g, void* ws, int64_t ws_bytes, cudaStream_t s) {
   if (g.batch == 0 || g.M == 0 || g.N == 0) return 0;
   if (g.K <= 16) return smallk_launch(g, s);
+  // warp-per-row pays one K/128-long latency chain per row: measured ahead of
+  // the cluster split-K tile for short K or many rows (cfg2: 256x10x128
+  // 4.6 vs 5.2 us; 1000x3x77 3.3 vs 6.6 us; but 128x10x256 6.7 vs 5.4 us)
+  if (g.N <= 16 && (g.K <= 160 || g.batch * g.M >= 1024) && !getenv_flag("PFB_SIMT_NO_NARROW"))
+    return narrow_launch(g, s);
   int splits = simt_splits(g);
   const bool no_cluster = getenv_flag("PFB_SIMT_NO_CLUSTER");
   // the workspace path only when clusters cannot hold the splits (or are off)

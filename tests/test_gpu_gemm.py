@@ -320,3 +320,24 @@ def test_gemm_pair_batched_alpha_accumulate(env, force):
     got = _run(env, a, b, force, transpose_b=True, accumulate_into=c0, alpha=alpha)
     want = c0 + alpha.reshape(3, 300)[:, :, None] * (a @ b)
     np.testing.assert_allclose(got, want, rtol=RTOL, atol=ATOL)
+
+
+@pytest.mark.parametrize("shape", [(128, 10, 256), (256, 10, 128), (1000, 3, 77), (5, 16, 40),
+                                   (2, 64, 7, 300)])
+@pytest.mark.parametrize("a_mn", [False, True])
+def test_gemm_narrow_n(env, shape, a_mn):
+    """N <= 16 (logits / class-dim cotangents): warp-per-row SIMT kernel."""
+    m, n, k = shape[:3]
+    bsz = shape[3] if len(shape) > 3 else 1
+    if bsz > 1:
+        m, n, k = shape[1], shape[2], shape[3]
+    r = np.random.default_rng(m + 7 * n + k)
+    a_shape, b_shape = ((bsz, m, k), (bsz, k, n)) if bsz > 1 else ((m, k), (k, n))
+    a, b = _operands(r, a_shape, b_shape)
+    got = _run(env, a, b, 1, a_mn=a_mn and bsz == 1)
+    np.testing.assert_allclose(got, a @ b, rtol=RTOL, atol=ATOL)
+    c0 = _f32(r, got.shape)
+    alpha = np.asarray(r.standard_normal(bsz * m), np.float32).astype(np.float64)
+    got2 = _run(env, a, b, 1, accumulate_into=c0, alpha=alpha)
+    want2 = c0 + alpha.reshape(got.shape[:-1])[..., None] * (a @ b)
+    np.testing.assert_allclose(got2, want2, rtol=RTOL, atol=ATOL)
