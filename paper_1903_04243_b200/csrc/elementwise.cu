@@ -761,7 +761,9 @@ static int fused_impl(int32_t n_in, const pfb_tensor* ins, int32_t n_steps,
   const bool small = n < (int64_t)0x7fffffff;
   const int ir = L.rank - 1;
   static const bool scalar_only = getenv_flag("PFB_FUSED_SCALAR");
-  const bool v4 = L.shape[ir] % 4 == 0 && !scalar_only;
+  // tiny tensors (per-example scalars): one element per thread so the
+  // program's latency chain runs on 4x the warps
+  const bool v4 = L.shape[ir] % 4 == 0 && !scalar_only && n >= 4096;
   // per-operand feed mode; the outputs share operand 0's (all must be aligned)
   uint32_t modes = 0;
   for (int o = 0; o <= n_in; ++o) {
