@@ -319,21 +319,28 @@ __global__ void __launch_bounds__(256) outer1_kernel(GemmArgs g, int64_t rows_pe
 // column -- a 64x64 tile would leave 84% of its lanes idle and still need
 // split-K for parallelism.
 template <int NMAX, bool KS>
-__global__ void __launch_bounds__(256) gemm_narrow_kernel(GemmArgs g) {
+__global__ void __launch_bounds__(256) gemm_narrow_kernel(GemmArgs g, int wpr) {
+  // wpr warps per output row split K (each a contiguous K range); their
+  // partial sums meet in shared memory in warp order (deterministic)
   pdl_enter();
-  const int lane = threadIdx.x & 31;
+  __shared__ float part[8][NMAX];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int rows_per_block = 8 / wpr;
   const int64_t rows = g.batch * g.M;
-  const int64_t row = (int64_t)blockIdx.x * 8 + (threadIdx.x >> 5);
-  if (row >= rows) return;
-  const int64_t b = row / g.M, m = row - b * g.M;
+  const int64_t row = (int64_t)blockIdx.x * rows_per_block + w / wpr;
+  const int sub = w % wpr;
+  const bool live = row < rows;
+  const int64_t b = live ? row / g.M : 0, m = live ? row - b * g.M : 0;
+  const int64_t kchunk = (g.K + wpr - 1) / wpr;
+  const int64_t k0 = sub * kchunk, k1 = live ? min(g.K, k0 + kchunk) : 0;
   const float* A = g.A + b * g.sab + m * g.sam;
   const float* B = g.B + b * g.sbb;
   float acc[NMAX];
 #pragma unroll
   for (int j = 0; j < NMAX; ++j) acc[j] = 0.f;
   // 4 k per lane per trip: all their loads are in flight together
-  int64_t k = lane;
-  for (; k + 96 < g.K; k += 128) {
+  int64_t k = k0 + lane;
+  for (; k + 96 < k1; k += 128) {
     float a[4];
     float bv[4][NMAX];
 #pragma unroll
@@ -349,7 +356,7 @@ __global__ void __launch_bounds__(256) gemm_narrow_kernel(GemmArgs g) {
 #pragma unroll
       for (int j = 0; j < NMAX; ++j) acc[j] = fmaf(a[u], bv[u][j], acc[j]);
   }
-  for (; k < g.K; k += 32) {
+  for (; k < k1; k += 32) {
     float a = __ldg(A + k * g.sak);
     if (KS) a *= __ldg(g.kscale + b * g.skb + k * g.skk);
     const float* bk = B + k * g.sbk;
@@ -366,7 +373,13 @@ __global__ void __launch_bounds__(256) gemm_narrow_kernel(GemmArgs g) {
 #pragma unroll
   for (int j = 0; j < NMAX; ++j)
     if (lane == j) v = acc[j];
-  if (lane < g.N) {
+  if (wpr > 1) {
+    if (lane < NMAX) part[w][lane] = v;
+    __syncthreads();
+    if (sub != 0) return;
+    for (int q = 1; q < wpr; ++q) v += lane < NMAX ? part[w + q][lane] : 0.f;
+  }
+  if (live && lane < g.N) {
     float* p = g.C + b * g.scb + m * g.scm + lane * g.scn;
     float x = v * (g.alpha_rows ? g.alpha_rows[row] : 1.f);
     if (g.accumulate) x += *p;
@@ -376,10 +389,14 @@ __global__ void __launch_bounds__(256) gemm_narrow_kernel(GemmArgs g) {
 
 static int narrow_launch(const GemmArgs& g, cudaStream_t s) {
   const int64_t rows = g.batch * g.M;
-  const int64_t blocks = (rows + 7) / 8;
+  // warps per row: keep each warp's K range within ~128 (one unrolled trip)
+  // while there are few rows to spread over the SMs
+  int wpr = 1;
+  while (wpr < 8 && g.K > 128 * wpr && rows * wpr < (int64_t)kNumSMs * 16) wpr *= 2;
+  const int64_t blocks = (rows * wpr + 7) / 8;
   if (blocks > 0x7fffffff) return PFB_E_UNSUPPORTED;
-  if (g.kscale) launch(gemm_narrow_kernel<16, true>, (unsigned)blocks, 256, 0, s, g);
-  else launch(gemm_narrow_kernel<16, false>, (unsigned)blocks, 256, 0, s, g);
+  if (g.kscale) launch(gemm_narrow_kernel<16, true>, (unsigned)blocks, 256, 0, s, g, wpr);
+  else launch(gemm_narrow_kernel<16, false>, (unsigned)blocks, 256, 0, s, g, wpr);
   return launch_status();
 }
 
@@ -462,10 +479,8 @@ static void launch_clustered(const GemmArgs& g, dim3 grid, int splits, int64_t k
 int gemm_simt(const GemmArgs& g, void* ws, int64_t ws_bytes, cudaStream_t s) {
   if (g.batch == 0 || g.M == 0 || g.N == 0) return 0;
   if (g.K <= 16) return smallk_launch(g, s);
-  // warp-per-row pays one K/128-long latency chain per row: measured ahead of
-  // the cluster split-K tile for short K or many rows (cfg2: 256x10x128
-  // 4.6 vs 5.2 us; 1000x3x77 3.3 vs 6.6 us; but 128x10x256 6.7 vs 5.4 us)
-  if (g.N <= 16 && (g.K <= 160 || g.batch * g.M >= 1024) && !getenv_flag("PFB_SIMT_NO_NARROW"))
+  // narrow N: warps per row (K split across up to 8 warps for few rows)
+  if (g.N <= 16 && !getenv_flag("PFB_SIMT_NO_NARROW"))
     return narrow_launch(g, s);
   int splits = simt_splits(g);
   const bool no_cluster = getenv_flag("PFB_SIMT_NO_CLUSTER");
