@@ -163,10 +163,20 @@ int pfb_row_dots(int32_t n, const pfb_tensor* xs, const pfb_tensor* ys, pfb_tens
  * PFB_ACT_* code.  Replaces the reference's matmul -> mul / add / tanh chain
  * (tensor.py:140-206). */
 enum pfb_act { PFB_ACT_NONE = 0, PFB_ACT_TANH = 1, PFB_ACT_SIGMOID = 2, PFB_ACT_RELU = 3 };
+/* derivative epilogues (autodiff.py tanh/sigmoid VJPs): out *= (1 - y^2) / y (1 - y) */
+enum pfb_dop { PFB_DOP_NONE = 0, PFB_DOP_DTANH = 1, PFB_DOP_DSIGMOID = 2 };
 int pfb_matmul_fused(const pfb_tensor* a, const pfb_tensor* b, pfb_tensor* out,
                      const pfb_tensor* kscale, const pfb_tensor* bias, int32_t act,
                      const float* alpha_rows, int32_t accumulate, int32_t force_path, void* ws,
                      int64_t ws_bytes, void* stream);
+/* pfb_matmul_fused plus a derivative epilogue: out *= (1 - y^2) (dop =
+ * PFB_DOP_DTANH) or y (1 - y) (PFB_DOP_DSIGMOID), y broadcast to out -- the
+ * cotangent multiply of the tanh / sigmoid VJPs (reference autodiff.py:106-111)
+ * applied to the GEMM that produces the cotangent. */
+int pfb_matmul_ep(const pfb_tensor* a, const pfb_tensor* b, pfb_tensor* out,
+                  const pfb_tensor* kscale, const pfb_tensor* bias, int32_t act,
+                  const pfb_tensor* dy, int32_t dop, const float* alpha_rows, int32_t accumulate,
+                  int32_t force_path, void* ws, int64_t ws_bytes, void* stream);
 
 /* device-resident while loops (csrc/loop.cu; reference interp.py:133-154 runs
  * the loop on the host): a CUDA graph with a conditional WHILE node.  The

@@ -57,6 +57,8 @@ _SIGNATURES = {
     "pfb_matmul_workspace": ([_P, _P, _P], ctypes.c_int64),
     "pfb_matmul": ([_P, _P, _P, _vp, _i64, _vp], ctypes.c_int),
     "pfb_matmul_ex": ([_P, _P, _P, _vp, _i32, _i32, _vp, _i64, _vp], ctypes.c_int),
+    "pfb_matmul_ep": ([_P, _P, _P, _P, _P, _i32, _P, _i32, _vp, _i32, _i32, _vp, _i64, _vp],
+                      ctypes.c_int),
     "pfb_matmul_dual_workspace": ([_P, _P, _P, _P, _P], ctypes.c_int64),
     "pfb_matmul_dual": ([_P, _P, _P, _P, _P, _P, _i32, _i32, _vp, _i64, _vp], ctypes.c_int),
     "pfb_concat": ([_i32, _P, _i32, _P, _vp], ctypes.c_int),

@@ -160,6 +160,15 @@ extern "C" int pfb_matmul_fused(const pfb_tensor* a, const pfb_tensor* b, pfb_te
                                 const pfb_tensor* kscale, const pfb_tensor* bias, int32_t act,
                                 const float* alpha_rows, int32_t accumulate, int32_t force_path,
                                 void* ws, int64_t ws_bytes, void* stream) {
+  return pfb_matmul_ep(a, b, out, kscale, bias, act, nullptr, PFB_DOP_NONE, alpha_rows, accumulate,
+                       force_path, ws, ws_bytes, stream);
+}
+
+extern "C" int pfb_matmul_ep(const pfb_tensor* a, const pfb_tensor* b, pfb_tensor* out,
+                             const pfb_tensor* kscale, const pfb_tensor* bias, int32_t act,
+                             const pfb_tensor* dy, int32_t dop, const float* alpha_rows,
+                             int32_t accumulate, int32_t force_path, void* ws, int64_t ws_bytes,
+                             void* stream) {
   GemmArgs g;
   if (int e = matmul_args(a, b, out, &g)) return e;
   g.alpha_rows = alpha_rows;
@@ -187,6 +196,16 @@ extern "C" int pfb_matmul_fused(const pfb_tensor* a, const pfb_tensor* b, pfb_te
       g.skb = 0; g.skk = st[0];
     }
     g.kscale = (const float*)kscale->data;
+  }
+  if (dop < PFB_DOP_NONE || dop > PFB_DOP_DSIGMOID || (dop && dy == nullptr)) return PFB_E_ARG;
+  if (dop) {
+    if (dy->dtype != PFB_F32) return PFB_E_DTYPE;
+    int64_t st[3];
+    if (!broadcast_strides(dy, out->rank, out->shape, st)) return PFB_E_SHAPE;
+    g.dy = (const float*)dy->data;
+    g.dop = dop;
+    if (batched) { g.sdb = st[0]; g.sdm = st[1]; g.sdn = st[2]; }
+    else { g.sdb = 0; g.sdm = st[0]; g.sdn = st[1]; }
   }
   if (g.K == 0 && (g.has_epi() || g.kscale)) return PFB_E_UNSUPPORTED;
   return matmul_impl(g, out, force_path, ws, ws_bytes, stream);

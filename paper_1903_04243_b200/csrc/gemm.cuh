@@ -22,8 +22,19 @@ struct GemmArgs {
   const float* bias = nullptr;    // nullable, broadcast to (batch, M, N) by strides
   int64_t sxb = 0, sxm = 0, sxn = 0;
   int act = 0;                    // PFB_ACT_*
-  __host__ __device__ bool has_epi() const { return bias != nullptr || act != 0; }
+  // derivative epilogue (autodiff's tanh'/sigmoid' cotangent multiply):
+  //   C *= (1 - y^2)  [PFB_DOP_DTANH]   or   C *= y (1 - y)  [PFB_DOP_DSIGMOID]
+  const float* dy = nullptr;      // y, broadcast to (batch, M, N) by strides
+  int64_t sdb = 0, sdm = 0, sdn = 0;
+  int dop = 0;
+  __host__ __device__ bool has_epi() const { return bias != nullptr || act != 0 || dop != 0; }
 };
+
+// the derivative factor of the epilogue at (b, m, n)
+__device__ __forceinline__ float dop_factor(int dop, const float* dy, int64_t off) {
+  const float y = __ldg(dy + off);
+  return dop == PFB_DOP_DTANH ? 1.f - y * y : y * (1.f - y);
+}
 
 __device__ __forceinline__ float apply_act(int act, float v) {
   switch (act) {
@@ -38,7 +49,9 @@ __device__ __forceinline__ float apply_act(int act, float v) {
 __device__ __forceinline__ float epi_value(const GemmArgs& g, int64_t b, int64_t m, int64_t n,
                                            float v) {
   if (g.bias) v += __ldg(g.bias + b * g.sxb + m * g.sxm + n * g.sxn);
-  return apply_act(g.act, v);
+  v = apply_act(g.act, v);
+  if (g.dop) v *= dop_factor(g.dop, g.dy, b * g.sdb + m * g.sdm + n * g.sdn);
+  return v;
 }
 
 __device__ __forceinline__ float kscale_at(const GemmArgs& g, int64_t b, int64_t k) {

@@ -70,6 +70,9 @@ struct PParams {
   int act;
   int tma_store;
   int chunk_kb;
+  const float* dy;  // derivative epilogue (GemmArgs::dop)
+  int64_t sdb, sdm, sdn;
+  int dop;
 };
 
 __device__ __forceinline__ void mbar_wait_cluster(uint64_t* bar, uint32_t parity) {
@@ -126,13 +129,16 @@ __device__ __forceinline__ void load_operand(const CUtensorMap* mh, const CUtens
 }
 
 __device__ __forceinline__ void epi4(const PParams& p, int bz, int row, int col, float4& v) {
-  if (p.bias == nullptr && p.act == 0) return;
+  if (p.bias == nullptr && p.act == 0 && p.dop == 0) return;
   float e[4] = {v.x, v.y, v.z, v.w};
 #pragma unroll
   for (int j = 0; j < 4; ++j) {
     if (p.bias && col + j < p.N)
       e[j] += __ldg(p.bias + (int64_t)bz * p.sxb + (int64_t)row * p.sxm + (int64_t)(col + j) * p.sxn);
     e[j] = apply_act(p.act, e[j]);
+    if (p.dop && col + j < p.N)
+      e[j] *= dop_factor(p.dop, p.dy,
+                         (int64_t)bz * p.sdb + (int64_t)row * p.sdm + (int64_t)(col + j) * p.sdn);
   }
   v = make_float4(e[0], e[1], e[2], e[3]);
 }
@@ -633,7 +639,8 @@ int gemm_tcgen05_pair(const GemmArgs& g, void* ws, int64_t ws_bytes, cudaStream_
   PParams p{(int)g.M, (int)g.N, (int)Kp, (int)g.batch,
             (int)((g.M + 255) / 256), (int)((g.N + bn - 1) / bn), a_bc, b_bc, am, bm, idesc,
             g.C, g.scb, g.scm, g.scn, g.alpha_rows, g.accumulate,
-            g.bias, g.sxb, g.sxm, g.sxn, g.act, tma_store, pair_chunk()};
+            g.bias, g.sxb, g.sxm, g.sxn, g.act, tma_store, pair_chunk(), g.dy, g.sdb, g.sdm,
+            g.sdn, g.dop};
   if (single)
     return bn == 256 ? launch_pair<256, true>(mah, mal, mbh, mbl, mc, p, s)
                      : launch_pair<128, true>(mah, mal, mbh, mbl, mc, p, s);

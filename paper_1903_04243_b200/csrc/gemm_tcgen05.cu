@@ -133,6 +133,9 @@ struct Params {
   int nk1;
   int a_mode2, b_mode2, a_bcast2, b_bcast2;
   uint32_t idesc2;
+  const float* dy;  // derivative epilogue (GemmArgs::dop)
+  int64_t sdb, sdm, sdn;
+  int dop;
 };
 
 __device__ __forceinline__ void stamp(const Params& p, int i) {
@@ -144,13 +147,16 @@ __device__ __forceinline__ void stamp(const Params& p, int i) {
 }
 
 __device__ __forceinline__ void epi4(const Params& p, int bz, int row, int col, float4& v) {
-  if (p.bias == nullptr && p.act == 0) return;
+  if (p.bias == nullptr && p.act == 0 && p.dop == 0) return;
   float e[4] = {v.x, v.y, v.z, v.w};
 #pragma unroll
   for (int j = 0; j < 4; ++j) {
     if (p.bias && col + j < p.N)
       e[j] += __ldg(p.bias + (int64_t)bz * p.sxb + (int64_t)row * p.sxm + (int64_t)(col + j) * p.sxn);
     e[j] = apply_act(p.act, e[j]);
+    if (p.dop && col + j < p.N)
+      e[j] *= dop_factor(p.dop, p.dy,
+                         (int64_t)bz * p.sdb + (int64_t)row * p.sdm + (int64_t)(col + j) * p.sdn);
   }
   v = make_float4(e[0], e[1], e[2], e[3]);
 }
@@ -783,7 +789,7 @@ static int launch_gemm(const GemmArgs& g, const PairFeed& f1, const PairFeed* f2
            (int)((g.M + BM - 1) / BM), (int)((g.N + BN - 1) / BN), f1.a_bc, f1.b_bc, f1.am, f1.bm,
            idesc_of(f1), g.C, g.scb, g.scm, g.scn, g.alpha_rows, g.accumulate, ksplit, kb_per,
            g.bias, g.sxb, g.sxm, g.sxn, g.act, 4096u, 512u, tma_store, tc_trace_buffer(),
-           nk1, q.am, q.bm, q.a_bc, q.b_bc, idesc_of(q)};
+           nk1, q.am, q.bm, q.a_bc, q.b_bc, idesc_of(q), g.dy, g.sdb, g.sdm, g.sdn, g.dop};
   const int64_t units = (int64_t)p.ntm * p.ntn * g.batch * ksplit;
   if (ksplit > 1) {
     // one CTA per (tile, k-split); the k-splits of a tile are one cluster

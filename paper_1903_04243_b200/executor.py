@@ -1188,19 +1188,22 @@ def _h_row_dots(ex, node, ins):
 
 def _h_matmul_ep(ex, node, ins):
     """matmul_ep (passes.fuse_matmul_epilogues): one GEMM launch computing
-    act(a @ diag(kscale) @ b + bias) -- prologue scale and epilogue in the
-    kernel (pfb_matmul_fused)."""
+    act(a @ diag(kscale) @ b + bias) [* dtanh(y) | * dsigmoid(y)] -- prologue
+    scale and epilogue in the kernel (pfb_matmul_ep)."""
     import ctypes
     at = node.attrs
     vals = [ex._dev(v) for v in ins]
     a, b = vals[0], vals[1]
     k = 2
-    ks = bias = None
+    ks = bias = dy = None
     if at.get("has_kscale"):
         ks = vals[k]
         k += 1
     if at.get("has_bias"):
         bias = vals[k]
+        k += 1
+    if at.get("dop"):
+        dy = vals[k]
     if a.rank == 2:
         shape = (a.shape[0], b.shape[1])
     else:
@@ -1210,14 +1213,19 @@ def _h_matmul_ep(ex, node, ins):
     ad, bd, od = a.desc(), b.desc(), out.desc()
     kd = ks.desc() if ks is not None else None
     xd = bias.desc() if bias is not None else None
+    yd = dy.desc() if dy is not None else None
     need = ex._lib.pfb_matmul_workspace(ad, bd, od)
     wp, wn = ex._ws_get(need) if need > 0 else (None, 0)
-    ex._call(ex._lib.pfb_matmul_fused, ad, bd, od,
+    ex._call(ex._lib.pfb_matmul_ep, ad, bd, od,
              ctypes.byref(kd) if kd is not None else None,
              ctypes.byref(xd) if xd is not None else None, _ACT_CODE[at.get("act")],
+             ctypes.byref(yd) if yd is not None else None, _DOP_CODE[at.get("dop")],
              None, 0, 0, wp, wn, ex._stream, what="matmul",
              work=(_abytes(*[v for v in vals] + [out]), flops))
     return [out]
+
+
+_DOP_CODE = {None: 0, "dtanh": 1, "dsigmoid": 2}
 
 
 def _h_matmul2(ex, node, ins):

@@ -269,6 +269,34 @@ def fuse_matmul_epilogues(g, keep=()):
     return count, rw.replaced
 
 
+def _const_is(g, key, value):
+    n = g.nodes[key[0]]
+    if n.kind != "constant" or key[1] != 0:
+        return False
+    v = n.attrs["value"]
+    return v.rank == 0 and float(v.data) == value
+
+
+def _dop_pattern(g, key):
+    """("dtanh", y) for sub(1, mul(y, y)); ("dsigmoid", y) for mul(y, sub(1, y))
+    (either operand order) -- the cotangent factors autodiff emits for the
+    tanh / sigmoid VJPs (autodiff.py, reference autodiff.py:108-111)."""
+    n = g.nodes[key[0]]
+    if key[1] != 0:
+        return None
+    if n.kind == "sub" and _const_is(g, n.inputs[0], 1.0):
+        m = g.nodes[n.inputs[1][0]]
+        if m.kind == "mul" and n.inputs[1][1] == 0 and tuple(m.inputs[0]) == tuple(m.inputs[1]):
+            return "dtanh", tuple(m.inputs[0])
+    if n.kind == "mul":
+        for j in (0, 1):
+            sn = g.nodes[n.inputs[1 - j][0]]
+            if (sn.kind == "sub" and n.inputs[1 - j][1] == 0 and _const_is(g, sn.inputs[0], 1.0)
+                    and tuple(sn.inputs[1]) == tuple(n.inputs[j])):
+                return "dsigmoid", tuple(n.inputs[j])
+    return None
+
+
 def _strip_units(shape):
     return tuple(d for d in shape if d != 1)
 
@@ -299,6 +327,7 @@ def _f5(rw, node):
     key = (node.id, 0)
     end = key
     bias = act = None
+    dop = dy = None
     while True:
         us = rw.users().get(key, [])
         if len(us) != 1 or key in rw.keep:
@@ -308,7 +337,10 @@ def _f5(rw, node):
         if osh is None or None in osh:
             break
         if un.kind == "reshape":
-            if _strip_units(osh) != _strip_units(sm) or not osh or osh[-1] != n_cols:
+            unfold = (len(osh) == 3 and len(sm) == 2 and osh[0] * osh[1] == sm[0]
+                      and osh[2] == sm[1])  # the fold path's [n*x, z] -> [n, x, z]
+            if not unfold and (_strip_units(osh) != _strip_units(sm) or not osh
+                               or osh[-1] != n_cols):
                 break
             key = (un.id, 0)
             continue
@@ -328,9 +360,33 @@ def _f5(rw, node):
             act = un.kind
             key = end = (un.id, 0)
             continue
+        if un.kind == "mul" and dop is None and not dual and tuple(osh) == tuple(g.ref_shape(key)):
+            pat = _dop_pattern(g, tuple(un.inputs[1 - idx]))
+            if pat is not None and g.ref_dtype(pat[1]) == g.ref_dtype(key):
+                ysh = g.ref_shape(pat[1])
+                if ysh is not None and None not in ysh and len(ysh) <= len(osh) and all(
+                        a in (1, o) for a, o in zip(ysh[::-1], tuple(osh)[::-1])):
+                    dop, dy = pat[0], Ref(g, *pat[1])
+                    end_before_dop = end
+                    key = end = (un.id, 0)
+                    continue
         break
-    if kscale is None and bias is None and act is None:
+    if kscale is None and bias is None and act is None and dop is None:
         return 0
+    esh = tuple(g.ref_shape(end))
+    if dop is not None:
+        # the epilogue addresses y in the GEMM's output coordinates
+        ysh = tuple(g.ref_shape(tuple((dy.nid, dy.port))))
+        ypad = (1,) * (len(esh) - len(ysh)) + ysh
+        if _strip_units(esh) == _strip_units(sm) and len(sm) == len(_strip_units(sm)):
+            keep_ax = [i for i, d in enumerate(esh) if d != 1]
+            dy = b.reshape(dy, [ypad[i] for i in keep_ax] or [1])
+        else:  # y does not map onto the GEMM's output rows: stop before the mul
+            dop = dy = None
+            end = end_before_dop
+            if kscale is None and bias is None and act is None:
+                return 0
+            esh = tuple(g.ref_shape(end))
     if dual:
         ins = [A, B, Ref(g, *node.inputs[2]), Ref(g, *node.inputs[3])] + (
             [bias] if bias is not None else [])
@@ -338,13 +394,12 @@ def _f5(rw, node):
                          {"act": act, "has_bias": bias is not None})
     else:
         ins = [A, B] + ([kscale] if kscale is not None else []) + (
-            [bias] if bias is not None else [])
+            [bias] if bias is not None else []) + ([dy] if dy is not None else [])
         new = g.add_node("matmul_ep", [(r.nid, r.port) for r in ins],
                          {"act": act, "has_kscale": kscale is not None,
-                          "has_bias": bias is not None})
+                          "has_bias": bias is not None, "dop": dop})
     out = Ref(g, new.id, 0)
-    esh = g.ref_shape(end)
-    if tuple(esh) != tuple(sm):
+    if tuple(esh) != tuple(g.ref_shape((new.id, 0))):
         out = b.reshape(out, list(esh))
     rw.redirect(end, out)
     return 1

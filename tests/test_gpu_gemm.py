@@ -341,3 +341,32 @@ def test_gemm_narrow_n(env, shape, a_mn):
     got2 = _run(env, a, b, 1, accumulate_into=c0, alpha=alpha)
     want2 = c0 + alpha.reshape(got.shape[:-1])[..., None] * (a @ b)
     np.testing.assert_allclose(got2, want2, rtol=RTOL, atol=ATOL)
+
+
+@pytest.mark.parametrize("force", [1, 3, 4, 5])
+@pytest.mark.parametrize("dop", [1, 2])
+def test_matmul_derivative_epilogue(env, force, dop):
+    """pfb_matmul_ep: out = (a @ b + bias) * (1 - y^2) | * y (1 - y), y broadcast."""
+    import ctypes
+    torch, lib, DArray, DType = env
+    dev = torch.device("cuda")
+    r = np.random.default_rng(40 + dop)
+    m, n, k = (300, 256, 96) if force != 1 else (128, 10, 64)
+    a, b = _operands(r, (m, k), (k, n))
+    y = np.tanh(_f32(r, (m, n)))
+    bias = _f32(r, (n,))
+    z = a @ b + bias
+    want = z * (1.0 - y * y) if dop == 1 else z * y * (1.0 - y)
+    A = DArray.from_numpy(a, DType.F64, dev)
+    B = _tview(DArray, DType, dev, b)
+    Y = DArray.from_numpy(y, DType.F64, dev)
+    X = DArray.from_numpy(bias, DType.F64, dev)
+    C = DArray.empty((m, n), DType.F64, dev)
+    ad, bd, cd, yd, xd = A.desc(), B.desc(), C.desc(), Y.desc(), X.desc()
+    need = lib.pfb_matmul_workspace(ad, bd, cd)
+    ws = torch.empty(max(need, 256), dtype=torch.uint8, device=dev)
+    rc = lib.pfb_matmul_ep(ad, bd, cd, None, ctypes.byref(xd), 0, ctypes.byref(yd), dop, None, 0,
+                           force, ws.data_ptr(), ws.numel(), torch.cuda.current_stream().cuda_stream)
+    assert rc == 0, rc
+    torch.cuda.synchronize()
+    np.testing.assert_allclose(C.to_numpy().astype(np.float64), want, rtol=RTOL, atol=ATOL)

@@ -202,3 +202,16 @@ def test_f3_integer_domain_groups():
                     out.extend(kinds(sg))
         return out
     assert "fused_int" in kinds(g2)
+
+
+def test_f5_derivative_epilogue():
+    """The tanh VJP's cotangent multiply cot * (1 - y^2) rides on the GEMM
+    that produces cot (cfg2's dlogits W2^T; cfg3's backprop chain)."""
+    w = WL.cfg2(WL.this_api(), n=6, model="mlp", d_h=16)
+    g, g2, m = _run_both(w)
+    live = _kinds(g2, [m[tuple(o)] for o in g.outputs])
+    assert any(n.kind == "matmul_ep" and n.attrs.get("dop") == "dtanh" for n in live)
+    w3 = WL.cfg3(WL.this_api(), width=16, out_dim=8)
+    g, g3, m3 = _run_both(w3)
+    live3 = _kinds(g3, [m3[tuple(o)] for o in g.outputs])
+    assert any(n.kind == "matmul_ep" and n.attrs.get("dop") == "dtanh" for n in live3)
