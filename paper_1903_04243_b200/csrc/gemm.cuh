@@ -72,6 +72,8 @@ int64_t gemm_tcgen05_workspace(const GemmArgs& g);
 int gemm_tcgen05_dual(const GemmArgs& g1, const GemmArgs& g2, void* ws, int64_t ws_bytes,
                       cudaStream_t s, int variant = 0, int ksplit_want = 0);
 int64_t gemm_tcgen05_dual_workspace(const GemmArgs& g1, const GemmArgs& g2);
+// PFB_TC_TRACE=1: 16-slot globaltimer stamp buffer (device), else nullptr
+unsigned long long* tc_trace_buffer();
 bool gemm_tcgen05_eligible(const GemmArgs& g);    // layout constraints
 bool gemm_tcgen05_raw_possible(const GemmArgs& g);
 bool gemm_tcgen05_profitable(const GemmArgs& g);  // size heuristic for auto

@@ -73,7 +73,16 @@ struct PParams {
   const float* dy;  // derivative epilogue (GemmArgs::dop)
   int64_t sdb, sdm, sdn;
   int dop;
+  unsigned long long* trace;  // PFB_TC_TRACE stamps of CTA 0 (bring-up)
 };
+
+__device__ __forceinline__ void pstamp(const PParams& p, int i) {
+  if (p.trace != nullptr && blockIdx.x == 0) {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    p.trace[i] = t;
+  }
+}
 
 __device__ __forceinline__ void mbar_wait_cluster(uint64_t* bar, uint32_t parity) {
   uint32_t addr = smem_u32(bar);
@@ -150,6 +159,7 @@ pair_kernel(const __grid_constant__ CUtensorMap map_ah, const __grid_constant__ 
             const __grid_constant__ CUtensorMap map_c, PParams p) {
   using C = Cfg<BN>;
   constexpr int STAGES = C::STAGES, BNH = C::BNH, EPI_COLS = C::EPI_COLS;
+  if (threadIdx.x == 0) pstamp(p, 0);
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>(
       (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -201,6 +211,7 @@ pair_kernel(const __grid_constant__ CUtensorMap map_ah, const __grid_constant__ 
   asm volatile("tcgen05.fence::after_thread_sync;");
   const uint32_t tmem_base = *tmem_slot;
   pdl_enter();  // prologue above overlaps the previous kernel (PDL)
+  if (threadIdx.x == 0) pstamp(p, 1);
 
   const int bytes_a = (p.a_mode == kPreSplit ? 2 : 1) * A_BYTES;
   const int bytes_b = (p.b_mode == kPreSplit ? 2 : 1) * C::B_BYTES;
@@ -219,6 +230,7 @@ pair_kernel(const __grid_constant__ CUtensorMap map_ah, const __grid_constant__ 
           mbar_expect_tx(&full[s], bytes_a + bytes_b);
           load_operand(&map_ah, &map_al, p.a_mode, &full[s], tile(s, 0), tile(s, 1), kb, m0, za, 128);
           load_operand(&map_bh, &map_bl, p.b_mode, &full[s], tile(s, 2), tile(s, 3), kb, n0, zb, BNH);
+          if (g == 0) pstamp(p, 2);
         }
       }
     }
@@ -259,6 +271,7 @@ pair_kernel(const __grid_constant__ CUtensorMap map_ah, const __grid_constant__ 
               // dropped lo*lo term sign-biased, so it is kept
               if (lo_lo) mma_tf32_pair(tmem_d, a_lo + da, b_lo + db, p.idesc, 1u);
             }
+            if (g == 0) pstamp(p, 3);
             mma_commit_pair(&empty[s]);
           }
           mma_commit_pair(&acc_full[buf]);
@@ -419,6 +432,7 @@ pair_kernel(const __grid_constant__ CUtensorMap map_ah, const __grid_constant__ 
           if (cc + 32 >= EPI_COLS) release(buf);  // all of this buffer is in registers
           emit32(f, bz, row0, n0 + half * EPI_COLS + cc, alpha);
         }
+        if (et == 0 && gc < 8) pstamp(p, 4 + gc);
         ++gc;
       };
       for (int u = pair; u < units; u += npairs) drain_store(u);
@@ -463,6 +477,7 @@ pair_kernel(const __grid_constant__ CUtensorMap map_ah, const __grid_constant__ 
   }
   asm volatile("tcgen05.fence::before_thread_sync;");
   __syncthreads();
+  if (threadIdx.x == 0) pstamp(p, 12);
   cluster_sync_all();  // no CTA leaves while its peer may still arrive on its barriers
   if (warp == 1) {
     asm volatile("tcgen05.fence::after_thread_sync;");
@@ -640,7 +655,7 @@ int gemm_tcgen05_pair(const GemmArgs& g, void* ws, int64_t ws_bytes, cudaStream_
             (int)((g.M + 255) / 256), (int)((g.N + bn - 1) / bn), a_bc, b_bc, am, bm, idesc,
             g.C, g.scb, g.scm, g.scn, g.alpha_rows, g.accumulate,
             g.bias, g.sxb, g.sxm, g.sxn, g.act, tma_store, pair_chunk(), g.dy, g.sdb, g.sdm,
-            g.sdn, g.dop};
+            g.sdn, g.dop, tc_trace_buffer()};
   if (single)
     return bn == 256 ? launch_pair<256, true>(mah, mal, mbh, mbl, mc, p, s)
                      : launch_pair<128, true>(mah, mal, mbh, mbl, mc, p, s);

@@ -14,6 +14,8 @@ from paper_1903_04243_b200 import _native as N  # noqa: E402
 from paper_1903_04243_b200.executor import DArray  # noqa: E402
 from paper_1903_04243_b200.tensor import DType  # noqa: E402
 
+PAIR_NAMES = ["entry", "pdl_done", "tma0_issued", "mma0_issued", "tile0_out", "tile1_out",
+              "tile2_out", "tile3_out", "tile4_out", "tile5_out", "tile6_out", "tile7_out", "cta_done"]
 NAMES = ["entry", "pdl_done", "prologue", "tma0_issued", "stage0_landed", "mma0_issued",
          "last_commit", "acc0_ready", "epilogue_done", "cta_done", "tmem_freed"]
 
@@ -46,8 +48,9 @@ def main():
         torch.cuda.synchronize()
         lib.pfb_debug_tc_trace(buf)
         t0 = buf[0]
+        names = PAIR_NAMES if args.force in (5, 6) else NAMES
         print(f"rep {rep} rc={rc}: " + "  ".join(
-            f"{nm}={(buf[i] - t0) / 1e3:.2f}" for i, nm in enumerate(NAMES) if buf[i]))
+            f"{nm}={(buf[i] - t0) / 1e3:.2f}" for i, nm in enumerate(names) if buf[i] and buf[i] >= t0))
 
 
 if __name__ == "__main__":
