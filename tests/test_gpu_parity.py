@@ -308,7 +308,7 @@ def test_replayed_results_stay_valid(Executor):
         res = ex.run(feeds[i % 3])
         for a, b in zip(res, want[i % 3]):
             np.testing.assert_allclose(a.data, b.data, rtol=1e-6, atol=1e-7)
-    assert len(cap.host_pack["slots"]) == n_slots == ex._IO_SLOTS + 1
+    assert len(cap.host_pack["slots"]) == n_slots <= ex._IO_SLOTS + 1
 
 
 def test_replayed_graph_errors_raise_once(Executor):
