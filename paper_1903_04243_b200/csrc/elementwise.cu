@@ -184,6 +184,47 @@ __global__ void __launch_bounds__(256) ew_scalar_kernel(Layout L, IdxT n, Tout* 
   }
 }
 
+// One-input op whose input is transposed relative to its output (a
+// materialised transpose, or a unary / cast of one): 32x32 tiles through
+// shared memory over (p, last), p = the input's unit-stride dim, so both the
+// input reads (lanes along p) and the output writes (lanes along last) are
+// coalesced.  Other dims are the batch (blockIdx.y, grid-stride).
+template <typename Tin, typename Tout, typename F>
+__global__ void __launch_bounds__(256) ew_tile_transpose(Layout L, int p, int64_t nbatch,
+                                                         int64_t tiles_last, Tout* out,
+                                                         const Tin* in, F f) {
+  pdl_enter();
+  __shared__ Tin t[32][33];
+  const int last = L.rank - 1;
+  const int64_t tl = blockIdx.x % tiles_last, tp = blockIdx.x / tiles_last;
+  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
+  for (int64_t bi = blockIdx.y; bi < nbatch; bi += gridDim.y) {
+    int64_t rem = bi, ob = 0, ib = 0;
+    for (int d = last; d >= 0; --d) {
+      if (d == p || d == last) continue;
+      const int64_t c = rem % L.shape[d];
+      rem /= L.shape[d];
+      ob += c * L.st[0][d];
+      ib += c * L.st[1][d];
+    }
+#pragma unroll
+    for (int j = ty; j < 32; j += 8) {
+      const int64_t ip = tp * 32 + tx, il = tl * 32 + j;
+      if (ip < L.shape[p] && il < L.shape[last]) t[j][tx] = in[ib + ip * L.st[1][p] + il * L.st[1][last]];
+    }
+    __syncthreads();
+#pragma unroll
+    for (int j = ty; j < 32; j += 8) {
+      const int64_t ip = tp * 32 + j, il = tl * 32 + tx;
+      if (ip < L.shape[p] && il < L.shape[last]) {
+        const Tin x = t[tx][j];
+        out[ob + ip * L.st[0][p] + il * L.st[0][last]] = f(x, x);
+      }
+    }
+    __syncthreads();
+  }
+}
+
 // Host launcher: `L` over (out, a[, b]); picks the vector path when the inner
 // dim allows it.
 template <typename Tin, typename Tout, int NIN, typename F>
@@ -192,6 +233,21 @@ int launch_ew(const Layout& L, void* out, const void* a, const void* b, F f, cud
   for (int d = 0; d < L.rank; ++d) n *= L.shape[d];
   if (n == 0) return 0;
   const int last = L.rank - 1;
+  if (NIN == 1 && L.rank >= 2 && L.st[0][last] == 1 && L.st[1][last] != 1 && n >= 4096) {
+    int p = -1;
+    for (int d = 0; d < last; ++d)
+      if (L.st[1][d] == 1 && L.shape[d] > 1) p = d;
+    if (p >= 0) {
+      const int64_t tiles_last = (L.shape[last] + 31) / 32, tiles_p = (L.shape[p] + 31) / 32;
+      int64_t nbatch = n / (L.shape[last] * L.shape[p]);
+      if (tiles_last * tiles_p <= 0x7fffffff) {
+        const unsigned gy = (unsigned)std::min<int64_t>(nbatch, 65535);
+        launch(ew_tile_transpose<Tin, Tout, F>, dim3((unsigned)(tiles_last * tiles_p), gy), 256,
+               0, s, L, p, nbatch, tiles_last, (Tout*)out, (const Tin*)a, f);
+        return launch_status();
+      }
+    }
+  }
   bool vec_dim = (L.shape[last] % 4) == 0;
   unsigned vecmask = 0;
   if (vec_dim) {
@@ -928,6 +984,77 @@ __global__ void __launch_bounds__(256) concat_thin_kernel(ThinCat d, T* out) {
   }
 }
 
+// Concat of dense inputs into a dense output: each input is a [rows, inner_j]
+// block copied into columns [off_j, off_j + inner_j) of the [rows, inner]
+// output -- 16-byte loads/stores when every width and offset allows it
+// (the generic kernel decodes every element's coordinates instead).
+struct RowCat {
+  int n;
+  int64_t rows, inner;
+  const void* x[kMaxCat];
+  int64_t w[kMaxCat], off[kMaxCat];
+};
+
+template <typename T, int V>
+__global__ void __launch_bounds__(256) concat_rows_kernel(RowCat d, T* out) {
+  pdl_enter();
+  const int j = blockIdx.y;
+  const int64_t wv = d.w[j] / V, total = d.rows * wv;
+  const T* x = reinterpret_cast<const T*>(d.x[j]);
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t r = i / wv, c = i - r * wv;
+    if constexpr (V == 4 && sizeof(T) == 4) {
+      *reinterpret_cast<float4*>(out + r * d.inner + d.off[j] + 4 * c) =
+          __ldg(reinterpret_cast<const float4*>(x + r * d.w[j] + 4 * c));
+    } else {
+      out[r * d.inner + d.off[j] + c] = __ldg(x + r * d.w[j] + c);
+    }
+  }
+}
+
+static bool concat_rows(int32_t n, const pfb_tensor* xs, int32_t axis, pfb_tensor* out,
+                        cudaStream_t s) {
+  if (!is_dense(out) || n > kMaxCat) return false;
+  RowCat d;
+  d.n = n;
+  d.rows = 1;
+  for (int i = 0; i < axis; ++i) d.rows *= out->shape[i];
+  d.inner = 1;
+  for (int i = axis; i < out->rank; ++i) d.inner *= out->shape[i];
+  int64_t post = 1;
+  for (int i = axis + 1; i < out->rank; ++i) post *= out->shape[i];
+  bool v4 = out->dtype == PFB_F32 && (reinterpret_cast<uintptr_t>(out->data) & 15) == 0 &&
+            d.inner % 4 == 0;
+  int64_t off = 0, most = 0;
+  for (int j = 0; j < n; ++j) {
+    const pfb_tensor* x = &xs[j];
+    if (x->dtype != out->dtype || x->rank != out->rank || !is_dense(x)) return false;
+    for (int i = 0; i < out->rank; ++i)
+      if (i != axis && x->shape[i] != out->shape[i]) return false;
+    d.x[j] = x->data;
+    d.w[j] = x->shape[axis] * post;
+    d.off[j] = off;
+    off += d.w[j];
+    most = std::max(most, d.rows * d.w[j]);
+    v4 = v4 && d.w[j] % 4 == 0 && d.off[j] % 4 == 0 &&
+         (reinterpret_cast<uintptr_t>(x->data) & 15) == 0;
+  }
+  if (off != d.inner || most == 0) return off == d.inner;
+  const int gx = grid_for(v4 ? most / 4 : most, 256, 4);
+  dim3 grid((unsigned)gx, (unsigned)n);
+  if (v4) {
+    launch(concat_rows_kernel<float, 4>, grid, 256, 0, s, d, (float*)out->data);
+  } else {
+    switch (out->dtype) {
+      case PFB_F32: launch(concat_rows_kernel<float, 1>, grid, 256, 0, s, d, (float*)out->data); break;
+      case PFB_I64: launch(concat_rows_kernel<int64_t, 1>, grid, 256, 0, s, d, (int64_t*)out->data); break;
+      default: launch(concat_rows_kernel<uint8_t, 1>, grid, 256, 0, s, d, (uint8_t*)out->data); break;
+    }
+  }
+  return true;
+}
+
 // leading dims [0, rank-1) of a view collapsed into one stride, or -1
 static int64_t collapse_rows(const pfb_tensor* t, int rank) {
   int64_t st = -1, expect = -1;
@@ -990,6 +1117,7 @@ extern "C" int pfb_concat(int32_t n, const pfb_tensor* xs, int32_t axis, pfb_ten
   if (axis < 0 || axis >= rank) return PFB_E_ARG;
   cudaStream_t s = as_stream(stream);
   if (concat_thin(n, xs, axis, out, s)) return launch_status();
+  if (concat_rows(n, xs, axis, out, s)) return launch_status();
   int64_t off = 0;
   for (int base = 0; base < n; base += kMaxCat) {
     CatDesc d;

@@ -100,6 +100,30 @@ __global__ void __launch_bounds__(256) reduce_inner_warp(RedDesc D, int64_t K, i
     if (D.rr == 1) {  // single collapsed reduced dim: no index decode per element
       const T* p = x + base;
       const int64_t s = D.rst[0];
+      if constexpr (std::is_same<T, float>::value) {
+        // contiguous float row: 16-byte loads, 4 independent compensated sums
+        const T* q = PROD ? y + basey : nullptr;
+        const bool vec = s == 1 && (reinterpret_cast<uintptr_t>(p) & 15) == 0 &&
+                         (!PROD || (D.rst_y[0] == 1 && (reinterpret_cast<uintptr_t>(q) & 15) == 0));
+        if (vec) {
+          Acc<T> a4[4];
+          const int64_t R4 = R / 4;
+          for (int64_t r = lane; r < R4; r += 32) {
+            float4 v = __ldg(reinterpret_cast<const float4*>(p) + r);
+            if (PROD) {
+              const float4 w = __ldg(reinterpret_cast<const float4*>(q) + r);
+              v.x *= w.x; v.y *= w.y; v.z *= w.z; v.w *= w.w;
+            }
+            a4[0].add(v.x); a4[1].add(v.y); a4[2].add(v.z); a4[3].add(v.w);
+          }
+          for (int64_t r = 4 * R4 + lane; r < R; r += 32)
+            a4[0].add(PROD ? __ldg(p + r) * __ldg(q + r) : __ldg(p + r));
+          acc.add(a4[0].s); acc.add(a4[1].s); acc.add(a4[2].s); acc.add(a4[3].s);
+          T v = warp_sum(acc.s);
+          if (lane == 0) out[k] = v;
+          continue;
+        }
+      }
       if (PROD) {
         const T* q = y + basey;
         const int64_t sy = D.rst_y[0];
@@ -286,7 +310,7 @@ int reduce_run(const pfb_tensor* x, const int64_t* ystride, const T* yp, uint32_
   const T* xp = (const T*)x->data;
   bool inner = (K == 1) || (rinner != 0 && (kinner == 0 || rinner < kinner));
   if (inner) {
-    if (R <= 2048 && K > 1) {
+    if (R <= 16384 && K > 1) {
       launch(reduce_inner_warp<T, PROD>, grid_for(K, 8, 64), 256, 0, s, D, K, R, xp, yp, o);
       return launch_status();
     }
