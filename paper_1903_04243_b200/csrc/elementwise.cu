@@ -157,17 +157,31 @@ __global__ void __launch_bounds__(256) ew_vec4_kernel(Layout L, IdxT nchunks, To
   pdl_enter();
   const int last = L.rank - 1;
   const int64_t so = L.st[0][last], sa = L.st[1][last], sb = NIN > 1 ? L.st[2][last] : 0;
-  for (IdxT c = blockIdx.x * (IdxT)blockDim.x + threadIdx.x; c < nchunks;
-       c += (IdxT)gridDim.x * blockDim.x) {
-    int64_t off[NIN + 1];
-    offsets<IdxT, NIN + 1>(L, c * 4, off);
-    Tin x[4], y[4];
-    load4(a + off[1], sa, vecmask & 2u, x);
-    if (NIN > 1) load4(b + off[2], sb, vecmask & 4u, y);
-    Tout r[4];
+  // U grid-stride chunks per trip: all U chunks' loads are issued before any
+  // is consumed (U x 16 bytes in flight per thread and input; U = 4 for
+  // byte-sized outputs, whose stores are only 4 bytes per thread)
+  constexpr int U = sizeof(Tout) == 1 ? 4 : 2;
+  const IdxT S = (IdxT)gridDim.x * blockDim.x;
+  for (IdxT c = blockIdx.x * (IdxT)blockDim.x + threadIdx.x; c < nchunks; c += U * S) {
+    int64_t off[U][NIN + 1];
+    Tin x[U][4], y[U][4];
 #pragma unroll
-    for (int k = 0; k < 4; ++k) r[k] = f(x[k], NIN > 1 ? y[k] : x[k]);
-    store4(out + off[0], so, vecmask & 1u, r);
+    for (int u = 0; u < U; ++u) {
+      if (u == 0 || c + u * S < nchunks) {
+        offsets<IdxT, NIN + 1>(L, (c + u * S) * 4, off[u]);
+        load4(a + off[u][1], sa, vecmask & 2u, x[u]);
+        if (NIN > 1) load4(b + off[u][2], sb, vecmask & 4u, y[u]);
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      if (u == 0 || c + u * S < nchunks) {
+        Tout r[4];
+#pragma unroll
+        for (int k = 0; k < 4; ++k) r[k] = f(x[u][k], NIN > 1 ? y[u][k] : x[u][k]);
+        store4(out + off[u][0], so, vecmask & 1u, r);
+      }
+    }
   }
 }
 
@@ -194,31 +208,57 @@ __global__ void __launch_bounds__(256) ew_tile_transpose(Layout L, int p, int64_
                                                          int64_t tiles_last, Tout* out,
                                                          const Tin* in, F f) {
   pdl_enter();
-  __shared__ Tin t[32][33];
+  // a block owns two adjacent 32x32 tiles along `last` (the loads of both are
+  // in flight before the exchange)
+  __shared__ Tin t[2][32][33];
   const int last = L.rank - 1;
-  const int64_t tl = blockIdx.x % tiles_last, tp = blockIdx.x / tiles_last;
+  const int64_t tl = 2 * (blockIdx.x % tiles_last), tp = blockIdx.x / tiles_last;
   const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
+  const int64_t np = L.shape[p], nl = L.shape[last];
+  const int64_t isp = L.st[1][p], isl = L.st[1][last], osp = L.st[0][p], osl = L.st[0][last];
+  // interior tiles: no bounds checks, addresses advance by hoisted strides
+  const bool full = (tp + 1) * 32 <= np && (tl + 2) * 32 <= nl;
   for (int64_t bi = blockIdx.y; bi < nbatch; bi += gridDim.y) {
-    int64_t rem = bi, ob = 0, ib = 0;
-    for (int d = last; d >= 0; --d) {
-      if (d == p || d == last) continue;
-      const int64_t c = rem % L.shape[d];
-      rem /= L.shape[d];
-      ob += c * L.st[0][d];
-      ib += c * L.st[1][d];
+    int64_t ob = 0, ib = 0;
+    if (L.rank > 2) {
+      int64_t rem = bi;
+      for (int d = last; d >= 0; --d) {
+        if (d == p || d == last) continue;
+        const int64_t c = rem % L.shape[d];
+        rem /= L.shape[d];
+        ob += c * L.st[0][d];
+        ib += c * L.st[1][d];
+      }
     }
+    const Tin* src = in + ib + (tp * 32 + tx) * isp + (tl * 32 + ty) * isl;
+    Tout* dst = out + ob + (tp * 32 + ty) * osp + (tl * 32 + tx) * osl;
+    if (full) {
+      Tin v[8];
 #pragma unroll
-    for (int j = ty; j < 32; j += 8) {
-      const int64_t ip = tp * 32 + tx, il = tl * 32 + j;
-      if (ip < L.shape[p] && il < L.shape[last]) t[j][tx] = in[ib + ip * L.st[1][p] + il * L.st[1][last]];
-    }
-    __syncthreads();
+      for (int u = 0; u < 8; ++u) v[u] = __ldg(src + u * 8 * isl);
 #pragma unroll
-    for (int j = ty; j < 32; j += 8) {
-      const int64_t ip = tp * 32 + j, il = tl * 32 + tx;
-      if (ip < L.shape[p] && il < L.shape[last]) {
-        const Tin x = t[tx][j];
-        out[ob + ip * L.st[0][p] + il * L.st[0][last]] = f(x, x);
+      for (int u = 0; u < 8; ++u) t[u >> 2][ty + 8 * (u & 3)][tx] = v[u];
+      __syncthreads();
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const Tin x = t[u >> 2][tx][ty + 8 * (u & 3)];
+        dst[(u & 3) * 8 * osp + (u >> 2) * 32 * osl] = f(x, x);
+      }
+    } else {
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const int j = ty + 8 * (u & 3) + 32 * (u >> 2);
+        if (tp * 32 + tx < np && tl * 32 + j < nl) t[u >> 2][j & 31][tx] = src[(j - ty) * isl];
+      }
+      __syncthreads();
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const int j = ty + 8 * (u & 3);
+        const int64_t il = tl * 32 + 32 * (u >> 2) + tx;
+        if (tp * 32 + j < np && il < nl) {
+          const Tin x = t[u >> 2][tx][j];
+          dst[(u & 3) * 8 * osp + (u >> 2) * 32 * osl] = f(x, x);
+        }
       }
     }
     __syncthreads();
@@ -238,7 +278,7 @@ int launch_ew(const Layout& L, void* out, const void* a, const void* b, F f, cud
     for (int d = 0; d < last; ++d)
       if (L.st[1][d] == 1 && L.shape[d] > 1) p = d;
     if (p >= 0) {
-      const int64_t tiles_last = (L.shape[last] + 31) / 32, tiles_p = (L.shape[p] + 31) / 32;
+      const int64_t tiles_last = (L.shape[last] + 63) / 64, tiles_p = (L.shape[p] + 31) / 32;
       int64_t nbatch = n / (L.shape[last] * L.shape[p]);
       if (tiles_last * tiles_p <= 0x7fffffff) {
         const unsigned gy = (unsigned)std::min<int64_t>(nbatch, 65535);

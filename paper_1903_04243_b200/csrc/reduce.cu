@@ -200,6 +200,46 @@ __global__ void __launch_bounds__(256) reduce_outer(RedDesc D, int64_t K, int64_
   }
 }
 
+// Outer reduction over a contiguous kept dim (fp32): a thread owns 4 adjacent
+// outputs (one 16-byte load per row) and 2 rows per trip, so each thread keeps
+// 32 bytes in flight per trip; R is split over blockIdx.y into partials
+// (ws[split*K + k]) added in split order by combine_partials.
+template <bool PROD>
+__global__ void __launch_bounds__(256) reduce_outer_vec(int64_t K4, int64_t R, int nsplit,
+                                                        const float* x, int64_t sx,
+                                                        const float* y, int64_t sy,
+                                                        float* dst) {
+  pdl_enter();
+  const int split = blockIdx.y;
+  const int64_t chunk = (R + nsplit - 1) / nsplit;
+  const int64_t r0 = split * chunk, r1 = min(R, r0 + chunk);
+  const int64_t k4 = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (k4 >= K4) return;
+  Acc<float> a[2][4];
+  auto row = [&](int64_t r) {
+    float4 v = __ldg(reinterpret_cast<const float4*>(x + r * sx) + k4);
+    if (PROD) {
+      const float4 w = __ldg(reinterpret_cast<const float4*>(y + r * sy) + k4);
+      v.x *= w.x; v.y *= w.y; v.z *= w.z; v.w *= w.w;
+    }
+    return v;
+  };
+  int64_t r = r0;
+  for (; r + 1 < r1; r += 2) {
+    const float4 v0 = row(r), v1 = row(r + 1);
+    a[0][0].add(v0.x); a[0][1].add(v0.y); a[0][2].add(v0.z); a[0][3].add(v0.w);
+    a[1][0].add(v1.x); a[1][1].add(v1.y); a[1][2].add(v1.z); a[1][3].add(v1.w);
+  }
+  if (r < r1) {
+    const float4 v0 = row(r);
+    a[0][0].add(v0.x); a[0][1].add(v0.y); a[0][2].add(v0.z); a[0][3].add(v0.w);
+  }
+  float4 o;
+  a[0][0].add(a[1][0].s); a[0][1].add(a[1][1].s); a[0][2].add(a[1][2].s); a[0][3].add(a[1][3].s);
+  o.x = a[0][0].s; o.y = a[0][1].s; o.z = a[0][2].s; o.w = a[0][3].s;
+  reinterpret_cast<float4*>(dst + (nsplit == 1 ? 0 : split * K4 * 4))[k4] = o;
+}
+
 // Outer reduction in one launch for moderate R: a block owns 32 outputs
 // (lanes) and splits R over its 8 warps; the 8 partial sums are combined in
 // warp order through shared memory (deterministic, no second pass).
@@ -257,6 +297,16 @@ __global__ void fill_zero(int64_t n, T* out) {
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
        i += (int64_t)gridDim.x * blockDim.x)
     out[i] = (T)0;
+}
+
+// partials [ns, K] -> out[K]: 8 warps per 32 outputs, fixed combine order
+template <typename T>
+static void combine_partials(int64_t K, int ns, const T* ws, T* o, cudaStream_t s) {
+  RedDesc P{};
+  P.kr = 1; P.kshape[0] = K; P.kst[0] = 1;
+  P.rr = 1; P.rshape[0] = ns; P.rst[0] = K;
+  launch(reduce_outer_tile<T, false>, (unsigned)((K + 31) / 32), 256, 0, s, P, K, (int64_t)ns, ws,
+         (const T*)nullptr, o);
 }
 
 static int collapse(int n, int64_t* shape, int64_t* st, int64_t* sty) {
@@ -329,6 +379,23 @@ int reduce_run(const pfb_tensor* x, const int64_t* ystride, const T* yp, uint32_
     launch(reduce_outer_tile<T, PROD>, (unsigned)((K + 31) / 32), 256, 0, s, D, K, R, xp, yp, o);
     return launch_status();
   }
+  if constexpr (std::is_same<T, float>::value) {
+    const float* yq = PROD ? (const float*)yp : nullptr;
+    auto al16 = [](const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; };
+    if (D.kr == 1 && D.rr == 1 && D.kst[0] == 1 && K % 4 == 0 && D.rst[0] % 4 == 0 && al16(xp) &&
+        al16(o) && (!PROD || (D.kst_y[0] == 1 && D.rst_y[0] % 4 == 0 && al16(yq))) && R >= 64) {
+      const int64_t K4 = K / 4;
+      const int gxv = (int)((K4 + 255) / 256);
+      int ns = (int)std::min<int64_t>(R / 16, (8ll * kNumSMs) / gxv + 1);
+      ns = max(1, min(ns, 1024));
+      if ((int64_t)ns * K * (int64_t)sizeof(T) > ws_bytes || ws == nullptr) ns = 1;
+      dim3 grid(gxv, ns);
+      launch(reduce_outer_vec<PROD>, grid, 256, 0, s, K4, R, ns, xp, D.rst[0], yq,
+             PROD ? D.rst_y[0] : (int64_t)0, ns == 1 ? o : (float*)ws);
+      if (ns > 1) combine_partials<T>(K, ns, (const T*)ws, o, s);
+      return launch_status();
+    }
+  }
   int gx = grid_for(K, 256, 8);
   int nsplit = 1;
   if ((int64_t)gx * 256 < 4ll * kNumSMs * 256 && R >= 64) {
@@ -338,7 +405,7 @@ int reduce_run(const pfb_tensor* x, const int64_t* ystride, const T* yp, uint32_
   }
   dim3 grid(gx, nsplit);
   launch(reduce_outer<T, PROD>, grid, 256, 0, s, D, K, R, nsplit, xp, yp, nsplit == 1 ? o : (T*)ws);
-  if (nsplit > 1) launch(sum_partials<T>, grid_for(K, 256), 256, 0, s, K, nsplit, false, (const T*)ws, o);
+  if (nsplit > 1) combine_partials<T>(K, nsplit, (const T*)ws, o, s);
   return launch_status();
 }
 

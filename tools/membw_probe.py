@@ -39,6 +39,7 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--mb", type=int, default=256, help="size of each fp32 operand in MB")
     ap.add_argument("--peak", type=float, default=6650.0, help="HBM GB/s (MEASURED_PEAKS or fallback)")
+    ap.add_argument("--only", default="", help="run only the cases whose name contains this")
     a = ap.parse_args()
     n = a.mb * (1 << 20) // 4
     rows = 16384
@@ -49,6 +50,8 @@ def main():
     cases = []
 
     def case(name, build, nbytes):
+        if a.only not in name:
+            return
         b = GraphBuilder()
         b.graph.set_outputs([build(b)])
         t, ex = timed(b.graph)
