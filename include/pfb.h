@@ -87,6 +87,13 @@ int pfb_fused_ew_multi(int32_t n_in, const pfb_tensor* ins, int32_t n_steps,
                        const int32_t* program, int32_t n_out, const int32_t* out_regs,
                        pfb_tensor* outs, void* stream);
 
+/* fused programs over >= min_elems elements run as kernels specialised to the
+ * program (NVRTC, sm_100a; csrc/fused_jit.cu), bit-identical to the
+ * interpreter kernel; enable = 0 forces the interpreter.  min_elems < 0 keeps
+ * the threshold (default 0: every program; env PFB_JIT_MIN; PFB_NO_JIT=1 disables).
+ * Returns 1 when the specialiser is available in this process. */
+int pfb_fused_jit_config(int32_t enable, int64_t min_elems);
+
 /* select(mask, a, b) = mask ? a : b with broadcasting (predicated cond /
  * while bodies; numpy.where semantics); any dtype, mask is bool. */
 /* integer-domain fused elementwise program (i64 / bool registers, int32

@@ -7,6 +7,7 @@
 // HBM-bound: 128-bit loads/stores on the inner dim whenever the operand is
 // unit-stride and 16-byte aligned; index math in 32 bits when it fits.
 #include "common.cuh"
+#include "fused.cuh"
 
 #include <algorithm>
 
@@ -384,24 +385,6 @@ int cast_from(const Layout& L, const pfb_tensor* x, pfb_tensor* out, cudaStream_
 // ----------------------------------------------------------------------------
 // fused elementwise programs (float registers; bool inputs read as 0/1)
 
-constexpr int kMaxSteps = 48;
-constexpr int kMaxRegs = 16;
-enum FusedOpc { F_LOAD = 64, F_CONST = 65, F_SELECT = 68 };
-
-constexpr int kMaxOuts = 8;
-struct FusedProgram {
-  int n_in, n_steps;
-  int in_dtype[8];
-  int code[kMaxSteps][4];  // opcode, dst, src1, src2 (src1 = input / const bits)
-  int n_out;               // outputs: registers stored after the program
-  int out_reg[kMaxOuts];
-  int out_dt[kMaxOuts];    // PFB_F32 or PFB_BOOL
-};
-
-struct FusedOuts {
-  void* p[kMaxOuts];
-};
-
 // One templated kernel for both widths: V = 4 runs the program on 4
 // consecutive elements of the innermost dim per thread (extent a multiple of
 // 4; contiguous operands move as 128-bit accesses), V = 1 on single elements.
@@ -709,6 +692,7 @@ extern "C" int pfb_fused_int(int32_t n_in, const pfb_tensor* ins, int32_t n_step
   const void* p[8];
   for (int k = 0; k < 8; ++k) p[k] = k < n_in ? ins[k].data : nullptr;
   cudaStream_t s = as_stream(stream);
+  if (fused_int_jit_launch(P, n >= (int64_t)0x7fffffff, L, n, fo, p, s)) return launch_status();
   const int grid = grid_for(n, 256);
 #define PFB_FI_CASE(K)                                                                         \
   case K:                                                                                      \
@@ -878,6 +862,7 @@ static int fused_impl(int32_t n_in, const pfb_tensor* ins, int32_t n_steps,
     modes |= m << (2 * o);
   }
   const int64_t ng = v4 ? n / 4 : n;
+  if (fused_jit_launch(P, v4 ? 4 : 1, !small, modes, L, ng, fo, p, s)) return launch_status();
   if (v4) {
     if (small) launch_fused<4, uint32_t>(n_in, L, (uint32_t)ng, P, modes, fo, p, s);
     else launch_fused<4, int64_t>(n_in, L, ng, P, modes, fo, p, s);

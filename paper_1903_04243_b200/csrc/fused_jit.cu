@@ -1,0 +1,434 @@
+// Specialising compiler for fused elementwise programs (pass F3 groups).
+//
+// The interpreter kernel (elementwise.cu fused_kernel) keeps the program's
+// register file in local memory and dispatches every step through a switch:
+// at HBM-scale tensors it is L1/issue bound (~30% of HBM on a 6-step chain,
+// profiles/r01/membw_b200.json), and at small sizes its per-step local-memory
+// round trips are the launch's latency.  For every group (PFB_JIT_MIN sets a
+// size floor) this file emits the program as straight-line CUDA C++ -- one
+// SSA value per
+// step and lane, the input feed modes and dtypes baked in, the same float
+// expressions the interpreter evaluates (np_max/np_min NaN rules, IEEE div,
+// expf/logf/tanhf), compiled with -fmad=false so no step is contracted into
+// an FMA the interpreter would not perform -- compiles it once with NVRTC for
+// sm_100a and caches the kernel per (program, feed modes, width, device).
+// Results are therefore the interpreter's, bit for bit; tests/test_gpu_jit.py
+// checks exactly that.
+//
+// NVRTC is dlopen'ed (no link-time dependency); without it, or with
+// PFB_NO_JIT=1, every group runs on the interpreter.  Module loads made while
+// a stream is being captured switch the thread to relaxed capture mode for
+// the load only.
+#include "fused.cuh"
+
+#include <cuda.h>
+#include <dlfcn.h>
+#include <nvrtc.h>
+
+#include <cstdarg>
+#include <cstdio>
+#include <mutex>
+#include <string>
+#include <unordered_map>
+
+namespace pfb {
+namespace {
+
+struct Nvrtc {
+  decltype(&nvrtcCreateProgram) create = nullptr;
+  decltype(&nvrtcCompileProgram) compile = nullptr;
+  decltype(&nvrtcGetProgramLogSize) log_size = nullptr;
+  decltype(&nvrtcGetProgramLog) log = nullptr;
+  decltype(&nvrtcGetCUBINSize) cubin_size = nullptr;
+  decltype(&nvrtcGetCUBIN) cubin = nullptr;
+  decltype(&nvrtcDestroyProgram) destroy = nullptr;
+  bool ok = false;
+};
+
+struct Driver {
+  decltype(&cuModuleLoadData) load = nullptr;
+  decltype(&cuModuleGetFunction) get = nullptr;
+  decltype(&cuLaunchKernelEx) launch = nullptr;
+  bool ok = false;
+};
+
+const Nvrtc& nvrtc() {
+  static Nvrtc n = [] {
+    Nvrtc r;
+    const char* names[] = {"libnvrtc.so.12", "/usr/local/cuda/lib64/libnvrtc.so.12", "libnvrtc.so"};
+    void* h = nullptr;
+    for (const char* nm : names)
+      if ((h = dlopen(nm, RTLD_NOW | RTLD_LOCAL))) break;
+    if (!h) return r;
+    r.create = (decltype(r.create))dlsym(h, "nvrtcCreateProgram");
+    r.compile = (decltype(r.compile))dlsym(h, "nvrtcCompileProgram");
+    r.log_size = (decltype(r.log_size))dlsym(h, "nvrtcGetProgramLogSize");
+    r.log = (decltype(r.log))dlsym(h, "nvrtcGetProgramLog");
+    r.cubin_size = (decltype(r.cubin_size))dlsym(h, "nvrtcGetCUBINSize");
+    r.cubin = (decltype(r.cubin))dlsym(h, "nvrtcGetCUBIN");
+    r.destroy = (decltype(r.destroy))dlsym(h, "nvrtcDestroyProgram");
+    r.ok = r.create && r.compile && r.log_size && r.log && r.cubin_size && r.cubin && r.destroy;
+    return r;
+  }();
+  return n;
+}
+
+template <typename F>
+bool entry(const char* name, F* out) {
+  cudaDriverEntryPointQueryResult q;
+  void* p = nullptr;
+  if (cudaGetDriverEntryPoint(name, &p, cudaEnableDefault, &q) != cudaSuccess ||
+      q != cudaDriverEntryPointSuccess || !p)
+    return false;
+  *out = reinterpret_cast<F>(p);
+  return true;
+}
+
+const Driver& driver() {
+  static Driver d = [] {
+    Driver r;
+    r.ok = entry("cuModuleLoadData", &r.load) && entry("cuModuleGetFunction", &r.get) &&
+           entry("cuLaunchKernelEx", &r.launch);
+    return r;
+  }();
+  return d;
+}
+
+// ---------------------------------------------------------------------------
+// source generation
+
+const char* kPrelude = R"(
+typedef long long i64;
+struct Layout { int rank; int nops; i64 shape[%d]; i64 st[%d][%d]; };
+struct Outs { void* p[%d]; };
+__device__ __forceinline__ float np_max(float a, float b) {
+  return (a != a) ? a : ((b != b) ? b : (a >= b ? a : b));
+}
+__device__ __forceinline__ float np_min(float a, float b) {
+  return (a != a) ? a : ((b != b) ? b : (a <= b ? a : b));
+}
+)";
+
+std::string fmt(const char* f, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, f);
+  vsnprintf(buf, sizeof buf, f, ap);
+  va_end(ap);
+  return buf;
+}
+
+std::string gen_source(const FusedProgram& P, int V, bool idx64, uint32_t modes) {
+  std::string s = fmt(kPrelude, kMaxRank, kMaxOps, kMaxRank, kMaxOuts);
+  const char* IT = idx64 ? "i64" : "unsigned";
+  const int nops = P.n_in + 1;
+  s += fmt("extern \"C\" __global__ void __launch_bounds__(256) pfb_fused_jit(Layout L, %s ngroups, "
+           "Outs outs, const void* i0, const void* i1, const void* i2, const void* i3, "
+           "const void* i4, const void* i5, const void* i6, const void* i7) {\n", IT);
+  s += "  asm volatile(\"griddepcontrol.wait;\" ::: \"memory\");\n"
+       "  asm volatile(\"griddepcontrol.launch_dependents;\" :::);\n"
+       "  const void* ins[8] = {i0, i1, i2, i3, i4, i5, i6, i7};\n"
+       "  const int ir = L.rank - 1;\n";
+  s += fmt("  for (%s g = blockIdx.x * (%s)blockDim.x + threadIdx.x; g < ngroups; "
+           "g += (%s)gridDim.x * blockDim.x) {\n", IT, IT, IT);
+  s += fmt("    i64 off[%d];\n", nops);
+  s += fmt("    { %s lin = g * %d;\n", IT, V);
+  s += fmt("      for (int o = 0; o < %d; ++o) off[o] = 0;\n", nops);
+  s += fmt("      for (int d = L.rank - 1; d >= 0; --d) {\n"
+           "        %s sh = (%s)L.shape[d]; %s q = lin / sh; %s c = lin - q * sh; lin = q;\n"
+           "        for (int o = 0; o < %d; ++o) off[o] += (i64)c * L.st[o][d];\n"
+           "      }\n    }\n", IT, IT, IT, IT, nops);
+  // input feeds (all loads first, as in the interpreter)
+  for (int k = 0; k < P.n_in; ++k) {
+    const int md = (modes >> (2 * (k + 1))) & 3;
+    const bool bl = P.in_dtype[k] == PFB_BOOL;
+    const char* T = bl ? "unsigned char" : "float";
+    s += fmt("    const %s* p%d = reinterpret_cast<const %s*>(ins[%d]) + off[%d];\n", T, k, T, k, k + 1);
+    if (V == 4 && md == 0) {
+      if (bl)
+        s += fmt("    const uchar4 w%d = __ldg(reinterpret_cast<const uchar4*>(p%d));\n", k, k);
+      else
+        s += fmt("    const float4 w%d = __ldg(reinterpret_cast<const float4*>(p%d));\n", k, k);
+      const char* f[4] = {"x", "y", "z", "w"};
+      for (int j = 0; j < 4; ++j) s += fmt("    const float in%d_%d = (float)w%d.%s;\n", k, j, k, f[j]);
+    } else if (md == 1) {
+      s += fmt("    const float in%d_0 = (float)__ldg(p%d);\n", k, k);
+      for (int j = 1; j < V; ++j) s += fmt("    const float in%d_%d = in%d_0;\n", k, j, k);
+    } else {
+      s += fmt("    const i64 sin%d = L.st[%d][ir];\n", k, k + 1);
+      for (int j = 0; j < V; ++j)
+        s += fmt("    const float in%d_%d = (float)__ldg(p%d + %d * sin%d);\n", k, j, k, j, k);
+    }
+  }
+  // the program: reg -> current SSA name
+  std::string reg[kMaxRegs];
+  for (int r = 0; r < kMaxRegs; ++r) reg[r] = "";
+  auto R = [&](int r, int j) { return reg[r].empty() ? std::string("0.f") : reg[r] + "_" + std::to_string(j); };
+  for (int st = 0; st < P.n_steps; ++st) {
+    const int op = P.code[st][0], dst = P.code[st][1], z = P.code[st][2], w = P.code[st][3];
+    const std::string nm = "v" + std::to_string(st);
+    for (int j = 0; j < V; ++j) {
+      std::string e;
+      if (op == F_LOAD) {
+        e = z < P.n_in ? fmt("in%d_%d", z, j) : std::string("0.f");
+      } else if (op == F_CONST) {
+        e = fmt("__int_as_float(%d)", z);
+      } else if (op == F_SELECT) {
+        e = "(" + R(z, j) + " != 0.f ? " + R(w, j) + " : " + R(dst, j) + ")";
+      } else {
+        const std::string x = R(z, j), y = R(w, j);
+        switch (op) {
+          case PFB_ADD: e = x + " + " + y; break;
+          case PFB_SUB: e = x + " - " + y; break;
+          case PFB_MUL: e = x + " * " + y; break;
+          case PFB_DIV: e = x + " / " + y; break;
+          case PFB_MAX: e = "np_max(" + x + ", " + y + ")"; break;
+          case PFB_MIN: e = "np_min(" + x + ", " + y + ")"; break;
+          case PFB_LESS: e = "(" + x + " < " + y + " ? 1.f : 0.f)"; break;
+          case PFB_EQUAL: e = "(" + x + " == " + y + " ? 1.f : 0.f)"; break;
+          case 16 + PFB_NEG: e = "-" + x; break;
+          case 16 + PFB_EXP: e = "expf(" + x + ")"; break;
+          case 16 + PFB_LOG: e = "logf(" + x + ")"; break;
+          case 16 + PFB_RELU: e = "np_max(" + x + ", 0.f)"; break;
+          case 16 + PFB_TANH: e = "tanhf(" + x + ")"; break;
+          case 16 + PFB_SIGMOID: e = "1.f / (1.f + expf(-" + x + "))"; break;
+          case 16 + PFB_SQUARE: e = x + " * " + x; break;
+          case 16 + PFB_LOGICAL_NOT: e = "(" + x + " == 0.f ? 1.f : 0.f)"; break;
+          case 66: e = "(" + x + " != 0.f ? 1.f : 0.f)"; break;
+          default: e = x; break;  // 67: move
+        }
+      }
+      s += fmt("    const float %s_%d = ", nm.c_str(), j) + e + ";\n";
+    }
+    reg[dst] = nm;
+  }
+  // outputs at operand 0's offsets
+  const bool vec = (modes & 3) == 0;
+  s += "    const i64 so = L.st[0][ir];\n    (void)so;\n";
+  for (int k = 0; k < P.n_out; ++k) {
+    const int r = P.out_reg[k];
+    if (P.out_dt[k] == PFB_BOOL) {
+      s += fmt("    { unsigned char* q = reinterpret_cast<unsigned char*>(outs.p[%d]) + off[0];\n", k);
+      if (V == 4 && vec)
+        s += "      *reinterpret_cast<uchar4*>(q) = make_uchar4(" + R(r, 0) + " != 0.f, " + R(r, 1) +
+             " != 0.f, " + R(r, 2) + " != 0.f, " + R(r, 3) + " != 0.f); }\n";
+      else {
+        for (int j = 0; j < V; ++j) s += fmt("      q[%d * so] = (unsigned char)(", j) + R(r, j) + " != 0.f);\n";
+        s += "    }\n";
+      }
+    } else {
+      s += fmt("    { float* q = reinterpret_cast<float*>(outs.p[%d]) + off[0];\n", k);
+      if (V == 4 && vec)
+        s += "      *reinterpret_cast<float4*>(q) = make_float4(" + R(r, 0) + ", " + R(r, 1) + ", " +
+             R(r, 2) + ", " + R(r, 3) + "); }\n";
+      else {
+        for (int j = 0; j < V; ++j) s += fmt("      q[%d * so] = ", j) + R(r, j) + ";\n";
+        s += "    }\n";
+      }
+    }
+  }
+  s += "  }\n}\n";
+  return s;
+}
+
+// integer domain (elementwise.cu fused_int_kernel): i64 registers, numpy
+// int64 wraparound through uint64 arithmetic, bool = 0/1, one element per
+// thread; ops the integer interpreter does not define move their operand
+std::string gen_source_int(const FusedProgram& P, bool idx64) {
+  std::string s = fmt(kPrelude, kMaxRank, kMaxOps, kMaxRank, kMaxOuts);
+  s += "typedef unsigned long long u64;\n";
+  const char* IT = idx64 ? "i64" : "unsigned";
+  const int nops = P.n_in + 1;
+  s += fmt("extern \"C\" __global__ void __launch_bounds__(256) pfb_fused_jit(Layout L, %s n, "
+           "Outs outs, const void* i0, const void* i1, const void* i2, const void* i3, "
+           "const void* i4, const void* i5, const void* i6, const void* i7) {\n", IT);
+  s += "  asm volatile(\"griddepcontrol.wait;\" ::: \"memory\");\n"
+       "  asm volatile(\"griddepcontrol.launch_dependents;\" :::);\n"
+       "  const void* ins[8] = {i0, i1, i2, i3, i4, i5, i6, i7};\n";
+  s += fmt("  for (%s e = blockIdx.x * (%s)blockDim.x + threadIdx.x; e < n; "
+           "e += (%s)gridDim.x * blockDim.x) {\n", IT, IT, IT);
+  s += fmt("    i64 off[%d];\n", nops);
+  s += fmt("    { %s lin = e;\n", IT);
+  s += fmt("      for (int o = 0; o < %d; ++o) off[o] = 0;\n", nops);
+  s += fmt("      for (int d = L.rank - 1; d >= 0; --d) {\n"
+           "        %s sh = (%s)L.shape[d]; %s q = lin / sh; %s c = lin - q * sh; lin = q;\n"
+           "        for (int o = 0; o < %d; ++o) off[o] += (i64)c * L.st[o][d];\n"
+           "      }\n    }\n", IT, IT, IT, IT, nops);
+  for (int k = 0; k < P.n_in; ++k) {
+    if (P.in_dtype[k] == PFB_BOOL)
+      s += fmt("    const i64 in%d = (i64)__ldg(reinterpret_cast<const unsigned char*>(ins[%d]) + off[%d]);\n",
+               k, k, k + 1);
+    else
+      s += fmt("    const i64 in%d = __ldg(reinterpret_cast<const long long*>(ins[%d]) + off[%d]);\n",
+               k, k, k + 1);
+  }
+  std::string reg[kMaxRegs];
+  auto R = [&](int r) { return reg[r].empty() ? std::string("(i64)0") : reg[r]; };
+  for (int st = 0; st < P.n_steps; ++st) {
+    const int op = P.code[st][0], dst = P.code[st][1], z = P.code[st][2], w = P.code[st][3];
+    std::string e;
+    if (op == F_LOAD) {
+      e = z < P.n_in ? fmt("in%d", z) : std::string("(i64)0");
+    } else if (op == F_CONST) {
+      e = fmt("(i64)(%d)", z);
+    } else if (op == F_SELECT) {
+      e = "(" + R(z) + " != 0 ? " + R(w) + " : " + R(dst) + ")";
+    } else {
+      const std::string a = R(z), b = R(w);
+      const std::string ua = "(u64)" + a, ub = "(u64)" + b;
+      switch (op) {
+        case PFB_ADD: e = "(i64)(" + ua + " + " + ub + ")"; break;
+        case PFB_SUB: e = "(i64)(" + ua + " - " + ub + ")"; break;
+        case PFB_MUL: e = "(i64)(" + ua + " * " + ub + ")"; break;
+        case PFB_MAX: e = "(" + a + " >= " + b + " ? " + a + " : " + b + ")"; break;
+        case PFB_MIN: e = "(" + a + " <= " + b + " ? " + a + " : " + b + ")"; break;
+        case PFB_LESS: e = "(i64)(" + a + " < " + b + ")"; break;
+        case PFB_EQUAL: e = "(i64)(" + a + " == " + b + ")"; break;
+        case 16 + PFB_NEG: e = "(i64)((u64)0 - " + ua + ")"; break;
+        case 16 + PFB_SQUARE: e = "(i64)(" + ua + " * " + ua + ")"; break;
+        case 16 + PFB_LOGICAL_NOT: e = "(i64)(" + a + " == 0)"; break;
+        case 66: e = "(i64)(" + a + " != 0)"; break;
+        default: e = a; break;
+      }
+    }
+    const std::string nm = "v" + std::to_string(st);
+    s += "    const i64 " + nm + " = " + e + ";\n";
+    reg[dst] = nm;
+  }
+  for (int k = 0; k < P.n_out; ++k) {
+    if (P.out_dt[k] == PFB_BOOL)
+      s += fmt("    reinterpret_cast<unsigned char*>(outs.p[%d])[off[0]] = (unsigned char)(", k) +
+           R(P.out_reg[k]) + " != 0);\n";
+    else
+      s += fmt("    reinterpret_cast<long long*>(outs.p[%d])[off[0]] = ", k) + R(P.out_reg[k]) + ";\n";
+  }
+  s += "  }\n}\n";
+  return s;
+}
+
+CUfunction compile(const std::string& src) {
+  const Nvrtc& N = nvrtc();
+  nvrtcProgram prog;
+  if (N.create(&prog, src.c_str(), "pfb_fused_jit.cu", 0, nullptr, nullptr) != NVRTC_SUCCESS)
+    return nullptr;
+  const char* opts[] = {"--gpu-architecture=sm_100a", "-fmad=false", "--std=c++17",
+                        "-default-device", "-lineinfo"};
+  nvrtcResult rc = N.compile(prog, 5, opts);
+  if (rc != NVRTC_SUCCESS) {
+    size_t n = 0;
+    N.log_size(prog, &n);
+    std::string log(n, '\0');
+    N.log(prog, &log[0]);
+    fprintf(stderr, "pfb: fused-program compile failed (interpreter used):\n%s\n", log.c_str());
+    N.destroy(&prog);
+    return nullptr;
+  }
+  size_t n = 0;
+  N.cubin_size(prog, &n);
+  std::string cubin(n, '\0');
+  N.cubin(prog, &cubin[0]);
+  N.destroy(&prog);
+  const Driver& D = driver();
+  CUmodule mod = nullptr;
+  CUfunction fn = nullptr;
+  // a load is not a stream operation; allow it while this thread captures
+  cudaStreamCaptureMode mode = cudaStreamCaptureModeRelaxed;
+  cudaThreadExchangeStreamCaptureMode(&mode);
+  CUresult r = D.load(&mod, cubin.data());
+  cudaThreadExchangeStreamCaptureMode(&mode);
+  if (r != CUDA_SUCCESS || D.get(&fn, mod, "pfb_fused_jit") != CUDA_SUCCESS) return nullptr;
+  return fn;
+}
+
+int g_jit_on = -1;           // -1: not yet read from PFB_NO_JIT
+int64_t g_jit_min = 0;       // PFB_JIT_MIN: smallest group specialised
+
+void jit_init() {
+  if (g_jit_on >= 0) return;
+  g_jit_on = getenv_flag("PFB_NO_JIT") ? 0 : 1;
+  if (const char* e = getenv("PFB_JIT_MIN")) g_jit_min = atoll(e);
+}
+
+}  // namespace
+
+namespace {
+
+// kernel for a program (integer: the i64 domain), compiled on first use
+CUfunction lookup(const FusedProgram& P, int V, bool idx64, uint32_t modes, bool integer) {
+  int dev = 0;
+  cudaGetDevice(&dev);
+  // cache key: the program's encoding and everything baked into the source
+  int32_t kb[9 + 8 + 4 * kMaxSteps + 2 * kMaxOuts];
+  int nk = 0;
+  kb[nk++] = dev; kb[nk++] = V; kb[nk++] = idx64; kb[nk++] = (int32_t)modes; kb[nk++] = integer;
+  kb[nk++] = P.n_in; kb[nk++] = P.n_steps; kb[nk++] = P.n_out;
+  for (int k = 0; k < P.n_in; ++k) kb[nk++] = P.in_dtype[k];
+  for (int t = 0; t < P.n_steps; ++t)
+    for (int j = 0; j < 4; ++j) kb[nk++] = P.code[t][j];
+  for (int k = 0; k < P.n_out; ++k) { kb[nk++] = P.out_reg[k]; kb[nk++] = P.out_dt[k]; }
+  const std::string key(reinterpret_cast<const char*>(kb), nk * sizeof(int32_t));
+  static std::mutex mu;
+  static std::unordered_map<std::string, CUfunction> cache;
+  std::lock_guard<std::mutex> g(mu);
+  auto it = cache.find(key);
+  if (it == cache.end())
+    it = cache.emplace(key, compile(integer ? gen_source_int(P, idx64)
+                                            : gen_source(P, V, idx64, modes))).first;
+  return it->second;
+}
+
+bool run(CUfunction fn, bool idx64, const Layout& L, int64_t nitems, const FusedOuts& outs,
+         const void* const* p, cudaStream_t s) {
+  CUlaunchConfig cfg = {};
+  cfg.gridDimX = grid_for(nitems, 256); cfg.gridDimY = 1; cfg.gridDimZ = 1;
+  cfg.blockDimX = 256; cfg.blockDimY = 1; cfg.blockDimZ = 1;
+  cfg.hStream = (CUstream)s;
+  CUlaunchAttribute attr[1];
+  attr[0].id = CU_LAUNCH_ATTRIBUTE_PROGRAMMATIC_STREAM_SERIALIZATION;
+  attr[0].value.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = pdl_enabled() ? 1 : 0;
+  Layout Lc = L;
+  FusedOuts oc = outs;
+  uint32_t n32 = (uint32_t)nitems;
+  int64_t n64 = nitems;
+  const void* ip[8];
+  for (int k = 0; k < 8; ++k) ip[k] = p[k];
+  void* args[11] = {&Lc, idx64 ? (void*)&n64 : (void*)&n32, &oc, &ip[0], &ip[1], &ip[2], &ip[3],
+                    &ip[4], &ip[5], &ip[6], &ip[7]};
+  return driver().launch(&cfg, fn, args, nullptr) == CUDA_SUCCESS;
+}
+
+bool usable(int64_t elems) {
+  jit_init();
+  return g_jit_on && elems >= g_jit_min && nvrtc().ok && driver().ok;
+}
+
+}  // namespace
+
+bool fused_jit_launch(const FusedProgram& P, int V, bool idx64, uint32_t modes, const Layout& L,
+                      int64_t ngroups, const FusedOuts& outs, const void* const* p,
+                      cudaStream_t s) {
+  if (!usable(ngroups * V)) return false;
+  CUfunction fn = lookup(P, V, idx64, modes, false);
+  return fn && run(fn, idx64, L, ngroups, outs, p, s);
+}
+
+bool fused_int_jit_launch(const FusedProgram& P, bool idx64, const Layout& L, int64_t n,
+                          const FusedOuts& outs, const void* const* p, cudaStream_t s) {
+  if (!usable(n)) return false;
+  CUfunction fn = lookup(P, 1, idx64, 0, true);
+  return fn && run(fn, idx64, L, n, outs, p, s);
+}
+
+}  // namespace pfb
+
+// Runtime control of the specialiser (tests compare it with the interpreter):
+// enable 0/1, min_elems < 0 keeps the current threshold.  Returns 1 when the
+// specialiser can run on this process (NVRTC + driver entry points found).
+extern "C" int pfb_fused_jit_config(int32_t enable, int64_t min_elems) {
+  pfb::jit_init();
+  pfb::g_jit_on = enable ? 1 : 0;
+  if (min_elems >= 0) pfb::g_jit_min = min_elems;
+  return pfb::nvrtc().ok && pfb::driver().ok;
+}

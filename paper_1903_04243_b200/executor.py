@@ -476,10 +476,11 @@ class Executor:
         slots = plan["slots"]
         if not slots:
             torch.cuda.synchronize(self.device)
-            # pinned host memory is bounded: fewer zero-copy slots for large
-            # results (cfg3 returns 7 GB per run); at least one plus the
-            # copy-out slot
-            n_zc = max(1, min(self._IO_SLOTS, (4 << 30) // max(plan["total"], 1)))
+            # pinned host memory is bounded (~16 GB per captured graph): fewer
+            # zero-copy slots for large results (cfg3 returns 7 GB per run),
+            # but at least two, so a caller holding the previous run's results
+            # does not push every run onto the copy-out slot
+            n_zc = max(2, min(self._IO_SLOTS, (16 << 30) // max(plan["total"], 1)))
             for _ in range(n_zc + 1):
                 pinned = torch.empty(plan["total"], dtype=torch.uint8, pin_memory=True)
                 raw = (ctypes.c_uint8 * plan["total"]).from_address(pinned.data_ptr())

@@ -1,0 +1,124 @@
+"""GPU: fused elementwise programs specialised by NVRTC (csrc/fused_jit.cu)
+against the interpreter kernel they replace.  The specialised kernel evaluates
+the same float expressions with FMA contraction off, so the bar here is
+bit-identity with the interpreter (whose own parity with the reference is
+test_gpu_parity.py's), on the bench programs, a slice of the reference's
+randomized corpus and an HBM-scale chain with NaN/inf inputs."""
+
+import gzip
+import json
+import pathlib
+
+import numpy as np
+import pytest
+
+from test_oracle_golden import PROGRAM_CASES, build_program
+
+pytestmark = pytest.mark.gpu
+
+GOLD = pathlib.Path(__file__).parent / "golden"
+
+
+@pytest.fixture(scope="module")
+def lib():
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    from paper_1903_04243_b200 import _native
+    L = _native.load()
+    yield L
+    L.pfb_fused_jit_config(1, 0)
+
+
+def _same(a, b):
+    a, b = np.asarray(a.data), np.asarray(b.data)
+    if a.shape != b.shape or a.dtype != b.dtype:
+        return False
+    if a.dtype.kind == "f":
+        return np.array_equal(a.view(np.uint32 if a.itemsize == 4 else np.uint64),
+                              b.view(np.uint32 if b.itemsize == 4 else np.uint64)) or \
+            np.array_equal(a, b, equal_nan=True)
+    return np.array_equal(a, b)
+
+
+def _both(lib, run):
+    lib.pfb_fused_jit_config(0, -1)
+    ref = run()
+    lib.pfb_fused_jit_config(1, 0)
+    got = run()
+    lib.pfb_fused_jit_config(1, 0)
+    return ref, got
+
+
+def test_specialiser_available(lib):
+    assert lib.pfb_fused_jit_config(1, -1) == 1, "NVRTC / driver entry points not found"
+
+
+@pytest.mark.parametrize("name", sorted(PROGRAM_CASES))
+def test_bench_program_specialised_equals_interpreter(name, lib):
+    from paper_1903_04243_b200.executor import Executor
+    w = build_program(name)
+
+    def run():
+        return Executor(w.graph).run(feeds=w.feeds)
+    ref, got = _both(lib, run)
+    assert len(ref) == len(got)
+    for j, (r, g) in enumerate(zip(ref, got)):
+        assert _same(r, g), f"{name} output {j} differs"
+
+
+def test_corpus_specialised_equals_interpreter(lib):
+    from paper_1903_04243_b200 import pfg
+    from paper_1903_04243_b200.executor import Executor, RngState, VariableStore
+    corpus = json.load(gzip.open(GOLD / "corpus.json.gz", "rt"))
+    bad = []
+    for key in sorted(corpus)[:120]:
+        c = corpus[key]
+        g = pfg.loads(c["vec"])
+
+        def run():
+            ex = Executor(g, store=VariableStore(g.variables), rng=RngState(c["seed"]))
+            try:
+                return ex.run()
+            except Exception as e:  # noqa: BLE001 -- both paths must fail alike
+                return type(e).__name__
+        ref, got = _both(lib, run)
+        if isinstance(ref, str) or isinstance(got, str):
+            if ref != got:
+                bad.append(f"{key}: {ref} vs {got}")
+            continue
+        for j, (r, o) in enumerate(zip(ref, got)):
+            if not _same(r, o):
+                bad.append(f"{key} out {j}")
+    assert not bad, bad[:8]
+
+
+def test_hbm_scale_chain_with_specials(lib):
+    """y*(1-tanh(x)^2)+x, max/select/compare steps, bool output, over 4M
+    elements with NaN / inf / signed zeros in the inputs."""
+    from paper_1903_04243_b200 import GraphBuilder
+    from paper_1903_04243_b200.executor import Executor
+    r = np.random.default_rng(3)
+    x = r.standard_normal((2048, 2048)).astype(np.float32)
+    y = r.standard_normal((2048, 2048)).astype(np.float32)
+    x.flat[::997] = np.nan
+    x.flat[5::1009] = np.inf
+    y.flat[7::1013] = -np.inf
+    x.flat[11::1019] = -0.0
+    b = GraphBuilder()
+    X, Y = b.const(x), b.const(y)
+    t = b.add(b.mul(Y, b.sub(b.f64(1.0), b.square(b.tanh(X)))), X)
+    m = b.max_(t, b.div(Y, b.exp(X)))
+    lt = b.less(m, b.f64(0.25))
+    b.graph.set_outputs([m, lt, b.sigmoid(b.sub(m, b.log(b.relu(Y))))])
+
+    def run():
+        return Executor(b.graph).run()
+    ref, got = _both(lib, run)
+    for j, (r_, g_) in enumerate(zip(ref, got)):
+        assert _same(r_, g_), f"output {j} differs"
+    with np.errstate(all="ignore"):
+        xd, yd = x.astype(np.float64), y.astype(np.float64)
+        want = np.maximum(yd * (1 - np.tanh(xd) ** 2) + xd, yd / np.exp(xd))
+    np.testing.assert_allclose(np.asarray(got[0].data, np.float64), want, rtol=1e-4, atol=1e-5,
+                               equal_nan=True)
