@@ -48,6 +48,7 @@ constexpr int BM = 128, BN = 128, BK = 32, STAGES = 3, UMMA_K = 8;
 constexpr int CHUNK_KB = PFB_CHUNK_KB;            // k-blocks accumulated in TMEM per chunk
 constexpr int TILE_BYTES = BM * BK * 4;           // 16 KB per operand tile
 constexpr int STAGE_BYTES = 4 * TILE_BYTES;       // A_hi, A_lo, B_hi, B_lo
+constexpr int kMaxSplit = 8;                      // k-splits per tile (cluster size)
 constexpr int EPI_WARPS = 8;                      // 2 per TMEM lane quarter, 64 columns each
 constexpr int EPI_COLS = BN / 2;
 constexpr int EPI_STAGE_FLOATS = 32 * 32;         // per epilogue warp: one 32x32 block,
@@ -501,11 +502,15 @@ gemm_kernel(const __grid_constant__ CUtensorMap map_ah, const __grid_constant__ 
     for (int idx = threadIdx.x; idx < (re - rb) * (BN / 4); idx += NUM_THREADS) {
       const int row = rb + idx / (BN / 4), ch = idx % (BN / 4);
       const uint32_t off = (uint32_t)(row * BN + 4 * (ch ^ (row & 7))) * 4u;
-      float4 v = ld_dsmem_f4(red + off, 0);
-      for (int q = 1; q < p.ksplit; ++q) {
-        const float4 w = ld_dsmem_f4(red + off, (uint32_t)q);
-        v.x += w.x; v.y += w.y; v.z += w.z; v.w += w.w;
-      }
+      // all partials requested before the first is added (rank order kept)
+      float4 w[kMaxSplit];
+#pragma unroll
+      for (int q = 0; q < kMaxSplit; ++q)
+        if (q < p.ksplit) w[q] = ld_dsmem_f4(red + off, (uint32_t)q);
+      float4 v = w[0];
+#pragma unroll
+      for (int q = 1; q < kMaxSplit; ++q)
+        if (q < p.ksplit) { v.x += w[q].x; v.y += w[q].y; v.z += w[q].z; v.w += w[q].w; }
       const int grow = m0 + row, col = n0 + 4 * ch;
       if (grow >= p.M) continue;
       const float alpha = p.alpha_rows ? __ldg(p.alpha_rows + (int64_t)bz * p.M + grow) : 1.f;
@@ -593,7 +598,7 @@ static int64_t align_up(int64_t x) { return (x + 255) / 256 * 256; }
 
 // K-splits so that (tiles x splits) covers the SMs, >= 2 chunks per split;
 // the splits of one tile form a thread-block cluster (<= 8, portable size)
-constexpr int kMaxCluster = 8;
+constexpr int kMaxCluster = kMaxSplit;
 static void choose_split(const GemmArgs& g, int* ksplit, int* kb_per) {
   const int64_t tiles = ((g.M + BM - 1) / BM) * ((g.N + BN - 1) / BN) * g.batch;
   const int64_t Kp = (g.K + 3) / 4 * 4;

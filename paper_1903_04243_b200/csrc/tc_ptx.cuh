@@ -167,7 +167,25 @@ __device__ __forceinline__ float lo_of_raw(float x) {
 
 __device__ __forceinline__ void split_tf32_smem(uint32_t hi, uint32_t lo, int n16, int t,
                                                 int nthreads) {
-  for (int i = t; i < n16; i += nthreads) {
+  // 4 vectors per thread per batch: the 4 loads issue back to back before
+  // the first is consumed (the asm statements keep their order, so a
+  // load-compute-store loop would wait out one shared-memory latency each)
+  int i = t;
+  for (; i + 3 * nthreads < n16; i += 4 * nthreads) {
+    float x[4][4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u)
+      asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];"
+                   : "=f"(x[u][0]), "=f"(x[u][1]), "=f"(x[u][2]), "=f"(x[u][3])
+                   : "r"(hi + 16 * (i + u * nthreads)));
+#pragma unroll
+    for (int u = 0; u < 4; ++u)
+      asm volatile("st.shared.v4.f32 [%0], {%1, %2, %3, %4};" ::"r"(lo + 16 * (i + u * nthreads)),
+                   "f"(lo_of_raw(x[u][0])), "f"(lo_of_raw(x[u][1])), "f"(lo_of_raw(x[u][2])),
+                   "f"(lo_of_raw(x[u][3]))
+                   : "memory");
+  }
+  for (; i < n16; i += nthreads) {
     float x0, x1, x2, x3;
     asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];"
                  : "=f"(x0), "=f"(x1), "=f"(x2), "=f"(x3)
