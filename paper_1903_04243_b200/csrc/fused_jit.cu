@@ -306,11 +306,12 @@ std::string gen_source_int(const FusedProgram& P, bool idx64) {
   return s;
 }
 
-CUfunction compile(const std::string& src) {
+// NVRTC: source -> sm_100a cubin (empty on failure; the log goes to stderr)
+std::string to_cubin(const std::string& src) {
   const Nvrtc& N = nvrtc();
   nvrtcProgram prog;
   if (N.create(&prog, src.c_str(), "pfb_fused_jit.cu", 0, nullptr, nullptr) != NVRTC_SUCCESS)
-    return nullptr;
+    return {};
   const char* opts[] = {"--gpu-architecture=sm_100a", "-fmad=false", "--std=c++17",
                         "-default-device", "-lineinfo"};
   nvrtcResult rc = N.compile(prog, 5, opts);
@@ -321,13 +322,19 @@ CUfunction compile(const std::string& src) {
     N.log(prog, &log[0]);
     fprintf(stderr, "pfb: fused-program compile failed (interpreter used):\n%s\n", log.c_str());
     N.destroy(&prog);
-    return nullptr;
+    return {};
   }
   size_t n = 0;
   N.cubin_size(prog, &n);
   std::string cubin(n, '\0');
   N.cubin(prog, &cubin[0]);
   N.destroy(&prog);
+  return cubin;
+}
+
+CUfunction compile(const std::string& src) {
+  const std::string cubin = to_cubin(src);
+  if (cubin.empty()) return nullptr;
   const Driver& D = driver();
   CUmodule mod = nullptr;
   CUfunction fn = nullptr;
@@ -431,4 +438,35 @@ extern "C" int pfb_fused_jit_config(int32_t enable, int64_t min_elems) {
   pfb::g_jit_on = enable ? 1 : 0;
   if (min_elems >= 0) pfb::g_jit_min = min_elems;
   return pfb::nvrtc().ok && pfb::driver().ok;
+}
+
+// Host-only check (no device needed): generate the specialised source for a
+// program and compile it with NVRTC for sm_100a.  0 = compiled, 1 = compile
+// error (log on stderr), PFB_E_UNSUPPORTED = NVRTC not found, PFB_E_ARG = bad
+// program.  integer != 0 selects the i64/bool domain (v ignored).
+extern "C" int pfb_fused_jit_check(int32_t integer, int32_t v, uint32_t modes, int32_t n_in,
+                                   const int32_t* in_dtypes, int32_t n_steps,
+                                   const int32_t* program, int32_t n_out, const int32_t* out_regs,
+                                   const int32_t* out_dtypes) {
+  using namespace pfb;
+  if (n_in < 1 || n_in > 8 || n_steps < 1 || n_steps > kMaxSteps || n_out < 1 ||
+      n_out > kMaxOuts || (v != 1 && v != 4))
+    return PFB_E_ARG;
+  if (!nvrtc().ok) return PFB_E_UNSUPPORTED;
+  FusedProgram P{};
+  P.n_in = n_in;
+  P.n_steps = n_steps;
+  P.n_out = n_out;
+  for (int k = 0; k < n_in; ++k) P.in_dtype[k] = in_dtypes[k];
+  for (int t = 0; t < n_steps; ++t) {
+    for (int j = 0; j < 4; ++j) P.code[t][j] = program[4 * t + j];
+    if (P.code[t][1] < 0 || P.code[t][1] >= kMaxRegs) return PFB_E_ARG;
+  }
+  for (int k = 0; k < n_out; ++k) {
+    if (out_regs[k] < 0 || out_regs[k] >= kMaxRegs) return PFB_E_ARG;
+    P.out_reg[k] = out_regs[k];
+    P.out_dt[k] = out_dtypes[k];
+  }
+  const std::string src = integer ? gen_source_int(P, false) : gen_source(P, v, false, modes);
+  return to_cubin(src).empty() ? 1 : 0;
 }

@@ -19,6 +19,16 @@ from paper_1903_04243_b200 import workloads as WL  # noqa: E402
 from paper_1903_04243_b200.executor import Executor  # noqa: E402
 
 
+def _shapes(fargs):
+    """shapes of the tensor descriptors among a launch's C-ABI arguments"""
+    out = []
+    for a in fargs:
+        a = getattr(a, "_obj", a)
+        if hasattr(a, "rank") and hasattr(a, "shape"):
+            out.append(tuple(a.shape[:a.rank]))
+    return " ".join(str(list(x)) for x in out)
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--config", default="cfg2_mlp")
@@ -56,12 +66,12 @@ def main():
             b.record()
             torch.cuda.synchronize()
             ts.append(a.elapsed_time(b) * 1e3)
-        rows.append((float(np.median(ts)), what, nbytes, flops))
+        rows.append((float(np.median(ts)), what, nbytes, flops, _shapes(fargs)))
     tot = sum(r[0] for r in rows)
     print(f"{args.config}: step (replayed) {step_us:.1f} us, {len(rows)} launches, "
           f"sum of isolated launches {tot:.1f} us")
     agg = collections.defaultdict(lambda: [0.0, 0, 0, 0])
-    for t, what, nb, fl in rows:
+    for t, what, nb, fl, _ in rows:
         a = agg[what]
         a[0] += t
         a[1] += 1
@@ -71,8 +81,8 @@ def main():
         print(f"  {what:14s} n={n:5d} {t:10.1f} us {100 * t / tot:5.1f}%  "
               f"{nb / max(t, 1e-9) / 1e3:8.1f} GB/s  {fl / max(t, 1e-9) / 1e6:8.2f} TFLOP/s")
     print("  slowest launches:")
-    for t, what, nb, fl in sorted(rows, reverse=True)[:args.top]:
-        print(f"    {t:9.2f} us  {what:14s} {nb / 1e6:9.2f} MB  {fl / 1e9:8.3f} GFLOP")
+    for t, what, nb, fl, shp in sorted(rows, reverse=True)[:args.top]:
+        print(f"    {t:9.2f} us  {what:14s} {nb / 1e6:9.2f} MB  {fl / 1e9:8.3f} GFLOP  {shp}")
 
 
 if __name__ == "__main__":
