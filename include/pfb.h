@@ -107,6 +107,8 @@ int pfb_fused_jit_check(int32_t integer, int32_t v, uint32_t modes, int32_t n_in
  * immediates; same encoding as pfb_fused_ew_multi): loop counters, index
  * arithmetic and masks of converted control flow (reference tensor.py:104-188
  * on i64/bool values), bit-exact with numpy int64 wraparound. */
+/* (an f32 output stores the register converted to float: the group's final
+ * cast i64 / bool -> f64, e.g. one-hot masks) */
 int pfb_fused_int(int32_t n_in, const pfb_tensor* ins, int32_t n_steps, const int32_t* program,
                   int32_t n_out, const int32_t* out_regs, pfb_tensor* outs, void* stream);
 int pfb_select(const pfb_tensor* mask, const pfb_tensor* a, const pfb_tensor* b, pfb_tensor* out,

@@ -638,6 +638,8 @@ __global__ void __launch_bounds__(256) fused_int_kernel(Layout L, IdxT n, FusedP
       const int64_t v = r[P.out_reg[k]];
       if (P.out_dt[k] == PFB_BOOL)
         reinterpret_cast<uint8_t*>(outs.p[k])[off[0]] = (uint8_t)(v != 0);
+      else if (P.out_dt[k] == PFB_F32)  // the group's final cast to f64 (fp32 storage)
+        reinterpret_cast<float*>(outs.p[k])[off[0]] = (float)v;
       else
         reinterpret_cast<long long*>(outs.p[k])[off[0]] = v;
     }
@@ -654,7 +656,8 @@ extern "C" int pfb_fused_int(int32_t n_in, const pfb_tensor* ins, int32_t n_step
   if (n_out < 1 || n_out > kMaxOuts) return PFB_E_ARG;
   const pfb_tensor* out = &outs[0];
   for (int k = 0; k < n_out; ++k) {
-    if (outs[k].dtype != PFB_I64 && outs[k].dtype != PFB_BOOL) return PFB_E_DTYPE;
+    if (outs[k].dtype != PFB_I64 && outs[k].dtype != PFB_BOOL && outs[k].dtype != PFB_F32)
+      return PFB_E_DTYPE;
     if (outs[k].rank != out->rank) return PFB_E_SHAPE;
     for (int d = 0; d < out->rank; ++d)
       if (outs[k].shape[d] != out->shape[d] ||

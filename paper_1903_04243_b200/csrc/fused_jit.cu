@@ -299,6 +299,8 @@ std::string gen_source_int(const FusedProgram& P, bool idx64) {
     if (P.out_dt[k] == PFB_BOOL)
       s += fmt("    reinterpret_cast<unsigned char*>(outs.p[%d])[off[0]] = (unsigned char)(", k) +
            R(P.out_reg[k]) + " != 0);\n";
+    else if (P.out_dt[k] == PFB_F32)
+      s += fmt("    reinterpret_cast<float*>(outs.p[%d])[off[0]] = (float)", k) + R(P.out_reg[k]) + ";\n";
     else
       s += fmt("    reinterpret_cast<long long*>(outs.p[%d])[off[0]] = ", k) + R(P.out_reg[k]) + ";\n";
   }

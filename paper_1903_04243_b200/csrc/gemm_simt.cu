@@ -432,6 +432,7 @@ static int simt_splits(const GemmArgs& g) {
   int64_t s = (kNumSMs + tiles - 1) / tiles;
   s = std::min<int64_t>(s, g.K / 32);
   s = std::min<int64_t>(s, 16);
+  if (const char* e = getenv("PFB_SIMT_SPLITS")) s = atoi(e);  // experiments
   return (int)std::max<int64_t>(s, 1);
 }
 

@@ -759,8 +759,14 @@ def _ew_eligible(g, node, domain="float"):
             return False
     elif k not in _INT_BIN and k not in _INT_UN and k not in ("cast", "select"):
         return False
-    if node.output_arity != 1 or node.out_dtypes[0] not in allowed:
+    if node.output_arity != 1:
         return False
+    if node.out_dtypes[0] not in allowed:
+        # an integer group may end in cast(i64 / bool -> f64) (one-hot and
+        # mask factors): its f64 output can only be the group's root, since
+        # no integer-domain op takes an f64 operand
+        if not (domain == "int" and k == "cast" and node.out_dtypes[0] == DType.F64):
+            return False
     sh = node.out_shapes[0]
     if sh is None or any(d is None for d in sh):
         return False
@@ -778,6 +784,8 @@ def _domains(g, node):
     if node.output_arity != 1:
         return ()
     dts = [node.out_dtypes[0]] + [g.ref_dtype(s_) for s_ in node.inputs]
+    if node.kind == "cast" and dts[0] == DType.F64 and dts[1] in (DType.I64, DType.BOOL):
+        return ("int", "float")  # i64 / bool -> f64: the end of an integer group
     if any(d == DType.I64 for d in dts):
         return ("int",)
     if any(d == DType.F64 for d in dts):

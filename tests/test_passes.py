@@ -215,3 +215,17 @@ def test_f5_derivative_epilogue():
     g, g3, m3 = _run_both(w3)
     live3 = _kinds(g3, [m3[tuple(o)] for o in g.outputs])
     assert any(n.kind == "matmul_ep" and n.attrs.get("dop") == "dtanh" for n in live3)
+
+
+def test_f3_integer_group_ending_in_float_cast():
+    """cfg4's per-step one-hot factor cast(equal(t, range), f64): the integer
+    compare and the cast to f64 are one `fused_int` launch with an f64
+    output (values unchanged, oracle)."""
+    from paper_1903_04243_b200.tensor import DType
+    w = WL.cfg4(WL.this_api(), n=3, steps=4, units=4)
+    g, g2, m = _run_both(w)
+    live = _kinds(g2, [m[tuple(o)] for o in g.outputs])
+    fi = [n for n in live if n.kind == "fused_int"]
+    assert any(DType.F64 in n.attrs["out_dtypes"] for n in fi)
+    assert not any(n.kind == "cast" and n.out_dtypes[0] == DType.F64 and
+                   g2.ref_dtype(n.inputs[0]) in (DType.BOOL, DType.I64) for n in live)
