@@ -1021,6 +1021,7 @@ struct RowCat {
   int64_t rows, inner;
   const void* x[kMaxCat];
   int64_t w[kMaxCat], off[kMaxCat];
+  int64_t rs[kMaxCat];  // input row stride (elements): w for a dense input
 };
 
 template <typename T, int V>
@@ -1034,9 +1035,9 @@ __global__ void __launch_bounds__(256) concat_rows_kernel(RowCat d, T* out) {
     const int64_t r = i / wv, c = i - r * wv;
     if constexpr (V == 4 && sizeof(T) == 4) {
       *reinterpret_cast<float4*>(out + r * d.inner + d.off[j] + 4 * c) =
-          __ldg(reinterpret_cast<const float4*>(x + r * d.w[j] + 4 * c));
+          __ldg(reinterpret_cast<const float4*>(x + r * d.rs[j] + 4 * c));
     } else {
-      out[r * d.inner + d.off[j] + c] = __ldg(x + r * d.w[j] + c);
+      out[r * d.inner + d.off[j] + c] = __ldg(x + r * d.rs[j] + c);
     }
   }
 }
@@ -1057,15 +1058,31 @@ static bool concat_rows(int32_t n, const pfb_tensor* xs, int32_t axis, pfb_tenso
   int64_t off = 0, most = 0;
   for (int j = 0; j < n; ++j) {
     const pfb_tensor* x = &xs[j];
-    if (x->dtype != out->dtype || x->rank != out->rank || !is_dense(x)) return false;
+    if (x->dtype != out->dtype || x->rank != out->rank) return false;
     for (int i = 0; i < out->rank; ++i)
       if (i != axis && x->shape[i] != out->shape[i]) return false;
+    // the input as [rows, w] rows: dims axis.. contiguous, dims ..axis one
+    // stride (a dense input, or a row-strided slice such as one time step
+    // of a [n, T, d] tensor)
+    int64_t expect = 1;
+    for (int i = out->rank - 1; i >= axis; --i) {
+      if (x->shape[i] != 1 && x->stride[i] != expect) return false;
+      expect *= x->shape[i];
+    }
+    int64_t rs = -1, next = -1;
+    for (int i = axis - 1; i >= 0; --i) {
+      if (x->shape[i] == 1) continue;
+      if (rs < 0) { rs = x->stride[i]; next = rs * x->shape[i]; continue; }
+      if (x->stride[i] != next) return false;
+      next *= x->shape[i];
+    }
     d.x[j] = x->data;
     d.w[j] = x->shape[axis] * post;
+    d.rs[j] = rs < 0 ? d.w[j] : rs;
     d.off[j] = off;
     off += d.w[j];
     most = std::max(most, d.rows * d.w[j]);
-    v4 = v4 && d.w[j] % 4 == 0 && d.off[j] % 4 == 0 &&
+    v4 = v4 && d.w[j] % 4 == 0 && d.off[j] % 4 == 0 && d.rs[j] % 4 == 0 &&
          (reinterpret_cast<uintptr_t>(x->data) & 15) == 0;
   }
   if (off != d.inner || most == 0) return off == d.inner;

@@ -709,10 +709,10 @@ static int64_t pair_need(const GemmArgs& g, int variant, int* am_out, int* bm_ou
   const int b_bc = g.sbb == 0 && g.batch > 1 && !(g.kscale && g.skb != 0);
   const int64_t ba = a_bc ? 1 : g.batch, bb = b_bc ? 1 : g.batch;
   int am = kPreSplit, bm = kPreSplit;
-  if (variant == 2) {
+  if (variant == 2 || variant == 3)  // 3: A raw, B pre-split
     am = raw_mode(g.A, g.M, g.K, ba, g.sab, g.sam, g.sak);
+  if (variant == 2 || variant == 4)  // 4: A pre-split, B raw
     bm = g.kscale ? kPreSplit : raw_mode(g.B, g.N, g.K, bb, g.sbb, g.sbn, g.sbk);
-  }
   *am_out = am;
   *bm_out = bm;
   return (am == kPreSplit ? 2 * align_up(ba * g.M * Kp * 4) : 0) +
@@ -828,6 +828,7 @@ int gemm_tcgen05(const GemmArgs& g, void* ws, int64_t ws_bytes, cudaStream_t s, 
   using namespace tc;
   if (!gemm_tcgen05_eligible(g)) return PFB_E_UNSUPPORTED;
   if (variant == 0) variant = (2.0 * g.M * g.N * g.K * g.batch < 4e9) ? 2 : 1;
+  if (const char* e = getenv("PFB_TC_VARIANT")) variant = atoi(e);  // experiments
   int am, bm;
   const int64_t need = pair_need(g, variant, &am, &bm);
   if (need > 0 && (ws == nullptr || ws_bytes < need)) return PFB_E_UNSUPPORTED;

@@ -415,3 +415,32 @@ def test_reference_random_corpus_on_device(Executor):
             if msg:
                 bad.append(f"{key} var {name}: {msg}")
     assert not bad, f"{len(bad)} mismatches: {bad[:8]}"
+
+
+@pytest.mark.parametrize("d,dt", [(512, "f32"), (6, "f32"), (8, "i64")])
+def test_concat_row_strided_slices(d, dt, Executor):
+    """concat([x[:, t, :], h], axis=1) with x[:, t, :] a row-strided slice of
+    [n, T, d] (cfg4's per-step GEMM operand): the row-copy path reads the
+    slice in place (vector and scalar variants), exact."""
+    import torch
+    from paper_1903_04243_b200 import _native as N
+    from paper_1903_04243_b200.executor import DArray
+    from paper_1903_04243_b200.tensor import DType
+    dev = torch.device("cuda")
+    n, T = 37, 5
+    tdt, DT = (torch.float32, DType.F64) if dt == "f32" else (torch.int64, DType.I64)
+    x = (torch.randn(n, T, d, device=dev) * 100).to(tdt)
+    h = (torch.randn(n, d + 4, device=dev) * 100).to(tdt)
+    out = torch.empty(n, 2 * d + 4, dtype=tdt, device=dev)
+    lib = N.lib()
+    for t in (0, 3):
+        X = DArray(x.reshape(-1), t * d, (n, d), (T * d, 1), DT)
+        H = DArray(h.reshape(-1), 0, tuple(h.shape), h.stride(), DT)
+        O = DArray(out.reshape(-1), 0, tuple(out.shape), out.stride(), DT)
+        descs = (N.PfbTensor * 2)(X.desc(), H.desc())
+        od = O.desc()
+        rc = lib.pfb_concat(2, descs, 1, od, torch.cuda.current_stream().cuda_stream)
+        assert rc == 0
+        torch.cuda.synchronize()
+        want = torch.cat([x[:, t, :], h], dim=1)
+        assert torch.equal(out, want)
