@@ -113,6 +113,11 @@ inline int grid_for(int64_t work, int block, int max_waves = 16) {
 // offsets of element `lin` (row-major over L.shape) for the first NOPS operands
 template <typename IdxT, int NOPS>
 __device__ __forceinline__ void offsets(const Layout& L, IdxT lin, int64_t* off) {
+  if (L.rank == 1) {  // collapsed to one dim (dense / scalar-broadcast operands): no division
+#pragma unroll
+    for (int o = 0; o < NOPS; ++o) off[o] = (int64_t)lin * L.st[o][0];
+    return;
+  }
 #pragma unroll
   for (int o = 0; o < NOPS; ++o) off[o] = 0;
   for (int d = L.rank - 1; d >= 0; --d) {

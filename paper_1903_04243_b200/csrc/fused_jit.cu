@@ -132,7 +132,9 @@ std::string gen_source(const FusedProgram& P, int V, bool idx64, uint32_t modes)
   s += fmt("  for (%s g = blockIdx.x * (%s)blockDim.x + threadIdx.x; g < ngroups; "
            "g += (%s)gridDim.x * blockDim.x) {\n", IT, IT, IT);
   s += fmt("    i64 off[%d];\n", nops);
-  s += fmt("    { %s lin = g * %d;\n", IT, V);
+  s += fmt("    if (L.rank == 1) { for (int o = 0; o < %d; ++o) off[o] = (i64)(g * %d) * L.st[o][0]; }\n",
+           nops, V);
+  s += fmt("    else { %s lin = g * %d;\n", IT, V);
   s += fmt("      for (int o = 0; o < %d; ++o) off[o] = 0;\n", nops);
   s += fmt("      for (int d = L.rank - 1; d >= 0; --d) {\n"
            "        %s sh = (%s)L.shape[d]; %s q = lin / sh; %s c = lin - q * sh; lin = q;\n"
@@ -248,7 +250,8 @@ std::string gen_source_int(const FusedProgram& P, bool idx64) {
   s += fmt("  for (%s e = blockIdx.x * (%s)blockDim.x + threadIdx.x; e < n; "
            "e += (%s)gridDim.x * blockDim.x) {\n", IT, IT, IT);
   s += fmt("    i64 off[%d];\n", nops);
-  s += fmt("    { %s lin = e;\n", IT);
+  s += fmt("    if (L.rank == 1) { for (int o = 0; o < %d; ++o) off[o] = (i64)e * L.st[o][0]; }\n", nops);
+  s += fmt("    else { %s lin = e;\n", IT);
   s += fmt("      for (int o = 0; o < %d; ++o) off[o] = 0;\n", nops);
   s += fmt("      for (int d = L.rank - 1; d >= 0; --d) {\n"
            "        %s sh = (%s)L.shape[d]; %s q = lin / sh; %s c = lin - q * sh; lin = q;\n"
