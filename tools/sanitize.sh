@@ -7,3 +7,7 @@ timeout 1500 compute-sanitizer --tool memcheck --leak-check no --print-limit 20 
 timeout 1500 compute-sanitizer --tool memcheck --leak-check no --print-limit 20 \
   python -m pytest tests/test_gpu_parity.py -q -x -k "kernel_vs_reference or worked_example or concat_many or replayed" \
   > gpurun_out/sanitize_parity.log 2>&1; echo "parity rc=$?"; tail -4 gpurun_out/sanitize_parity.log
+timeout 1500 compute-sanitizer --tool memcheck --leak-check no --print-limit 20 \
+  python -m pytest tests/test_gpu_jit.py tests/test_gpu_parity.py -q -x \
+  -k "hbm_scale or (specialised and (cfg2 or cfg5)) or row_strided or reduce" \
+  > gpurun_out/sanitize_jit.log 2>&1; echo "jit rc=$?"; tail -4 gpurun_out/sanitize_jit.log
