@@ -109,6 +109,8 @@ bool autotune_enabled() {
 int run_path(const GemmArgs& g, int path, void* ws, int64_t ws_bytes, cudaStream_t s) {
   switch (path) {
     case 1: return gemm_simt(g, ws, ws_bytes, s);
+    case 10: return gemm_simt_v(g, ws, ws_bytes, s, 4, false);  // SIMT, 4 k-splits (cluster)
+    case 11: return gemm_simt_v(g, ws, ws_bytes, s, 16, true);  // SIMT, 16 k-splits (workspace)
     case 3: return gemm_tcgen05(g, ws, ws_bytes, s, 1);
     case 4: return gemm_tcgen05(g, ws, ws_bytes, s, 2);
     case 7: return gemm_tcgen05(g, ws, ws_bytes, s, 2, 2);  // raw feed, 2 / 4 k-splits
@@ -143,7 +145,8 @@ extern "C" int64_t pfb_matmul_workspace(const pfb_tensor* a, const pfb_tensor* b
                                         pfb_tensor* out) {
   GemmArgs g;
   if (matmul_args(a, b, out, &g)) return 0;
-  return std::max(gemm_tcgen05_workspace(g), gemm_simt_workspace(g));
+  return std::max(std::max(gemm_tcgen05_workspace(g), gemm_simt_workspace(g)),
+                  gemm_simt_workspace_max(g));
 }
 
 static int matmul_impl(GemmArgs& g, pfb_tensor* out, int32_t force_path, void* ws,
@@ -228,7 +231,7 @@ static int matmul_impl(GemmArgs& g, pfb_tensor* out, int32_t force_path, void* w
   // 5 / 6 = CTA-pair tcgen05 (cta_group::2) with pre-split / raw operands.
   // PFB_DISABLE_TCGEN05=1 pins auto to SIMT (A/B testing, bring-up).
   static const bool tc_off = getenv("PFB_DISABLE_TCGEN05") && getenv("PFB_DISABLE_TCGEN05")[0] == '1';
-  if (force_path >= 1 && force_path <= 9) return run_path(g, force_path, ws, ws_bytes, s);
+  if (force_path >= 1 && force_path <= 11) return run_path(g, force_path, ws, ws_bytes, s);
   const bool tc_ok = !tc_off && gemm_tcgen05_eligible(g) &&
                      ws_bytes >= gemm_tcgen05_workspace(g) && ws != nullptr &&
                      (double)g.batch * g.M * g.N * g.K >= (double)(1 << 20);
@@ -245,9 +248,10 @@ static int matmul_impl(GemmArgs& g, pfb_tensor* out, int32_t force_path, void* w
     cudaStreamIsCapturing(s, &st);
     if (autotune_enabled() && !accumulate && st == cudaStreamCaptureStatusNone) {
       // every candidate runs twice; the last one timed leaves C computed
-      int cand[9];
+      int cand[11];
       int ncand = 0;
       cand[ncand++] = 1;
+      if (gemm_simt_splittable(g)) { cand[ncand++] = 10; cand[ncand++] = 11; }
       cand[ncand++] = 3;
       // forced k-splits only where tiles leave SMs idle (the model's split
       // choice is a heuristic; the timing decides)

@@ -59,6 +59,10 @@ __device__ __forceinline__ float kscale_at(const GemmArgs& g, int64_t b, int64_t
 }
 
 int gemm_simt(const GemmArgs& g, void* ws, int64_t ws_bytes, cudaStream_t s);
+int gemm_simt_v(const GemmArgs& g, void* ws, int64_t ws_bytes, cudaStream_t s, int splits_want,
+                bool ws_reduce);
+bool gemm_simt_splittable(const GemmArgs& g);
+int64_t gemm_simt_workspace_max(const GemmArgs& g);
 int64_t gemm_simt_workspace(const GemmArgs& g);
 // returns PFB_E_UNSUPPORTED when the shape/layout is not eligible
 // variant: 0 = auto, 1 = operands pre-split by split_kernel, 2 = raw operands

@@ -437,6 +437,7 @@ static int simt_splits(const GemmArgs& g) {
 }
 
 constexpr int kMaxSimtCluster = 16;  // non-portable cluster size (B200 supports 16)
+constexpr int kSimtWsSplits = 16;    // autotuner candidate: k-splits reduced through the workspace
 
 static bool cluster16_ok() {
   static int ok = -1;
@@ -477,14 +478,40 @@ static void launch_clustered(const GemmArgs& g, dim3 grid, int splits, int64_t k
   cudaLaunchKernelEx(&cfg, gemm_simt_kernel<KS, true>, g, splits, kchunk, (float*)nullptr);
 }
 
-int gemm_simt(const GemmArgs& g, void* ws, int64_t ws_bytes, cudaStream_t s) {
+bool gemm_simt_splittable(const GemmArgs& g) {
+  const int64_t tiles = ((g.N + BN - 1) / BN) * ((g.M + BM - 1) / BM) * g.batch;
+  return g.K > 16 && g.N > 16 && g.K >= 64 && tiles < kNumSMs &&
+         (int64_t)g.batch * g.M * g.N < 0x7fffffff;
+}
+
+int64_t gemm_simt_workspace_max(const GemmArgs& g) {
+  return gemm_simt_splittable(g) ? (int64_t)kSimtWsSplits * g.batch * g.M * g.N * 4 : 0;
+}
+
+// splits_want > 0 (autotuner candidates): that many k-splits, reduced over
+// DSMEM in one cluster (ws_reduce false, <= cluster limit) or through the
+// workspace by a second kernel (ws_reduce true; PFB_E_UNSUPPORTED when the
+// workspace is too small)
+int gemm_simt_v(const GemmArgs& g, void* ws, int64_t ws_bytes, cudaStream_t s, int splits_want,
+                bool ws_reduce) {
   if (g.batch == 0 || g.M == 0 || g.N == 0) return 0;
   if (g.K <= 16) return smallk_launch(g, s);
   // narrow N: warps per row (K split across up to 8 warps for few rows)
   if (g.N <= 16 && !getenv_flag("PFB_SIMT_NO_NARROW"))
     return narrow_launch(g, s);
   int splits = simt_splits(g);
-  const bool no_cluster = getenv_flag("PFB_SIMT_NO_CLUSTER");
+  bool no_cluster = getenv_flag("PFB_SIMT_NO_CLUSTER");
+  if (splits_want > 0) {
+    if (!gemm_simt_splittable(g)) return PFB_E_UNSUPPORTED;
+    splits = (int)std::max<int64_t>(1, std::min<int64_t>(splits_want, g.K / 32));
+    if (ws_reduce) {
+      if (ws == nullptr || ws_bytes < (int64_t)splits * g.batch * g.M * g.N * 4)
+        return PFB_E_UNSUPPORTED;
+      no_cluster = true;
+    } else {
+      splits = std::min(splits, cluster_cap());
+    }
+  }
   // the workspace path only when clusters cannot hold the splits (or are off)
   bool use_ws = splits > 1 && (no_cluster || splits > cluster_cap());
   if (use_ws && (ws == nullptr || ws_bytes < (int64_t)splits * g.batch * g.M * g.N * 4)) {
@@ -509,6 +536,10 @@ int gemm_simt(const GemmArgs& g, void* ws, int64_t ws_bytes, cudaStream_t s) {
   if (splits > 1)
     launch(splitk_reduce, grid_for(g.batch * g.M * g.N, 256), 256, 0, s, g, splits, (const float*)ws);
   return launch_status();
+}
+
+int gemm_simt(const GemmArgs& g, void* ws, int64_t ws_bytes, cudaStream_t s) {
+  return gemm_simt_v(g, ws, ws_bytes, s, 0, false);
 }
 
 }  // namespace pfb
