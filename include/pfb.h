@@ -92,6 +92,9 @@ int pfb_fused_ew_multi(int32_t n_in, const pfb_tensor* ins, int32_t n_steps,
  * interpreter kernel; enable = 0 forces the interpreter.  min_elems < 0 keeps
  * the threshold (default 0: every program; env PFB_JIT_MIN; PFB_NO_JIT=1 disables).
  * Returns 1 when the specialiser is available in this process. */
+/* number of kernels this library has launched in the process (a launch
+ * recorded into a CUDA graph counts once, at capture) */
+int64_t pfb_kernel_launches(void);
 int pfb_fused_jit_config(int32_t enable, int64_t min_elems);
 /* host-only check, no device: generate the specialised kernel for a program
  * (integer: i64/bool domain; v: 1 or 4 lanes; modes: 2-bit feed mode per

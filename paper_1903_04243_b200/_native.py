@@ -47,6 +47,7 @@ _SIGNATURES = {
     "pfb_fused_ew_multi": ([_i32, _P, _i32, ctypes.POINTER(_i32), _i32, ctypes.POINTER(_i32), _P,
                             _vp], ctypes.c_int),
     "pfb_fused_jit_config": ([_i32, ctypes.c_int64], ctypes.c_int),
+    "pfb_kernel_launches": ([], ctypes.c_int64),
     "pfb_fused_jit_check": ([_i32, _i32, _u32, _i32, ctypes.POINTER(_i32), _i32, ctypes.POINTER(_i32),
                              _i32, ctypes.POINTER(_i32), ctypes.POINTER(_i32)], ctypes.c_int),
     "pfb_fused_int": ([_i32, _P, _i32, ctypes.POINTER(_i32), _i32, ctypes.POINTER(_i32), _P,

@@ -1,5 +1,6 @@
 // Shared helpers for the libpfb kernels (sm_100a).
 #pragma once
+#include <atomic>
 #include <cuda_runtime.h>
 #include <stdint.h>
 #include <math.h>
@@ -153,9 +154,17 @@ inline bool pdl_enabled() {
   return on;
 }
 
+// kernels launched by this library (every launch site bumps it; the
+// executor reports the difference across a run or a graph capture)
+inline std::atomic<long long>& kernel_launches() {
+  static std::atomic<long long> n{0};
+  return n;
+}
+
 template <typename... KArgs, typename... Args>
 inline void launch(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s,
                    Args&&... args) {
+  kernel_launches()++;
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = grid;
   cfg.blockDim = block;

@@ -408,6 +408,7 @@ bool run(CUfunction fn, bool idx64, const Layout& L, int64_t nitems, const Fused
   for (int k = 0; k < 8; ++k) ip[k] = p[k];
   void* args[11] = {&Lc, idx64 ? (void*)&n64 : (void*)&n32, &oc, &ip[0], &ip[1], &ip[2], &ip[3],
                     &ip[4], &ip[5], &ip[6], &ip[7]};
+  kernel_launches()++;
   return driver().launch(&cfg, fn, args, nullptr) == CUDA_SUCCESS;
 }
 

@@ -585,6 +585,7 @@ static int launch_pair(const CUtensorMap& mah, const CUtensorMap& mal, const CUt
   at[1].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = at;
   cfg.numAttrs = pdl_enabled() ? 2 : 1;
+  kernel_launches()++;
   cudaLaunchKernelEx(&cfg, pair_kernel<BN, SINGLE>, mah, mal, mbh, mbl, mc, p);
   return launch_status();
 }

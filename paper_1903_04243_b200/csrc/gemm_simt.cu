@@ -475,6 +475,7 @@ static void launch_clustered(const GemmArgs& g, dim3 grid, int splits, int64_t k
   at[1].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = at;
   cfg.numAttrs = pdl_enabled() ? 2 : 1;
+  kernel_launches()++;
   cudaLaunchKernelEx(&cfg, gemm_simt_kernel<KS, true>, g, splits, kchunk, (float*)nullptr);
 }
 

@@ -812,6 +812,7 @@ static int launch_gemm(const GemmArgs& g, const PairFeed& f1, const PairFeed* f2
     at[1].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = at;
     cfg.numAttrs = pdl_enabled() ? 2 : 1;
+    kernel_launches()++;
     cudaLaunchKernelEx(&cfg, gemm_kernel, f1.ah, f1.al, f1.bh, f1.bl, mc, q.ah, q.al, q.bh, q.bl, p);
   } else {
     const int grid = (int)std::min<int64_t>(units, num_sms());

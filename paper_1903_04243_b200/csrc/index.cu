@@ -97,18 +97,23 @@ __global__ void check_cover(const int32_t* cnt, int64_t total, int32_t* err) {
   if (bits && (threadIdx.x & 31) == 0) set_err(err, bits);
 }
 
+// err != nullptr: an out-of-range row index is reported here (by the row's
+// first element) instead of by a separate bounds-check launch
 template <typename T, bool ADD>
 __global__ void __launch_bounds__(256) scatter_kernel(Layout Lt, int64_t k, int64_t D,
                                                       const int64_t* idx, int64_t idx_st,
                                                       int64_t total, const T* src, int64_t srow,
-                                                      T* out, int64_t orow) {
+                                                      T* out, int64_t orow, int32_t* err) {
   pdl_enter();
   const int64_t n = k * D;
   for (int64_t lin = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; lin < n;
        lin += (int64_t)gridDim.x * blockDim.x) {
     int64_t i = lin / D, t = lin - i * D;
     int64_t r = idx[i * idx_st];
-    if (r < 0 || r >= total) continue;  // reported by the bounds pass
+    if (r < 0 || r >= total) {
+      if (t == 0) set_err(err, PFB_DEV_OOB);
+      continue;
+    }
     int64_t off[2];
     offsets<int64_t, 2>(Lt, t, off);
     T v = src[i * srow + off[1]];
@@ -135,7 +140,7 @@ __global__ void check_bounds(const int64_t* idx, int64_t st, int64_t k, int64_t 
 
 template <typename T, bool ADD>
 int scatter_part(const pfb_tensor* idx, const pfb_tensor* src, int64_t total, pfb_tensor* out,
-                 cudaStream_t s) {
+                 int32_t* err, cudaStream_t s) {
   int64_t k = idx->rank == 0 ? 1 : idx->shape[0];
   int64_t idx_st = idx->rank == 0 ? 0 : idx->stride[0];
   int s0 = idx->rank == 0 ? 0 : 1;  // first tail dim of src
@@ -147,25 +152,30 @@ int scatter_part(const pfb_tensor* idx, const pfb_tensor* src, int64_t total, pf
     if (src->shape[s0 + d] != out->shape[1 + d]) return PFB_E_SHAPE;
     D *= out->shape[1 + d];
   }
-  if (k == 0 || D == 0) return 0;
+  if (k == 0) return 0;
+  if (D == 0) {  // empty rows: nothing moves, the indices are still checked
+    if (err) launch(check_bounds, grid_for(k, 256), 256, 0, s, (const int64_t*)idx->data, idx_st, k,
+                    total, err);
+    return launch_status();
+  }
   const int64_t* st[2] = {out->stride + 1, src->stride + s0};
   Layout Lt = make_layout(tail_rank, out->shape + 1, 2, st);
   int64_t srow = s0 ? src->stride[0] : 0;
   launch(scatter_kernel<T, ADD>, grid_for(k * D, 256), 256, 0, s, 
       Lt, k, D, (const int64_t*)idx->data, idx_st, total, (const T*)src->data, srow,
-      (T*)out->data, out->stride[0]);
+      (T*)out->data, out->stride[0], err);
   return launch_status();
 }
 
 template <bool ADD>
 int scatter_dispatch(const pfb_tensor* idx, const pfb_tensor* src, int64_t total, pfb_tensor* out,
-                     cudaStream_t s) {
+                     int32_t* err, cudaStream_t s) {
   switch (out->dtype) {
-    case PFB_F32: return scatter_part<float, ADD>(idx, src, total, out, s);
-    case PFB_I64: return scatter_part<int64_t, ADD>(idx, src, total, out, s);
+    case PFB_F32: return scatter_part<float, ADD>(idx, src, total, out, err, s);
+    case PFB_I64: return scatter_part<int64_t, ADD>(idx, src, total, out, err, s);
     default:
       if (ADD) return PFB_E_DTYPE;
-      return scatter_part<uint8_t, false>(idx, src, total, out, s);
+      return scatter_part<uint8_t, false>(idx, src, total, out, err, s);
   }
 }
 
@@ -345,17 +355,12 @@ extern "C" int pfb_scatter_rows(int32_t n_parts, const pfb_tensor* index_sets,
                                                  ws_count, dev_err);
     }
     launch(check_cover, grid_for(total, 256), 256, 0, s, ws_count, total, dev_err);
-  } else {
-    for (int p = 0; p < n_parts; ++p) {
-      const pfb_tensor* ix = &index_sets[p];
-      int64_t k = ix->rank == 0 ? 1 : ix->shape[0];
-      if (k) launch(check_bounds, grid_for(k, 256), 256, 0, s, (const int64_t*)ix->data,
-                                                           ix->rank ? ix->stride[0] : 0, k, total,
-                                                           dev_err);
-    }
   }
+  // (total == 0: every index is out of range; the scatter kernels report it)
   for (int p = 0; p < n_parts; ++p) {
-    if (int e = scatter_dispatch<false>(&index_sets[p], &parts[p], total, out, s)) return e;
+    if (int e = scatter_dispatch<false>(&index_sets[p], &parts[p], total, out,
+                                        total > 0 ? nullptr : dev_err, s))
+      return e;
   }
   return launch_status();
 }
@@ -367,11 +372,8 @@ extern "C" int pfb_scatter_add_rows(const pfb_tensor* idx, const pfb_tensor* upd
   cudaStream_t s = as_stream(stream);
   int64_t n = numel(out);
   if (n) cudaMemsetAsync(out->data, 0, n * dtype_size(out->dtype), s);
-  int64_t k = idx->rank == 0 ? 1 : idx->shape[0];
-  if (k) launch(check_bounds, grid_for(k, 256), 256, 0, s, (const int64_t*)idx->data,
-                                                       idx->rank ? idx->stride[0] : 0, k, total,
-                                                       dev_err);
-  if (int e = scatter_dispatch<true>(idx, updates, total, out, s)) return e;
+  // index bounds are checked inside the scatter kernel (one launch)
+  if (int e = scatter_dispatch<true>(idx, updates, total, out, dev_err, s)) return e;
   return launch_status();
 }
 

@@ -47,6 +47,7 @@ extern "C" int pfb_loop_create(void** loop, uint64_t* handle) {
 // `counter` (nullable, device u64) counts the invocations
 extern "C" int pfb_set_condition(uint64_t handle, const void* flag, void* counter,
                                  void* stream) {
+  kernel_launches()++;
   set_condition_kernel<<<1, 1, 0, as_stream(stream)>>>((cudaGraphConditionalHandle)handle,
                                                        (const uint8_t*)flag,
                                                        (unsigned long long*)counter);

@@ -111,3 +111,7 @@ extern "C" int pfb_pack(int32_t n, const pfb_tensor* xs, void* dst, const int64_
   }
   return 0;
 }
+
+// kernels this library has launched so far in the process (graph captures
+// included: a captured launch is counted once, when recorded)
+extern "C" int64_t pfb_kernel_launches(void) { return pfb::kernel_launches().load(); }

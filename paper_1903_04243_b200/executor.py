@@ -831,16 +831,21 @@ class Executor:
         brackets the launch with CUDA events on the executing stream and
         records (what, algorithmic bytes, flops, start, end) for roofline
         accounting."""
-        self.launch_count += 1
-        if self.kernel_timer is None:
+        # kernels, not entry points: the library's own launch counter (an
+        # entry point may launch several, e.g. operand split + GEMM)
+        k0 = self._lib.pfb_kernel_launches()
+        try:
+            if self.kernel_timer is None:
+                _raise_status(fn(*args), what)
+                return
+            st, en = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            st.record()
             _raise_status(fn(*args), what)
-            return
-        st, en = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        st.record()
-        _raise_status(fn(*args), what)
-        en.record()
-        nbytes, flops = work if work is not None else (0, 0)
-        self.kernel_timer.append((what, nbytes, flops, st, en, fn, args))
+            en.record()
+            nbytes, flops = work if work is not None else (0, 0)
+            self.kernel_timer.append((what, nbytes, flops, st, en, fn, args))
+        finally:
+            self.launch_count += self._lib.pfb_kernel_launches() - k0
 
     def _dense(self, x):
         if x.is_dense():
