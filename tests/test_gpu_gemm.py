@@ -370,3 +370,20 @@ def test_matmul_derivative_epilogue(env, force, dop):
     assert rc == 0, rc
     torch.cuda.synchronize()
     np.testing.assert_allclose(C.to_numpy().astype(np.float64), want, rtol=RTOL, atol=ATOL)
+
+
+@pytest.mark.parametrize("shape", [(128, 256, 784), (784, 256, 128), (37, 300, 1000), (3, 160, 96, 2)])
+@pytest.mark.parametrize("force", [10, 11])
+def test_gemm_simt_split_candidates(env, shape, force):
+    """The autotuner's SIMT k-split candidates (10: 4 splits reduced over
+    DSMEM in one cluster, 11: 16 splits reduced through the workspace), cfg2's
+    shapes plus ragged / batched ones."""
+    r = np.random.default_rng(sum(shape) + force)
+    if len(shape) == 4:
+        m, n, k, bsz = shape
+        a, b = _operands(r, (bsz, m, k), (bsz, k, n))
+    else:
+        m, n, k = shape
+        a, b = _operands(r, (m, k), (k, n))
+    got = _run(env, a, b, force, transpose_b=True)
+    np.testing.assert_allclose(got, a @ b, rtol=RTOL, atol=ATOL)
