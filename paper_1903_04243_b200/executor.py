@@ -560,7 +560,13 @@ class Executor:
             with torch.cuda.graph(graph):
                 self._stream = torch.cuda.current_stream(self.device).cuda_stream
                 env = self._run_graph(sub, {"capture": list(caps), "carried": static}, feeds)
-            outs = [env[tuple(o)] for o in sub.outputs]
+                outs = [env[tuple(o)] for o in sub.outputs]
+                # an output that is a static input or a view of one (a
+                # passthrough, a permutation of the carried values, a
+                # transpose) would be overwritten by the next trip's copy of
+                # the carried values into the static inputs: detach it
+                outs = [self._dense_copy(v) if isinstance(v, DArray) and _aliases(v, static)
+                        else v for v in outs]
             if all(isinstance(v, DArray) for v in outs):
                 cap = _Captured(graph, static, outs, self._ws, self._err, list(self._err_nodes))
                 cap.launches = self.launch_count - l0
@@ -654,8 +660,22 @@ class Executor:
                 outs = [benv[tuple(o)] for o in bg.outputs]
                 if not all(isinstance(v, DArray) for v in outs):
                     raise RuntimeError("loop body result is not on the device")
-                for src, dst in zip(outs, state):
-                    if src.size and (src.ptr != dst.ptr or src.strides != dst.strides):
+                # carried results that alias the loop state (a passthrough
+                # in another position, a permutation, a transposed view) are
+                # staged first, so no state buffer is overwritten before
+                # every result has been read
+                srcs = []
+                for j, src in enumerate(outs):
+                    same = (src.ptr == state[j].ptr and src.strides == state[j].strides
+                            and src.shape == state[j].shape)
+                    if same or not src.size:
+                        srcs.append(None)
+                    elif _aliases(src, state):
+                        srcs.append(self._dense_copy(src))
+                    else:
+                        srcs.append(src)
+                for src, dst in zip(srcs, state):
+                    if src is not None:
                         self._call(self._lib.pfb_copy, src.desc(), dst.desc(), self._stream,
                                    what="copy")
                 cond_to_handle()
@@ -1009,6 +1029,12 @@ class _Captured:
         self.host_pack = None
         self.launches = 0
         self.dispatches = 0
+
+
+def _aliases(v, arrays):
+    """True when DArray `v` shares storage with any of `arrays`."""
+    p = v.buf.untyped_storage().data_ptr()
+    return any(a.buf.untyped_storage().data_ptr() == p for a in arrays)
 
 
 def _feed_signature(feeds):

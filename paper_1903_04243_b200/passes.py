@@ -410,6 +410,27 @@ def _f5(rw, node):
 
 _NO_LICM = frozenset({"read_variable", "assign", "assign_add", "random_uniform", "placeholder",
                       "loop_var", "carried", "capture", "constant"})
+# ops that raise on their data (index out of range, scatter collision /
+# incomplete cover): hoisted out of a while body they would run -- and raise
+# -- on a zero-trip loop whose body the reference never evaluates
+_MAY_RAISE = frozenset({"gather_rows", "scatter_rows", "scatter_add_rows"})
+
+
+def _provably_safe(g, wnode, body, n):
+    """A raising op may still move when it cannot raise: a gather by a
+    constant index (in the body, or captured from a constant of the
+    enclosing graph) that is in range of x's static leading dimension."""
+    if n.kind != "gather_rows":
+        return False
+    src = body.nodes[n.inputs[1][0]]
+    if src.kind == "capture":
+        pref = wnode.inputs[wnode.block.num_carried + src.attrs["index"]]
+        src = g.nodes[pref[0]]
+    xs = body.ref_shape(tuple(n.inputs[0]))
+    if src.kind != "constant" or not xs or xs[0] is None:
+        return False
+    v = np.asarray(src.attrs["value"].data)
+    return bool(((v >= 0) & (v < xs[0])).all())
 
 
 def hoist_loop_invariants(g):
@@ -440,7 +461,8 @@ def _licm_while(g, wnode):
         if n.kind in ("capture", "constant"):
             inv.add(n.id)
         elif (n.kind not in _NO_LICM and n.block is None and n.inputs and not n.control_deps
-              and all(src in inv for src, _ in n.inputs)):
+              and all(src in inv for src, _ in n.inputs)
+              and (n.kind not in _MAY_RAISE or _provably_safe(g, wnode, body, n))):
             inv.add(n.id)
             movable.append(n)
     if not movable:

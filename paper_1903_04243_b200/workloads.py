@@ -53,10 +53,23 @@ def _f32(a):
     return np.asarray(a, dtype=np.float32).astype(np.float64)
 
 
-def _pfor(api, b, body, n, shard, **kw):
+def _pfor(api, b, body, n, shard, mode="vectorize", **kw):
+    """`mode`: the reference's pfor modes (apps.py:28-45) -- "vectorize" (the
+    hot path), "parfor" (per-iteration SIMD interpreter) and "fallback"
+    (every op through the sequential while loop); the latter two are the
+    CPU loop baselines bench.py times beside the device."""
+    if mode != "vectorize":
+        kw["mode"] = mode
     if shard is not None:
         return api.pfor(b, body, n, shard=shard, **kw)
     return api.pfor(b, body, n, **kw)
+
+
+def _jac(api, b, y, w, shard, mode):
+    kw = {} if mode == "vectorize" else {"mode": mode}
+    if shard is not None:
+        kw["shard"] = shard
+    return api.jacobian(b, y, w, **kw)
 
 
 # ----------------------------------------------------------------------------
@@ -70,7 +83,8 @@ def _mlp_params(r, d_in, d_h, d_out):
     return W1, b1, W2, b2
 
 
-def cfg1(api, batch=32, d_in=784, d_h=256, d_out=10, variant="batch", shard=None, registry=None):
+def cfg1(api, batch=32, d_in=784, d_h=256, d_out=10, variant="batch", shard=None, registry=None,
+         mode="vectorize"):
     """variant "batch": batch_jacobian [B,10,784] (pfor over examples of
     jacobian(y_b, x_b)); variant "full": jacobian(y, x) [B,10,B,784]."""
     r = np.random.default_rng(0)
@@ -87,19 +101,15 @@ def cfg1(api, batch=32, d_in=784, d_h=256, d_out=10, variant="batch", shard=None
 
     if variant == "full":
         y = net(b, x, batch)
-        if shard is not None:
-            J = api.jacobian(b, y, x, shard=shard)
-            units = shard[1] - shard[0]
-        else:
-            J = api.jacobian(b, y, x)
-            units = batch * d_out
+        J = _jac(api, b, y, x, shard, mode)
+        units = batch * d_out if shard is None else shard[1] - shard[0]
         b.graph.set_outputs([J])
     else:
         def body(bb, i):
             xb = bb.gather(x, i)
             yb = bb.reshape(net(bb, xb, 1), [d_out])
-            return [api.jacobian(bb, yb, xb)]
-        (J,) = _pfor(api, b, body, batch, shard, **kw)
+            return [_jac(api, bb, yb, xb, None, mode)]
+        (J,) = _pfor(api, b, body, batch, shard, mode, **kw)
         b.graph.set_outputs([J])
         units = (batch if shard is None else shard[1] - shard[0]) * d_out
     return Workload(f"cfg1_{variant}", b.graph, {"x": x0}, units, "jacobian rows",
@@ -138,7 +148,7 @@ def _maxpool2x2(bb, x, h, w):
 
 
 def cfg2(api, n=128, model="mlp", clip=1.0, materialize=False, shard=None, registry=None,
-         d_h=256):
+         d_h=256, mode="vectorize"):
     """model "mlp": 784-d_h-10 tanh; model "conv": reference bench mnist_like.
     Outputs: norms [n], per-parameter clipped sums (+ stacked clipped grads when
     `materialize`)."""
@@ -180,7 +190,7 @@ def cfg2(api, n=128, model="mlp", clip=1.0, materialize=False, shard=None, regis
         return [norm] + clipped
 
     kw = {} if registry is None else {"registry": registry}
-    outs = _pfor(api, b, body, n, shard, **kw)
+    outs = _pfor(api, b, body, n, shard, mode, **kw)
     norms, stacked = outs[0], outs[1:]
     sums = [b.reduce_sum(s, [0]) for s in stacked]
     b.graph.set_outputs([norms] + sums + (list(stacked) if materialize else []))
@@ -194,7 +204,7 @@ def cfg2(api, n=128, model="mlp", clip=1.0, materialize=False, shard=None, regis
 # ----------------------------------------------------------------------------
 # cfg3: full jacobian of a 4-layer FC net wrt all weights
 
-def cfg3(api, width=4096, out_dim=1024, rows=None, shard=None):
+def cfg3(api, width=4096, out_dim=1024, rows=None, shard=None, mode="vectorize"):
     """jacobian(y, W_l) for l = 0..3.  `shard=(lo, hi)` builds output rows
     lo..hi-1 only (the per-rank / per-chunk form); `rows` is a convenience for
     shard=(0, rows)."""
@@ -211,19 +221,13 @@ def cfg3(api, width=4096, out_dim=1024, rows=None, shard=None):
     y = b.reshape(b.matmul(h, cW[3]), [out_dim])
     if rows is not None and shard is None:
         shard = (0, rows)
-    outs = []
-    for l in range(4):
-        if shard is not None:
-            outs.append(api.jacobian(b, y, cW[l], shard=shard))
-        else:
-            outs.append(api.jacobian(b, y, cW[l]))
-    b.graph.set_outputs(outs)
+    b.graph.set_outputs([_jac(api, b, y, cW[l], shard, mode) for l in range(4)])
     units = out_dim if shard is None else shard[1] - shard[0]
     return Workload("cfg3", b.graph, {"x": x0}, units, "jacobian rows",
                     {"width": width, "out_dim": out_dim, "shard": shard})
 
 
-def cfg3_rows(api, width, out_dim, rows_idx):
+def cfg3_rows(api, width, out_dim, rows_idx, mode="vectorize"):
     """Reference-compatible row sampling (no shard= in the reference): the
     jacobian of gather(y, rows) -- SURVEY.md §8d."""
     r = np.random.default_rng(0)
@@ -238,7 +242,7 @@ def cfg3_rows(api, width, out_dim, rows_idx):
         h = b.tanh(b.matmul(h, cW[l]))
     y = b.reshape(b.matmul(h, cW[3]), [out_dim])
     ys = b.gather(y, b.const(np.asarray(rows_idx, dtype=np.int64)))
-    b.graph.set_outputs([api.jacobian(b, ys, cW[l]) for l in range(4)])
+    b.graph.set_outputs([_jac(api, b, ys, cW[l], None, mode) for l in range(4)])
     return Workload("cfg3_rows", b.graph, {"x": x0}, len(rows_idx), "jacobian rows",
                     {"width": width, "out_dim": out_dim, "rows": list(rows_idx)})
 
@@ -246,7 +250,7 @@ def cfg3_rows(api, width, out_dim, rows_idx):
 # ----------------------------------------------------------------------------
 # cfg4: per-example gradients of an unrolled 1-layer LSTM (reference bench cell)
 
-def cfg4(api, n=256, steps=64, units=512, shard=None, registry=None):
+def cfg4(api, n=256, steps=64, units=512, shard=None, registry=None, mode="vectorize"):
     r = np.random.default_rng(0)
     X0 = _f32(r.standard_normal((n, steps, units)))
     Wg0 = _f32(r.standard_normal((2 * units, 4 * units)) / 8.0)
@@ -275,7 +279,7 @@ def cfg4(api, n=256, steps=64, units=512, shard=None, registry=None):
         return api.gradient(bb.graph, loss, [bb._imp(Wg), bb._imp(Bg)], emit=bb)
 
     kw = {} if registry is None else {"registry": registry}
-    outs = _pfor(api, b, body, n, shard, **kw)
+    outs = _pfor(api, b, body, n, shard, mode, **kw)
     b.graph.set_outputs(outs)
     units_n = n if shard is None else shard[1] - shard[0]
     return Workload("cfg4", b.graph, {"x": X0}, units_n, "per-example gradients",
@@ -286,7 +290,7 @@ def cfg4(api, n=256, steps=64, units=512, shard=None, registry=None):
 # cfg5: auto-batched variable-length RNN (per-example while + cond)
 
 def cfg5(api, n=1024, max_len=100, units=256, shard=None, registry=None, masked=False,
-         unroll=1):
+         unroll=1, mode="vectorize"):
     """`masked=True` converts the per-example while/cond with predication
     (Policy(masked_control=True)) instead of the reference's compaction:
     same values, fixed shapes (CUDA-graph capturable loop body)."""
@@ -323,7 +327,7 @@ def cfg5(api, n=1024, max_len=100, units=256, shard=None, registry=None, masked=
     if masked:
         from .vectorize import Policy
         kw["policy"] = Policy(masked_control=True, unroll=unroll)
-    (H,) = _pfor(api, b, body, n, shard, **kw)
+    (H,) = _pfor(api, b, body, n, shard, mode, **kw)
     b.graph.set_outputs([H])
     sel = slice(None) if shard is None else slice(shard[0], shard[1])
     units_n = n if shard is None else shard[1] - shard[0]
@@ -333,3 +337,61 @@ def cfg5(api, n=1024, max_len=100, units=256, shard=None, registry=None, masked=
 
 
 BUILDERS = {"cfg1": cfg1, "cfg2": cfg2, "cfg3": cfg3, "cfg4": cfg4, "cfg5": cfg5}
+
+
+# ----------------------------------------------------------------------------
+# bench configurations (bench.py lines and the bench-scale parity tests)
+
+# name: (builder, kwargs at bench size, unit, oracle sample)
+# The oracle sample is what the CPU checker can run in seconds at bench size:
+# None = the whole program; a list of shards = those iterations only
+# (sharded pfor is bit-identical to the unsharded one).
+BENCH_CONFIGS = {
+    "cfg4": ("cfg4", dict(n=256, steps=64, units=512), "per-example grads/s", [(0, 1), (255, 256)]),
+    "cfg2_mlp": ("cfg2", dict(n=128, model="mlp"), "per-example grads/s", None),
+    "cfg2_conv": ("cfg2", dict(n=128, model="conv"), "per-example grads/s", None),
+    "cfg1_batch": ("cfg1", dict(batch=32, variant="batch"), "jacobian rows/s", None),
+    "cfg1_full": ("cfg1", dict(batch=32, variant="full"), "jacobian rows/s", None),
+    "cfg3": ("cfg3", dict(width=4096, out_dim=1024, rows=32), "jacobian rows/s", [(0, 1), (31, 32)]),
+    "cfg5": ("cfg5", dict(n=1024, max_len=100, units=256, masked=True, unroll=4), "examples/s",
+             None),
+    "cfg5_compact": ("cfg5", dict(n=1024, max_len=100, units=256), "examples/s", None),
+}
+
+
+def bench_workload(name, world=1, rank=0, api=None, **over):
+    """The bench program of config `name` for one rank of `world`.
+
+    Weak scaling over the sharded iteration space: the global problem has
+    `world` times the per-GPU iterations and rank r runs the block
+    `dist.shard_range(total, world, r)` through `shard=(lo, hi)` -- distinct
+    jacobian rows (cfg1_full, cfg3) or distinct examples (cfg1_batch, cfg2,
+    cfg4, cfg5) per rank.  cfg5's examples are first dealt by length
+    (`dist.balanced_order`) so every rank gets a similar trip-count mix."""
+    from .dist import balanced_order, shard_range
+    api = api or this_api()
+    builder, kw, _, _ = BENCH_CONFIGS[name]
+    kw = dict(kw, **over)
+    if world == 1:
+        return BUILDERS[builder](api, **kw)
+    if name == "cfg3":
+        rows = kw.pop("rows")
+        lo, hi = shard_range(rows * world, world, rank)
+        return cfg3(api, shard=(lo, hi), **kw)
+    key = "batch" if builder == "cfg1" else "n"
+    per = kw[key]
+    total = per * world
+    kw[key] = total
+    if name == "cfg1_full":
+        lo, hi = shard_range(total * kw.get("d_out", 10), world, rank)
+    else:
+        lo, hi = shard_range(total, world, rank)
+    w = BUILDERS[builder](api, shard=(lo, hi), **kw)
+    if builder == "cfg5":
+        perm, _ = balanced_order(w.feeds["lengths"], world)
+        w.feeds = {k: np.ascontiguousarray(v[perm]) for k, v in w.feeds.items()}
+        w.meta["tokens"] = int(w.feeds["lengths"][lo:hi].sum())
+        w.meta["order"] = "dist.balanced_order"
+    w.meta["shard"] = (lo, hi)
+    w.meta["global_units"] = total * (kw.get("d_out", 10) if name == "cfg1_full" else 1)
+    return w
