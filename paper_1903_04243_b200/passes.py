@@ -406,6 +406,112 @@ def _f5(rw, node):
 
 
 # ----------------------------------------------------------------------------
+# F9: a column slice of a GEMM result -> a GEMM over the sliced columns
+
+_VIEW_KINDS = frozenset({"reshape", "transpose"})
+
+
+def _nonunit(shape):
+    return [(i, d) for i, d in enumerate(shape) if d != 1]
+
+
+def slice_matmul_columns(g, keep=()):
+    """F9 in place on `g` (a private copy).  matmul(A, B) whose only live
+    reader is a chain of views (reshape / transpose) ending in
+    gather_rows(., idx) along the GEMM's column axis, idx a constant vector,
+    becomes matmul(A, B[..., idx]) followed by the same views: only the
+    gathered columns are computed.  Each output element is the same dot
+    product as before (the K reduction does not depend on N), so values are
+    bit-identical.  In the LSTM backward (cfg4) the GEMM dz_t Wg^T yields the
+    cotangent of [x_t, h_{t-1}]; only the h half is live, so this halves
+    every backward-step GEMM.  Returns (count, moved outputs)."""
+    rw = _Rewriter(g, keep)
+    rw.replaced = {}
+    live = live_set(g, set(keep))
+    count = 0
+    for node in list(g.topo_order()):
+        if node.id in g.nodes and node.kind == "matmul" and node.id in live:
+            count += _f9(rw, node, live)
+    return count, rw.replaced
+
+
+def _f9(rw, node, live):
+    g = rw.g
+    key = (node.id, 0)
+    ysh = node.out_shapes[0]
+    if ysh is None or None in ysh or len(ysh) not in (2, 3) or key in rw.keep:
+        return 0
+    naxis = len(ysh) - 1  # the GEMM's column axis in the current value
+    chain = []
+    cur, shape = key, tuple(ysh)
+    while True:
+        us = [(n, i) for n, i in rw.users().get(cur, []) if n.id in live]
+        if len(us) != 1 or cur in rw.keep and cur != key:
+            return 0
+        u, _ = us[0]
+        if u.kind == "transpose":
+            perm = tuple(u.attrs["perm"])
+            naxis = perm.index(naxis)
+            chain.append(u)
+            cur, shape = (u.id, 0), tuple(u.out_shapes[0])
+        elif u.kind == "reshape":
+            osh = u.out_shapes[0]
+            if osh is None or None in osh:
+                return 0
+            a, b_ = _nonunit(shape), _nonunit(osh)
+            if [d for _, d in a] != [d for _, d in b_]:
+                return 0  # merges or splits real axes
+            pos = [j for j, (i, _) in enumerate(a) if i == naxis]
+            if not pos:
+                return 0
+            naxis = b_[pos[0]][0]
+            chain.append(u)
+            cur, shape = (u.id, 0), tuple(osh)
+        elif u.kind == "gather_rows" and u.inputs[0] == cur and naxis == 0:
+            idx_node = g.nodes[u.inputs[1][0]]
+            if idx_node.kind != "constant":
+                return 0
+            idx = np.asarray(idx_node.attrs["value"].data)
+            if idx.ndim != 1 or len(idx) >= ysh[-1] or u.id in rw.keep:
+                return 0
+            break
+        else:
+            return 0
+    b = rw.b
+    k = len(idx)
+    B = Ref(g, *node.inputs[1])
+    bsh = g.ref_shape(node.inputs[1])
+    r = len(bsh)
+    # B[..., idx]: bring the column axis to the front, gather, move it back
+    front = [r - 1] + list(range(r - 1))
+    back = list(range(1, r)) + [0]
+    Bs = b.transpose(b.gather(b.transpose(B, front), Ref(g, *u.inputs[1])), back)
+    y = b.matmul(Ref(g, *node.inputs[0]), Bs)
+    # replay the view chain with the column extent k
+    nax = len(ysh) - 1
+    for v in chain:
+        if v.kind == "transpose":
+            perm = tuple(v.attrs["perm"])
+            y = b.transpose(y, list(perm))
+            nax = perm.index(nax)
+        else:
+            osh = list(v.out_shapes[0])
+            cur_sh = g.ref_shape((y.nid, y.port))
+            a = _nonunit(cur_sh) if k != 1 else [(i, d) for i, d in enumerate(cur_sh)
+                                                  if d != 1 or i == nax]
+            j = [t for t, (i, _) in enumerate(a) if i == nax][0]
+            tgt = [i for i, d in enumerate(osh) if d != 1]
+            newax = tgt[j]
+            osh[newax] = k
+            y = b.reshape(y, osh)
+            nax = newax
+    if tuple(g.ref_shape((y.nid, y.port))) != tuple(u.out_shapes[0]):
+        return 0  # (leaves the added nodes dead; the executor's DCE drops them)
+    rw.redirect((u.id, 0), y)
+    return 1
+
+
+# ----------------------------------------------------------------------------
 # F8: loop-invariant code motion out of while bodies
 
 _NO_LICM = frozenset({"read_variable", "assign", "assign_add", "random_uniform", "placeholder",
@@ -699,6 +805,8 @@ def fuse_row_dots(g, keep=()):
 
 
 def _optimize_in_place(g, keep, elementwise=True):
+    _, moved9 = slice_matmul_columns(g, keep)
+    keep = [moved9.get(k, k) for k in keep]
     _, moved = fuse_outer_products(g, keep)
     keep = [moved.get(k, k) for k in keep]
     _, moved4 = fuse_reductions(g, keep)
@@ -731,6 +839,8 @@ def optimize(g, keep_keys, elementwise=True):
     hoist_loop_invariants(dst)
     _optimize_blocks(dst, elementwise)
     keep = [mapping[k] for k in keep_keys]
+    _, moved9 = slice_matmul_columns(dst, keep)
+    keep = [moved9.get(k, k) for k in keep]
     _, moved = fuse_outer_products(dst, keep)
     keep = [moved.get(k, k) for k in keep]
     _, moved4 = fuse_reductions(dst, keep)
@@ -746,6 +856,7 @@ def optimize(g, keep_keys, elementwise=True):
         _, moved3 = fuse_elementwise(dst, keep)
     final = {}
     for k, v in mapping.items():
+        v = moved9.get(v, v)
         v = moved.get(v, v)
         v = moved4.get(v, v)
         v = moved6.get(v, v)
@@ -998,6 +1109,7 @@ def fuse_elementwise(g, keep=()):
             built = build(root, group, domain)
         return None if built is None else (group, built)
 
+    groups = []  # [root, group, domain, built], reverse topo order of roots
     for root in reversed(topo):
         if root.id in assigned or root.id not in live:
             continue
@@ -1006,6 +1118,12 @@ def fuse_elementwise(g, keep=()):
         if not cands:
             continue
         domain, (group, built) = max(cands, key=lambda c: len(c[1][0]))
+        groups.append([root, group, domain, built])
+        assigned |= group
+
+    groups = _merge_groups(g, groups, users, pos, live, build)
+
+    for root, group, domain, built in groups:
         order, externals, outs, prog, regs = built
         if domain == "int":
             new = g.add_node("fused_int", externals,
@@ -1032,7 +1150,98 @@ def fuse_elementwise(g, keep=()):
             users[(new.id, k)] = set(ext)
             if key in keep:
                 moved[key] = (new.id, k)
-        assigned |= group
         fused += 1
     g._topo_cache = None
     return fused, moved
+
+
+def _merge_groups(g, groups, users, pos, live, build):
+    """Merge same-shape, same-domain elementwise groups that are siblings
+    (read a common tensor) or producer -> consumer, when the union has no
+    path leaving and re-entering it through other nodes (which would make the
+    fused node depend on itself) and its register program fits.  The LSTM
+    backward step's gate cotangents (four groups reading dh and the saved
+    gates) become one multi-output launch."""
+    by_node = {}
+    for gi, grp in enumerate(groups):
+        for nid in grp[1]:
+            by_node[nid] = gi
+    alive = [True] * len(groups)
+
+    def shape_of(grp):
+        return grp[0].out_shapes[0]
+
+    def inputs_of(grp):
+        return {src for nid in grp[1] for src in g.nodes[nid].inputs if src[0] not in grp[1]}
+
+    def creates_cycle(union):
+        """Is there a path union -> (other nodes / other groups, each group
+        contracted to one node) -> union?  Only nodes before the union's last
+        position can lead back into it."""
+        hi = max(pos[i] for i in union)
+        seen = set()
+        todo = [u for nid in union for p_ in range(g.nodes[nid].output_arity)
+                for u in users.get((nid, p_), ()) if u not in union]
+        while todo:
+            u = todo.pop()
+            if u in union:
+                return True
+            if u in seen or u not in pos:
+                continue
+            gi = by_node.get(u)
+            grouped = gi is not None and alive[gi]
+            if pos[u] > hi and not (grouped and min(pos[m] for m in groups[gi][1]) <= hi):
+                continue
+            seen.add(u)
+            members = groups[gi][1] if grouped else (u,)
+            for m in members:
+                seen.add(m)
+                for p_ in range(g.nodes[m].output_arity):
+                    for v in users.get((m, p_), ()):
+                        if v in union:
+                            return True
+                        if v not in seen:
+                            todo.append(v)
+        return False
+
+    changed = True
+    while changed:
+        changed = False
+        for bi, b in enumerate(groups):
+            if not alive[bi]:
+                continue
+            b_in = inputs_of(b)
+            related = set()
+            for src in b_in:
+                if src[0] in by_node:
+                    related.add(by_node[src[0]])  # producer group
+                for u in users.get(src, ()):
+                    if u in by_node:
+                        related.add(by_node[u])  # sibling reading the same tensor
+            related.discard(bi)
+            for ai in sorted(related, key=lambda i: -pos[groups[i][0].id]):
+                if not alive[ai] or not alive[bi]:
+                    continue
+                a = groups[ai]
+                if a[2] != b[2] or shape_of(a) != shape_of(b):
+                    continue
+                union = a[1] | b[1]
+                if creates_cycle(union):
+                    continue
+                root = a[0] if pos[a[0].id] > pos[b[0].id] else b[0]
+                built = build(root, union, a[2])
+                if built is None:
+                    continue
+                keep_i, drop_i = (ai, bi) if root is a[0] else (bi, ai)
+                groups[keep_i] = [root, union, a[2], built]
+                alive[drop_i] = False
+                for nid in union:
+                    by_node[nid] = keep_i
+                changed = True
+                if drop_i == bi:
+                    break
+                b = groups[bi]
+                b_in = inputs_of(b)
+    out = [grp for grp, ok in zip(groups, alive) if ok]
+    out.sort(key=lambda grp: -pos[grp[0].id])
+    return out

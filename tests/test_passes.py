@@ -229,3 +229,13 @@ def test_f3_integer_group_ending_in_float_cast():
     assert any(DType.F64 in n.attrs["out_dtypes"] for n in fi)
     assert not any(n.kind == "cast" and n.out_dtypes[0] == DType.F64 and
                    g2.ref_dtype(n.inputs[0]) in (DType.BOOL, DType.I64) for n in live)
+
+
+def test_f9_backward_gemm_computes_only_live_columns():
+    """cfg4: the backward GEMM dz_t Wg^T yields d[x_t, h]; only dh is live,
+    so after F9 every per-step backward GEMM has N = units, not 2*units."""
+    w = WL.cfg4(WL.this_api(), n=3, steps=4, units=4)
+    g, g2, m = _run_both(w)
+    live = _kinds(g2, [m[tuple(o)] for o in g.outputs])
+    bwd = [n for n in live if n.kind == "matmul" and len(n.out_shapes[0]) == 2]
+    assert bwd and all(n.out_shapes[0] == (3, 4) for n in bwd), [n.out_shapes for n in bwd]
