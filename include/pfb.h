@@ -197,6 +197,24 @@ int pfb_matmul_ep(const pfb_tensor* a, const pfb_tensor* b, pfb_tensor* out,
                   const pfb_tensor* dy, int32_t dop, const float* alpha_rows, int32_t accumulate,
                   int32_t force_path, void* ws, int64_t ws_bytes, void* stream);
 
+/* Pre-split weights: the tf32 hi / lo planes of a loop-invariant B operand
+ * ([K, N] or [batch, K, N] view, any strides), made once and reused by every
+ * GEMM that reads it (the executor caches them per constant weight -- the
+ * LSTM's Wg is read by 127 GEMMs per step).  pfb_gemm_planes_bytes: the
+ * buffer size (0: not splittable); pfb_gemm_split_planes writes it.
+ * pfb_matmul_ep2 / pfb_matmul_dual2 = pfb_matmul_ep / pfb_matmul_dual with the
+ * planes of B (nullable): the tcgen05 path then splits only A (3 products). */
+int64_t pfb_gemm_planes_bytes(const pfb_tensor* b);
+int pfb_gemm_split_planes(const pfb_tensor* b, void* planes, void* stream);
+int pfb_matmul_ep2(const pfb_tensor* a, const pfb_tensor* b, pfb_tensor* out,
+                   const pfb_tensor* kscale, const pfb_tensor* bias, int32_t act,
+                   const pfb_tensor* dy, int32_t dop, const void* b_planes, int32_t force_path,
+                   void* ws, int64_t ws_bytes, void* stream);
+int pfb_matmul_dual2(const pfb_tensor* a1, const pfb_tensor* b1, const pfb_tensor* a2,
+                     const pfb_tensor* b2, pfb_tensor* out, const pfb_tensor* bias, int32_t act,
+                     const void* b1_planes, const void* b2_planes, int32_t force_path, void* ws,
+                     int64_t ws_bytes, void* stream);
+
 /* device-resident while loops (csrc/loop.cu; reference interp.py:133-154 runs
  * the loop on the host): a CUDA graph with a conditional WHILE node.  The
  * caller captures a `head` graph (condition -> pfb_set_condition) and an

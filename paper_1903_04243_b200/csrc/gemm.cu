@@ -55,7 +55,8 @@ std::mutex g_mu;
 
 ShapeKey key_of(const GemmArgs& g) {
   return ShapeKey(g.batch, g.M, g.N, g.K, g.sak == 1, g.sam == 1, g.sbk == 1, g.sbn == 1,
-                  (g.sab == 0 ? 1 : (g.sbb == 0 ? 2 : 0)) + 4 * gemm_tcgen05_raw_possible(g));
+                  (g.sab == 0 ? 1 : (g.sbb == 0 ? 2 : 0)) + 4 * gemm_tcgen05_raw_possible(g) +
+                      8 * (g.b_hi != nullptr));
 }
 
 // PFB_GEMM_TUNE_FILE: persist choices across processes (a profiling run under
@@ -167,13 +168,71 @@ extern "C" int pfb_matmul_fused(const pfb_tensor* a, const pfb_tensor* b, pfb_te
                        force_path, ws, ws_bytes, stream);
 }
 
+static int matmul_ep_impl(const pfb_tensor* a, const pfb_tensor* b, pfb_tensor* out,
+                          const pfb_tensor* kscale, const pfb_tensor* bias, int32_t act,
+                          const pfb_tensor* dy, int32_t dop, const float* alpha_rows,
+                          int32_t accumulate, const void* b_planes, int32_t force_path, void* ws,
+                          int64_t ws_bytes, void* stream);
+
 extern "C" int pfb_matmul_ep(const pfb_tensor* a, const pfb_tensor* b, pfb_tensor* out,
                              const pfb_tensor* kscale, const pfb_tensor* bias, int32_t act,
                              const pfb_tensor* dy, int32_t dop, const float* alpha_rows,
                              int32_t accumulate, int32_t force_path, void* ws, int64_t ws_bytes,
                              void* stream) {
+  return matmul_ep_impl(a, b, out, kscale, bias, act, dy, dop, alpha_rows, accumulate, nullptr,
+                        force_path, ws, ws_bytes, stream);
+}
+
+// B as the GEMM consumes it: batch, K, N and the batch stride of a [K, N] or
+// [batch, K, N] view (batch stride 0 = one matrix shared by the batch)
+static bool planes_args(const pfb_tensor* b, GemmArgs* g) {
+  if (b->dtype != PFB_F32 || (b->rank != 2 && b->rank != 3)) return false;
+  const int r = b->rank;
+  *g = GemmArgs{r == 3 ? b->shape[0] : 1, 1, b->shape[r - 1], b->shape[r - 2],
+                nullptr, 0, 0, 1, (const float*)b->data, r == 3 ? b->stride[0] : 0,
+                b->stride[r - 2], b->stride[r - 1], nullptr, 0, 0, 1, nullptr, 0};
+  return g->K > 0 && g->N > 0;
+}
+
+static const float* planes_lo(const GemmArgs& g, const void* planes) {
+  return reinterpret_cast<const float*>(static_cast<const char*>(planes) + gemm_planes_bytes(g) / 2);
+}
+
+extern "C" int64_t pfb_gemm_planes_bytes(const pfb_tensor* b) {
+  GemmArgs g;
+  return planes_args(b, &g) ? gemm_planes_bytes(g) : 0;
+}
+
+extern "C" int pfb_gemm_split_planes(const pfb_tensor* b, void* planes, void* stream) {
+  GemmArgs g;
+  if (!planes_args(b, &g) || planes == nullptr) return PFB_E_ARG;
+  const int64_t Kp = (g.K + 3) / 4 * 4;
+  const int64_t bb = (g.sbb == 0 && g.batch > 1) ? 1 : g.batch;
+  float* hi = static_cast<float*>(planes);
+  tc_split_launch(g.B, bb, g.N, g.K, Kp, g.sbb, g.sbn, g.sbk, hi, const_cast<float*>(planes_lo(g, planes)),
+                  nullptr, 0, 0, as_stream(stream));
+  return launch_status();
+}
+
+extern "C" int pfb_matmul_ep2(const pfb_tensor* a, const pfb_tensor* b, pfb_tensor* out,
+                              const pfb_tensor* kscale, const pfb_tensor* bias, int32_t act,
+                              const pfb_tensor* dy, int32_t dop, const void* b_planes,
+                              int32_t force_path, void* ws, int64_t ws_bytes, void* stream) {
+  return matmul_ep_impl(a, b, out, kscale, bias, act, dy, dop, nullptr, 0, b_planes, force_path,
+                        ws, ws_bytes, stream);
+}
+
+static int matmul_ep_impl(const pfb_tensor* a, const pfb_tensor* b, pfb_tensor* out,
+                          const pfb_tensor* kscale, const pfb_tensor* bias, int32_t act,
+                          const pfb_tensor* dy, int32_t dop, const float* alpha_rows,
+                          int32_t accumulate, const void* b_planes, int32_t force_path, void* ws,
+                          int64_t ws_bytes, void* stream) {
   GemmArgs g;
   if (int e = matmul_args(a, b, out, &g)) return e;
+  if (b_planes != nullptr && kscale == nullptr) {
+    g.b_hi = static_cast<const float*>(b_planes);
+    g.b_lo = planes_lo(g, b_planes);
+  }
   g.alpha_rows = alpha_rows;
   g.accumulate = accumulate;
   if (act < PFB_ACT_NONE || act > PFB_ACT_RELU) return PFB_E_ARG;
@@ -351,9 +410,19 @@ extern "C" int pfb_matmul_dual(const pfb_tensor* a1, const pfb_tensor* b1, const
                                const pfb_tensor* b2, pfb_tensor* out, const pfb_tensor* bias,
                                int32_t act, int32_t force_path, void* ws, int64_t ws_bytes,
                                void* stream) {
+  return pfb_matmul_dual2(a1, b1, a2, b2, out, bias, act, nullptr, nullptr, force_path, ws,
+                          ws_bytes, stream);
+}
+
+extern "C" int pfb_matmul_dual2(const pfb_tensor* a1, const pfb_tensor* b1, const pfb_tensor* a2,
+                                const pfb_tensor* b2, pfb_tensor* out, const pfb_tensor* bias,
+                                int32_t act, const void* b1_planes, const void* b2_planes,
+                                int32_t force_path, void* ws, int64_t ws_bytes, void* stream) {
   GemmArgs g1, g2;
   if (int e = matmul_args(a1, b1, out, &g1)) return e;
   if (int e = matmul_args(a2, b2, out, &g2)) return e;
+  if (b1_planes) { g1.b_hi = static_cast<const float*>(b1_planes); g1.b_lo = planes_lo(g1, b1_planes); }
+  if (b2_planes) { g2.b_hi = static_cast<const float*>(b2_planes); g2.b_lo = planes_lo(g2, b2_planes); }
   if (act < PFB_ACT_NONE || act > PFB_ACT_RELU) return PFB_E_ARG;
   g1.act = act;
   if (bias) {
@@ -373,7 +442,8 @@ extern "C" int pfb_matmul_dual(const pfb_tensor* a1, const pfb_tensor* b1, const
                      ws_bytes >= gemm_tcgen05_dual_workspace(g1, g2) &&
                      (double)g1.batch * g1.M * g1.N * (g1.K + g2.K) >= (double)(1 << 20);
   if (!tc_ok) return dual_path(g1, g2, 1, out, ws, ws_bytes, s);
-  const auto key = std::make_tuple(key_of(g1), g2.K, (int)(g2.sak == 1) + 2 * (int)(g2.sbk == 1));
+  const auto key = std::make_tuple(key_of(g1), g2.K, (int)(g2.sak == 1) + 2 * (int)(g2.sbk == 1) +
+                                                      4 * (int)(g2.b_hi != nullptr));
   int path = 0;
   {
     std::lock_guard<std::mutex> lk(g_mu);

@@ -27,6 +27,12 @@ struct GemmArgs {
   const float* dy = nullptr;      // y, broadcast to (batch, M, N) by strides
   int64_t sdb = 0, sdm = 0, sdn = 0;
   int dop = 0;
+  // nullable: B's dense K-major tf32 hi / lo planes [bb][N][Kp], made once by
+  // pfb_gemm_split_planes for a loop-invariant weight (the executor caches
+  // them per constant); the tcgen05 path then reads B with no split at all
+  // and needs 3 products (B's RN split keeps the dropped lo*lo term unbiased)
+  const float* b_hi = nullptr;
+  const float* b_lo = nullptr;
   __host__ __device__ bool has_epi() const { return bias != nullptr || act != 0 || dop != 0; }
 };
 
@@ -85,6 +91,7 @@ bool gemm_tcgen05_profitable(const GemmArgs& g);  // size heuristic for auto
 // variant 1 = pre-split planes, 2 = raw TMA feed where the layout allows it
 int gemm_tcgen05_pair(const GemmArgs& g, void* ws, int64_t ws_bytes, cudaStream_t s, int variant);
 // dense K-major hi/lo tf32 planes [batch][rows][Kp] of an operand view
+int64_t gemm_planes_bytes(const GemmArgs& g);  // both planes of B (0: not splittable)
 void tc_split_launch(const float* x, int64_t batch, int64_t rows, int64_t K, int64_t Kp, int64_t sb,
                      int64_t sr, int64_t sk, float* hi, float* lo, const float* kscale,
                      int64_t skb, int64_t skk, cudaStream_t s);

@@ -660,6 +660,13 @@ int64_t gemm_tcgen05_workspace(const GemmArgs& g) {
   return 2 * tc::align_up(ba * g.M * Kp * 4) + 2 * tc::align_up(bb * g.N * Kp * 4);
 }
 
+int64_t gemm_planes_bytes(const GemmArgs& g) {
+  if (g.kscale) return 0;
+  const int64_t Kp = (g.K + 3) / 4 * 4;
+  const int64_t bb = (g.sbb == 0 && g.batch > 1) ? 1 : g.batch;
+  return 2 * tc::align_up(bb * g.N * Kp * 4);
+}
+
 bool gemm_tcgen05_eligible(const GemmArgs& g) {
   if (g.K < 8 || g.M < 1 || g.N < 8) return false;
   return !(g.M > (1ll << 31) || g.N > (1ll << 31) || g.K > (1ll << 31) || g.batch > 65535 ||
@@ -711,12 +718,12 @@ static int64_t pair_need(const GemmArgs& g, int variant, int* am_out, int* bm_ou
   int am = kPreSplit, bm = kPreSplit;
   if (variant == 2 || variant == 3)  // 3: A raw, B pre-split
     am = raw_mode(g.A, g.M, g.K, ba, g.sab, g.sam, g.sak);
-  if (variant == 2 || variant == 4)  // 4: A pre-split, B raw
+  if ((variant == 2 || variant == 4) && !g.b_hi)  // 4: A pre-split, B raw
     bm = g.kscale ? kPreSplit : raw_mode(g.B, g.N, g.K, bb, g.sbb, g.sbn, g.sbk);
   *am_out = am;
   *bm_out = bm;
   return (am == kPreSplit ? 2 * align_up(ba * g.M * Kp * 4) : 0) +
-         (bm == kPreSplit ? 2 * align_up(bb * g.N * Kp * 4) : 0);
+         (bm == kPreSplit && !g.b_hi ? 2 * align_up(bb * g.N * Kp * 4) : 0);
 }
 
 static int prep_pair(const GemmArgs& g, int variant, char*& w, cudaStream_t s, PairFeed* f) {
@@ -738,7 +745,10 @@ static int prep_pair(const GemmArgs& g, int variant, char*& w, cudaStream_t s, P
     if (!make_raw_map(&f->ah, f->am, g.A, g.M, g.K, ba, g.sab, g.sam, g.sak)) return PFB_E_UNSUPPORTED;
     f->al = f->ah;
   }
-  if (f->bm == kPreSplit) {
+  if (f->bm == kPreSplit && g.b_hi) {  // planes made once by pfb_gemm_split_planes
+    if (!make_map(&f->bh, g.b_hi, Kp, g.N, bb) || !make_map(&f->bl, g.b_lo, Kp, g.N, bb))
+      return PFB_E_UNSUPPORTED;
+  } else if (f->bm == kPreSplit) {
     float* bh = reinterpret_cast<float*>(w); w += align_up(bb * g.N * Kp * 4);
     float* bl = reinterpret_cast<float*>(w); w += align_up(bb * g.N * Kp * 4);
     dim3 gb((unsigned)((Kp + 31) / 32), (unsigned)((g.N + 31) / 32), (unsigned)bb);

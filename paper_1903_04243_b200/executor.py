@@ -280,6 +280,8 @@ class Executor:
         self._err_nodes = []
         self._dvars = {}
         self.kernel_timer = None
+        self._const_ctx = None
+        self._planes = {}
 
     # -- public API ------------------------------------------------------------
 
@@ -895,6 +897,15 @@ class Executor:
         for r in roots:
             remaining[r] = remaining.get(r, 0) + 1
         env = {}
+        saved_ctx = self._const_ctx
+        self._const_ctx = (g, plan.const_nodes)
+        try:
+            self._run_nodes(g, plan, env, binder, feeds, remaining)
+        finally:
+            self._const_ctx = saved_ctx
+        return env
+
+    def _run_nodes(self, g, plan, env, binder, feeds, remaining):
         for node in plan.order:
             hoist = (self.hoist_constants and node.id in plan.const_nodes
                      and node.kind != "constant")
@@ -915,7 +926,31 @@ class Executor:
                 remaining[key] = c
                 if c <= 0:
                     env.pop(key, None)
-        return env
+
+    def _b_planes(self, node, port, b):
+        """Pre-split tf32 hi/lo planes of a GEMM's B operand when it is a
+        loop-invariant constant (hoisted) -- made once per executor and
+        reused by every launch that reads that weight (pfb_gemm_split_planes).
+        Returns a device pointer or None."""
+        g, consts = self._const_ctx if self._const_ctx is not None else (None, ())
+        src = node.inputs[port]
+        if not self.hoist_constants or g is None or src[0] not in consts:
+            return None
+        key = (id(g), tuple(src))
+        ent = self._planes.get(key)
+        if ent is None:
+            if torch.cuda.is_current_stream_capturing():
+                return None
+            d = b.desc()
+            nbytes = self._lib.pfb_gemm_planes_bytes(d)
+            if nbytes <= 0:
+                self._planes[key] = ent = (None,)
+            else:
+                buf = torch.empty(nbytes, dtype=torch.uint8, device=self.device)
+                _raise_status(self._lib.pfb_gemm_split_planes(d, buf.data_ptr(), self._stream),
+                              "matmul")
+                self._planes[key] = ent = (buf,)
+        return None if ent[0] is None else ent[0].data_ptr()
 
     def _eval_node(self, g, node, env, binder, feeds):
         k = node.kind
@@ -1171,6 +1206,11 @@ def _h_matmul(ex, node, ins):
     ad, bd, od = a.desc(), b.desc(), out.desc()
     need = ex._lib.pfb_matmul_workspace(ad, bd, od)
     wp, wn = ex._ws_get(need) if need > 0 else (None, 0)
+    planes = ex._b_planes(node, 1, b)
+    if planes is not None:
+        ex._call(ex._lib.pfb_matmul_ep2, ad, bd, od, None, None, 0, None, 0, planes, 0,
+                 wp, wn, ex._stream, what="matmul", work=(_abytes(a, b, out), flops))
+        return [out]
     ex._call(ex._lib.pfb_matmul, ad, bd, od, wp, wn, ex._stream, what="matmul",
              work=(_abytes(a, b, out), flops))
     return [out]
@@ -1252,11 +1292,12 @@ def _h_matmul_ep(ex, node, ins):
     yd = dy.desc() if dy is not None else None
     need = ex._lib.pfb_matmul_workspace(ad, bd, od)
     wp, wn = ex._ws_get(need) if need > 0 else (None, 0)
-    ex._call(ex._lib.pfb_matmul_ep, ad, bd, od,
+    planes = ex._b_planes(node, 1, b) if ks is None else None
+    ex._call(ex._lib.pfb_matmul_ep2, ad, bd, od,
              ctypes.byref(kd) if kd is not None else None,
              ctypes.byref(xd) if xd is not None else None, _ACT_CODE[at.get("act")],
              ctypes.byref(yd) if yd is not None else None, _DOP_CODE[at.get("dop")],
-             None, 0, 0, wp, wn, ex._stream, what="matmul",
+             planes, 0, wp, wn, ex._stream, what="matmul",
              work=(_abytes(*[v for v in vals] + [out]), flops))
     return [out]
 
@@ -1289,8 +1330,9 @@ def _h_matmul2(ex, node, ins):
     xd = bias.desc() if bias is not None else None
     need = ex._lib.pfb_matmul_dual_workspace(d[0], d[1], d[2], d[3], od)
     wp, wn = ex._ws_get(need) if need > 0 else (None, 0)
-    ex._call(ex._lib.pfb_matmul_dual, d[0], d[1], d[2], d[3], od,
-             ctypes.byref(xd) if xd is not None else None, _ACT_CODE[at.get("act")], 0,
+    p1, p2 = ex._b_planes(node, 1, b1), ex._b_planes(node, 3, b2)
+    ex._call(ex._lib.pfb_matmul_dual2, d[0], d[1], d[2], d[3], od,
+             ctypes.byref(xd) if xd is not None else None, _ACT_CODE[at.get("act")], p1, p2, 0,
              wp, wn, ex._stream, what="matmul", work=(_abytes(*vals, out), flops))
     return [out]
 

@@ -15,6 +15,7 @@ from paper_1903_04243_b200.executor import DArray  # noqa: E402
 from paper_1903_04243_b200.tensor import DType  # noqa: E402
 
 GRAPH = False
+PLANES = False
 SHAPES = [(10240, 784, 256, 1), (256, 1024, 2048, 1), (256, 2048, 1024, 1),
           (4096, 4096, 4096, 1), (1024, 2048, 64, 64)]
 
@@ -35,10 +36,22 @@ def run(lib, m, n, k, bsz, force, iters):
     need = lib.pfb_matmul_workspace(ad, bd, cd)
     ws = torch.empty(max(need, 256), dtype=torch.uint8, device=dev)
     wp, wn = ws.data_ptr(), ws.numel()
+    planes = None
+    if PLANES:  # B's hi/lo planes made once (a loop-invariant weight)
+        pb = torch.empty(lib.pfb_gemm_planes_bytes(bd), dtype=torch.uint8, device=dev)
+        lib.pfb_gemm_split_planes(bd, pb.data_ptr(), s)
+        planes = pb.data_ptr()
+
+    def call(stream):
+        if planes is not None:
+            return lib.pfb_matmul_ep2(ad, bd, cd, None, None, 0, None, 0, planes, force, wp, wn,
+                                      stream)
+        return lib.pfb_matmul_ex(ad, bd, cd, None, 0, force, wp, wn, stream)
+
     for _ in range(3):
-        rc = lib.pfb_matmul_ex(ad, bd, cd, None, 0, force, wp, wn, s)
+        rc = call(s)
         if rc != 0:
-            raise RuntimeError(f"pfb_matmul_ex returned {rc}")
+            raise RuntimeError(f"matmul returned {rc}")
     torch.cuda.synchronize()
     st, en = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     if GRAPH:
@@ -48,7 +61,7 @@ def run(lib, m, n, k, bsz, force, iters):
         with torch.cuda.stream(cs):
             with torch.cuda.graph(g, stream=cs):
                 for _ in range(iters):
-                    lib.pfb_matmul_ex(ad, bd, cd, None, 0, force, wp, wn, cs.cuda_stream)
+                    call(cs.cuda_stream)
         g.replay()
         torch.cuda.synchronize()
         st.record()
@@ -63,7 +76,7 @@ def run(lib, m, n, k, bsz, force, iters):
     torch.cuda._sleep(int(20e6))
     st.record()
     for _ in range(iters):
-        lib.pfb_matmul_ex(ad, bd, cd, None, 0, force, wp, wn, s)
+        call(s)
     en.record()
     torch.cuda.synchronize()
     ms = st.elapsed_time(en) / iters
@@ -79,9 +92,11 @@ def main():
     ap.add_argument("--shape", type=int, nargs="+")
     ap.add_argument("--iters", type=int, default=20)
     ap.add_argument("--graph", action="store_true", help="time a replayed CUDA graph")
+    ap.add_argument("--planes", action="store_true", help="B pre-split once (pfb_matmul_ep2)")
     args = ap.parse_args()
-    global GRAPH
+    global GRAPH, PLANES
     GRAPH = args.graph
+    PLANES = args.planes
     lib = N.lib()
     shapes = [tuple(args.shape) + ((1,) if len(args.shape) == 3 else ())] if args.shape else SHAPES
     for shp in shapes:
