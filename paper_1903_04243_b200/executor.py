@@ -864,7 +864,7 @@ class Executor:
             st.record()
             _raise_status(fn(*args), what)
             en.record()
-            nbytes, flops = work if work is not None else (0, 0)
+            nbytes, flops = work if work is not None else (_desc_bytes(args), 0)
             self.kernel_timer.append((what, nbytes, flops, st, en, fn, args))
         finally:
             self.launch_count += self._lib.pfb_kernel_launches() - k0
@@ -1064,6 +1064,26 @@ class _Captured:
         self.host_pack = None
         self.launches = 0
         self.dispatches = 0
+
+
+_ITEMSIZE = {0: 4, 1: 8, 2: 1}  # pfb dtype codes: f32, i64, u8-bool
+
+
+def _desc_bytes(args):
+    """Default algorithmic bytes of a launch: every tensor descriptor among
+    its arguments read or written once (distinct elements, stride-0
+    broadcast axes counted once)."""
+    total = 0
+    for a in args:
+        ds = a if isinstance(a, ctypes.Array) and len(a) and isinstance(a[0], N.PfbTensor) else \
+            [a] if isinstance(a, N.PfbTensor) else ()
+        for d in ds:
+            n = 1
+            for i in range(d.rank):
+                if d.stride[i] != 0:
+                    n *= d.shape[i]
+            total += n * _ITEMSIZE.get(d.dtype, 4)
+    return total
 
 
 def _aliases(v, arrays):

@@ -112,6 +112,9 @@ def fuse_outer_products(g, keep=()):
             count += _f2(rw, node)
         elif node.kind == "reduce_sum":
             count += _f1(rw, node)
+    for node in list(g.topo_order()):  # after F2 has claimed its outer-product trees
+        if node.id in g.nodes and node.kind == "add":
+            count += _f11(rw, node)
     return count, rw.replaced
 
 
@@ -182,6 +185,46 @@ def _f2(rw, node):
     a_cat = b.concat([a for a, _ in leaves], 2)                       # [n, p, T]
     bt = b.concat([b.transpose(bb, [0, 2, 1]) for _, bb in leaves], 2)  # [n, q, T]
     out = b.matmul(a_cat, b.transpose(bt, [0, 2, 1]))                  # K-major B view
+    rw.redirect((node.id, 0), out)
+    return 1
+
+
+def _f11(rw, node, min_leaves=9):
+    """F11: a single-use add tree over T >= 9 same-shape leaves -> one
+    reduce_sum over the leaves stacked on a trailing axis (one launch instead
+    of T-1; smaller trees are left to F3, whose fused kernels take up to 8
+    inputs).  cfg4's per-example bias gradient dBg = sum_t dz_t: for [n,1,q]
+    leaves the stack is built exactly like F2's K-major B operand (the
+    transposed dz_t columns), so CSE then shares that concat and the sum
+    only reads it.  Summation order changes (fp32 rounding only)."""
+    g, b = rw.g, rw.b
+    shape = g.ref_shape((node.id, 0))
+    if shape is None or None in shape or not shape:
+        return 0
+    users = rw.users().get((node.id, 0), [])
+    if len(users) == 1 and users[0][0].kind == "add" and (node.id, 0) not in rw.keep:
+        up = users[0][0]
+        if g.ref_shape(up.inputs[0]) == g.ref_shape(up.inputs[1]) == shape:
+            return 0  # handled from the top of the tree
+    leaves, stack = [], [(node.id, 0)]
+    while stack:
+        key = stack.pop()
+        n = rw.node(key)
+        if n.kind == "add" and (key == (node.id, 0) or rw.single_use(key)) and \
+                g.ref_shape(n.inputs[0]) == g.ref_shape(n.inputs[1]) == shape:
+            stack.extend([n.inputs[1], n.inputs[0]])
+            continue
+        leaves.append(key)
+    if len(leaves) < min_leaves or g.ref_dtype((node.id, 0)) != g.ref_dtype(leaves[0]):
+        return 0
+    leaves.reverse()
+    refs = [Ref(g, *k) for k in leaves]
+    if len(shape) == 3 and shape[1] == 1:
+        cat = b.concat([b.transpose(r, [0, 2, 1]) for r in refs], 2)  # [n, q, T]
+        out = b.reshape(b.reduce_sum(cat, [2]), list(shape))
+    else:
+        cat = b.concat([b.reshape(r, list(shape) + [1]) for r in refs], len(shape))
+        out = b.reduce_sum(cat, [len(shape)])
     rw.redirect((node.id, 0), out)
     return 1
 
@@ -403,6 +446,82 @@ def _f5(rw, node):
         out = b.reshape(out, list(esh))
     rw.redirect(end, out)
     return 1
+
+
+# ----------------------------------------------------------------------------
+# F10: common-subexpression elimination
+
+_NO_CSE = frozenset({"read_variable", "assign", "assign_add", "random_uniform", "placeholder",
+                     "loop_var", "carried", "capture"})
+
+
+def _freeze(v):
+    """Hashable, value-exact key of an attribute value."""
+    from .tensor import TensorValue
+    if isinstance(v, TensorValue):
+        a = np.ascontiguousarray(v.data)
+        return ("T", v.dtype.value, a.dtype.str, a.shape, a.tobytes())
+    if isinstance(v, np.ndarray):
+        a = np.ascontiguousarray(v)
+        return ("A", a.dtype.str, a.shape, a.tobytes())
+    if isinstance(v, dict):
+        return ("D",) + tuple(sorted((k, _freeze(x)) for k, x in v.items()))
+    if isinstance(v, (list, tuple)):
+        return ("L",) + tuple(_freeze(x) for x in v)
+    if hasattr(v, "value") and hasattr(v, "name"):  # enums (DType)
+        return ("E", type(v).__name__, v.name)
+    return ("V", repr(v))
+
+
+def eliminate_common_subexpressions(g, keep=()):
+    """F10 in place on `g` (a private copy): pure, block-free nodes with the
+    same kind, attributes and (already merged) inputs -- constants compared by
+    value -- are computed once; their readers are redirected to the first.
+    `jacobian(y, W_l)` for several l (cfg3) builds one pfor per call, each
+    re-deriving the same backward chain from y (reference apps.py:59-80,
+    autodiff.py:181-200); after conversion those chains are identical
+    subgraphs and collapse into one.  Values are unchanged.  Returns
+    (count, moved outputs)."""
+    rw = _Rewriter(g, keep)
+    rw.replaced = {}
+    seen = {}
+    canon = {}  # (nid, port) -> canonical (nid, port)
+    count = 0
+    for node in list(g.topo_order()):
+        ins = tuple(canon.get(tuple(src), tuple(src)) for src in node.inputs)
+        if ins != tuple(tuple(x) for x in node.inputs):
+            node.inputs = list(ins)
+            g._topo_cache = None
+        if (node.kind in _NO_CSE or node.block is not None or node.control_deps
+                or node.output_arity == 0):
+            continue
+        try:
+            key = (node.kind, _freeze(node.attrs), ins)
+        except Exception:
+            continue
+        first = seen.get(key)
+        if first is None:
+            seen[key] = node.id
+            continue
+        for p in range(node.output_arity):
+            canon[(node.id, p)] = (first, p)
+            if (node.id, p) in rw.keep:
+                rw.keep.discard((node.id, p))
+                rw.keep.add((first, p))
+                rw.replaced[(node.id, p)] = (first, p)
+        count += 1
+    # readers created before a later duplicate was seen are already redirected
+    # (topological order); outputs of the graph itself:
+    g.outputs = [tuple(canon.get(tuple(o), tuple(o))) for o in g.outputs] if g.outputs else g.outputs
+    dup = {k[0]: v[0] for k, v in canon.items()}
+    for n in g.nodes.values():
+        if n.control_deps & dup.keys():
+            n.control_deps = {dup.get(d, d) for d in n.control_deps}
+    for nid in dup:  # the duplicates: no reader is left
+        g.nodes.pop(nid, None)
+    rw._users = None
+    g._topo_cache = None
+    return count, rw.replaced
 
 
 # ----------------------------------------------------------------------------
@@ -805,10 +924,14 @@ def fuse_row_dots(g, keep=()):
 
 
 def _optimize_in_place(g, keep, elementwise=True):
+    _, moved10 = eliminate_common_subexpressions(g, keep)
+    keep = [moved10.get(k, k) for k in keep]
     _, moved9 = slice_matmul_columns(g, keep)
     keep = [moved9.get(k, k) for k in keep]
     _, moved = fuse_outer_products(g, keep)
     keep = [moved.get(k, k) for k in keep]
+    _, moved10b = eliminate_common_subexpressions(g, keep)
+    keep = [moved10b.get(k, k) for k in keep]
     _, moved4 = fuse_reductions(g, keep)
     keep = [moved4.get(k, k) for k in keep]
     _, moved6 = fuse_row_dots(g, keep)
@@ -839,10 +962,14 @@ def optimize(g, keep_keys, elementwise=True):
     hoist_loop_invariants(dst)
     _optimize_blocks(dst, elementwise)
     keep = [mapping[k] for k in keep_keys]
+    _, moved10 = eliminate_common_subexpressions(dst, keep)
+    keep = [moved10.get(k, k) for k in keep]
     _, moved9 = slice_matmul_columns(dst, keep)
     keep = [moved9.get(k, k) for k in keep]
     _, moved = fuse_outer_products(dst, keep)
     keep = [moved.get(k, k) for k in keep]
+    _, moved10b = eliminate_common_subexpressions(dst, keep)
+    keep = [moved10b.get(k, k) for k in keep]
     _, moved4 = fuse_reductions(dst, keep)
     keep = [moved4.get(k, k) for k in keep]
     _, moved6 = fuse_row_dots(dst, keep)
@@ -856,8 +983,10 @@ def optimize(g, keep_keys, elementwise=True):
         _, moved3 = fuse_elementwise(dst, keep)
     final = {}
     for k, v in mapping.items():
+        v = moved10.get(v, v)
         v = moved9.get(v, v)
         v = moved.get(v, v)
+        v = moved10b.get(v, v)
         v = moved4.get(v, v)
         v = moved6.get(v, v)
         v = moved7.get(v, v)

@@ -239,3 +239,31 @@ def test_f9_backward_gemm_computes_only_live_columns():
     live = _kinds(g2, [m[tuple(o)] for o in g.outputs])
     bwd = [n for n in live if n.kind == "matmul" and len(n.out_shapes[0]) == 2]
     assert bwd and all(n.out_shapes[0] == (3, 4) for n in bwd), [n.out_shapes for n in bwd]
+
+
+def test_f10_cse_shares_the_backward_chain_of_the_jacobians():
+    """cfg3 builds jacobian(y, W_l) for l = 0..3, each re-deriving the
+    backward chain from y; after CSE the chain GEMMs run once: 3 forward
+    GEMMs + 3 chain GEMMs (the reference emits 3 + 6)."""
+    w = WL.cfg3(WL.this_api(), width=16, out_dim=8)
+    g, g2, m = _run_both(w)
+    live = _kinds(g2, [m[tuple(o)] for o in g.outputs])
+    gemms = [n for n in live if n.kind in ("matmul", "matmul_ep")
+             and g2.ref_shape(n.inputs[0])[-1] != 1]  # (K=1 outer products excluded)
+    assert len(gemms) == 6, [(n.kind, n.out_shapes) for n in gemms]
+
+
+def test_f11_long_add_chain_becomes_one_reduction_sharing_f2_operand():
+    """cfg4's bias gradient sum_t dz_t (T-1 adds) becomes one reduce_sum over
+    F2's K-major dz concat (shared through CSE): no add nodes remain."""
+    w = WL.cfg4(WL.this_api(), n=3, steps=12, units=4)
+    g, g2, m = _run_both(w)
+    live = _kinds(g2, [m[tuple(o)] for o in g.outputs])
+    assert not [n for n in live if n.kind == "add"]
+    red = [n for n in live if n.kind == "reduce_sum"]
+    assert len(red) == 1
+    cat = g2.nodes[red[0].inputs[0][0]]
+    assert cat.kind == "concat" and len(cat.inputs) == 12
+    # the same concat feeds the F2 GEMM (through its K-major transpose view)
+    readers = [n for n in live if any(tuple(s) == (cat.id, 0) for s in n.inputs)]
+    assert len(readers) == 2
