@@ -232,6 +232,15 @@ int pfb_im2col(const pfb_tensor* x, int32_t k1, int32_t k2, pfb_tensor* out, voi
 int pfb_conv2d(const pfb_tensor* x, const pfb_tensor* f, pfb_tensor* out, void* stream);
 int pfb_conv2d_input_grad(const pfb_tensor* gy, const pfb_tensor* f, pfb_tensor* out,
                           void* stream);
+/* per-example filter gradient, the conv2d VJP w.r.t. the filter without the
+ * im2col buffer (reference autodiff.py conv2d VJP: matmul(im2col(x)^T, gy),
+ * tensor.py:209-229; passes.fuse_conv_filter_grads):
+ *   out[b, (p*k2+q)*c + ci, o] = sum_{i,j} x[b, i+p-p1, j+q-p2, ci] gy[b, i, j, o]
+ * x [b,h,w,c], gy [b,h,w,o] dense, out [b, k1*k2*c, o]; sq_norm (nullable,
+ * [b]) receives each example's sum of squares (the per-example norm term).
+ * PFB_E_UNSUPPORTED where no tiled kernel exists for (k1*k2*c, o). */
+int pfb_conv2d_filter_grad(const pfb_tensor* x, const pfb_tensor* gy, int32_t k1, int32_t k2,
+                           pfb_tensor* out, pfb_tensor* sq_norm, void* stream);
 
 /* indexing (reference tensor.py:306-360, interp.py:210-221) */
 int pfb_gather_rows(const pfb_tensor* x, const pfb_tensor* idx, pfb_tensor* out,

@@ -65,6 +65,7 @@ _SIGNATURES = {
                       ctypes.c_int),
     "pfb_matmul_dual_workspace": ([_P, _P, _P, _P, _P], ctypes.c_int64),
     "pfb_gemm_planes_bytes": ([_P], ctypes.c_int64),
+    "pfb_conv2d_filter_grad": ([_P, _P, _i32, _i32, _P, _P, _vp], ctypes.c_int),
     "pfb_gemm_split_planes": ([_P, _vp, _vp], ctypes.c_int),
     "pfb_matmul_ep2": ([_P, _P, _P, _P, _P, _i32, _P, _i32, _vp, _i32, _vp, _i64, _vp],
                        ctypes.c_int),

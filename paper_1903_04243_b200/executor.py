@@ -1375,6 +1375,39 @@ def _h_conv(ex, node, ins):
     return [out]
 
 
+def _h_conv_filter_grad(ex, node, ins):
+    """conv_filter_grad (passes.fuse_conv_filter_grads): per-example filter
+    gradients im2col(x_b)^T gy_b in one launch without the im2col buffer
+    (pfb_conv2d_filter_grad); shapes without a tiled kernel run im2col + a
+    batched GEMM on the device instead."""
+    x, gy = (ex._dense(ex._dev(v)) for v in ins)
+    k1, k2 = node.attrs["k1"], node.attrs["k2"]
+    n, h, w, c = x.shape
+    o = gy.shape[3]
+    out = ex._empty((n, k1 * k2 * c, o), x.dtype)
+    flops = 2 * n * h * w * k1 * k2 * c * o
+    status = []
+
+    def fused(*args):  # PFB_E_UNSUPPORTED -> the im2col form below
+        rc = ex._lib.pfb_conv2d_filter_grad(*args)
+        status.append(rc)
+        return 0 if rc == N.E_UNSUPPORTED else rc
+    ex._call(fused, x.desc(), gy.desc(), k1, k2, out.desc(), None, ex._stream,
+             what="conv_filter_grad", work=(_abytes(x, gy, out), flops))
+    if status[-1] == 0:
+        return [out]
+    cols = ex._empty((n, h, w, k1 * k2 * c), x.dtype)
+    ex._call(ex._lib.pfb_im2col, x.desc(), k1, k2, cols.desc(), ex._stream, what="im2col")
+    a = cols.view((n, k1 * k2 * c, h * w), (h * w * k1 * k2 * c, 1, k1 * k2 * c))
+    b = gy.view((n, h * w, o), (h * w * o, o, 1))
+    ad, bd, od = a.desc(), b.desc(), out.desc()
+    need = ex._lib.pfb_matmul_workspace(ad, bd, od)
+    wp, wn = ex._ws_get(need) if need > 0 else (None, 0)
+    ex._call(ex._lib.pfb_matmul, ad, bd, od, wp, wn, ex._stream, what="matmul",
+             work=(_abytes(a, b, out), flops))
+    return [out]
+
+
 def _h_im2col(ex, node, ins):
     x = ex._dense(ex._dev(ins[0]))
     if x.rank != 4:
@@ -1763,6 +1796,7 @@ _HANDLERS.update({
     "cast": _h_cast, "matmul": _h_matmul, "conv2d": _h_conv, "conv2d_input_grad": _h_conv,
     "im2col": _h_im2col, "reduce_sum": _h_reduce_sum, "concat": _h_concat, "stack": _h_stack,
     "matmul_ep": _h_matmul_ep,
+    "conv_filter_grad": _h_conv_filter_grad,
     "row_dots": _h_row_dots,
     "fused_ewm": _h_fused_multi,
     "matmul2": _h_matmul2,

@@ -449,6 +449,65 @@ def _f5(rw, node):
 
 
 # ----------------------------------------------------------------------------
+# F12: per-example conv filter gradients without the im2col buffer
+
+def fuse_conv_filter_grads(g, keep=()):
+    """F12 in place on `g` (a private copy): the conv2d VJP's filter gradient
+    matmul(transpose(reshape(im2col(x))), reshape(gy)) -- per example
+    im2col(x_i)^T gy_i, reference autodiff.py conv2d VJP over tensor.py:209-229
+    -- becomes one `conv_filter_grad(x, gy)` node: a kernel that reads each
+    image window in shared memory and reduces the k1*k2*c x o filter gradient
+    in registers, so the [n, h, w, k1*k2*c] im2col buffer (9x the image for a
+    3x3 filter) is never written (cfg2 ConvNet).  Same sums, different order
+    (fp32 rounding).  Returns (count, moved outputs)."""
+    rw = _Rewriter(g, keep)
+    rw.replaced = {}
+    count = 0
+    for node in list(g.topo_order()):
+        if node.id in g.nodes and node.kind == "matmul":
+            count += _f12(rw, node)
+    return count, rw.replaced
+
+
+def _f12(rw, node):
+    g, b = rw.g, rw.b
+    out_sh = g.ref_shape((node.id, 0))
+    t = rw.node(node.inputs[0])
+    if out_sh is None or None in out_sh or t.kind != "transpose" or node.inputs[0][1] != 0:
+        return 0
+    batched = len(out_sh) == 3
+    if tuple(t.attrs["perm"]) != ((0, 2, 1) if batched else (1, 0)):
+        return 0
+    key = tuple(t.inputs[0])
+    flat = g.ref_shape(key)
+    while rw.node(key).kind == "reshape" and key[1] == 0:
+        key = tuple(rw.node(key).inputs[0])
+    im = rw.node(key)
+    if im.kind != "im2col" or key[1] != 0:
+        return 0
+    xsh = g.ref_shape(tuple(im.inputs[0]))
+    if xsh is None or None in xsh or len(xsh) != 4:
+        return 0
+    n, h, w, c = xsh
+    k1, k2 = im.attrs["k1"], im.attrs["k2"]
+    kc = k1 * k2 * c
+    if tuple(flat) != ((n, h * w, kc) if batched else (h * w, kc)) or (not batched and n != 1):
+        return 0
+    bsh = g.ref_shape(node.inputs[1])
+    if bsh is None or None in bsh or tuple(bsh[:-1]) != ((n, h * w) if batched else (h * w,)):
+        return 0
+    o = bsh[-1]
+    gy = b.reshape(Ref(g, *node.inputs[1]), [n, h, w, o])
+    new = g.add_node("conv_filter_grad", [tuple(im.inputs[0]), (gy.nid, gy.port)],
+                     {"k1": k1, "k2": k2})
+    out = Ref(g, new.id, 0)
+    if not batched:
+        out = b.reshape(out, [kc, o])
+    rw.redirect((node.id, 0), out)
+    return 1
+
+
+# ----------------------------------------------------------------------------
 # F10: common-subexpression elimination
 
 _NO_CSE = frozenset({"read_variable", "assign", "assign_add", "random_uniform", "placeholder",
@@ -930,6 +989,8 @@ def _optimize_in_place(g, keep, elementwise=True):
     keep = [moved9.get(k, k) for k in keep]
     _, moved = fuse_outer_products(g, keep)
     keep = [moved.get(k, k) for k in keep]
+    _, moved12 = fuse_conv_filter_grads(g, keep)
+    keep = [moved12.get(k, k) for k in keep]
     _, moved10b = eliminate_common_subexpressions(g, keep)
     keep = [moved10b.get(k, k) for k in keep]
     _, moved4 = fuse_reductions(g, keep)
@@ -968,6 +1029,8 @@ def optimize(g, keep_keys, elementwise=True):
     keep = [moved9.get(k, k) for k in keep]
     _, moved = fuse_outer_products(dst, keep)
     keep = [moved.get(k, k) for k in keep]
+    _, moved12 = fuse_conv_filter_grads(dst, keep)
+    keep = [moved12.get(k, k) for k in keep]
     _, moved10b = eliminate_common_subexpressions(dst, keep)
     keep = [moved10b.get(k, k) for k in keep]
     _, moved4 = fuse_reductions(dst, keep)
@@ -986,6 +1049,7 @@ def optimize(g, keep_keys, elementwise=True):
         v = moved10.get(v, v)
         v = moved9.get(v, v)
         v = moved.get(v, v)
+        v = moved12.get(v, v)
         v = moved10b.get(v, v)
         v = moved4.get(v, v)
         v = moved6.get(v, v)
