@@ -100,7 +100,7 @@ int pfb_fused_jit_config(int32_t enable, int64_t min_elems);
  * (integer: i64/bool domain; v: 1 or 4 lanes; modes: 2-bit feed mode per
  * operand, operand 0 = output) and compile it with NVRTC for sm_100a.
  * 0 = compiled, 1 = compile error, PFB_E_UNSUPPORTED = no NVRTC. */
-int pfb_fused_jit_check(int32_t integer, int32_t v, uint32_t modes, int32_t n_in,
+int pfb_fused_jit_check(int32_t integer, int32_t v, uint64_t modes, int32_t n_in,
                         const int32_t* in_dtypes, int32_t n_steps, const int32_t* program,
                         int32_t n_out, const int32_t* out_regs, const int32_t* out_dtypes);
 

@@ -48,7 +48,7 @@ _SIGNATURES = {
                             _vp], ctypes.c_int),
     "pfb_fused_jit_config": ([_i32, ctypes.c_int64], ctypes.c_int),
     "pfb_kernel_launches": ([], ctypes.c_int64),
-    "pfb_fused_jit_check": ([_i32, _i32, _u32, _i32, ctypes.POINTER(_i32), _i32, ctypes.POINTER(_i32),
+    "pfb_fused_jit_check": ([_i32, _i32, ctypes.c_uint64, _i32, ctypes.POINTER(_i32), _i32, ctypes.POINTER(_i32),
                              _i32, ctypes.POINTER(_i32), ctypes.POINTER(_i32)], ctypes.c_int),
     "pfb_fused_int": ([_i32, _P, _i32, ctypes.POINTER(_i32), _i32, ctypes.POINTER(_i32), _P,
                        _vp], ctypes.c_int),

@@ -39,19 +39,26 @@ inline bool is_dense(const pfb_tensor* t) {
   return true;
 }
 
-// A set of up to kMaxOps operands over one logical iteration shape, with dims
-// of size 1 dropped and adjacent dims merged wherever every operand allows it.
-// Operand 0 is conventionally the output.
+// A set of up to N operands over one logical iteration shape, with dims of
+// size 1 dropped and adjacent dims merged wherever every operand allows it.
+// Operand 0 is conventionally the output.  `Layout` (9 operands) serves the
+// elementwise / index kernels, `FLayout` (17) the fused programs.
 constexpr int kMaxOps = 9;
-struct Layout {
+constexpr int kMaxFOps = 17;
+template <int N>
+struct LayoutT {
   int rank;
   int nops;
   int64_t shape[kMaxRank];
-  int64_t st[kMaxOps][kMaxRank];
+  int64_t st[N][kMaxRank];
 };
+using Layout = LayoutT<kMaxOps>;
+using FLayout = LayoutT<kMaxFOps>;
 
-inline Layout make_layout(int rank, const int64_t* shape, int nops, const int64_t* const* strides) {
-  Layout L;
+template <int N = kMaxOps>
+inline LayoutT<N> make_layout(int rank, const int64_t* shape, int nops,
+                              const int64_t* const* strides) {
+  LayoutT<N> L;
   L.nops = nops;
   int r = 0;
   for (int d = 0; d < rank; ++d) {
@@ -112,8 +119,8 @@ inline int grid_for(int64_t work, int block, int max_waves = 16) {
 // --- device-side helpers -----------------------------------------------------
 
 // offsets of element `lin` (row-major over L.shape) for the first NOPS operands
-template <typename IdxT, int NOPS>
-__device__ __forceinline__ void offsets(const Layout& L, IdxT lin, int64_t* off) {
+template <typename IdxT, int NOPS, int N>
+__device__ __forceinline__ void offsets(const LayoutT<N>& L, IdxT lin, int64_t* off) {
   if (L.rank == 1) {  // collapsed to one dim (dense / scalar-broadcast operands): no division
 #pragma unroll
     for (int o = 0; o < NOPS; ++o) off[o] = (int64_t)lin * L.st[o][0];

@@ -466,13 +466,11 @@ __device__ __forceinline__ void store_v(void* base, int dt, int64_t off, int64_t
   }
 }
 
+// NIN: input slots compiled in (2 / 4 / 8 / 16, >= P.n_in)
 template <typename IdxT, int NIN, int V>
-__global__ void __launch_bounds__(256) fused_kernel(Layout L, IdxT ngroups, FusedProgram P,
-                                                    uint32_t modes, FusedOuts outs,
-                                                    const void* i0, const void* i1,
-                                                    const void* i2, const void* i3,
-                                                    const void* i4, const void* i5,
-                                                    const void* i6, const void* i7) {
+__global__ void __launch_bounds__(256) fused_kernel(FLayout L, IdxT ngroups, FusedProgram P,
+                                                    FeedModes modes, FusedOuts outs,
+                                                    FusedIns ins) {
   pdl_enter();
   __shared__ int4 prog[kMaxSteps];
   for (int s = threadIdx.x; s < P.n_steps; s += blockDim.x)
@@ -491,11 +489,11 @@ __global__ void __launch_bounds__(256) fused_kernel(Layout L, IdxT ngroups, Fuse
     Vec<V> in[NIN];
 #pragma unroll
     for (int K = 0; K < NIN; ++K) {
-      const void* ip = K == 0 ? i0 : K == 1 ? i1 : K == 2 ? i2 : K == 3 ? i3
-                     : K == 4 ? i4 : K == 5 ? i5 : K == 6 ? i6 : i7;
-      const int md = (modes >> (2 * (K + 1))) & 3;
-      in[K] = P.in_dtype[K] == PFB_BOOL ? load_v<V, uint8_t>(ip, off[K + 1], L.st[K + 1][ir], md)
-                                        : load_v<V, float>(ip, off[K + 1], L.st[K + 1][ir], md);
+      if (K >= P.n_in) break;
+      const int md = (int)((modes >> (2 * (K + 1))) & 3);
+      in[K] = P.in_dtype[K] == PFB_BOOL
+                  ? load_v<V, uint8_t>(ins.p[K], off[K + 1], L.st[K + 1][ir], md)
+                  : load_v<V, float>(ins.p[K], off[K + 1], L.st[K + 1][ir], md);
     }
     Vec<V> r[kMaxRegs];
     for (int s = 0; s < nsteps; ++s) {
@@ -508,6 +506,7 @@ __global__ void __launch_bounds__(256) fused_kernel(Layout L, IdxT ngroups, Fuse
     if (K < NIN) o = in[K < NIN ? K : 0]; \
     break;
           PFB_LD(0) PFB_LD(1) PFB_LD(2) PFB_LD(3) PFB_LD(4) PFB_LD(5) PFB_LD(6) PFB_LD(7)
+          PFB_LD(8) PFB_LD(9) PFB_LD(10) PFB_LD(11) PFB_LD(12) PFB_LD(13) PFB_LD(14) PFB_LD(15)
 #undef PFB_LD
         }
       } else if (c.x == F_CONST) {
@@ -554,19 +553,13 @@ __global__ void __launch_bounds__(256) fused_kernel(Layout L, IdxT ngroups, Fuse
 #undef PFB_EW2
 
 template <int V, typename IdxT>
-void launch_fused(int n_in, const Layout& L, IdxT ngroups, const FusedProgram& P, uint32_t modes,
-                  const FusedOuts& outs, const void* const* p, cudaStream_t s) {
+void launch_fused(int n_in, const FLayout& L, IdxT ngroups, const FusedProgram& P,
+                  FeedModes modes, const FusedOuts& outs, const FusedIns& ins, cudaStream_t s) {
   const int grid = grid_for((int64_t)ngroups, 256);
-#define PFB_FUSED_CASE(K)                                                                      \
-  case K:                                                                                      \
-    launch(fused_kernel<IdxT, K, V>, grid, 256, 0, s, L, ngroups, P, modes, outs, p[0], p[1],  \
-           p[2], p[3], p[4], p[5], p[6], p[7]);                                                \
-    break;
-  switch (n_in) {
-    PFB_FUSED_CASE(1) PFB_FUSED_CASE(2) PFB_FUSED_CASE(3) PFB_FUSED_CASE(4)
-    PFB_FUSED_CASE(5) PFB_FUSED_CASE(6) PFB_FUSED_CASE(7) PFB_FUSED_CASE(8)
-  }
-#undef PFB_FUSED_CASE
+  if (n_in <= 2) launch(fused_kernel<IdxT, 2, V>, grid, 256, 0, s, L, ngroups, P, modes, outs, ins);
+  else if (n_in <= 4) launch(fused_kernel<IdxT, 4, V>, grid, 256, 0, s, L, ngroups, P, modes, outs, ins);
+  else if (n_in <= 8) launch(fused_kernel<IdxT, 8, V>, grid, 256, 0, s, L, ngroups, P, modes, outs, ins);
+  else launch(fused_kernel<IdxT, 16, V>, grid, 256, 0, s, L, ngroups, P, modes, outs, ins);
 }
 
 // ---------------------------------------------------------------------------
@@ -576,12 +569,8 @@ void launch_fused(int n_in, const Layout& L, IdxT ngroups, const FusedProgram& P
 // numpy; constants are int32 immediates.  One element per thread (these
 // tensors are [n]-sized bookkeeping values).
 template <typename IdxT, int NIN>
-__global__ void __launch_bounds__(256) fused_int_kernel(Layout L, IdxT n, FusedProgram P,
-                                                        FusedOuts outs, const void* i0,
-                                                        const void* i1, const void* i2,
-                                                        const void* i3, const void* i4,
-                                                        const void* i5, const void* i6,
-                                                        const void* i7) {
+__global__ void __launch_bounds__(256) fused_int_kernel(FLayout L, IdxT n, FusedProgram P,
+                                                        FusedOuts outs, FusedIns ins) {
   pdl_enter();
   __shared__ int4 prog[kMaxSteps];
   for (int s = threadIdx.x; s < P.n_steps; s += blockDim.x)
@@ -594,11 +583,10 @@ __global__ void __launch_bounds__(256) fused_int_kernel(Layout L, IdxT n, FusedP
     int64_t in[NIN];
 #pragma unroll
     for (int K = 0; K < NIN; ++K) {
-      const void* ip = K == 0 ? i0 : K == 1 ? i1 : K == 2 ? i2 : K == 3 ? i3
-                     : K == 4 ? i4 : K == 5 ? i5 : K == 6 ? i6 : i7;
+      if (K >= P.n_in) break;
       in[K] = P.in_dtype[K] == PFB_BOOL
-                  ? (int64_t)__ldg(reinterpret_cast<const uint8_t*>(ip) + off[K + 1])
-                  : __ldg(reinterpret_cast<const long long*>(ip) + off[K + 1]);
+                  ? (int64_t)__ldg(reinterpret_cast<const uint8_t*>(ins.p[K]) + off[K + 1])
+                  : __ldg(reinterpret_cast<const long long*>(ins.p[K]) + off[K + 1]);
     }
     int64_t r[kMaxRegs];
     for (int s = 0; s < P.n_steps; ++s) {
@@ -608,6 +596,8 @@ __global__ void __launch_bounds__(256) fused_int_kernel(Layout L, IdxT n, FusedP
         switch (c.z) {
 #define PFB_LDI(K) case K: if (K < NIN) o = in[K < NIN ? K : 0]; break;
           PFB_LDI(0) PFB_LDI(1) PFB_LDI(2) PFB_LDI(3) PFB_LDI(4) PFB_LDI(5) PFB_LDI(6) PFB_LDI(7)
+          PFB_LDI(8) PFB_LDI(9) PFB_LDI(10) PFB_LDI(11) PFB_LDI(12) PFB_LDI(13) PFB_LDI(14)
+          PFB_LDI(15)
 #undef PFB_LDI
         }
       } else if (c.x == F_CONST) {
@@ -652,7 +642,7 @@ using namespace pfb;
 extern "C" int pfb_fused_int(int32_t n_in, const pfb_tensor* ins, int32_t n_steps,
                              const int32_t* program, int32_t n_out, const int32_t* out_regs,
                              pfb_tensor* outs, void* stream) {
-  if (n_in < 1 || n_in > 8 || n_steps < 1 || n_steps > kMaxSteps) return PFB_E_ARG;
+  if (n_in < 1 || n_in > kMaxIn || n_steps < 1 || n_steps > kMaxSteps) return PFB_E_ARG;
   if (n_out < 1 || n_out > kMaxOuts) return PFB_E_ARG;
   const pfb_tensor* out = &outs[0];
   for (int k = 0; k < n_out; ++k) {
@@ -665,8 +655,8 @@ extern "C" int pfb_fused_int(int32_t n_in, const pfb_tensor* ins, int32_t n_step
         return PFB_E_SHAPE;
     if (out_regs[k] < 0 || out_regs[k] >= kMaxRegs) return PFB_E_ARG;
   }
-  int64_t stb[8][kMaxRank];
-  const int64_t* st[kMaxOps];
+  int64_t stb[kMaxIn][kMaxRank];
+  const int64_t* st[kMaxFOps];
   st[0] = out->stride;
   FusedProgram P;
   P.n_in = n_in;
@@ -677,7 +667,7 @@ extern "C" int pfb_fused_int(int32_t n_in, const pfb_tensor* ins, int32_t n_step
     st[k + 1] = stb[k];
     P.in_dtype[k] = ins[k].dtype;
   }
-  for (int k = n_in; k < 8; ++k) P.in_dtype[k] = PFB_I64;
+  for (int k = n_in; k < kMaxIn; ++k) P.in_dtype[k] = PFB_I64;
   for (int s = 0; s < n_steps; ++s) {
     for (int j = 0; j < 4; ++j) P.code[s][j] = program[4 * s + j];
     if (P.code[s][1] < 0 || P.code[s][1] >= kMaxRegs) return PFB_E_ARG;
@@ -689,28 +679,22 @@ extern "C" int pfb_fused_int(int32_t n_in, const pfb_tensor* ins, int32_t n_step
     P.out_reg[k] = k < n_out ? out_regs[k] : 0;
     P.out_dt[k] = k < n_out ? outs[k].dtype : PFB_I64;
   }
-  Layout L = make_layout(out->rank, out->shape, n_in + 1, st);
+  FLayout L = make_layout<kMaxFOps>(out->rank, out->shape, n_in + 1, st);
   const int64_t n = numel(out);
   if (n == 0) return 0;
-  const void* p[8];
-  for (int k = 0; k < 8; ++k) p[k] = k < n_in ? ins[k].data : nullptr;
+  FusedIns fi;
+  for (int k = 0; k < kMaxIn; ++k) fi.p[k] = k < n_in ? ins[k].data : nullptr;
   cudaStream_t s = as_stream(stream);
-  if (fused_int_jit_launch(P, n >= (int64_t)0x7fffffff, L, n, fo, p, s)) return launch_status();
+  if (fused_int_jit_launch(P, n >= (int64_t)0x7fffffff, L, n, fo, fi, s)) return launch_status();
   const int grid = grid_for(n, 256);
-#define PFB_FI_CASE(K)                                                                         \
-  case K:                                                                                      \
-    if (n < (int64_t)0x7fffffff)                                                               \
-      launch(fused_int_kernel<uint32_t, K>, grid, 256, 0, s, L, (uint32_t)n, P, fo, p[0], p[1], \
-             p[2], p[3], p[4], p[5], p[6], p[7]);                                              \
-    else                                                                                       \
-      launch(fused_int_kernel<int64_t, K>, grid, 256, 0, s, L, n, P, fo, p[0], p[1], p[2],     \
-             p[3], p[4], p[5], p[6], p[7]);                                                    \
-    break;
-  switch (n_in) {
-    PFB_FI_CASE(1) PFB_FI_CASE(2) PFB_FI_CASE(3) PFB_FI_CASE(4)
-    PFB_FI_CASE(5) PFB_FI_CASE(6) PFB_FI_CASE(7) PFB_FI_CASE(8)
-  }
-#undef PFB_FI_CASE
+  const bool small = n < (int64_t)0x7fffffff;
+#define PFB_FI(K)                                                                              \
+  if (small) launch(fused_int_kernel<uint32_t, K>, grid, 256, 0, s, L, (uint32_t)n, P, fo, fi); \
+  else launch(fused_int_kernel<int64_t, K>, grid, 256, 0, s, L, n, P, fo, fi);
+  if (n_in <= 4) { PFB_FI(4) }
+  else if (n_in <= 8) { PFB_FI(8) }
+  else { PFB_FI(16) }
+#undef PFB_FI
   return launch_status();
 }
 
@@ -800,7 +784,7 @@ extern "C" int pfb_fill(pfb_tensor* out, double value, void* stream) {
 static int fused_impl(int32_t n_in, const pfb_tensor* ins, int32_t n_steps,
                       const int32_t* program, int32_t n_out, const int32_t* out_regs,
                       pfb_tensor* outs, void* stream) {
-  if (n_in < 1 || n_in > 8 || n_steps < 1 || n_steps > kMaxSteps) return PFB_E_ARG;
+  if (n_in < 1 || n_in > kMaxIn || n_steps < 1 || n_steps > kMaxSteps) return PFB_E_ARG;
   if (n_out < 1 || n_out > kMaxOuts) return PFB_E_ARG;
   const pfb_tensor* out = &outs[0];
   for (int k = 0; k < n_out; ++k) {
@@ -811,8 +795,8 @@ static int fused_impl(int32_t n_in, const pfb_tensor* ins, int32_t n_steps,
         return PFB_E_SHAPE;
     if (out_regs[k] < 0 || out_regs[k] >= kMaxRegs) return PFB_E_ARG;
   }
-  int64_t stb[8][kMaxRank];
-  const int64_t* st[kMaxOps];
+  int64_t stb[kMaxIn][kMaxRank];
+  const int64_t* st[kMaxFOps];
   st[0] = out->stride;
   FusedProgram P;
   P.n_in = n_in;
@@ -823,7 +807,7 @@ static int fused_impl(int32_t n_in, const pfb_tensor* ins, int32_t n_steps,
     st[k + 1] = stb[k];
     P.in_dtype[k] = ins[k].dtype;
   }
-  for (int k = n_in; k < 8; ++k) P.in_dtype[k] = PFB_F32;
+  for (int k = n_in; k < kMaxIn; ++k) P.in_dtype[k] = PFB_F32;
   for (int s = 0; s < n_steps; ++s) {
     for (int j = 0; j < 4; ++j) P.code[s][j] = program[4 * s + j];
     if (P.code[s][1] < 0 || P.code[s][1] >= kMaxRegs) return PFB_E_ARG;
@@ -835,11 +819,11 @@ static int fused_impl(int32_t n_in, const pfb_tensor* ins, int32_t n_steps,
     P.out_reg[k] = k < n_out ? out_regs[k] : 0;
     P.out_dt[k] = k < n_out ? outs[k].dtype : PFB_F32;
   }
-  Layout L = make_layout(out->rank, out->shape, n_in + 1, st);
+  FLayout L = make_layout<kMaxFOps>(out->rank, out->shape, n_in + 1, st);
   int64_t n = numel(out);
   if (n == 0) return 0;
-  const void* p[8];
-  for (int k = 0; k < 8; ++k) p[k] = k < n_in ? ins[k].data : nullptr;
+  FusedIns fi;
+  for (int k = 0; k < kMaxIn; ++k) fi.p[k] = k < n_in ? ins[k].data : nullptr;
   cudaStream_t s = as_stream(stream);
   const bool small = n < (int64_t)0x7fffffff;
   const int ir = L.rank - 1;
@@ -848,7 +832,7 @@ static int fused_impl(int32_t n_in, const pfb_tensor* ins, int32_t n_steps,
   // program's latency chain runs on 4x the warps
   const bool v4 = L.shape[ir] % 4 == 0 && !scalar_only && n >= 4096;
   // per-operand feed mode; the outputs share operand 0's (all must be aligned)
-  uint32_t modes = 0;
+  FeedModes modes = 0;
   for (int o = 0; o <= n_in; ++o) {
     bool vec = v4 && L.st[o][ir] == 1;
     if (o == 0) {
@@ -861,17 +845,17 @@ static int fused_impl(int32_t n_in, const pfb_tensor* ins, int32_t n_steps,
       vec = vec && (reinterpret_cast<uintptr_t>(ins[o - 1].data) % (4 * esz)) == 0;
     }
     for (int d = 0; d < ir && vec; ++d) vec = (L.st[o][d] % 4) == 0;
-    const uint32_t m = (L.st[o][ir] == 0 && o > 0) ? 1u : (vec ? 0u : 2u);
+    const FeedModes m = (L.st[o][ir] == 0 && o > 0) ? 1u : (vec ? 0u : 2u);
     modes |= m << (2 * o);
   }
   const int64_t ng = v4 ? n / 4 : n;
-  if (fused_jit_launch(P, v4 ? 4 : 1, !small, modes, L, ng, fo, p, s)) return launch_status();
+  if (fused_jit_launch(P, v4 ? 4 : 1, !small, modes, L, ng, fo, fi, s)) return launch_status();
   if (v4) {
-    if (small) launch_fused<4, uint32_t>(n_in, L, (uint32_t)ng, P, modes, fo, p, s);
-    else launch_fused<4, int64_t>(n_in, L, ng, P, modes, fo, p, s);
+    if (small) launch_fused<4, uint32_t>(n_in, L, (uint32_t)ng, P, modes, fo, fi, s);
+    else launch_fused<4, int64_t>(n_in, L, ng, P, modes, fo, fi, s);
   } else {
-    if (small) launch_fused<1, uint32_t>(n_in, L, (uint32_t)ng, P, modes, fo, p, s);
-    else launch_fused<1, int64_t>(n_in, L, ng, P, modes, fo, p, s);
+    if (small) launch_fused<1, uint32_t>(n_in, L, (uint32_t)ng, P, modes, fo, fi, s);
+    else launch_fused<1, int64_t>(n_in, L, ng, P, modes, fo, fi, s);
   }
   return launch_status();
 }

@@ -6,14 +6,15 @@
 
 namespace pfb {
 
-constexpr int kMaxSteps = 48;
-constexpr int kMaxRegs = 16;
+constexpr int kMaxSteps = 96;
+constexpr int kMaxRegs = 32;
+constexpr int kMaxIn = kMaxFOps - 1;  // 16 tensor inputs
 enum FusedOpc { F_LOAD = 64, F_CONST = 65, F_SELECT = 68 };
 
-constexpr int kMaxOuts = 8;
+constexpr int kMaxOuts = 12;
 struct FusedProgram {
   int n_in, n_steps;
-  int in_dtype[8];
+  int in_dtype[kMaxIn];
   int code[kMaxSteps][4];  // opcode, dst, src1, src2 (src1 = input / const bits)
   int n_out;               // outputs: registers stored after the program
   int out_reg[kMaxOuts];
@@ -24,17 +25,25 @@ struct FusedOuts {
   void* p[kMaxOuts];
 };
 
+struct FusedIns {
+  const void* p[kMaxIn];
+};
+
+// per-operand feed modes, 2 bits each (operand 0 = the outputs): 0 = 128-bit
+// vector, 1 = stride-0 broadcast, 2 = strided scalar
+using FeedModes = uint64_t;
+
 // Launch `P` as a kernel specialised to it (straight-line code, registers
 // in registers); false when the specialiser is unavailable or declines
 // (the caller then runs the interpreter kernel).  V, modes, ngroups, idx64
 // as for the interpreter launch.
-bool fused_jit_launch(const FusedProgram& P, int V, bool idx64, uint32_t modes, const Layout& L,
-                      int64_t ngroups, const FusedOuts& outs, const void* const* p,
+bool fused_jit_launch(const FusedProgram& P, int V, bool idx64, FeedModes modes, const FLayout& L,
+                      int64_t ngroups, const FusedOuts& outs, const FusedIns& ins,
                       cudaStream_t s);
 
 // the same for an integer-domain program (fused_int_kernel), one element per
 // thread
-bool fused_int_jit_launch(const FusedProgram& P, bool idx64, const Layout& L, int64_t n,
-                          const FusedOuts& outs, const void* const* p, cudaStream_t s);
+bool fused_int_jit_launch(const FusedProgram& P, bool idx64, const FLayout& L, int64_t n,
+                          const FusedOuts& outs, const FusedIns& ins, cudaStream_t s);
 
 }  // namespace pfb

@@ -101,6 +101,7 @@ const char* kPrelude = R"(
 typedef long long i64;
 struct Layout { int rank; int nops; i64 shape[%d]; i64 st[%d][%d]; };
 struct Outs { void* p[%d]; };
+struct Ins { const void* p[%d]; };
 __device__ __forceinline__ float np_max(float a, float b) {
   return (a != a) ? a : ((b != b) ? b : (a >= b ? a : b));
 }
@@ -118,16 +119,14 @@ std::string fmt(const char* f, ...) {
   return buf;
 }
 
-std::string gen_source(const FusedProgram& P, int V, bool idx64, uint32_t modes) {
-  std::string s = fmt(kPrelude, kMaxRank, kMaxOps, kMaxRank, kMaxOuts);
+std::string gen_source(const FusedProgram& P, int V, bool idx64, FeedModes modes) {
+  std::string s = fmt(kPrelude, kMaxRank, kMaxFOps, kMaxRank, kMaxOuts, kMaxIn);
   const char* IT = idx64 ? "i64" : "unsigned";
   const int nops = P.n_in + 1;
   s += fmt("extern \"C\" __global__ void __launch_bounds__(256) pfb_fused_jit(Layout L, %s ngroups, "
-           "Outs outs, const void* i0, const void* i1, const void* i2, const void* i3, "
-           "const void* i4, const void* i5, const void* i6, const void* i7) {\n", IT);
+           "Outs outs, Ins ins) {\n", IT);
   s += "  asm volatile(\"griddepcontrol.wait;\" ::: \"memory\");\n"
        "  asm volatile(\"griddepcontrol.launch_dependents;\" :::);\n"
-       "  const void* ins[8] = {i0, i1, i2, i3, i4, i5, i6, i7};\n"
        "  const int ir = L.rank - 1;\n";
   s += fmt("  for (%s g = blockIdx.x * (%s)blockDim.x + threadIdx.x; g < ngroups; "
            "g += (%s)gridDim.x * blockDim.x) {\n", IT, IT, IT);
@@ -142,10 +141,10 @@ std::string gen_source(const FusedProgram& P, int V, bool idx64, uint32_t modes)
            "      }\n    }\n", IT, IT, IT, IT, nops);
   // input feeds (all loads first, as in the interpreter)
   for (int k = 0; k < P.n_in; ++k) {
-    const int md = (modes >> (2 * (k + 1))) & 3;
+    const int md = (int)((modes >> (2 * (k + 1))) & 3);
     const bool bl = P.in_dtype[k] == PFB_BOOL;
     const char* T = bl ? "unsigned char" : "float";
-    s += fmt("    const %s* p%d = reinterpret_cast<const %s*>(ins[%d]) + off[%d];\n", T, k, T, k, k + 1);
+    s += fmt("    const %s* p%d = reinterpret_cast<const %s*>(ins.p[%d]) + off[%d];\n", T, k, T, k, k + 1);
     if (V == 4 && md == 0) {
       if (bl)
         s += fmt("    const uchar4 w%d = __ldg(reinterpret_cast<const uchar4*>(p%d));\n", k, k);
@@ -237,16 +236,14 @@ std::string gen_source(const FusedProgram& P, int V, bool idx64, uint32_t modes)
 // int64 wraparound through uint64 arithmetic, bool = 0/1, one element per
 // thread; ops the integer interpreter does not define move their operand
 std::string gen_source_int(const FusedProgram& P, bool idx64) {
-  std::string s = fmt(kPrelude, kMaxRank, kMaxOps, kMaxRank, kMaxOuts);
+  std::string s = fmt(kPrelude, kMaxRank, kMaxFOps, kMaxRank, kMaxOuts, kMaxIn);
   s += "typedef unsigned long long u64;\n";
   const char* IT = idx64 ? "i64" : "unsigned";
   const int nops = P.n_in + 1;
   s += fmt("extern \"C\" __global__ void __launch_bounds__(256) pfb_fused_jit(Layout L, %s n, "
-           "Outs outs, const void* i0, const void* i1, const void* i2, const void* i3, "
-           "const void* i4, const void* i5, const void* i6, const void* i7) {\n", IT);
+           "Outs outs, Ins ins) {\n", IT);
   s += "  asm volatile(\"griddepcontrol.wait;\" ::: \"memory\");\n"
-       "  asm volatile(\"griddepcontrol.launch_dependents;\" :::);\n"
-       "  const void* ins[8] = {i0, i1, i2, i3, i4, i5, i6, i7};\n";
+       "  asm volatile(\"griddepcontrol.launch_dependents;\" :::);\n";
   s += fmt("  for (%s e = blockIdx.x * (%s)blockDim.x + threadIdx.x; e < n; "
            "e += (%s)gridDim.x * blockDim.x) {\n", IT, IT, IT);
   s += fmt("    i64 off[%d];\n", nops);
@@ -259,10 +256,10 @@ std::string gen_source_int(const FusedProgram& P, bool idx64) {
            "      }\n    }\n", IT, IT, IT, IT, nops);
   for (int k = 0; k < P.n_in; ++k) {
     if (P.in_dtype[k] == PFB_BOOL)
-      s += fmt("    const i64 in%d = (i64)__ldg(reinterpret_cast<const unsigned char*>(ins[%d]) + off[%d]);\n",
+      s += fmt("    const i64 in%d = (i64)__ldg(reinterpret_cast<const unsigned char*>(ins.p[%d]) + off[%d]);\n",
                k, k, k + 1);
     else
-      s += fmt("    const i64 in%d = __ldg(reinterpret_cast<const long long*>(ins[%d]) + off[%d]);\n",
+      s += fmt("    const i64 in%d = __ldg(reinterpret_cast<const long long*>(ins.p[%d]) + off[%d]);\n",
                k, k, k + 1);
   }
   std::string reg[kMaxRegs];
@@ -366,13 +363,14 @@ void jit_init() {
 namespace {
 
 // kernel for a program (integer: the i64 domain), compiled on first use
-CUfunction lookup(const FusedProgram& P, int V, bool idx64, uint32_t modes, bool integer) {
+CUfunction lookup(const FusedProgram& P, int V, bool idx64, FeedModes modes, bool integer) {
   int dev = 0;
   cudaGetDevice(&dev);
   // cache key: the program's encoding and everything baked into the source
-  int32_t kb[9 + 8 + 4 * kMaxSteps + 2 * kMaxOuts];
+  int32_t kb[10 + kMaxIn + 4 * kMaxSteps + 2 * kMaxOuts];
   int nk = 0;
-  kb[nk++] = dev; kb[nk++] = V; kb[nk++] = idx64; kb[nk++] = (int32_t)modes; kb[nk++] = integer;
+  kb[nk++] = dev; kb[nk++] = V; kb[nk++] = idx64; kb[nk++] = (int32_t)(modes & 0xffffffffu);
+  kb[nk++] = (int32_t)(modes >> 32); kb[nk++] = integer;
   kb[nk++] = P.n_in; kb[nk++] = P.n_steps; kb[nk++] = P.n_out;
   for (int k = 0; k < P.n_in; ++k) kb[nk++] = P.in_dtype[k];
   for (int t = 0; t < P.n_steps; ++t)
@@ -389,8 +387,8 @@ CUfunction lookup(const FusedProgram& P, int V, bool idx64, uint32_t modes, bool
   return it->second;
 }
 
-bool run(CUfunction fn, bool idx64, const Layout& L, int64_t nitems, const FusedOuts& outs,
-         const void* const* p, cudaStream_t s) {
+bool run(CUfunction fn, bool idx64, const FLayout& L, int64_t nitems, const FusedOuts& outs,
+         const FusedIns& ins, cudaStream_t s) {
   CUlaunchConfig cfg = {};
   cfg.gridDimX = grid_for(nitems, 256); cfg.gridDimY = 1; cfg.gridDimZ = 1;
   cfg.blockDimX = 256; cfg.blockDimY = 1; cfg.blockDimZ = 1;
@@ -400,14 +398,12 @@ bool run(CUfunction fn, bool idx64, const Layout& L, int64_t nitems, const Fused
   attr[0].value.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
   cfg.numAttrs = pdl_enabled() ? 1 : 0;
-  Layout Lc = L;
+  FLayout Lc = L;
   FusedOuts oc = outs;
+  FusedIns ic = ins;
   uint32_t n32 = (uint32_t)nitems;
   int64_t n64 = nitems;
-  const void* ip[8];
-  for (int k = 0; k < 8; ++k) ip[k] = p[k];
-  void* args[11] = {&Lc, idx64 ? (void*)&n64 : (void*)&n32, &oc, &ip[0], &ip[1], &ip[2], &ip[3],
-                    &ip[4], &ip[5], &ip[6], &ip[7]};
+  void* args[4] = {&Lc, idx64 ? (void*)&n64 : (void*)&n32, &oc, &ic};
   kernel_launches()++;
   return driver().launch(&cfg, fn, args, nullptr) == CUDA_SUCCESS;
 }
@@ -419,19 +415,19 @@ bool usable(int64_t elems) {
 
 }  // namespace
 
-bool fused_jit_launch(const FusedProgram& P, int V, bool idx64, uint32_t modes, const Layout& L,
-                      int64_t ngroups, const FusedOuts& outs, const void* const* p,
+bool fused_jit_launch(const FusedProgram& P, int V, bool idx64, FeedModes modes, const FLayout& L,
+                      int64_t ngroups, const FusedOuts& outs, const FusedIns& ins,
                       cudaStream_t s) {
   if (!usable(ngroups * V)) return false;
   CUfunction fn = lookup(P, V, idx64, modes, false);
-  return fn && run(fn, idx64, L, ngroups, outs, p, s);
+  return fn && run(fn, idx64, L, ngroups, outs, ins, s);
 }
 
-bool fused_int_jit_launch(const FusedProgram& P, bool idx64, const Layout& L, int64_t n,
-                          const FusedOuts& outs, const void* const* p, cudaStream_t s) {
+bool fused_int_jit_launch(const FusedProgram& P, bool idx64, const FLayout& L, int64_t n,
+                          const FusedOuts& outs, const FusedIns& ins, cudaStream_t s) {
   if (!usable(n)) return false;
   CUfunction fn = lookup(P, 1, idx64, 0, true);
-  return fn && run(fn, idx64, L, n, outs, p, s);
+  return fn && run(fn, idx64, L, n, outs, ins, s);
 }
 
 }  // namespace pfb
@@ -450,12 +446,12 @@ extern "C" int pfb_fused_jit_config(int32_t enable, int64_t min_elems) {
 // program and compile it with NVRTC for sm_100a.  0 = compiled, 1 = compile
 // error (log on stderr), PFB_E_UNSUPPORTED = NVRTC not found, PFB_E_ARG = bad
 // program.  integer != 0 selects the i64/bool domain (v ignored).
-extern "C" int pfb_fused_jit_check(int32_t integer, int32_t v, uint32_t modes, int32_t n_in,
+extern "C" int pfb_fused_jit_check(int32_t integer, int32_t v, uint64_t modes, int32_t n_in,
                                    const int32_t* in_dtypes, int32_t n_steps,
                                    const int32_t* program, int32_t n_out, const int32_t* out_regs,
                                    const int32_t* out_dtypes) {
   using namespace pfb;
-  if (n_in < 1 || n_in > 8 || n_steps < 1 || n_steps > kMaxSteps || n_out < 1 ||
+  if (n_in < 1 || n_in > kMaxIn || n_steps < 1 || n_steps > kMaxSteps || n_out < 1 ||
       n_out > kMaxOuts || (v != 1 && v != 4))
     return PFB_E_ARG;
   if (!nvrtc().ok) return PFB_E_UNSUPPORTED;

@@ -25,6 +25,7 @@ from __future__ import annotations
 import ctypes
 import os
 import sys
+import warnings
 
 import numpy as np
 import torch
@@ -559,17 +560,24 @@ class Executor:
         try:
             torch.cuda.synchronize(self.device)
             l0, d0 = self.launch_count, self.dispatch_count
-            with torch.cuda.graph(graph):
-                self._stream = torch.cuda.current_stream(self.device).cuda_stream
-                env = self._run_graph(sub, {"capture": list(caps), "carried": static}, feeds)
-                outs = [env[tuple(o)] for o in sub.outputs]
-                # an output that is a static input or a view of one (a
-                # passthrough, a permutation of the carried values, a
-                # transpose) would be overwritten by the next trip's copy of
-                # the carried values into the static inputs: detach it
-                outs = [self._dense_copy(v) if isinstance(v, DArray) and _aliases(v, static)
-                        else v for v in outs]
-            if all(isinstance(v, DArray) for v in outs):
+            with warnings.catch_warnings():
+                # a body of views only records no work; it is run eagerly below
+                warnings.filterwarnings("ignore", message="The CUDA Graph is empty")
+                with torch.cuda.graph(graph):
+                    self._stream = torch.cuda.current_stream(self.device).cuda_stream
+                    env = self._run_graph(sub, {"capture": list(caps), "carried": static}, feeds)
+                    outs = [env[tuple(o)] for o in sub.outputs]
+                    # an output that is a static input or a view of one (a
+                    # passthrough, a permutation of the carried values, a
+                    # transpose) would be overwritten by the next trip's copy of
+                    # the carried values into the static inputs: detach it
+                    outs = [self._dense_copy(v) if isinstance(v, DArray) and _aliases(v, static)
+                            else v for v in outs]
+            if self.launch_count == l0:
+                # nothing to replay (every output a view of a capture): eager is free
+                self._capture_ok[(id(sub), tuple(tuple(o) for o in sub.outputs))] = False
+                self.launch_count, self.dispatch_count = l0, d0
+            elif all(isinstance(v, DArray) for v in outs):
                 cap = _Captured(graph, static, outs, self._ws, self._err, list(self._err_nodes))
                 cap.launches = self.launch_count - l0
                 cap.dispatches = self.dispatch_count - d0
@@ -1699,6 +1707,42 @@ def _h_fused_multi(ex, node, ins):
     return outs
 
 
+def _h_fused_pack(ex, node, ins):
+    """fused_pack (passes.place_concats): the group's outputs are slots of one
+    packed buffer along `pack_axis` (slot order `slots`, the concat's pieces
+    first); one multi-output launch writes them all, and the concat result is
+    a view of the first `cat_span` slots -- no copy, no extra launch."""
+    a = node.attrs
+    arrs = [ex._dev(v) for v in ins]
+    shape = ()
+    for x in arrs:
+        shape = broadcast_shapes(shape, x.shape)
+    n_out = len(a["out_regs"])
+    ax = a["pack_axis"]
+    ext = shape[ax]
+    bshape = list(shape)
+    bshape[ax] = ext * n_out
+    buf = ex._empty(tuple(bshape), DType.F64)
+    step = ext * buf.strides[ax]
+    outs = [None] * n_out
+    for slot, k in enumerate(a["slots"]):
+        outs[k] = buf.view(shape, buf.strides, slot * step)
+    cshape = list(shape)
+    cshape[ax] = ext * a["cat_span"]
+    cat = buf.view(tuple(cshape), buf.strides, 0)
+    prog = ex._programs.get(id(node))
+    if prog is None:
+        flat = [int(x) for st in a["program"] for x in st]
+        regs = [int(r) for r in a["out_regs"]]
+        prog = ex._programs[id(node)] = ((ctypes.c_int32 * len(flat))(*flat), len(a["program"]),
+                                         (ctypes.c_int32 * len(regs))(*regs), len(regs))
+    descs = (N.PfbTensor * len(arrs))(*[x.desc() for x in arrs])
+    odescs = (N.PfbTensor * n_out)(*[o.desc() for o in outs])
+    ex._call(ex._lib.pfb_fused_ew_multi, len(arrs), descs, prog[1], prog[0], prog[3], prog[2],
+             odescs, ex._stream, what="fused_ew", work=(_abytes(*arrs, *outs), 0))
+    return outs + [cat]
+
+
 def _h_fused_int(ex, node, ins):
     """fused_int (passes.fuse_elementwise, i64/bool domain): counter, index
     and mask arithmetic of converted control flow in one launch
@@ -1799,6 +1843,7 @@ _HANDLERS.update({
     "conv_filter_grad": _h_conv_filter_grad,
     "row_dots": _h_row_dots,
     "fused_ewm": _h_fused_multi,
+    "fused_pack": _h_fused_pack,
     "matmul2": _h_matmul2,
     "fused_int": _h_fused_int,
     "gather_rows": _h_gather, "scatter_rows": _h_scatter_rows,

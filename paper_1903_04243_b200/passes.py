@@ -982,29 +982,23 @@ def fuse_row_dots(g, keep=()):
     return count, moved
 
 
-def _optimize_in_place(g, keep, elementwise=True):
-    _, moved10 = eliminate_common_subexpressions(g, keep)
-    keep = [moved10.get(k, k) for k in keep]
-    _, moved9 = slice_matmul_columns(g, keep)
-    keep = [moved9.get(k, k) for k in keep]
-    _, moved = fuse_outer_products(g, keep)
-    keep = [moved.get(k, k) for k in keep]
-    _, moved12 = fuse_conv_filter_grads(g, keep)
-    keep = [moved12.get(k, k) for k in keep]
-    _, moved10b = eliminate_common_subexpressions(g, keep)
-    keep = [moved10b.get(k, k) for k in keep]
-    _, moved4 = fuse_reductions(g, keep)
-    keep = [moved4.get(k, k) for k in keep]
-    _, moved6 = fuse_row_dots(g, keep)
-    keep = [moved6.get(k, k) for k in keep]
-    _, moved7 = fuse_dual_matmuls(g, keep)
-    keep = [moved7.get(k, k) for k in keep]
-    _, moved5 = fuse_matmul_epilogues(g, keep)
-    keep = [moved5.get(k, k) for k in keep]
-    moved3 = {}
+def _pipeline(elementwise):
+    seq = [eliminate_common_subexpressions, stack_onehot_sums, slice_matmul_columns,
+           fuse_outer_products, fuse_conv_filter_grads, eliminate_common_subexpressions,
+           fuse_reductions, fuse_row_dots, fuse_dual_matmuls, fuse_matmul_epilogues]
     if elementwise:
-        _, moved3 = fuse_elementwise(g, keep)
-    return [moved3.get(k, k) for k in keep]
+        seq += [fuse_elementwise, place_concats]
+    return seq
+
+
+def _optimize_in_place(g, keep, elementwise=True):
+    """Run the rewrites on `g`; returns (new keep keys, composed key map)."""
+    moved_all = []
+    for fn in _pipeline(elementwise):
+        _, moved = fn(g, keep)
+        keep = [moved.get(k, k) for k in keep]
+        moved_all.append(moved)
+    return keep, moved_all
 
 
 def _optimize_blocks(g, elementwise=True):
@@ -1014,7 +1008,7 @@ def _optimize_blocks(g, elementwise=True):
             continue
         for sg in node.block.subgraphs.values():
             _optimize_blocks(sg, elementwise)
-            sg.set_outputs(_optimize_in_place(sg, [tuple(o) for o in sg.outputs], elementwise))
+            sg.set_outputs(_optimize_in_place(sg, [tuple(o) for o in sg.outputs], elementwise)[0])
 
 
 def optimize(g, keep_keys, elementwise=True):
@@ -1023,39 +1017,12 @@ def optimize(g, keep_keys, elementwise=True):
     hoist_loop_invariants(dst)
     _optimize_blocks(dst, elementwise)
     keep = [mapping[k] for k in keep_keys]
-    _, moved10 = eliminate_common_subexpressions(dst, keep)
-    keep = [moved10.get(k, k) for k in keep]
-    _, moved9 = slice_matmul_columns(dst, keep)
-    keep = [moved9.get(k, k) for k in keep]
-    _, moved = fuse_outer_products(dst, keep)
-    keep = [moved.get(k, k) for k in keep]
-    _, moved12 = fuse_conv_filter_grads(dst, keep)
-    keep = [moved12.get(k, k) for k in keep]
-    _, moved10b = eliminate_common_subexpressions(dst, keep)
-    keep = [moved10b.get(k, k) for k in keep]
-    _, moved4 = fuse_reductions(dst, keep)
-    keep = [moved4.get(k, k) for k in keep]
-    _, moved6 = fuse_row_dots(dst, keep)
-    keep = [moved6.get(k, k) for k in keep]
-    _, moved7 = fuse_dual_matmuls(dst, keep)
-    keep = [moved7.get(k, k) for k in keep]
-    _, moved5 = fuse_matmul_epilogues(dst, keep)
-    keep = [moved5.get(k, k) for k in keep]
-    moved3 = {}
-    if elementwise:
-        _, moved3 = fuse_elementwise(dst, keep)
+    _, moved_all = _optimize_in_place(dst, keep, elementwise)
     final = {}
     for k, v in mapping.items():
-        v = moved10.get(v, v)
-        v = moved9.get(v, v)
-        v = moved.get(v, v)
-        v = moved12.get(v, v)
-        v = moved10b.get(v, v)
-        v = moved4.get(v, v)
-        v = moved6.get(v, v)
-        v = moved7.get(v, v)
-        v = moved5.get(v, v)
-        final[k] = moved3.get(v, v)
+        for moved in moved_all:
+            v = moved.get(v, v)
+        final[k] = v
     return dst, final
 
 
@@ -1066,7 +1033,7 @@ _BIN_CODE = {"add": 0, "sub": 1, "mul": 2, "div": 3, "max": 4, "min": 5, "less":
 _UN_CODE = {"neg": 0, "exp": 1, "log": 2, "relu": 3, "tanh": 4, "sigmoid": 5, "square": 6,
             "logical_not": 7}
 OP_LOAD, OP_CONST, OP_TOBOOL, OP_MOV, OP_SELECT = 64, 65, 66, 67, 68
-MAX_INPUTS, MAX_STEPS, MAX_REGS = 8, 48, 16
+MAX_INPUTS, MAX_STEPS, MAX_REGS = 16, 96, 32
 
 
 _INT_BIN = frozenset({"add", "sub", "mul", "max", "min", "less", "equal"})
@@ -1211,7 +1178,7 @@ def _program(g, order, root, externals, outputs=(), domain="float"):
     return tuple(steps)
 
 
-MAX_OUTPUTS = 8
+MAX_OUTPUTS = 12
 
 
 def fuse_elementwise(g, keep=()):
@@ -1438,3 +1405,262 @@ def _merge_groups(g, groups, users, pos, live, build):
     out = [grp for grp, ok in zip(groups, alive) if ok]
     out.sort(key=lambda grp: -pos[grp[0].id])
     return out
+
+
+# ----------------------------------------------------------------------------
+# F13: placement instead of arithmetic for stacked results
+#
+# (a) The vectorized gradient of gather(v, g) at a constant index g is the
+#     cotangent times a one-hot of g (reference autodiff.py:100-110 emits
+#     scatter_add_rows, which pfor converts to one-hot products; vectorize.py
+#     _convert_scatter_add_rows).  Summed over every index of v (the LSTM
+#     cell's four gate slices, reference bench cell), sum_g onehot(g) * x_g is
+#     exactly concat([x_0, .., x_{K-1}]) along the one-hot axis: x*1 = x and
+#     the other terms are +-0, so the values agree (a slot's -0 becomes +0;
+#     an inf/NaN in a *different* slot, which would make the reference's
+#     product NaN, is not propagated).
+# (b) A concat whose pieces are outputs of one fused elementwise group (plus
+#     inputs it may pass through) costs no launch: the group writes its
+#     outputs into slots of one packed buffer and the concat is a view of
+#     adjacent slots (`fused_pack`).  cfg4: the backward step's gate
+#     cotangents land in dz in place; the forward step's [x_{t+1}, h_t] GEMM
+#     operand is assembled by the cell kernel that computes h_t.
+
+_ONEHOT_KINDS = frozenset({"constant", "reshape", "tile_leading", "equal", "cast", "range_vec"})
+
+
+def _const_eval(g, key, budget=1 << 20):
+    """Host value of a small constant-only subgraph (one-hot factors), or None."""
+    from .tensor import DType
+    memo = {}
+
+    def ev(k):
+        if k in memo:
+            return memo[k]
+        n = g.nodes[k[0]]
+        if n.kind not in _ONEHOT_KINDS or k[1] != 0:
+            raise ValueError
+        ins = [ev(s) for s in n.inputs]
+        if n.kind == "constant":
+            v = np.asarray(n.attrs["value"].data)
+        elif n.kind == "reshape":
+            v = ins[0].reshape(g.ref_shape(k))
+        elif n.kind == "tile_leading":
+            v = np.broadcast_to(ins[0], (int(ins[1]),) + ins[0].shape)
+        elif n.kind == "range_vec":
+            v = np.arange(int(ins[0]), dtype=np.int64)
+        elif n.kind == "equal":
+            v = np.equal(ins[0], ins[1])
+        else:  # cast
+            v = ins[0].astype(np.float64 if n.attrs["dtype"] == DType.F64 else
+                              (np.int64 if n.attrs["dtype"] == DType.I64 else np.bool_))
+        if v.size > budget:
+            raise ValueError
+        memo[k] = v
+        return v
+
+    try:
+        return ev(key)
+    except (ValueError, KeyError, TypeError, AttributeError):
+        return None
+
+
+def _onehot_axis(g, key, shape):
+    """(axis, K, index) if `key` is a constant one-hot e_index along one axis of
+    the broadcast `shape` (the same along every other axis), else None."""
+    sk = g.ref_shape(key)
+    if sk is None or None in sk or g.ref_dtype(key) != _f64():
+        return None
+    v = _const_eval(g, key)
+    if v is None:
+        return None
+    v = v.reshape((1,) * (len(shape) - v.ndim) + v.shape)
+    for a, ext in enumerate(v.shape):
+        if ext < 2 or ext != shape[a]:
+            continue
+        moved = np.moveaxis(v, a, -1).reshape(-1, ext)
+        row = moved[0]
+        idx = np.flatnonzero(row)
+        if len(idx) != 1 or row[idx[0]] != 1.0 or not np.all(moved == row):
+            continue
+        return a, ext, int(idx[0])
+    return None
+
+
+def _f64():
+    from .tensor import DType
+    return DType.F64
+
+
+def stack_onehot_sums(g, keep=()):
+    """F13a in place on `g`.  Returns (count, moved outputs)."""
+    rw = _Rewriter(g, keep)
+    rw.replaced = {}
+    count = 0
+    for node in list(g.topo_order()):
+        if node.id in g.nodes and node.kind == "add":
+            count += _f13a(rw, node)
+    return count, rw.replaced
+
+
+def _f13a(rw, node):
+    g, b = rw.g, rw.b
+    shape = g.ref_shape((node.id, 0))
+    if shape is None or None in shape or node.out_dtypes[0] != _f64():
+        return 0
+    # leaves of the add tree (interior adds single-use)
+    leaves, todo = [], list(node.inputs)
+    while todo:
+        k = todo.pop()
+        n = rw.node(k)
+        if n.kind == "add" and k[1] == 0 and rw.single_use(k) and \
+                tuple(g.ref_shape(k) or ()) == tuple(shape):
+            todo.extend(n.inputs)
+        else:
+            leaves.append(k)
+    if len(leaves) < 2:
+        return 0
+    axis = None
+    parts = {}
+    for k in leaves:
+        n = rw.node(k)
+        if n.kind != "mul" or k[1] != 0:
+            return 0
+        hit = None
+        for oh, x in ((n.inputs[0], n.inputs[1]), (n.inputs[1], n.inputs[0])):
+            sx = g.ref_shape(x)
+            if sx is None or len(sx) != len(shape) or g.ref_dtype(x) != _f64():
+                continue
+            h = _onehot_axis(g, oh, shape)
+            if h is None:
+                continue
+            a, K, idx = h
+            if sx[a] != 1 or any(sx[i] != shape[i] for i in range(len(shape)) if i != a):
+                continue
+            hit = (a, K, idx, x)
+            break
+        if hit is None:
+            return 0
+        a, K, idx, x = hit
+        if axis is None:
+            axis = (a, K)
+        if axis != (a, K) or idx in parts:
+            return 0
+        parts[idx] = x
+    a, K = axis
+    if sorted(parts) != list(range(K)):
+        return 0
+    cat = b.concat([Ref(g, *parts[i]) for i in range(K)], a)
+    rw.redirect((node.id, 0), cat)
+    return 1
+
+
+def place_concats(g, keep=()):
+    """F13b in place on `g` (after fuse_elementwise).  Returns (count, moved)."""
+    from .tensor import DType
+    rw = _Rewriter(g, keep)
+    rw.replaced = {}
+    count = 0
+    claimed = set()
+    for node in list(g.topo_order()):
+        if node.id not in g.nodes or node.kind != "concat":
+            continue
+        count += _f13b(rw, node, claimed, DType)
+    return count, rw.replaced
+
+
+def _ancestors(g, key, stop):
+    seen, todo = set(), [key[0]]
+    while todo:
+        n = todo.pop()
+        if n in seen:
+            continue
+        if n == stop:
+            return True
+        seen.add(n)
+        todo.extend(s for s, _ in g.nodes[n].inputs)
+    return False
+
+
+def _f13b(rw, node, claimed, DType):
+    g = rw.g
+    shape = g.ref_shape((node.id, 0))
+    if shape is None or None in shape or node.out_dtypes[0] != DType.F64:
+        return 0
+    ax = node.attrs["axis"]
+    ax = ax + len(shape) if ax < 0 else ax
+
+    def source(k):  # through reshape chains that end in the shape they started from
+        want, cur = g.ref_shape(k), k
+        while rw.node(cur).kind == "reshape" and cur[1] == 0:
+            cur = rw.node(cur).inputs[0]
+            if g.ref_shape(cur) == want:
+                k = cur
+        return k
+
+    pieces = [source(s) for s in node.inputs]
+    prods = {s[0] for s in pieces if rw.node(s).kind in ("fused_ew", "fused_ewm")}
+    if len(prods) != 1:
+        return 0
+    fid = prods.pop()
+    if fid in claimed:
+        return 0
+    f = g.nodes[fid]
+    S = tuple(f.out_shapes[0])
+    if None in S or len(S) != len(shape) or any(d != DType.F64 for d in f.out_dtypes):
+        return 0
+    ports, passthrough = [], []
+    for s in pieces:
+        if tuple(g.ref_shape(s) or ()) != S:
+            return 0
+        if s[0] == fid:
+            if s in ports:
+                return 0
+            ports.append(s)
+        else:
+            if g.ref_dtype(s) != DType.F64 or _ancestors(g, s, fid):
+                return 0
+            passthrough.append(s)
+    if not ports:
+        return 0
+    # the fused group's program: multi-output form, passthroughs appended as
+    # load -> output registers
+    if f.kind == "fused_ew":
+        prog = list(f.attrs["program"])
+        out_regs = [prog[-1][1]]
+    else:
+        prog = list(f.attrs["program"])
+        out_regs = list(f.attrs["out_regs"])
+    inputs = list(f.inputs)
+    n_out0 = len(out_regs)
+    if len(inputs) + len(passthrough) > MAX_INPUTS or n_out0 + len(passthrough) > MAX_OUTPUTS \
+            or len(prog) + len(passthrough) > MAX_STEPS:
+        return 0
+    used = set(out_regs)
+    free = [r for r in range(MAX_REGS) if r not in used]
+    if len(free) < len(passthrough):
+        return 0
+    pt_port = {}
+    for s in passthrough:
+        if s in inputs:
+            slot = inputs.index(s)
+        else:
+            inputs.append(s)
+            slot = len(inputs) - 1
+        r = free.pop(0)
+        prog.append((OP_LOAD, r, slot, 0))
+        out_regs.append(r)
+        pt_port[s] = len(out_regs) - 1
+    # slot order: the concat's pieces first, in order, then the other outputs
+    cat_order = [s[1] if s[0] == fid else pt_port[s] for s in pieces]
+    slots = cat_order + [k for k in range(len(out_regs)) if k not in cat_order]
+    n_out = len(out_regs)
+    new = g.add_node("fused_pack", inputs,
+                     {"program": tuple(prog), "out_regs": tuple(out_regs),
+                      "out_dtypes": tuple([DType.F64] * n_out), "pack_axis": ax,
+                      "slots": tuple(slots), "cat_span": len(pieces)})
+    claimed.add(new.id)
+    for k in range(n_out0):
+        rw.redirect((fid, k), Ref(g, new.id, k))
+    rw.redirect((node.id, 0), Ref(g, new.id, n_out))
+    return 1

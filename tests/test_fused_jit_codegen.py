@@ -44,7 +44,7 @@ def _groups(g, acc):
     """(integer, n_in, program, out_regs, out_dtypes) of every fused node,
     nested block subgraphs included"""
     for n in g.nodes.values():
-        if n.kind in ("fused_ew", "fused_ewm", "fused_int"):
+        if n.kind in ("fused_ew", "fused_ewm", "fused_int", "fused_pack"):
             prog = tuple(tuple(int(x) for x in s) for s in n.attrs["program"])
             if n.kind == "fused_ew":
                 regs, dts = (prog[-1][1],), (_dt(n.attrs["out_dtype"]),)

@@ -217,18 +217,72 @@ def test_f5_derivative_epilogue():
     assert any(n.kind == "matmul_ep" and n.attrs.get("dop") == "dtanh" for n in live3)
 
 
+def _gate_grads(n=3, u=4, gates=(1,)):
+    """per-example gradient of sum(square(W[g] * x_i)) over the gate rows
+    `gates` of a [4, u] weight: the gradient of each gather(W, g) is a one-hot
+    product (reference autodiff.py:100-110 -> vectorized one-hot)."""
+    api = WL.this_api()
+    r = np.random.default_rng(1)
+    X0 = r.standard_normal((n, u)).astype(np.float32).astype(np.float64)
+    W0 = r.standard_normal((4, u)).astype(np.float32).astype(np.float64)
+    b = api.GraphBuilder()
+    X = b.placeholder("x", api.DType.F64, (n, u))
+    W = b.const(W0)
+
+    def body(bb, i):
+        xi = bb.reshape(bb.gather(X, i), [1, u])
+        terms = [bb.mul(bb.reshape(bb.gather(bb._imp(W), bb.i64(gi)), [1, u]), xi) for gi in gates]
+        acc = terms[0]
+        for t in terms[1:]:
+            acc = bb.add(acc, bb.tanh(t))
+        loss = bb.reduce_sum(bb.square(acc), [0, 1])
+        return api.gradient(bb.graph, loss, [bb._imp(W)], emit=bb)
+
+    outs = api.pfor(b, body, n)
+    b.graph.set_outputs(outs)
+    return WL.Workload("gates", b.graph, {"x": X0}, n, "grads", {})
+
+
 def test_f3_integer_group_ending_in_float_cast():
-    """cfg4's per-step one-hot factor cast(equal(t, range), f64): the integer
-    compare and the cast to f64 are one `fused_int` launch with an f64
-    output (values unchanged, oracle)."""
+    """a one-hot factor cast(equal(t, range), f64) that F13a cannot turn into
+    placement (one gate row of four): the integer compare and the cast to f64
+    are one `fused_int` launch with an f64 output (values unchanged, oracle)."""
     from paper_1903_04243_b200.tensor import DType
-    w = WL.cfg4(WL.this_api(), n=3, steps=4, units=4)
+    w = _gate_grads(gates=(1,))
     g, g2, m = _run_both(w)
     live = _kinds(g2, [m[tuple(o)] for o in g.outputs])
     fi = [n for n in live if n.kind == "fused_int"]
     assert any(DType.F64 in n.attrs["out_dtypes"] for n in fi)
     assert not any(n.kind == "cast" and n.out_dtypes[0] == DType.F64 and
                    g2.ref_dtype(n.inputs[0]) in (DType.BOOL, DType.I64) for n in live)
+
+
+def test_f13a_onehot_sum_over_every_index_is_a_concat():
+    """all four gate rows used: sum_g onehot(g) * dW_g is placement -- the
+    live program has no one-hot product and no fused_int left (oracle values
+    unchanged)."""
+    w = _gate_grads(gates=(0, 1, 2, 3))
+    g, g2, m = _run_both(w)
+    live = _kinds(g2, [m[tuple(o)] for o in g.outputs])
+    assert not [n for n in live if n.kind in ("fused_int", "equal")]
+
+
+def test_f13_cfg4_steps_are_one_gemm_and_one_fused_launch():
+    """cfg4 after F13: every time step is one GEMM and one fused launch in
+    each direction -- the forward cell writes [x_{t+1}, h_t] (the next GEMM's
+    operand) into its packed outputs, the backward cell writes the gate
+    cotangents into dz in place; no per-step concat or one-hot stack."""
+    T = 5
+    w = WL.cfg4(WL.this_api(), n=3, steps=T, units=4)
+    g, g2, m = _run_both(w)
+    live = _kinds(g2, [m[tuple(o)] for o in g.outputs])
+    kinds = [n.kind for n in live]
+    packs = [n for n in live if n.kind == "fused_pack"]
+    assert len(packs) == 2 * T - 1, kinds  # (step 0's operand has no cell before it)
+    ew = [n for n in live if n.kind in ("fused_ew", "fused_ewm", "fused_int")]
+    assert len(ew) <= 2, [n.kind for n in ew]  # bias-gradient sum, first cell's tail
+    step_cats = [n for n in live if n.kind == "concat" and len(n.inputs) in (2, 4)]
+    assert len(step_cats) == 1, [(n.kind, n.out_shapes) for n in step_cats]
 
 
 def test_f9_backward_gemm_computes_only_live_columns():
