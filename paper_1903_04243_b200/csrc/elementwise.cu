@@ -969,9 +969,9 @@ __global__ void __launch_bounds__(256) concat_kernel(CatDesc d, T* out) {
 constexpr int kThinCat = 128;
 struct ThinCat {
   int n;
-  int64_t R, ost_row, off;
+  int64_t R, R1, ost_row, off;  // R rows = R0 x R1 (outer x inner row dims)
   const void* x[kThinCat];
-  int64_t rs[kThinCat];  // row stride of each input (collapsed leading dims)
+  int64_t rs0[kThinCat], rs1[kThinCat];  // per input: outer / inner row strides
 };
 
 template <typename T>
@@ -981,18 +981,20 @@ __global__ void __launch_bounds__(256) concat_thin_kernel(ThinCat d, T* out) {
   const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
   const int64_t r0 = (int64_t)blockIdx.x * 32;
   const int c0 = blockIdx.y * 32;
+  const int64_t r = r0 + tx;
+  const int64_t ro = r / d.R1, ri = r - ro * d.R1;
 #pragma unroll
   for (int i = ty; i < 32; i += 8) {
     const int c = c0 + i;
-    const int64_t r = r0 + tx;
-    if (c < d.n && r < d.R) tile[i][tx] = __ldg(reinterpret_cast<const T*>(d.x[c]) + r * d.rs[c]);
+    if (c < d.n && r < d.R)
+      tile[i][tx] = __ldg(reinterpret_cast<const T*>(d.x[c]) + ro * d.rs0[c] + ri * d.rs1[c]);
   }
   __syncthreads();
 #pragma unroll
   for (int i = ty; i < 32; i += 8) {
-    const int64_t r = r0 + i;
+    const int64_t rr = r0 + i;
     const int c = c0 + tx;
-    if (c < d.n && r < d.R) out[r * d.ost_row + d.off + c] = tile[tx][i];
+    if (c < d.n && rr < d.R) out[rr * d.ost_row + d.off + c] = tile[tx][i];
   }
 }
 
@@ -1096,36 +1098,47 @@ static int64_t collapse_rows(const pfb_tensor* t, int rank) {
   return st < 0 ? 0 : st;
 }
 
+// rows of a [.., R1, 1] view as (outer, inner) strides: dims [0, rank-2)
+// collapsed into one outer stride, dim rank-2 the inner one; false when the
+// outer dims do not collapse
+static bool rows2(const pfb_tensor* t, int rank, int64_t* s0, int64_t* s1) {
+  *s1 = t->shape[rank - 2] == 1 ? 0 : t->stride[rank - 2];
+  int64_t st = -1, expect = -1;
+  for (int i = rank - 3; i >= 0; --i) {
+    if (t->shape[i] == 1) continue;
+    if (st < 0) { st = t->stride[i]; expect = st * t->shape[i]; continue; }
+    if (t->stride[i] != expect) return false;
+    expect *= t->shape[i];
+  }
+  *s0 = st < 0 ? 0 : st;
+  return true;
+}
+
 static bool concat_thin(int32_t n, const pfb_tensor* xs, int32_t axis, pfb_tensor* out,
                         cudaStream_t s) {
   const int rank = out->rank;
   if (axis != rank - 1 || rank < 2 || out->stride[axis] != 1 || n < 8) return false;
+  if (out->shape[axis] != n) return false;
   ThinCat d;
   d.R = 1;
   for (int i = 0; i < rank - 1; ++i) d.R *= out->shape[i];
+  d.R1 = out->shape[rank - 2];
   d.ost_row = collapse_rows(out, rank);
-  if (d.ost_row < 0 || d.R == 0) return false;
-  for (int base = 0; base < n; base += kThinCat) {
-    d.n = std::min(kThinCat, n - base);
-    d.off = base;
-    for (int j = 0; j < d.n; ++j) {
-      const pfb_tensor* x = &xs[base + j];
-      if (x->rank != rank || x->shape[axis] != 1 || x->dtype != out->dtype) return false;
-      for (int i = 0; i < rank - 1; ++i)
-        if (x->shape[i] != out->shape[i]) return false;
-      const int64_t rs = collapse_rows(x, rank);
-      if (rs < 0) return false;
-      d.x[j] = x->data;
-      d.rs[j] = rs;
-    }
+  if (d.ost_row < 0 || d.R == 0 || d.R1 == 0) return false;
+  for (int j = 0; j < n; ++j) {
+    const pfb_tensor* x = &xs[j];
+    if (x->rank != rank || x->shape[axis] != 1 || x->dtype != out->dtype) return false;
+    for (int i = 0; i < rank - 1; ++i)
+      if (x->shape[i] != out->shape[i]) return false;
+    int64_t a, b;
+    if (!rows2(x, rank, &a, &b)) return false;
   }
-  if (out->shape[axis] != n) return false;
   for (int base = 0; base < n; base += kThinCat) {
     d.n = std::min(kThinCat, n - base);
     d.off = base;
     for (int j = 0; j < d.n; ++j) {
       d.x[j] = xs[base + j].data;
-      d.rs[j] = collapse_rows(&xs[base + j], rank);
+      rows2(&xs[base + j], rank, &d.rs0[j], &d.rs1[j]);
     }
     dim3 grid((unsigned)((d.R + 31) / 32), (unsigned)((d.n + 31) / 32));
     switch (out->dtype) {

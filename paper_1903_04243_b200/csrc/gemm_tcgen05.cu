@@ -137,6 +137,8 @@ struct Params {
   const float* dy;  // derivative epilogue (GemmArgs::dop)
   int64_t sdb, sdm, sdn;
   int dop;
+  int chunk_kb;     // k-blocks accumulated in TMEM per chunk (CHUNK_KB unless overridden)
+  int products;     // PFB_TC_PRODUCTS=1: hi*hi only (timing experiments; not fp32-accurate)
 };
 
 __device__ __forceinline__ void stamp(const Params& p, int i) {
@@ -283,14 +285,14 @@ gemm_kernel(const __grid_constant__ CUtensorMap map_ah, const __grid_constant__ 
       for (int u = blockIdx.x; u < ntiles; u += ustride) {
         const int ks = u % p.ksplit;
         const int kb0 = ks * p.kb_per_split, kb1 = min(nk, kb0 + p.kb_per_split);
-        const int uchunks = (kb1 - kb0 + CHUNK_KB - 1) / CHUNK_KB;
+        const int uchunks = (kb1 - kb0 + p.chunk_kb - 1) / p.chunk_kb;
         for (int c = 0; c < uchunks; ++c, ++gc) {
           const int buf = gc & 1;
           if (gc >= 2) mbar_wait(&acc_empty[buf], ((gc >> 1) - 1) & 1);
           asm volatile("tcgen05.fence::after_thread_sync;");
           const uint32_t tmem_d = tmem_base + (uint32_t)(buf * BN);
-          const int kb_beg = kb0 + c * CHUNK_KB;
-          const int kb_end = min(kb1, kb_beg + CHUNK_KB);
+          const int kb_beg = kb0 + c * p.chunk_kb;
+          const int kb_end = min(kb1, kb_beg + p.chunk_kb);
           for (int kb = kb_beg; kb < kb_end; ++kb, ++g) {
             const int s = g % STAGES;
             mbar_wait(split_smem ? &ready[s] : &full[s], (g / STAGES) & 1);
@@ -316,6 +318,7 @@ gemm_kernel(const __grid_constant__ CUtensorMap map_ah, const __grid_constant__ 
               const uint64_t da = astep * k, db = bstep * k;
               const uint32_t acc = (kb > kb_beg || k > 0) ? 1u : 0u;
               mma_tf32(tmem_d, a_hi + da, b_hi + db, idesc, acc);
+              if (p.products == 1) continue;
               mma_tf32(tmem_d, a_hi + da, b_lo + db, idesc, 1u);
               mma_tf32(tmem_d, a_lo + da, b_hi + db, idesc, 1u);
               // both operands raw: hi = trunc_tf32 on both sides makes the
@@ -375,14 +378,14 @@ gemm_kernel(const __grid_constant__ CUtensorMap map_ah, const __grid_constant__ 
       const int bz = t / tiles_per_batch, r = t % tiles_per_batch;
       const int m0 = (r / p.ntn) * BM, n0 = (r % p.ntn) * BN;
       const int kb0 = ks * p.kb_per_split, kb1 = min(nk, kb0 + p.kb_per_split);
-      const int uchunks = (kb1 - kb0 + CHUNK_KB - 1) / CHUNK_KB;
+      const int uchunks = (kb1 - kb0 + p.chunk_kb - 1) / p.chunk_kb;
 #pragma unroll
       for (int j = 0; j < EPI_COLS; ++j) acc[j] = 0.f;
       // split chunk c's stages, then drain chunk c-1 (the MMA works on
       // chunk c-1 while the stages of chunk c are being split)
       for (int c = 0; c < uchunks; ++c) {
         if (split_smem) {
-          const int kb_beg = kb0 + c * CHUNK_KB, kb_end = min(kb1, kb_beg + CHUNK_KB);
+          const int kb_beg = kb0 + c * p.chunk_kb, kb_end = min(kb1, kb_beg + p.chunk_kb);
           for (int kb = kb_beg; kb < kb_end; ++kb) split_stage(kb);
         }
         if (c > 0) drain();
@@ -599,7 +602,17 @@ static int64_t align_up(int64_t x) { return (x + 255) / 256 * 256; }
 // K-splits so that (tiles x splits) covers the SMs, >= 2 chunks per split;
 // the splits of one tile form a thread-block cluster (<= 8, portable size)
 constexpr int kMaxCluster = kMaxSplit;
+static int chunk_kb() {
+  static const int c = [] {
+    const char* e = getenv("PFB_TC_CHUNK");
+    const int v = e ? atoi(e) : CHUNK_KB;
+    return v >= 1 && v <= 16 ? v : CHUNK_KB;
+  }();
+  return c;
+}
+
 static void choose_split(const GemmArgs& g, int* ksplit, int* kb_per) {
+  const int CHUNK_KB = chunk_kb();
   const int64_t tiles = ((g.M + BM - 1) / BM) * ((g.N + BN - 1) / BN) * g.batch;
   const int64_t Kp = (g.K + 3) / 4 * 4;
   const int nk = (int)((Kp + BK - 1) / BK);
@@ -804,7 +817,8 @@ static int launch_gemm(const GemmArgs& g, const PairFeed& f1, const PairFeed* f2
            (int)((g.M + BM - 1) / BM), (int)((g.N + BN - 1) / BN), f1.a_bc, f1.b_bc, f1.am, f1.bm,
            idesc_of(f1), g.C, g.scb, g.scm, g.scn, g.alpha_rows, g.accumulate, ksplit, kb_per,
            g.bias, g.sxb, g.sxm, g.sxn, g.act, 4096u, 512u, tma_store, tc_trace_buffer(),
-           nk1, q.am, q.bm, q.a_bc, q.b_bc, idesc_of(q), g.dy, g.sdb, g.sdm, g.sdn, g.dop};
+           nk1, q.am, q.bm, q.a_bc, q.b_bc, idesc_of(q), g.dy, g.sdb, g.sdm, g.sdn, g.dop,
+           chunk_kb(), getenv("PFB_TC_PRODUCTS") ? atoi(getenv("PFB_TC_PRODUCTS")) : 3};
   const int64_t units = (int64_t)p.ntm * p.ntn * g.batch * ksplit;
   if (ksplit > 1) {
     // one CTA per (tile, k-split); the k-splits of a tile are one cluster

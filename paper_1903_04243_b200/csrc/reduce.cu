@@ -139,6 +139,39 @@ __global__ void __launch_bounds__(256) reduce_inner_warp(RedDesc D, int64_t K, i
   }
 }
 
+// short contiguous float rows (R <= 128, R % 4 == 0, one reduced dim of
+// unit stride): LPR = R/4 lanes (a power of two) per row, 32/LPR rows per
+// warp, one 16-byte load per lane; 4 row groups are loaded before any is
+// reduced, so a warp keeps 4 loads in flight instead of one row's worth
+template <int LPR>
+__global__ void __launch_bounds__(256) reduce_inner_short(RedDesc D, int64_t K, int R4,
+                                                          const float* __restrict__ x,
+                                                          float* __restrict__ out) {
+  pdl_enter();
+  constexpr int RPW = 32 / LPR;  // rows per warp pass
+  const int lane = threadIdx.x & 31, sub = lane % LPR, rw = lane / LPR;
+  const int64_t warps = (int64_t)gridDim.x * 8;
+  const int64_t w0 = blockIdx.x * 8ll + (threadIdx.x >> 5);
+  for (int64_t k0 = w0 * RPW * 4; k0 < K; k0 += warps * RPW * 4) {
+    float4 v[4];
+    int64_t kk[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      kk[u] = k0 + u * RPW + rw;
+      v[u] = make_float4(0.f, 0.f, 0.f, 0.f);
+      if (kk[u] < K && sub < R4)
+        v[u] = __ldg(reinterpret_cast<const float4*>(x + decode(D.kr, D.kshape, D.kst, kk[u])) + sub);
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      float t = (v[u].x + v[u].y) + (v[u].z + v[u].w);
+#pragma unroll
+      for (int o = LPR / 2; o > 0; o >>= 1) t += __shfl_xor_sync(0xffffffffu, t, o);
+      if (sub == 0 && kk[u] < K) out[kk[u]] = t;
+    }
+  }
+}
+
 // block per (output, split); partial -> out[k] (nsplit==1) or ws[k*nsplit+split]
 template <typename T, bool PROD>
 __global__ void __launch_bounds__(256) reduce_inner_block(RedDesc D, int64_t K, int64_t R,
@@ -360,6 +393,24 @@ int reduce_run(const pfb_tensor* x, const int64_t* ystride, const T* yp, uint32_
   const T* xp = (const T*)x->data;
   bool inner = (K == 1) || (rinner != 0 && (kinner == 0 || rinner < kinner));
   if (inner) {
+    if constexpr (std::is_same<T, float>::value && !PROD) {
+      // short rows: several rows per warp (cfg4's bias gradient: R = T = 64)
+      bool aligned = D.rr == 1 && D.rst[0] == 1 && R % 4 == 0 && R <= 128 && K > 1 &&
+                     (reinterpret_cast<uintptr_t>(xp) & 15) == 0;
+      for (int d = 0; d < D.kr && aligned; ++d) aligned = D.kshape[d] == 1 || D.kst[d] % 4 == 0;
+      if (aligned) {
+        const int R4 = (int)(R / 4);
+        const int lpr = R4 <= 4 ? 4 : (R4 <= 8 ? 8 : (R4 <= 16 ? 16 : 32));
+        const int64_t per_block = 8 * (32 / lpr) * 4;  // rows per block per pass
+        const unsigned grid =
+            (unsigned)std::min<int64_t>((K + per_block - 1) / per_block, (int64_t)kNumSMs * 32);
+        if (lpr == 4) launch(reduce_inner_short<4>, grid, 256, 0, s, D, K, R4, xp, o);
+        else if (lpr == 8) launch(reduce_inner_short<8>, grid, 256, 0, s, D, K, R4, xp, o);
+        else if (lpr == 16) launch(reduce_inner_short<16>, grid, 256, 0, s, D, K, R4, xp, o);
+        else launch(reduce_inner_short<32>, grid, 256, 0, s, D, K, R4, xp, o);
+        return launch_status();
+      }
+    }
     if (R <= 16384 && K > 1) {
       launch(reduce_inner_warp<T, PROD>, grid_for(K, 8, 64), 256, 0, s, D, K, R, xp, yp, o);
       return launch_status();

@@ -444,3 +444,62 @@ def test_concat_row_strided_slices(d, dt, Executor):
         torch.cuda.synchronize()
         want = torch.cat([x[:, t, :], h], dim=1)
         assert torch.equal(out, want)
+
+
+@pytest.mark.parametrize("shape", [(5, 7, 64), (3, 1000, 12), (2, 333, 128), (4, 3, 4),
+                                   (257, 8, 100)])
+def test_reduce_short_inner_rows(shape, Executor):
+    """inner reductions over short contiguous rows (the several-rows-per-warp
+    kernel; cfg4's bias gradient sums T = 64 per row), plus an offset view
+    whose rows are not 16-byte aligned (the general warp kernel)."""
+    from paper_1903_04243_b200 import GraphBuilder
+    r = np.random.default_rng(sum(shape))
+    a = np.asarray(r.standard_normal(shape), np.float32).astype(np.float64)
+    b = GraphBuilder()
+    x = b.const(a)
+    red = b.reduce_sum(x, [2])
+    tail = b.reduce_sum(b.gather(b.transpose(x, [2, 0, 1]),
+                                 b.const(np.arange(1, shape[2], dtype=np.int64))), [0])
+    b.graph.set_outputs([red, tail])
+    got, got_t = Executor(b.graph).run()
+    check(got, a.sum(axis=2))
+    check(got_t, np.transpose(a, [2, 0, 1])[1:].sum(axis=0))
+
+
+@pytest.mark.parametrize("units", [4, 64])
+def test_packed_concat_slots_cfg4(units, Executor):
+    """F13: cfg4 with packed fused outputs (the forward cell writes the next
+    GEMM operand [x_{t+1}, h_t], the backward cell writes dz in place) against
+    the oracle on the unoptimized graph."""
+    from oracle import OracleExecutor
+    from paper_1903_04243_b200 import workloads as WL
+    w = WL.cfg4(WL.this_api(), n=8, steps=6, units=units)
+    ex = Executor(w.graph)
+    got = ex.run(feeds=w.feeds)
+    want = OracleExecutor(w.graph).run(feeds=w.feeds)
+    for g_, r_ in zip(got, want):
+        check(g_, r_.data)
+    assert "fused_pack" in {n.kind for n in ex._exec_graph.nodes.values()}
+
+
+@pytest.mark.parametrize("n_in", [8, 64])
+def test_concat_thin_two_level_rows(n_in, Executor):
+    """thin concat whose pieces are transposed slices of packed buffers
+    ([n, 1, 8w] -> slot [n, 1, 2w] -> [n, 2w, 1]): rows with an outer and an
+    inner stride (cfg4's F2 operand after F13)."""
+    from paper_1903_04243_b200 import GraphBuilder
+    r = np.random.default_rng(n_in)
+    w = 24
+    bufs = [r.standard_normal((5, 1, 8 * w)) for _ in range(n_in)]
+    b = GraphBuilder()
+    parts = []
+    for bf in bufs:
+        v = b.reshape(b.const(bf), [5, 8, w])
+        sl = b.gather(b.transpose(v, [1, 0, 2]), b.const(np.array([3, 4], dtype=np.int64)))
+        sl = b.reshape(b.transpose(sl, [1, 0, 2]), [5, 1, 2 * w])  # may materialise
+        parts.append(b.transpose(sl, [0, 2, 1]))
+    b.graph.set_outputs([b.concat(parts, 2)])
+    got = Executor(b.graph, cuda_graph=False).run()[0].data
+    want = np.concatenate([np.transpose(bf.reshape(5, 8, w)[:, 3:5].reshape(5, 1, 2 * w), (0, 2, 1))
+                           for bf in bufs], axis=2)
+    np.testing.assert_allclose(np.asarray(got, np.float64), want, rtol=1e-6, atol=1e-7)

@@ -4,7 +4,7 @@ sys.path.insert(0, str(pathlib.Path(__file__).resolve().parent.parent))
 import sys, collections
 from paper_1903_04243_b200 import workloads as WL, passes
 cfg = sys.argv[1] if len(sys.argv) > 1 else "cfg4"
-kw = dict(n=4, steps=3, units=64) if cfg == "cfg4" else {}
+kw = {"cfg4": dict(n=4, steps=3, units=64), "cfg2": dict(n=128, model=sys.argv[2] if len(sys.argv) > 2 else "mlp")}.get(cfg, {})
 w = WL.BUILDERS[cfg](WL.this_api(), **kw)
 keys=[tuple(o) for o in w.graph.outputs]
 dst, m = passes.optimize(w.graph, keys)

@@ -27,6 +27,11 @@ WANT = {
     "launch__grid_size": "grid",
     "launch__block_size": "block",
     "l1tex__data_bank_conflicts_pipe_lsu_mem_shared.sum": "smem_bank_conflicts",
+    "lts__throughput.avg.pct_of_peak_sustained_elapsed": "l2_pct",
+    "lts__t_bytes.sum": "l2_bytes",
+    "l1tex__data_pipe_lsu_wavefronts_mem_shared.sum.pct_of_peak_sustained_elapsed": "smem_lsu_pct",
+    "smsp__inst_executed.sum": "inst_executed",
+    "sm__pipe_tensor_cycles_active.avg.pct_of_peak_sustained_elapsed": "tensor_pct",
 }
 
 
