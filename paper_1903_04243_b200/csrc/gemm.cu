@@ -117,6 +117,15 @@ int run_path(const GemmArgs& g, int path, void* ws, int64_t ws_bytes, cudaStream
     case 7: return gemm_tcgen05(g, ws, ws_bytes, s, 2, 2);  // raw feed, 2 / 4 k-splits
     case 8: return gemm_tcgen05(g, ws, ws_bytes, s, 2, 4);
     case 9: return gemm_tcgen05(g, ws, ws_bytes, s, 1, 4);  // pre-split, 4 k-splits
+    // narrow tiles (skinny M: N-parallel instead of k-split reductions)
+    case 12: return gemm_tcgen05(g, ws, ws_bytes, s, 2, 0, 64);
+    case 13: return gemm_tcgen05(g, ws, ws_bytes, s, 2, 0, 32);
+    case 14: return gemm_tcgen05(g, ws, ws_bytes, s, 2, 2, 32);
+    case 15: return gemm_tcgen05(g, ws, ws_bytes, s, 2, 4, 32);
+    case 16: return gemm_tcgen05(g, ws, ws_bytes, s, 2, 2, 64);
+    case 17: return gemm_tcgen05(g, ws, ws_bytes, s, 2, 4, 64);
+    case 18: return gemm_tcgen05(g, ws, ws_bytes, s, 2, 8, 64);
+    case 19: return gemm_tcgen05(g, ws, ws_bytes, s, 2, 8, 32);
     case 5: return gemm_tcgen05_pair(g, ws, ws_bytes, s, 1);
     case 6: return gemm_tcgen05_pair(g, ws, ws_bytes, s, 2);
     default: return gemm_tcgen05(g, ws, ws_bytes, s, 0);
@@ -290,7 +299,7 @@ static int matmul_impl(GemmArgs& g, pfb_tensor* out, int32_t force_path, void* w
   // 5 / 6 = CTA-pair tcgen05 (cta_group::2) with pre-split / raw operands.
   // PFB_DISABLE_TCGEN05=1 pins auto to SIMT (A/B testing, bring-up).
   static const bool tc_off = getenv("PFB_DISABLE_TCGEN05") && getenv("PFB_DISABLE_TCGEN05")[0] == '1';
-  if (force_path >= 1 && force_path <= 11) return run_path(g, force_path, ws, ws_bytes, s);
+  if (force_path >= 1 && force_path <= 19) return run_path(g, force_path, ws, ws_bytes, s);
   const bool tc_ok = !tc_off && gemm_tcgen05_eligible(g) &&
                      ws_bytes >= gemm_tcgen05_workspace(g) && ws != nullptr &&
                      (double)g.batch * g.M * g.N * g.K >= (double)(1 << 20);
@@ -307,7 +316,7 @@ static int matmul_impl(GemmArgs& g, pfb_tensor* out, int32_t force_path, void* w
     cudaStreamIsCapturing(s, &st);
     if (autotune_enabled() && !accumulate && st == cudaStreamCaptureStatusNone) {
       // every candidate runs twice; the last one timed leaves C computed
-      int cand[11];
+      int cand[20];
       int ncand = 0;
       cand[ncand++] = 1;
       if (gemm_simt_splittable(g)) { cand[ncand++] = 10; cand[ncand++] = 11; }
@@ -320,6 +329,8 @@ static int matmul_impl(GemmArgs& g, pfb_tensor* out, int32_t force_path, void* w
       if (gemm_tcgen05_raw_possible(g)) {
         cand[ncand++] = 4;
         if (few_tiles) { cand[ncand++] = 7; cand[ncand++] = 8; }
+        if (few_tiles && g.M <= 512)
+          for (int c : {12, 13, 14, 15, 16, 17, 18, 19}) cand[ncand++] = c;
       }
       if (g.M > 128 && !tc_pair_off()) {
         cand[ncand++] = 5;
@@ -366,6 +377,8 @@ int dual_path(const GemmArgs& g1, const GemmArgs& g2, int path, pfb_tensor* out,
               int64_t ws_bytes, cudaStream_t s) {
   if (path == 2 || path == 3)
     return gemm_tcgen05_dual(g1, g2, ws, ws_bytes, s, path == 2 ? 2 : 1);
+  if (path == 4 || path == 5)  // raw feed, narrow tiles
+    return gemm_tcgen05_dual(g1, g2, ws, ws_bytes, s, 2, 0, path == 4 ? 64 : 32);
   GemmArgs h1 = g1, h2 = g2;
   h1.bias = nullptr;
   h1.act = 0;
@@ -436,7 +449,7 @@ extern "C" int pfb_matmul_dual2(const pfb_tensor* a1, const pfb_tensor* b1, cons
   cudaStream_t s = as_stream(stream);
   if (g1.batch == 0 || g1.M == 0 || g1.N == 0) return 0;
   static const bool tc_off = getenv_flag("PFB_DISABLE_TCGEN05") || getenv_flag("PFB_DISABLE_DUAL");
-  if (force_path >= 1 && force_path <= 3) return dual_path(g1, g2, force_path, out, ws, ws_bytes, s);
+  if (force_path >= 1 && force_path <= 5) return dual_path(g1, g2, force_path, out, ws, ws_bytes, s);
   const bool tc_ok = !tc_off && g1.K > 0 && g2.K > 0 && gemm_tcgen05_eligible(g1) &&
                      gemm_tcgen05_eligible(g2) && ws != nullptr &&
                      ws_bytes >= gemm_tcgen05_dual_workspace(g1, g2) &&
@@ -456,7 +469,10 @@ extern "C" int pfb_matmul_dual2(const pfb_tensor* a1, const pfb_tensor* b1, cons
     if (!autotune_enabled() || st != cudaStreamCaptureStatusNone)
       return dual_path(g1, g2, 2, out, ws, ws_bytes, s);
     float best = 1e30f;
-    for (int cand : {1, 3, 2}) {
+    const bool skinny = g1.M <= 512 &&
+                        ((g1.M + 127) / 128) * ((g1.N + 127) / 128) * g1.batch < 148;
+    for (int cand : {1, 3, 2, 4, 5}) {
+      if (cand >= 4 && !skinny) continue;
       const float t = time_dual(g1, g2, cand, out, ws, ws_bytes, s);
       if (t < best) { best = t; path = cand; }
     }

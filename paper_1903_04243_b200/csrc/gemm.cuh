@@ -74,13 +74,14 @@ int64_t gemm_simt_workspace(const GemmArgs& g);
 // variant: 0 = auto, 1 = operands pre-split by split_kernel, 2 = raw operands
 // fed by TMA and split in shared memory wherever the layout allows it
 // ksplit_want > 0 forces that many k-splits (autotune candidates), 0 = model
+// bn: tile width (MMA N) 128, 64 or 32 (skinny-M problems: more CTAs over N)
 int gemm_tcgen05(const GemmArgs& g, void* ws, int64_t ws_bytes, cudaStream_t s, int variant = 0,
-                 int ksplit_want = 0);
+                 int ksplit_want = 0, int bn = 128);
 int64_t gemm_tcgen05_workspace(const GemmArgs& g);
 // C = epi(A1 B1 + A2 B2) in one tcgen05 launch (consecutive K ranges of one
 // accumulation); g1 carries C and the epilogue, g2 only its operands
 int gemm_tcgen05_dual(const GemmArgs& g1, const GemmArgs& g2, void* ws, int64_t ws_bytes,
-                      cudaStream_t s, int variant = 0, int ksplit_want = 0);
+                      cudaStream_t s, int variant = 0, int ksplit_want = 0, int bn = 128);
 int64_t gemm_tcgen05_dual_workspace(const GemmArgs& g1, const GemmArgs& g2);
 // PFB_TC_TRACE=1: 16-slot globaltimer stamp buffer (device), else nullptr
 unsigned long long* tc_trace_buffer();

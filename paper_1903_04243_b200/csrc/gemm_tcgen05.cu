@@ -41,27 +41,39 @@
 namespace pfb {
 namespace tc {
 
-constexpr int BM = 128, BN = 128, BK = 32, STAGES = 3, UMMA_K = 8;
+constexpr int BM = 128, BK = 32, UMMA_K = 8;
 #ifndef PFB_CHUNK_KB
 #define PFB_CHUNK_KB 2
 #endif
 constexpr int CHUNK_KB = PFB_CHUNK_KB;            // k-blocks accumulated in TMEM per chunk
-constexpr int TILE_BYTES = BM * BK * 4;           // 16 KB per operand tile
-constexpr int STAGE_BYTES = 4 * TILE_BYTES;       // A_hi, A_lo, B_hi, B_lo
+constexpr int TILE_BYTES = BM * BK * 4;           // 16 KB per A operand tile
 constexpr int kMaxSplit = 8;                      // k-splits per tile (cluster size)
-constexpr int EPI_WARPS = 8;                      // 2 per TMEM lane quarter, 64 columns each
-constexpr int EPI_COLS = BN / 2;
+constexpr int EPI_WARPS = 8;                      // split warps; the first DRAIN_WARPS drain
 constexpr int EPI_STAGE_FLOATS = 32 * 32;         // per epilogue warp: one 32x32 block,
                                                   // 16B chunks XOR-swizzled by row
-// layout: [stages][epilogue staging, 4 KB per warp, 1 KB aligned for TMA][barriers]
-constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + 1024 /*align*/ + 256 /*barriers*/ +
-                           EPI_WARPS * EPI_STAGE_FLOATS * 4;
-constexpr int NUM_THREADS = 64 + 32 * EPI_WARPS;  // TMA, MMA, 8 epilogue warps
-constexpr int TMEM_COLS = 2 * BN;                 // double-buffered chunk accumulator
+constexpr int NUM_THREADS = 64 + 32 * EPI_WARPS;  // TMA, MMA, 8 split / epilogue warps
 
-// kind::tf32, D=f32, M=128, N=BN; bit 15/16 = A/B MN-major (set per call)
-constexpr uint32_t kIdesc = (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(BN >> 3) << 17) |
-                            ((uint32_t)(BM >> 4) << 24);
+// Tile width BN (the MMA's N): 128 (square tiles), 64 or 32 (skinny-M
+// problems: more CTAs over N instead of k-splits that must be reduced).
+// layout: [stages][epilogue staging, 4 KB per warp, 1 KB aligned for TMA][barriers]
+template <int BN_>
+struct TileCfg {
+  static constexpr int BN = BN_;
+  static constexpr int B_BYTES = BN * BK * 4;                 // one B plane per stage
+  static constexpr int STAGE_BYTES = 2 * TILE_BYTES + 2 * B_BYTES;  // A_hi, A_lo, B_hi, B_lo
+  static constexpr int STAGES = BN == 128 ? 3 : 4;
+  // 8 warps x 64 columns (BN 128), 8 x 32 (BN 64), 4 x 32 (BN 32): warp w
+  // owns TMEM lanes 32*(w%4)..+31 and DCOLS columns from (w/4)*DCOLS
+  static constexpr int DRAIN_WARPS = BN >= 64 ? 8 : 4;
+  static constexpr int DCOLS = BN * 4 / DRAIN_WARPS;
+  static constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + 1024 /*align*/ + 256 /*barriers*/ +
+                                    EPI_WARPS * EPI_STAGE_FLOATS * 4;
+  static constexpr int TMEM_COLS = 2 * BN < 32 ? 32 : 2 * BN;  // double-buffered chunks
+  // kind::tf32, D=f32, M=128, N=BN; bit 15/16 = A/B MN-major (set per call)
+  static constexpr uint32_t IDESC = (1u << 4) | (2u << 7) | (2u << 10) |
+                                    ((uint32_t)(BN >> 3) << 17) | ((uint32_t)(BM >> 4) << 24);
+  static_assert(SMEM_BYTES <= 232448, "shared memory");
+};
 
 // ---------------------------------------------------------------------------
 // split: x (view [batch, rows, K], any strides) -> dense hi, lo [batch, rows, Kp]
@@ -139,6 +151,8 @@ struct Params {
   int dop;
   int chunk_kb;     // k-blocks accumulated in TMEM per chunk (CHUNK_KB unless overridden)
   int products;     // PFB_TC_PRODUCTS=1: hi*hi only (timing experiments; not fp32-accurate)
+  int exp;          // PFB_TC_EXP bits (timing experiments, wrong results): 1 = no TMA after
+                    // the first ring fill, 2 = no smem split
 };
 
 __device__ __forceinline__ void stamp(const Params& p, int i) {
@@ -166,27 +180,101 @@ __device__ __forceinline__ void epi4(const Params& p, int bz, int row, int col, 
 
 __device__ __forceinline__ void tma_load_operand(const CUtensorMap* mh, const CUtensorMap* ml,
                                                  int mode, uint64_t* bar, uint8_t* dst_hi,
-                                                 uint8_t* dst_lo, int kb, int row0, int z) {
+                                                 uint8_t* dst_lo, int kb, int row0, int z,
+                                                 int rows) {
   if (mode == kRawMN) {
-#pragma unroll
-    for (int j = 0; j < BM / 32; ++j) tma_load_3d(mh, bar, dst_hi + j * 4096, row0 + 32 * j, kb * BK, z);
+    for (int j = 0; j < rows / 32; ++j) tma_load_3d(mh, bar, dst_hi + j * 4096, row0 + 32 * j, kb * BK, z);
   } else {
     tma_load_3d(mh, bar, dst_hi, kb * BK, row0, z);
     if (mode == kPreSplit) tma_load_3d(ml, bar, dst_lo, kb * BK, row0, z);
   }
 }
 
-// raw tiles split in place (tc_ptx.cuh), 256 accumulator threads
-__device__ __forceinline__ void split_tile_smem(uint8_t* hi, uint8_t* lo, int t) {
-  split_tf32_smem(smem_u32(hi), smem_u32(lo), TILE_BYTES / 16, t, 32 * EPI_WARPS);
+// raw tiles split in place (tc_ptx.cuh), 256 split threads
+__device__ __forceinline__ void split_tile_smem(uint8_t* hi, uint8_t* lo, int bytes, int t) {
+  split_tf32_smem(smem_u32(hi), smem_u32(lo), bytes / 16, t, 32 * EPI_WARPS);
 }
 
+// Rows [rb, re) of the split-K tile summed over the cluster's KS partial
+// tiles (each CTA's own smem, rows x BN floats, 16-byte chunks XOR-swizzled by
+// row), in rank order -> the epilogue -> C.  Up to 16 remote 16-byte loads are
+// issued before the first is added (DSMEM latency ~200 cycles each).
+__device__ __forceinline__ float4 ld_dsmem_f4_nv(uint32_t remote) {
+  float4 v;
+  asm("ld.shared::cluster.v4.f32 {%0, %1, %2, %3}, [%4];"
+      : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w)
+      : "r"(remote));
+  return v;
+}
+
+template <int KS, int BN>
+__device__ __forceinline__ void cluster_reduce(const Params& p, uint32_t red, int rb, int re,
+                                               int m0, int n0, int bz) {
+  constexpr int PER = 16 / KS;  // items per pass per thread
+  uint32_t base[KS];
+#pragma unroll
+  for (int q = 0; q < KS; ++q)
+    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(base[q]) : "r"(red), "r"(q));
+  const int items = (re - rb) * (BN / 4);
+  float* cbase = p.C + bz * p.scb;
+  for (int i0 = threadIdx.x; i0 < items; i0 += PER * NUM_THREADS) {
+    float4 w[PER][KS];
+#pragma unroll
+    for (int j = 0; j < PER; ++j) {
+      const int idx = i0 + j * NUM_THREADS;
+      if (idx < items) {
+        const int row = rb + idx / (BN / 4), ch = idx % (BN / 4);
+        const uint32_t off = (uint32_t)(row * BN + 4 * (ch ^ (row & 7))) * 4u;
+#pragma unroll
+        for (int q = 0; q < KS; ++q) w[j][q] = ld_dsmem_f4_nv(base[q] + off);
+      }
+    }
+#pragma unroll
+    for (int j = 0; j < PER; ++j) {
+      const int idx = i0 + j * NUM_THREADS;
+      if (idx >= items) continue;
+      float4 v = w[j][0];
+#pragma unroll
+      for (int q = 1; q < KS; ++q) { v.x += w[j][q].x; v.y += w[j][q].y; v.z += w[j][q].z; v.w += w[j][q].w; }
+      const int row = rb + idx / (BN / 4), ch = idx % (BN / 4);
+      const int grow = m0 + row, col = n0 + 4 * ch;
+      if (grow >= p.M) continue;
+      const float alpha = p.alpha_rows ? __ldg(p.alpha_rows + (int64_t)bz * p.M + grow) : 1.f;
+      v.x *= alpha; v.y *= alpha; v.z *= alpha; v.w *= alpha;
+      float* q = cbase + (int64_t)grow * p.scm + (int64_t)col * p.scn;
+      if (p.scn == 1 && col + 3 < p.N && ((reinterpret_cast<uintptr_t>(q) & 15) == 0)) {
+        if (p.accumulate) {
+          const float4 o = *reinterpret_cast<const float4*>(q);
+          v.x += o.x; v.y += o.y; v.z += o.z; v.w += o.w;
+        }
+        epi4(p, bz, grow, col, v);
+        *reinterpret_cast<float4*>(q) = v;
+      } else {
+        if (p.accumulate) {
+          if (col < p.N) v.x += q[0];
+          if (col + 1 < p.N) v.y += q[p.scn];
+          if (col + 2 < p.N) v.z += q[2 * p.scn];
+          if (col + 3 < p.N) v.w += q[3 * p.scn];
+        }
+        epi4(p, bz, grow, col, v);
+        const float e[4] = {v.x, v.y, v.z, v.w};
+        for (int jj = 0; jj < 4; ++jj)
+          if (col + jj < p.N) q[(int64_t)jj * p.scn] = e[jj];
+      }
+    }
+  }
+}
+
+template <int BN_>
 __global__ void __launch_bounds__(NUM_THREADS, 1)
 gemm_kernel(const __grid_constant__ CUtensorMap map_ah, const __grid_constant__ CUtensorMap map_al,
             const __grid_constant__ CUtensorMap map_bh, const __grid_constant__ CUtensorMap map_bl,
             const __grid_constant__ CUtensorMap map_c, const __grid_constant__ CUtensorMap map_ah2,
             const __grid_constant__ CUtensorMap map_al2, const __grid_constant__ CUtensorMap map_bh2,
             const __grid_constant__ CUtensorMap map_bl2, Params p) {
+  using C = TileCfg<BN_>;
+  constexpr int BN = C::BN, STAGES = C::STAGES, STAGE_BYTES = C::STAGE_BYTES;
+  constexpr int DCOLS = C::DCOLS, DRAIN_WARPS = C::DRAIN_WARPS;
   stamp(p, 0);
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>(
@@ -211,7 +299,10 @@ gemm_kernel(const __grid_constant__ CUtensorMap map_ah, const __grid_constant__ 
   const bool split_smem = p.a_mode != kPreSplit || p.b_mode != kPreSplit ||
                           (dual && (p.a_mode2 != kPreSplit || p.b_mode2 != kPreSplit));
 
-  auto tile = [&](int s, int which) { return smem + s * STAGE_BYTES + which * TILE_BYTES; };
+  auto tile = [&](int s, int which) {
+    return smem + s * STAGE_BYTES + (which < 2 ? which * TILE_BYTES
+                                               : 2 * TILE_BYTES + (which - 2) * C::B_BYTES);
+  };
   // which: 0 = A_hi, 1 = A_lo, 2 = B_hi, 3 = B_lo
 
   if (threadIdx.x == 0) {
@@ -222,7 +313,7 @@ gemm_kernel(const __grid_constant__ CUtensorMap map_ah, const __grid_constant__ 
     }
     for (int b = 0; b < 2; ++b) {
       mbar_init(&acc_full[b], 1);
-      mbar_init(&acc_empty[b], 32 * EPI_WARPS);
+      mbar_init(&acc_empty[b], 32 * DRAIN_WARPS);
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&map_ah)) : "memory");
@@ -237,7 +328,7 @@ gemm_kernel(const __grid_constant__ CUtensorMap map_ah, const __grid_constant__ 
   if (warp == 1) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
                      smem_u32(tmem_slot)),
-                 "r"(TMEM_COLS));
+                 "r"(C::TMEM_COLS));
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
   }
   asm volatile("tcgen05.fence::before_thread_sync;");
@@ -251,10 +342,11 @@ gemm_kernel(const __grid_constant__ CUtensorMap map_ah, const __grid_constant__ 
   pdl_enter();
   if (threadIdx.x == 0) stamp(p, 2);
 
-  auto tile_bytes = [&](int mode) { return (mode == kPreSplit ? 2 : 1) * TILE_BYTES; };
+  auto a_bytes = [&](int mode) { return (mode == kPreSplit ? 2 : 1) * TILE_BYTES; };
+  auto b_bytes = [&](int mode) { return (mode == kPreSplit ? 2 : 1) * C::B_BYTES; };
 
   if (warp == 0) {
-    if (lane == 0) {
+    if (lane == 0 && !(p.exp & 32)) {
       int g = 0;
       for (int u = blockIdx.x; u < ntiles; u += ustride) {
         const int t = u / p.ksplit, ks = u % p.ksplit;
@@ -264,74 +356,87 @@ gemm_kernel(const __grid_constant__ CUtensorMap map_ah, const __grid_constant__ 
         for (int kb = kb0; kb < kb1; ++kb, ++g) {
           const int s = g % STAGES;
           if (g >= STAGES) mbar_wait(&empty[s], ((g / STAGES) - 1) & 1);
+          if (g < 16) stamp(p, 80 + g);
           if (kb < p.nk1) {
             const int za = p.a_bcast ? 0 : bz, zb = p.b_bcast ? 0 : bz;
-            mbar_expect_tx(&full[s], tile_bytes(p.a_mode) + tile_bytes(p.b_mode));
-            tma_load_operand(&map_ah, &map_al, p.a_mode, &full[s], tile(s, 0), tile(s, 1), kb, m0, za);
-            tma_load_operand(&map_bh, &map_bl, p.b_mode, &full[s], tile(s, 2), tile(s, 3), kb, n0, zb);
+            if (g < 16) stamp(p, 16 + g);
+            mbar_expect_tx(&full[s], a_bytes(p.a_mode) + b_bytes(p.b_mode));
+            tma_load_operand(&map_ah, &map_al, p.a_mode, &full[s], tile(s, 0), tile(s, 1), kb, m0, za, BM);
+            tma_load_operand(&map_bh, &map_bl, p.b_mode, &full[s], tile(s, 2), tile(s, 3), kb, n0, zb, BN);
           } else {
             const int za = p.a_bcast2 ? 0 : bz, zb = p.b_bcast2 ? 0 : bz, k2 = kb - p.nk1;
-            mbar_expect_tx(&full[s], tile_bytes(p.a_mode2) + tile_bytes(p.b_mode2));
-            tma_load_operand(&map_ah2, &map_al2, p.a_mode2, &full[s], tile(s, 0), tile(s, 1), k2, m0, za);
-            tma_load_operand(&map_bh2, &map_bl2, p.b_mode2, &full[s], tile(s, 2), tile(s, 3), k2, n0, zb);
+            mbar_expect_tx(&full[s], a_bytes(p.a_mode2) + b_bytes(p.b_mode2));
+            tma_load_operand(&map_ah2, &map_al2, p.a_mode2, &full[s], tile(s, 0), tile(s, 1), k2, m0, za, BM);
+            tma_load_operand(&map_bh2, &map_bl2, p.b_mode2, &full[s], tile(s, 2), tile(s, 3), k2, n0, zb, BN);
           }
           if (g == 0) stamp(p, 3);
         }
       }
     }
   } else if (warp == 1) {
-    if (lane == 0) {
-      int g = 0, gc = 0;
-      for (int u = blockIdx.x; u < ntiles; u += ustride) {
-        const int ks = u % p.ksplit;
-        const int kb0 = ks * p.kb_per_split, kb1 = min(nk, kb0 + p.kb_per_split);
-        const int uchunks = (kb1 - kb0 + p.chunk_kb - 1) / p.chunk_kb;
-        for (int c = 0; c < uchunks; ++c, ++gc) {
-          const int buf = gc & 1;
-          if (gc >= 2) mbar_wait(&acc_empty[buf], ((gc >> 1) - 1) & 1);
-          asm volatile("tcgen05.fence::after_thread_sync;");
-          const uint32_t tmem_d = tmem_base + (uint32_t)(buf * BN);
-          const int kb_beg = kb0 + c * p.chunk_kb;
-          const int kb_end = min(kb1, kb_beg + p.chunk_kb);
-          for (int kb = kb_beg; kb < kb_end; ++kb, ++g) {
-            const int s = g % STAGES;
-            mbar_wait(split_smem ? &ready[s] : &full[s], (g / STAGES) & 1);
+    // the whole warp runs the loop (warp-uniform control flow: descriptors
+    // and TMEM addresses stay in uniform registers); one elected lane issues
+    // each k-block's MMAs and commits
+    int g = 0, gc = 0;
+    for (int u = blockIdx.x; u < ntiles; u += ustride) {
+      const int ks = u % p.ksplit;
+      const int kb0 = ks * p.kb_per_split, kb1 = min(nk, kb0 + p.kb_per_split);
+      const int uchunks = (kb1 - kb0 + p.chunk_kb - 1) / p.chunk_kb;
+      for (int c = 0; c < uchunks; ++c, ++gc) {
+        const int buf = gc & 1;
+        if (gc >= 2 && !(p.exp & 4)) mbar_wait(&acc_empty[buf], ((gc >> 1) - 1) & 1);
+        asm volatile("tcgen05.fence::after_thread_sync;");
+        const uint32_t tmem_d = tmem_base + (uint32_t)(buf * BN);
+        const int kb_beg = kb0 + c * p.chunk_kb;
+        const int kb_end = min(kb1, kb_beg + p.chunk_kb);
+        for (int kb = kb_beg; kb < kb_end; ++kb, ++g) {
+          const int s = g % STAGES;
+          if (!(p.exp & 16)) mbar_wait(split_smem ? &ready[s] : &full[s], (g / STAGES) & 1);
+          if (lane == 0) {
             if (g == 0) stamp(p, 5);
-            asm volatile("tcgen05.fence::after_thread_sync;");
-            const uint32_t a0 = smem_u32(tile(s, 0)), a1 = smem_u32(tile(s, 1));
-            const uint32_t b0 = smem_u32(tile(s, 2)), b1 = smem_u32(tile(s, 3));
-            const bool second = kb >= p.nk1;
-            const int am_ = second ? p.a_mode2 : p.a_mode, bm_ = second ? p.b_mode2 : p.b_mode;
-            const uint32_t idesc = second ? p.idesc2 : p.idesc;
-            const bool amn = am_ == kRawMN, bmn = bm_ == kRawMN;
-            const uint64_t a_hi = amn ? smem_desc_mn_sw128(a0, p.mn_lbo, p.mn_sbo) : smem_desc_sw128(a0);
-            const uint64_t a_lo = amn ? smem_desc_mn_sw128(a1, p.mn_lbo, p.mn_sbo) : smem_desc_sw128(a1);
-            const uint64_t b_hi = bmn ? smem_desc_mn_sw128(b0, p.mn_lbo, p.mn_sbo) : smem_desc_sw128(b0);
-            const uint64_t b_lo = bmn ? smem_desc_mn_sw128(b1, p.mn_lbo, p.mn_sbo) : smem_desc_sw128(b1);
-            // k-step advance: +32 B inside the swizzle row (K-major) or one
-            // 1 KB atom (MN-major)
-            const uint64_t astep = amn ? (1024 >> 4) : ((UMMA_K * 4) >> 4);
-            const uint64_t bstep = bmn ? (1024 >> 4) : ((UMMA_K * 4) >> 4);
-            const bool lo_lo = am_ != kPreSplit && bm_ != kPreSplit;
+            if (g < 16) stamp(p, 64 + g);
+            if (g < 16 && p.trace != nullptr && blockIdx.x == 0) p.trace[96 + g] = clock64();
+          }
+          asm volatile("tcgen05.fence::after_thread_sync;");
+          const uint32_t a0 = smem_u32(tile(s, 0)), a1 = smem_u32(tile(s, 1));
+          const uint32_t b0 = smem_u32(tile(s, 2)), b1 = smem_u32(tile(s, 3));
+          const bool second = kb >= p.nk1;
+          const int am_ = second ? p.a_mode2 : p.a_mode, bm_ = second ? p.b_mode2 : p.b_mode;
+          const uint32_t idesc = second ? p.idesc2 : p.idesc;
+          const bool amn = am_ == kRawMN, bmn = bm_ == kRawMN;
+          const uint64_t a_hi = amn ? smem_desc_mn_sw128(a0, p.mn_lbo, p.mn_sbo) : smem_desc_sw128(a0);
+          const uint64_t a_lo = amn ? smem_desc_mn_sw128(a1, p.mn_lbo, p.mn_sbo) : smem_desc_sw128(a1);
+          const uint64_t b_hi = bmn ? smem_desc_mn_sw128(b0, p.mn_lbo, p.mn_sbo) : smem_desc_sw128(b0);
+          const uint64_t b_lo = bmn ? smem_desc_mn_sw128(b1, p.mn_lbo, p.mn_sbo) : smem_desc_sw128(b1);
+          // k-step advance: +32 B inside the swizzle row (K-major) or one
+          // 1 KB atom (MN-major)
+          const uint64_t astep = amn ? (1024 >> 4) : ((UMMA_K * 4) >> 4);
+          const uint64_t bstep = bmn ? (1024 >> 4) : ((UMMA_K * 4) >> 4);
+          const bool lo_lo = am_ != kPreSplit && bm_ != kPreSplit;
+          const bool three = p.products != 1;
+          if (elect_one()) {
 #pragma unroll
             for (int k = 0; k < BK / UMMA_K; ++k) {
               const uint64_t da = astep * k, db = bstep * k;
               const uint32_t acc = (kb > kb_beg || k > 0) ? 1u : 0u;
               mma_tf32(tmem_d, a_hi + da, b_hi + db, idesc, acc);
-              if (p.products == 1) continue;
-              mma_tf32(tmem_d, a_hi + da, b_lo + db, idesc, 1u);
-              mma_tf32(tmem_d, a_lo + da, b_hi + db, idesc, 1u);
-              // both operands raw: hi = trunc_tf32 on both sides makes the
-              // dropped lo*lo term sign-biased, so it is kept
-              if (lo_lo) mma_tf32(tmem_d, a_lo + da, b_lo + db, idesc, 1u);
+              if (three) {
+                mma_tf32(tmem_d, a_hi + da, b_lo + db, idesc, 1u);
+                mma_tf32(tmem_d, a_lo + da, b_hi + db, idesc, 1u);
+                // both operands raw: hi = trunc_tf32 on both sides makes the
+                // dropped lo*lo term sign-biased, so it is kept
+                if (lo_lo) mma_tf32(tmem_d, a_lo + da, b_lo + db, idesc, 1u);
+              }
             }
             mma_commit(&empty[s]);
           }
-          mma_commit(&acc_full[buf]);
+          __syncwarp();
         }
+        if (elect_one()) mma_commit(&acc_full[buf]);
+        __syncwarp();
       }
-      stamp(p, 6);
     }
+    if (lane == 0) stamp(p, 6);
     __syncwarp();
   } else {
     // ---- split + accumulators + epilogue (warps 2..9): warp w owns TMEM
@@ -346,32 +451,38 @@ gemm_kernel(const __grid_constant__ CUtensorMap map_ah, const __grid_constant__ 
       const int s = gs % STAGES;
       mbar_wait(&full[s], (gs / STAGES) & 1);
       if (gs == 0 && et == 0) stamp(p, 4);
+      if (gs < 16 && et == 0) stamp(p, 32 + gs);
       const bool second = kb >= p.nk1;
-      if ((second ? p.a_mode2 : p.a_mode) != kPreSplit) split_tile_smem(tile(s, 0), tile(s, 1), et);
-      if ((second ? p.b_mode2 : p.b_mode) != kPreSplit) split_tile_smem(tile(s, 2), tile(s, 3), et);
+      if ((second ? p.a_mode2 : p.a_mode) != kPreSplit && !(p.exp & 2))
+        split_tile_smem(tile(s, 0), tile(s, 1), TILE_BYTES, et);
+      if ((second ? p.b_mode2 : p.b_mode) != kPreSplit && !(p.exp & 2))
+        split_tile_smem(tile(s, 2), tile(s, 3), C::B_BYTES, et);
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
       __syncwarp();
       if (lane == 0) mbar_arrive(&ready[s]);
+      if (gs < 16 && et == 0) stamp(p, 48 + gs);
       ++gs;
     };
-    float acc[EPI_COLS];
+    float acc[DCOLS];
+    const bool drains = (warp - 2) < DRAIN_WARPS;
     auto drain = [&]() {
       const int buf = gc & 1;
-      mbar_wait(&acc_full[buf], (gc >> 1) & 1);
-      if (gc == 0 && et == 0) stamp(p, 7);
+      ++gc;
+      if (!drains || (p.exp & 4)) return;
+      mbar_wait(&acc_full[buf], ((gc - 1) >> 1) & 1);
+      if (gc == 1 && et == 0) stamp(p, 7);
       asm volatile("tcgen05.fence::after_thread_sync;");
 #pragma unroll
-      for (int cc = 0; cc < EPI_COLS; cc += 32) {
+      for (int cc = 0; cc < DCOLS; cc += 32) {
         uint32_t v[32];
         tmem_ld32(tmem_base + ((uint32_t)(quarter * 32) << 16) +
-                      (uint32_t)(buf * BN + half * EPI_COLS + cc), v);
+                      (uint32_t)(buf * BN + half * DCOLS + cc), v);
         asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 #pragma unroll
         for (int j = 0; j < 32; ++j) acc[cc + j] += __uint_as_float(v[j]);
       }
       asm volatile("tcgen05.fence::before_thread_sync;");
       mbar_arrive(&acc_empty[buf]);
-      ++gc;
     };
     for (int u = blockIdx.x; u < ntiles; u += ustride) {
       const int t = u / p.ksplit, ks = u % p.ksplit;
@@ -380,25 +491,27 @@ gemm_kernel(const __grid_constant__ CUtensorMap map_ah, const __grid_constant__ 
       const int kb0 = ks * p.kb_per_split, kb1 = min(nk, kb0 + p.kb_per_split);
       const int uchunks = (kb1 - kb0 + p.chunk_kb - 1) / p.chunk_kb;
 #pragma unroll
-      for (int j = 0; j < EPI_COLS; ++j) acc[j] = 0.f;
+      for (int j = 0; j < DCOLS; ++j) acc[j] = 0.f;
       // split chunk c's stages, then drain chunk c-1 (the MMA works on
       // chunk c-1 while the stages of chunk c are being split)
       for (int c = 0; c < uchunks; ++c) {
         if (split_smem) {
           const int kb_beg = kb0 + c * p.chunk_kb, kb_end = min(kb1, kb_beg + p.chunk_kb);
-          for (int kb = kb_beg; kb < kb_end; ++kb) split_stage(kb);
+          if (!(p.exp & 32))
+            for (int kb = kb_beg; kb < kb_end; ++kb) split_stage(kb);
         }
         if (c > 0) drain();
       }
       drain();
+      if (!drains) continue;
       if (clustered) {
         // partial tile -> own smem (stage area is idle: every MMA of this
-        // CTA's only unit has completed), rows x 32 float4, XOR-swizzled
+        // CTA's only unit has completed), rows x BN/4 float4, XOR-swizzled
         float* red = reinterpret_cast<float*>(smem);
         const int row = quarter * 32 + lane;
 #pragma unroll
-        for (int j = 0; j < EPI_COLS / 4; ++j) {
-          const int ch = half * (EPI_COLS / 4) + j;
+        for (int j = 0; j < DCOLS / 4; ++j) {
+          const int ch = half * (DCOLS / 4) + j;
           *reinterpret_cast<float4*>(red + row * BN + 4 * (ch ^ (row & 7))) =
               make_float4(acc[4 * j], acc[4 * j + 1], acc[4 * j + 2], acc[4 * j + 3]);
         }
@@ -413,10 +526,10 @@ gemm_kernel(const __grid_constant__ CUtensorMap map_ah, const __grid_constant__ 
         const float alpha =
             (p.alpha_rows && grow < p.M) ? __ldg(p.alpha_rows + (int64_t)bz * p.M + grow) : 1.f;
 #pragma unroll
-        for (int cc = 0; cc < EPI_COLS; cc += 32) {
+        for (int cc = 0; cc < DCOLS; cc += 32) {
           if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
           __syncwarp();
-          const int col0 = n0 + half * EPI_COLS + cc;
+          const int col0 = n0 + half * DCOLS + cc;
 #pragma unroll
           for (int q = 0; q < 8; ++q) {
             float4 v = make_float4(acc[cc + 4 * q] * alpha, acc[cc + 4 * q + 1] * alpha,
@@ -439,14 +552,14 @@ gemm_kernel(const __grid_constant__ CUtensorMap map_ah, const __grid_constant__ 
       const int64_t ldm = p.scm, ldn = p.scn;
       const int sub_r = lane >> 3, sub_c = (lane & 7) * 4;
 #pragma unroll
-      for (int cc = 0; cc < EPI_COLS; cc += 32) {
+      for (int cc = 0; cc < DCOLS; cc += 32) {
 #pragma unroll
         for (int q = 0; q < 8; ++q)
           *reinterpret_cast<float4*>(stage + lane * 32 + 4 * (q ^ (lane & 7))) =
               make_float4(acc[cc + 4 * q], acc[cc + 4 * q + 1], acc[cc + 4 * q + 2],
                           acc[cc + 4 * q + 3]);
         __syncwarp();
-        const int col = n0 + half * EPI_COLS + cc + sub_c;
+        const int col = n0 + half * DCOLS + cc + sub_c;
 #pragma unroll 4
         for (int i = 0; i < 32; i += 4) {
           const int row = row0 + i + sub_r;
@@ -501,50 +614,21 @@ gemm_kernel(const __grid_constant__ CUtensorMap map_ah, const __grid_constant__ 
     const int rows_per = (BM + p.ksplit - 1) / p.ksplit;
     const int rb = rank * rows_per, re = min(BM, rb + rows_per);
     const uint32_t red = smem_u32(smem);
-    float* cbase = p.C + bz * p.scb;
-    for (int idx = threadIdx.x; idx < (re - rb) * (BN / 4); idx += NUM_THREADS) {
-      const int row = rb + idx / (BN / 4), ch = idx % (BN / 4);
-      const uint32_t off = (uint32_t)(row * BN + 4 * (ch ^ (row & 7))) * 4u;
-      // all partials requested before the first is added (rank order kept)
-      float4 w[kMaxSplit];
-#pragma unroll
-      for (int q = 0; q < kMaxSplit; ++q)
-        if (q < p.ksplit) w[q] = ld_dsmem_f4(red + off, (uint32_t)q);
-      float4 v = w[0];
-#pragma unroll
-      for (int q = 1; q < kMaxSplit; ++q)
-        if (q < p.ksplit) { v.x += w[q].x; v.y += w[q].y; v.z += w[q].z; v.w += w[q].w; }
-      const int grow = m0 + row, col = n0 + 4 * ch;
-      if (grow >= p.M) continue;
-      const float alpha = p.alpha_rows ? __ldg(p.alpha_rows + (int64_t)bz * p.M + grow) : 1.f;
-      v.x *= alpha; v.y *= alpha; v.z *= alpha; v.w *= alpha;
-      float* q = cbase + (int64_t)grow * p.scm + (int64_t)col * p.scn;
-      if (p.scn == 1 && col + 3 < p.N && ((reinterpret_cast<uintptr_t>(q) & 15) == 0)) {
-        if (p.accumulate) {
-          const float4 o = *reinterpret_cast<const float4*>(q);
-          v.x += o.x; v.y += o.y; v.z += o.z; v.w += o.w;
-        }
-        epi4(p, bz, grow, col, v);
-        *reinterpret_cast<float4*>(q) = v;
-      } else {
-        if (p.accumulate) {
-          if (col < p.N) v.x += q[0];
-          if (col + 1 < p.N) v.y += q[p.scn];
-          if (col + 2 < p.N) v.z += q[2 * p.scn];
-          if (col + 3 < p.N) v.w += q[3 * p.scn];
-        }
-        epi4(p, bz, grow, col, v);
-        const float e[4] = {v.x, v.y, v.z, v.w};
-        for (int j = 0; j < 4; ++j)
-          if (col + j < p.N) q[(int64_t)j * p.scn] = e[j];
-      }
+    switch (p.ksplit) {
+      case 2: cluster_reduce<2, BN>(p, red, rb, re, m0, n0, bz); break;
+      case 3: cluster_reduce<3, BN>(p, red, rb, re, m0, n0, bz); break;
+      case 4: cluster_reduce<4, BN>(p, red, rb, re, m0, n0, bz); break;
+      case 5: cluster_reduce<5, BN>(p, red, rb, re, m0, n0, bz); break;
+      case 6: cluster_reduce<6, BN>(p, red, rb, re, m0, n0, bz); break;
+      case 7: cluster_reduce<7, BN>(p, red, rb, re, m0, n0, bz); break;
+      default: cluster_reduce<8, BN>(p, red, rb, re, m0, n0, bz); break;
     }
     cluster_sync_all();  // peers' smem stays live until every CTA has read it
   }
   if (warp == 1) {
     asm volatile("tcgen05.fence::after_thread_sync;");
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base),
-                 "r"(TMEM_COLS));
+                 "r"(C::TMEM_COLS));
     if (lane == 0) stamp(p, 10);
   }
 }
@@ -552,10 +636,11 @@ gemm_kernel(const __grid_constant__ CUtensorMap map_ah, const __grid_constant__ 
 // --- host side -------------------------------------------------------------
 
 // dense K-major plane [batch][rows][Kp]
-static bool make_map(CUtensorMap* map, const float* base, int64_t Kp, int64_t rows, int64_t batch) {
+static bool make_map(CUtensorMap* map, const float* base, int64_t Kp, int64_t rows, int64_t batch,
+                     int box_rows = BM) {
   cuuint64_t dims[3] = {(cuuint64_t)Kp, (cuuint64_t)rows, (cuuint64_t)batch};
   cuuint64_t strides[2] = {(cuuint64_t)(Kp * 4), (cuuint64_t)(rows * Kp * 4)};
-  cuuint32_t box[3] = {BK, BM, 1};
+  cuuint32_t box[3] = {BK, (cuuint32_t)box_rows, 1};
   return encode(map, base, dims, strides, box);
 }
 
@@ -572,12 +657,12 @@ static int raw_mode(const float* base, int64_t rows, int64_t K, int64_t nb, int6
 }
 
 static bool make_raw_map(CUtensorMap* map, int mode, const float* base, int64_t rows, int64_t K,
-                         int64_t nb, int64_t sb, int64_t sr, int64_t sk) {
+                         int64_t nb, int64_t sb, int64_t sr, int64_t sk, int box_rows = BM) {
   if (mode == kRawK) {
     const int64_t ld = rows == 1 ? (K + 3) / 4 * 4 : sr;
     cuuint64_t dims[3] = {(cuuint64_t)K, (cuuint64_t)rows, (cuuint64_t)nb};
     cuuint64_t strides[2] = {(cuuint64_t)(ld * 4), (cuuint64_t)((nb == 1 ? ld * rows : sb) * 4)};
-    cuuint32_t box[3] = {BK, BM, 1};
+    cuuint32_t box[3] = {BK, (cuuint32_t)box_rows, 1};
     return encode(map, base, dims, strides, box);
   }
   cuuint64_t dims[3] = {(cuuint64_t)rows, (cuuint64_t)K, (cuuint64_t)nb};
@@ -611,7 +696,7 @@ static int chunk_kb() {
   return c;
 }
 
-static void choose_split(const GemmArgs& g, int* ksplit, int* kb_per) {
+static void choose_split(const GemmArgs& g, int* ksplit, int* kb_per, int BN = 128) {
   const int CHUNK_KB = chunk_kb();
   const int64_t tiles = ((g.M + BM - 1) / BM) * ((g.N + BN - 1) / BN) * g.batch;
   const int64_t Kp = (g.K + 3) / 4 * 4;
@@ -657,8 +742,8 @@ static unsigned long long* g_trace = nullptr;
 unsigned long long* tc_trace_buffer() {
   static const bool on = getenv_flag("PFB_TC_TRACE");
   if (on && g_trace == nullptr) {
-    cudaMalloc(&g_trace, 16 * sizeof(unsigned long long));
-    cudaMemset(g_trace, 0, 16 * sizeof(unsigned long long));
+    cudaMalloc(&g_trace, 128 * sizeof(unsigned long long));
+    cudaMemset(g_trace, 0, 128 * sizeof(unsigned long long));
   }
   return on ? g_trace : nullptr;
 }
@@ -739,7 +824,8 @@ static int64_t pair_need(const GemmArgs& g, int variant, int* am_out, int* bm_ou
          (bm == kPreSplit && !g.b_hi ? 2 * align_up(bb * g.N * Kp * 4) : 0);
 }
 
-static int prep_pair(const GemmArgs& g, int variant, char*& w, cudaStream_t s, PairFeed* f) {
+static int prep_pair(const GemmArgs& g, int variant, char*& w, cudaStream_t s, PairFeed* f,
+                     int bn = 128) {
   f->Kp = (g.K + 3) / 4 * 4;
   const int64_t Kp = f->Kp;
   // a per-batch kscale makes B's planes differ per batch even for a shared B
@@ -758,8 +844,9 @@ static int prep_pair(const GemmArgs& g, int variant, char*& w, cudaStream_t s, P
     if (!make_raw_map(&f->ah, f->am, g.A, g.M, g.K, ba, g.sab, g.sam, g.sak)) return PFB_E_UNSUPPORTED;
     f->al = f->ah;
   }
+  if (f->bm == kRawMN && bn % 32 != 0) f->bm = kPreSplit;
   if (f->bm == kPreSplit && g.b_hi) {  // planes made once by pfb_gemm_split_planes
-    if (!make_map(&f->bh, g.b_hi, Kp, g.N, bb) || !make_map(&f->bl, g.b_lo, Kp, g.N, bb))
+    if (!make_map(&f->bh, g.b_hi, Kp, g.N, bb, bn) || !make_map(&f->bl, g.b_lo, Kp, g.N, bb, bn))
       return PFB_E_UNSUPPORTED;
   } else if (f->bm == kPreSplit) {
     float* bh = reinterpret_cast<float*>(w); w += align_up(bb * g.N * Kp * 4);
@@ -767,9 +854,11 @@ static int prep_pair(const GemmArgs& g, int variant, char*& w, cudaStream_t s, P
     dim3 gb((unsigned)((Kp + 31) / 32), (unsigned)((g.N + 31) / 32), (unsigned)bb);
     launch(split_kernel, gb, 256, 0, s, g.B, g.N, g.K, Kp, g.sbb, g.sbn, g.sbk, bh, bl, g.kscale,
            g.skb, g.skk);
-    if (!make_map(&f->bh, bh, Kp, g.N, bb) || !make_map(&f->bl, bl, Kp, g.N, bb)) return PFB_E_UNSUPPORTED;
+    if (!make_map(&f->bh, bh, Kp, g.N, bb, bn) || !make_map(&f->bl, bl, Kp, g.N, bb, bn))
+      return PFB_E_UNSUPPORTED;
   } else {
-    if (!make_raw_map(&f->bh, f->bm, g.B, g.N, g.K, bb, g.sbb, g.sbn, g.sbk)) return PFB_E_UNSUPPORTED;
+    if (!make_raw_map(&f->bh, f->bm, g.B, g.N, g.K, bb, g.sbb, g.sbn, g.sbk, bn))
+      return PFB_E_UNSUPPORTED;
     f->bl = f->bh;
   }
   return 0;
@@ -777,11 +866,14 @@ static int prep_pair(const GemmArgs& g, int variant, char*& w, cudaStream_t s, P
 
 // g carries the output, epilogue and (for the split model) the total K;
 // f2 == nullptr: one operand pair
+template <int BN>
 static int launch_gemm(const GemmArgs& g, const PairFeed& f1, const PairFeed* f2, cudaStream_t s,
                        int ksplit_want) {
+  using C = TileCfg<BN>;
   static bool attr = false;
   if (!attr) {
-    cudaFuncSetAttribute(gemm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES);
+    cudaFuncSetAttribute(gemm_kernel<BN>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         C::SMEM_BYTES);
     attr = true;
   }
   const int nk1 = (int)((f1.Kp + BK - 1) / BK);
@@ -789,7 +881,7 @@ static int launch_gemm(const GemmArgs& g, const PairFeed& f1, const PairFeed* f2
   GemmArgs gm = g;
   gm.K = (int64_t)nk * BK;
   int ksplit, kb_per;
-  choose_split(gm, &ksplit, &kb_per);
+  choose_split(gm, &ksplit, &kb_per, BN);
   if (const char* e = getenv("PFB_TC_KSPLIT")) ksplit_want = atoi(e);  // bring-up override
   if (ksplit_want > 0) {  // autotuner candidate / override: this many k-splits
     const int want = std::max(1, std::min(ksplit_want, kMaxCluster));
@@ -810,7 +902,7 @@ static int launch_gemm(const GemmArgs& g, const PairFeed& f1, const PairFeed* f2
     tma_store = encode(&mc, g.C, dims, strides, box) ? 1 : 0;
   }
   auto idesc_of = [](const PairFeed& f) {
-    return kIdesc | ((uint32_t)(f.am == kRawMN) << 15) | ((uint32_t)(f.bm == kRawMN) << 16);
+    return C::IDESC | ((uint32_t)(f.am == kRawMN) << 15) | ((uint32_t)(f.bm == kRawMN) << 16);
   };
   const PairFeed& q = f2 ? *f2 : f1;
   Params p{(int)g.M, (int)g.N, nk * BK, (int)g.batch,
@@ -818,14 +910,15 @@ static int launch_gemm(const GemmArgs& g, const PairFeed& f1, const PairFeed* f2
            idesc_of(f1), g.C, g.scb, g.scm, g.scn, g.alpha_rows, g.accumulate, ksplit, kb_per,
            g.bias, g.sxb, g.sxm, g.sxn, g.act, 4096u, 512u, tma_store, tc_trace_buffer(),
            nk1, q.am, q.bm, q.a_bc, q.b_bc, idesc_of(q), g.dy, g.sdb, g.sdm, g.sdn, g.dop,
-           chunk_kb(), getenv("PFB_TC_PRODUCTS") ? atoi(getenv("PFB_TC_PRODUCTS")) : 3};
+           chunk_kb(), getenv("PFB_TC_PRODUCTS") ? atoi(getenv("PFB_TC_PRODUCTS")) : 3,
+           getenv("PFB_TC_EXP") ? atoi(getenv("PFB_TC_EXP")) : 0};
   const int64_t units = (int64_t)p.ntm * p.ntn * g.batch * ksplit;
   if (ksplit > 1) {
     // one CTA per (tile, k-split); the k-splits of a tile are one cluster
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3((unsigned)units);
     cfg.blockDim = dim3(NUM_THREADS);
-    cfg.dynamicSmemBytes = SMEM_BYTES;
+    cfg.dynamicSmemBytes = C::SMEM_BYTES;
     cfg.stream = s;
     cudaLaunchAttribute at[2];
     at[0].id = cudaLaunchAttributeClusterDimension;
@@ -837,19 +930,27 @@ static int launch_gemm(const GemmArgs& g, const PairFeed& f1, const PairFeed* f2
     cfg.attrs = at;
     cfg.numAttrs = pdl_enabled() ? 2 : 1;
     kernel_launches()++;
-    cudaLaunchKernelEx(&cfg, gemm_kernel, f1.ah, f1.al, f1.bh, f1.bl, mc, q.ah, q.al, q.bh, q.bl, p);
+    cudaLaunchKernelEx(&cfg, gemm_kernel<BN>, f1.ah, f1.al, f1.bh, f1.bl, mc, q.ah, q.al, q.bh, q.bl,
+                       p);
   } else {
     const int grid = (int)std::min<int64_t>(units, num_sms());
-    launch(gemm_kernel, grid, NUM_THREADS, SMEM_BYTES, s, f1.ah, f1.al, f1.bh, f1.bl, mc, q.ah,
+    launch(gemm_kernel<BN>, grid, NUM_THREADS, C::SMEM_BYTES, s, f1.ah, f1.al, f1.bh, f1.bl, mc, q.ah,
            q.al, q.bh, q.bl, p);
   }
   return launch_status();
 }
 
+static int launch_bn(int bn, const GemmArgs& g, const PairFeed& f1, const PairFeed* f2,
+                     cudaStream_t s, int ksplit_want) {
+  if (bn == 32) return launch_gemm<32>(g, f1, f2, s, ksplit_want);
+  if (bn == 64) return launch_gemm<64>(g, f1, f2, s, ksplit_want);
+  return launch_gemm<128>(g, f1, f2, s, ksplit_want);
+}
+
 }  // namespace tc
 
 int gemm_tcgen05(const GemmArgs& g, void* ws, int64_t ws_bytes, cudaStream_t s, int variant,
-                 int ksplit_want) {
+                 int ksplit_want, int bn) {
   using namespace tc;
   if (!gemm_tcgen05_eligible(g)) return PFB_E_UNSUPPORTED;
   if (variant == 0) variant = (2.0 * g.M * g.N * g.K * g.batch < 4e9) ? 2 : 1;
@@ -858,9 +959,11 @@ int gemm_tcgen05(const GemmArgs& g, void* ws, int64_t ws_bytes, cudaStream_t s, 
   const int64_t need = pair_need(g, variant, &am, &bm);
   if (need > 0 && (ws == nullptr || ws_bytes < need)) return PFB_E_UNSUPPORTED;
   char* w = static_cast<char*>(ws);
+  if (const char* e = getenv("PFB_TC_BN")) bn = atoi(e);  // experiments
+  if (bn != 32 && bn != 64) bn = 128;
   PairFeed f;
-  if (int e = prep_pair(g, variant, w, s, &f)) return e;
-  return launch_gemm(g, f, nullptr, s, ksplit_want);
+  if (int e = prep_pair(g, variant, w, s, &f, bn)) return e;
+  return launch_bn(bn, g, f, nullptr, s, ksplit_want);
 }
 
 int64_t gemm_tcgen05_dual_workspace(const GemmArgs& g1, const GemmArgs& g2) {
@@ -870,7 +973,7 @@ int64_t gemm_tcgen05_dual_workspace(const GemmArgs& g1, const GemmArgs& g2) {
 // C = epi(A1 B1 + A2 B2): both pairs accumulate into one TMEM tile (the
 // K ranges are consecutive k-blocks of one launch); g1 carries C/epilogue.
 int gemm_tcgen05_dual(const GemmArgs& g1, const GemmArgs& g2, void* ws, int64_t ws_bytes,
-                      cudaStream_t s, int variant, int ksplit_want) {
+                      cudaStream_t s, int variant, int ksplit_want, int bn) {
   using namespace tc;
   if (!gemm_tcgen05_eligible(g1) || !gemm_tcgen05_eligible(g2)) return PFB_E_UNSUPPORTED;
   if (g1.M != g2.M || g1.N != g2.N || g1.batch != g2.batch || g2.kscale) return PFB_E_UNSUPPORTED;
@@ -879,10 +982,11 @@ int gemm_tcgen05_dual(const GemmArgs& g1, const GemmArgs& g2, void* ws, int64_t 
   const int64_t need = pair_need(g1, variant, &a1, &b1) + pair_need(g2, variant, &a2, &b2);
   if (need > 0 && (ws == nullptr || ws_bytes < need)) return PFB_E_UNSUPPORTED;
   char* w = static_cast<char*>(ws);
+  if (bn != 32 && bn != 64) bn = 128;
   PairFeed f1, f2;
-  if (int e = prep_pair(g1, variant, w, s, &f1)) return e;
-  if (int e = prep_pair(g2, variant, w, s, &f2)) return e;
-  return launch_gemm(g1, f1, &f2, s, ksplit_want);
+  if (int e = prep_pair(g1, variant, w, s, &f1, bn)) return e;
+  if (int e = prep_pair(g2, variant, w, s, &f2, bn)) return e;
+  return launch_bn(bn, g1, f1, &f2, s, ksplit_want);
 }
 
 }  // namespace pfb
@@ -890,6 +994,6 @@ int gemm_tcgen05_dual(const GemmArgs& g1, const GemmArgs& g2, void* ws, int64_t 
 extern "C" int pfb_debug_tc_trace(unsigned long long* out16) {
   if (pfb::g_trace == nullptr) return PFB_E_UNSUPPORTED;
   cudaDeviceSynchronize();
-  return cudaMemcpy(out16, pfb::g_trace, 16 * sizeof(unsigned long long), cudaMemcpyDeviceToHost) ==
+  return cudaMemcpy(out16, pfb::g_trace, 128 * sizeof(unsigned long long), cudaMemcpyDeviceToHost) ==
                  cudaSuccess ? 0 : PFB_E_ARG;
 }

@@ -197,6 +197,15 @@ __device__ __forceinline__ void split_tf32_smem(uint32_t hi, uint32_t lo, int n1
   }
 }
 
+// one lane of the (converged) warp returns true (elect.sync)
+__device__ __forceinline__ bool elect_one() {
+  uint32_t pred = 0;
+  asm volatile(
+      "{\n\t.reg .pred P;\n\telect.sync _|P, 0xffffffff;\n\tselp.u32 %0, 1, 0, P;\n\t}"
+      : "=r"(pred));
+  return pred != 0;
+}
+
 // named barrier over `nthreads` threads (id 0 is __syncthreads)
 __device__ __forceinline__ void named_bar(int id, int nthreads) {
   asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");

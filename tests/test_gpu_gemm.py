@@ -387,3 +387,35 @@ def test_gemm_simt_split_candidates(env, shape, force):
         a, b = _operands(r, (m, k), (k, n))
     got = _run(env, a, b, force, transpose_b=True)
     np.testing.assert_allclose(got, a @ b, rtol=RTOL, atol=ATOL)
+
+
+# Narrow tcgen05 tiles (BN 64 / 32) for skinny-M problems: 12 / 13 = model
+# k-split, 14-17 = forced 2 / 4 k-splits (cluster DSMEM reduction).
+NARROW_SHAPES = [(256, 2048, 1024), (256, 512, 2048), (200, 300, 100), (513, 129, 1000),
+                 (96, 160, 37), (64, 520, 256)]
+
+
+@pytest.mark.parametrize("shape", NARROW_SHAPES)
+@pytest.mark.parametrize("layout", ["a_k/b_mn", "a_k/b_k", "a_mn/b_k"])
+@pytest.mark.parametrize("force", [12, 13, 14, 15, 16, 17])
+def test_gemm_tcgen05_narrow_tiles(env, shape, layout, force):
+    m, n, k = shape
+    r = np.random.default_rng(m * 5 + n + k)
+    a, b = _operands(r, (m, k), (k, n))
+    got = _run(env, a, b, force, transpose_b=layout.endswith("b_k"),
+               a_mn=layout.startswith("a_mn"))
+    np.testing.assert_allclose(got, a @ b, rtol=RTOL, atol=ATOL)
+
+
+@pytest.mark.parametrize("force", [13, 15, 17])
+def test_gemm_narrow_tiles_epilogue(env, force):
+    """bias + tanh epilogue and alpha-rows / accumulate on the narrow tiles."""
+    r = np.random.default_rng(31)
+    a, b = _operands(r, (256, 1024), (1024, 512))
+    bias = _f32(r, (512,))
+    got = _run_fused(env, a, b, force, bias=bias, act=1)
+    np.testing.assert_allclose(got, np.tanh(a @ b + bias), rtol=RTOL, atol=ATOL)
+    c0 = _f32(r, (256, 512))
+    alpha = np.asarray(r.standard_normal(256), np.float32).astype(np.float64)
+    got = _run(env, a, b, force, accumulate_into=c0, alpha=alpha)
+    np.testing.assert_allclose(got, c0 + alpha[:, None] * (a @ b), rtol=RTOL, atol=ATOL)

@@ -1,0 +1,167 @@
+// Microbenchmark: the GEMM kernel's exact MMA operand pattern (3 stages x
+// {A_hi, A_lo, B_hi, B_lo} 16 KB tiles, 4 k-steps x 3 products per stage)
+// vs a single repeated operand pair.  Cycles per MMA, one CTA per SM.
+#include <cstdio>
+#include <cstdlib>
+#include <cstdint>
+#include <cuda_runtime.h>
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ uint64_t desc_sw128(uint32_t addr) {
+  uint64_t d = 0;
+  d |= (uint64_t)((addr & 0x3FFFF) >> 4);
+  d |= (uint64_t)(16 >> 4) << 16;
+  d |= (uint64_t)(1024 >> 4) << 32;
+  d |= (uint64_t)1 << 46;
+  d |= (uint64_t)2 << 61;
+  return d;
+}
+__device__ __forceinline__ void mma(uint32_t tm, uint64_t a, uint64_t b, uint32_t idesc, uint32_t acc) {
+  asm volatile("{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
+               "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n}"
+               ::"r"(tm), "l"(a), "l"(b), "r"(idesc), "r"(acc));
+}
+
+__global__ void __launch_bounds__(320, 1) bench(int mode, uint32_t idesc, int reps, long long* out) {
+  if (mode == 9) {
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+    asm volatile("griddepcontrol.launch_dependents;" :::);
+  }
+  extern __shared__ uint8_t raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(raw) + 1023) & ~uintptr_t(1023));
+  __shared__ uint64_t bar, done, emp[3], fin;
+  __shared__ uint32_t tslot;
+  for (int i = threadIdx.x; i < 192 * 1024 / 4; i += blockDim.x) {
+    uint32_t h = (uint32_t)i * 2654435761u + blockIdx.x;
+    h ^= h >> 13; h *= 0x5bd1e995u; h ^= h >> 15;
+    float v = (float)(h & 0xffff) / 65536.f - 0.5f;
+    // lo planes (tiles 1 and 3 of each 64 KB stage) hold x - tf32(x)-sized values
+    const int tile = (i * 4 / 16384) & 3;
+    if (mode >= 7 && (tile == 1 || tile == 3)) v = v * 1.0e-4f;
+    if (mode >= 8) {  // full-precision fp32 values (low mantissa bits set)
+      v = v * 3.14159265f + 1.0e-7f * (float)(h >> 16);
+    }
+    reinterpret_cast<float*>(smem)[i] = v;
+  }
+  if (threadIdx.x == 0) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&bar)));
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&fin)));
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&done)));
+    for (int j = 0; j < 3; ++j) asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&emp[j])));
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (threadIdx.x < 32) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 256;" ::"r"(smem_u32(&tslot)));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  asm volatile("tcgen05.fence::before_thread_sync;");
+  __syncthreads();
+  if (threadIdx.x == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(&done)) : "memory");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;");
+  const uint32_t tm = tslot;
+  if (threadIdx.x == 0) {
+    long long t0 = clock64();
+    int n = 0;
+    for (int r = 0; r < reps; ++r) {
+      for (int s = 0; s < 3; ++s) {
+        const uint8_t* st = smem + s * 65536;
+        const uint64_t ah = desc_sw128(smem_u32(st)), al = desc_sw128(smem_u32(st + 16384));
+        const uint64_t bh = desc_sw128(smem_u32(st + 32768)), bl = desc_sw128(smem_u32(st + 49152));
+        if (mode >= 3) {
+          asm volatile("{\n.reg .pred P1;\nW2:\nmbarrier.try_wait.parity.shared::cta.b64 P1, [%0], 0;\n@!P1 bra W2;\n}"
+                       ::"r"(smem_u32(&done)) : "memory");
+          asm volatile("tcgen05.fence::after_thread_sync;");
+        }
+        for (int k = 0; k < 4; ++k) {
+          const uint64_t d = 2 * k;
+          if (mode == 10) {  // kernel-like: D alternates columns 0 / 128 per 2 stages, reset per chunk
+            const uint32_t td = tm + (uint32_t)(((r * 3 + s) / 2) & 1) * 128;
+            const uint32_t acc = (((r * 3 + s) % 2) != 0 || k > 0) ? 1u : 0u;
+            mma(td, ah + d, bh + d, idesc, acc);
+            mma(td, ah + d, bl + d, idesc, 1);
+            mma(td, al + d, bh + d, idesc, 1);
+          } else if (mode == 0 || mode >= 3) {
+            mma(tm, ah + d, bh + d, idesc, n++);
+            mma(tm, ah + d, bl + d, idesc, 1);
+            mma(tm, al + d, bh + d, idesc, 1);
+          } else if (mode == 1) {  // same operands every time
+            mma(tm, ah, bh, idesc, n++);
+            mma(tm, ah, bh, idesc, 1);
+            mma(tm, ah, bh, idesc, 1);
+          } else {  // k-step offsets only
+            mma(tm, ah + d, bh + d, idesc, n++);
+            mma(tm, ah + d, bh + d, idesc, 1);
+            mma(tm, ah + d, bh + d, idesc, 1);
+          }
+        }
+        if (mode >= 4)
+          asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];"
+                       ::"r"(smem_u32(&emp[s])) : "memory");
+      }
+    }
+    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];"
+                 ::"r"(smem_u32(&bar)) : "memory");
+    asm volatile("{\n.reg .pred P1;\nW:\nmbarrier.try_wait.parity.shared::cta.b64 P1, [%0], 0;\n@!P1 bra W;\n}"
+                 ::"r"(smem_u32(&bar)) : "memory");
+    if (blockIdx.x == 0) out[0] = clock64() - t0;
+    if (mode == 5 || mode == 6) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(&fin)) : "memory");
+  } else if (mode == 6) {
+    // other warps: proxy fences + shared stores in a loop until the MMAs finish
+    uint32_t ok = 0;
+    float* q = reinterpret_cast<float*>(smem + 196608 - 4096);
+    int it = 0;
+    while (!ok) {
+      q[threadIdx.x] = (float)it++;
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      asm volatile("{\n.reg .pred P1;\nmbarrier.test_wait.parity.shared::cta.b64 P1, [%1], 0;\nselp.u32 %0, 1, 0, P1;\n}"
+                   : "=r"(ok) : "r"(smem_u32(&fin)) : "memory");
+    }
+  } else if (mode == 5) {
+    // other warps wait on a barrier that completes only at the end (spinning try_wait)
+    asm volatile("{\n.reg .pred P1;\nW3:\nmbarrier.try_wait.parity.shared::cta.b64 P1, [%0], 0;\n@!P1 bra W3;\n}"
+                 ::"r"(smem_u32(&fin)) : "memory");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;");
+  __syncthreads();
+  if (threadIdx.x < 32)
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 256;" ::"r"(tm));
+}
+
+int main(int argc, char** argv) {
+  long long* d;
+  cudaMalloc(&d, 8);
+  const int reps = argc > 1 ? atoi(argv[1]) : 100;
+  const uint32_t idesc = (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(128 >> 3) << 17) | ((uint32_t)(128 >> 4) << 24);
+  cudaFuncSetAttribute(bench, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+  for (int mode : {4, 10}) {
+    for (int grid : {1, 148}) {
+     if (mode == 9) {
+      // back-to-back launches with programmatic dependent launch (as the GEMMs run)
+      cudaFuncSetAttribute(bench, cudaFuncAttributeMaxDynamicSharedMemorySize, 230 * 1024);
+      cudaLaunchConfig_t cfg = {};
+      cfg.gridDim = dim3(grid); cfg.blockDim = dim3(320); cfg.dynamicSmemBytes = 230 * 1024;
+      cudaLaunchAttribute at[1];
+      at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+      at[0].val.programmaticStreamSerializationAllowed = 1;
+      cfg.attrs = at; cfg.numAttrs = 1;
+      for (int r = 0; r < 4; ++r) cudaLaunchKernelEx(&cfg, bench, mode, idesc, reps, d);
+      cudaError_t e = cudaDeviceSynchronize();
+      long long cyc = 0;
+      cudaMemcpy(&cyc, d, 8, cudaMemcpyDeviceToHost);
+      printf("mode %d (PDL, 320 thr, 230 KB) grid %3d: %6.1f cycles/MMA (%s)\n", mode, grid, (double)cyc / (reps * 36), cudaGetErrorString(e));
+      continue;
+     }
+      bench<<<grid, (mode == 5 || mode == 6) ? 320 : 128, 200 * 1024>>>(mode, idesc, reps, d);
+      bench<<<grid, (mode == 5 || mode == 6) ? 320 : 128, 200 * 1024>>>(mode, idesc, reps, d);
+      cudaError_t e = cudaDeviceSynchronize();
+      long long cyc = 0;
+      cudaMemcpy(&cyc, d, 8, cudaMemcpyDeviceToHost);
+      printf("mode %d grid %3d: %6.1f cycles/MMA (%s)\n", mode, grid, (double)cyc / (reps * 36), cudaGetErrorString(e));
+    }
+  }
+  return 0;
+}

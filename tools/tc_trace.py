@@ -1,7 +1,12 @@
 """Phase timing of one tcgen05 GEMM launch (CTA 0), from globaltimer stamps.
 
-    PFB_TC_TRACE=1 python tools/tc_trace.py --force 4 --shape M N K [B]
-"""
+    PFB_TC_TRACE=1 python tools/tc_trace.py --force 4 --shape M N K [--planes] [--graph N]
+
+--planes: B pre-split once (pfb_matmul_ep2, as the executor does for
+constant weights).  --graph N: the traced launch is the last of N launches
+replayed back to back in a CUDA graph (steady state, programmatic dependent
+launch), instead of one launch after an idle gap.  Per k-block (first 16 of
+CTA 0): TMA issue, stage landed (split warps), split done, MMA issue."""
 import argparse
 import ctypes
 import pathlib
@@ -24,6 +29,8 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--force", type=int, default=4)
     ap.add_argument("--shape", type=int, nargs="+", required=True)
+    ap.add_argument("--planes", action="store_true")
+    ap.add_argument("--graph", type=int, default=0)
     args = ap.parse_args()
     m, n, k = args.shape[:3]
     lib = N.lib()
@@ -37,20 +44,53 @@ def main():
     B = Bt.view([k, n], [1, k])
     C = DArray(c.reshape(-1), 0, c.shape, c.stride(), DType.F64)
     s = torch.cuda.current_stream().cuda_stream
-    need = lib.pfb_matmul_workspace(A.desc(), B.desc(), C.desc())
+    ad, bd, cd = A.desc(), B.desc(), C.desc()
+    need = lib.pfb_matmul_workspace(ad, bd, cd)
     ws = torch.empty(max(need, 256), dtype=torch.uint8, device=dev)
-    buf = (ctypes.c_ulonglong * 16)()
-    for rep in range(4):
+    planes = None
+    if args.planes:
+        pb = torch.empty(lib.pfb_gemm_planes_bytes(bd), dtype=torch.uint8, device=dev)
+        lib.pfb_gemm_split_planes(bd, pb.data_ptr(), s)
+        planes = pb.data_ptr()
+
+    def call(stream):
+        if planes is not None:
+            return lib.pfb_matmul_ep2(ad, bd, cd, None, None, 0, None, 0, planes, args.force,
+                                      ws.data_ptr(), ws.numel(), stream)
+        return lib.pfb_matmul_ex(ad, bd, cd, None, 0, args.force, ws.data_ptr(), ws.numel(), stream)
+
+    buf = (ctypes.c_ulonglong * 128)()
+    call(s)  # trace buffer allocated outside any capture
+    torch.cuda.synchronize()
+    for rep in range(3):
         torch.cuda.synchronize()
-        torch.cuda._sleep(1000000)
-        rc = lib.pfb_matmul_ex(A.desc(), B.desc(), C.desc(), None, 0, args.force, ws.data_ptr(),
-                               ws.numel(), s)
+        if args.graph:
+            g = torch.cuda.CUDAGraph()
+            cs = torch.cuda.Stream()
+            with torch.cuda.stream(cs):
+                with torch.cuda.graph(g, stream=cs):
+                    for _ in range(args.graph):
+                        rc = call(cs.cuda_stream)
+            g.replay()
+        else:
+            torch.cuda._sleep(1000000)
+            rc = call(s)
         torch.cuda.synchronize()
         lib.pfb_debug_tc_trace(buf)
         t0 = buf[0]
         names = PAIR_NAMES if args.force in (5, 6) else NAMES
         print(f"rep {rep} rc={rc}: " + "  ".join(
             f"{nm}={(buf[i] - t0) / 1e3:.2f}" for i, nm in enumerate(names) if buf[i] and buf[i] >= t0))
+        if args.force not in (5, 6):
+            cyc = [buf[96 + kb] for kb in range(16)]
+            print("   mma_start deltas (SM cycles):", [int(cyc[i + 1] - cyc[i]) for i in range(15) if cyc[i + 1]])
+            print("   kb  tma_issue  landed  split_done  mma_start")
+            for kb in range(16):
+                v = [buf[16 * j + kb] for j in (1, 2, 3, 4)]
+                if not v[0] or v[0] < t0:
+                    break
+                print("   %2d  " % kb + "  ".join("%8.2f" % ((x - t0) / 1e3) if x >= t0 else "   -    "
+                                                 for x in v))
 
 
 if __name__ == "__main__":
