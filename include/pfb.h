@@ -86,6 +86,18 @@ int pfb_fused_ew(int32_t n_in, const pfb_tensor* ins, int32_t n_steps, const int
 int pfb_fused_ew_multi(int32_t n_in, const pfb_tensor* ins, int32_t n_steps,
                        const int32_t* program, int32_t n_out, const int32_t* out_regs,
                        pfb_tensor* outs, void* stream);
+/* pfb_fused_ew_multi whose inputs may be split-K partial sums (pass F15):
+ * parts[2k] = S_k, parts[2k+1] = st_k -- input k is the sum of S_k copies at
+ * element offsets j*st_k (j = 0..S_k-1), summed left to right as loaded;
+ * S_k <= 1 = a plain input.  The partials are those of pfb_matmul_parts.
+ * Specialised kernels only: PFB_E_UNSUPPORTED without NVRTC (the caller then
+ * reduces the partials itself). */
+int pfb_fused_ew_parts(int32_t n_in, const pfb_tensor* ins, const int64_t* parts,
+                       int32_t n_steps, const int32_t* program, int32_t n_out,
+                       const int32_t* out_regs, pfb_tensor* outs, void* stream);
+/* 1 when pfb_fused_ew_parts can run in this process now (NVRTC found, the
+ * specialiser enabled) */
+int pfb_fused_parts_ok(void);
 
 /* fused programs over >= min_elems elements run as kernels specialised to the
  * program (NVRTC, sm_100a; csrc/fused_jit.cu), bit-identical to the
@@ -210,6 +222,19 @@ int pfb_matmul_ep2(const pfb_tensor* a, const pfb_tensor* b, pfb_tensor* out,
                    const pfb_tensor* kscale, const pfb_tensor* bias, int32_t act,
                    const pfb_tensor* dy, int32_t dop, const void* b_planes, int32_t force_path,
                    void* ws, int64_t ws_bytes, void* stream);
+/* Split-K partials GEMM (pass F15; the reference's tensor.matmul,
+ * tensor.py:195-206, for a skinny-M 2-D product whose consumers are fused
+ * elementwise groups -- the LSTM's per-step GEMMs): parts[s] = A[:, K_s] @
+ * B[K_s, :] (+ bias in s = 0), s < S, no reduction; the consumer sums the
+ * partials (pfb_fused_ew_parts).  pfb_matmul_parts_count: S for this shape
+ * (< 2: use pfb_matmul_ep2); parts is [S, M, N] with unit column stride;
+ * b_planes as for pfb_matmul_ep2 (nullable: B is split into the workspace,
+ * pfb_matmul_parts_workspace bytes). */
+int pfb_matmul_parts_count(const pfb_tensor* a, const pfb_tensor* b, const pfb_tensor* out);
+int64_t pfb_matmul_parts_workspace(const pfb_tensor* a, const pfb_tensor* b, const pfb_tensor* out);
+int pfb_matmul_parts(const pfb_tensor* a, const pfb_tensor* b, pfb_tensor* parts,
+                     const pfb_tensor* bias, const void* b_planes, void* ws, int64_t ws_bytes,
+                     void* stream);
 int pfb_matmul_dual2(const pfb_tensor* a1, const pfb_tensor* b1, const pfb_tensor* a2,
                      const pfb_tensor* b2, pfb_tensor* out, const pfb_tensor* bias, int32_t act,
                      const void* b1_planes, const void* b2_planes, int32_t force_path, void* ws,

@@ -46,6 +46,9 @@ _SIGNATURES = {
     "pfb_fused_ew": ([_i32, _P, _i32, ctypes.POINTER(_i32), _P, _vp], ctypes.c_int),
     "pfb_fused_ew_multi": ([_i32, _P, _i32, ctypes.POINTER(_i32), _i32, ctypes.POINTER(_i32), _P,
                             _vp], ctypes.c_int),
+    "pfb_fused_ew_parts": ([_i32, _P, ctypes.POINTER(ctypes.c_int64), _i32, ctypes.POINTER(_i32),
+                            _i32, ctypes.POINTER(_i32), _P, _vp], ctypes.c_int),
+    "pfb_fused_parts_ok": ([], ctypes.c_int),
     "pfb_fused_jit_config": ([_i32, ctypes.c_int64], ctypes.c_int),
     "pfb_kernel_launches": ([], ctypes.c_int64),
     "pfb_fused_jit_check": ([_i32, _i32, ctypes.c_uint64, _i32, ctypes.POINTER(_i32), _i32, ctypes.POINTER(_i32),
@@ -69,6 +72,9 @@ _SIGNATURES = {
     "pfb_gemm_split_planes": ([_P, _vp, _vp], ctypes.c_int),
     "pfb_matmul_ep2": ([_P, _P, _P, _P, _P, _i32, _P, _i32, _vp, _i32, _vp, _i64, _vp],
                        ctypes.c_int),
+    "pfb_matmul_parts_count": ([_P, _P, _P], ctypes.c_int),
+    "pfb_matmul_parts_workspace": ([_P, _P, _P], ctypes.c_int64),
+    "pfb_matmul_parts": ([_P, _P, _P, _P, _vp, _vp, _i64, _vp], ctypes.c_int),
     "pfb_matmul_dual2": ([_P, _P, _P, _P, _P, _P, _i32, _vp, _vp, _i32, _vp, _i64, _vp],
                          ctypes.c_int),
     "pfb_matmul_dual": ([_P, _P, _P, _P, _P, _P, _i32, _i32, _vp, _i64, _vp], ctypes.c_int),

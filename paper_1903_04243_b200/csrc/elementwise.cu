@@ -783,8 +783,17 @@ extern "C" int pfb_fill(pfb_tensor* out, double value, void* stream) {
 
 static int fused_impl(int32_t n_in, const pfb_tensor* ins, int32_t n_steps,
                       const int32_t* program, int32_t n_out, const int32_t* out_regs,
-                      pfb_tensor* outs, void* stream) {
+                      pfb_tensor* outs, void* stream, const int64_t* parts = nullptr) {
   if (n_in < 1 || n_in > kMaxIn || n_steps < 1 || n_steps > kMaxSteps) return PFB_E_ARG;
+  PartsSpec PS{};
+  if (parts) {
+    for (int k = 0; k < n_in; ++k) {
+      PS.S[k] = (int)parts[2 * k];
+      PS.st[k] = parts[2 * k + 1];
+      if (PS.S[k] > kMaxParts || (PS.S[k] > 1 && ins[k].dtype != PFB_F32)) return PFB_E_ARG;
+    }
+    if (!PS.any()) parts = nullptr;
+  }
   if (n_out < 1 || n_out > kMaxOuts) return PFB_E_ARG;
   const pfb_tensor* out = &outs[0];
   for (int k = 0; k < n_out; ++k) {
@@ -843,13 +852,16 @@ static int fused_impl(int32_t n_in, const pfb_tensor* ins, int32_t n_steps,
     } else {
       const int64_t esz = ins[o - 1].dtype == PFB_F32 ? 4 : 1;
       vec = vec && (reinterpret_cast<uintptr_t>(ins[o - 1].data) % (4 * esz)) == 0;
+      if (parts && PS.S[o - 1] > 1) vec = vec && PS.st[o - 1] % 4 == 0;
     }
     for (int d = 0; d < ir && vec; ++d) vec = (L.st[o][d] % 4) == 0;
     const FeedModes m = (L.st[o][ir] == 0 && o > 0) ? 1u : (vec ? 0u : 2u);
     modes |= m << (2 * o);
   }
   const int64_t ng = v4 ? n / 4 : n;
-  if (fused_jit_launch(P, v4 ? 4 : 1, !small, modes, L, ng, fo, fi, s)) return launch_status();
+  if (fused_jit_launch(P, v4 ? 4 : 1, !small, modes, L, ng, fo, fi, s, parts ? &PS : nullptr))
+    return launch_status();
+  if (parts) return PFB_E_UNSUPPORTED;  // partial sums: specialised kernels only
   if (v4) {
     if (small) launch_fused<4, uint32_t>(n_in, L, (uint32_t)ng, P, modes, fo, fi, s);
     else launch_fused<4, int64_t>(n_in, L, ng, P, modes, fo, fi, s);
@@ -871,6 +883,12 @@ extern "C" int pfb_fused_ew_multi(int32_t n_in, const pfb_tensor* ins, int32_t n
                                   const int32_t* program, int32_t n_out, const int32_t* out_regs,
                                   pfb_tensor* outs, void* stream) {
   return fused_impl(n_in, ins, n_steps, program, n_out, out_regs, outs, stream);
+}
+
+extern "C" int pfb_fused_ew_parts(int32_t n_in, const pfb_tensor* ins, const int64_t* parts,
+                                  int32_t n_steps, const int32_t* program, int32_t n_out,
+                                  const int32_t* out_regs, pfb_tensor* outs, void* stream) {
+  return fused_impl(n_in, ins, n_steps, program, n_out, out_regs, outs, stream, parts);
 }
 
 // ---------------------------------------------------------------------------

@@ -33,13 +33,27 @@ struct FusedIns {
 // vector, 1 = stride-0 broadcast, 2 = strided scalar
 using FeedModes = uint64_t;
 
+// Split-K partial-sum inputs (pass F15): input k is the sum of S[k] copies
+// at element offsets j * st[k] (j = 0..S[k]-1, summed left to right as
+// loaded); S[k] <= 1 = a plain input.  Only the specialised kernels take them.
+constexpr int kMaxParts = 32;
+struct PartsSpec {
+  int S[kMaxIn];
+  int64_t st[kMaxIn];
+  bool any() const {
+    for (int k = 0; k < kMaxIn; ++k)
+      if (S[k] > 1) return true;
+    return false;
+  }
+};
+
 // Launch `P` as a kernel specialised to it (straight-line code, registers
 // in registers); false when the specialiser is unavailable or declines
 // (the caller then runs the interpreter kernel).  V, modes, ngroups, idx64
 // as for the interpreter launch.
 bool fused_jit_launch(const FusedProgram& P, int V, bool idx64, FeedModes modes, const FLayout& L,
                       int64_t ngroups, const FusedOuts& outs, const FusedIns& ins,
-                      cudaStream_t s);
+                      cudaStream_t s, const PartsSpec* parts = nullptr);
 
 // the same for an integer-domain program (fused_int_kernel), one element per
 // thread

@@ -119,12 +119,20 @@ std::string fmt(const char* f, ...) {
   return buf;
 }
 
-std::string gen_source(const FusedProgram& P, int V, bool idx64, FeedModes modes) {
+std::string gen_source(const FusedProgram& P, int V, bool idx64, FeedModes modes,
+                       const PartsSpec* PS = nullptr) {
   std::string s = fmt(kPrelude, kMaxRank, kMaxFOps, kMaxRank, kMaxOuts, kMaxIn);
   const char* IT = idx64 ? "i64" : "unsigned";
   const int nops = P.n_in + 1;
-  s += fmt("extern \"C\" __global__ void __launch_bounds__(256) pfb_fused_jit(Layout L, %s ngroups, "
-           "Outs outs, Ins ins) {\n", IT);
+  auto nparts = [&](int k) { return (PS && PS->S[k] > 1) ? PS->S[k] : 1; };
+  if (PS) {
+    s += fmt("struct Parts { i64 st[%d]; };\n", kMaxIn);
+    s += fmt("extern \"C\" __global__ void __launch_bounds__(256) pfb_fused_jit(Layout L, %s ngroups, "
+             "Outs outs, Ins ins, Parts PT) {\n", IT);
+  } else {
+    s += fmt("extern \"C\" __global__ void __launch_bounds__(256) pfb_fused_jit(Layout L, %s ngroups, "
+             "Outs outs, Ins ins) {\n", IT);
+  }
   s += "  asm volatile(\"griddepcontrol.wait;\" ::: \"memory\");\n"
        "  asm volatile(\"griddepcontrol.launch_dependents;\" :::);\n"
        "  const int ir = L.rank - 1;\n";
@@ -145,7 +153,33 @@ std::string gen_source(const FusedProgram& P, int V, bool idx64, FeedModes modes
     const bool bl = P.in_dtype[k] == PFB_BOOL;
     const char* T = bl ? "unsigned char" : "float";
     s += fmt("    const %s* p%d = reinterpret_cast<const %s*>(ins.p[%d]) + off[%d];\n", T, k, T, k, k + 1);
-    if (V == 4 && md == 0) {
+    const int np = bl ? 1 : nparts(k);
+    if (np > 1) {
+      // split-K partials: every part loaded first, then summed in split order
+      const char* f[4] = {"x", "y", "z", "w"};
+      if (V == 4 && md == 0) {
+        for (int q = 0; q < np; ++q)
+          s += fmt("    const float4 w%d_%d = __ldg(reinterpret_cast<const float4*>(p%d + %d * PT.st[%d]));\n",
+                   k, q, k, q, k);
+        for (int j = 0; j < 4; ++j) {
+          std::string e = fmt("w%d_0.%s", k, f[j]);
+          for (int q = 1; q < np; ++q) e = "(" + e + fmt(" + w%d_%d.%s)", k, q, f[j]);
+          s += fmt("    const float in%d_%d = ", k, j) + e + ";\n";
+        }
+      } else {
+        if (md != 1) s += fmt("    const i64 sin%d = L.st[%d][ir];\n", k, k + 1);
+        const int nv = md == 1 ? 1 : V;
+        for (int j = 0; j < nv; ++j) {
+          for (int q = 0; q < np; ++q)
+            s += fmt("    const float r%d_%d_%d = __ldg(p%d + %d * PT.st[%d]%s);\n", k, j, q, k, q, k,
+                     md == 1 ? "" : fmt(" + %d * sin%d", j, k).c_str());
+          std::string e = fmt("r%d_%d_0", k, j);
+          for (int q = 1; q < np; ++q) e = "(" + e + fmt(" + r%d_%d_%d)", k, j, q);
+          s += fmt("    const float in%d_%d = ", k, j) + e + ";\n";
+        }
+        for (int j = nv; j < V; ++j) s += fmt("    const float in%d_%d = in%d_0;\n", k, j, k);
+      }
+    } else if (V == 4 && md == 0) {
       if (bl)
         s += fmt("    const uchar4 w%d = __ldg(reinterpret_cast<const uchar4*>(p%d));\n", k, k);
       else
@@ -363,11 +397,12 @@ void jit_init() {
 namespace {
 
 // kernel for a program (integer: the i64 domain), compiled on first use
-CUfunction lookup(const FusedProgram& P, int V, bool idx64, FeedModes modes, bool integer) {
+CUfunction lookup(const FusedProgram& P, int V, bool idx64, FeedModes modes, bool integer,
+                  const PartsSpec* PS = nullptr) {
   int dev = 0;
   cudaGetDevice(&dev);
   // cache key: the program's encoding and everything baked into the source
-  int32_t kb[10 + kMaxIn + 4 * kMaxSteps + 2 * kMaxOuts];
+  int32_t kb[11 + 2 * kMaxIn + 4 * kMaxSteps + 2 * kMaxOuts];
   int nk = 0;
   kb[nk++] = dev; kb[nk++] = V; kb[nk++] = idx64; kb[nk++] = (int32_t)(modes & 0xffffffffu);
   kb[nk++] = (int32_t)(modes >> 32); kb[nk++] = integer;
@@ -376,6 +411,9 @@ CUfunction lookup(const FusedProgram& P, int V, bool idx64, FeedModes modes, boo
   for (int t = 0; t < P.n_steps; ++t)
     for (int j = 0; j < 4; ++j) kb[nk++] = P.code[t][j];
   for (int k = 0; k < P.n_out; ++k) { kb[nk++] = P.out_reg[k]; kb[nk++] = P.out_dt[k]; }
+  kb[nk++] = PS != nullptr;
+  if (PS)
+    for (int k = 0; k < P.n_in; ++k) kb[nk++] = PS->S[k];
   const std::string key(reinterpret_cast<const char*>(kb), nk * sizeof(int32_t));
   static std::mutex mu;
   static std::unordered_map<std::string, CUfunction> cache;
@@ -383,12 +421,12 @@ CUfunction lookup(const FusedProgram& P, int V, bool idx64, FeedModes modes, boo
   auto it = cache.find(key);
   if (it == cache.end())
     it = cache.emplace(key, compile(integer ? gen_source_int(P, idx64)
-                                            : gen_source(P, V, idx64, modes))).first;
+                                            : gen_source(P, V, idx64, modes, PS))).first;
   return it->second;
 }
 
 bool run(CUfunction fn, bool idx64, const FLayout& L, int64_t nitems, const FusedOuts& outs,
-         const FusedIns& ins, cudaStream_t s) {
+         const FusedIns& ins, cudaStream_t s, const PartsSpec* PS = nullptr) {
   CUlaunchConfig cfg = {};
   cfg.gridDimX = grid_for(nitems, 256); cfg.gridDimY = 1; cfg.gridDimZ = 1;
   cfg.blockDimX = 256; cfg.blockDimY = 1; cfg.blockDimZ = 1;
@@ -403,7 +441,10 @@ bool run(CUfunction fn, bool idx64, const FLayout& L, int64_t nitems, const Fuse
   FusedIns ic = ins;
   uint32_t n32 = (uint32_t)nitems;
   int64_t n64 = nitems;
-  void* args[4] = {&Lc, idx64 ? (void*)&n64 : (void*)&n32, &oc, &ic};
+  struct { int64_t st[kMaxIn]; } pt;
+  if (PS)
+    for (int k = 0; k < kMaxIn; ++k) pt.st[k] = PS->st[k];
+  void* args[5] = {&Lc, idx64 ? (void*)&n64 : (void*)&n32, &oc, &ic, &pt};
   kernel_launches()++;
   return driver().launch(&cfg, fn, args, nullptr) == CUDA_SUCCESS;
 }
@@ -417,10 +458,11 @@ bool usable(int64_t elems) {
 
 bool fused_jit_launch(const FusedProgram& P, int V, bool idx64, FeedModes modes, const FLayout& L,
                       int64_t ngroups, const FusedOuts& outs, const FusedIns& ins,
-                      cudaStream_t s) {
-  if (!usable(ngroups * V)) return false;
-  CUfunction fn = lookup(P, V, idx64, modes, false);
-  return fn && run(fn, idx64, L, ngroups, outs, ins, s);
+                      cudaStream_t s, const PartsSpec* parts) {
+  if (parts && !parts->any()) parts = nullptr;
+  if (!usable(parts ? INT64_MAX : ngroups * V)) return false;
+  CUfunction fn = lookup(P, V, idx64, modes, false, parts);
+  return fn && run(fn, idx64, L, ngroups, outs, ins, s, parts);
 }
 
 bool fused_int_jit_launch(const FusedProgram& P, bool idx64, const FLayout& L, int64_t n,
@@ -441,6 +483,10 @@ extern "C" int pfb_fused_jit_config(int32_t enable, int64_t min_elems) {
   if (min_elems >= 0) pfb::g_jit_min = min_elems;
   return pfb::nvrtc().ok && pfb::driver().ok;
 }
+
+// Can fused groups take split-K partial-sum inputs (pfb_fused_ew_parts) in
+// this process right now (specialiser available and enabled)?
+extern "C" int pfb_fused_parts_ok(void) { return pfb::usable(INT64_MAX) ? 1 : 0; }
 
 // Host-only check (no device needed): generate the specialised source for a
 // program and compile it with NVRTC for sm_100a.  0 = compiled, 1 = compile

@@ -483,3 +483,58 @@ extern "C" int pfb_matmul_dual2(const pfb_tensor* a1, const pfb_tensor* b1, cons
   if (e == PFB_E_UNSUPPORTED && path != 1) return dual_path(g1, g2, 1, out, ws, ws_bytes, s);
   return e;
 }
+
+// ---------------------------------------------------------------------------
+// Split-K partials (executor pass F15, gemm_parts.cu): for a skinny GEMM whose
+// only consumers are fused elementwise groups, the k-splits write their
+// partial tiles to parts[s] and the consumer sums them as it loads (split
+// order, left to right), so the GEMM has no reduction phase.
+
+static int parts_args(const pfb_tensor* a, const pfb_tensor* b, const pfb_tensor* out,
+                      const void* b_planes, GemmArgs* g) {
+  if (a->rank != 2 || b->rank != 2) return PFB_E_RANK;
+  if (int e = matmul_args(a, b, const_cast<pfb_tensor*>(out), g)) return e;
+  if (b_planes != nullptr) {
+    g->b_hi = static_cast<const float*>(b_planes);
+    g->b_lo = planes_lo(*g, b_planes);
+  }
+  return 0;
+}
+
+extern "C" int pfb_matmul_parts_count(const pfb_tensor* a, const pfb_tensor* b,
+                                          const pfb_tensor* out) {
+  static const bool off = getenv_flag("PFB_NO_PARTS");
+  GemmArgs g;
+  if (off || parts_args(a, b, out, nullptr, &g)) return 0;
+  return gemm_parts_count(g);
+}
+
+extern "C" int64_t pfb_matmul_parts_workspace(const pfb_tensor* a, const pfb_tensor* b,
+                                              const pfb_tensor* out) {
+  GemmArgs g;
+  if (parts_args(a, b, out, nullptr, &g)) return 0;
+  return gemm_parts_workspace(g);
+}
+
+extern "C" int pfb_matmul_parts(const pfb_tensor* a, const pfb_tensor* b, pfb_tensor* parts,
+                                const pfb_tensor* bias, const void* b_planes, void* ws,
+                                int64_t ws_bytes, void* stream) {
+  if (parts->rank != 3 || parts->dtype != PFB_F32 || parts->stride[2] != 1) return PFB_E_SHAPE;
+  pfb_tensor out = *parts;
+  out.rank = 2;
+  out.shape[0] = parts->shape[1]; out.shape[1] = parts->shape[2];
+  out.stride[0] = parts->stride[1]; out.stride[1] = parts->stride[2];
+  GemmArgs g;
+  if (int e = parts_args(a, b, &out, b_planes, &g)) return e;
+  if (bias) {
+    if (bias->dtype != PFB_F32) return PFB_E_DTYPE;
+    int64_t st[2];
+    if (!broadcast_strides(bias, 2, out.shape, st)) return PFB_E_SHAPE;
+    g.bias = (const float*)bias->data;
+    g.sxb = 0; g.sxm = st[0]; g.sxn = st[1];
+  }
+  const int S = gemm_parts_count(g);
+  if (S < 1 || parts->shape[0] != S) return PFB_E_SHAPE;
+  return gemm_parts(g, S, (float*)parts->data, parts->stride[0], parts->stride[1], ws, ws_bytes,
+                    as_stream(stream));
+}

@@ -1,0 +1,324 @@
+// Split-K partials GEMM for skinny-M problems (pass F15, pfb_matmul_parts):
+//
+//   parts[s] = A[:, Ks] @ B[Ks, :]  (+ bias in s = 0)     s = 0..S-1
+//
+// One CTA per (128-row tile, BN-column tile, k-split).  Each split's whole K
+// range (<= 8 k-blocks of 32) accumulates in TMEM -- no chunked register
+// accumulation, no reduction: the consumer (a fused elementwise group) sums
+// the S partials as it loads them.  This is the shape of the LSTM's per-step
+// GEMMs (M = 256 examples, 128 of them per step, reference bench cell /
+// BASELINE cfg4), where the reduced GEMM spent ~30% of its time in the
+// cluster reduction (barriers waiting on the slowest CTA of the cluster, then
+// DSMEM round trips).  BN = 128 by default: BN = 256 (every tcgen05.mma a
+// 128x256x8 instruction, full TF32 issue rate -- 128-wide MMAs cost ~60
+// cycles each regardless of N, tools/experiments/mma_rate.cu) doubles the
+// partials the consumer must read and measured slower on the cfg4 step
+// (3.24 vs 2.69 ms, tools/experiments/parts_knobs.sh; PFB_PARTS_BN).
+//
+// 3xTF32 as in gemm_tcgen05.cu: A raw (the tensor core truncates it: hi =
+// trunc(x); lo = rn(x - hi) written beside it in smem by the split warps),
+// B as pre-split RN hi/lo planes; products A_hi B_hi + A_hi B_lo + A_lo B_hi.
+// TMEM accumulation over <= 256 of K stays at fp32-SIMT accuracy
+// (tests/test_gpu_parts.py).
+//
+// Warps: 0 TMA producer, 1 TMEM allocator + MMA issuer, 2..9 split A tiles,
+// then drain TMEM (warp w: lanes 32*(w%4).., columns half (w-2)/4) through a
+// swizzled smem block and TMA-store 32x32 blocks of parts[s].
+#include <cuda.h>
+#include <cudaTypedefs.h>
+
+#include <algorithm>
+
+#include "fused.cuh"
+#include "gemm.cuh"
+#include "tc_ptx.cuh"
+
+namespace pfb {
+namespace tcs {
+
+using namespace tc;
+
+constexpr int BM = 128, BK = 32, UMMA_K = 8;
+constexpr int A_BYTES = BM * BK * 4;  // 16 KB raw A tile (lo beside it)
+constexpr int WARPS = 10, NUM_THREADS = 32 * WARPS, SPLIT_WARPS = 8;
+constexpr int kMaxKb = 8;             // k-blocks per split (K <= 256 in TMEM)
+
+template <int BN>
+struct Cfg {
+  static constexpr int B_BYTES = BN * BK * 4;
+  static constexpr int STAGE = 2 * A_BYTES + 2 * B_BYTES;
+  static constexpr int STAGES = BN == 256 ? 2 : 3;
+  static constexpr int SMEM = STAGES * STAGE + 1024 + 256;
+  static constexpr uint32_t IDESC = (1u << 4) | (2u << 7) | (2u << 10) |
+                                    ((uint32_t)(BN >> 3) << 17) | ((uint32_t)(BM >> 4) << 24);
+  static_assert(SMEM <= 232448, "shared memory");
+  static_assert(SPLIT_WARPS * 4096 <= STAGES * STAGE, "epilogue staging reuses the stages");
+};
+
+struct Params {
+  int M, N, nk, kb_per, ntn, S;
+  const float* bias;  // split 0 only; broadcast strides
+  int64_t sxm, sxn;
+};
+
+template <int BN>
+__global__ void __launch_bounds__(NUM_THREADS, 1)
+parts_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ CUtensorMap map_bh,
+             const __grid_constant__ CUtensorMap map_bl, const __grid_constant__ CUtensorMap map_c,
+             Params p) {
+  using C = Cfg<BN>;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>(
+      (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + C::STAGES * C::STAGE);
+  uint64_t* full = bars;                  // TMA -> split warps
+  uint64_t* ready = bars + C::STAGES;     // split -> MMA
+  uint64_t* empty = bars + 2 * C::STAGES; // MMA -> TMA
+  uint64_t* acc_full = bars + 3 * C::STAGES;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_full + 1);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int u = blockIdx.x;
+  const int s_idx = u % p.S, t = u / p.S;
+  const int m0 = (t / p.ntn) * BM, n0 = (t % p.ntn) * BN;
+  const int kb0 = s_idx * p.kb_per, kb1 = min(p.nk, kb0 + p.kb_per);
+  const int nkb = kb1 - kb0;
+  auto stage = [&](int s) { return smem + s * C::STAGE; };
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < C::STAGES; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&ready[s], SPLIT_WARPS);
+      mbar_init(&empty[s], 1);
+    }
+    mbar_init(acc_full, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&map_a)) : "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&map_bh)) : "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&map_bl)) : "memory");
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                     smem_u32(tmem_slot)), "r"(BN));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;");
+  const uint32_t tmem = *tmem_slot;
+  pdl_enter();
+
+  if (warp == 0) {
+    if (lane == 0) {
+      for (int g = 0; g < nkb; ++g) {
+        const int s = g % C::STAGES, kb = kb0 + g;
+        if (g >= C::STAGES) mbar_wait(&empty[s], ((g / C::STAGES) - 1) & 1);
+        mbar_expect_tx(&full[s], A_BYTES + 2 * C::B_BYTES);
+        tma_load_3d(&map_a, &full[s], stage(s), kb * BK, m0, 0);
+        tma_load_3d(&map_bh, &full[s], stage(s) + 2 * A_BYTES, kb * BK, n0, 0);
+        tma_load_3d(&map_bl, &full[s], stage(s) + 2 * A_BYTES + C::B_BYTES, kb * BK, n0, 0);
+      }
+    }
+  } else if (warp == 1) {
+    for (int g = 0; g < nkb; ++g) {
+      const int s = g % C::STAGES;
+      mbar_wait(&ready[s], (g / C::STAGES) & 1);
+      asm volatile("tcgen05.fence::after_thread_sync;");
+      const uint64_t ah = smem_desc_sw128(smem_u32(stage(s)));
+      const uint64_t al = smem_desc_sw128(smem_u32(stage(s) + A_BYTES));
+      const uint64_t bh = smem_desc_sw128(smem_u32(stage(s) + 2 * A_BYTES));
+      const uint64_t bl = smem_desc_sw128(smem_u32(stage(s) + 2 * A_BYTES + C::B_BYTES));
+      if (elect_one()) {
+#pragma unroll
+        for (int k = 0; k < BK / UMMA_K; ++k) {
+          const uint64_t d = (UMMA_K * 4) >> 4;  // +32 B inside the swizzle row
+          const uint32_t acc = (g > 0 || k > 0) ? 1u : 0u;
+          mma_tf32(tmem, ah + d * k, bh + d * k, C::IDESC, acc);
+          mma_tf32(tmem, ah + d * k, bl + d * k, C::IDESC, 1u);
+          mma_tf32(tmem, al + d * k, bh + d * k, C::IDESC, 1u);
+        }
+        mma_commit(&empty[s]);
+        if (g == nkb - 1) mma_commit(acc_full);
+      }
+      __syncwarp();
+    }
+  } else {
+    const int et = threadIdx.x - 64;  // 0..255
+    for (int g = 0; g < nkb; ++g) {
+      const int s = g % C::STAGES;
+      mbar_wait(&full[s], (g / C::STAGES) & 1);
+      split_tf32_smem(smem_u32(stage(s)), smem_u32(stage(s) + A_BYTES), A_BYTES / 16, et,
+                      32 * SPLIT_WARPS);
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&ready[s]);
+    }
+    // ---- epilogue: TMEM -> (+ bias) -> swizzled 32x32 block -> TMA store
+    const int quarter = warp & 3, half = (warp - 2) >> 2;
+    float* blk = reinterpret_cast<float*>(smem) + (warp - 2) * 1024;  // stage memory is idle
+    mbar_wait(acc_full, 0);
+    asm volatile("tcgen05.fence::after_thread_sync;");
+    const int row0 = m0 + quarter * 32;
+    const bool add_bias = p.bias != nullptr && s_idx == 0;
+#pragma unroll 1
+    for (int cc = 0; cc < BN / 2; cc += 32) {
+      const int col0 = n0 + half * (BN / 2) + cc;
+      uint32_t v[32];
+      tmem_ld32(tmem + ((uint32_t)(quarter * 32) << 16) + (uint32_t)(half * (BN / 2) + cc), v);
+      float bv = 0.f;  // bias of column col0 + lane (row-broadcast bias)
+      if (add_bias && p.sxm == 0 && col0 + lane < p.N) bv = __ldg(p.bias + (int64_t)(col0 + lane) * p.sxn);
+      asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+      if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+      __syncwarp();
+#pragma unroll
+      for (int q = 0; q < 8; ++q) {
+        float x[4];
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          x[j] = __uint_as_float(v[4 * q + j]);
+          if (add_bias) {
+            if (p.sxm == 0) {
+              x[j] += __shfl_sync(0xffffffffu, bv, 4 * q + j);
+            } else if (row0 + lane < p.M && col0 + 4 * q + j < p.N) {
+              x[j] += __ldg(p.bias + (int64_t)(row0 + lane) * p.sxm +
+                            (int64_t)(col0 + 4 * q + j) * p.sxn);
+            }
+          }
+        }
+        *reinterpret_cast<float4*>(blk + lane * 32 + 4 * (q ^ (lane & 7))) =
+            make_float4(x[0], x[1], x[2], x[3]);
+      }
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      __syncwarp();
+      if (lane == 0) {
+        tma_store_3d(&map_c, blk, col0, row0, s_idx);
+        asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+      }
+    }
+    if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;");
+  __syncthreads();
+  if (warp == 1) {
+    asm volatile("tcgen05.fence::after_thread_sync;");
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(BN));
+  }
+}
+
+// K-split count: enough (tile, split) units to cover the SMs, <= kMaxKb
+// k-blocks (TMEM accumulation depth) per split, >= 2 k-blocks each
+static int plan(int64_t M, int64_t N, int64_t K, int BN, int* kb_per) {
+  static const int smax = [] {  // PFB_PARTS_SMAX: cap on S (experiments)
+    const char* e = getenv("PFB_PARTS_SMAX");
+    return e ? std::max(1, atoi(e)) : kMaxParts;
+  }();
+  const int64_t tiles = ((M + BM - 1) / BM) * ((N + BN - 1) / BN);
+  const int64_t nk = ((K + 3) / 4 * 4 + BK - 1) / BK;
+  int64_t S = std::min<int64_t>(smax, std::max<int64_t>(1, 148 / tiles));
+  S = std::max<int64_t>(S, (nk + kMaxKb - 1) / kMaxKb);  // TMEM depth bound
+  S = std::min<int64_t>(S, std::max<int64_t>(1, nk / 2));
+  int64_t per = (nk + S - 1) / S;
+  S = (nk + per - 1) / per;
+  if (per > kMaxKb || S * tiles > 4 * 148) return 0;
+  *kb_per = (int)per;
+  return (int)S;
+}
+
+template <int BN>
+static int launch(const GemmArgs& g, const CUtensorMap& ma, const CUtensorMap& mbh,
+                  const CUtensorMap& mbl, const CUtensorMap& mc, int S, int kb_per,
+                  cudaStream_t s) {
+  using C = Cfg<BN>;
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(parts_kernel<BN>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
+    attr = true;
+  }
+  Params p;
+  p.M = (int)g.M; p.N = (int)g.N;
+  p.nk = (int)(((g.K + 3) / 4 * 4 + BK - 1) / BK);
+  p.kb_per = kb_per;
+  p.ntn = (int)((g.N + BN - 1) / BN);
+  p.S = S;
+  p.bias = g.bias; p.sxm = g.sxm; p.sxn = g.sxn;
+  const int units = (int)(((g.M + BM - 1) / BM) * p.ntn * S);
+  pfb::launch(parts_kernel<BN>, dim3(units), dim3(NUM_THREADS), C::SMEM, s, ma, mbh, mbl, mc, p);
+  return launch_status();
+}
+
+}  // namespace tcs
+
+static int parts_bn(const GemmArgs& g) {
+  static const int env = [] {
+    const char* e = getenv("PFB_PARTS_BN");
+    return e ? atoi(e) : 0;
+  }();
+  if (env == 128 || env == 256) return env;
+  return 128;
+}
+
+// S for pfb_matmul_parts (0: not applicable): batch 1, A K-major and
+// TMA-readable as is, B pre-split (planes) or splittable into the workspace
+int gemm_parts_count(const GemmArgs& g) {
+  using namespace tcs;
+  if (g.batch != 1 || g.M < 1 || g.N < 8 || g.K < 64 || g.kscale || g.accumulate || g.act ||
+      g.dop || g.alpha_rows)
+    return 0;
+  if (g.sak != 1 || (g.M > 1 && ((g.sam * 4) % 16 != 0 || g.sam < g.K)) ||
+      (reinterpret_cast<uintptr_t>(g.A) & 15) != 0)
+    return 0;
+  int per;
+  return plan(g.M, g.N, g.K, parts_bn(g), &per);
+}
+
+int64_t gemm_parts_workspace(const GemmArgs& g) {
+  if (g.b_hi) return 0;
+  const int64_t Kp = (g.K + 3) / 4 * 4;
+  return 2 * ((g.N * Kp * 4 + 255) / 256 * 256);
+}
+
+int gemm_parts(const GemmArgs& g, int S, float* parts, int64_t part_stride, int64_t ldc,
+               void* ws, int64_t ws_bytes, cudaStream_t s) {
+  using namespace tcs;
+  const int BN = parts_bn(g);
+  int kb_per = 0;
+  if (gemm_parts_count(g) != S || plan(g.M, g.N, g.K, BN, &kb_per) != S) return PFB_E_UNSUPPORTED;
+  if ((part_stride * 4) % 16 != 0 || (ldc * 4) % 16 != 0 || (reinterpret_cast<uintptr_t>(parts) & 15))
+    return PFB_E_UNSUPPORTED;
+  const int64_t Kp = (g.K + 3) / 4 * 4;
+  const float* bh = g.b_hi;
+  const float* bl = g.b_lo;
+  if (!bh) {
+    if (ws == nullptr || ws_bytes < gemm_parts_workspace(g)) return PFB_E_UNSUPPORTED;
+    float* h = static_cast<float*>(ws);
+    float* l = reinterpret_cast<float*>(static_cast<char*>(ws) + (g.N * Kp * 4 + 255) / 256 * 256);
+    tc_split_launch(g.B, 1, g.N, g.K, Kp, 0, g.sbn, g.sbk, h, l, nullptr, 0, 0, s);
+    bh = h;
+    bl = l;
+  }
+  CUtensorMap ma, mbh, mbl, mc;
+  {
+    const int64_t ld = g.M == 1 ? Kp : g.sam;
+    cuuint64_t dims[3] = {(cuuint64_t)g.K, (cuuint64_t)g.M, 1};
+    cuuint64_t strides[2] = {(cuuint64_t)(ld * 4), (cuuint64_t)(ld * g.M * 4)};
+    cuuint32_t box[3] = {BK, BM, 1};
+    if (!encode(&ma, g.A, dims, strides, box)) return PFB_E_UNSUPPORTED;
+  }
+  {
+    cuuint64_t dims[3] = {(cuuint64_t)Kp, (cuuint64_t)g.N, 1};
+    cuuint64_t strides[2] = {(cuuint64_t)(Kp * 4), (cuuint64_t)(g.N * Kp * 4)};
+    cuuint32_t box[3] = {BK, (cuuint32_t)BN, 1};
+    if (!encode(&mbh, bh, dims, strides, box) || !encode(&mbl, bl, dims, strides, box))
+      return PFB_E_UNSUPPORTED;
+  }
+  {
+    cuuint64_t dims[3] = {(cuuint64_t)g.N, (cuuint64_t)g.M, (cuuint64_t)S};
+    cuuint64_t strides[2] = {(cuuint64_t)(ldc * 4), (cuuint64_t)(part_stride * 4)};
+    cuuint32_t box[3] = {32, 32, 1};
+    if (!encode(&mc, parts, dims, strides, box)) return PFB_E_UNSUPPORTED;
+  }
+  return BN == 256 ? tcs::launch<256>(g, ma, mbh, mbl, mc, S, kb_per, s)
+                   : tcs::launch<128>(g, ma, mbh, mbl, mc, S, kb_per, s);
+}
+
+}  // namespace pfb

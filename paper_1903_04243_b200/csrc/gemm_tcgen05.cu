@@ -163,19 +163,49 @@ __device__ __forceinline__ void stamp(const Params& p, int i) {
   }
 }
 
-__device__ __forceinline__ void epi4(const Params& p, int bz, int row, int col, float4& v) {
-  if (p.bias == nullptr && p.act == 0 && p.dop == 0) return;
+__device__ __forceinline__ void epi4(const Params& p, int bz, int row, int col, float4& v,
+                                     const float* bias) {
+  if (bias == nullptr && p.act == 0 && p.dop == 0) return;
   float e[4] = {v.x, v.y, v.z, v.w};
 #pragma unroll
   for (int j = 0; j < 4; ++j) {
-    if (p.bias && col + j < p.N)
-      e[j] += __ldg(p.bias + (int64_t)bz * p.sxb + (int64_t)row * p.sxm + (int64_t)(col + j) * p.sxn);
+    if (bias && col + j < p.N)
+      e[j] += __ldg(bias + (int64_t)bz * p.sxb + (int64_t)row * p.sxm + (int64_t)(col + j) * p.sxn);
     e[j] = apply_act(p.act, e[j]);
     if (p.dop && col + j < p.N)
       e[j] *= dop_factor(p.dop, p.dy,
                          (int64_t)bz * p.sdb + (int64_t)row * p.sdm + (int64_t)(col + j) * p.sdn);
   }
   v = make_float4(e[0], e[1], e[2], e[3]);
+}
+
+// epilogue operands of 4 consecutive columns, loaded ahead of use (the
+// loads of a whole block are issued before the first is consumed: one
+// memory round trip per block instead of one per element)
+struct Epi4 {
+  float b[4], y[4];
+};
+
+__device__ __forceinline__ void epi4_load(const Params& p, const float* bias, int bz, int row,
+                                          int col, Epi4& e) {
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    const bool ok = col + j < p.N;
+    e.b[j] = (bias && ok) ? __ldg(bias + (int64_t)bz * p.sxb + (int64_t)row * p.sxm +
+                                  (int64_t)(col + j) * p.sxn) : 0.f;
+    e.y[j] = (p.dop && ok) ? __ldg(p.dy + (int64_t)bz * p.sdb + (int64_t)row * p.sdm +
+                                   (int64_t)(col + j) * p.sdn) : 0.f;
+  }
+}
+
+__device__ __forceinline__ void epi4_apply(const Params& p, const Epi4& e, float4& v) {
+  float x[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    x[j] = apply_act(p.act, x[j] + e.b[j]);
+    if (p.dop) x[j] *= p.dop == PFB_DOP_DTANH ? 1.f - e.y[j] * e.y[j] : e.y[j] * (1.f - e.y[j]);
+  }
+  v = make_float4(x[0], x[1], x[2], x[3]);
 }
 
 __device__ __forceinline__ void tma_load_operand(const CUtensorMap* mh, const CUtensorMap* ml,
@@ -217,8 +247,11 @@ __device__ __forceinline__ void cluster_reduce(const Params& p, uint32_t red, in
     asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(base[q]) : "r"(red), "r"(q));
   const int items = (re - rb) * (BN / 4);
   float* cbase = p.C + bz * p.scb;
+  const float* rbias = p.alpha_rows != nullptr ? p.bias : nullptr;  // else in split 0's partial
+  const bool has_epi = rbias != nullptr || p.act != 0 || p.dop != 0;
   for (int i0 = threadIdx.x; i0 < items; i0 += PER * NUM_THREADS) {
     float4 w[PER][KS];
+    Epi4 ep[PER];
 #pragma unroll
     for (int j = 0; j < PER; ++j) {
       const int idx = i0 + j * NUM_THREADS;
@@ -227,6 +260,7 @@ __device__ __forceinline__ void cluster_reduce(const Params& p, uint32_t red, in
         const uint32_t off = (uint32_t)(row * BN + 4 * (ch ^ (row & 7))) * 4u;
 #pragma unroll
         for (int q = 0; q < KS; ++q) w[j][q] = ld_dsmem_f4_nv(base[q] + off);
+        if (has_epi && m0 + row < p.M) epi4_load(p, rbias, bz, m0 + row, n0 + 4 * ch, ep[j]);
       }
     }
 #pragma unroll
@@ -247,7 +281,7 @@ __device__ __forceinline__ void cluster_reduce(const Params& p, uint32_t red, in
           const float4 o = *reinterpret_cast<const float4*>(q);
           v.x += o.x; v.y += o.y; v.z += o.z; v.w += o.w;
         }
-        epi4(p, bz, grow, col, v);
+        if (has_epi) epi4_apply(p, ep[j], v);
         *reinterpret_cast<float4*>(q) = v;
       } else {
         if (p.accumulate) {
@@ -256,7 +290,7 @@ __device__ __forceinline__ void cluster_reduce(const Params& p, uint32_t red, in
           if (col + 2 < p.N) v.z += q[2 * p.scn];
           if (col + 3 < p.N) v.w += q[3 * p.scn];
         }
-        epi4(p, bz, grow, col, v);
+        if (has_epi) epi4_apply(p, ep[j], v);
         const float e[4] = {v.x, v.y, v.z, v.w};
         for (int jj = 0; jj < 4; ++jj)
           if (col + jj < p.N) q[(int64_t)jj * p.scn] = e[jj];
@@ -341,6 +375,11 @@ gemm_kernel(const __grid_constant__ CUtensorMap map_ah, const __grid_constant__ 
   if (threadIdx.x == 0) stamp(p, 1);
   pdl_enter();
   if (threadIdx.x == 0) stamp(p, 2);
+  if (threadIdx.x == 0 && p.trace != nullptr && blockIdx.x < 160) {  // per-CTA start
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    p.trace[192 + blockIdx.x] = t;
+  }
 
   auto a_bytes = [&](int mode) { return (mode == kPreSplit ? 2 : 1) * TILE_BYTES; };
   auto b_bytes = [&](int mode) { return (mode == kPreSplit ? 2 : 1) * C::B_BYTES; };
@@ -357,7 +396,9 @@ gemm_kernel(const __grid_constant__ CUtensorMap map_ah, const __grid_constant__ 
           const int s = g % STAGES;
           if (g >= STAGES) mbar_wait(&empty[s], ((g / STAGES) - 1) & 1);
           if (g < 16) stamp(p, 80 + g);
-          if (kb < p.nk1) {
+          if ((p.exp & 1) && g >= STAGES) {
+            mbar_arrive(&full[s]);  // experiment: stages reused without reloading
+          } else if (kb < p.nk1) {
             const int za = p.a_bcast ? 0 : bz, zb = p.b_bcast ? 0 : bz;
             if (g < 16) stamp(p, 16 + g);
             mbar_expect_tx(&full[s], a_bytes(p.a_mode) + b_bytes(p.b_mode));
@@ -490,8 +531,21 @@ gemm_kernel(const __grid_constant__ CUtensorMap map_ah, const __grid_constant__ 
       const int m0 = (r / p.ntn) * BM, n0 = (r % p.ntn) * BN;
       const int kb0 = ks * p.kb_per_split, kb1 = min(nk, kb0 + p.kb_per_split);
       const int uchunks = (kb1 - kb0 + p.chunk_kb - 1) / p.chunk_kb;
+      // the bias starts the accumulation of split 0 (its loads overlap the
+      // k-loop instead of stalling the epilogue); a row scale must not scale it
+      const float* abias = (ks == 0 && p.alpha_rows == nullptr) ? p.bias : nullptr;
+      if (abias != nullptr && drains) {
+        const int grow = m0 + quarter * 32 + lane;
+        const int64_t rb = (int64_t)bz * p.sxb + (int64_t)grow * p.sxm;
 #pragma unroll
-      for (int j = 0; j < DCOLS; ++j) acc[j] = 0.f;
+        for (int j = 0; j < DCOLS; ++j) {
+          const int col = n0 + half * DCOLS + j;
+          acc[j] = (grow < p.M && col < p.N) ? __ldg(abias + rb + (int64_t)col * p.sxn) : 0.f;
+        }
+      } else {
+#pragma unroll
+        for (int j = 0; j < DCOLS; ++j) acc[j] = 0.f;
+      }
       // split chunk c's stages, then drain chunk c-1 (the MMA works on
       // chunk c-1 while the stages of chunk c are being split)
       for (int c = 0; c < uchunks; ++c) {
@@ -504,6 +558,8 @@ gemm_kernel(const __grid_constant__ CUtensorMap map_ah, const __grid_constant__ 
       }
       drain();
       if (!drains) continue;
+      // bias: folded into split 0's accumulator above unless rows are scaled
+      const float* ubias = (p.alpha_rows != nullptr && ks == 0) ? p.bias : nullptr;
       if (clustered) {
         // partial tile -> own smem (stage area is idle: every MMA of this
         // CTA's only unit has completed), rows x BN/4 float4, XOR-swizzled
@@ -525,17 +581,26 @@ gemm_kernel(const __grid_constant__ CUtensorMap map_ah, const __grid_constant__ 
         const int grow = row0 + lane;
         const float alpha =
             (p.alpha_rows && grow < p.M) ? __ldg(p.alpha_rows + (int64_t)bz * p.M + grow) : 1.f;
+        const bool epi = (ubias != nullptr || p.act != 0 || p.dop != 0) && grow < p.M;
 #pragma unroll
         for (int cc = 0; cc < DCOLS; cc += 32) {
           if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
           __syncwarp();
           const int col0 = n0 + half * DCOLS + cc;
 #pragma unroll
-          for (int q = 0; q < 8; ++q) {
-            float4 v = make_float4(acc[cc + 4 * q] * alpha, acc[cc + 4 * q + 1] * alpha,
-                                   acc[cc + 4 * q + 2] * alpha, acc[cc + 4 * q + 3] * alpha);
-            if (grow < p.M) epi4(p, bz, grow, col0 + 4 * q, v);
-            *reinterpret_cast<float4*>(stage + lane * 32 + 4 * (q ^ (lane & 7))) = v;
+          for (int h = 0; h < 8; h += 4) {
+            Epi4 e[4];
+            if (epi) {
+#pragma unroll
+              for (int q = 0; q < 4; ++q) epi4_load(p, ubias, bz, grow, col0 + 4 * (h + q), e[q]);
+            }
+#pragma unroll
+            for (int q = h; q < h + 4; ++q) {
+              float4 v = make_float4(acc[cc + 4 * q] * alpha, acc[cc + 4 * q + 1] * alpha,
+                                     acc[cc + 4 * q + 2] * alpha, acc[cc + 4 * q + 3] * alpha);
+              if (epi) epi4_apply(p, e[q - h], v);
+              *reinterpret_cast<float4*>(stage + lane * 32 + 4 * (q ^ (lane & 7))) = v;
+            }
           }
           asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
           __syncwarp();
@@ -575,7 +640,7 @@ gemm_kernel(const __grid_constant__ CUtensorMap map_ah, const __grid_constant__ 
                 const float4 o = *reinterpret_cast<const float4*>(q);
                 v.x += o.x; v.y += o.y; v.z += o.z; v.w += o.w;
               }
-              epi4(p, bz, row, col, v);
+              epi4(p, bz, row, col, v, ubias);
               *reinterpret_cast<float4*>(q) = v;
             } else {
               if (p.accumulate) {
@@ -585,7 +650,7 @@ gemm_kernel(const __grid_constant__ CUtensorMap map_ah, const __grid_constant__ 
                 if (col + 2 < p.N) v.z += qq[2 * ldn];
                 if (col + 3 < p.N) v.w += qq[3 * ldn];
               }
-              epi4(p, bz, row, col, v);
+              epi4(p, bz, row, col, v, ubias);
               const float e[4] = {v.x, v.y, v.z, v.w};
 #pragma unroll
               for (int j = 0; j < 4; ++j)
@@ -630,6 +695,11 @@ gemm_kernel(const __grid_constant__ CUtensorMap map_ah, const __grid_constant__ 
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base),
                  "r"(C::TMEM_COLS));
     if (lane == 0) stamp(p, 10);
+    if (lane == 0 && p.trace != nullptr && blockIdx.x < 160) {  // per-CTA end
+      unsigned long long t;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+      p.trace[352 + blockIdx.x] = t;
+    }
   }
 }
 
@@ -742,8 +812,8 @@ static unsigned long long* g_trace = nullptr;
 unsigned long long* tc_trace_buffer() {
   static const bool on = getenv_flag("PFB_TC_TRACE");
   if (on && g_trace == nullptr) {
-    cudaMalloc(&g_trace, 128 * sizeof(unsigned long long));
-    cudaMemset(g_trace, 0, 128 * sizeof(unsigned long long));
+    cudaMalloc(&g_trace, 512 * sizeof(unsigned long long));
+    cudaMemset(g_trace, 0, 512 * sizeof(unsigned long long));
   }
   return on ? g_trace : nullptr;
 }
@@ -994,6 +1064,6 @@ int gemm_tcgen05_dual(const GemmArgs& g1, const GemmArgs& g2, void* ws, int64_t 
 extern "C" int pfb_debug_tc_trace(unsigned long long* out16) {
   if (pfb::g_trace == nullptr) return PFB_E_UNSUPPORTED;
   cudaDeviceSynchronize();
-  return cudaMemcpy(out16, pfb::g_trace, 128 * sizeof(unsigned long long), cudaMemcpyDeviceToHost) ==
+  return cudaMemcpy(out16, pfb::g_trace, 512 * sizeof(unsigned long long), cudaMemcpyDeviceToHost) ==
                  cudaSuccess ? 0 : PFB_E_ARG;
 }

@@ -58,18 +58,29 @@ def _numel(shape):
     return n
 
 
+class PartsPending(Exception):
+    """A value held as unreduced split-K partials reached code that needs its
+    elements (the executor reduces it and retries)."""
+
+
 class DArray:
-    """A device tensor view: flat typed torch buffer + element offset/shape/strides."""
+    """A device tensor view: flat typed torch buffer + element offset/shape/strides.
 
-    __slots__ = ("buf", "offset", "shape", "strides", "dtype", "host")
+    `parts` = (S, stride): the value is the sum of S copies of this view at
+    element offsets j * stride -- the split-K partials of a GEMM whose
+    consumers sum them as they load (pass F15, pfb_matmul_parts); views of it
+    keep the partials, anything else reduces them first."""
 
-    def __init__(self, buf, offset, shape, strides, dtype):
+    __slots__ = ("buf", "offset", "shape", "strides", "dtype", "host", "parts")
+
+    def __init__(self, buf, offset, shape, strides, dtype, parts=None):
         self.buf = buf
         self.offset = offset
         self.shape = tuple(int(d) for d in shape)
         self.strides = tuple(int(s) for s in strides)
         self.dtype = dtype
         self.host = None  # host copy of a small constant index vector (view gathers)
+        self.parts = parts
 
     @staticmethod
     def empty(shape, dtype, device):
@@ -104,6 +115,11 @@ class DArray:
         return True
 
     def desc(self):
+        if self.parts is not None:
+            raise PartsPending()
+        return self.desc_part0()
+
+    def desc_part0(self):
         t = N.PfbTensor()
         t.data = self.ptr
         t.dtype = _CODE[self.dtype]
@@ -114,9 +130,11 @@ class DArray:
         return t
 
     def view(self, shape, strides, extra_offset=0):
-        return DArray(self.buf, self.offset + extra_offset, shape, strides, self.dtype)
+        return DArray(self.buf, self.offset + extra_offset, shape, strides, self.dtype, self.parts)
 
     def torch_view(self):
+        if self.parts is not None:
+            raise PartsPending()
         if self.size == 0:
             return torch.empty(self.shape, dtype=self.buf.dtype, device=self.buf.device)
         return self.buf.as_strided(self.shape, self.strides,
@@ -208,7 +226,33 @@ class _Plan:
             elif (n.kind not in _NO_HOIST and n.block is None and n.inputs
                   and all(src in self.const_nodes for src, _ in n.inputs)):
                 self.const_nodes.add(n.id)
+        # F15: GEMMs whose every use reaches a fused elementwise group through
+        # views only (and no graph output) may return unreduced partials
+        cons = {}
+        for n in self.order:
+            for src, _ in n.inputs:
+                cons.setdefault(src, []).append(n)
+        root_ids = set(roots)
 
+        def sums_on_load(nid, depth=0):
+            if nid in root_ids or depth > 16 or nid not in cons:
+                return False
+            for c in cons[nid]:
+                if c.kind in _PARTS_VIEW_KINDS:
+                    if not sums_on_load(c.id, depth + 1):
+                        return False
+                elif c.kind not in _PARTS_SUM_KINDS:
+                    return False
+            return True
+
+        self.parts_ok = {n.id for n in self.order
+                         if n.kind in ("matmul", "matmul_ep") and n.id not in self.const_nodes
+                         and sums_on_load(n.id)}
+
+
+_PARTS_VIEW_KINDS = frozenset({"reshape", "transpose", "gather_rows", "slice_leading"})
+_PARTS_SUM_KINDS = frozenset({"fused_ew", "fused_ewm", "fused_pack"})
+_PARTS_AWARE = _PARTS_VIEW_KINDS | _PARTS_SUM_KINDS | {"tile_leading"}
 
 _NO_HOIST = STATEFUL_KINDS | {"placeholder", "capture", "carried", "loop_var", "where_true",
                               "complement"}
@@ -282,6 +326,9 @@ class Executor:
         self._dvars = {}
         self.kernel_timer = None
         self._const_ctx = None
+        self._parts_ok = None  # F15: GEMM node ids of the running plan that may return partials
+        self.parts_made = 0     # F15 GEMMs that returned partials / partials reduced by a
+        self.parts_reduced = 0  # consumer that could not sum them on load
         self._planes = {}
 
     # -- public API ------------------------------------------------------------
@@ -905,12 +952,16 @@ class Executor:
         for r in roots:
             remaining[r] = remaining.get(r, 0) + 1
         env = {}
-        saved_ctx = self._const_ctx
+        saved_ctx, saved_parts = self._const_ctx, self._parts_ok
         self._const_ctx = (g, plan.const_nodes)
+        self._parts_ok = plan.parts_ok
         try:
             self._run_nodes(g, plan, env, binder, feeds, remaining)
         finally:
-            self._const_ctx = saved_ctx
+            self._const_ctx, self._parts_ok = saved_ctx, saved_parts
+        for r in roots:  # (F15 never applies to outputs; defensive)
+            if isinstance(env.get(r), DArray) and env[r].parts is not None:
+                env[r] = self._reduce_parts(env[r])
         return env
 
     def _run_nodes(self, g, plan, env, binder, feeds, remaining):
@@ -1020,7 +1071,26 @@ class Executor:
         h = _HANDLERS.get(k)
         if h is None:
             raise E.PforVecError(f"no evaluation rule for kind {k!r}")
-        return h(self, node, ins)
+        if k not in _PARTS_AWARE:
+            ins = [self._reduce_parts(v) for v in ins]
+            return h(self, node, ins)
+        try:
+            return h(self, node, ins)
+        except PartsPending:
+            return h(self, node, [self._reduce_parts(v) for v in ins])
+
+    def _reduce_parts(self, v):
+        """The value of a split-K partials view (F15) as an ordinary tensor."""
+        if not isinstance(v, DArray) or v.parts is None:
+            return v
+        self.parts_reduced += 1
+        S, st = v.parts
+        stacked = DArray(v.buf, v.offset, (S,) + v.shape, (st,) + v.strides, v.dtype)
+        out = self._empty(v.shape, v.dtype)
+        wp, wn = self._ws_get(min(8 * max(1, _numel(v.shape)) * 1024, 1 << 26))
+        self._call(self._lib.pfb_reduce_sum, stacked.desc(), 1, out.desc(), wp, wn, self._stream,
+                   what="reduce_sum", work=(_abytes(stacked, out), 0))
+        return out
 
     def _feed(self, name, value, dtype):
         """Placeholder value on the device.  Host feeds are copied into one
@@ -1229,12 +1299,15 @@ def _h_matmul(ex, node, ins):
         raise E.RankError(f"matmul: unsupported ranks {a.rank} x {b.rank}")
     if a.dtype != DType.F64:
         raise E.DTypeMismatch("matmul: only f64 (fp32 on device) is on the B200 path")
+    planes = ex._b_planes(node, 1, b)
+    res = _matmul_parts(ex, node, a, b, None, planes)
+    if res is not None:
+        return [res]
     out = ex._empty(shape, a.dtype)
     flops = 2 * _numel(shape) * a.shape[-1]
     ad, bd, od = a.desc(), b.desc(), out.desc()
     need = ex._lib.pfb_matmul_workspace(ad, bd, od)
     wp, wn = ex._ws_get(need) if need > 0 else (None, 0)
-    planes = ex._b_planes(node, 1, b)
     if planes is not None:
         ex._call(ex._lib.pfb_matmul_ep2, ad, bd, od, None, None, 0, None, 0, planes, 0,
                  wp, wn, ex._stream, what="matmul", work=(_abytes(a, b, out), flops))
@@ -1245,6 +1318,32 @@ def _h_matmul(ex, node, ins):
 
 
 _ACT_CODE = {None: 0, "tanh": 1, "sigmoid": 2, "relu": 3}
+
+
+def _matmul_parts(ex, node, a, b, bias, planes):
+    """F15: a skinny 2-D GEMM whose uses all sum on load (plan.parts_ok) runs
+    as pfb_matmul_parts -- S k-splits, no reduction -- and returns a partials
+    view (DArray.parts); None when the shape or the consumers do not allow it."""
+    if (node.id not in (ex._parts_ok or ()) or a.rank != 2 or b.rank != 2
+            or a.dtype != DType.F64 or not ex._lib.pfb_fused_parts_ok()):
+        return None
+    shape = (a.shape[0], b.shape[1])
+    probe = DArray(a.buf, 0, shape, _dense_strides(shape), a.dtype)
+    ad, bd = a.desc(), b.desc()
+    S = ex._lib.pfb_matmul_parts_count(ad, bd, probe.desc())
+    if S < 2:
+        return None
+    stacked = ex._empty((S,) + shape, a.dtype)
+    need = 0 if planes is not None else ex._lib.pfb_matmul_parts_workspace(ad, bd, probe.desc())
+    wp, wn = ex._ws_get(need) if need > 0 else (None, 0)
+    xd = bias.desc() if bias is not None else None
+    flops = 2 * _numel(shape) * a.shape[-1]
+    ex._call(ex._lib.pfb_matmul_parts, ad, bd, stacked.desc(),
+             ctypes.byref(xd) if xd is not None else None, planes, wp, wn, ex._stream,
+             what="matmul", work=(_abytes(a, b, stacked) + (_abytes(bias) if bias is not None else 0),
+                                  flops))
+    ex.parts_made += 1
+    return DArray(stacked.buf, 0, shape, _dense_strides(shape), a.dtype, (S, _numel(shape)))
 
 
 def _rows_view(x):
@@ -1312,6 +1411,10 @@ def _h_matmul_ep(ex, node, ins):
         shape = (a.shape[0], b.shape[1])
     else:
         shape = (a.shape[0], a.shape[1], b.shape[2])
+    if ks is None and dy is None and at.get("act") is None:
+        res = _matmul_parts(ex, node, a, b, bias, ex._b_planes(node, 1, b))
+        if res is not None:
+            return [res]
     out = ex._empty(shape, a.dtype)
     flops = 2 * _numel(shape) * a.shape[-1]
     ad, bd, od = a.desc(), b.desc(), out.desc()
@@ -1580,8 +1683,8 @@ def _h_reshape(ex, node, ins):
         return [HostVal(x.value.reshape(shape), x.dtype)]
     if x.is_dense():
         return [x.view(shape, _dense_strides(shape))]
-    try:
-        v = x.torch_view().view(shape)
+    try:  # strides of the reshaped view, if one exists (no data touched)
+        v = torch.empty_strided(x.shape, x.strides, device="meta").view(shape)
         return [x.view(shape, v.stride())]
     except RuntimeError:
         d = ex._dense(x)
@@ -1666,6 +1769,29 @@ def _h_range_vec(ex, node, ins):
     return [out]
 
 
+def _fused_launch(ex, arrs, prog, regs, nregs, outs):
+    """One fused-program launch; inputs held as split-K partials (F15) go
+    through pfb_fused_ew_parts, which sums them as it loads."""
+    odescs = (N.PfbTensor * len(outs))(*[o.desc() for o in outs])
+    if any(a.parts is not None for a in arrs) and not ex._lib.pfb_fused_parts_ok():
+        arrs = [ex._reduce_parts(a) for a in arrs]
+    if any(a.parts is not None for a in arrs):
+        spec = []
+        for a in arrs:
+            spec += list(a.parts) if a.parts is not None else [1, 0]
+        pa = (ctypes.c_int64 * len(spec))(*spec)
+        descs = (N.PfbTensor * len(arrs))(*[a.desc_part0() for a in arrs])
+        nbytes = sum(_abytes(a) * (a.parts[0] if a.parts else 1) for a in arrs)
+        ex._call(ex._lib.pfb_fused_ew_parts, len(arrs), descs, pa, prog[1], prog[0], nregs, regs,
+                 odescs, ex._stream, what="fused_ew",
+                 work=(nbytes + _abytes(*outs), 0))
+        return
+    descs = (N.PfbTensor * len(arrs))(*[a.desc() for a in arrs])
+    ex._call(ex._lib.pfb_fused_ew_multi, len(arrs), descs, prog[1], prog[0], nregs, regs,
+             odescs, ex._stream, what="fused_ew",
+             work=(_abytes(*arrs, *outs), 0))
+
+
 def _h_fused(ex, node, ins):
     """fused_ew (passes.fuse_elementwise): one launch for a chain of elementwise
     ops; the program rides in the node attrs."""
@@ -1679,6 +1805,10 @@ def _h_fused(ex, node, ins):
         flat = [int(x) for step in node.attrs["program"] for x in step]
         prog = ex._programs[id(node)] = ((ctypes.c_int32 * len(flat))(*flat),
                                          len(node.attrs["program"]))
+    if any(a.parts is not None for a in arrs):
+        last = node.attrs["program"][-1][1]
+        _fused_launch(ex, arrs, prog, (ctypes.c_int32 * 1)(last), 1, [out])
+        return [out]
     descs = (N.PfbTensor * len(arrs))(*[a.desc() for a in arrs])
     ex._call(ex._lib.pfb_fused_ew, len(arrs), descs, prog[1], prog[0], out.desc(), ex._stream,
              what="fused_ew", work=(_abytes(*arrs, out), 0))
@@ -1700,10 +1830,7 @@ def _h_fused_multi(ex, node, ins):
         prog = ex._programs[id(node)] = ((ctypes.c_int32 * len(flat))(*flat),
                                          len(node.attrs["program"]),
                                          (ctypes.c_int32 * len(regs))(*regs), len(regs))
-    descs = (N.PfbTensor * len(arrs))(*[a.desc() for a in arrs])
-    odescs = (N.PfbTensor * len(outs))(*[o.desc() for o in outs])
-    ex._call(ex._lib.pfb_fused_ew_multi, len(arrs), descs, prog[1], prog[0], prog[3], prog[2],
-             odescs, ex._stream, what="fused_ew", work=(_abytes(*arrs, *outs), 0))
+    _fused_launch(ex, arrs, prog, prog[2], prog[3], outs)
     return outs
 
 
@@ -1736,10 +1863,7 @@ def _h_fused_pack(ex, node, ins):
         regs = [int(r) for r in a["out_regs"]]
         prog = ex._programs[id(node)] = ((ctypes.c_int32 * len(flat))(*flat), len(a["program"]),
                                          (ctypes.c_int32 * len(regs))(*regs), len(regs))
-    descs = (N.PfbTensor * len(arrs))(*[x.desc() for x in arrs])
-    odescs = (N.PfbTensor * n_out)(*[o.desc() for o in outs])
-    ex._call(ex._lib.pfb_fused_ew_multi, len(arrs), descs, prog[1], prog[0], prog[3], prog[2],
-             odescs, ex._stream, what="fused_ew", work=(_abytes(*arrs, *outs), 0))
+    _fused_launch(ex, arrs, prog, prog[2], prog[3], outs)
     return outs + [cat]
 
 

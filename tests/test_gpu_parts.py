@@ -1,0 +1,152 @@
+"""GPU: pass F15 -- split-K partials GEMM (pfb_matmul_parts) and fused groups
+that sum the partials as they load (pfb_fused_ew_parts), against f64 numpy
+(reference tensor.matmul, tensor.py:195-206) and against the executor with
+partials disabled."""
+
+import ctypes
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+RTOL, ATOL = 1e-4, 1e-5
+
+
+@pytest.fixture(scope="module")
+def env():
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    from paper_1903_04243_b200 import _native as N
+    from paper_1903_04243_b200.executor import DArray
+    from paper_1903_04243_b200.tensor import DType
+    return torch, N.lib(), DArray, DType
+
+
+def _parts(env, a, b, bias=None, planes=False, b_kmajor=True):
+    torch, lib, DArray, DType = env
+    dev = torch.device("cuda")
+    A = DArray.from_numpy(a, DType.F64, dev)
+    if b_kmajor:  # the executor's weights: B^T stored densely ([N, K]), B a transposed view
+        Bt = DArray.from_numpy(b.T.copy(), DType.F64, dev)
+        B = Bt.view((b.shape[0], b.shape[1]), (1, b.shape[0]))
+    else:
+        B = DArray.from_numpy(b, DType.F64, dev)
+    m, n = a.shape[0], b.shape[1]
+    probe = DArray.empty((m, n), DType.F64, dev)
+    ad, bd = A.desc(), B.desc()
+    S = lib.pfb_matmul_parts_count(ad, bd, probe.desc())
+    if S < 1:
+        return None, 0
+    P = DArray.empty((S, m, n), DType.F64, dev)
+    pb = None
+    if planes:
+        pb = torch.empty(lib.pfb_gemm_planes_bytes(bd), dtype=torch.uint8, device=dev)
+        assert lib.pfb_gemm_split_planes(bd, pb.data_ptr(), None) == 0
+    need = lib.pfb_matmul_parts_workspace(ad, bd, probe.desc())
+    ws = torch.empty(max(need, 256), dtype=torch.uint8, device=dev)
+    xd = None
+    if bias is not None:
+        X = DArray.from_numpy(bias, DType.F64, dev)
+        xd = ctypes.byref(X.desc())
+    rc = lib.pfb_matmul_parts(ad, bd, P.desc(), xd, pb.data_ptr() if pb is not None else None,
+                              ws.data_ptr(), ws.numel(), None)
+    assert rc == 0
+    torch.cuda.synchronize()
+    return P.to_numpy(), S
+
+
+@pytest.mark.parametrize("m,n,k", [(256, 2048, 1024), (256, 512, 2048), (256, 2048, 512),
+                                   (200, 300, 520), (64, 136, 100)])
+@pytest.mark.parametrize("planes", [False, True])
+def test_matmul_parts_sum_matches_f64(env, m, n, k, planes):
+    r = np.random.default_rng(m + n + k)
+    a = r.standard_normal((m, k)).astype(np.float32)
+    b = (r.standard_normal((k, n)) / np.sqrt(k)).astype(np.float32)
+    bias = r.standard_normal((n,)).astype(np.float32)
+    parts, S = _parts(env, a, b, bias, planes)
+    assert S >= 1 and parts is not None
+    got = parts.astype(np.float64).sum(0)
+    want = a.astype(np.float64) @ b.astype(np.float64) + bias
+    np.testing.assert_allclose(got, want, rtol=RTOL, atol=ATOL)
+
+
+def test_matmul_parts_row_bias_and_row_major_b(env):
+    r = np.random.default_rng(7)
+    a = r.standard_normal((256, 640)).astype(np.float32)
+    b = (r.standard_normal((640, 384)) / 25).astype(np.float32)
+    bias = r.standard_normal((256, 384)).astype(np.float32)  # a full matrix addend
+    parts, S = _parts(env, a, b, bias, planes=False, b_kmajor=False)
+    assert S >= 2
+    want = a.astype(np.float64) @ b.astype(np.float64) + bias
+    np.testing.assert_allclose(parts.astype(np.float64).sum(0), want, rtol=RTOL, atol=ATOL)
+
+
+def test_fused_parts_feed_sums_in_split_order(env):
+    """An elementwise program over partials: each input summed left to right
+    in fp32 as loaded -- bit-identical to numpy's fp32 left fold."""
+    torch, lib, DArray, DType = env
+    from paper_1903_04243_b200 import _native as N
+    dev = torch.device("cuda")
+    r = np.random.default_rng(3)
+    S, shape = 5, (64, 96)
+    parts = r.standard_normal((S,) + shape).astype(np.float32)
+    c = r.standard_normal(shape).astype(np.float32)
+    P = DArray.from_numpy(parts, DType.F64, dev)
+    C = DArray.from_numpy(c, DType.F64, dev)
+    view = P.view(shape, P.strides[1:])
+    out = DArray.empty(shape, DType.F64, dev)
+    # program: r0 = load in0 (partials); r1 = load in1; r3 = tanh(r0) * r1
+    ops = _opcodes()
+    prog = [(64, 0, 0, 0), (64, 1, 1, 0), (ops["tanh"], 2, 0, 0), (ops["mul"], 3, 2, 1)]
+    flat = (ctypes.c_int32 * 16)(*[x for st in prog for x in st])
+    spec = (ctypes.c_int64 * 4)(S, int(np.prod(shape)), 1, 0)
+    ins = (N.PfbTensor * 2)(view.desc_part0(), C.desc())
+    outs = (N.PfbTensor * 1)(out.desc())
+    regs = (ctypes.c_int32 * 1)(3)
+    if not lib.pfb_fused_parts_ok():
+        pytest.skip("specialiser unavailable")
+    assert lib.pfb_fused_ew_parts(2, ins, spec, 4, flat, 1, regs, outs, None) == 0
+    torch.cuda.synchronize()
+    acc = parts[0].copy()
+    for j in range(1, S):
+        acc = (acc + parts[j]).astype(np.float32)
+    got = out.to_numpy()
+    want = (np.tanh(acc.astype(np.float64)) * c).astype(np.float32)
+    np.testing.assert_allclose(got, want, rtol=1e-6, atol=1e-6)
+    # the sum itself is exact in split order: program r2 = r0 (move)
+    prog2 = [(64, 0, 0, 0), (64, 1, 1, 0), (ops["add"], 2, 0, 1)]
+    flat2 = (ctypes.c_int32 * 12)(*[x for st in prog2 for x in st])
+    zero = DArray.from_numpy(np.zeros(shape, np.float32), DType.F64, dev)
+    ins2 = (N.PfbTensor * 2)(view.desc_part0(), zero.desc())
+    regs2 = (ctypes.c_int32 * 1)(2)
+    assert lib.pfb_fused_ew_parts(2, ins2, spec, 3, flat2, 1, regs2, outs, None) == 0
+    torch.cuda.synchronize()
+    np.testing.assert_array_equal(out.to_numpy(), acc)
+
+
+def _opcodes():
+    from paper_1903_04243_b200 import passes
+    return {"add": passes._BIN_CODE["add"], "mul": passes._BIN_CODE["mul"],
+            "tanh": 16 + passes._UN_CODE["tanh"]}
+
+
+def test_cfg4_partials_match_reduced_executor(env, monkeypatch):
+    """The LSTM program (cfg4 shapes with M = 256 examples, where the per-step
+    GEMMs take the partials path) equals the same program with F15 off."""
+    torch, lib, DArray, DType = env
+    from paper_1903_04243_b200 import workloads as WL
+    from paper_1903_04243_b200.executor import Executor
+    w = WL.BUILDERS["cfg4"](WL.this_api(), n=256, steps=4, units=256)
+    ex = Executor(w.graph, device="cuda:0", cuda_graph=False)
+    got = ex.run(feeds=w.feeds)
+    # every per-step GEMM (4 forward, 3 backward) returned partials and every
+    # consumer summed them on load
+    assert ex.parts_made == 7 and ex.parts_reduced == 0, (ex.parts_made, ex.parts_reduced)
+    ex2 = Executor(w.graph, device="cuda:0")
+    monkeypatch.setattr(ex2._lib, "pfb_fused_parts_ok", lambda: 0)
+    want = ex2.run(feeds=w.feeds)
+    for g_, w_ in zip(got, want):
+        np.testing.assert_allclose(np.asarray(g_.data, np.float64), np.asarray(w_.data, np.float64),
+                                   rtol=RTOL, atol=ATOL)

@@ -137,7 +137,7 @@ int main(int argc, char** argv) {
   const int reps = argc > 1 ? atoi(argv[1]) : 100;
   const uint32_t idesc = (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(128 >> 3) << 17) | ((uint32_t)(128 >> 4) << 24);
   cudaFuncSetAttribute(bench, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-  for (int mode : {4, 10}) {
+  for (int mode : {0, 1, 2, 3, 4, 7, 8, 10}) {
     for (int grid : {1, 148}) {
      if (mode == 9) {
       // back-to-back launches with programmatic dependent launch (as the GEMMs run)

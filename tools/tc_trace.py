@@ -31,6 +31,7 @@ def main():
     ap.add_argument("--shape", type=int, nargs="+", required=True)
     ap.add_argument("--planes", action="store_true")
     ap.add_argument("--graph", type=int, default=0)
+    ap.add_argument("--parts", action="store_true", help="split-K partials (pfb_matmul_parts)")
     args = ap.parse_args()
     m, n, k = args.shape[:3]
     lib = N.lib()
@@ -53,13 +54,21 @@ def main():
         lib.pfb_gemm_split_planes(bd, pb.data_ptr(), s)
         planes = pb.data_ptr()
 
+    if args.parts:
+        S = lib.pfb_matmul_parts_count(ad, bd, cd)
+        pt = torch.empty(S, m, n, device=dev)
+        pd = DArray(pt.reshape(-1), 0, pt.shape, pt.stride(), DType.F64).desc()
+
     def call(stream):
+        if args.parts:
+            return lib.pfb_matmul_parts(pd, bd, pd, None, planes, ws.data_ptr(), ws.numel(), stream) \
+                if False else lib.pfb_matmul_parts(ad, bd, pd, None, planes, ws.data_ptr(), ws.numel(), stream)
         if planes is not None:
             return lib.pfb_matmul_ep2(ad, bd, cd, None, None, 0, None, 0, planes, args.force,
                                       ws.data_ptr(), ws.numel(), stream)
         return lib.pfb_matmul_ex(ad, bd, cd, None, 0, args.force, ws.data_ptr(), ws.numel(), stream)
 
-    buf = (ctypes.c_ulonglong * 128)()
+    buf = (ctypes.c_ulonglong * 512)()
     call(s)  # trace buffer allocated outside any capture
     torch.cuda.synchronize()
     for rep in range(3):
@@ -81,6 +90,13 @@ def main():
         names = PAIR_NAMES if args.force in (5, 6) else NAMES
         print(f"rep {rep} rc={rc}: " + "  ".join(
             f"{nm}={(buf[i] - t0) / 1e3:.2f}" for i, nm in enumerate(names) if buf[i] and buf[i] >= t0))
+        st_ = [buf[192 + i] for i in range(160) if buf[192 + i] >= t0]
+        en_ = [buf[352 + i] for i in range(160) if buf[352 + i] >= t0]
+        if st_ and en_:
+            import statistics as S_
+            print("   per-CTA start (us): min %.2f med %.2f max %.2f | end: min %.2f med %.2f max %.2f (n=%d)" % (
+                (min(st_) - t0) / 1e3, (S_.median(st_) - t0) / 1e3, (max(st_) - t0) / 1e3,
+                (min(en_) - t0) / 1e3, (S_.median(en_) - t0) / 1e3, (max(en_) - t0) / 1e3, len(en_)))
         if args.force not in (5, 6):
             cyc = [buf[96 + kb] for kb in range(16)]
             print("   mma_start deltas (SM cycles):", [int(cyc[i + 1] - cyc[i]) for i in range(15) if cyc[i + 1]])
