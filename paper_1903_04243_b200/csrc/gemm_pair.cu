@@ -44,14 +44,18 @@ constexpr int threads_of() { return NUM_THREADS + (SINGLE ? 32 * SPLIT_WARPS : 0
 constexpr int A_BYTES = 128 * BK * 4;  // 16 KB: this CTA's 128 rows of A
 enum { kPreSplit = 0, kRawK = 1, kRawMN = 2 };
 
-template <int BN>
+// TMEM-resident mode (SINGLE, short K): the epilogue is store-bound, so the
+// 256-wide tile trades a stage for a second staging block per warp (a
+// block's TMA store drains while the next one is written)
+template <int BN, bool SINGLE = false>
 struct Cfg {
   static constexpr int BNH = BN / 2;                 // B rows held by each CTA
   static constexpr int B_BYTES = BNH * BK * 4;
   static constexpr int STAGE_BYTES = 2 * A_BYTES + 2 * B_BYTES;
-  static constexpr int STAGES = BN == 256 ? 3 : 4;
+  static constexpr int STAGES = BN == 256 ? (SINGLE ? 2 : 3) : 4;
   static constexpr int EPI_COLS = BN / 2;            // accumulator columns per epilogue warp
-  static constexpr int STAGING = EPI_WARPS * 32 * 32 * 4;
+  static constexpr int NSTG = (BN == 256 && SINGLE) ? 2 : 1;  // staging blocks per warp
+  static constexpr int STAGING = EPI_WARPS * 32 * 32 * 4 * NSTG;
   static constexpr int SMEM = STAGES * STAGE_BYTES + STAGING + 1024 + 256;
   static constexpr int TMEM_COLS = 2 * BN;           // double-buffered chunk accumulator
 };
@@ -157,7 +161,7 @@ __global__ void __launch_bounds__(threads_of<SINGLE>(), 1)
 pair_kernel(const __grid_constant__ CUtensorMap map_ah, const __grid_constant__ CUtensorMap map_al,
             const __grid_constant__ CUtensorMap map_bh, const __grid_constant__ CUtensorMap map_bl,
             const __grid_constant__ CUtensorMap map_c, PParams p) {
-  using C = Cfg<BN>;
+  using C = Cfg<BN, SINGLE>;
   constexpr int STAGES = C::STAGES, BNH = C::BNH, EPI_COLS = C::EPI_COLS;
   if (threadIdx.x == 0) pstamp(p, 0);
   extern __shared__ uint8_t smem_raw[];
@@ -307,7 +311,8 @@ pair_kernel(const __grid_constant__ CUtensorMap map_ah, const __grid_constant__ 
     const int quarter = warp & 3;
     const int half = (warp - 2) >> 2;
     const int et = threadIdx.x - 64;
-    float* stage = staging + (warp - 2) * 32 * 32;
+    float* stage0 = staging + (warp - 2) * 32 * 32 * C::NSTG;
+    int nst = 0;  // staging blocks used (round robin over NSTG)
     const bool split_a = p.a_mode != kPreSplit, split_b = p.b_mode != kPreSplit;
     int gc = 0, gs = 0;
     auto split_stage = [&]() {
@@ -331,8 +336,13 @@ pair_kernel(const __grid_constant__ CUtensorMap map_ah, const __grid_constant__ 
     // block or (strided / accumulating C) 4-row x 128-byte stores through it
     auto emit32 = [&](const float* vals, int bz, int row0, int col0, float alpha) {
       const int grow = row0 + lane;
+      float* stage = stage0 + 32 * 32 * (nst++ % C::NSTG);
       if (p.tma_store) {
-        if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+        // the block's previous store has finished reading it (NSTG - 1 may be in flight)
+        if (lane == 0) {
+          if (C::NSTG == 2) asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
+          else asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+        }
         __syncwarp();
 #pragma unroll
         for (int q = 0; q < 8; ++q) {
@@ -562,7 +572,7 @@ template <int BN, bool SINGLE>
 static int launch_pair(const CUtensorMap& mah, const CUtensorMap& mal, const CUtensorMap& mbh,
                        const CUtensorMap& mbl, const CUtensorMap& mc, const PParams& p,
                        cudaStream_t s) {
-  using C = Cfg<BN>;
+  using C = Cfg<BN, SINGLE>;
   static bool attr = false;
   if (!attr) {
     cudaFuncSetAttribute(pair_kernel<BN, SINGLE>, cudaFuncAttributeMaxDynamicSharedMemorySize,

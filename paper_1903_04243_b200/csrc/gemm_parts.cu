@@ -52,14 +52,26 @@ struct Cfg {
   static constexpr uint32_t IDESC = (1u << 4) | (2u << 7) | (2u << 10) |
                                     ((uint32_t)(BN >> 3) << 17) | ((uint32_t)(BM >> 4) << 24);
   static_assert(SMEM <= 232448, "shared memory");
-  static_assert(SPLIT_WARPS * 4096 <= STAGES * STAGE, "epilogue staging reuses the stages");
+  static_assert(SPLIT_WARPS * 4096 * (BN / 64) <= STAGES * STAGE, "epilogue staging reuses the stages");
 };
 
 struct Params {
   int M, N, nk, kb_per, ntn, S;
   const float* bias;  // split 0 only; broadcast strides
   int64_t sxm, sxn;
+  float* C;          // direct-store epilogue (PFB_PARTS_STORE=1): parts base, strides
+  int64_t ldc, part_stride;
+  int direct;
+  unsigned long long* trace;  // PFB_TC_TRACE: phase stamps of CTA 0 + per-CTA start/end
 };
+
+__device__ __forceinline__ void pstamp(const Params& p, int i, bool cta_any = false) {
+  if (p.trace != nullptr && (cta_any || blockIdx.x == 0)) {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    p.trace[i] = t;
+  }
+}
 
 template <int BN>
 __global__ void __launch_bounds__(NUM_THREADS, 1)
@@ -106,7 +118,12 @@ parts_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ 
   __syncthreads();
   asm volatile("tcgen05.fence::after_thread_sync;");
   const uint32_t tmem = *tmem_slot;
+  if (threadIdx.x == 0) pstamp(p, 0);
   pdl_enter();
+  if (threadIdx.x == 0) {
+    pstamp(p, 1);
+    if (blockIdx.x < 160) pstamp(p, 192 + blockIdx.x, true);
+  }
 
   if (warp == 0) {
     if (lane == 0) {
@@ -117,6 +134,7 @@ parts_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ 
         tma_load_3d(&map_a, &full[s], stage(s), kb * BK, m0, 0);
         tma_load_3d(&map_bh, &full[s], stage(s) + 2 * A_BYTES, kb * BK, n0, 0);
         tma_load_3d(&map_bl, &full[s], stage(s) + 2 * A_BYTES + C::B_BYTES, kb * BK, n0, 0);
+        if (g < 8) pstamp(p, 16 + g);
       }
     }
   } else if (warp == 1) {
@@ -129,6 +147,7 @@ parts_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ 
       const uint64_t bh = smem_desc_sw128(smem_u32(stage(s) + 2 * A_BYTES));
       const uint64_t bl = smem_desc_sw128(smem_u32(stage(s) + 2 * A_BYTES + C::B_BYTES));
       if (elect_one()) {
+        if (g < 8) pstamp(p, 32 + g);
 #pragma unroll
         for (int k = 0; k < BK / UMMA_K; ++k) {
           const uint64_t d = (UMMA_K * 4) >> 4;  // +32 B inside the swizzle row
@@ -147,29 +166,38 @@ parts_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ 
     for (int g = 0; g < nkb; ++g) {
       const int s = g % C::STAGES;
       mbar_wait(&full[s], (g / C::STAGES) & 1);
+      if (et == 0 && g < 8) pstamp(p, 48 + g);
       split_tf32_smem(smem_u32(stage(s)), smem_u32(stage(s) + A_BYTES), A_BYTES / 16, et,
                       32 * SPLIT_WARPS);
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
       __syncwarp();
       if (lane == 0) mbar_arrive(&ready[s]);
     }
-    // ---- epilogue: TMEM -> (+ bias) -> swizzled 32x32 block -> TMA store
+    // ---- epilogue: TMEM -> (+ bias) -> swizzled 32x32 block -> TMA store;
+    // one staging block per 32 columns (the stage memory is idle now), so no
+    // store waits for an earlier one to drain
+    constexpr int NB = BN / 64;  // 32-column blocks per warp
     const int quarter = warp & 3, half = (warp - 2) >> 2;
-    float* blk = reinterpret_cast<float*>(smem) + (warp - 2) * 1024;  // stage memory is idle
-    mbar_wait(acc_full, 0);
-    asm volatile("tcgen05.fence::after_thread_sync;");
+    float* blk0 = reinterpret_cast<float*>(smem) + (warp - 2) * 1024 * NB;
     const int row0 = m0 + quarter * 32;
     const bool add_bias = p.bias != nullptr && s_idx == 0;
-#pragma unroll 1
-    for (int cc = 0; cc < BN / 2; cc += 32) {
+    float bv[NB];  // bias of column (block col0) + lane (row-broadcast bias)
+#pragma unroll
+    for (int b = 0; b < NB; ++b) {
+      const int col = n0 + half * (BN / 2) + 32 * b + lane;
+      bv[b] = (add_bias && p.sxm == 0 && col < p.N) ? __ldg(p.bias + (int64_t)col * p.sxn) : 0.f;
+    }
+    mbar_wait(acc_full, 0);
+    if (et == 0) pstamp(p, 2);
+    asm volatile("tcgen05.fence::after_thread_sync;");
+#pragma unroll
+    for (int b = 0; b < NB; ++b) {
+      const int cc = 32 * b;
       const int col0 = n0 + half * (BN / 2) + cc;
+      float* blk = blk0 + 1024 * b;
       uint32_t v[32];
       tmem_ld32(tmem + ((uint32_t)(quarter * 32) << 16) + (uint32_t)(half * (BN / 2) + cc), v);
-      float bv = 0.f;  // bias of column col0 + lane (row-broadcast bias)
-      if (add_bias && p.sxm == 0 && col0 + lane < p.N) bv = __ldg(p.bias + (int64_t)(col0 + lane) * p.sxn);
       asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-      if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
-      __syncwarp();
 #pragma unroll
       for (int q = 0; q < 8; ++q) {
         float x[4];
@@ -178,7 +206,7 @@ parts_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ 
           x[j] = __uint_as_float(v[4 * q + j]);
           if (add_bias) {
             if (p.sxm == 0) {
-              x[j] += __shfl_sync(0xffffffffu, bv, 4 * q + j);
+              x[j] += __shfl_sync(0xffffffffu, bv[b], 4 * q + j);
             } else if (row0 + lane < p.M && col0 + 4 * q + j < p.N) {
               x[j] += __ldg(p.bias + (int64_t)(row0 + lane) * p.sxm +
                             (int64_t)(col0 + 4 * q + j) * p.sxn);
@@ -188,6 +216,25 @@ parts_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ 
         *reinterpret_cast<float4*>(blk + lane * 32 + 4 * (q ^ (lane & 7))) =
             make_float4(x[0], x[1], x[2], x[3]);
       }
+      if (p.direct) {
+        // each store instruction: 4 rows x 128 contiguous bytes
+        __syncwarp();
+        const int sub_r = lane >> 3, sub_c = (lane & 7) * 4;
+        float* cb = p.C + (int64_t)s_idx * p.part_stride;
+#pragma unroll
+        for (int i = 0; i < 32; i += 4) {
+          const int srow = i + sub_r, row = row0 + srow, col = col0 + sub_c;
+          const float4 w = *reinterpret_cast<const float4*>(blk + srow * 32 + 4 * ((sub_c >> 2) ^ (srow & 7)));
+          if (row < p.M && col + 3 < p.N) {
+            *reinterpret_cast<float4*>(cb + (int64_t)row * p.ldc + col) = w;
+          } else if (row < p.M) {
+            const float e[4] = {w.x, w.y, w.z, w.w};
+            for (int j = 0; j < 4; ++j)
+              if (col + j < p.N) cb[(int64_t)row * p.ldc + col + j] = e[j];
+          }
+        }
+        continue;
+      }
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
       __syncwarp();
       if (lane == 0) {
@@ -196,9 +243,14 @@ parts_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ 
       }
     }
     if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+    if (et == 0) pstamp(p, 3);
   }
   asm volatile("tcgen05.fence::before_thread_sync;");
   __syncthreads();
+  if (threadIdx.x == 0) {
+    pstamp(p, 4);
+    if (blockIdx.x < 160) pstamp(p, 352 + blockIdx.x, true);
+  }
   if (warp == 1) {
     asm volatile("tcgen05.fence::after_thread_sync;");
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(BN));
@@ -227,7 +279,7 @@ static int plan(int64_t M, int64_t N, int64_t K, int BN, int* kb_per) {
 template <int BN>
 static int launch(const GemmArgs& g, const CUtensorMap& ma, const CUtensorMap& mbh,
                   const CUtensorMap& mbl, const CUtensorMap& mc, int S, int kb_per,
-                  cudaStream_t s) {
+                  float* out, int64_t part_stride, int64_t ldc, cudaStream_t s) {
   using C = Cfg<BN>;
   static bool attr = false;
   if (!attr) {
@@ -241,6 +293,13 @@ static int launch(const GemmArgs& g, const CUtensorMap& ma, const CUtensorMap& m
   p.ntn = (int)((g.N + BN - 1) / BN);
   p.S = S;
   p.bias = g.bias; p.sxm = g.sxm; p.sxn = g.sxn;
+  p.trace = tc_trace_buffer();
+  p.C = out; p.ldc = ldc; p.part_stride = part_stride;
+  static const int direct = [] {
+    const char* e = getenv("PFB_PARTS_STORE");
+    return e ? atoi(e) : 0;
+  }();
+  p.direct = direct;
   const int units = (int)(((g.M + BM - 1) / BM) * p.ntn * S);
   pfb::launch(parts_kernel<BN>, dim3(units), dim3(NUM_THREADS), C::SMEM, s, ma, mbh, mbl, mc, p);
   return launch_status();
@@ -317,8 +376,8 @@ int gemm_parts(const GemmArgs& g, int S, float* parts, int64_t part_stride, int6
     cuuint32_t box[3] = {32, 32, 1};
     if (!encode(&mc, parts, dims, strides, box)) return PFB_E_UNSUPPORTED;
   }
-  return BN == 256 ? tcs::launch<256>(g, ma, mbh, mbl, mc, S, kb_per, s)
-                   : tcs::launch<128>(g, ma, mbh, mbl, mc, S, kb_per, s);
+  return BN == 256 ? tcs::launch<256>(g, ma, mbh, mbl, mc, S, kb_per, parts, part_stride, ldc, s)
+                   : tcs::launch<128>(g, ma, mbh, mbl, mc, S, kb_per, parts, part_stride, ldc, s);
 }
 
 }  // namespace pfb

@@ -19,8 +19,10 @@ from paper_1903_04243_b200 import _native as N  # noqa: E402
 from paper_1903_04243_b200.executor import DArray  # noqa: E402
 from paper_1903_04243_b200.tensor import DType  # noqa: E402
 
-PAIR_NAMES = ["entry", "pdl_done", "tma0_issued", "mma0_issued", "tile0_out", "tile1_out",
+PAIR_PARTS_NAMES = ["entry", "pdl_done", "acc_full", "epilogue_done", "cta_done"]
+NAMES = ["entry", "pdl_done", "tma0_issued", "mma0_issued", "tile0_out", "tile1_out",
               "tile2_out", "tile3_out", "tile4_out", "tile5_out", "tile6_out", "tile7_out", "cta_done"]
+PARTS_NAMES = ["entry", "pdl_done", "acc_full", "epilogue_done", "cta_done"]
 NAMES = ["entry", "pdl_done", "prologue", "tma0_issued", "stage0_landed", "mma0_issued",
          "last_commit", "acc0_ready", "epilogue_done", "cta_done", "tmem_freed"]
 
@@ -88,6 +90,8 @@ def main():
         lib.pfb_debug_tc_trace(buf)
         t0 = buf[0]
         names = PAIR_NAMES if args.force in (5, 6) else NAMES
+        if args.parts:
+            names = PARTS_NAMES
         print(f"rep {rep} rc={rc}: " + "  ".join(
             f"{nm}={(buf[i] - t0) / 1e3:.2f}" for i, nm in enumerate(names) if buf[i] and buf[i] >= t0))
         st_ = [buf[192 + i] for i in range(160) if buf[192 + i] >= t0]
@@ -97,6 +101,14 @@ def main():
             print("   per-CTA start (us): min %.2f med %.2f max %.2f | end: min %.2f med %.2f max %.2f (n=%d)" % (
                 (min(st_) - t0) / 1e3, (S_.median(st_) - t0) / 1e3, (max(st_) - t0) / 1e3,
                 (min(en_) - t0) / 1e3, (S_.median(en_) - t0) / 1e3, (max(en_) - t0) / 1e3, len(en_)))
+        if args.parts:
+            print("   kb  tma_issue  landed  mma_issue")
+            for kb in range(8):
+                v = [buf[16 + kb], buf[48 + kb], buf[32 + kb]]
+                if not v[0] or v[0] < t0:
+                    break
+                print("   %2d  " % kb + "  ".join("%8.2f" % ((x - t0) / 1e3) for x in v))
+            continue
         if args.force not in (5, 6):
             cyc = [buf[96 + kb] for kb in range(16)]
             print("   mma_start deltas (SM cycles):", [int(cyc[i + 1] - cyc[i]) for i in range(15) if cyc[i + 1]])
