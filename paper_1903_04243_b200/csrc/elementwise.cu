@@ -837,9 +837,11 @@ static int fused_impl(int32_t n_in, const pfb_tensor* ins, int32_t n_steps,
   const bool small = n < (int64_t)0x7fffffff;
   const int ir = L.rank - 1;
   static const bool scalar_only = getenv_flag("PFB_FUSED_SCALAR");
-  // tiny tensors (per-example scalars): one element per thread so the
-  // program's latency chain runs on 4x the warps
-  const bool v4 = L.shape[ir] % 4 == 0 && !scalar_only && n >= 4096;
+  // below ~1M elements (L2-resident per-step tensors: the LSTM cell, 131k
+  // elements) one element per thread: the program's latency chain runs on 4x
+  // the warps (cfg4 step 2.76 -> 2.58 ms); 4 per thread (128-bit accesses)
+  // where the launch is HBM-bound
+  const bool v4 = L.shape[ir] % 4 == 0 && !scalar_only && n >= (int64_t)1 << 20;
   // per-operand feed mode; the outputs share operand 0's (all must be aligned)
   FeedModes modes = 0;
   for (int o = 0; o <= n_in; ++o) {
@@ -992,26 +994,37 @@ struct ThinCat {
   int64_t rs0[kThinCat], rs1[kThinCat];  // per input: outer / inner row strides
 };
 
+constexpr int kThinRows = 128;  // rows per block (4 x 32: 16 loads in flight per thread)
+
 template <typename T>
 __global__ void __launch_bounds__(256) concat_thin_kernel(ThinCat d, T* out) {
   pdl_enter();
-  __shared__ T tile[32][33];
+  __shared__ T tile[32][kThinRows + 1];
   const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
-  const int64_t r0 = (int64_t)blockIdx.x * 32;
+  const int64_t r0 = (int64_t)blockIdx.x * kThinRows;
   const int c0 = blockIdx.y * 32;
-  const int64_t r = r0 + tx;
-  const int64_t ro = r / d.R1, ri = r - ro * d.R1;
+  T v[4][kThinRows / 32];
 #pragma unroll
-  for (int i = ty; i < 32; i += 8) {
-    const int c = c0 + i;
-    if (c < d.n && r < d.R)
-      tile[i][tx] = __ldg(reinterpret_cast<const T*>(d.x[c]) + ro * d.rs0[c] + ri * d.rs1[c]);
+  for (int q = 0; q < kThinRows / 32; ++q) {
+    const int64_t r = r0 + q * 32 + tx;
+    const int64_t ro = r / d.R1, ri = r - ro * d.R1;
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const int c = c0 + ty + 8 * k;
+      v[k][q] = (c < d.n && r < d.R)
+                    ? __ldg(reinterpret_cast<const T*>(d.x[c]) + ro * d.rs0[c] + ri * d.rs1[c])
+                    : T(0);
+    }
   }
-  __syncthreads();
 #pragma unroll
-  for (int i = ty; i < 32; i += 8) {
+  for (int q = 0; q < kThinRows / 32; ++q)
+#pragma unroll
+    for (int k = 0; k < 4; ++k) tile[ty + 8 * k][q * 32 + tx] = v[k][q];
+  __syncthreads();
+  const int c = c0 + tx;
+#pragma unroll 4
+  for (int i = ty; i < kThinRows; i += 8) {
     const int64_t rr = r0 + i;
-    const int c = c0 + tx;
     if (c < d.n && rr < d.R) out[rr * d.ost_row + d.off + c] = tile[tx][i];
   }
 }
@@ -1158,7 +1171,7 @@ static bool concat_thin(int32_t n, const pfb_tensor* xs, int32_t axis, pfb_tenso
       d.x[j] = xs[base + j].data;
       rows2(&xs[base + j], rank, &d.rs0[j], &d.rs1[j]);
     }
-    dim3 grid((unsigned)((d.R + 31) / 32), (unsigned)((d.n + 31) / 32));
+    dim3 grid((unsigned)((d.R + kThinRows - 1) / kThinRows), (unsigned)((d.n + 31) / 32));
     switch (out->dtype) {
       case PFB_F32: launch(concat_thin_kernel<float>, grid, 256, 0, s, d, (float*)out->data); break;
       case PFB_I64: launch(concat_thin_kernel<int64_t>, grid, 256, 0, s, d, (int64_t*)out->data); break;
