@@ -251,6 +251,7 @@ pair_kernel(const __grid_constant__ CUtensorMap map_ah, const __grid_constant__ 
         for (int c = 0; c < nchunks; ++c, ++gc) {
           const int buf = gc & 1;
           if (gc >= 2) mbar_wait_cluster(&acc_empty[buf], ((gc >> 1) - 1) & 1);
+          if (gc < 16) pstamp(p, 16 + gc);
           asm volatile("tcgen05.fence::after_thread_sync;");
           const uint32_t tmem_d = tmem_base + (uint32_t)(buf * BN);
           const int kb_beg = c * chunk, kb_end = min(nk, kb_beg + chunk);
@@ -279,6 +280,7 @@ pair_kernel(const __grid_constant__ CUtensorMap map_ah, const __grid_constant__ 
             mma_commit_pair(&empty[s]);
           }
           mma_commit_pair(&acc_full[buf]);
+          if (gc < 16) pstamp(p, 32 + gc);
         }
       }
     }
@@ -427,6 +429,7 @@ pair_kernel(const __grid_constant__ CUtensorMap map_ah, const __grid_constant__ 
         tile_of(u, &bz, &m0, &n0);
         const int buf = gc & 1;
         mbar_wait(&acc_full[buf], (gc >> 1) & 1);
+        if (et == 0 && gc < 16) pstamp(p, 48 + gc);
         asm volatile("tcgen05.fence::after_thread_sync;");
         const int row0 = m0 + quarter * 32;
         const float alpha = alpha_of(bz, row0 + lane);

@@ -2,10 +2,11 @@
 //
 //   parts[s] = A[:, Ks] @ B[Ks, :]  (+ bias in s = 0)     s = 0..S-1
 //
-// One CTA per (128-row tile, BN-column tile, k-split).  Each split's whole K
-// range (<= 8 k-blocks of 32) accumulates in TMEM -- no chunked register
-// accumulation, no reduction: the consumer (a fused elementwise group) sums
-// the S partials as it loads them.  This is the shape of the LSTM's per-step
+// One CTA per (128-row tile, BN-column tile, k-split).  Each split's K range
+// (<= 8 k-blocks of 32) accumulates in 64-deep TMEM chunks summed in fp32
+// registers (double-buffered TMEM: chunk c drains while c+1 multiplies); no
+// reduction across splits: the consumer (a fused elementwise group) sums the
+// S partials as it loads them.  This is the shape of the LSTM's per-step
 // GEMMs (M = 256 examples, 128 of them per step, reference bench cell /
 // BASELINE cfg4), where the reduced GEMM spent ~30% of its time in the
 // cluster reduction (barriers waiting on the slowest CTA of the cluster, then
@@ -18,8 +19,10 @@
 // 3xTF32 as in gemm_tcgen05.cu: A raw (the tensor core truncates it: hi =
 // trunc(x); lo = rn(x - hi) written beside it in smem by the split warps),
 // B as pre-split RN hi/lo planes; products A_hi B_hi + A_hi B_lo + A_lo B_hi.
-// TMEM accumulation over <= 256 of K stays at fp32-SIMT accuracy
-// (tests/test_gpu_parts.py).
+// (Whole-split accumulation in TMEM -- 256 of K -- measured 2.9e-5 abs error
+// on cfg4's gradients, outside atol 1e-5: the in-TMEM accumulation truncates;
+// the 64-deep chunks bring it back to SIMT-fp32 level, tests/test_gpu_parts.py,
+// tests/test_gpu_bench_scale.py.)
 //
 // Warps: 0 TMA producer, 1 TMEM allocator + MMA issuer, 2..9 split A tiles,
 // then drain TMEM (warp w: lanes 32*(w%4).., columns half (w-2)/4) through a
@@ -41,7 +44,8 @@ using namespace tc;
 constexpr int BM = 128, BK = 32, UMMA_K = 8;
 constexpr int A_BYTES = BM * BK * 4;  // 16 KB raw A tile (lo beside it)
 constexpr int WARPS = 10, NUM_THREADS = 32 * WARPS, SPLIT_WARPS = 8;
-constexpr int kMaxKb = 8;             // k-blocks per split (K <= 256 in TMEM)
+constexpr int kMaxKb = 8;             // k-blocks per split
+constexpr int CHUNK = 2;              // k-blocks per TMEM chunk (64 deep, then fp32 registers)
 
 template <int BN>
 struct Cfg {
@@ -49,6 +53,7 @@ struct Cfg {
   static constexpr int STAGE = 2 * A_BYTES + 2 * B_BYTES;
   static constexpr int STAGES = BN == 256 ? 2 : 3;
   static constexpr int SMEM = STAGES * STAGE + 1024 + 256;
+  static_assert(2 * BN <= 512, "double-buffered TMEM chunks");
   static constexpr uint32_t IDESC = (1u << 4) | (2u << 7) | (2u << 10) |
                                     ((uint32_t)(BN >> 3) << 17) | ((uint32_t)(BM >> 4) << 24);
   static_assert(SMEM <= 232448, "shared memory");
@@ -86,8 +91,9 @@ parts_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ 
   uint64_t* full = bars;                  // TMA -> split warps
   uint64_t* ready = bars + C::STAGES;     // split -> MMA
   uint64_t* empty = bars + 2 * C::STAGES; // MMA -> TMA
-  uint64_t* acc_full = bars + 3 * C::STAGES;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_full + 1);
+  uint64_t* acc_full = bars + 3 * C::STAGES;  // [2] MMA -> drain warps (chunk done)
+  uint64_t* acc_empty = acc_full + 2;         // [2] drain warps -> MMA
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_empty + 2);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int u = blockIdx.x;
@@ -95,6 +101,7 @@ parts_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ 
   const int m0 = (t / p.ntn) * BM, n0 = (t % p.ntn) * BN;
   const int kb0 = s_idx * p.kb_per, kb1 = min(p.nk, kb0 + p.kb_per);
   const int nkb = kb1 - kb0;
+  const int nch = (nkb + CHUNK - 1) / CHUNK;  // TMEM chunks (64 deep) of this split
   auto stage = [&](int s) { return smem + s * C::STAGE; };
 
   if (threadIdx.x == 0) {
@@ -103,7 +110,10 @@ parts_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ 
       mbar_init(&ready[s], SPLIT_WARPS);
       mbar_init(&empty[s], 1);
     }
-    mbar_init(acc_full, 1);
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(&acc_full[b], 1);
+      mbar_init(&acc_empty[b], SPLIT_WARPS);
+    }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&map_a)) : "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&map_bh)) : "memory");
@@ -111,7 +121,7 @@ parts_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ 
   }
   if (warp == 1) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
-                     smem_u32(tmem_slot)), "r"(BN));
+                     smem_u32(tmem_slot)), "r"(2 * BN));
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
   }
   asm volatile("tcgen05.fence::before_thread_sync;");
@@ -138,84 +148,103 @@ parts_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ 
       }
     }
   } else if (warp == 1) {
-    for (int g = 0; g < nkb; ++g) {
-      const int s = g % C::STAGES;
-      mbar_wait(&ready[s], (g / C::STAGES) & 1);
+    // chunk c accumulates k-blocks [c*CHUNK, ..) into TMEM buffer c&1 (the
+    // tensor core's in-TMEM accumulation truncates: 64-deep chunks summed in
+    // fp32 registers keep the result at SIMT-fp32 accuracy, gemm_tcgen05.cu)
+    int g = 0;
+    for (int c = 0; c < nch; ++c) {
+      const int buf = c & 1;
+      if (c >= 2) mbar_wait(&acc_empty[buf], ((c >> 1) - 1) & 1);
       asm volatile("tcgen05.fence::after_thread_sync;");
-      const uint64_t ah = smem_desc_sw128(smem_u32(stage(s)));
-      const uint64_t al = smem_desc_sw128(smem_u32(stage(s) + A_BYTES));
-      const uint64_t bh = smem_desc_sw128(smem_u32(stage(s) + 2 * A_BYTES));
-      const uint64_t bl = smem_desc_sw128(smem_u32(stage(s) + 2 * A_BYTES + C::B_BYTES));
-      if (elect_one()) {
-        if (g < 8) pstamp(p, 32 + g);
+      const uint32_t td = tmem + (uint32_t)(buf * BN);
+      const int gend = min(nkb, (c + 1) * CHUNK);
+      for (; g < gend; ++g) {
+        const int s = g % C::STAGES;
+        mbar_wait(&ready[s], (g / C::STAGES) & 1);
+        asm volatile("tcgen05.fence::after_thread_sync;");
+        const uint64_t ah = smem_desc_sw128(smem_u32(stage(s)));
+        const uint64_t al = smem_desc_sw128(smem_u32(stage(s) + A_BYTES));
+        const uint64_t bh = smem_desc_sw128(smem_u32(stage(s) + 2 * A_BYTES));
+        const uint64_t bl = smem_desc_sw128(smem_u32(stage(s) + 2 * A_BYTES + C::B_BYTES));
+        if (elect_one()) {
+          if (g < 8) pstamp(p, 32 + g);
 #pragma unroll
-        for (int k = 0; k < BK / UMMA_K; ++k) {
-          const uint64_t d = (UMMA_K * 4) >> 4;  // +32 B inside the swizzle row
-          const uint32_t acc = (g > 0 || k > 0) ? 1u : 0u;
-          mma_tf32(tmem, ah + d * k, bh + d * k, C::IDESC, acc);
-          mma_tf32(tmem, ah + d * k, bl + d * k, C::IDESC, 1u);
-          mma_tf32(tmem, al + d * k, bh + d * k, C::IDESC, 1u);
+          for (int k = 0; k < BK / UMMA_K; ++k) {
+            const uint64_t d = (UMMA_K * 4) >> 4;  // +32 B inside the swizzle row
+            const uint32_t acc = (g > c * CHUNK || k > 0) ? 1u : 0u;
+            mma_tf32(td, ah + d * k, bh + d * k, C::IDESC, acc);
+            mma_tf32(td, ah + d * k, bl + d * k, C::IDESC, 1u);
+            mma_tf32(td, al + d * k, bh + d * k, C::IDESC, 1u);
+          }
+          mma_commit(&empty[s]);
+          if (g == gend - 1) mma_commit(&acc_full[buf]);
         }
-        mma_commit(&empty[s]);
-        if (g == nkb - 1) mma_commit(acc_full);
+        __syncwarp();
       }
-      __syncwarp();
     }
   } else {
     const int et = threadIdx.x - 64;  // 0..255
-    for (int g = 0; g < nkb; ++g) {
-      const int s = g % C::STAGES;
-      mbar_wait(&full[s], (g / C::STAGES) & 1);
-      if (et == 0 && g < 8) pstamp(p, 48 + g);
-      split_tf32_smem(smem_u32(stage(s)), smem_u32(stage(s) + A_BYTES), A_BYTES / 16, et,
-                      32 * SPLIT_WARPS);
-      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&ready[s]);
-    }
-    // ---- epilogue: TMEM -> (+ bias) -> swizzled 32x32 block -> TMA store;
-    // one staging block per 32 columns (the stage memory is idle now), so no
-    // store waits for an earlier one to drain
-    constexpr int NB = BN / 64;  // 32-column blocks per warp
     const int quarter = warp & 3, half = (warp - 2) >> 2;
-    float* blk0 = reinterpret_cast<float*>(smem) + (warp - 2) * 1024 * NB;
     const int row0 = m0 + quarter * 32;
+    constexpr int DC = BN / 2;  // accumulator columns per warp
+    float acc[DC];
+    // split 0 starts from the bias (row-broadcast or full matrix)
     const bool add_bias = p.bias != nullptr && s_idx == 0;
-    float bv[NB];  // bias of column (block col0) + lane (row-broadcast bias)
 #pragma unroll
-    for (int b = 0; b < NB; ++b) {
-      const int col = n0 + half * (BN / 2) + 32 * b + lane;
-      bv[b] = (add_bias && p.sxm == 0 && col < p.N) ? __ldg(p.bias + (int64_t)col * p.sxn) : 0.f;
+    for (int j = 0; j < DC; ++j) {
+      const int col = n0 + half * DC + j;
+      acc[j] = (add_bias && row0 + lane < p.M && col < p.N)
+                   ? __ldg(p.bias + (int64_t)(row0 + lane) * p.sxm + (int64_t)col * p.sxn)
+                   : 0.f;
     }
-    mbar_wait(acc_full, 0);
+    int g = 0;
+    auto drain = [&](int c) {
+      const int buf = c & 1;
+      mbar_wait(&acc_full[buf], (c >> 1) & 1);
+      asm volatile("tcgen05.fence::after_thread_sync;");
+#pragma unroll
+      for (int cc = 0; cc < DC; cc += 32) {
+        uint32_t v[32];
+        tmem_ld32(tmem + ((uint32_t)(quarter * 32) << 16) + (uint32_t)(buf * BN + half * DC + cc), v);
+        asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+        for (int j = 0; j < 32; ++j) acc[cc + j] += __uint_as_float(v[j]);
+      }
+      asm volatile("tcgen05.fence::before_thread_sync;");
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&acc_empty[buf]);
+    };
+    // split chunk c's stages, then drain chunk c-1 (the MMA works on chunk
+    // c-1 while chunk c is split)
+    for (int c = 0; c < nch; ++c) {
+      const int gend = min(nkb, (c + 1) * CHUNK);
+      for (; g < gend; ++g) {
+        const int s = g % C::STAGES;
+        mbar_wait(&full[s], (g / C::STAGES) & 1);
+        if (et == 0 && g < 8) pstamp(p, 48 + g);
+        split_tf32_smem(smem_u32(stage(s)), smem_u32(stage(s) + A_BYTES), A_BYTES / 16, et,
+                        32 * SPLIT_WARPS);
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&ready[s]);
+      }
+      if (c > 0) drain(c - 1);
+    }
+    drain(nch - 1);
     if (et == 0) pstamp(p, 2);
-    asm volatile("tcgen05.fence::after_thread_sync;");
+    // ---- epilogue: registers -> swizzled 32x32 blocks (one per 32 columns;
+    // the stage memory is idle now) -> TMA store of parts[s_idx]
+    constexpr int NB = DC / 32;
+    float* blk0 = reinterpret_cast<float*>(smem) + (warp - 2) * 1024 * NB;
 #pragma unroll
     for (int b = 0; b < NB; ++b) {
-      const int cc = 32 * b;
-      const int col0 = n0 + half * (BN / 2) + cc;
+      const int col0 = n0 + half * DC + 32 * b;
       float* blk = blk0 + 1024 * b;
-      uint32_t v[32];
-      tmem_ld32(tmem + ((uint32_t)(quarter * 32) << 16) + (uint32_t)(half * (BN / 2) + cc), v);
-      asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 #pragma unroll
-      for (int q = 0; q < 8; ++q) {
-        float x[4];
-#pragma unroll
-        for (int j = 0; j < 4; ++j) {
-          x[j] = __uint_as_float(v[4 * q + j]);
-          if (add_bias) {
-            if (p.sxm == 0) {
-              x[j] += __shfl_sync(0xffffffffu, bv[b], 4 * q + j);
-            } else if (row0 + lane < p.M && col0 + 4 * q + j < p.N) {
-              x[j] += __ldg(p.bias + (int64_t)(row0 + lane) * p.sxm +
-                            (int64_t)(col0 + 4 * q + j) * p.sxn);
-            }
-          }
-        }
+      for (int q = 0; q < 8; ++q)
         *reinterpret_cast<float4*>(blk + lane * 32 + 4 * (q ^ (lane & 7))) =
-            make_float4(x[0], x[1], x[2], x[3]);
-      }
+            make_float4(acc[32 * b + 4 * q], acc[32 * b + 4 * q + 1], acc[32 * b + 4 * q + 2],
+                        acc[32 * b + 4 * q + 3]);
       if (p.direct) {
         // each store instruction: 4 rows x 128 contiguous bytes
         __syncwarp();
@@ -253,7 +282,7 @@ parts_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ 
   }
   if (warp == 1) {
     asm volatile("tcgen05.fence::after_thread_sync;");
-    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(BN));
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(2 * BN));
   }
 }
 

@@ -952,13 +952,13 @@ class Executor:
         for r in roots:
             remaining[r] = remaining.get(r, 0) + 1
         env = {}
-        saved_ctx, saved_parts = self._const_ctx, self._parts_ok
+        saved = self._const_ctx, self._parts_ok
         self._const_ctx = (g, plan.const_nodes)
         self._parts_ok = plan.parts_ok
         try:
             self._run_nodes(g, plan, env, binder, feeds, remaining)
         finally:
-            self._const_ctx, self._parts_ok = saved_ctx, saved_parts
+            self._const_ctx, self._parts_ok = saved
         for r in roots:  # (F15 never applies to outputs; defensive)
             if isinstance(env.get(r), DArray) and env[r].parts is not None:
                 env[r] = self._reduce_parts(env[r])

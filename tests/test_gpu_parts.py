@@ -150,3 +150,4 @@ def test_cfg4_partials_match_reduced_executor(env, monkeypatch):
     for g_, w_ in zip(got, want):
         np.testing.assert_allclose(np.asarray(g_.data, np.float64), np.asarray(w_.data, np.float64),
                                    rtol=RTOL, atol=ATOL)
+

@@ -34,17 +34,19 @@ def main():
     ap.add_argument("--planes", action="store_true")
     ap.add_argument("--graph", type=int, default=0)
     ap.add_argument("--parts", action="store_true", help="split-K partials (pfb_matmul_parts)")
+    ap.add_argument("--batch", type=int, default=1, help="batched GEMM (the F2 shape: --batch 256)")
     args = ap.parse_args()
     m, n, k = args.shape[:3]
     lib = N.lib()
     lib.pfb_debug_tc_trace.argtypes = [ctypes.POINTER(ctypes.c_ulonglong)]
     dev = torch.device("cuda")
-    a = torch.randn(m, k, device=dev)
-    bt = torch.randn(n, k, device=dev)
-    c = torch.empty(m, n, device=dev)
+    bs = args.batch
+    a = torch.randn(*((bs,) if bs > 1 else ()), m, k, device=dev)
+    bt = torch.randn(*((bs,) if bs > 1 else ()), n, k, device=dev)
+    c = torch.empty(*((bs,) if bs > 1 else ()), m, n, device=dev)
     A = DArray(a.reshape(-1), 0, a.shape, a.stride(), DType.F64)
     Bt = DArray(bt.reshape(-1), 0, bt.shape, bt.stride(), DType.F64)
-    B = Bt.view([k, n], [1, k])
+    B = Bt.view([k, n], [1, k]) if bs == 1 else Bt.view([bs, k, n], [n * k, 1, k])
     C = DArray(c.reshape(-1), 0, c.shape, c.stride(), DType.F64)
     s = torch.cuda.current_stream().cuda_stream
     ad, bd, cd = A.desc(), B.desc(), C.desc()
@@ -109,6 +111,14 @@ def main():
                     break
                 print("   %2d  " % kb + "  ".join("%8.2f" % ((x - t0) / 1e3) for x in v))
             continue
+        if args.force in (5, 6):
+            print("   tile  mma_start  mma_done  drain_start  drained")
+            for t in range(16):
+                v = [buf[16 + t], buf[32 + t], buf[48 + t], buf[4 + t] if t < 8 else 0]
+                if not v[0] or v[0] < t0:
+                    break
+                print("   %2d  " % t + "  ".join("%8.2f" % ((x - t0) / 1e3) if x >= t0 else "   -    "
+                                                for x in v))
         if args.force not in (5, 6):
             cyc = [buf[96 + kb] for kb in range(16)]
             print("   mma_start deltas (SM cycles):", [int(cyc[i + 1] - cyc[i]) for i in range(15) if cyc[i + 1]])
