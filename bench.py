@@ -325,9 +325,11 @@ def roofline_of_step(ex, step_fn, flush, dev, ms_per_step):
     """One instrumented eager step records every launch (entry point, exact
     arguments, algorithmic bytes/flops, CUDA events on the executing stream).
     The kernel kind with the largest share of that step is the dominant one;
-    each of its launches is then re-issued alone between CUDA events (L2
-    flushed before each) and achieved = its algorithmic work summed over the
-    step's launches of that kind / their summed durations."""
+    each of its launches is then re-issued alone between CUDA events, warm
+    (as inside the step: the per-step GEMMs' weights stay in L2 across the 64
+    steps; the step's timed region flushes L2 only between steps), and
+    achieved = its algorithmic work summed over the step's launches of that
+    kind / their summed durations."""
     import torch
     hbm, tflops, src = load_peaks()
     tc_peak = tflops / 2 / 3  # fp32-accurate tensor-core GEMM: TF32 dense ~ bf16/2, 3 passes
@@ -348,8 +350,8 @@ def roofline_of_step(ex, step_fn, flush, dev, ms_per_step):
     for r in same[:256]:
         fn, fargs = r[5], r[6]
         d = []
+        fn(*fargs)
         for _ in range(3):
-            flush.zero_()
             s_ev, e_ev = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             s_ev.record()
             fn(*fargs)

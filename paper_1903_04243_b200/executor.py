@@ -1340,7 +1340,7 @@ def _matmul_parts(ex, node, a, b, bias, planes):
     flops = 2 * _numel(shape) * a.shape[-1]
     ex._call(ex._lib.pfb_matmul_parts, ad, bd, stacked.desc(),
              ctypes.byref(xd) if xd is not None else None, planes, wp, wn, ex._stream,
-             what="matmul", work=(_abytes(a, b, stacked) + (_abytes(bias) if bias is not None else 0),
+             what="matmul_parts", work=(_abytes(a, b, stacked) + (_abytes(bias) if bias is not None else 0),
                                   flops))
     ex.parts_made += 1
     return DArray(stacked.buf, 0, shape, _dense_strides(shape), a.dtype, (S, _numel(shape)))

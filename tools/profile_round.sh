@@ -37,6 +37,6 @@ unset PFB_GEMM_TUNE_FILE
 # GEMMs); capture that shape in isolation with its autotuned path (the
 # CTA-pair kernel, TMEM-resident mode, raw feed: --force 6)
 timeout 900 ncu -f --set full --clock-control none --import-source on -k regex:pair_kernel -c 1 \
-  -o $OUT/full_cfg4 python tools/gemm_probe.py --force 6 --shape 1024 2048 64 256 --iters 1 > $OUT/full_cfg4.log 2>&1
-python tools/ncu_summary.py $OUT/full_cfg4.ncu-rep --json $OUT/full_cfg4.json > $OUT/full_cfg4.txt 2>&1
+  -o $OUT/full_cfg4_f2 python tools/gemm_probe.py --force 6 --shape 1024 2048 64 256 --iters 1 > $OUT/full_cfg4_f2.log 2>&1
+python tools/ncu_summary.py $OUT/full_cfg4_f2.ncu-rep --json $OUT/full_cfg4_f2.json > $OUT/full_cfg4_f2.txt 2>&1
 ls -la $OUT
