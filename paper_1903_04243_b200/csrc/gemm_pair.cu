@@ -303,6 +303,7 @@ pair_kernel(const __grid_constant__ CUtensorMap map_ah, const __grid_constant__ 
                           32 * SPLIT_WARPS);
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
         named_bar(2, 32 * SPLIT_WARPS);
+        if (st_ == 0 && kb == nk - 1 && g / nk < 16) pstamp(p, 64 + g / nk);
         if (st_ == 0) {
           if (rank == 0) mbar_arrive(&ready[s]);
           else mbar_arrive_remote(&ready[s], 0);

@@ -19,8 +19,7 @@ from paper_1903_04243_b200 import _native as N  # noqa: E402
 from paper_1903_04243_b200.executor import DArray  # noqa: E402
 from paper_1903_04243_b200.tensor import DType  # noqa: E402
 
-PAIR_PARTS_NAMES = ["entry", "pdl_done", "acc_full", "epilogue_done", "cta_done"]
-NAMES = ["entry", "pdl_done", "tma0_issued", "mma0_issued", "tile0_out", "tile1_out",
+PAIR_NAMES = ["entry", "pdl_done", "tma0_issued", "mma0_issued", "tile0_out", "tile1_out",
               "tile2_out", "tile3_out", "tile4_out", "tile5_out", "tile6_out", "tile7_out", "cta_done"]
 PARTS_NAMES = ["entry", "pdl_done", "acc_full", "epilogue_done", "cta_done"]
 NAMES = ["entry", "pdl_done", "prologue", "tma0_issued", "stage0_landed", "mma0_issued",
@@ -112,9 +111,9 @@ def main():
                 print("   %2d  " % kb + "  ".join("%8.2f" % ((x - t0) / 1e3) for x in v))
             continue
         if args.force in (5, 6):
-            print("   tile  mma_start  mma_done  drain_start  drained")
+            print("   tile  mma_start  mma_done  drain_start  drained  split_done")
             for t in range(16):
-                v = [buf[16 + t], buf[32 + t], buf[48 + t], buf[4 + t] if t < 8 else 0]
+                v = [buf[16 + t], buf[32 + t], buf[48 + t], buf[4 + t] if t < 8 else 0, buf[64 + t]]
                 if not v[0] or v[0] < t0:
                     break
                 print("   %2d  " % t + "  ".join("%8.2f" % ((x - t0) / 1e3) if x >= t0 else "   -    "
