@@ -235,6 +235,17 @@ int64_t pfb_matmul_parts_workspace(const pfb_tensor* a, const pfb_tensor* b, con
 int pfb_matmul_parts(const pfb_tensor* a, const pfb_tensor* b, pfb_tensor* parts,
                      const pfb_tensor* bias, const void* b_planes, void* ws, int64_t ws_bytes,
                      void* stream);
+/* the dual-operand form (a1 @ b1 + a2 @ b2, as pfb_matmul_dual2): the
+ * k-splits run over both K ranges back to back */
+int pfb_matmul_dual_parts_count(const pfb_tensor* a1, const pfb_tensor* b1, const pfb_tensor* a2,
+                                const pfb_tensor* b2, const pfb_tensor* out);
+int64_t pfb_matmul_dual_parts_workspace(const pfb_tensor* a1, const pfb_tensor* b1,
+                                        const pfb_tensor* a2, const pfb_tensor* b2,
+                                        const pfb_tensor* out);
+int pfb_matmul_dual_parts(const pfb_tensor* a1, const pfb_tensor* b1, const pfb_tensor* a2,
+                          const pfb_tensor* b2, pfb_tensor* parts, const pfb_tensor* bias,
+                          const void* b1_planes, const void* b2_planes, void* ws,
+                          int64_t ws_bytes, void* stream);
 int pfb_matmul_dual2(const pfb_tensor* a1, const pfb_tensor* b1, const pfb_tensor* a2,
                      const pfb_tensor* b2, pfb_tensor* out, const pfb_tensor* bias, int32_t act,
                      const void* b1_planes, const void* b2_planes, int32_t force_path, void* ws,

@@ -75,6 +75,9 @@ _SIGNATURES = {
     "pfb_matmul_parts_count": ([_P, _P, _P], ctypes.c_int),
     "pfb_matmul_parts_workspace": ([_P, _P, _P], ctypes.c_int64),
     "pfb_matmul_parts": ([_P, _P, _P, _P, _vp, _vp, _i64, _vp], ctypes.c_int),
+    "pfb_matmul_dual_parts_count": ([_P, _P, _P, _P, _P], ctypes.c_int),
+    "pfb_matmul_dual_parts_workspace": ([_P, _P, _P, _P, _P], ctypes.c_int64),
+    "pfb_matmul_dual_parts": ([_P, _P, _P, _P, _P, _P, _vp, _vp, _vp, _i64, _vp], ctypes.c_int),
     "pfb_matmul_dual2": ([_P, _P, _P, _P, _P, _P, _i32, _vp, _vp, _i32, _vp, _i64, _vp],
                          ctypes.c_int),
     "pfb_matmul_dual": ([_P, _P, _P, _P, _P, _P, _i32, _i32, _vp, _i64, _vp], ctypes.c_int),

@@ -535,6 +535,58 @@ extern "C" int pfb_matmul_parts(const pfb_tensor* a, const pfb_tensor* b, pfb_te
   }
   const int S = gemm_parts_count(g);
   if (S < 1 || parts->shape[0] != S) return PFB_E_SHAPE;
-  return gemm_parts(g, S, (float*)parts->data, parts->stride[0], parts->stride[1], ws, ws_bytes,
+  return gemm_parts(g, nullptr, S, (float*)parts->data, parts->stride[0], parts->stride[1], ws, ws_bytes,
                     as_stream(stream));
+}
+
+// Dual-operand form (a1 @ b1 + a2 @ b2, passes.fuse_dual_matmuls): the k-splits
+// run over both K ranges back to back (cfg5's RNN cell x_t Wx + h Wh, whose
+// row sums and select consume the partials).
+static int dual_parts_args(const pfb_tensor* a1, const pfb_tensor* b1, const pfb_tensor* a2,
+                           const pfb_tensor* b2, const pfb_tensor* out, const void* p1,
+                           const void* p2, GemmArgs* g1, GemmArgs* g2) {
+  if (int e = parts_args(a1, b1, out, p1, g1)) return e;
+  return parts_args(a2, b2, out, p2, g2);
+}
+
+extern "C" int pfb_matmul_dual_parts_count(const pfb_tensor* a1, const pfb_tensor* b1,
+                                           const pfb_tensor* a2, const pfb_tensor* b2,
+                                           const pfb_tensor* out) {
+  static const bool off = getenv_flag("PFB_NO_PARTS");
+  GemmArgs g1, g2;
+  if (off || dual_parts_args(a1, b1, a2, b2, out, nullptr, nullptr, &g1, &g2)) return 0;
+  return gemm_parts_count(g1, &g2);
+}
+
+extern "C" int64_t pfb_matmul_dual_parts_workspace(const pfb_tensor* a1, const pfb_tensor* b1,
+                                                   const pfb_tensor* a2, const pfb_tensor* b2,
+                                                   const pfb_tensor* out) {
+  GemmArgs g1, g2;
+  if (dual_parts_args(a1, b1, a2, b2, out, nullptr, nullptr, &g1, &g2)) return 0;
+  return gemm_parts_workspace(g1, &g2);
+}
+
+extern "C" int pfb_matmul_dual_parts(const pfb_tensor* a1, const pfb_tensor* b1,
+                                     const pfb_tensor* a2, const pfb_tensor* b2,
+                                     pfb_tensor* parts, const pfb_tensor* bias,
+                                     const void* b1_planes, const void* b2_planes, void* ws,
+                                     int64_t ws_bytes, void* stream) {
+  if (parts->rank != 3 || parts->dtype != PFB_F32 || parts->stride[2] != 1) return PFB_E_SHAPE;
+  pfb_tensor out = *parts;
+  out.rank = 2;
+  out.shape[0] = parts->shape[1]; out.shape[1] = parts->shape[2];
+  out.stride[0] = parts->stride[1]; out.stride[1] = parts->stride[2];
+  GemmArgs g1, g2;
+  if (int e = dual_parts_args(a1, b1, a2, b2, &out, b1_planes, b2_planes, &g1, &g2)) return e;
+  if (bias) {
+    if (bias->dtype != PFB_F32) return PFB_E_DTYPE;
+    int64_t st[2];
+    if (!broadcast_strides(bias, 2, out.shape, st)) return PFB_E_SHAPE;
+    g1.bias = (const float*)bias->data;
+    g1.sxb = 0; g1.sxm = st[0]; g1.sxn = st[1];
+  }
+  const int S = gemm_parts_count(g1, &g2);
+  if (S < 1 || parts->shape[0] != S) return PFB_E_SHAPE;
+  return gemm_parts(g1, &g2, S, (float*)parts->data, parts->stride[0], parts->stride[1], ws,
+                    ws_bytes, as_stream(stream));
 }

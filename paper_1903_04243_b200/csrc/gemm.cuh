@@ -93,10 +93,11 @@ bool gemm_tcgen05_profitable(const GemmArgs& g);  // size heuristic for auto
 int gemm_tcgen05_pair(const GemmArgs& g, void* ws, int64_t ws_bytes, cudaStream_t s, int variant);
 // split-K partials GEMM (gemm_parts.cu): S k-splits of a batch-1 GEMM written
 // to parts + s*part_stride (row stride ldc), bias in split 0, no reduction
-int gemm_parts_count(const GemmArgs& g);  // S (0: not applicable)
-int64_t gemm_parts_workspace(const GemmArgs& g);
-int gemm_parts(const GemmArgs& g, int S, float* parts, int64_t part_stride, int64_t ldc, void* ws,
-               int64_t ws_bytes, cudaStream_t s);
+// g2 (nullable): a dual GEMM's second operand pair (parts = sums over both K ranges)
+int gemm_parts_count(const GemmArgs& g, const GemmArgs* g2 = nullptr);  // S (0: not applicable)
+int64_t gemm_parts_workspace(const GemmArgs& g, const GemmArgs* g2 = nullptr);
+int gemm_parts(const GemmArgs& g, const GemmArgs* g2, int S, float* parts, int64_t part_stride,
+               int64_t ldc, void* ws, int64_t ws_bytes, cudaStream_t s);
 // dense K-major hi/lo tf32 planes [batch][rows][Kp] of an operand view
 int64_t gemm_planes_bytes(const GemmArgs& g);  // both planes of B (0: not splittable)
 void tc_split_launch(const float* x, int64_t batch, int64_t rows, int64_t K, int64_t Kp, int64_t sb,

@@ -62,6 +62,7 @@ struct Cfg {
 
 struct Params {
   int M, N, nk, kb_per, ntn, S;
+  int nk1;            // k-blocks of the first operand pair (dual GEMM: the rest from map_*2)
   const float* bias;  // split 0 only; broadcast strides
   int64_t sxm, sxn;
   float* C;          // direct-store epilogue (PFB_PARTS_STORE=1): parts base, strides
@@ -82,7 +83,8 @@ template <int BN>
 __global__ void __launch_bounds__(NUM_THREADS, 1)
 parts_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ CUtensorMap map_bh,
              const __grid_constant__ CUtensorMap map_bl, const __grid_constant__ CUtensorMap map_c,
-             Params p) {
+             const __grid_constant__ CUtensorMap map_a2, const __grid_constant__ CUtensorMap map_bh2,
+             const __grid_constant__ CUtensorMap map_bl2, Params p) {
   using C = Cfg<BN>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>(
@@ -141,9 +143,12 @@ parts_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ 
         const int s = g % C::STAGES, kb = kb0 + g;
         if (g >= C::STAGES) mbar_wait(&empty[s], ((g / C::STAGES) - 1) & 1);
         mbar_expect_tx(&full[s], A_BYTES + 2 * C::B_BYTES);
-        tma_load_3d(&map_a, &full[s], stage(s), kb * BK, m0, 0);
-        tma_load_3d(&map_bh, &full[s], stage(s) + 2 * A_BYTES, kb * BK, n0, 0);
-        tma_load_3d(&map_bl, &full[s], stage(s) + 2 * A_BYTES + C::B_BYTES, kb * BK, n0, 0);
+        const bool second = kb >= p.nk1;
+        const int kc = (second ? kb - p.nk1 : kb) * BK;
+        tma_load_3d(second ? &map_a2 : &map_a, &full[s], stage(s), kc, m0, 0);
+        tma_load_3d(second ? &map_bh2 : &map_bh, &full[s], stage(s) + 2 * A_BYTES, kc, n0, 0);
+        tma_load_3d(second ? &map_bl2 : &map_bl, &full[s], stage(s) + 2 * A_BYTES + C::B_BYTES, kc,
+                    n0, 0);
         if (g < 8) pstamp(p, 16 + g);
       }
     }
@@ -306,8 +311,7 @@ static int plan(int64_t M, int64_t N, int64_t K, int BN, int* kb_per) {
 }
 
 template <int BN>
-static int launch(const GemmArgs& g, const CUtensorMap& ma, const CUtensorMap& mbh,
-                  const CUtensorMap& mbl, const CUtensorMap& mc, int S, int kb_per,
+static int launch(const GemmArgs& g, const CUtensorMap* maps, int nk1, int nk, int S, int kb_per,
                   float* out, int64_t part_stride, int64_t ldc, cudaStream_t s) {
   using C = Cfg<BN>;
   static bool attr = false;
@@ -317,7 +321,8 @@ static int launch(const GemmArgs& g, const CUtensorMap& ma, const CUtensorMap& m
   }
   Params p;
   p.M = (int)g.M; p.N = (int)g.N;
-  p.nk = (int)(((g.K + 3) / 4 * 4 + BK - 1) / BK);
+  p.nk = nk;
+  p.nk1 = nk1;
   p.kb_per = kb_per;
   p.ntn = (int)((g.N + BN - 1) / BN);
   p.S = S;
@@ -330,8 +335,20 @@ static int launch(const GemmArgs& g, const CUtensorMap& ma, const CUtensorMap& m
   }();
   p.direct = direct;
   const int units = (int)(((g.M + BM - 1) / BM) * p.ntn * S);
-  pfb::launch(parts_kernel<BN>, dim3(units), dim3(NUM_THREADS), C::SMEM, s, ma, mbh, mbl, mc, p);
+  pfb::launch(parts_kernel<BN>, dim3(units), dim3(NUM_THREADS), C::SMEM, s, maps[0], maps[1],
+              maps[2], maps[3], maps[4], maps[5], maps[6], p);
   return launch_status();
+}
+
+static int64_t kblocks(const GemmArgs& g) { return ((g.K + 3) / 4 * 4 + BK - 1) / BK; }
+
+// A K-major and TMA-readable as is, batch 1, no prologue / epilogue beyond a bias
+static bool parts_operand_ok(const GemmArgs& g) {
+  if (g.batch != 1 || g.M < 1 || g.N < 8 || g.K < 8 || g.kscale || g.accumulate || g.act ||
+      g.dop || g.alpha_rows)
+    return false;
+  return g.sak == 1 && (g.M == 1 || ((g.sam * 4) % 16 == 0 && g.sam >= g.K)) &&
+         (reinterpret_cast<uintptr_t>(g.A) & 15) == 0;
 }
 
 }  // namespace tcs
@@ -345,68 +362,86 @@ static int parts_bn(const GemmArgs& g) {
   return 128;
 }
 
-// S for pfb_matmul_parts (0: not applicable): batch 1, A K-major and
-// TMA-readable as is, B pre-split (planes) or splittable into the workspace
-int gemm_parts_count(const GemmArgs& g) {
+// S for pfb_matmul_parts (0: not applicable); g2 (nullable): the second
+// operand pair of a dual GEMM (K ranges concatenated, same M, N)
+int gemm_parts_count(const GemmArgs& g, const GemmArgs* g2) {
   using namespace tcs;
-  if (g.batch != 1 || g.M < 1 || g.N < 8 || g.K < 64 || g.kscale || g.accumulate || g.act ||
-      g.dop || g.alpha_rows)
+  if (!parts_operand_ok(g) || (g2 && (!parts_operand_ok(*g2) || g2->M != g.M || g2->N != g.N)))
     return 0;
-  if (g.sak != 1 || (g.M > 1 && ((g.sam * 4) % 16 != 0 || g.sam < g.K)) ||
-      (reinterpret_cast<uintptr_t>(g.A) & 15) != 0)
-    return 0;
+  const int64_t nk = kblocks(g) + (g2 ? kblocks(*g2) : 0);
+  if (nk < 2) return 0;
   int per;
-  return plan(g.M, g.N, g.K, parts_bn(g), &per);
+  return plan(g.M, g.N, nk * BK, parts_bn(g), &per);
 }
 
-int64_t gemm_parts_workspace(const GemmArgs& g) {
-  if (g.b_hi) return 0;
-  const int64_t Kp = (g.K + 3) / 4 * 4;
-  return 2 * ((g.N * Kp * 4 + 255) / 256 * 256);
+int64_t gemm_parts_workspace(const GemmArgs& g, const GemmArgs* g2) {
+  auto one = [](const GemmArgs& x) -> int64_t {
+    if (x.b_hi) return 0;
+    const int64_t Kp = (x.K + 3) / 4 * 4;
+    return 2 * ((x.N * Kp * 4 + 255) / 256 * 256);
+  };
+  return one(g) + (g2 ? one(*g2) : 0);
 }
 
-int gemm_parts(const GemmArgs& g, int S, float* parts, int64_t part_stride, int64_t ldc,
-               void* ws, int64_t ws_bytes, cudaStream_t s) {
+// the A map and the B hi / lo maps of one operand pair (B split into the
+// workspace at `w` when it has no pre-split planes)
+static int pair_maps(const GemmArgs& g, int BN, char*& w, cudaStream_t s, CUtensorMap* m) {
   using namespace tcs;
-  const int BN = parts_bn(g);
-  int kb_per = 0;
-  if (gemm_parts_count(g) != S || plan(g.M, g.N, g.K, BN, &kb_per) != S) return PFB_E_UNSUPPORTED;
-  if ((part_stride * 4) % 16 != 0 || (ldc * 4) % 16 != 0 || (reinterpret_cast<uintptr_t>(parts) & 15))
-    return PFB_E_UNSUPPORTED;
   const int64_t Kp = (g.K + 3) / 4 * 4;
   const float* bh = g.b_hi;
   const float* bl = g.b_lo;
   if (!bh) {
-    if (ws == nullptr || ws_bytes < gemm_parts_workspace(g)) return PFB_E_UNSUPPORTED;
-    float* h = static_cast<float*>(ws);
-    float* l = reinterpret_cast<float*>(static_cast<char*>(ws) + (g.N * Kp * 4 + 255) / 256 * 256);
+    float* h = reinterpret_cast<float*>(w);
+    w += (g.N * Kp * 4 + 255) / 256 * 256;
+    float* l = reinterpret_cast<float*>(w);
+    w += (g.N * Kp * 4 + 255) / 256 * 256;
     tc_split_launch(g.B, 1, g.N, g.K, Kp, 0, g.sbn, g.sbk, h, l, nullptr, 0, 0, s);
     bh = h;
     bl = l;
   }
-  CUtensorMap ma, mbh, mbl, mc;
   {
     const int64_t ld = g.M == 1 ? Kp : g.sam;
     cuuint64_t dims[3] = {(cuuint64_t)g.K, (cuuint64_t)g.M, 1};
     cuuint64_t strides[2] = {(cuuint64_t)(ld * 4), (cuuint64_t)(ld * g.M * 4)};
     cuuint32_t box[3] = {BK, BM, 1};
-    if (!encode(&ma, g.A, dims, strides, box)) return PFB_E_UNSUPPORTED;
+    if (!encode(&m[0], g.A, dims, strides, box)) return PFB_E_UNSUPPORTED;
   }
-  {
-    cuuint64_t dims[3] = {(cuuint64_t)Kp, (cuuint64_t)g.N, 1};
-    cuuint64_t strides[2] = {(cuuint64_t)(Kp * 4), (cuuint64_t)(g.N * Kp * 4)};
-    cuuint32_t box[3] = {BK, (cuuint32_t)BN, 1};
-    if (!encode(&mbh, bh, dims, strides, box) || !encode(&mbl, bl, dims, strides, box))
-      return PFB_E_UNSUPPORTED;
+  cuuint64_t dims[3] = {(cuuint64_t)Kp, (cuuint64_t)g.N, 1};
+  cuuint64_t strides[2] = {(cuuint64_t)(Kp * 4), (cuuint64_t)(g.N * Kp * 4)};
+  cuuint32_t box[3] = {BK, (cuuint32_t)BN, 1};
+  if (!encode(&m[1], bh, dims, strides, box) || !encode(&m[2], bl, dims, strides, box))
+    return PFB_E_UNSUPPORTED;
+  return 0;
+}
+
+int gemm_parts(const GemmArgs& g, const GemmArgs* g2, int S, float* parts, int64_t part_stride,
+               int64_t ldc, void* ws, int64_t ws_bytes, cudaStream_t s) {
+  using namespace tcs;
+  const int BN = parts_bn(g);
+  const int nk1 = (int)kblocks(g), nk = nk1 + (g2 ? (int)kblocks(*g2) : 0);
+  int kb_per = 0;
+  if (gemm_parts_count(g, g2) != S || plan(g.M, g.N, (int64_t)nk * BK, BN, &kb_per) != S)
+    return PFB_E_UNSUPPORTED;
+  if ((part_stride * 4) % 16 != 0 || (ldc * 4) % 16 != 0 || (reinterpret_cast<uintptr_t>(parts) & 15))
+    return PFB_E_UNSUPPORTED;
+  const int64_t need = gemm_parts_workspace(g, g2);
+  if (need > 0 && (ws == nullptr || ws_bytes < need)) return PFB_E_UNSUPPORTED;
+  char* w = static_cast<char*>(ws);
+  CUtensorMap maps[7];  // A, B hi, B lo, C, A2, B2 hi, B2 lo
+  if (int e = pair_maps(g, BN, w, s, &maps[0])) return e;
+  if (g2) {
+    if (int e = pair_maps(*g2, BN, w, s, &maps[4])) return e;
+  } else {
+    maps[4] = maps[0]; maps[5] = maps[1]; maps[6] = maps[2];  // unused (nk1 == nk)
   }
   {
     cuuint64_t dims[3] = {(cuuint64_t)g.N, (cuuint64_t)g.M, (cuuint64_t)S};
     cuuint64_t strides[2] = {(cuuint64_t)(ldc * 4), (cuuint64_t)(part_stride * 4)};
     cuuint32_t box[3] = {32, 32, 1};
-    if (!encode(&mc, parts, dims, strides, box)) return PFB_E_UNSUPPORTED;
+    if (!encode(&maps[3], parts, dims, strides, box)) return PFB_E_UNSUPPORTED;
   }
-  return BN == 256 ? tcs::launch<256>(g, ma, mbh, mbl, mc, S, kb_per, parts, part_stride, ldc, s)
-                   : tcs::launch<128>(g, ma, mbh, mbl, mc, S, kb_per, parts, part_stride, ldc, s);
+  return BN == 256 ? tcs::launch<256>(g, maps, nk1, nk, S, kb_per, parts, part_stride, ldc, s)
+                   : tcs::launch<128>(g, maps, nk1, nk, S, kb_per, parts, part_stride, ldc, s);
 }
 
 }  // namespace pfb

@@ -200,7 +200,10 @@ def _raise_status(code, what):
 class _Plan:
     """Per-(graph, requested outputs) liveness: live node set + use counts."""
 
-    def __init__(self, g, roots):
+    def __init__(self, g, roots, const_caps=()):
+        """`const_caps`: indices of this (sub-)graph's captures whose values are
+        hoisted constants of the enclosing graph (loop-invariant weights):
+        they seed the constant-derived set like constants do."""
         live = set()
         todo = list(roots) + [n.id for n in g.nodes.values() if n.kind in STATEFUL_KINDS
                               or (n.block is not None and _block_has_state(n.block))]
@@ -221,7 +224,7 @@ class _Plan:
         # executor evaluates them once and reuses the device values
         self.const_nodes = set()
         for n in self.order:
-            if n.kind == "constant":
+            if n.kind == "constant" or (n.kind == "capture" and n.attrs["index"] in const_caps):
                 self.const_nodes.add(n.id)
             elif (n.kind not in _NO_HOIST and n.block is None and n.inputs
                   and all(src in self.const_nodes for src, _ in n.inputs)):
@@ -241,18 +244,22 @@ class _Plan:
                 if c.kind in _PARTS_VIEW_KINDS:
                     if not sums_on_load(c.id, depth + 1):
                         return False
-                elif c.kind not in _PARTS_SUM_KINDS:
+                elif c.kind not in _PARTS_USE_KINDS:
                     return False
             return True
 
         self.parts_ok = {n.id for n in self.order
-                         if n.kind in ("matmul", "matmul_ep") and n.id not in self.const_nodes
+                         if n.kind in ("matmul", "matmul_ep", "matmul2")
+                         and n.id not in self.const_nodes
                          and sums_on_load(n.id)}
 
 
 _PARTS_VIEW_KINDS = frozenset({"reshape", "transpose", "gather_rows", "slice_leading"})
 _PARTS_SUM_KINDS = frozenset({"fused_ew", "fused_ewm", "fused_pack"})
-_PARTS_AWARE = _PARTS_VIEW_KINDS | _PARTS_SUM_KINDS | {"tile_leading"}
+# a row reduction reduces the partials once (cached per GEMM output, so the
+# fused consumers of the same GEMM then read the reduced value too)
+_PARTS_USE_KINDS = _PARTS_SUM_KINDS | {"reduce_sum"}
+_PARTS_AWARE = _PARTS_VIEW_KINDS | _PARTS_SUM_KINDS | {"tile_leading", "reduce_sum"}
 
 _NO_HOIST = STATEFUL_KINDS | {"placeholder", "capture", "carried", "loop_var", "where_true",
                               "complement"}
@@ -329,6 +336,8 @@ class Executor:
         self._parts_ok = None  # F15: GEMM node ids of the running plan that may return partials
         self.parts_made = 0     # F15 GEMMs that returned partials / partials reduced by a
         self.parts_reduced = 0  # consumer that could not sum them on load
+        self._parts_dense = {}  # id(partials buffer) -> (reduced buffer, partials) for this run
+        self._const_caps = {}   # id(sub-graph) -> capture indices that are constants outside
         self._planes = {}
 
     # -- public API ------------------------------------------------------------
@@ -939,11 +948,20 @@ class Executor:
             raise E.BudgetExceeded(f"step budget {self.budget} exceeded at node {node.id}")
 
     def _plan(self, g, roots):
-        key = (id(g), tuple(roots))
+        cc = self._const_caps.get(id(g), frozenset())
+        key = (id(g), tuple(roots), cc)
         p = self._plans.get(key)
         if p is None:
-            p = self._plans[key] = _Plan(g, [r[0] for r in roots])
+            p = self._plans[key] = _Plan(g, [r[0] for r in roots], cc)
         return p
+
+    def _note_const_caps(self, caps_keys, subgraphs):
+        """Captures of a cond/while block that are hoisted constants here: the
+        block's sub-graphs treat them as constants (weight planes, hoisting)."""
+        consts = self._const_ctx[1] if self._const_ctx is not None else ()
+        cc = frozenset(i for i, r in enumerate(caps_keys) if r[0] in consts)
+        for sg in subgraphs:
+            self._const_caps[id(sg)] = cc
 
     def _run_graph(self, g, binder, feeds, roots=None):
         roots = list(roots) if roots is not None else [tuple(o) for o in g.outputs]
@@ -952,13 +970,14 @@ class Executor:
         for r in roots:
             remaining[r] = remaining.get(r, 0) + 1
         env = {}
-        saved = self._const_ctx, self._parts_ok
+        saved = self._const_ctx, self._parts_ok, self._parts_dense
         self._const_ctx = (g, plan.const_nodes)
         self._parts_ok = plan.parts_ok
+        self._parts_dense = {}
         try:
             self._run_nodes(g, plan, env, binder, feeds, remaining)
         finally:
-            self._const_ctx, self._parts_ok = saved
+            self._const_ctx, self._parts_ok, self._parts_dense = saved
         for r in roots:  # (F15 never applies to outputs; defensive)
             if isinstance(env.get(r), DArray) and env[r].parts is not None:
                 env[r] = self._reduce_parts(env[r])
@@ -1018,6 +1037,7 @@ class Executor:
         if k == "cond":
             self._tick(node)
             c = self._host_bool(env[node.inputs[0]])
+            self._note_const_caps(node.inputs[1:], node.block.subgraphs.values())
             sub = node.block.subgraphs["then" if c else "else"]
             senv = self._run_graph(sub, {"capture": [env[r] for r in node.inputs[1:]]}, feeds)
             return [senv[tuple(o)] for o in sub.outputs]
@@ -1027,6 +1047,7 @@ class Executor:
             car = [env[r] for r in node.inputs[:nc]]
             caps = [env[r] for r in node.inputs[nc:]]
             cg, bg = node.block.subgraphs["cond"], node.block.subgraphs["body"]
+            self._note_const_caps(node.inputs[nc:], (cg, bg))
             res = self._device_loop(node, cg, bg, car, caps, feeds)
             if res is not None:
                 return res
@@ -1079,18 +1100,26 @@ class Executor:
         except PartsPending:
             return h(self, node, [self._reduce_parts(v) for v in ins])
 
-    def _reduce_parts(self, v):
-        """The value of a split-K partials view (F15) as an ordinary tensor."""
+    def _reduce_parts(self, v, count=True):
+        """The value of a split-K partials view (F15) as an ordinary tensor:
+        the GEMM's whole output is reduced once (one launch) and cached for the
+        run, so every other view of it maps onto the reduced buffer."""
         if not isinstance(v, DArray) or v.parts is None:
             return v
-        self.parts_reduced += 1
         S, st = v.parts
-        stacked = DArray(v.buf, v.offset, (S,) + v.shape, (st,) + v.strides, v.dtype)
-        out = self._empty(v.shape, v.dtype)
-        wp, wn = self._ws_get(min(8 * max(1, _numel(v.shape)) * 1024, 1 << 26))
-        self._call(self._lib.pfb_reduce_sum, stacked.desc(), 1, out.desc(), wp, wn, self._stream,
-                   what="reduce_sum", work=(_abytes(stacked, out), 0))
-        return out
+        dense = self._parts_dense.get(id(v.buf))
+        if dense is None:
+            if count:
+                self.parts_reduced += 1
+            stacked = DArray(v.buf, 0, (S, st), (st, 1), v.dtype)
+            dense = self._empty((st,), v.dtype)
+            wp, wn = self._ws_get(min(8 * max(1, st) * 1024, 1 << 26))
+            self._call(self._lib.pfb_reduce_sum, stacked.desc(), 1, dense.desc(), wp, wn,
+                       self._stream, what="reduce_sum", work=(_abytes(stacked, dense), 0))
+            self._parts_dense[id(v.buf)] = (dense, v.buf)  # (keeps the partials' id unique)
+        else:
+            dense = dense[0]
+        return DArray(dense.buf, v.offset, v.shape, v.strides, v.dtype)
 
     def _feed(self, name, value, dtype):
         """Placeholder value on the device.  Host feeds are copied into one
@@ -1454,14 +1483,27 @@ def _h_matmul2(ex, node, ins):
     shape = (a1.shape[0], b1.shape[1])
     if (a2.shape[0], b2.shape[1]) != shape:
         raise E.IncompatibleShapes(f"matmul2: {shape} vs {(a2.shape[0], b2.shape[1])}")
-    out = ex._empty(shape, a1.dtype)
     flops = 2 * _numel(shape) * (a1.shape[1] + a2.shape[1])
     d = [x.desc() for x in (a1, b1, a2, b2)]
-    od = out.desc()
     xd = bias.desc() if bias is not None else None
+    p1, p2 = ex._b_planes(node, 1, b1), ex._b_planes(node, 3, b2)
+    if at.get("act") is None and node.id in (ex._parts_ok or ()) and ex._lib.pfb_fused_parts_ok():
+        probe = DArray(a1.buf, 0, shape, _dense_strides(shape), a1.dtype)
+        S = ex._lib.pfb_matmul_dual_parts_count(d[0], d[1], d[2], d[3], probe.desc())
+        if S >= 2:
+            stacked = ex._empty((S,) + shape, a1.dtype)
+            need = ex._lib.pfb_matmul_dual_parts_workspace(d[0], d[1], d[2], d[3], probe.desc())
+            wp, wn = ex._ws_get(need) if need > 0 else (None, 0)
+            ex._call(ex._lib.pfb_matmul_dual_parts, d[0], d[1], d[2], d[3], stacked.desc(),
+                     ctypes.byref(xd) if xd is not None else None, p1, p2, wp, wn, ex._stream,
+                     what="matmul_parts", work=(_abytes(*vals, stacked), flops))
+            ex.parts_made += 1
+            return [DArray(stacked.buf, 0, shape, _dense_strides(shape), a1.dtype,
+                           (S, _numel(shape)))]
+    out = ex._empty(shape, a1.dtype)
+    od = out.desc()
     need = ex._lib.pfb_matmul_dual_workspace(d[0], d[1], d[2], d[3], od)
     wp, wn = ex._ws_get(need) if need > 0 else (None, 0)
-    p1, p2 = ex._b_planes(node, 1, b1), ex._b_planes(node, 3, b2)
     ex._call(ex._lib.pfb_matmul_dual2, d[0], d[1], d[2], d[3], od,
              ctypes.byref(xd) if xd is not None else None, _ACT_CODE[at.get("act")], p1, p2, 0,
              wp, wn, ex._stream, what="matmul", work=(_abytes(*vals, out), flops))
@@ -1533,10 +1575,11 @@ def _h_reduce_sum(ex, node, ins):
     x = ex._dev(ins[0])
     axes = normalize_axes(node.attrs["axes"], x.rank)
     if not axes:
-        return [ins[0]]
+        return [ex._reduce_parts(ins[0])]
     shape = tuple(d for i, d in enumerate(x.shape) if i not in axes)
     if all(x.shape[ax] == 1 for ax in axes):  # sum over extent-1 axes: a view
         return [x.view(shape, tuple(st for i, st in enumerate(x.strides) if i not in axes))]
+    x = ex._reduce_parts(x)
     mask = 0
     for ax in axes:
         mask |= 1 << ax
@@ -1773,8 +1816,12 @@ def _fused_launch(ex, arrs, prog, regs, nregs, outs):
     """One fused-program launch; inputs held as split-K partials (F15) go
     through pfb_fused_ew_parts, which sums them as it loads."""
     odescs = (N.PfbTensor * len(outs))(*[o.desc() for o in outs])
-    if any(a.parts is not None for a in arrs) and not ex._lib.pfb_fused_parts_ok():
-        arrs = [ex._reduce_parts(a) for a in arrs]
+    if any(a.parts is not None for a in arrs):
+        if not ex._lib.pfb_fused_parts_ok():
+            arrs = [ex._reduce_parts(a) for a in arrs]
+        else:  # partials already reduced for another consumer: read the reduced value
+            arrs = [ex._reduce_parts(a) if a.parts is not None and id(a.buf) in ex._parts_dense
+                    else a for a in arrs]
     if any(a.parts is not None for a in arrs):
         spec = []
         for a in arrs:

@@ -151,3 +151,49 @@ def test_cfg4_partials_match_reduced_executor(env, monkeypatch):
         np.testing.assert_allclose(np.asarray(g_.data, np.float64), np.asarray(w_.data, np.float64),
                                    rtol=RTOL, atol=ATOL)
 
+
+
+@pytest.mark.parametrize("m,n,k1,k2", [(1024, 256, 256, 256), (300, 200, 96, 200)])
+def test_matmul_dual_parts_sum_matches_f64(env, m, n, k1, k2):
+    """a1 @ b1 + a2 @ b2 (cfg5's RNN cell) as split-K partials over both K ranges."""
+    torch, lib, DArray, DType = env
+    dev = torch.device("cuda")
+    r = np.random.default_rng(m + k1)
+    a1 = r.standard_normal((m, k1)).astype(np.float32)
+    a2 = r.standard_normal((m, k2)).astype(np.float32)
+    b1 = (r.standard_normal((k1, n)) / 16).astype(np.float32)
+    b2 = (r.standard_normal((k2, n)) / 16).astype(np.float32)
+    A1, A2 = DArray.from_numpy(a1, DType.F64, dev), DArray.from_numpy(a2, DType.F64, dev)
+    B1, B2 = DArray.from_numpy(b1, DType.F64, dev), DArray.from_numpy(b2, DType.F64, dev)
+    probe = DArray.empty((m, n), DType.F64, dev)
+    d = [x.desc() for x in (A1, B1, A2, B2)]
+    S = lib.pfb_matmul_dual_parts_count(d[0], d[1], d[2], d[3], probe.desc())
+    assert S >= 2
+    P = DArray.empty((S, m, n), DType.F64, dev)
+    need = lib.pfb_matmul_dual_parts_workspace(d[0], d[1], d[2], d[3], probe.desc())
+    ws = torch.empty(max(need, 256), dtype=torch.uint8, device=dev)
+    assert lib.pfb_matmul_dual_parts(d[0], d[1], d[2], d[3], P.desc(), None, None, None,
+                                     ws.data_ptr(), ws.numel(), None) == 0
+    torch.cuda.synchronize()
+    want = a1.astype(np.float64) @ b1 + a2.astype(np.float64) @ b2
+    np.testing.assert_allclose(P.to_numpy().astype(np.float64).sum(0), want, rtol=RTOL, atol=ATOL)
+
+
+def test_cfg5_partials_match_reduced_executor(env, monkeypatch):
+    """cfg5 (masked, unrolled device loop): the per-trip dual GEMMs return
+    partials, summed by the row-sum reduction and the select group."""
+    torch, lib, DArray, DType = env
+    from paper_1903_04243_b200 import workloads as WL
+    from paper_1903_04243_b200.executor import Executor
+    w = WL.BUILDERS["cfg5"](WL.this_api(), n=512, max_len=12, units=256, masked=True, unroll=4)
+    ex = Executor(w.graph, device="cuda:0", cuda_graph=False)
+    got = ex.run(feeds=w.feeds)
+    # each GEMM's partials are reduced once, by its row sum, and the select
+    # group then reads the reduced value
+    assert ex.parts_made > 0 and ex.parts_reduced == ex.parts_made, (ex.parts_made, ex.parts_reduced)
+    ex2 = Executor(w.graph, device="cuda:0", cuda_graph=False)
+    monkeypatch.setattr(ex2._lib, "pfb_fused_parts_ok", lambda: 0)
+    want = ex2.run(feeds=w.feeds)
+    for g_, w_ in zip(got, want):
+        np.testing.assert_allclose(np.asarray(g_.data, np.float64), np.asarray(w_.data, np.float64),
+                                   rtol=RTOL, atol=ATOL)
