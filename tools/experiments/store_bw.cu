@@ -3,7 +3,9 @@
 //   mode 0: TMA store, box {32 cols, 32 rows} (4 KB, per warp)     -- current epilogues
 //   mode 1: TMA store, box {32 cols, 128 rows} (16 KB, 4 warps)
 //   mode 2: TMA store, 3-D box {32 cols, 128 rows, 4 col-blocks} (64 KB, 8 warps... 2 halves)
-//   mode 3: st.global.v4 from registers (4 rows x 128 B per warp instruction)
+//   mode 3: st.global.v4 through a smem transpose (4 rows x 128 B per warp instruction)
+//   mode 4: st.global.v4 straight from registers (lane = row: 32 rows x 16 B per instruction)
+// Measured (profiles/r02/README.md): modes 0-3 5.9-6.1 TB/s, mode 4 1.5 TB/s.
 //   nvcc -gencode arch=compute_100a,code=sm_100a -O3 -o store_bw store_bw.cu -lcuda && ./store_bw
 #include <cuda.h>
 #include <cudaTypedefs.h>
@@ -33,6 +35,18 @@ __global__ void __launch_bounds__(256, 1) store_kernel(const __grid_constant__ C
   for (int t = blockIdx.x; t < tiles; t += gridDim.x, buf ^= 1) {
     const int m0 = (t / (N / TN)) * TM, n0 = (t % (N / TN)) * TN;
     float* st = smem + buf * (TM * TN);
+    if (mode == 4) {
+      // registers -> global, no shared memory: lane = row, 32 consecutive columns
+      // per lane as 8 x 16-byte stores (each warp instruction: 32 rows x 16 B)
+      for (int cb = 0; cb < 2; ++cb) {
+        const int col0 = n0 + half * 64 + cb * 32;
+        float* rowp = C + (int64_t)(m0 + quarter * 32 + lane) * N + col0;
+#pragma unroll
+        for (int q = 0; q < 8; ++q)
+          *reinterpret_cast<float4*>(rowp + 4 * q) = make_float4(t, q, cb, lane);
+      }
+      continue;
+    }
     if (mode == 3) {
       // registers -> smem transpose -> 4-row x 128-byte stores
       float* blk = smem + warp * 1024;
@@ -117,9 +131,9 @@ int main() {
   cudaFuncSetAttribute(store_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   int sms = 0;
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
-  const char* names[4] = {"TMA box 32x32 (4 KB/warp)", "TMA box 32x128 (16 KB)", "TMA 3-D box 32x128x4 (64 KB)",
-                          "st.global.v4 via smem transpose"};
-  for (int mode = 0; mode < 4; ++mode) {
+  const char* names[5] = {"TMA box 32x32 (4 KB/warp)", "TMA box 32x128 (16 KB)", "TMA 3-D box 32x128x4 (64 KB)",
+                          "st.global.v4 via smem transpose", "st.global.v4 from registers (row/lane)"};
+  for (int mode = 0; mode < 5; ++mode) {
     if (mode == 2 && r != CUDA_SUCCESS) continue;
     cudaEvent_t a, b;
     cudaEventCreate(&a);
