@@ -369,7 +369,11 @@ int gemm_parts_count(const GemmArgs& g, const GemmArgs* g2) {
   if (!parts_operand_ok(g) || (g2 && (!parts_operand_ok(*g2) || g2->M != g.M || g2->N != g.N)))
     return 0;
   const int64_t nk = kblocks(g) + (g2 ? kblocks(*g2) : 0);
-  if (nk < 2) return 0;
+  // small products (cfg1's 32x256x784 forward) stay on the autotuned paths:
+  // the partials cost their consumers S reads and win only where the k-loop
+  // and the cluster reduction are long (cfg4's per-step GEMMs: >= 268M MACs)
+  if (nk < 2 || (double)g.M * g.N * nk * BK < (double)(1 << 26)) return 0;
+  if (g.N % 4 != 0) return 0;  // the [S, M, N] partials' rows must be 16-byte aligned (TMA store)
   int per;
   return plan(g.M, g.N, nk * BK, parts_bn(g), &per);
 }

@@ -58,7 +58,7 @@ def _parts(env, a, b, bias=None, planes=False, b_kmajor=True):
 
 
 @pytest.mark.parametrize("m,n,k", [(256, 2048, 1024), (256, 512, 2048), (256, 2048, 512),
-                                   (200, 300, 520), (64, 136, 100)])
+                                   (200, 600, 600), (130, 1028, 520)])
 @pytest.mark.parametrize("planes", [False, True])
 def test_matmul_parts_sum_matches_f64(env, m, n, k, planes):
     r = np.random.default_rng(m + n + k)
@@ -72,11 +72,26 @@ def test_matmul_parts_sum_matches_f64(env, m, n, k, planes):
     np.testing.assert_allclose(got, want, rtol=RTOL, atol=ATOL)
 
 
+def test_matmul_parts_declines_small_products(env):
+    """cfg1's 32x256x784 forward GEMM stays on the autotuned reduced paths."""
+    torch, lib, DArray, DType = env
+    dev = torch.device("cuda")
+    a = DArray.empty((32, 784), DType.F64, dev)
+    b = DArray.empty((784, 256), DType.F64, dev)
+    c = DArray.empty((32, 256), DType.F64, dev)
+    assert lib.pfb_matmul_parts_count(a.desc(), b.desc(), c.desc()) == 0
+    # and rows of N = 1030 floats (not 16-byte aligned) are declined, not failed
+    a2 = DArray.empty((256, 1024), DType.F64, dev)
+    b2 = DArray.empty((1024, 1030), DType.F64, dev)
+    c2 = DArray.empty((256, 1030), DType.F64, dev)
+    assert lib.pfb_matmul_parts_count(a2.desc(), b2.desc(), c2.desc()) == 0
+
+
 def test_matmul_parts_row_bias_and_row_major_b(env):
     r = np.random.default_rng(7)
     a = r.standard_normal((256, 640)).astype(np.float32)
-    b = (r.standard_normal((640, 384)) / 25).astype(np.float32)
-    bias = r.standard_normal((256, 384)).astype(np.float32)  # a full matrix addend
+    b = (r.standard_normal((640, 512)) / 25).astype(np.float32)
+    bias = r.standard_normal((256, 512)).astype(np.float32)  # a full matrix addend
     parts, S = _parts(env, a, b, bias, planes=False, b_kmajor=False)
     assert S >= 2
     want = a.astype(np.float64) @ b.astype(np.float64) + bias
@@ -153,7 +168,7 @@ def test_cfg4_partials_match_reduced_executor(env, monkeypatch):
 
 
 
-@pytest.mark.parametrize("m,n,k1,k2", [(1024, 256, 256, 256), (300, 200, 96, 200)])
+@pytest.mark.parametrize("m,n,k1,k2", [(1024, 256, 256, 256), (520, 264, 96, 440)])
 def test_matmul_dual_parts_sum_matches_f64(env, m, n, k1, k2):
     """a1 @ b1 + a2 @ b2 (cfg5's RNN cell) as split-K partials over both K ranges."""
     torch, lib, DArray, DType = env
