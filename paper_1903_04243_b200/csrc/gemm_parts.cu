@@ -65,9 +65,6 @@ struct Params {
   int nk1;            // k-blocks of the first operand pair (dual GEMM: the rest from map_*2)
   const float* bias;  // split 0 only; broadcast strides
   int64_t sxm, sxn;
-  float* C;          // direct-store epilogue (PFB_PARTS_STORE=1): parts base, strides
-  int64_t ldc, part_stride;
-  int direct;
   unsigned long long* trace;  // PFB_TC_TRACE: phase stamps of CTA 0 + per-CTA start/end
 };
 
@@ -250,25 +247,6 @@ parts_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ 
         *reinterpret_cast<float4*>(blk + lane * 32 + 4 * (q ^ (lane & 7))) =
             make_float4(acc[32 * b + 4 * q], acc[32 * b + 4 * q + 1], acc[32 * b + 4 * q + 2],
                         acc[32 * b + 4 * q + 3]);
-      if (p.direct) {
-        // each store instruction: 4 rows x 128 contiguous bytes
-        __syncwarp();
-        const int sub_r = lane >> 3, sub_c = (lane & 7) * 4;
-        float* cb = p.C + (int64_t)s_idx * p.part_stride;
-#pragma unroll
-        for (int i = 0; i < 32; i += 4) {
-          const int srow = i + sub_r, row = row0 + srow, col = col0 + sub_c;
-          const float4 w = *reinterpret_cast<const float4*>(blk + srow * 32 + 4 * ((sub_c >> 2) ^ (srow & 7)));
-          if (row < p.M && col + 3 < p.N) {
-            *reinterpret_cast<float4*>(cb + (int64_t)row * p.ldc + col) = w;
-          } else if (row < p.M) {
-            const float e[4] = {w.x, w.y, w.z, w.w};
-            for (int j = 0; j < 4; ++j)
-              if (col + j < p.N) cb[(int64_t)row * p.ldc + col + j] = e[j];
-          }
-        }
-        continue;
-      }
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
       __syncwarp();
       if (lane == 0) {
@@ -312,7 +290,7 @@ static int plan(int64_t M, int64_t N, int64_t K, int BN, int* kb_per) {
 
 template <int BN>
 static int launch(const GemmArgs& g, const CUtensorMap* maps, int nk1, int nk, int S, int kb_per,
-                  float* out, int64_t part_stride, int64_t ldc, cudaStream_t s) {
+                  cudaStream_t s) {
   using C = Cfg<BN>;
   static bool attr = false;
   if (!attr) {
@@ -328,12 +306,6 @@ static int launch(const GemmArgs& g, const CUtensorMap* maps, int nk1, int nk, i
   p.S = S;
   p.bias = g.bias; p.sxm = g.sxm; p.sxn = g.sxn;
   p.trace = tc_trace_buffer();
-  p.C = out; p.ldc = ldc; p.part_stride = part_stride;
-  static const int direct = [] {
-    const char* e = getenv("PFB_PARTS_STORE");
-    return e ? atoi(e) : 0;
-  }();
-  p.direct = direct;
   const int units = (int)(((g.M + BM - 1) / BM) * p.ntn * S);
   pfb::launch(parts_kernel<BN>, dim3(units), dim3(NUM_THREADS), C::SMEM, s, maps[0], maps[1],
               maps[2], maps[3], maps[4], maps[5], maps[6], p);
@@ -444,8 +416,8 @@ int gemm_parts(const GemmArgs& g, const GemmArgs* g2, int S, float* parts, int64
     cuuint32_t box[3] = {32, 32, 1};
     if (!encode(&maps[3], parts, dims, strides, box)) return PFB_E_UNSUPPORTED;
   }
-  return BN == 256 ? tcs::launch<256>(g, maps, nk1, nk, S, kb_per, parts, part_stride, ldc, s)
-                   : tcs::launch<128>(g, maps, nk1, nk, S, kb_per, parts, part_stride, ldc, s);
+  return BN == 256 ? tcs::launch<256>(g, maps, nk1, nk, S, kb_per, s)
+                   : tcs::launch<128>(g, maps, nk1, nk, S, kb_per, s);
 }
 
 }  // namespace pfb
