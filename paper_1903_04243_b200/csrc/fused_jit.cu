@@ -25,6 +25,8 @@
 #include <dlfcn.h>
 #include <nvrtc.h>
 
+#include <algorithm>
+#include <cmath>
 #include <cstdarg>
 #include <cstdio>
 #include <mutex>
@@ -119,8 +121,43 @@ std::string fmt(const char* f, ...) {
   return buf;
 }
 
+// Offsets of every operand for group index g, straight-line with the
+// layout's shape and strides as literals (divisions by constants, zero-stride
+// terms dropped, 32-bit arithmetic when every offset fits): the generic loop
+// over the layout's dims costs ~10 instructions per operand and dim, which
+// dominated small many-input groups (the LSTM cell: 19 operands x 3 dims).
+std::string gen_offsets(const FLayout& L, int nops, int V, bool idx64, bool off32) {
+  std::string s;
+  const char* IT = idx64 ? "i64" : "unsigned";
+  const char* OT = off32 ? "int" : "i64";
+  s += fmt("    %s lin = g * %d;\n", IT, V);
+  std::string terms[kMaxFOps];
+  for (int d = L.rank - 1; d >= 0; --d) {
+    std::string c;
+    if (d == 0) {
+      c = "lin";
+    } else {
+      s += fmt("    const %s c%d = lin %% (%s)%lld; lin /= (%s)%lld;\n", IT, d, IT,
+               (long long)L.shape[d], IT, (long long)L.shape[d]);
+      c = fmt("c%d", d);
+    }
+    for (int o = 0; o < nops; ++o) {
+      const long long st = (long long)L.st[o][d];
+      if (st == 0) continue;
+      std::string t = st == 1 ? fmt("(%s)%s", OT, c.c_str())
+                              : fmt("(%s)%s * (%s)%lld", OT, c.c_str(), OT, st);
+      terms[o] += (terms[o].empty() ? "" : " + ") + t;
+    }
+  }
+  s += fmt("    i64 off[%d];\n", nops);
+  for (int o = 0; o < nops; ++o)
+    s += fmt("    off[%d] = (i64)(%s);\n", o, terms[o].empty() ? "0" : terms[o].c_str());
+  return s;
+}
+
 std::string gen_source(const FusedProgram& P, int V, bool idx64, FeedModes modes,
-                       const PartsSpec* PS = nullptr) {
+                       const PartsSpec* PS = nullptr, const FLayout* LS = nullptr,
+                       bool off32 = false) {
   std::string s = fmt(kPrelude, kMaxRank, kMaxFOps, kMaxRank, kMaxOuts, kMaxIn);
   const char* IT = idx64 ? "i64" : "unsigned";
   const int nops = P.n_in + 1;
@@ -138,15 +175,19 @@ std::string gen_source(const FusedProgram& P, int V, bool idx64, FeedModes modes
        "  const int ir = L.rank - 1;\n";
   s += fmt("  for (%s g = blockIdx.x * (%s)blockDim.x + threadIdx.x; g < ngroups; "
            "g += (%s)gridDim.x * blockDim.x) {\n", IT, IT, IT);
-  s += fmt("    i64 off[%d];\n", nops);
-  s += fmt("    if (L.rank == 1) { for (int o = 0; o < %d; ++o) off[o] = (i64)(g * %d) * L.st[o][0]; }\n",
-           nops, V);
-  s += fmt("    else { %s lin = g * %d;\n", IT, V);
-  s += fmt("      for (int o = 0; o < %d; ++o) off[o] = 0;\n", nops);
-  s += fmt("      for (int d = L.rank - 1; d >= 0; --d) {\n"
-           "        %s sh = (%s)L.shape[d]; %s q = lin / sh; %s c = lin - q * sh; lin = q;\n"
-           "        for (int o = 0; o < %d; ++o) off[o] += (i64)c * L.st[o][d];\n"
-           "      }\n    }\n", IT, IT, IT, IT, nops);
+  if (LS) {
+    s += gen_offsets(*LS, nops, V, idx64, off32);
+  } else {
+    s += fmt("    i64 off[%d];\n", nops);
+    s += fmt("    if (L.rank == 1) { for (int o = 0; o < %d; ++o) off[o] = (i64)(g * %d) * L.st[o][0]; }\n",
+             nops, V);
+    s += fmt("    else { %s lin = g * %d;\n", IT, V);
+    s += fmt("      for (int o = 0; o < %d; ++o) off[o] = 0;\n", nops);
+    s += fmt("      for (int d = L.rank - 1; d >= 0; --d) {\n"
+             "        %s sh = (%s)L.shape[d]; %s q = lin / sh; %s c = lin - q * sh; lin = q;\n"
+             "        for (int o = 0; o < %d; ++o) off[o] += (i64)c * L.st[o][d];\n"
+             "      }\n    }\n", IT, IT, IT, IT, nops);
+  }
   // input feeds (all loads first, as in the interpreter)
   for (int k = 0; k < P.n_in; ++k) {
     const int md = (int)((modes >> (2 * (k + 1))) & 3);
@@ -385,11 +426,13 @@ CUfunction compile(const std::string& src) {
 
 int g_jit_on = -1;           // -1: not yet read from PFB_NO_JIT
 int64_t g_jit_min = 0;       // PFB_JIT_MIN: smallest group specialised
+int64_t g_jit_layout_min = 32768;  // PFB_JIT_LAYOUT_MIN: smallest group with its layout baked in
 
 void jit_init() {
   if (g_jit_on >= 0) return;
   g_jit_on = getenv_flag("PFB_NO_JIT") ? 0 : 1;
   if (const char* e = getenv("PFB_JIT_MIN")) g_jit_min = atoll(e);
+  if (const char* e = getenv("PFB_JIT_LAYOUT_MIN")) g_jit_layout_min = atoll(e);
 }
 
 }  // namespace
@@ -398,11 +441,11 @@ namespace {
 
 // kernel for a program (integer: the i64 domain), compiled on first use
 CUfunction lookup(const FusedProgram& P, int V, bool idx64, FeedModes modes, bool integer,
-                  const PartsSpec* PS = nullptr) {
+                  const PartsSpec* PS = nullptr, const FLayout* LS = nullptr, bool off32 = false) {
   int dev = 0;
   cudaGetDevice(&dev);
   // cache key: the program's encoding and everything baked into the source
-  int32_t kb[11 + 2 * kMaxIn + 4 * kMaxSteps + 2 * kMaxOuts];
+  int32_t kb[14 + 2 * kMaxIn + 4 * kMaxSteps + 2 * kMaxOuts + 2 * kMaxRank * (kMaxFOps + 1)];
   int nk = 0;
   kb[nk++] = dev; kb[nk++] = V; kb[nk++] = idx64; kb[nk++] = (int32_t)(modes & 0xffffffffu);
   kb[nk++] = (int32_t)(modes >> 32); kb[nk++] = integer;
@@ -414,6 +457,19 @@ CUfunction lookup(const FusedProgram& P, int V, bool idx64, FeedModes modes, boo
   kb[nk++] = PS != nullptr;
   if (PS)
     for (int k = 0; k < P.n_in; ++k) kb[nk++] = PS->S[k];
+  kb[nk++] = LS != nullptr;
+  if (LS) {  // the layout baked into the source (64-bit values as two words)
+    kb[nk++] = LS->rank;
+    kb[nk++] = off32;
+    for (int d = 0; d < LS->rank; ++d) {
+      kb[nk++] = (int32_t)LS->shape[d];
+      kb[nk++] = (int32_t)(LS->shape[d] >> 32);
+      for (int o = 0; o <= P.n_in; ++o) {
+        kb[nk++] = (int32_t)LS->st[o][d];
+        kb[nk++] = (int32_t)(LS->st[o][d] >> 32);
+      }
+    }
+  }
   const std::string key(reinterpret_cast<const char*>(kb), nk * sizeof(int32_t));
   static std::mutex mu;
   static std::unordered_map<std::string, CUfunction> cache;
@@ -421,7 +477,7 @@ CUfunction lookup(const FusedProgram& P, int V, bool idx64, FeedModes modes, boo
   auto it = cache.find(key);
   if (it == cache.end())
     it = cache.emplace(key, compile(integer ? gen_source_int(P, idx64)
-                                            : gen_source(P, V, idx64, modes, PS))).first;
+                                            : gen_source(P, V, idx64, modes, PS, LS, off32))).first;
   return it->second;
 }
 
@@ -461,7 +517,20 @@ bool fused_jit_launch(const FusedProgram& P, int V, bool idx64, FeedModes modes,
                       cudaStream_t s, const PartsSpec* parts) {
   if (parts && !parts->any()) parts = nullptr;
   if (!usable(parts ? INT64_MAX : ngroups * V)) return false;
-  CUfunction fn = lookup(P, V, idx64, modes, false, parts);
+  // groups of >= 32K elements (the ones a step repeats: cfg4's cell, cfg5's
+  // select) get the layout baked in; small ones share one kernel per program
+  const FLayout* LS = ngroups * V >= g_jit_layout_min ? &L : nullptr;
+  bool off32 = false;
+  if (LS) {
+    double mx = 0;
+    for (int o = 0; o <= P.n_in; ++o) {
+      double m = 0;
+      for (int d = 0; d < L.rank; ++d) m += (double)(L.shape[d] - 1) * std::fabs((double)L.st[o][d]);
+      mx = std::max(mx, m);
+    }
+    off32 = mx < 2147483647.0;
+  }
+  CUfunction fn = lookup(P, V, idx64, modes, false, parts, LS, off32);
   return fn && run(fn, idx64, L, ngroups, outs, ins, s, parts);
 }
 
