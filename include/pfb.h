@@ -95,6 +95,11 @@ int pfb_fused_ew_multi(int32_t n_in, const pfb_tensor* ins, int32_t n_steps,
 int pfb_fused_ew_parts(int32_t n_in, const pfb_tensor* ins, const int64_t* parts,
                        int32_t n_steps, const int32_t* program, int32_t n_out,
                        const int32_t* out_regs, pfb_tensor* outs, void* stream);
+/* out[i] = sum_s sum_k x_s[i, k], x_s = x + s * part_stride (x: [rows, W] view
+ * with unit inner stride): the row sums of a GEMM result still held as
+ * split-K partials (pass F15; reference tensor.reduce_sum, tensor.py:279-283). */
+int pfb_row_sum_parts(const pfb_tensor* x, int32_t parts, int64_t part_stride, pfb_tensor* out,
+                      void* stream);
 /* 1 when pfb_fused_ew_parts can run in this process now (NVRTC found, the
  * specialiser enabled) */
 int pfb_fused_parts_ok(void);

@@ -570,3 +570,57 @@ extern "C" int pfb_row_dots(int32_t n, const pfb_tensor* xs, const pfb_tensor* y
   launch(row_dots_kernel, dim3((unsigned)d.rows, (unsigned)n), 256, 0, as_stream(stream), d);
   return launch_status();
 }
+
+// ---------------------------------------------------------------------------
+// Row sums of split-K partials (pass F15): out[i] = sum_s sum_k P_s[i, k] with
+// P_s = x + s * part_stride ([rows, W], unit inner stride) -- the row
+// reduction of a GEMM result that is still held as partials (cfg5's
+// `reduce_sum(z) < 0` mask), so the partials need not be reduced into a
+// tensor first.  One CTA per row; fixed per-thread order + tree: deterministic.
+
+namespace pfb {
+__global__ void __launch_bounds__(256) row_sum_parts_kernel(const float* __restrict__ x,
+                                                            int64_t rs, int64_t W, int S,
+                                                            int64_t ps, float* out, int64_t so) {
+  pdl_enter();
+  const int64_t i = blockIdx.x;
+  Acc<float> acc;
+  const bool vec = (W % 4 == 0) && (rs % 4 == 0) && (ps % 4 == 0) &&
+                   ((reinterpret_cast<uintptr_t>(x) & 15) == 0);
+  for (int s = 0; s < S; ++s) {
+    const float* r = x + s * ps + i * rs;
+    if (vec) {
+      const float4* r4 = reinterpret_cast<const float4*>(r);
+      for (int64_t k = threadIdx.x; k < W / 4; k += blockDim.x) {
+        const float4 a = __ldg(r4 + k);
+        acc.add((a.x + a.y) + (a.z + a.w));
+      }
+    } else {
+      for (int64_t k = threadIdx.x; k < W; k += blockDim.x) acc.add(__ldg(r + k));
+    }
+  }
+  __shared__ float red[8];
+  const float v = warp_sum(acc.s);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = v;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    float t = 0.f;
+    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) t += red[w];
+    out[i * so] = t;
+  }
+}
+}  // namespace pfb
+
+extern "C" int pfb_row_sum_parts(const pfb_tensor* x, int32_t parts, int64_t part_stride,
+                                 pfb_tensor* out, void* stream) {
+  using namespace pfb;
+  if (x->dtype != PFB_F32 || out->dtype != PFB_F32) return PFB_E_DTYPE;
+  if (x->rank != 2 || out->rank != 1 || out->shape[0] != x->shape[0] || parts < 1)
+    return PFB_E_SHAPE;
+  if (x->shape[1] > 1 && x->stride[1] != 1) return PFB_E_UNSUPPORTED;
+  if (x->shape[0] == 0) return 0;
+  launch(row_sum_parts_kernel, dim3((unsigned)x->shape[0]), dim3(256), 0, as_stream(stream),
+         (const float*)x->data, x->stride[0], x->shape[1], (int)parts, part_stride,
+         (float*)out->data, out->stride[0]);
+  return launch_status();
+}

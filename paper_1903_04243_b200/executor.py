@@ -1579,6 +1579,14 @@ def _h_reduce_sum(ex, node, ins):
     shape = tuple(d for i, d in enumerate(x.shape) if i not in axes)
     if all(x.shape[ax] == 1 for ax in axes):  # sum over extent-1 axes: a view
         return [x.view(shape, tuple(st for i, st in enumerate(x.strides) if i not in axes))]
+    rows = _rows_view(x) if x.parts is not None and id(x.buf) not in ex._parts_dense else None
+    if rows is not None and list(axes) == list(range(1, x.rank)) and x.dtype == DType.F64:
+        # F15: row sums straight from the split-K partials (no reduced tensor)
+        out = ex._empty(shape, x.dtype)
+        S, pst = x.parts
+        ex._call(ex._lib.pfb_row_sum_parts, rows.desc_part0(), S, pst, out.desc(), ex._stream,
+                 what="reduce_sum", work=(_abytes(rows) * S + _abytes(out), 0))
+        return [out]
     x = ex._reduce_parts(x)
     mask = 0
     for ax in axes:
