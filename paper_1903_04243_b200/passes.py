@@ -987,7 +987,7 @@ def _pipeline(elementwise):
            fuse_outer_products, fuse_conv_filter_grads, eliminate_common_subexpressions,
            fuse_reductions, fuse_row_dots, fuse_dual_matmuls, fuse_matmul_epilogues]
     if elementwise:
-        seq += [fuse_elementwise, place_concats]
+        seq += [sink_unit_reshapes, fuse_elementwise, place_concats]
     return seq
 
 
@@ -1024,6 +1024,69 @@ def optimize(g, keep_keys, elementwise=True):
             v = moved.get(v, v)
         final[k] = v
     return dst, final
+
+
+# ----------------------------------------------------------------------------
+# F14: unit-dim reshapes of elementwise results move onto their operands
+#
+# reshape(less(r, 0), [n, 1, 1]) == less(reshape(r, [n, 1, 1]), 0): with the
+# reshape on the operand, the elementwise op has the broadcast shape of the
+# group that reads it and F3 absorbs it (the op is evaluated per element of
+# the group's output on the broadcast operand -- the same values).  cfg5's
+# per-step `reduce_sum(z) < 0` mask then costs no launch of its own.
+
+def _nonunit_dims(shape):
+    return [d for d in shape if d != 1]
+
+
+def sink_unit_reshapes(g, keep=()):
+    """F14 in place on `g` (a private copy).  Returns (count, moved outputs)."""
+    rw = _Rewriter(g, keep)
+    rw.replaced = {}
+    live = live_set(g, keep)
+    count = 0
+    for node in list(g.topo_order()):
+        if node.id not in g.nodes or node.kind != "reshape" or node.id not in live:
+            continue
+        count += _f14(rw, node, live)
+    return count, rw.replaced
+
+
+def _f14(rw, node, live):
+    g = rw.g
+    src = tuple(node.inputs[0])
+    e = rw.node(src)
+    readers = [n for n, _ in rw.users().get(src, []) if n.id in live]
+    if src[1] != 0 or len(readers) != 1 or src in rw.keep or e.output_arity != 1:
+        return 0
+    if e.kind not in _CHEAP_BCAST or not (_ew_eligible(g, e, "float") or _ew_eligible(g, e, "int")):
+        return 0
+    es, rs = g.ref_shape(src), g.ref_shape((node.id, 0))
+    if es is None or rs is None or None in es or None in rs or tuple(es) == tuple(rs):
+        return 0
+    # only for a broadcast operand of an elementwise reader (what F3 can then
+    # absorb); a reshape feeding a concat or a GEMM keeps the op where it is
+    rr = [n for n, _ in rw.users().get((node.id, 0), []) if n.id in live]
+    if not rr or not all((_ew_eligible(g, n, "float") or _ew_eligible(g, n, "int"))
+                         and tuple(n.out_shapes[0] or ()) != tuple(rs) for n in rr):
+        return 0
+    if _nonunit_dims(es) != _nonunit_dims(rs):
+        return 0
+    ins = []
+    for k in e.inputs:
+        sk = g.ref_shape(tuple(k))
+        if sk is None or None in sk:
+            return 0
+        if len(sk) == 0:
+            ins.append(tuple(k))
+        elif tuple(sk) == tuple(es):
+            r = g.add_node("reshape", [tuple(k)], {"shape": list(rs)})
+            ins.append((r.id, 0))
+        else:
+            return 0
+    new = g.add_node(e.kind, ins, dict(e.attrs))
+    rw.redirect((node.id, 0), Ref(g, new.id, 0))
+    return 1
 
 
 # ----------------------------------------------------------------------------
@@ -1069,6 +1132,16 @@ def _ew_eligible(g, node, domain="float"):
     if k == "select" and g.ref_dtype(node.inputs[0]) != DType.BOOL:
         return False
     return True
+
+
+_CHEAP_BCAST = frozenset({"less", "equal", "add", "sub", "mul", "neg", "logical_not", "select"})
+
+
+def _broadcasts_to(sh, shape):
+    if sh is None or len(sh) > len(shape):
+        return False
+    sh = (1,) * (len(shape) - len(sh)) + tuple(sh)
+    return all(a == b or a == 1 for a, b in zip(sh, shape))
 
 
 def _domains(g, node):
@@ -1216,9 +1289,17 @@ def fuse_elementwise(g, keep=()):
                     p = g.nodes[src[0]]
                     if p.id in group or p.id in assigned or src[1] != 0:
                         continue
-                    if not _ew_eligible(g, p, domain) or p.out_shapes[0] != shape:
+                    if not _ew_eligible(g, p, domain):
                         continue
                     outside = users.get(src, set()) - group
+                    if p.out_shapes[0] != shape:
+                        # a producer of a broadcast operand (F14): evaluated per
+                        # element of the group's shape, so only cheap ops
+                        # (compares, add/sub/mul, neg, logical not, select) and
+                        # only when nothing else reads it
+                        if (outside or src in keep or p.kind not in _CHEAP_BCAST
+                                or not _broadcasts_to(p.out_shapes[0], shape)):
+                            continue
                     if multi:
                         if any(pos[u] <= rpos for u in outside):
                             continue

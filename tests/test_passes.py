@@ -321,3 +321,19 @@ def test_f11_long_add_chain_becomes_one_reduction_sharing_f2_operand():
     # the same concat feeds the F2 GEMM (through its K-major transpose view)
     readers = [n for n in live if any(tuple(s) == (cat.id, 0) for s in n.inputs)]
     assert len(readers) == 2
+
+
+def test_f14_mask_compare_is_absorbed_into_the_select_group():
+    """cfg5 (masked, unrolled): reshape(less(reduce_sum(z), 0), [n, 1, 1])
+    becomes less(reshape(.), 0), which F3 evaluates inside the select group
+    per element of [n, 1, units] -- the loop body keeps no standalone compare
+    (oracle values unchanged)."""
+    from paper_1903_04243_b200 import passes
+    w = WL.cfg5(WL.this_api(), n=6, max_len=5, units=8, masked=True, unroll=2)
+    g, g2, m = _run_both(w)
+    bodies = [n.block.subgraphs["body"] for n in g2.nodes.values() if n.kind == "while"]
+    assert bodies
+    for body in bodies:
+        live = passes.live_set(body, [tuple(o) for o in body.outputs])
+        kinds = [body.nodes[i].kind for i in live]
+        assert "less" not in kinds and kinds.count("fused_ew") >= 2, sorted(kinds)
