@@ -284,6 +284,13 @@ int pfb_conv2d_filter_grad(const pfb_tensor* x, const pfb_tensor* gy, int32_t k1
                            pfb_tensor* out, pfb_tensor* sq_norm, void* stream);
 
 /* indexing (reference tensor.py:306-360, interp.py:210-221) */
+/* out[j, (q,) ...] = x[j, idx[j, (q)], ...] for x [n, m, ...], idx [n] or [n, q]:
+ * pfor's gather with a stacked operand and a stacked index (the reference's
+ * per-iteration fallback loop over tensor.gather_rows, tensor.py:306-318, and
+ * vectorize.py:271-273) in one launch; an index outside [0, m) sets
+ * PFB_DEV_OOB in dev_err. */
+int pfb_gather_stacked(const pfb_tensor* x, const pfb_tensor* idx, pfb_tensor* out,
+                       int32_t* dev_err, void* stream);
 int pfb_gather_rows(const pfb_tensor* x, const pfb_tensor* idx, pfb_tensor* out,
                     int32_t* dev_err, void* stream);
 int pfb_scatter_rows(int32_t n_parts, const pfb_tensor* index_sets, const pfb_tensor* parts,

@@ -9,11 +9,14 @@ namespace pfb {
 // ---------------------------------------------------------------------------
 // gather_rows: out[i, ...] = x[idx[i], ...]
 
-template <typename T, bool VEC>
+// SEG (gather_stacked): index i belongs to segment i / seg, whose rows start
+// at x + (i / seg) * seg_st -- out[j, q] = x[j, idx[j, q]], bounds [0, nrows)
+template <typename T, bool VEC, bool SEG = false>
 __global__ void __launch_bounds__(256) gather_kernel(Layout Lt, int64_t k, int64_t D,
                                                      const T* x, int64_t xrow, int64_t nrows,
                                                      const int64_t* idx, int64_t idx_st, T* out,
-                                                     int64_t orow, int32_t* err) {
+                                                     int64_t orow, int32_t* err, int64_t seg = 1,
+                                                     int64_t seg_st = 0) {
   pdl_enter();
   const int64_t per = VEC ? D / 4 : D;
   const int64_t total = k * per;
@@ -23,6 +26,7 @@ __global__ void __launch_bounds__(256) gather_kernel(Layout Lt, int64_t k, int64
     int64_t r = __ldg(idx + i * idx_st);
     bool ok = r >= 0 && r < nrows;
     if (!ok) set_err(err, PFB_DEV_OOB);
+    if constexpr (SEG) r += (i / seg) * (seg_st / xrow);  // seg_st % xrow == 0 (checked)
     if (VEC) {
       float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
       if constexpr (sizeof(T) == 4) {
@@ -62,11 +66,11 @@ int gather_run(const pfb_tensor* x, const pfb_tensor* idx, pfb_tensor* out, int3
   if (vec)
     launch(gather_kernel<T, true>, grid, 256, 0, s, Lt, k, D, (const T*)x->data, x->stride[0],
                                                  x->shape[0], (const int64_t*)idx->data, idx_st,
-                                                 (T*)out->data, orow, err);
+                                                 (T*)out->data, orow, err, (int64_t)1, (int64_t)0);
   else
     launch(gather_kernel<T, false>, grid, 256, 0, s, Lt, k, D, (const T*)x->data, x->stride[0],
                                                   x->shape[0], (const int64_t*)idx->data, idx_st,
-                                                  (T*)out->data, orow, err);
+                                                  (T*)out->data, orow, err, (int64_t)1, (int64_t)0);
   return launch_status();
 }
 
@@ -325,6 +329,64 @@ __global__ void rng_kernel(float* out, int64_t n, uint64_t dctr) {
 }  // namespace pfb
 
 using namespace pfb;
+
+// gather_stacked (x [n, m, ...], idx [n] or [n, q]): out[j, (q,) ...] =
+// x[j, idx[j, (q)], ...] -- pfor's gather with a stacked operand AND a stacked
+// index in one launch (the reference falls back to a sequential loop,
+// vectorize.py:271-273); an index outside [0, m) sets PFB_DEV_OOB.
+template <typename T>
+int gather_stacked_run(const pfb_tensor* x, const pfb_tensor* idx, pfb_tensor* out, int32_t* err,
+                       cudaStream_t s) {
+  const int64_t n = x->shape[0], m = x->shape[1];
+  const int64_t q = idx->rank == 2 ? idx->shape[1] : 1;
+  if (idx->shape[0] != n) return PFB_E_SHAPE;
+  if (idx->rank == 2 && q > 1 && idx->stride[0] != q * idx->stride[1]) return PFB_E_UNSUPPORTED;
+  const int64_t idx_st = idx->rank == 2 ? idx->stride[1] : idx->stride[0];
+  const int tail_rank = x->rank - 2;
+  const int o0 = idx->rank;  // first tail dim of out
+  if (out->rank != tail_rank + o0 || out->shape[0] != n || (idx->rank == 2 && out->shape[1] != q))
+    return PFB_E_SHAPE;
+  int64_t D = 1;
+  for (int d = 0; d < tail_rank; ++d) {
+    if (out->shape[o0 + d] != x->shape[2 + d]) return PFB_E_SHAPE;
+    D *= x->shape[2 + d];
+  }
+  // out rows [n * q] must be one stride apart; x's segment stride a multiple of its row stride
+  const int64_t orow = out->stride[o0 - 1];
+  if (idx->rank == 2 && q > 1 && out->stride[0] != q * orow) return PFB_E_UNSUPPORTED;
+  const int64_t xrow = x->stride[1];
+  if (n * q == 0 || D == 0) return 0;
+  if (xrow == 0 || x->stride[0] % xrow != 0) return PFB_E_UNSUPPORTED;
+  int64_t tail_shape[kMaxRank];
+  for (int d = 0; d < tail_rank; ++d) tail_shape[d] = x->shape[2 + d];
+  const int64_t* st[2] = {out->stride + o0, x->stride + 2};
+  Layout Lt = make_layout(tail_rank, tail_shape, 2, st);
+  const bool vec = sizeof(T) == 4 && Lt.rank == 1 && Lt.st[0][0] == 1 && Lt.st[1][0] == 1 &&
+                   D % 4 == 0 && xrow % 4 == 0 && x->stride[0] % 4 == 0 && orow % 4 == 0 &&
+                   (uintptr_t)x->data % 16 == 0 && (uintptr_t)out->data % 16 == 0;
+  const int64_t k = n * q;
+  const int grid = grid_for(k * (vec ? D / 4 : D), 256);
+  if (vec)
+    launch(gather_kernel<T, true, true>, grid, 256, 0, s, Lt, k, D, (const T*)x->data, xrow, m,
+           (const int64_t*)idx->data, idx_st, (T*)out->data, orow, err, (int64_t)q, (int64_t)x->stride[0]);
+  else
+    launch(gather_kernel<T, false, true>, grid, 256, 0, s, Lt, k, D, (const T*)x->data, xrow, m,
+           (const int64_t*)idx->data, idx_st, (T*)out->data, orow, err, (int64_t)q, (int64_t)x->stride[0]);
+  return launch_status();
+}
+
+extern "C" int pfb_gather_stacked(const pfb_tensor* x, const pfb_tensor* idx, pfb_tensor* out,
+                                  int32_t* dev_err, void* stream) {
+  if (idx->dtype != PFB_I64) return PFB_E_DTYPE;
+  if (idx->rank < 1 || idx->rank > 2 || x->rank < 2) return PFB_E_RANK;
+  if (x->dtype != out->dtype) return PFB_E_DTYPE;
+  cudaStream_t s = as_stream(stream);
+  switch (x->dtype) {
+    case PFB_F32: return gather_stacked_run<float>(x, idx, out, dev_err, s);
+    case PFB_I64: return gather_stacked_run<int64_t>(x, idx, out, dev_err, s);
+    default: return gather_stacked_run<uint8_t>(x, idx, out, dev_err, s);
+  }
+}
 
 extern "C" int pfb_gather_rows(const pfb_tensor* x, const pfb_tensor* idx, pfb_tensor* out,
                                int32_t* dev_err, void* stream) {

@@ -1693,6 +1693,23 @@ def _h_gather(ex, node, ins):
     return [out]
 
 
+def _h_gather_stacked(ex, node, ins):
+    """gather_stacked (vectorize.conv_gather_b200): out[j] = x[j][idx[j]], one
+    kernel (pfb_gather_stacked); an index outside [0, m) sets the device
+    error word -> ExecError(IndexOutOfBounds)."""
+    x, idx = ex._dev(ins[0]), ex._dev(ins[1])
+    if idx.dtype != DType.I64:
+        raise E.DTypeMismatch("gather_rows: index must be i64")
+    if x.rank < 2 or not 1 <= idx.rank <= 2 or idx.shape[0] != x.shape[0]:
+        raise E.IncompatibleShapes(f"gather_stacked: {x.shape} vs index {idx.shape}")
+    out = ex._empty(tuple(idx.shape) + x.shape[2:], x.dtype)
+    if idx.rank == 2:
+        idx = ex._dense(idx)
+    ex._call(ex._lib.pfb_gather_stacked, x.desc(), idx.desc(), out.desc(), ex._err_slot(node),
+             ex._stream, what="gather_rows")
+    return [out]
+
+
 def _h_scatter_rows(ex, node, ins):
     n = node.attrs["num_parts"]
     sets = [ex._dev(v) for v in ins[:n]]
@@ -2025,7 +2042,7 @@ _HANDLERS.update({
     "fused_pack": _h_fused_pack,
     "matmul2": _h_matmul2,
     "fused_int": _h_fused_int,
-    "gather_rows": _h_gather, "scatter_rows": _h_scatter_rows,
+    "gather_rows": _h_gather, "gather_stacked": _h_gather_stacked, "scatter_rows": _h_scatter_rows,
     "scatter_add_rows": _h_scatter_add, "reshape": _h_reshape, "transpose": _h_transpose,
     "slice_leading": _h_slice_leading, "tile_leading": _h_tile_leading,
     "where_true": _h_where_true, "complement": _h_complement, "dim0": _h_dim0,

@@ -697,7 +697,7 @@ _NO_LICM = frozenset({"read_variable", "assign", "assign_add", "random_uniform",
 # ops that raise on their data (index out of range, scatter collision /
 # incomplete cover): hoisted out of a while body they would run -- and raise
 # -- on a zero-trip loop whose body the reference never evaluates
-_MAY_RAISE = frozenset({"gather_rows", "scatter_rows", "scatter_add_rows"})
+_MAY_RAISE = frozenset({"gather_rows", "gather_stacked", "scatter_rows", "scatter_add_rows"})
 
 
 def _provably_safe(g, wnode, body, n):

@@ -137,8 +137,9 @@ def test_f7_dual_matmul_sum_and_concat():
 
 @pytest.mark.parametrize("kw", [dict(masked=True, unroll=4), dict(masked=True, unroll=1), dict()])
 def test_f8_loop_invariants_leave_the_while_body(kw):
-    """F8: the per-trip row-index iota (range_vec of a captured size) and its
-    products move out of cfg5's while body as new captures -- values unchanged."""
+    """F8: no per-trip iota is left in cfg5's while body (the B200 registry's
+    stacked gather needs none; a range_vec of a captured size would move out
+    as a new capture) -- values unchanged."""
     w = WL.cfg5(WL.this_api(), n=6, max_len=5, units=8, **kw)
     g, g2, _ = _run_both(w)
 
@@ -151,7 +152,7 @@ def test_f8_loop_invariants_leave_the_while_body(kw):
     w0, k0 = body_kinds(g)
     w1, k1 = body_kinds(g2)
     assert "range_vec" not in k1
-    if kw:  # masked conversion: the hoisted values arrive as new captures
+    if "range_vec" in k0:  # hoisted values arrive as new captures
         assert len(w1.inputs) > len(w0.inputs)
 
 
