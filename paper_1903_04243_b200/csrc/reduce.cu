@@ -579,35 +579,43 @@ extern "C" int pfb_row_dots(int32_t n, const pfb_tensor* xs, const pfb_tensor* y
 // tensor first.  One CTA per row; fixed per-thread order + tree: deterministic.
 
 namespace pfb {
-__global__ void __launch_bounds__(256) row_sum_parts_kernel(const float* __restrict__ x,
+__global__ void __launch_bounds__(128) row_sum_parts_kernel(const float* __restrict__ x,
                                                             int64_t rs, int64_t W, int S,
                                                             int64_t ps, float* out, int64_t so) {
   pdl_enter();
+  // one 128-thread CTA per row; its (partial, column) items spread over the
+  // CTA in batches of 4 loads issued before they are added (cfg5: 8 partials
+  // x 64 float4 = one batch per thread); fixed order, shuffle + smem tree
   const int64_t i = blockIdx.x;
   Acc<float> acc;
   const bool vec = (W % 4 == 0) && (rs % 4 == 0) && (ps % 4 == 0) &&
                    ((reinterpret_cast<uintptr_t>(x) & 15) == 0);
-  for (int s = 0; s < S; ++s) {
-    const float* r = x + s * ps + i * rs;
-    if (vec) {
-      const float4* r4 = reinterpret_cast<const float4*>(r);
-      for (int64_t k = threadIdx.x; k < W / 4; k += blockDim.x) {
-        const float4 a = __ldg(r4 + k);
-        acc.add((a.x + a.y) + (a.z + a.w));
+  const int64_t wv = vec ? W / 4 : W, items = (int64_t)S * wv;
+  for (int64_t it0 = threadIdx.x; it0 < items; it0 += 4 * (int64_t)blockDim.x) {
+    float v[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int64_t it = it0 + u * (int64_t)blockDim.x;
+      v[u] = 0.f;
+      if (it < items) {
+        const int64_t s = it / wv, k = it - s * wv;
+        const float* r = x + s * ps + i * rs;
+        if (vec) {
+          const float4 a = __ldg(reinterpret_cast<const float4*>(r) + k);
+          v[u] = (a.x + a.y) + (a.z + a.w);
+        } else {
+          v[u] = __ldg(r + k);
+        }
       }
-    } else {
-      for (int64_t k = threadIdx.x; k < W; k += blockDim.x) acc.add(__ldg(r + k));
     }
+#pragma unroll
+    for (int u = 0; u < 4; ++u) acc.add(v[u]);
   }
-  __shared__ float red[8];
+  __shared__ float red[4];
   const float v = warp_sum(acc.s);
   if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = v;
   __syncthreads();
-  if (threadIdx.x == 0) {
-    float t = 0.f;
-    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) t += red[w];
-    out[i * so] = t;
-  }
+  if (threadIdx.x == 0) out[i * so] = (red[0] + red[1]) + (red[2] + red[3]);
 }
 }  // namespace pfb
 
@@ -619,7 +627,7 @@ extern "C" int pfb_row_sum_parts(const pfb_tensor* x, int32_t parts, int64_t par
     return PFB_E_SHAPE;
   if (x->shape[1] > 1 && x->stride[1] != 1) return PFB_E_UNSUPPORTED;
   if (x->shape[0] == 0) return 0;
-  launch(row_sum_parts_kernel, dim3((unsigned)x->shape[0]), dim3(256), 0, as_stream(stream),
+  launch(row_sum_parts_kernel, dim3((unsigned)x->shape[0]), dim3(128), 0, as_stream(stream),
          (const float*)x->data, x->stride[0], x->shape[1], (int)parts, part_stride,
          (float*)out->data, out->stride[0]);
   return launch_status();
