@@ -150,6 +150,9 @@ int pfb_fill(pfb_tensor* out, double value, void* stream);
 /* pack n dense tensors into one byte buffer at dst + dst_offsets[i] (one
  * launch per 16): the executor's single D2H of a run's outputs and device
  * error words (reference Executor.run returns host values, interp.py:109-125). */
+/* n dense copies srcs[k] -> dsts[k] (same dtype and element count) in one
+ * launch: a device-resident loop's carried values back into its state */
+int pfb_copy_many(int32_t n, const pfb_tensor* srcs, const pfb_tensor* dsts, void* stream);
 int pfb_pack(int32_t n, const pfb_tensor* xs, void* dst, const int64_t* dst_offsets, void* stream);
 /* concat of n same-dtype inputs (any strides) along `axis` into out, in one
  * launch per 24 inputs (reference tensor.concat, tensor.py:383-393). */

@@ -60,6 +60,7 @@ _SIGNATURES = {
     "pfb_select": ([_P, _P, _P, _P, _vp], ctypes.c_int),
     "pfb_reduce_sum": ([_P, _u32, _P, _vp, _i64, _vp], ctypes.c_int),
     "pfb_copy": ([_P, _P, _vp], ctypes.c_int),
+    "pfb_copy_many": ([_i32, _P, _P, _vp], ctypes.c_int),
     "pfb_pack": ([_i32, _P, _vp, ctypes.POINTER(_i64), _vp], ctypes.c_int),
     "pfb_fill": ([_P, _f64, _vp], ctypes.c_int),
     "pfb_matmul_workspace": ([_P, _P, _P], ctypes.c_int64),

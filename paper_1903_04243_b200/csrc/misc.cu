@@ -112,6 +112,58 @@ extern "C" int pfb_pack(int32_t n, const pfb_tensor* xs, void* dst, const int64_
   return 0;
 }
 
+// copy_many: several dense tensor copies in one launch (a device-resident
+// loop's carried values written back into its static state each trip).
+
+namespace pfb {
+struct CopyDesc {
+  const uint8_t* src[kMaxPack];
+  uint8_t* dst[kMaxPack];
+  int64_t bytes[kMaxPack];
+};
+
+__global__ void __launch_bounds__(256) copy_many_kernel(CopyDesc d) {
+  pdl_enter();
+  const int t = blockIdx.y;
+  const uint8_t* s = d.src[t];
+  uint8_t* o = d.dst[t];
+  const int64_t nb = d.bytes[t];
+  const bool vec = ((reinterpret_cast<uintptr_t>(s) | reinterpret_cast<uintptr_t>(o)) & 15) == 0;
+  const int64_t n16 = vec ? nb / 16 : 0;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n16; i += stride)
+    reinterpret_cast<int4*>(o)[i] = __ldg(reinterpret_cast<const int4*>(s) + i);
+  for (int64_t i = 16 * n16 + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < nb; i += stride)
+    o[i] = s[i];
+}
+}  // namespace pfb
+
+extern "C" int pfb_copy_many(int32_t n, const pfb_tensor* srcs, const pfb_tensor* dsts,
+                             void* stream) {
+  if (n < 0) return PFB_E_ARG;
+  cudaStream_t s = as_stream(stream);
+  for (int base = 0; base < n; base += kMaxPack) {
+    CopyDesc d = {};
+    const int m = n - base < kMaxPack ? n - base : kMaxPack;
+    int64_t most = 0;
+    for (int j = 0; j < m; ++j) {
+      const pfb_tensor* x = &srcs[base + j];
+      const pfb_tensor* y = &dsts[base + j];
+      if (!is_dense(x) || !is_dense(y) || x->dtype != y->dtype || numel(x) != numel(y))
+        return PFB_E_UNSUPPORTED;
+      d.src[j] = static_cast<const uint8_t*>(x->data);
+      d.dst[j] = static_cast<uint8_t*>(y->data);
+      d.bytes[j] = numel(x) * dtype_size(x->dtype);
+      if (d.bytes[j] > most) most = d.bytes[j];
+    }
+    if (most == 0) continue;
+    const int gx = grid_for((most + 15) / 16, 256, 2);
+    launch(copy_many_kernel, dim3((unsigned)gx, (unsigned)m), 256, 0, s, d);
+    if (int e = launch_status()) return e;
+  }
+  return 0;
+}
+
 // kernels this library has launched so far in the process (graph captures
 // included: a captured launch is counted once, when recorded)
 extern "C" int64_t pfb_kernel_launches(void) { return pfb::kernel_launches().load(); }

@@ -590,9 +590,9 @@ class Executor:
             cap = self._capture_sub(sub, caps, car, feeds, sig)
             if cap is None:
                 return self._run_graph(sub, bind, feeds)
-        for src, dst in zip(car, cap.inputs):
-            if src.size:
-                self._call(self._lib.pfb_copy, src.desc(), dst.desc(), self._stream, what="copy")
+        # (outputs never alias the static inputs -- detached at capture -- so
+        # the copies may run concurrently in one launch)
+        self._copy_pairs([(src, dst) for src, dst in zip(car, cap.inputs) if src.size])
         cap.graph.replay()
         self.launch_count += cap.launches
         self.dispatch_count += cap.dispatches
@@ -740,10 +740,7 @@ class Executor:
                         srcs.append(self._dense_copy(src))
                     else:
                         srcs.append(src)
-                for src, dst in zip(srcs, state):
-                    if src is not None:
-                        self._call(self._lib.pfb_copy, src.desc(), dst.desc(), self._stream,
-                                   what="copy")
+                self._copy_pairs([(src, dst) for src, dst in zip(srcs, state) if src is not None])
                 cond_to_handle()
             l2 = self.launch_count
             rc = self._lib.pfb_loop_finalize(loop, ctypes.c_void_p(head.raw_cuda_graph()),
@@ -932,6 +929,22 @@ class Executor:
             self.kernel_timer.append((what, nbytes, flops, st, en, fn, args))
         finally:
             self.launch_count += self._lib.pfb_kernel_launches() - k0
+
+    def _copy_pairs(self, pairs):
+        """src -> dst copies: the dense ones in one launch (pfb_copy_many)."""
+        dense = [(a, b) for a, b in pairs if a.is_dense() and b.is_dense() and a.size == b.size]
+        rest = [(a, b) for a, b in pairs if (a, b) not in dense]
+        if len(dense) == 1:
+            rest += dense
+            dense = []
+        if dense:
+            n = len(dense)
+            xs = (N.PfbTensor * n)(*[a.desc() for a, _ in dense])
+            ys = (N.PfbTensor * n)(*[b.desc() for _, b in dense])
+            self._call(self._lib.pfb_copy_many, n, xs, ys, self._stream, what="copy",
+                       work=(2 * _abytes(*[a for a, _ in dense]), 0))
+        for a, b in rest:
+            self._call(self._lib.pfb_copy, a.desc(), b.desc(), self._stream, what="copy")
 
     def _dense(self, x):
         if x.is_dense():
