@@ -95,6 +95,19 @@ int pfb_fused_ew_multi(int32_t n_in, const pfb_tensor* ins, int32_t n_steps,
 int pfb_fused_ew_parts(int32_t n_in, const pfb_tensor* ins, const int64_t* parts,
                        int32_t n_steps, const int32_t* program, int32_t n_out,
                        const int32_t* out_regs, pfb_tensor* outs, void* stream);
+/* pfb_fused_ew_parts with row-sum feeds (pass F16): rowsum[k] >= 0 makes
+ * input k the sum of input rowsum[k] over the row (the innermost dim of the
+ * outputs' layout) -- ins[k] then only describes the broadcast shape (its
+ * data is not read); rowsum[k] < 0 = a normal input.  The sums are computed
+ * in the kernel (one row per block: a whole number of warps, <= 1024 wide),
+ * so a row reduction feeding an elementwise group costs no launch of its own
+ * (cfg5's per-step `reduce_sum(z) < 0` branch mask; reference
+ * tensor.reduce_sum, tensor.py:279-283).  parts nullable.  PFB_E_UNSUPPORTED
+ * when the row does not fit or NVRTC is absent (the caller then computes the
+ * sums with pfb_row_sum_parts / pfb_reduce_sum). */
+int pfb_fused_ew_rows(int32_t n_in, const pfb_tensor* ins, const int64_t* parts,
+                      const int32_t* rowsum, int32_t n_steps, const int32_t* program,
+                      int32_t n_out, const int32_t* out_regs, pfb_tensor* outs, void* stream);
 /* out[i] = sum_s sum_k x_s[i, k], x_s = x + s * part_stride (x: [rows, W] view
  * with unit inner stride): the row sums of a GEMM result still held as
  * split-K partials (pass F15; reference tensor.reduce_sum, tensor.py:279-283). */

@@ -783,8 +783,19 @@ extern "C" int pfb_fill(pfb_tensor* out, double value, void* stream) {
 
 static int fused_impl(int32_t n_in, const pfb_tensor* ins, int32_t n_steps,
                       const int32_t* program, int32_t n_out, const int32_t* out_regs,
-                      pfb_tensor* outs, void* stream, const int64_t* parts = nullptr) {
+                      pfb_tensor* outs, void* stream, const int64_t* parts = nullptr,
+                      const int32_t* rowsum = nullptr) {
   if (n_in < 1 || n_in > kMaxIn || n_steps < 1 || n_steps > kMaxSteps) return PFB_E_ARG;
+  int RS[kMaxIn];
+  if (rowsum) {
+    bool any = false;
+    for (int k = 0; k < n_in; ++k) {
+      RS[k] = rowsum[k] < 0 ? -1 : rowsum[k];
+      if (RS[k] >= n_in) return PFB_E_ARG;
+      any = any || RS[k] >= 0;
+    }
+    if (!any) rowsum = nullptr;
+  }
   PartsSpec PS{};
   if (parts) {
     for (int k = 0; k < n_in; ++k) {
@@ -841,7 +852,7 @@ static int fused_impl(int32_t n_in, const pfb_tensor* ins, int32_t n_steps,
   // elements) one element per thread: the program's latency chain runs on 4x
   // the warps (cfg4 step 2.76 -> 2.58 ms); 4 per thread (128-bit accesses)
   // where the launch is HBM-bound
-  const bool v4 = L.shape[ir] % 4 == 0 && !scalar_only && n >= (int64_t)1 << 20;
+  const bool v4 = !rowsum && L.shape[ir] % 4 == 0 && !scalar_only && n >= (int64_t)1 << 20;
   // per-operand feed mode; the outputs share operand 0's (all must be aligned)
   FeedModes modes = 0;
   for (int o = 0; o <= n_in; ++o) {
@@ -861,6 +872,11 @@ static int fused_impl(int32_t n_in, const pfb_tensor* ins, int32_t n_steps,
     modes |= m << (2 * o);
   }
   const int64_t ng = v4 ? n / 4 : n;
+  if (rowsum) {  // F16 row-sum feeds: the specialised row kernel or nothing
+    if (!fused_rows_jit_launch(P, modes, L, n, fo, fi, s, parts ? &PS : nullptr, RS))
+      return PFB_E_UNSUPPORTED;
+    return launch_status();
+  }
   if (fused_jit_launch(P, v4 ? 4 : 1, !small, modes, L, ng, fo, fi, s, parts ? &PS : nullptr))
     return launch_status();
   if (parts) return PFB_E_UNSUPPORTED;  // partial sums: specialised kernels only
@@ -891,6 +907,13 @@ extern "C" int pfb_fused_ew_parts(int32_t n_in, const pfb_tensor* ins, const int
                                   int32_t n_steps, const int32_t* program, int32_t n_out,
                                   const int32_t* out_regs, pfb_tensor* outs, void* stream) {
   return fused_impl(n_in, ins, n_steps, program, n_out, out_regs, outs, stream, parts);
+}
+
+extern "C" int pfb_fused_ew_rows(int32_t n_in, const pfb_tensor* ins, const int64_t* parts,
+                                 const int32_t* rowsum, int32_t n_steps, const int32_t* program,
+                                 int32_t n_out, const int32_t* out_regs, pfb_tensor* outs,
+                                 void* stream) {
+  return fused_impl(n_in, ins, n_steps, program, n_out, out_regs, outs, stream, parts, rowsum);
 }
 
 // ---------------------------------------------------------------------------

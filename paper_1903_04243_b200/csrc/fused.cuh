@@ -55,6 +55,14 @@ bool fused_jit_launch(const FusedProgram& P, int V, bool idx64, FeedModes modes,
                       int64_t ngroups, const FusedOuts& outs, const FusedIns& ins,
                       cudaStream_t s, const PartsSpec* parts = nullptr);
 
+// Row-sum feeds (pass F16): rowsum[k] >= 0 makes input k the sum of input
+// rowsum[k] (after its partials) over the layout's innermost dim, computed in
+// the kernel (one row per block); false when the shape does not fit (the
+// caller then materialises the sums).  V = 1, specialised kernels only.
+bool fused_rows_jit_launch(const FusedProgram& P, FeedModes modes, const FLayout& L, int64_t n,
+                           const FusedOuts& outs, const FusedIns& ins, cudaStream_t s,
+                           const PartsSpec* parts, const int* rowsum);
+
 // the same for an integer-domain program (fused_int_kernel), one element per
 // thread
 bool fused_int_jit_launch(const FusedProgram& P, bool idx64, const FLayout& L, int64_t n,

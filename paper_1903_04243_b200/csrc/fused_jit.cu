@@ -157,18 +157,20 @@ std::string gen_offsets(const FLayout& L, int nops, int V, bool idx64, bool off3
 
 std::string gen_source(const FusedProgram& P, int V, bool idx64, FeedModes modes,
                        const PartsSpec* PS = nullptr, const FLayout* LS = nullptr,
-                       bool off32 = false) {
+                       bool off32 = false, const int* RS = nullptr) {
   std::string s = fmt(kPrelude, kMaxRank, kMaxFOps, kMaxRank, kMaxOuts, kMaxIn);
   const char* IT = idx64 ? "i64" : "unsigned";
   const int nops = P.n_in + 1;
   auto nparts = [&](int k) { return (PS && PS->S[k] > 1) ? PS->S[k] : 1; };
+  // row-sum feeds: one row per block, blockDim = the row (baked layout)
+  const int nthr = (RS && LS) ? (int)LS->shape[LS->rank - 1] : 256;
   if (PS) {
     s += fmt("struct Parts { i64 st[%d]; };\n", kMaxIn);
-    s += fmt("extern \"C\" __global__ void __launch_bounds__(256) pfb_fused_jit(Layout L, %s ngroups, "
-             "Outs outs, Ins ins, Parts PT) {\n", IT);
+    s += fmt("extern \"C\" __global__ void __launch_bounds__(%d) pfb_fused_jit(Layout L, %s ngroups, "
+             "Outs outs, Ins ins, Parts PT) {\n", nthr, IT);
   } else {
-    s += fmt("extern \"C\" __global__ void __launch_bounds__(256) pfb_fused_jit(Layout L, %s ngroups, "
-             "Outs outs, Ins ins) {\n", IT);
+    s += fmt("extern \"C\" __global__ void __launch_bounds__(%d) pfb_fused_jit(Layout L, %s ngroups, "
+             "Outs outs, Ins ins) {\n", nthr, IT);
   }
   s += "  asm volatile(\"griddepcontrol.wait;\" ::: \"memory\");\n"
        "  asm volatile(\"griddepcontrol.launch_dependents;\" :::);\n"
@@ -190,6 +192,7 @@ std::string gen_source(const FusedProgram& P, int V, bool idx64, FeedModes modes
   }
   // input feeds (all loads first, as in the interpreter)
   for (int k = 0; k < P.n_in; ++k) {
+    if (RS && RS[k] >= 0) continue;  // a row sum of another input (below)
     const int md = (int)((modes >> (2 * (k + 1))) & 3);
     const bool bl = P.in_dtype[k] == PFB_BOOL;
     const char* T = bl ? "unsigned char" : "float";
@@ -234,6 +237,24 @@ std::string gen_source(const FusedProgram& P, int V, bool idx64, FeedModes modes
       s += fmt("    const i64 sin%d = L.st[%d][ir];\n", k, k + 1);
       for (int j = 0; j < V; ++j)
         s += fmt("    const float in%d_%d = (float)__ldg(p%d + %d * sin%d);\n", k, j, k, j, k);
+    }
+  }
+  // row-sum feeds (pass F16): input k = the sum of input RS[k] over the row
+  // (the layout's innermost dim, one row per block of blockDim = W threads,
+  // V = 1): each thread's value, a fixed xor-shuffle tree per warp, then the
+  // warps' sums left to right -- the same order in every block
+  if (RS) {
+    bool any = false;
+    for (int k = 0; k < P.n_in; ++k) {
+      if (RS[k] < 0) continue;
+      if (!any) s += "    __shared__ float rs_red[32];\n    const int rs_w = threadIdx.x >> 5, rs_l = threadIdx.x & 31;\n";
+      any = true;
+      s += fmt("    float in%d_0;\n    { float v = in%d_0;\n", k, RS[k]);
+      s += "      for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);\n"
+           "      if (rs_l == 0) rs_red[rs_w] = v;\n      __syncthreads();\n"
+           "      float t = rs_red[0];\n      for (int w = 1; w < (int)(blockDim.x >> 5); ++w) t += rs_red[w];\n"
+           "      __syncthreads();\n";
+      s += fmt("      in%d_0 = t; }\n", k);
     }
   }
   // the program: reg -> current SSA name
@@ -441,11 +462,12 @@ namespace {
 
 // kernel for a program (integer: the i64 domain), compiled on first use
 CUfunction lookup(const FusedProgram& P, int V, bool idx64, FeedModes modes, bool integer,
-                  const PartsSpec* PS = nullptr, const FLayout* LS = nullptr, bool off32 = false) {
+                  const PartsSpec* PS = nullptr, const FLayout* LS = nullptr, bool off32 = false,
+                  const int* RS = nullptr) {
   int dev = 0;
   cudaGetDevice(&dev);
   // cache key: the program's encoding and everything baked into the source
-  int32_t kb[14 + 2 * kMaxIn + 4 * kMaxSteps + 2 * kMaxOuts + 2 * kMaxRank * (kMaxFOps + 1)];
+  int32_t kb[15 + 3 * kMaxIn + 4 * kMaxSteps + 2 * kMaxOuts + 2 * kMaxRank * (kMaxFOps + 1)];
   int nk = 0;
   kb[nk++] = dev; kb[nk++] = V; kb[nk++] = idx64; kb[nk++] = (int32_t)(modes & 0xffffffffu);
   kb[nk++] = (int32_t)(modes >> 32); kb[nk++] = integer;
@@ -457,6 +479,9 @@ CUfunction lookup(const FusedProgram& P, int V, bool idx64, FeedModes modes, boo
   kb[nk++] = PS != nullptr;
   if (PS)
     for (int k = 0; k < P.n_in; ++k) kb[nk++] = PS->S[k];
+  kb[nk++] = RS != nullptr;
+  if (RS)
+    for (int k = 0; k < P.n_in; ++k) kb[nk++] = RS[k];
   kb[nk++] = LS != nullptr;
   if (LS) {  // the layout baked into the source (64-bit values as two words)
     kb[nk++] = LS->rank;
@@ -477,15 +502,15 @@ CUfunction lookup(const FusedProgram& P, int V, bool idx64, FeedModes modes, boo
   auto it = cache.find(key);
   if (it == cache.end())
     it = cache.emplace(key, compile(integer ? gen_source_int(P, idx64)
-                                            : gen_source(P, V, idx64, modes, PS, LS, off32))).first;
+                                            : gen_source(P, V, idx64, modes, PS, LS, off32, RS))).first;
   return it->second;
 }
 
 bool run(CUfunction fn, bool idx64, const FLayout& L, int64_t nitems, const FusedOuts& outs,
-         const FusedIns& ins, cudaStream_t s, const PartsSpec* PS = nullptr) {
+         const FusedIns& ins, cudaStream_t s, const PartsSpec* PS = nullptr, int block = 256) {
   CUlaunchConfig cfg = {};
-  cfg.gridDimX = grid_for(nitems, 256); cfg.gridDimY = 1; cfg.gridDimZ = 1;
-  cfg.blockDimX = 256; cfg.blockDimY = 1; cfg.blockDimZ = 1;
+  cfg.gridDimX = grid_for(nitems, block); cfg.gridDimY = 1; cfg.gridDimZ = 1;
+  cfg.blockDimX = block; cfg.blockDimY = 1; cfg.blockDimZ = 1;
   cfg.hStream = (CUstream)s;
   CUlaunchAttribute attr[1];
   attr[0].id = CU_LAUNCH_ATTRIBUTE_PROGRAMMATIC_STREAM_SERIALIZATION;
@@ -532,6 +557,37 @@ bool fused_jit_launch(const FusedProgram& P, int V, bool idx64, FeedModes modes,
   }
   CUfunction fn = lookup(P, V, idx64, modes, false, parts, LS, off32);
   return fn && run(fn, idx64, L, ngroups, outs, ins, s, parts);
+}
+
+bool fused_rows_jit_launch(const FusedProgram& P, FeedModes modes, const FLayout& L,
+                           int64_t n, const FusedOuts& outs, const FusedIns& ins, cudaStream_t s,
+                           const PartsSpec* parts, const int* rowsum) {
+  if (parts && !parts->any()) parts = nullptr;
+  if (!usable(INT64_MAX) || L.rank < 1) return false;
+  const int ir = L.rank - 1;
+  const int64_t W = L.shape[ir];
+  // one row per block: W threads, a whole number of warps, rows = every
+  // coordinate of the outer dims; each row-sum input broadcasts along the
+  // row and varies along every outer dim (so a row is exactly its extent-1
+  // axes)
+  if (W < 32 || W > 1024 || W % 32 != 0 || n % W != 0) return false;
+  for (int k = 0; k < P.n_in; ++k) {
+    if (rowsum[k] < 0) continue;
+    if (rowsum[k] >= P.n_in || rowsum[k] == k || rowsum[rowsum[k]] >= 0 ||
+        P.in_dtype[rowsum[k]] != PFB_F32 || L.st[k + 1][ir] != 0)
+      return false;
+    for (int d = 0; d < ir; ++d)
+      if (L.shape[d] > 1 && L.st[k + 1][d] == 0) return false;
+  }
+  double mx = 0;
+  for (int o = 0; o <= P.n_in; ++o) {
+    double m = 0;
+    for (int d = 0; d < L.rank; ++d) m += (double)(L.shape[d] - 1) * std::fabs((double)L.st[o][d]);
+    mx = std::max(mx, m);
+  }
+  const bool idx64 = n >= (int64_t)0x7fffffff;
+  CUfunction fn = lookup(P, 1, idx64, modes, false, parts, &L, mx < 2147483647.0, rowsum);
+  return fn && run(fn, idx64, L, n, outs, ins, s, parts, (int)W);
 }
 
 bool fused_int_jit_launch(const FusedProgram& P, bool idx64, const FLayout& L, int64_t n,

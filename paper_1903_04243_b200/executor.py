@@ -1877,6 +1877,62 @@ def _fused_launch(ex, arrs, prog, regs, nregs, outs):
              work=(_abytes(*arrs, *outs), 0))
 
 
+def _fused_rows(ex, node, arrs, prog, regs, nregs, outs):
+    """A group with row-sum feeds (pass F16, attrs["rowsum"] = ((k, j), ..)):
+    input k is the sum of input j over the row, computed by the group's own
+    kernel (pfb_fused_ew_rows; slot k carries input j's array, described with
+    the sum's broadcast shape [n, 1, .., 1]).  Rows the kernel does not take
+    (not a whole number of warps, > 1024 wide, no NVRTC) get their sums
+    materialised first (reduce_sum as before) and the group runs as usual."""
+    rs = dict(node.attrs["rowsum"])
+    shape = outs[0].shape
+    bshape = (shape[0],) + (1,) * (len(shape) - 1)
+    views = list(arrs)
+    for k, j in rs.items():
+        x = arrs[j]
+        views[k] = DArray(x.buf, x.offset, bshape, (x.strides[0],) + (0,) * (len(shape) - 1),
+                          x.dtype)
+    if ex._lib.pfb_fused_parts_ok():
+        views = [ex._reduce_parts(a) if a.parts is not None and id(a.buf) in ex._parts_dense
+                 else a for a in views]
+        spec = []
+        for a in views:
+            spec += list(a.parts) if a.parts is not None else [1, 0]
+        pa = (ctypes.c_int64 * len(spec))(*spec)
+        rsa = (ctypes.c_int32 * len(views))(*[rs.get(k, -1) for k in range(len(views))])
+        descs = (N.PfbTensor * len(views))(*[a.desc_part0() for a in views])
+        odescs = (N.PfbTensor * len(outs))(*[o.desc() for o in outs])
+        nbytes = sum(_abytes(a) * (a.parts[0] if a.parts else 1)
+                     for k, a in enumerate(views) if k not in rs)
+        status = []
+
+        def rows(*args):  # PFB_E_UNSUPPORTED -> materialised sums below
+            rc = ex._lib.pfb_fused_ew_rows(*args)
+            status.append(rc)
+            return 0 if rc == N.E_UNSUPPORTED else rc
+        ex._call(rows, len(views), descs, pa, rsa, prog[1], prog[0], nregs, regs, odescs,
+                 ex._stream, what="fused_ew", work=(nbytes + _abytes(*outs), 0))
+        if status[-1] == 0:
+            return
+    for k, j in rs.items():
+        stub = _NodeStub({"axes": tuple(range(1, len(shape)))})
+        (sm,) = _h_reduce_sum(ex, stub, [arrs[j]])
+        views[k] = sm.view(bshape, (sm.strides[0],) + (0,) * (len(shape) - 1))
+    if any(a.parts is not None for a in views) or nregs != 1:
+        _fused_launch(ex, views, prog, regs, nregs, outs)
+        return
+    descs = (N.PfbTensor * len(views))(*[a.desc() for a in views])
+    ex._call(ex._lib.pfb_fused_ew, len(views), descs, prog[1], prog[0], outs[0].desc(), ex._stream,
+             what="fused_ew", work=(_abytes(*views, *outs), 0))
+
+
+class _NodeStub:
+    __slots__ = ("attrs",)
+
+    def __init__(self, attrs):
+        self.attrs = attrs
+
+
 def _h_fused(ex, node, ins):
     """fused_ew (passes.fuse_elementwise): one launch for a chain of elementwise
     ops; the program rides in the node attrs."""
@@ -1890,6 +1946,10 @@ def _h_fused(ex, node, ins):
         flat = [int(x) for step in node.attrs["program"] for x in step]
         prog = ex._programs[id(node)] = ((ctypes.c_int32 * len(flat))(*flat),
                                          len(node.attrs["program"]))
+    if node.attrs.get("rowsum"):
+        last = node.attrs["program"][-1][1]
+        _fused_rows(ex, node, arrs, prog, (ctypes.c_int32 * 1)(last), 1, [out])
+        return [out]
     if any(a.parts is not None for a in arrs):
         last = node.attrs["program"][-1][1]
         _fused_launch(ex, arrs, prog, (ctypes.c_int32 * 1)(last), 1, [out])
@@ -1915,7 +1975,10 @@ def _h_fused_multi(ex, node, ins):
         prog = ex._programs[id(node)] = ((ctypes.c_int32 * len(flat))(*flat),
                                          len(node.attrs["program"]),
                                          (ctypes.c_int32 * len(regs))(*regs), len(regs))
-    _fused_launch(ex, arrs, prog, prog[2], prog[3], outs)
+    if node.attrs.get("rowsum"):
+        _fused_rows(ex, node, arrs, prog, prog[2], prog[3], outs)
+    else:
+        _fused_launch(ex, arrs, prog, prog[2], prog[3], outs)
     return outs
 
 

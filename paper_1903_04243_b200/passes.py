@@ -987,7 +987,7 @@ def _pipeline(elementwise):
            fuse_outer_products, fuse_conv_filter_grads, eliminate_common_subexpressions,
            fuse_reductions, fuse_row_dots, fuse_dual_matmuls, fuse_matmul_epilogues]
     if elementwise:
-        seq += [sink_unit_reshapes, fuse_elementwise, place_concats]
+        seq += [sink_unit_reshapes, fuse_elementwise, place_concats, fuse_row_sums]
     return seq
 
 
@@ -1745,3 +1745,68 @@ def _f13b(rw, node, claimed, DType):
         rw.redirect((fid, k), Ref(g, new.id, k))
     rw.redirect((node.id, 0), Ref(g, new.id, n_out))
     return 1
+
+
+# ----------------------------------------------------------------------------
+# F16: row sums computed by the elementwise group that reads them
+#
+# fused(..., X, reshape(reduce_sum(X, axes 1..), [n, 1, .., 1]), ...) -- a row
+# sum of one of the group's own inputs, broadcast back along the row (cfg5's
+# per-step branch mask `reduce_sum(z) < 0`, whose compare F14 already moved
+# into the select group) -- becomes a row-sum feed of the group
+# (attrs["rowsum"] = ((k, j), ...): input k is the row sum of input j, and
+# slot k carries X itself).  The executor's row kernel sums each row in the
+# block that evaluates it (pfb_fused_ew_rows): the reduction is no longer a
+# launch of its own (reference tensor.reduce_sum, tensor.py:279-283; the
+# values are the same sums in a different fp32 association).
+
+def fuse_row_sums(g, keep=()):
+    """F16 in place on `g` (a private copy).  Returns (count, moved outputs)."""
+    from .tensor import DType, normalize_axes
+    rw = _Rewriter(g, keep)
+    rw.replaced = {}
+    live = live_set(g, keep)
+
+    def live_uses(key):  # readers among the live nodes (dead ones linger until DCE)
+        if key in rw.keep:
+            return 2
+        return sum(1 for n, _ in rw.users().get(key, []) if n.id in live)
+    count = 0
+    for node in list(g.topo_order()):
+        if node.id not in live or node.kind not in ("fused_ew", "fused_ewm") or node.attrs.get("rowsum"):
+            continue
+        osh = g.ref_shape((node.id, 0))
+        if osh is None or None in osh or len(osh) < 2:
+            continue
+        ins = [tuple(i) for i in node.inputs]
+        bshape = (osh[0],) + (1,) * (len(osh) - 1)
+        rs = []
+        for k, src in enumerate(ins):
+            ksh = g.ref_shape(src)
+            if ksh is None or tuple(ksh) != bshape:
+                continue
+            key = src
+            while rw.node(key).kind == "reshape" and live_uses(key) == 1:
+                key = tuple(rw.node(key).inputs[0])
+            r = rw.node(key)
+            if r.kind != "reduce_sum" or key[1] != 0 or live_uses(key) != 1:
+                continue
+            x = tuple(r.inputs[0])
+            xsh = g.ref_shape(x)
+            if xsh is None or tuple(xsh) != tuple(osh) or r.out_dtypes[0] != DType.F64 or x not in ins:
+                continue
+            if tuple(sorted(normalize_axes(r.attrs["axes"], len(xsh)))) != tuple(range(1, len(xsh))):
+                continue
+            j = ins.index(x)
+            if any(jj == k for _, jj in rs):
+                continue
+            rs.append((k, j))
+        if not rs:
+            continue
+        for k, j in rs:
+            node.inputs[k] = node.inputs[j]
+        node.attrs["rowsum"] = tuple(rs)
+        rw._users = None
+        g._topo_cache = None
+        count += 1
+    return count, rw.replaced

@@ -212,3 +212,45 @@ def test_cfg5_partials_match_reduced_executor(env, monkeypatch):
     for g_, w_ in zip(got, want):
         np.testing.assert_allclose(np.asarray(g_.data, np.float64), np.asarray(w_.data, np.float64),
                                    rtol=RTOL, atol=ATOL)
+
+
+@pytest.mark.parametrize("rows,W,S", [(1024, 256, 3), (37, 1024, 1), (300, 64, 2), (5, 40, 1)])
+def test_fused_row_sum_feed(env, rows, W, S):
+    """pfb_fused_ew_rows (pass F16): input 1 is the row sum of input 0 (its
+    split-K partials summed first), computed inside the group's kernel;
+    against f64 numpy.  Rows that are not a whole number of warps are
+    declined (PFB_E_UNSUPPORTED) for the executor's materialised fallback."""
+    torch, lib, DArray, DType = env
+    from paper_1903_04243_b200 import _native as N
+    if not lib.pfb_fused_parts_ok():
+        pytest.skip("specialiser unavailable")
+    dev = torch.device("cuda")
+    r = np.random.default_rng(rows + W)
+    shape = (rows, 1, W)
+    parts = r.standard_normal((S,) + shape).astype(np.float32)
+    c = r.standard_normal(shape).astype(np.float32)
+    P = DArray.from_numpy(parts, DType.F64, dev)
+    C = DArray.from_numpy(c, DType.F64, dev)
+    x = P.view(shape, P.strides[1:])
+    rs = x.view((rows, 1, 1), (x.strides[0], 0, 0))
+    out = DArray.empty(shape, DType.F64, dev)
+    ops = _opcodes()
+    # r0 = in0 (partials), r1 = in1 (row sum of in0), r2 = in2; r3 = r1 * r2 + r0
+    prog = [(64, 0, 0, 0), (64, 1, 1, 0), (64, 2, 2, 0), (ops["mul"], 3, 1, 2),
+            (ops["add"], 4, 3, 0)]
+    flat = (ctypes.c_int32 * 20)(*[v for st in prog for v in st])
+    spec = (ctypes.c_int64 * 6)(S, rows * W, 1, 0, 1, 0)
+    rsum = (ctypes.c_int32 * 3)(-1, 0, -1)
+    ins = (N.PfbTensor * 3)(x.desc_part0(), rs.desc_part0(), C.desc())
+    outs = (N.PfbTensor * 1)(out.desc())
+    regs = (ctypes.c_int32 * 1)(4)
+    rc = lib.pfb_fused_ew_rows(3, ins, spec, rsum, 5, flat, 1, regs, outs, None)
+    if W % 32:
+        assert rc == N.E_UNSUPPORTED
+        return
+    assert rc == 0
+    torch.cuda.synchronize()
+    z = parts.astype(np.float64).sum(0)
+    want = z.sum(axis=2, keepdims=True) * c + z
+    np.testing.assert_allclose(out.to_numpy().astype(np.float64), want, rtol=RTOL,
+                               atol=ATOL * np.sqrt(W) * 4)

@@ -338,3 +338,25 @@ def test_f14_mask_compare_is_absorbed_into_the_select_group():
         live = passes.live_set(body, [tuple(o) for o in body.outputs])
         kinds = [body.nodes[i].kind for i in live]
         assert "less" not in kinds and kinds.count("fused_ew") >= 2, sorted(kinds)
+
+
+def test_f16_row_sum_is_computed_by_the_select_group():
+    """cfg5 (masked, unrolled): the per-step `reduce_sum(z)` whose only reader
+    is the select group becomes a row-sum feed of that group (attrs
+    "rowsum"): no reduce_sum over the step's rows stays live in the loop body
+    (oracle values unchanged)."""
+    from paper_1903_04243_b200 import passes
+    w = WL.cfg5(WL.this_api(), n=6, max_len=5, units=8, masked=True, unroll=2)
+    g, g2, m = _run_both(w)
+    bodies = [n.block.subgraphs["body"] for n in g2.nodes.values() if n.kind == "while"]
+    assert bodies
+    for body in bodies:
+        live = passes.live_set(body, [tuple(o) for o in body.outputs])
+        nodes = [body.nodes[i] for i in live]
+        fused = [n for n in nodes if n.kind == "fused_ew" and n.attrs.get("rowsum")]
+        assert len(fused) == 2, sorted(n.kind for n in nodes)
+        for f in fused:
+            for k, j in f.attrs["rowsum"]:
+                assert tuple(f.inputs[k]) == tuple(f.inputs[j])
+        rows = [n for n in nodes if n.kind == "reduce_sum" and len(body.ref_shape(n.inputs[0])) == 3]
+        assert not rows, rows
