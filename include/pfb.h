@@ -307,6 +307,14 @@ int pfb_conv2d_filter_grad(const pfb_tensor* x, const pfb_tensor* gy, int32_t k1
  * PFB_DEV_OOB in dev_err. */
 int pfb_gather_stacked(const pfb_tensor* x, const pfb_tensor* idx, pfb_tensor* out,
                        int32_t* dev_err, void* stream);
+/* q <= 8 pfb_gather_stacked calls on one operand in one launch (pass F17:
+ * the per-step x_t gathers of an unrolled loop body): out[g][j, ...] =
+ * x[j, idx[g][j], ...], idx[g] [n]; dev_err[g] (nullable array, nullable
+ * entries) gets PFB_DEV_OOB for an index of vector g outside [0, m).  fp32
+ * with contiguous 16-byte-aligned rows; PFB_E_UNSUPPORTED otherwise (gather
+ * one vector at a time with pfb_gather_stacked). */
+int pfb_gather_stacked_many(const pfb_tensor* x, int32_t q, const pfb_tensor* idx,
+                            pfb_tensor* out, int32_t* const* dev_err, void* stream);
 int pfb_gather_rows(const pfb_tensor* x, const pfb_tensor* idx, pfb_tensor* out,
                     int32_t* dev_err, void* stream);
 int pfb_scatter_rows(int32_t n_parts, const pfb_tensor* index_sets, const pfb_tensor* parts,

@@ -99,6 +99,7 @@ _SIGNATURES = {
     "pfb_conv2d_input_grad": ([_P, _P, _P, _vp], ctypes.c_int),
     "pfb_gather_rows": ([_P, _P, _P, _vp, _vp], ctypes.c_int),
     "pfb_gather_stacked": ([_P, _P, _P, _vp, _vp], ctypes.c_int),
+    "pfb_gather_stacked_many": ([_P, _i32, _P, _P, _vp, _vp], ctypes.c_int),
     "pfb_scatter_rows": ([_i32, _P, _P, _i64, _P, _vp, _vp, _vp], ctypes.c_int),
     "pfb_scatter_add_rows": ([_P, _P, _i64, _P, _vp, _vp], ctypes.c_int),
     "pfb_where_true": ([_P, _P, _vp, _vp, _i64, _vp], ctypes.c_int),

@@ -388,6 +388,86 @@ extern "C" int pfb_gather_stacked(const pfb_tensor* x, const pfb_tensor* idx, pf
   }
 }
 
+// several gather_stacked of one operand (pass F17: the per-step x_t gathers
+// of an unrolled loop body) in one launch: out_g[j, :] = x[j, idx_g[j], :],
+// g = 0..q-1, each index vector with its own error word.  fp32 rows with a
+// contiguous 16-byte-aligned tail only (128-bit accesses); anything else is
+// PFB_E_UNSUPPORTED (the caller then gathers one index vector at a time).
+namespace pfb {
+constexpr int kMaxGathers = 8;
+struct GatherMany {
+  const int64_t* idx[kMaxGathers];
+  int64_t idx_st[kMaxGathers];
+  float* out[kMaxGathers];
+  int64_t orow[kMaxGathers];
+  int32_t* err[kMaxGathers];
+};
+
+__global__ void __launch_bounds__(256) gather_many_kernel(int q, int64_t n, int64_t per,
+                                                          const float* x, int64_t xrow,
+                                                          int64_t xseg, int64_t m, GatherMany G) {
+  pdl_enter();
+  const int64_t rows = (int64_t)q * n, total = rows * per;
+  for (int64_t lin = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; lin < total;
+       lin += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t rr = lin / per, t = (lin - rr * per) * 4;
+    const int g = (int)(rr / n);
+    const int64_t j = rr - (int64_t)g * n;
+    const int64_t r = __ldg(G.idx[g] + j * G.idx_st[g]);
+    const bool ok = r >= 0 && r < m;
+    if (!ok) set_err(G.err[g], PFB_DEV_OOB);
+    float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+    if (ok) v = __ldg(reinterpret_cast<const float4*>(x + j * xseg + r * xrow + t));
+    *reinterpret_cast<float4*>(G.out[g] + j * G.orow[g] + t) = v;
+  }
+}
+}  // namespace pfb
+
+extern "C" int pfb_gather_stacked_many(const pfb_tensor* x, int32_t q, const pfb_tensor* idx,
+                                       pfb_tensor* out, int32_t* const* dev_err, void* stream) {
+  if (q < 1 || q > kMaxGathers) return PFB_E_ARG;
+  if (x->rank < 2) return PFB_E_RANK;
+  if (x->dtype != PFB_F32) return PFB_E_UNSUPPORTED;
+  const int64_t n = x->shape[0], m = x->shape[1];
+  int64_t D = 1;
+  for (int d = 2; d < x->rank; ++d) D *= x->shape[d];
+  // x's tail contiguous (one row of D elements per (j, r))
+  int64_t e = 1;
+  for (int d = x->rank - 1; d >= 2; --d) {
+    if (x->shape[d] != 1 && x->stride[d] != e) return PFB_E_UNSUPPORTED;
+    e *= x->shape[d];
+  }
+  const int64_t xrow = x->stride[1], xseg = x->stride[0];
+  if (D % 4 || xrow % 4 || xseg % 4 || (uintptr_t)x->data % 16) return PFB_E_UNSUPPORTED;
+  GatherMany G;
+  for (int g = 0; g < q; ++g) {
+    const pfb_tensor& I = idx[g];
+    const pfb_tensor& O = out[g];
+    if (I.dtype != PFB_I64) return PFB_E_DTYPE;
+    if (I.rank != 1 || I.shape[0] != n) return PFB_E_SHAPE;
+    if (O.dtype != PFB_F32 || O.rank != x->rank - 1 || O.shape[0] != n) return PFB_E_SHAPE;
+    int64_t eo = 1;
+    for (int d = O.rank - 1; d >= 1; --d) {
+      if (O.shape[d] != x->shape[d + 1]) return PFB_E_SHAPE;
+      if (O.shape[d] != 1 && O.stride[d] != eo) return PFB_E_UNSUPPORTED;
+      eo *= O.shape[d];
+    }
+    const int64_t orow = O.rank == 1 ? 0 : O.stride[0];
+    if ((O.rank > 1 && orow % 4) || (uintptr_t)O.data % 16) return PFB_E_UNSUPPORTED;
+    G.idx[g] = (const int64_t*)I.data;
+    G.idx_st[g] = I.stride[0];
+    G.out[g] = (float*)O.data;
+    G.orow[g] = orow;
+    G.err[g] = dev_err ? dev_err[g] : nullptr;
+  }
+  if (n == 0 || D == 0) return 0;
+  const int64_t per = D / 4;
+  cudaStream_t s = as_stream(stream);
+  launch(gather_many_kernel, grid_for((int64_t)q * n * per, 256), 256, 0, s, (int)q, n, per,
+         (const float*)x->data, xrow, xseg, m, G);
+  return launch_status();
+}
+
 extern "C" int pfb_gather_rows(const pfb_tensor* x, const pfb_tensor* idx, pfb_tensor* out,
                                int32_t* dev_err, void* stream) {
   if (idx->dtype != PFB_I64) return PFB_E_DTYPE;

@@ -1723,6 +1723,45 @@ def _h_gather_stacked(ex, node, ins):
     return [out]
 
 
+class _ErrSite:
+    """The node an error word reports (a merged node reports its originals)."""
+    __slots__ = ("id",)
+
+    def __init__(self, nid):
+        self.id = nid
+
+
+def _h_gather_stacked_many(ex, node, ins):
+    """gather_stacked_many (pass F17): the q gather_stacked of one operand in
+    one launch (pfb_gather_stacked_many); each index vector keeps its own
+    error word, reported as the gather node it replaced.  Layouts the merged
+    kernel does not take gather one vector at a time."""
+    x = ex._dev(ins[0])
+    idxs = [ex._dev(v) for v in ins[1:]]
+    for idx in idxs:
+        if idx.dtype != DType.I64:
+            raise E.DTypeMismatch("gather_rows: index must be i64")
+        if x.rank < 2 or idx.rank != 1 or idx.shape[0] != x.shape[0]:
+            raise E.IncompatibleShapes(f"gather_stacked: {x.shape} vs index {idx.shape}")
+    outs = [ex._empty(tuple(idx.shape) + x.shape[2:], x.dtype) for idx in idxs]
+    orig = node.attrs["orig"]
+    q = len(idxs)
+    errs = (ctypes.c_void_p * q)(*[ex._err_slot(_ErrSite(orig[g])) for g in range(q)])
+    status = []
+
+    def many(*args):  # PFB_E_UNSUPPORTED -> one launch per index vector below
+        rc = ex._lib.pfb_gather_stacked_many(*args)
+        status.append(rc)
+        return 0 if rc == N.E_UNSUPPORTED else rc
+    ex._call(many, x.desc(), q, (N.PfbTensor * q)(*[i.desc() for i in idxs]),
+             (N.PfbTensor * q)(*[o.desc() for o in outs]), errs, ex._stream, what="gather_rows")
+    if status[-1] == N.E_UNSUPPORTED:
+        for g in range(q):
+            ex._call(ex._lib.pfb_gather_stacked, x.desc(), idxs[g].desc(), outs[g].desc(),
+                     errs[g], ex._stream, what="gather_rows")
+    return outs
+
+
 def _h_scatter_rows(ex, node, ins):
     n = node.attrs["num_parts"]
     sets = [ex._dev(v) for v in ins[:n]]
@@ -2118,7 +2157,8 @@ _HANDLERS.update({
     "fused_pack": _h_fused_pack,
     "matmul2": _h_matmul2,
     "fused_int": _h_fused_int,
-    "gather_rows": _h_gather, "gather_stacked": _h_gather_stacked, "scatter_rows": _h_scatter_rows,
+    "gather_rows": _h_gather, "gather_stacked": _h_gather_stacked,
+    "gather_stacked_many": _h_gather_stacked_many, "scatter_rows": _h_scatter_rows,
     "scatter_add_rows": _h_scatter_add, "reshape": _h_reshape, "transpose": _h_transpose,
     "slice_leading": _h_slice_leading, "tile_leading": _h_tile_leading,
     "where_true": _h_where_true, "complement": _h_complement, "dim0": _h_dim0,

@@ -988,6 +988,7 @@ def _pipeline(elementwise):
            fuse_reductions, fuse_row_dots, fuse_dual_matmuls, fuse_matmul_epilogues]
     if elementwise:
         seq += [sink_unit_reshapes, fuse_elementwise, place_concats, fuse_row_sums]
+    seq += [merge_sibling_gathers]
     return seq
 
 
@@ -1809,4 +1810,46 @@ def fuse_row_sums(g, keep=()):
         rw._users = None
         g._topo_cache = None
         count += 1
+    return count, rw.replaced
+
+
+# ----------------------------------------------------------------------------
+# F17: sibling gathers of one operand become one launch
+#
+# An unrolled loop body gathers x_t = x[j, t_j + u] for every unrolled step u
+# (cfg5: gather_stacked(X, t + u), u = 0..3); the index vectors are known at
+# the top of the trip, so the q gathers can run as one node
+# (gather_stacked_many, one kernel) instead of one launch per step.  Only
+# gathers whose indices do not depend on one another's results merge (the
+# merged node must be placeable before all of them); each keeps its own
+# bounds check / error report (attrs["orig"]).
+
+def merge_sibling_gathers(g, keep=(), max_q=8):
+    """F17 in place on `g` (a private copy).  Returns (count, moved outputs)."""
+    rw = _Rewriter(g, keep)
+    rw.replaced = {}
+    live = live_set(g, keep)
+    groups = {}
+    for node in g.topo_order():
+        if node.id in live and node.kind == "gather_stacked":
+            sx, si = g.ref_shape(node.inputs[0]), g.ref_shape(node.inputs[1])
+            if sx is None or si is None or len(si) != 1:
+                continue
+            groups.setdefault(tuple(node.inputs[0]), []).append(node)
+    count = 0
+    for x, nodes in groups.items():
+        nodes = nodes[:max_q]
+        if len(nodes) < 2:
+            continue
+        ids = {n.id for n in nodes}
+        # no index may depend on a gather of the group (the merged node would
+        # then feed its own input)
+        if any(_ancestors(g, tuple(n.inputs[1]), m) for n in nodes for m in ids):
+            continue
+        new = g.add_node("gather_stacked_many", [x] + [tuple(n.inputs[1]) for n in nodes],
+                         {"orig": tuple(n.id for n in nodes)})
+        for k, n in enumerate(nodes):
+            rw.redirect((n.id, 0), Ref(g, new.id, k))
+        count += 1
+    g._topo_cache = None
     return count, rw.replaced

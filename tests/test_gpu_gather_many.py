@@ -1,0 +1,86 @@
+"""GPU: pass F17 -- sibling gather_stacked of one operand in one launch
+(pfb_gather_stacked_many) against numpy fancy indexing (reference
+tensor.gather_rows per iteration, tensor.py:306-318): bit-exact values, and
+an out-of-range index of any merged vector raises IndexOutOfBounds naming the
+gather it replaced."""
+
+import ctypes
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def env():
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    from paper_1903_04243_b200 import _native as N
+    from paper_1903_04243_b200.executor import DArray
+    from paper_1903_04243_b200.tensor import DType
+    return torch, N, DArray, DType
+
+
+@pytest.mark.parametrize("n,m,d,q", [(1024, 100, 256, 4), (7, 3, 8, 2), (33, 5, 12, 8)])
+def test_gather_many_bit_exact(env, n, m, d, q):
+    torch, N, DArray, DType = env
+    lib = N.lib()
+    dev = torch.device("cuda")
+    r = np.random.default_rng(n + q)
+    x = r.standard_normal((n, m, d)).astype(np.float32)
+    idx = [r.integers(0, m, n).astype(np.int64) for _ in range(q)]
+    X = DArray.from_numpy(x, DType.F64, dev)
+    I = [DArray.from_numpy(i, DType.I64, dev) for i in idx]
+    O = [DArray.empty((n, d), DType.F64, dev) for _ in range(q)]
+    err = torch.zeros(q, dtype=torch.int32, device=dev)
+    errs = (ctypes.c_void_p * q)(*[err.data_ptr() + 4 * g for g in range(q)])
+    rc = lib.pfb_gather_stacked_many(X.desc(), q, (N.PfbTensor * q)(*[i.desc() for i in I]),
+                                     (N.PfbTensor * q)(*[o.desc() for o in O]), errs, None)
+    assert rc == 0
+    torch.cuda.synchronize()
+    for g in range(q):
+        np.testing.assert_array_equal(O[g].to_numpy(), x[np.arange(n), idx[g]])
+    assert not err.any()
+    # one out-of-range entry in vector 1 sets that vector's error word only
+    bad = idx[1].copy()
+    bad[n // 2] = m
+    I[1] = DArray.from_numpy(bad, DType.I64, dev)
+    rc = lib.pfb_gather_stacked_many(X.desc(), q, (N.PfbTensor * q)(*[i.desc() for i in I]),
+                                     (N.PfbTensor * q)(*[o.desc() for o in O]), errs, None)
+    assert rc == 0
+    torch.cuda.synchronize()
+    e = err.cpu().numpy()
+    assert e[1] & N.DEV_OOB and not e[0] and not e[2:].any()
+
+
+def test_gather_many_declines_unaligned_rows(env):
+    torch, N, DArray, DType = env
+    lib = N.lib()
+    dev = torch.device("cuda")
+    X = DArray.from_numpy(np.zeros((4, 3, 6), np.float32), DType.F64, dev)
+    I = [DArray.from_numpy(np.zeros(4, np.int64), DType.I64, dev) for _ in range(2)]
+    O = [DArray.empty((4, 6), DType.F64, dev) for _ in range(2)]
+    rc = lib.pfb_gather_stacked_many(X.desc(), 2, (N.PfbTensor * 2)(*[i.desc() for i in I]),
+                                     (N.PfbTensor * 2)(*[o.desc() for o in O]), None, None)
+    assert rc == N.E_UNSUPPORTED
+
+
+def test_cfg5_merged_gathers_raise_out_of_range(env):
+    """A length past max_len makes the merged per-trip gathers read x[j, t]
+    with t = max_len: ExecError(IndexOutOfBounds) from the device loop, as
+    with one gather per step."""
+    torch, N, DArray, DType = env
+    from paper_1903_04243_b200 import errors, workloads as WL
+    from paper_1903_04243_b200.executor import Executor
+    w = WL.BUILDERS["cfg5"](WL.this_api(), n=64, max_len=8, units=32, masked=True, unroll=4)
+    feeds = dict(w.feeds)
+    ok = Executor(w.graph, device="cuda:0").run(feeds=feeds)
+    assert ok
+    lengths = np.array(feeds["lengths"]).copy()
+    lengths[5] = 9
+    feeds["lengths"] = lengths
+    with pytest.raises(errors.ExecError) as e:
+        Executor(w.graph, device="cuda:0").run(feeds=feeds)
+    assert isinstance(e.value.cause, errors.IndexOutOfBounds)

@@ -360,3 +360,40 @@ def test_f16_row_sum_is_computed_by_the_select_group():
                 assert tuple(f.inputs[k]) == tuple(f.inputs[j])
         rows = [n for n in nodes if n.kind == "reduce_sum" and len(body.ref_shape(n.inputs[0])) == 3]
         assert not rows, rows
+
+
+def test_f17_sibling_gathers_of_one_operand_merge():
+    """cfg5 (masked, unrolled x4): the four per-step x_t gathers of a trip
+    (indices known at the top of the trip) become one gather_stacked_many
+    node (one launch); values unchanged on the oracle."""
+    from paper_1903_04243_b200 import passes
+    w = WL.cfg5(WL.this_api(), n=6, max_len=9, units=8, masked=True, unroll=4)
+    g, g2, m = _run_both(w)
+    bodies = [n.block.subgraphs["body"] for n in g2.nodes.values() if n.kind == "while"]
+    assert bodies
+    for body in bodies:
+        live = passes.live_set(body, [tuple(o) for o in body.outputs])
+        kinds = [body.nodes[i].kind for i in live]
+        assert "gather_stacked" not in kinds and kinds.count("gather_stacked_many") == 1, kinds
+        (gm,) = [body.nodes[i] for i in live if body.nodes[i].kind == "gather_stacked_many"]
+        assert len(gm.attrs["orig"]) == 4
+
+
+def test_f17_keeps_dependent_gathers_apart():
+    """A gather whose index is computed from another gather's result of the
+    same operand cannot merge with it."""
+    from paper_1903_04243_b200 import passes
+    from paper_1903_04243_b200.builder import GraphBuilder
+    from paper_1903_04243_b200.tensor import DType
+    b = GraphBuilder()
+    x = b.placeholder("x", DType.F64, (4, 3, 4))
+    i0 = b.placeholder("i", DType.I64, (4,))
+    g1 = b.graph.add_node("gather_stacked", [x, i0], {})
+    j = b.cast(b.reduce_sum(b.graph.out(g1.id, 0), [1]), DType.I64)
+    g2 = b.graph.add_node("gather_stacked", [x, j], {})
+    keys = [(g2.id, 0)]
+    b.graph.set_outputs(keys)
+    dst, mp = passes.optimize(b.graph, keys)
+    live = passes.live_set(dst, [mp[k] for k in keys])
+    kinds = [dst.nodes[n].kind for n in live]
+    assert kinds.count("gather_stacked") == 2 and "gather_stacked_many" not in kinds
