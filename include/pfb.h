@@ -280,6 +280,12 @@ int pfb_matmul_dual2(const pfb_tensor* a1, const pfb_tensor* b1, const pfb_tenso
  * head -> WHILE { iter } and each pfb_loop_launch runs the whole loop. */
 int pfb_loop_create(void** loop, uint64_t* handle);
 int pfb_set_condition(uint64_t handle, const void* flag, void* counter, void* stream);
+/* the predicated while's test any(mask) (vectorize._convert_while_masked's
+ * less(0, reduce_sum(cast(active, i64))), reference interp.py:240-355 loop
+ * test) straight into the handle: one launch per trip instead of four.
+ * mask: n dense u8 bools. */
+int pfb_set_condition_any(uint64_t handle, const void* mask, int64_t n, void* counter,
+                          void* stream);
 int pfb_loop_finalize(void* loop, void* head_graph, void* iter_graph);
 int pfb_loop_launch(void* loop, void* stream);
 int pfb_loop_destroy(void* loop);

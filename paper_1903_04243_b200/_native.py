@@ -89,6 +89,7 @@ _SIGNATURES = {
     "pfb_loop_create": ([ctypes.POINTER(ctypes.c_void_p), ctypes.POINTER(ctypes.c_uint64)],
                         ctypes.c_int),
     "pfb_set_condition": ([ctypes.c_uint64, _vp, _vp, _vp], ctypes.c_int),
+    "pfb_set_condition_any": ([ctypes.c_uint64, _vp, ctypes.c_int64, _vp, _vp], ctypes.c_int),
     "pfb_loop_finalize": ([_vp, _vp, _vp], ctypes.c_int),
     "pfb_loop_launch": ([_vp, _vp], ctypes.c_int),
     "pfb_loop_destroy": ([_vp], ctypes.c_int),

@@ -26,6 +26,23 @@ __global__ void set_condition_kernel(cudaGraphConditionalHandle h, const uint8_t
   cudaGraphSetConditional(h, flag[0] ? 1u : 0u);
   if (counter) *counter += 1;
 }
+// the predicated while's test, any(active) (vectorize._convert_while_masked:
+// less(0, reduce_sum(cast(active, i64)))), straight into the handle: one
+// launch instead of cast + reduction + compare + set
+__global__ void __launch_bounds__(1024) set_condition_any_kernel(cudaGraphConditionalHandle h,
+                                                                 const uint8_t* mask, int64_t n,
+                                                                 unsigned long long* counter) {
+  int any = 0;
+  const int64_t n4 = ((reinterpret_cast<uintptr_t>(mask) & 3) == 0) ? n / 4 : 0;
+  for (int64_t i = threadIdx.x; i < n4; i += blockDim.x)
+    any |= reinterpret_cast<const uint32_t*>(mask)[i] != 0u;
+  for (int64_t i = 4 * n4 + threadIdx.x; i < n; i += blockDim.x) any |= mask[i] != 0;
+  any = __syncthreads_or(any);
+  if (threadIdx.x == 0) {
+    cudaGraphSetConditional(h, any ? 1u : 0u);
+    if (counter) *counter += 1;
+  }
+}
 }  // namespace pfb
 
 using namespace pfb;
@@ -51,6 +68,17 @@ extern "C" int pfb_set_condition(uint64_t handle, const void* flag, void* counte
   set_condition_kernel<<<1, 1, 0, as_stream(stream)>>>((cudaGraphConditionalHandle)handle,
                                                        (const uint8_t*)flag,
                                                        (unsigned long long*)counter);
+  return launch_status();
+}
+
+// any(mask[0..n)) -> the loop's conditional handle (mask: dense u8 bools)
+extern "C" int pfb_set_condition_any(uint64_t handle, const void* mask, int64_t n, void* counter,
+                                     void* stream) {
+  if (n < 0) return PFB_E_ARG;
+  kernel_launches()++;
+  const int threads = n >= 4096 ? 1024 : 256;
+  set_condition_any_kernel<<<1, threads, 0, as_stream(stream)>>>(
+      (cudaGraphConditionalHandle)handle, (const uint8_t*)mask, n, (unsigned long long*)counter);
   return launch_status();
 }
 

@@ -707,7 +707,15 @@ class Executor:
             torch.cuda.synchronize(self.device)
             bind = {"capture": list(caps), "carried": state}
 
+            any_src = _any_mask_test(cg)
+
             def cond_to_handle():
+                if any_src is not None:  # any(active): one launch (pfb_set_condition_any)
+                    m = state[any_src]
+                    _raise_status(self._lib.pfb_set_condition_any(handle.value, m.ptr, m.size,
+                                                                  counter.data_ptr(), self._stream),
+                                  "while")
+                    return
                 cenv = self._run_graph(cg, bind, feeds)
                 flag = cenv[tuple(cg.outputs[0])]
                 if not isinstance(flag, DArray) or flag.dtype != DType.BOOL or flag.size != 1:
@@ -1721,6 +1729,30 @@ def _h_gather_stacked(ex, node, ins):
     ex._call(ex._lib.pfb_gather_stacked, x.desc(), idx.desc(), out.desc(), ex._err_slot(node),
              ex._stream, what="gather_rows")
     return [out]
+
+
+def _any_mask_test(cg):
+    """Carried index k when the loop test `cg` is any(carried[k]) for a dense
+    bool vector -- less(0, reduce_sum(cast(carried[k], i64), [0])), the
+    predicated while of vectorize._convert_while_masked -- else None."""
+    if len(cg.outputs) != 1:
+        return None
+    less = cg.nodes[cg.outputs[0][0]]
+    if less.kind != "less":
+        return None
+    zero, red = (cg.nodes[i[0]] for i in less.inputs)
+    if zero.kind != "constant" or np.asarray(zero.attrs["value"].data).shape != () or \
+            int(zero.attrs["value"].data) != 0 or red.kind != "reduce_sum":
+        return None
+    cast = cg.nodes[red.inputs[0][0]]
+    if cast.kind != "cast" or cast.attrs["dtype"] != DType.I64:
+        return None
+    src = cg.nodes[cast.inputs[0][0]]
+    sh = cg.ref_shape(cast.inputs[0])
+    if src.kind != "carried" or cg.ref_dtype(cast.inputs[0]) != DType.BOOL or sh is None or \
+            len(sh) != 1 or list(red.attrs["axes"]) not in ([0], [-1]):
+        return None
+    return src.attrs["index"]
 
 
 class _ErrSite:

@@ -1347,7 +1347,10 @@ def fuse_elementwise(g, keep=()):
         if built is None:
             group = grow(root, False, domain)
             if len(group) < 2:
-                return None
+                # a lone integer op (the loop-trip `select` of a predicated
+                # while body) may still merge with a sibling group below;
+                # unmerged singletons are dropped after merging
+                return (group, None) if domain == "int" and len(group) == 1 else None
             built = build(root, group, domain)
         return None if built is None else (group, built)
 
@@ -1364,6 +1367,7 @@ def fuse_elementwise(g, keep=()):
         assigned |= group
 
     groups = _merge_groups(g, groups, users, pos, live, build)
+    groups = [grp for grp in groups if grp[3] is not None]
 
     for root, group, domain, built in groups:
         order, externals, outs, prog, regs = built

@@ -397,3 +397,19 @@ def test_f17_keeps_dependent_gathers_apart():
     live = passes.live_set(dst, [mp[k] for k in keys])
     kinds = [dst.nodes[n].kind for n in live]
     assert kinds.count("gather_stacked") == 2 and "gather_stacked_many" not in kinds
+
+
+def test_masked_while_test_is_recognised_as_any():
+    """The predicated while's loop test (vectorize._convert_while_masked:
+    less(0, reduce_sum(cast(active, i64)))) survives the passes in the shape
+    the device loop turns into one pfb_set_condition_any launch per trip."""
+    from paper_1903_04243_b200.executor import _any_mask_test
+    w = WL.cfg5(WL.this_api(), n=6, max_len=5, units=8, masked=True, unroll=2)
+    keys = [tuple(o) for o in w.graph.outputs]
+    g2, _ = optimize(w.graph, keys)
+    loops = [n for n in g2.nodes.values() if n.kind == "while"]
+    assert loops
+    for n in loops:
+        assert _any_mask_test(n.block.subgraphs["cond"]) == 0
+        # a body is not a loop test
+        assert _any_mask_test(n.block.subgraphs["body"]) is None
