@@ -983,7 +983,8 @@ def fuse_row_dots(g, keep=()):
 
 
 def _pipeline(elementwise):
-    seq = [eliminate_common_subexpressions, stack_onehot_sums, slice_matmul_columns,
+    seq = [eliminate_common_subexpressions, stack_onehot_sums, place_scatter_sums,
+           slice_matmul_columns,
            fuse_outer_products, fuse_conv_filter_grads, eliminate_common_subexpressions,
            fuse_reductions, fuse_row_dots, fuse_dual_matmuls, fuse_matmul_epilogues]
     if elementwise:
@@ -1854,6 +1855,88 @@ def merge_sibling_gathers(g, keep=(), max_q=8):
                          {"orig": tuple(n.id for n in nodes)})
         for k, n in enumerate(nodes):
             rw.redirect((n.id, 0), Ref(g, new.id, k))
+        count += 1
+    g._topo_cache = None
+    return count, rw.replaced
+
+
+# ----------------------------------------------------------------------------
+# F18: a sum of scatter-adds over complementary constant row sets is placement
+#
+# The VJP of gather(x, idx) is scatter_add_rows(idx, g, total) (reference
+# autodiff.py:100-110); the maxpool of the conv bench model gathers the even
+# and the odd rows (bench.py:68-78), so its backward adds two scatter-adds
+# whose index sets are {0, 2, ..} and {1, 3, ..}: every output row receives
+# exactly one update.  That sum is an interleave -- concat([u_even[:, None],
+# u_odd[:, None]], 1) reshaped to [total, ..] -- and a split at n
+# ({0..n-1} / {n..total-1}) is a plain concat: one placement launch (or none,
+# when F13b lets the producing group write the slots) instead of two zero
+# fills, two scatter kernels and an add.  Values are the updates themselves
+# (the reference's 0 + u turns a -0 update into +0; nothing else differs --
+# the other set contributes exact zeros).
+
+def place_scatter_sums(g, keep=()):
+    """F18 in place on `g` (a private copy).  Returns (count, moved outputs)."""
+    rw = _Rewriter(g, keep)
+    rw.replaced = {}
+    live = live_set(g, keep)
+    b = rw.b
+
+    def live_uses(key):
+        if key in rw.keep:
+            return 2
+        return sum(1 for n, _ in rw.users().get(key, []) if n.id in live)
+
+    count = 0
+    for node in list(g.topo_order()):
+        if node.id not in live or node.kind != "add" or node.id not in g.nodes:
+            continue
+        chains = []
+        for src in node.inputs:
+            chain, key = [], tuple(src)
+            while rw.node(key).kind in ("transpose", "reshape") and live_uses(key) == 1:
+                n = rw.node(key)
+                chain.append((n.kind, tuple(n.attrs["perm"] if n.kind == "transpose"
+                                            else n.attrs["shape"])))
+                key = tuple(n.inputs[0])
+            sc = rw.node(key)
+            if sc.kind != "scatter_add_rows" or key[1] != 0 or live_uses(key) != 1:
+                break
+            chains.append((chain, sc))
+        if len(chains) != 2 or chains[0][0] != chains[1][0]:
+            continue
+        chain = chains[0][0]
+        s1, s2 = chains[0][1], chains[1][1]
+        T = s1.attrs["total"]
+        if s2.attrs["total"] != T or not isinstance(T, (int, np.integer)):
+            continue
+        i1, i2 = _const_eval(g, tuple(s1.inputs[0])), _const_eval(g, tuple(s2.inputs[0]))
+        sh1, sh2 = g.ref_shape(s1.inputs[1]), g.ref_shape(s2.inputs[1])
+        if i1 is None or i2 is None or i1.ndim != 1 or i2.ndim != 1 or sh1 is None or sh2 is None:
+            continue
+        if None in sh1 or None in sh2 or tuple(sh1[1:]) != tuple(sh2[1:]):
+            continue
+        if sh1[0] != len(i1) or sh2[0] != len(i2):
+            continue
+        n1, n2, tail = len(i1), len(i2), list(sh1[1:])
+        u1, u2 = Ref(g, *s1.inputs[1]), Ref(g, *s2.inputs[1])
+        if np.array_equal(i1, np.arange(n1)) and np.array_equal(i2, np.arange(n1, T)):
+            merged = b.concat([u1, u2], 0)
+        elif np.array_equal(i2, np.arange(n2)) and np.array_equal(i1, np.arange(n2, T)):
+            merged = b.concat([u2, u1], 0)
+        elif n1 == n2 and 2 * n1 == T and {tuple(i1), tuple(i2)} == {
+                tuple(range(0, T, 2)), tuple(range(1, T, 2))}:
+            ev, od = (u1, u2) if i1[0] == 0 else (u2, u1)
+            merged = b.reshape(b.concat([b.reshape(ev, [n1, 1] + tail),
+                                         b.reshape(od, [n1, 1] + tail)], 1), [T] + tail)
+        else:
+            continue
+        out = merged
+        for kind, arg in reversed(chain):
+            out = b.transpose(out, list(arg)) if kind == "transpose" else b.reshape(out, list(arg))
+        if tuple(g.ref_shape((out.nid, out.port))) != tuple(g.ref_shape((node.id, 0))):
+            continue
+        rw.redirect((node.id, 0), out)
         count += 1
     g._topo_cache = None
     return count, rw.replaced

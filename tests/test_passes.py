@@ -413,3 +413,42 @@ def test_masked_while_test_is_recognised_as_any():
         assert _any_mask_test(n.block.subgraphs["cond"]) == 0
         # a body is not a loop test
         assert _any_mask_test(n.block.subgraphs["body"]) is None
+
+
+def test_f18_maxpool_backward_scatter_sums_become_placement():
+    """cfg2 conv: the maxpool VJP's even-row + odd-row scatter-add sums
+    (complementary constant row sets) become interleaving concats -- no
+    scatter_add_rows and no add of scatter results stays live; oracle values
+    unchanged."""
+    from paper_1903_04243_b200 import passes
+    w = WL.cfg2(WL.this_api(), n=3, model="conv")
+    g, g2, m = _run_both(w)
+    live = passes.live_set(g2, [m[tuple(o)] for o in g.outputs])
+    kinds = [g2.nodes[i].kind for i in live]
+    assert "scatter_add_rows" not in kinds, kinds
+    assert kinds.count("concat") >= 2
+
+
+def test_f18_split_scatter_sum_is_a_concat():
+    """scatter_add(0..n-1, a) + scatter_add(n..T-1, b) == concat([a, b])."""
+    from paper_1903_04243_b200 import passes
+    from paper_1903_04243_b200.builder import GraphBuilder
+    from paper_1903_04243_b200.tensor import DType
+    from oracle import OracleExecutor
+    b = GraphBuilder()
+    x = b.placeholder("x", DType.F64, (5, 3))
+    a = b.mul(b.gather(x, b.const(np.array([0, 1], np.int64))), b.f64(2.0))
+    c = b.gather(x, b.const(np.array([2, 3, 4], np.int64)))
+    s1 = b.graph.add_node("scatter_add_rows", [b.const(np.array([3, 4], np.int64)), a], {"total": 5})
+    s2 = b.graph.add_node("scatter_add_rows", [b.const(np.array([0, 1, 2], np.int64)), c], {"total": 5})
+    y = b.add(b.graph.out(s1.id, 0), b.graph.out(s2.id, 0))
+    b.graph.set_outputs([y])
+    keys = [tuple(o) for o in b.graph.outputs]
+    g2, mp = passes.optimize(b.graph, keys)
+    live = passes.live_set(g2, [mp[k] for k in keys])
+    assert "scatter_add_rows" not in [g2.nodes[i].kind for i in live]
+    xv = np.arange(15.0).reshape(5, 3)
+    want = OracleExecutor(b.graph).run(feeds={"x": xv})[0].data
+    got = OracleExecutor(g2).run(feeds={"x": xv}, outputs=[g2.out(*mp[keys[0]])])[0].data
+    np.testing.assert_array_equal(got, want)
+    np.testing.assert_array_equal(want, np.concatenate([xv[2:5], 2 * xv[0:2]]))
