@@ -126,11 +126,20 @@ std::string fmt(const char* f, ...) {
 // terms dropped, 32-bit arithmetic when every offset fits): the generic loop
 // over the layout's dims costs ~10 instructions per operand and dim, which
 // dominated small many-input groups (the LSTM cell: 19 operands x 3 dims).
-std::string gen_offsets(const FLayout& L, int nops, int V, bool idx64, bool off32) {
+std::string gen_offsets(const FLayout& L, int nops, int V, bool idx64, bool off32, int lpr = 0) {
   std::string s;
   const char* IT = idx64 ? "i64" : "unsigned";
   const char* OT = off32 ? "int" : "i64";
-  s += fmt("    %s lin = g * %d;\n", IT, V);
+  if (lpr > 0) {  // short rows (F16): lanes [lpr*r, lpr*r + W) of a warp hold row r
+    const long long W = (long long)L.shape[L.rank - 1];
+    long long R = 1;
+    for (int d = 0; d < L.rank - 1; ++d) R *= (long long)L.shape[d];
+    s += fmt("    const %s rw_r = g / %d, rw_c = g %% %d;\n", IT, lpr, lpr);
+    s += fmt("    const bool valid = rw_c < %lld && rw_r < %lld;\n", W, R);
+    s += fmt("    %s lin = valid ? rw_r * %lld + rw_c : 0;\n", IT, W);
+  } else {
+    s += fmt("    %s lin = g * %d;\n", IT, V);
+  }
   std::string terms[kMaxFOps];
   for (int d = L.rank - 1; d >= 0; --d) {
     std::string c;
@@ -157,13 +166,13 @@ std::string gen_offsets(const FLayout& L, int nops, int V, bool idx64, bool off3
 
 std::string gen_source(const FusedProgram& P, int V, bool idx64, FeedModes modes,
                        const PartsSpec* PS = nullptr, const FLayout* LS = nullptr,
-                       bool off32 = false, const int* RS = nullptr) {
+                       bool off32 = false, const int* RS = nullptr, int lpr = 0) {
   std::string s = fmt(kPrelude, kMaxRank, kMaxFOps, kMaxRank, kMaxOuts, kMaxIn);
   const char* IT = idx64 ? "i64" : "unsigned";
   const int nops = P.n_in + 1;
   auto nparts = [&](int k) { return (PS && PS->S[k] > 1) ? PS->S[k] : 1; };
   // row-sum feeds: one row per block, blockDim = the row (baked layout)
-  const int nthr = (RS && LS) ? (int)LS->shape[LS->rank - 1] : 256;
+  const int nthr = (RS && LS && lpr == 0) ? (int)LS->shape[LS->rank - 1] : 256;
   if (PS) {
     s += fmt("struct Parts { i64 st[%d]; };\n", kMaxIn);
     s += fmt("extern \"C\" __global__ void __launch_bounds__(%d) pfb_fused_jit(Layout L, %s ngroups, "
@@ -178,7 +187,7 @@ std::string gen_source(const FusedProgram& P, int V, bool idx64, FeedModes modes
   s += fmt("  for (%s g = blockIdx.x * (%s)blockDim.x + threadIdx.x; g < ngroups; "
            "g += (%s)gridDim.x * blockDim.x) {\n", IT, IT, IT);
   if (LS) {
-    s += gen_offsets(*LS, nops, V, idx64, off32);
+    s += gen_offsets(*LS, nops, V, idx64, off32, lpr);
   } else {
     s += fmt("    i64 off[%d];\n", nops);
     s += fmt("    if (L.rank == 1) { for (int o = 0; o < %d; ++o) off[o] = (i64)(g * %d) * L.st[o][0]; }\n",
@@ -247,6 +256,13 @@ std::string gen_source(const FusedProgram& P, int V, bool idx64, FeedModes modes
     bool any = false;
     for (int k = 0; k < P.n_in; ++k) {
       if (RS[k] < 0) continue;
+      if (lpr > 0) {  // short rows: a segmented xor tree inside each lpr-lane group
+        s += fmt("    float in%d_0;\n    { float v = valid ? in%d_0 : 0.f;\n", k, RS[k]);
+        s += fmt("      for (int o = %d; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);\n",
+                 lpr / 2);
+        s += fmt("      in%d_0 = v; }\n", k);
+        continue;
+      }
       if (!any) s += "    __shared__ float rs_red[32];\n    const int rs_w = threadIdx.x >> 5, rs_l = threadIdx.x & 31;\n";
       any = true;
       s += fmt("    float in%d_0;\n    { float v = in%d_0;\n", k, RS[k]);
@@ -302,6 +318,7 @@ std::string gen_source(const FusedProgram& P, int V, bool idx64, FeedModes modes
   // outputs at operand 0's offsets
   const bool vec = (modes & 3) == 0;
   s += "    const i64 so = L.st[0][ir];\n    (void)so;\n";
+  if (lpr > 0) s += "    if (!valid) continue;\n";
   for (int k = 0; k < P.n_out; ++k) {
     const int r = P.out_reg[k];
     if (P.out_dt[k] == PFB_BOOL) {
@@ -463,11 +480,11 @@ namespace {
 // kernel for a program (integer: the i64 domain), compiled on first use
 CUfunction lookup(const FusedProgram& P, int V, bool idx64, FeedModes modes, bool integer,
                   const PartsSpec* PS = nullptr, const FLayout* LS = nullptr, bool off32 = false,
-                  const int* RS = nullptr) {
+                  const int* RS = nullptr, int lpr = 0) {
   int dev = 0;
   cudaGetDevice(&dev);
   // cache key: the program's encoding and everything baked into the source
-  int32_t kb[15 + 3 * kMaxIn + 4 * kMaxSteps + 2 * kMaxOuts + 2 * kMaxRank * (kMaxFOps + 1)];
+  int32_t kb[16 + 3 * kMaxIn + 4 * kMaxSteps + 2 * kMaxOuts + 2 * kMaxRank * (kMaxFOps + 1)];
   int nk = 0;
   kb[nk++] = dev; kb[nk++] = V; kb[nk++] = idx64; kb[nk++] = (int32_t)(modes & 0xffffffffu);
   kb[nk++] = (int32_t)(modes >> 32); kb[nk++] = integer;
@@ -480,6 +497,7 @@ CUfunction lookup(const FusedProgram& P, int V, bool idx64, FeedModes modes, boo
   if (PS)
     for (int k = 0; k < P.n_in; ++k) kb[nk++] = PS->S[k];
   kb[nk++] = RS != nullptr;
+  kb[nk++] = lpr;
   if (RS)
     for (int k = 0; k < P.n_in; ++k) kb[nk++] = RS[k];
   kb[nk++] = LS != nullptr;
@@ -502,7 +520,7 @@ CUfunction lookup(const FusedProgram& P, int V, bool idx64, FeedModes modes, boo
   auto it = cache.find(key);
   if (it == cache.end())
     it = cache.emplace(key, compile(integer ? gen_source_int(P, idx64)
-                                            : gen_source(P, V, idx64, modes, PS, LS, off32, RS))).first;
+                                            : gen_source(P, V, idx64, modes, PS, LS, off32, RS, lpr))).first;
   return it->second;
 }
 
@@ -570,7 +588,16 @@ bool fused_rows_jit_launch(const FusedProgram& P, FeedModes modes, const FLayout
   // coordinate of the outer dims; each row-sum input broadcasts along the
   // row and varies along every outer dim (so a row is exactly its extent-1
   // axes)
-  if (W < 32 || W > 1024 || W % 32 != 0 || n % W != 0) return false;
+  // rows shorter than a warp: lpr = the next power of two >= W lanes per
+  // row, several rows per warp (cfg2's softmax over 10 logits)
+  int lpr = 0;
+  if (W < 32) {
+    lpr = 1;
+    while (lpr < W) lpr *= 2;
+  } else if (W > 1024 || W % 32 != 0) {
+    return false;
+  }
+  if (n % W != 0) return false;
   for (int k = 0; k < P.n_in; ++k) {
     if (rowsum[k] < 0) continue;
     if (rowsum[k] >= P.n_in || rowsum[k] == k || rowsum[rowsum[k]] >= 0 ||
@@ -586,6 +613,13 @@ bool fused_rows_jit_launch(const FusedProgram& P, FeedModes modes, const FLayout
     mx = std::max(mx, m);
   }
   const bool idx64 = n >= (int64_t)0x7fffffff;
+  if (lpr > 0) {  // one thread per (row, lane) of the padded rows, whole warps
+    const int64_t rows = n / W;
+    const int64_t ng = (rows * lpr + 31) / 32 * 32;
+    CUfunction fn = lookup(P, 1, idx64 || ng >= (int64_t)0x7fffffff, modes, false, parts, &L,
+                           mx < 2147483647.0, rowsum, lpr);
+    return fn && run(fn, idx64 || ng >= (int64_t)0x7fffffff, L, ng, outs, ins, s, parts, 256);
+  }
   CUfunction fn = lookup(P, 1, idx64, modes, false, parts, &L, mx < 2147483647.0, rowsum);
   return fn && run(fn, idx64, L, n, outs, ins, s, parts, (int)W);
 }

@@ -1791,9 +1791,16 @@ def fuse_row_sums(g, keep=()):
             ksh = g.ref_shape(src)
             if ksh is None or tuple(ksh) != bshape:
                 continue
-            key = src
-            while rw.node(key).kind == "reshape" and live_uses(key) == 1:
-                key = tuple(rw.node(key).inputs[0])
+            key, post = src, []
+            while True:
+                while rw.node(key).kind == "reshape" and live_uses(key) == 1:
+                    key = tuple(rw.node(key).inputs[0])
+                e = rw.node(key)
+                op = _row_post_op(g, e) if live_uses(key) == 1 and len(post) < 4 else None
+                if op is None:
+                    break
+                post.append(op[0])
+                key = op[1]
             r = rw.node(key)
             if r.kind != "reduce_sum" or key[1] != 0 or live_uses(key) != 1:
                 continue
@@ -1806,6 +1813,11 @@ def fuse_row_sums(g, keep=()):
             j = ins.index(x)
             if any(jj == k for _, jj in rs):
                 continue
+            if post:
+                prog = _with_post_ops(node, k, post[::-1])
+                if prog is None:
+                    continue
+                node.attrs["program"] = prog
             rs.append((k, j))
         if not rs:
             continue
@@ -1940,3 +1952,55 @@ def place_scatter_sums(g, keep=()):
         count += 1
     g._topo_cache = None
     return count, rw.replaced
+
+
+def _row_post_op(g, e):
+    """(step template, operand key) when `e` is an elementwise op on a per-row
+    value whose other operand (if any) is a scalar constant -- F16 moves it
+    into the reading group's program after the row-sum load (cfg2's softmax
+    `1 / sum(exp(z))`).  Template: ("un", code) or ("bin", code, bits, const_left)."""
+    import struct
+    from .tensor import DType
+    if e.output_arity != 1 or e.out_dtypes[0] != DType.F64:
+        return None
+    if e.kind in _UN_CODE and e.kind != "logical_not":
+        return ("un", 16 + _UN_CODE[e.kind]), tuple(e.inputs[0])
+    if e.kind in _BIN_CODE and e.kind not in ("less", "equal"):
+        for side in (0, 1):
+            c = _const_scalar_f(g, tuple(e.inputs[side]))
+            if c is not None and _const_scalar_f(g, tuple(e.inputs[1 - side])) is None:
+                bits = struct.unpack("<i", struct.pack("<f", c))[0]
+                return ("bin", _BIN_CODE[e.kind], bits, side == 0), tuple(e.inputs[1 - side])
+    return None
+
+
+def _with_post_ops(node, k, post):
+    """The group's program with `post` (innermost first) applied to input k
+    right after its load: load r; [const t]; r = op(.., r, ..).  None when the
+    input is loaded more than once, is an output register, or no register /
+    step is free."""
+    prog = [tuple(st) for st in node.attrs["program"]]
+    loads = [i for i, st in enumerate(prog) if st[0] == OP_LOAD and st[2] == k]
+    if len(loads) != 1:
+        return None
+    i = loads[0]
+    r = prog[i][1]
+    outs = node.attrs.get("out_regs", (prog[-1][1],))
+    used = {st[1] for st in prog} | {st[2] for st in prog if st[0] not in (OP_LOAD, OP_CONST)} | \
+        {st[3] for st in prog if st[0] not in (OP_LOAD, OP_CONST)}
+    free = [t for t in range(MAX_REGS) if t not in used]
+    if r in outs or not free:
+        return None
+    t = free[0]
+    extra = []
+    for op in post:
+        if op[0] == "un":
+            extra.append((op[1], r, r, r))
+        else:
+            _, code, bits, const_left = op
+            extra.append((OP_CONST, t, bits, 0))
+            extra.append((code, r, t, r) if const_left else (code, r, r, t))
+    prog = prog[:i + 1] + extra + prog[i + 1:]
+    if len(prog) > MAX_STEPS:
+        return None
+    return tuple(prog)

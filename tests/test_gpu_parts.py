@@ -214,12 +214,14 @@ def test_cfg5_partials_match_reduced_executor(env, monkeypatch):
                                    rtol=RTOL, atol=ATOL)
 
 
-@pytest.mark.parametrize("rows,W,S", [(1024, 256, 3), (37, 1024, 1), (300, 64, 2), (5, 40, 1)])
+@pytest.mark.parametrize("rows,W,S", [(1024, 256, 3), (37, 1024, 1), (300, 64, 2), (5, 40, 1),
+                                      (129, 10, 2), (128, 10, 1), (33, 3, 1), (50, 32, 1)])
 def test_fused_row_sum_feed(env, rows, W, S):
     """pfb_fused_ew_rows (pass F16): input 1 is the row sum of input 0 (its
     split-K partials summed first), computed inside the group's kernel;
     against f64 numpy.  Rows that are not a whole number of warps are
-    declined (PFB_E_UNSUPPORTED) for the executor's materialised fallback."""
+    declined (PFB_E_UNSUPPORTED) for the executor's materialised fallback;
+    rows shorter than a warp share warps (lanes padded to a power of two)."""
     torch, lib, DArray, DType = env
     from paper_1903_04243_b200 import _native as N
     if not lib.pfb_fused_parts_ok():
@@ -245,7 +247,7 @@ def test_fused_row_sum_feed(env, rows, W, S):
     outs = (N.PfbTensor * 1)(out.desc())
     regs = (ctypes.c_int32 * 1)(4)
     rc = lib.pfb_fused_ew_rows(3, ins, spec, rsum, 5, flat, 1, regs, outs, None)
-    if W % 32:
+    if W % 32 and W > 32:
         assert rc == N.E_UNSUPPORTED
         return
     assert rc == 0
