@@ -63,8 +63,31 @@ def test_bench_program_specialised_equals_interpreter(name, lib):
         return Executor(w.graph).run(feeds=w.feeds)
     ref, got = _both(lib, run)
     assert len(ref) == len(got)
+    # a group with row-sum feeds (pass F16) sums its rows in the specialised
+    # kernel; with the specialiser off the executor materialises the sums with
+    # the reduction kernel first -- the same sums in another fp32
+    # association, so those programs agree to rounding, not bit for bit
+    rows = _has_rowsum(w.graph)
     for j, (r, g) in enumerate(zip(ref, got)):
-        assert _same(r, g), f"{name} output {j} differs"
+        if rows:
+            np.testing.assert_allclose(np.asarray(g.data, np.float64), np.asarray(r.data, np.float64),
+                                       rtol=1e-5, atol=1e-7, err_msg=f"{name} output {j}")
+        else:
+            assert _same(r, g), f"{name} output {j} differs"
+
+
+def _has_rowsum(graph):
+    from paper_1903_04243_b200 import passes
+    g2, _ = passes.optimize(graph, [tuple(o) for o in graph.outputs])
+
+    def scan(g):
+        for n in g.nodes.values():
+            if n.attrs.get("rowsum"):
+                return True
+            if n.block is not None and any(scan(sg) for sg in n.block.subgraphs.values()):
+                return True
+        return False
+    return scan(g2)
 
 
 def test_corpus_specialised_equals_interpreter(lib):
