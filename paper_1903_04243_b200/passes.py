@@ -1933,19 +1933,37 @@ def place_scatter_sums(g, keep=()):
         n1, n2, tail = len(i1), len(i2), list(sh1[1:])
         u1, u2 = Ref(g, *s1.inputs[1]), Ref(g, *s2.inputs[1])
         if np.array_equal(i1, np.arange(n1)) and np.array_equal(i2, np.arange(n1, T)):
-            merged = b.concat([u1, u2], 0)
+            first, second, inter = u1, u2, False
         elif np.array_equal(i2, np.arange(n2)) and np.array_equal(i1, np.arange(n2, T)):
-            merged = b.concat([u2, u1], 0)
+            first, second, inter = u2, u1, False
         elif n1 == n2 and 2 * n1 == T and {tuple(i1), tuple(i2)} == {
                 tuple(range(0, T, 2)), tuple(range(1, T, 2))}:
-            ev, od = (u1, u2) if i1[0] == 0 else (u2, u1)
-            merged = b.reshape(b.concat([b.reshape(ev, [n1, 1] + tail),
-                                         b.reshape(od, [n1, 1] + tail)], 1), [T] + tail)
+            first, second = (u1, u2) if i1[0] == 0 else (u2, u1)
+            inter = True
         else:
             continue
-        out = merged
-        for kind, arg in reversed(chain):
-            out = b.transpose(out, list(arg)) if kind == "transpose" else b.reshape(out, list(arg))
+        if len(chain) == 1 and chain[0][0] == "transpose":
+            # place in the consumer's layout: the pieces as transposed views
+            # (usually undoing the transpose that produced them) and the
+            # concat along the axis the scatter axis lands on
+            perm = list(chain[0][1])
+            a = perm.index(0)
+            p1, p2 = b.transpose(first, perm), b.transpose(second, perm)
+            osh = list(g.ref_shape((node.id, 0)))
+            if inter:
+                ins = lambda r: b.reshape(r, osh[:a] + [n1, 1] + osh[a + 1:])  # noqa: E731
+                out = b.reshape(b.concat([ins(p1), ins(p2)], a + 1), osh)
+            else:
+                out = b.concat([p1, p2], a)
+        else:
+            if inter:
+                merged = b.reshape(b.concat([b.reshape(first, [n1, 1] + tail),
+                                             b.reshape(second, [n1, 1] + tail)], 1), [T] + tail)
+            else:
+                merged = b.concat([first, second], 0)
+            out = merged
+            for kind, arg in reversed(chain):
+                out = b.transpose(out, list(arg)) if kind == "transpose" else b.reshape(out, list(arg))
         if tuple(g.ref_shape((out.nid, out.port))) != tuple(g.ref_shape((node.id, 0))):
             continue
         rw.redirect((node.id, 0), out)
