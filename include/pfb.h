@@ -286,6 +286,13 @@ int pfb_set_condition(uint64_t handle, const void* flag, void* counter, void* st
  * mask: n dense u8 bools. */
 int pfb_set_condition_any(uint64_t handle, const void* mask, int64_t n, void* counter,
                           void* stream);
+/* pfb_copy_many (the loop's carried write-back) that also sets the loop's
+ * conditional to any(srcs[any_pair]) (u8 bools, the predicated while's
+ * active mask): one launch per trip for both.  scratch: 2 device int32,
+ * zero before the first call (the kernel leaves them zero).  n <= 16. */
+int pfb_copy_many_cond(int32_t n, const pfb_tensor* srcs, const pfb_tensor* dsts,
+                       int32_t any_pair, uint64_t handle, void* counter, void* scratch,
+                       void* stream);
 int pfb_loop_finalize(void* loop, void* head_graph, void* iter_graph);
 int pfb_loop_launch(void* loop, void* stream);
 int pfb_loop_destroy(void* loop);

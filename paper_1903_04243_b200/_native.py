@@ -90,6 +90,7 @@ _SIGNATURES = {
                         ctypes.c_int),
     "pfb_set_condition": ([ctypes.c_uint64, _vp, _vp, _vp], ctypes.c_int),
     "pfb_set_condition_any": ([ctypes.c_uint64, _vp, ctypes.c_int64, _vp, _vp], ctypes.c_int),
+    "pfb_copy_many_cond": ([_i32, _P, _P, _i32, ctypes.c_uint64, _vp, _vp, _vp], ctypes.c_int),
     "pfb_loop_finalize": ([_vp, _vp, _vp], ctypes.c_int),
     "pfb_loop_launch": ([_vp, _vp], ctypes.c_int),
     "pfb_loop_destroy": ([_vp], ctypes.c_int),

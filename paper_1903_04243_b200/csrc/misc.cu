@@ -136,7 +136,75 @@ __global__ void __launch_bounds__(256) copy_many_kernel(CopyDesc d) {
   for (int64_t i = 16 * n16 + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < nb; i += stride)
     o[i] = s[i];
 }
+// copy_many + the predicated while's loop test: pair `any_pair` is the
+// active mask (u8 bools); every block of that pair ORs its bytes into
+// scratch[0], every block takes a ticket (scratch[1]) and the last one sets
+// the CUDA-graph conditional to any(mask) and resets the scratch words for
+// the next trip -- the write-back and the test in one launch
+__global__ void __launch_bounds__(256) copy_many_cond_kernel(CopyDesc d, int any_pair,
+                                                             cudaGraphConditionalHandle h,
+                                                             unsigned long long* counter,
+                                                             int* scratch) {
+  pdl_enter();
+  const int t = blockIdx.y;
+  const uint8_t* s = d.src[t];
+  uint8_t* o = d.dst[t];
+  const int64_t nb = d.bytes[t];
+  const bool vec = ((reinterpret_cast<uintptr_t>(s) | reinterpret_cast<uintptr_t>(o)) & 15) == 0;
+  const int64_t n16 = vec ? nb / 16 : 0;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  int any = 0;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n16; i += stride) {
+    const int4 v = __ldg(reinterpret_cast<const int4*>(s) + i);
+    reinterpret_cast<int4*>(o)[i] = v;
+    any |= (v.x | v.y | v.z | v.w) != 0;
+  }
+  for (int64_t i = 16 * n16 + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < nb; i += stride) {
+    const uint8_t v = s[i];
+    o[i] = v;
+    any |= v != 0;
+  }
+  any = __syncthreads_or(t == any_pair && any);
+  if (threadIdx.x == 0) {
+    if (any) atomicOr(&scratch[0], 1);
+    __threadfence();
+    const unsigned total = gridDim.x * gridDim.y;
+    if ((unsigned)atomicAdd(&scratch[1], 1) == total - 1) {
+      __threadfence();
+      const int flag = atomicOr(&scratch[0], 0);
+      cudaGraphSetConditional(h, flag ? 1u : 0u);
+      if (counter) *counter += 1;
+      scratch[0] = 0;
+      scratch[1] = 0;
+    }
+  }
+}
 }  // namespace pfb
+
+extern "C" int pfb_copy_many_cond(int32_t n, const pfb_tensor* srcs, const pfb_tensor* dsts,
+                                  int32_t any_pair, uint64_t handle, void* counter, void* scratch,
+                                  void* stream) {
+  if (n < 1 || n > kMaxPack || any_pair < 0 || any_pair >= n || scratch == nullptr)
+    return PFB_E_ARG;
+  if (srcs[any_pair].dtype != PFB_BOOL) return PFB_E_DTYPE;
+  CopyDesc d = {};
+  int64_t most = 0;
+  for (int j = 0; j < n; ++j) {
+    const pfb_tensor* x = &srcs[j];
+    const pfb_tensor* y = &dsts[j];
+    if (!is_dense(x) || !is_dense(y) || x->dtype != y->dtype || numel(x) != numel(y))
+      return PFB_E_UNSUPPORTED;
+    d.src[j] = static_cast<const uint8_t*>(x->data);
+    d.dst[j] = static_cast<uint8_t*>(y->data);
+    d.bytes[j] = numel(x) * dtype_size(x->dtype);
+    if (d.bytes[j] > most) most = d.bytes[j];
+  }
+  const int gx = grid_for(most > 0 ? (most + 15) / 16 : 1, 256, 2);
+  launch(copy_many_cond_kernel, dim3((unsigned)gx, (unsigned)n), 256, 0, as_stream(stream), d,
+         (int)any_pair, (cudaGraphConditionalHandle)handle, (unsigned long long*)counter,
+         (int*)scratch);
+  return launch_status();
+}
 
 extern "C" int pfb_copy_many(int32_t n, const pfb_tensor* srcs, const pfb_tensor* dsts,
                              void* stream) {

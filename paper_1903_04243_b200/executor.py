@@ -708,6 +708,7 @@ class Executor:
             bind = {"capture": list(caps), "carried": state}
 
             any_src = _any_mask_test(cg)
+            scratch = torch.zeros(2, dtype=torch.int32, device=self.device)
 
             def cond_to_handle():
                 if any_src is not None:  # any(active): one launch (pfb_set_condition_any)
@@ -748,8 +749,21 @@ class Executor:
                         srcs.append(self._dense_copy(src))
                     else:
                         srcs.append(src)
-                self._copy_pairs([(src, dst) for src, dst in zip(srcs, state) if src is not None])
-                cond_to_handle()
+                pairs = [(src, dst) for src, dst in zip(srcs, state) if src is not None]
+                mpos = next((i for i, (_, dst) in enumerate(pairs)
+                             if any_src is not None and dst is state[any_src]), None)
+                if mpos is not None and len(pairs) <= 16 and \
+                        all(a.is_dense() and b.is_dense() for a, b in pairs):
+                    # write-back + any(active) in one launch (pfb_copy_many_cond)
+                    xs = (N.PfbTensor * len(pairs))(*[a.desc() for a, _ in pairs])
+                    ys = (N.PfbTensor * len(pairs))(*[b.desc() for _, b in pairs])
+                    self._call(self._lib.pfb_copy_many_cond, len(pairs), xs, ys, mpos,
+                               handle.value, counter.data_ptr(), scratch.data_ptr(),
+                               self._stream, what="copy",
+                               work=(2 * _abytes(*[a for a, _ in pairs]), 0))
+                else:
+                    self._copy_pairs(pairs)
+                    cond_to_handle()
             l2 = self.launch_count
             rc = self._lib.pfb_loop_finalize(loop, ctypes.c_void_p(head.raw_cuda_graph()),
                                              ctypes.c_void_p(it.raw_cuda_graph()))
@@ -757,6 +771,7 @@ class Executor:
                 raise RuntimeError(f"pfb_loop_finalize failed ({rc})")
             lp = _DeviceLoop(loop.value, state, counter, (head, it), self._ws, self._err,
                              list(self._err_nodes))
+            lp.scratch = scratch
             lp.head_launches, lp.iter_launches = l1 - l0 + 1, l2 - l1 + 1
             self._launches = l0
             self._loops[sig] = lp

@@ -84,3 +84,26 @@ def test_cfg5_merged_gathers_raise_out_of_range(env):
     with pytest.raises(errors.ExecError) as e:
         Executor(w.graph, device="cuda:0").run(feeds=feeds)
     assert isinstance(e.value.cause, errors.IndexOutOfBounds)
+
+
+def test_cfg5_device_loop_trips_and_launches(env):
+    """The predicated device loop of cfg5 (unroll 4): one pass of the head and
+    exactly ceil(max(lengths) / 4) trips per run (the loop test any(active)
+    is set by the write-back kernel, pfb_copy_many_cond), and per trip only
+    the per-step work plus the trip's index group, merged gather and
+    write-back: 4 GEMMs + 4 select groups + 3 launches."""
+    torch, N, DArray, DType = env
+    from paper_1903_04243_b200 import workloads as WL
+    from paper_1903_04243_b200.executor import Executor
+    w = WL.BUILDERS["cfg5"](WL.this_api(), n=512, max_len=23, units=256, masked=True, unroll=4)
+    ex = Executor(w.graph, device="cuda:0")
+    for _ in range(3):
+        ex.run(feeds=w.feeds)
+    assert ex._loops, ex.capture_failures
+    (lp,) = ex._loops.values()
+    assert lp.iter_launches <= 11, lp.iter_launches
+    c0 = int(lp.counter.item())
+    ex.run(feeds=w.feeds)
+    torch.cuda.synchronize()
+    trips = -(-int(np.max(w.feeds["lengths"])) // 4)
+    assert int(lp.counter.item()) - c0 == 1 + trips
