@@ -63,9 +63,15 @@ __device__ __forceinline__ void cp_async4(float* smem, const float* gmem, bool p
 
 constexpr int NST = 4;  // k-tiles in flight (cp.async ring)
 
+// split-K tile tickets of the workspace path (last split reduces); every
+// launch leaves them zero.  One stream at a time per process uses them (the
+// executor's), so a launch never shares a ticket with a concurrent one.
+constexpr unsigned kSimtTiles = 1u << 16;
+__device__ unsigned g_simt_tiles[kSimtTiles];
+
 template <bool KS, bool CL>
 __global__ void __launch_bounds__(256) gemm_simt_kernel(GemmArgs g, int splits, int64_t kchunk,
-                                                        float* partials) {
+                                                        float* partials, bool tile_reduce) {
   pdl_enter();
   // NST-deep cp.async ring of A/B k-tiles: a CTA's whole K range (<= 4
   // k-tiles for split-K shapes) is requested at once, so a small GEMM pays
@@ -199,6 +205,34 @@ __global__ void __launch_bounds__(256) gemm_simt_kernel(GemmArgs g, int splits, 
 #pragma unroll
       for (int j = 0; j < 4; ++j)
         if (n0 + tn + j < g.N) P[gm * g.N + n0 + tn + j] = acc[i][j];
+    }
+    // the last split of this tile to finish sums all partials of the tile in
+    // split order (the reduce kernel's order: deterministic) and applies the
+    // epilogue -- no second launch.  Tile tickets wrap to 0 (atomicInc), so
+    // the counters are clean for the next launch.
+    if (!tile_reduce) return;
+    __shared__ unsigned last;
+    __threadfence();
+    __syncthreads();
+    if (tid == 0) {
+      const unsigned tile = ((unsigned)bz * gridDim.y + blockIdx.y) * gridDim.x + blockIdx.x;
+      last = atomicInc(&g_simt_tiles[tile], (unsigned)splits - 1) == (unsigned)splits - 1;
+    }
+    __syncthreads();
+    if (last) {
+      __threadfence();
+      const int64_t per = g.M * g.N, total = g.batch * per;
+      for (int e = tid; e < BM * BN; e += 256) {
+        const int64_t gm = m0 + e / BN, gn = n0 + e % BN;
+        if (gm >= g.M || gn >= g.N) continue;
+        const int64_t off = bz * per + gm * g.N + gn;
+        float v = 0.f;
+        for (int q = 0; q < splits; ++q) v += __ldcg(partials + (int64_t)q * total + off);
+        if (g.alpha_rows) v *= g.alpha_rows[bz * g.M + gm];
+        float* c = g.C + bz * g.scb + gm * g.scm + gn * g.scn;
+        if (g.accumulate) v += *c;
+        *c = epi_value(g, bz, gm, gn, v);
+      }
     }
   }
 }
@@ -476,7 +510,7 @@ static void launch_clustered(const GemmArgs& g, dim3 grid, int splits, int64_t k
   cfg.attrs = at;
   cfg.numAttrs = pdl_enabled() ? 2 : 1;
   kernel_launches()++;
-  cudaLaunchKernelEx(&cfg, gemm_simt_kernel<KS, true>, g, splits, kchunk, (float*)nullptr);
+  cudaLaunchKernelEx(&cfg, gemm_simt_kernel<KS, true>, g, splits, kchunk, (float*)nullptr, false);
 }
 
 bool gemm_simt_splittable(const GemmArgs& g) {
@@ -530,12 +564,19 @@ int gemm_simt_v(const GemmArgs& g, void* ws, int64_t ws_bytes, cudaStream_t s, i
     return launch_status();
   }
   float* part = splits > 1 ? (float*)ws : nullptr;
-  if (g.kscale)
-    launch(gemm_simt_kernel<true, false>, grid, 256, 0, s, g, splits, kchunk, part);
-  else
-    launch(gemm_simt_kernel<false, false>, grid, 256, 0, s, g, splits, kchunk, part);
-  if (splits > 1)
+  if (splits > 1 && (int64_t)grid.x * grid.y * (grid.z / splits) > (int64_t)kSimtTiles) {
+    // more tiles than tickets: partials, then the reduce kernel
+    if (g.kscale)
+      launch(gemm_simt_kernel<true, false>, grid, 256, 0, s, g, splits, kchunk, part, false);
+    else
+      launch(gemm_simt_kernel<false, false>, grid, 256, 0, s, g, splits, kchunk, part, false);
     launch(splitk_reduce, grid_for(g.batch * g.M * g.N, 256), 256, 0, s, g, splits, (const float*)ws);
+    return launch_status();
+  }
+  if (g.kscale)
+    launch(gemm_simt_kernel<true, false>, grid, 256, 0, s, g, splits, kchunk, part, true);
+  else
+    launch(gemm_simt_kernel<false, false>, grid, 256, 0, s, g, splits, kchunk, part, true);
   return launch_status();
 }
 

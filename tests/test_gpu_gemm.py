@@ -419,3 +419,21 @@ def test_gemm_narrow_tiles_epilogue(env, force):
     alpha = np.asarray(r.standard_normal(256), np.float32).astype(np.float64)
     got = _run(env, a, b, force, accumulate_into=c0, alpha=alpha)
     np.testing.assert_allclose(got, c0 + alpha[:, None] * (a @ b), rtol=RTOL, atol=ATOL)
+
+
+@pytest.mark.parametrize("shape", [(128, 256, 784), (784, 256, 128), (70, 130, 600), (3, 200, 90, 500)])
+def test_gemm_simt_splitk_last_tile_reduce(env, shape):
+    """SIMT split-K through the workspace (path 11, 16 k-splits): the last
+    split of each tile sums the partials in split order and applies alpha /
+    accumulate -- one launch, deterministic (bit-identical reruns, so the
+    tile tickets are clean after every launch), against f64."""
+    r = np.random.default_rng(sum(shape))
+    *bt, m, n, k = shape
+    a, b = _operands(r, tuple(bt) + (m, k), tuple(bt) + (k, n))
+    c0 = _f32(r, tuple(bt) + (m, n))
+    alpha = _f32(r, (int(np.prod(bt or [1])) * m,))
+    runs = [_run(env, a, b, 11, accumulate_into=c0, alpha=alpha) for _ in range(3)]
+    want = (a @ b) * alpha.reshape(tuple(bt) + (m, 1)) + c0
+    np.testing.assert_allclose(runs[0], want, rtol=RTOL, atol=ATOL)
+    for x in runs[1:]:
+        np.testing.assert_array_equal(x, runs[0])
