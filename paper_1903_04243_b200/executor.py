@@ -752,8 +752,9 @@ class Executor:
                 pairs = [(src, dst) for src, dst in zip(srcs, state) if src is not None]
                 mpos = next((i for i, (_, dst) in enumerate(pairs)
                              if any_src is not None and dst is state[any_src]), None)
-                if mpos is not None and len(pairs) <= 16 and \
-                        all(a.is_dense() and b.is_dense() for a, b in pairs):
+                fused_test = mpos is not None and len(pairs) <= 16 and \
+                    all(a.is_dense() and b.is_dense() for a, b in pairs)
+                if fused_test:
                     # write-back + any(active) in one launch (pfb_copy_many_cond)
                     xs = (N.PfbTensor * len(pairs))(*[a.desc() for a, _ in pairs])
                     ys = (N.PfbTensor * len(pairs))(*[b.desc() for _, b in pairs])
@@ -772,7 +773,9 @@ class Executor:
             lp = _DeviceLoop(loop.value, state, counter, (head, it), self._ws, self._err,
                              list(self._err_nodes))
             lp.scratch = scratch
-            lp.head_launches, lp.iter_launches = l1 - l0 + 1, l2 - l1 + 1
+            # (+1: the set-condition kernel, launched outside _call; a trip
+            # whose write-back kernel sets the condition has none)
+            lp.head_launches, lp.iter_launches = l1 - l0 + 1, l2 - l1 + (0 if fused_test else 1)
             self._launches = l0
             self._loops[sig] = lp
         except Exception as e:  # the loop stays on the host
