@@ -107,3 +107,26 @@ def test_cfg5_device_loop_trips_and_launches(env):
     torch.cuda.synchronize()
     trips = -(-int(np.max(w.feeds["lengths"])) // 4)
     assert int(lp.counter.item()) - c0 == 1 + trips
+
+
+def test_replay_reads_device_feeds_in_place(env):
+    """run_device with the same device tensors: from the second run on, the
+    captured graph reads the feeds in place (no copy into static inputs), and
+    it sees in-place updates of them; results equal a fresh executor's."""
+    torch, N, DArray, DType = env
+    from paper_1903_04243_b200 import workloads as WL
+    from paper_1903_04243_b200.executor import Executor
+    w = WL.BUILDERS["cfg2"](WL.this_api(), n=32, model="mlp")
+    dev = torch.device("cuda:0")
+    feeds = {k: torch.as_tensor(np.asarray(v, np.float32)).to(dev) for k, v in w.feeds.items()}
+    ex = Executor(w.graph, device="cuda:0")
+    for _ in range(4):
+        ex.run_device(feeds)
+    assert any(len(k) == 3 for k in ex._captures), list(ex._captures)
+    feeds["x"].mul_(0.5)
+    got = [o.to_numpy() for o in ex.run_device(feeds)]
+    want = Executor(w.graph, device="cuda:0", cuda_graph=False).run(
+        feeds={k: v.cpu().numpy() for k, v in feeds.items()})
+    for g_, w_ in zip(got, want):
+        np.testing.assert_allclose(np.asarray(g_, np.float64), np.asarray(w_.data, np.float64),
+                                   rtol=1e-5, atol=1e-6)
