@@ -1348,10 +1348,11 @@ def fuse_elementwise(g, keep=()):
         if built is None:
             group = grow(root, False, domain)
             if len(group) < 2:
-                # a lone integer op (the loop-trip `select` of a predicated
-                # while body) may still merge with a sibling group below;
-                # unmerged singletons are dropped after merging
-                return (group, None) if domain == "int" and len(group) == 1 else None
+                # a lone op (the loop-trip `select` of a predicated while
+                # body, the maxpool's backward mask compare) may still merge
+                # with a sibling / producer group below; unmerged singletons
+                # are dropped after merging
+                return (group, None) if len(group) == 1 else None
             built = build(root, group, domain)
         return None if built is None else (group, built)
 
@@ -2007,7 +2008,12 @@ def _with_post_ops(node, k, post):
     used = {st[1] for st in prog} | {st[2] for st in prog if st[0] not in (OP_LOAD, OP_CONST)} | \
         {st[3] for st in prog if st[0] not in (OP_LOAD, OP_CONST)}
     free = [t for t in range(MAX_REGS) if t not in used]
-    if r in outs or not free:
+    last_write = {}
+    for j, st in enumerate(prog):
+        last_write[st[1]] = j
+    # the loaded value itself must not be an output (a passthrough); a later
+    # step that reuses r as an output register overwrites it anyway
+    if (r in outs and last_write.get(r) == i) or not free:
         return None
     t = free[0]
     extra = []
