@@ -12,10 +12,10 @@ mkdir -p $OUT
 CONFIGS=${CONFIGS:-"cfg2_mlp cfg1_full cfg1_batch cfg2_conv cfg3 cfg4 cfg5"}
 declare -A TOP=( [cfg2_mlp]="regex:gemm_simt" [cfg1_full]="regex:gemm_kernel|pair_kernel" \
                  [cfg3]="regex:outer1|gemm_smallk" [cfg4]="regex:parts_kernel" \
-                 [cfg5]="regex:gemm" [cfg2_conv]="regex:pfb_fused_jit|fused_kernel|conv2d" \
+                 [cfg5]="regex:pfb_fused_jit" [cfg2_conv]="regex:pfb_fused_jit|fused_kernel|conv2d" \
                  [cfg1_batch]="regex:gemm" )
 declare -A SKIP=( [cfg2_mlp]=6 [cfg1_full]=3 [cfg1_batch]=3 [cfg2_conv]=3 [cfg3]=3 \
-                  [cfg4]=3 [cfg5]=3 )
+                  [cfg4]=3 [cfg5]=40 )
 for c in $CONFIGS; do
   export PFB_GEMM_TUNE_FILE=$OUT/tune_$c.txt
   rm -f $PFB_GEMM_TUNE_FILE
