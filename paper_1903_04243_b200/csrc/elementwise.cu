@@ -790,8 +790,12 @@ static int fused_impl(int32_t n_in, const pfb_tensor* ins, int32_t n_steps,
   if (rowsum) {
     bool any = false;
     for (int k = 0; k < n_in; ++k) {
+      // j | op << 16: the sum of input j (op: a unary program opcode applied
+      // to it first, 0 = none)
       RS[k] = rowsum[k] < 0 ? -1 : rowsum[k];
-      if (RS[k] >= n_in) return PFB_E_ARG;
+      const int op = RS[k] < 0 ? 0 : RS[k] >> 16;
+      if (RS[k] >= 0 && ((RS[k] & 0xffff) >= n_in || (op != 0 && (op < 16 || op > 16 + PFB_SQUARE))))
+        return PFB_E_ARG;
       any = any || RS[k] >= 0;
     }
     if (!any) rowsum = nullptr;

@@ -164,6 +164,22 @@ std::string gen_offsets(const FLayout& L, int nops, int V, bool idx64, bool off3
   return s;
 }
 
+// a unary program opcode (16 + PFB_*) applied to expression x, as the
+// program steps evaluate it; op 0 = x itself
+std::string unary_expr(int op, const std::string& x) {
+  switch (op) {
+    case 0: return x;
+    case 16 + PFB_NEG: return "(-" + x + ")";
+    case 16 + PFB_EXP: return "expf(" + x + ")";
+    case 16 + PFB_LOG: return "logf(" + x + ")";
+    case 16 + PFB_RELU: return "np_max(" + x + ", 0.f)";
+    case 16 + PFB_TANH: return "tanhf(" + x + ")";
+    case 16 + PFB_SIGMOID: return "(1.f / (1.f + expf(-" + x + ")))";
+    case 16 + PFB_SQUARE: return "(" + x + " * " + x + ")";
+    default: return x;
+  }
+}
+
 std::string gen_source(const FusedProgram& P, int V, bool idx64, FeedModes modes,
                        const PartsSpec* PS = nullptr, const FLayout* LS = nullptr,
                        bool off32 = false, const int* RS = nullptr, int lpr = 0) {
@@ -256,8 +272,9 @@ std::string gen_source(const FusedProgram& P, int V, bool idx64, FeedModes modes
     bool any = false;
     for (int k = 0; k < P.n_in; ++k) {
       if (RS[k] < 0) continue;
+      const std::string x = unary_expr(RS[k] >> 16, fmt("in%d_0", RS[k] & 0xffff));
       if (lpr > 0) {  // short rows: a segmented xor tree inside each lpr-lane group
-        s += fmt("    float in%d_0;\n    { float v = valid ? in%d_0 : 0.f;\n", k, RS[k]);
+        s += fmt("    float in%d_0;\n    { float v = valid ? ", k) + x + " : 0.f;\n";
         s += fmt("      for (int o = %d; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);\n",
                  lpr / 2);
         s += fmt("      in%d_0 = v; }\n", k);
@@ -265,7 +282,7 @@ std::string gen_source(const FusedProgram& P, int V, bool idx64, FeedModes modes
       }
       if (!any) s += "    __shared__ float rs_red[32];\n    const int rs_w = threadIdx.x >> 5, rs_l = threadIdx.x & 31;\n";
       any = true;
-      s += fmt("    float in%d_0;\n    { float v = in%d_0;\n", k, RS[k]);
+      s += fmt("    float in%d_0;\n    { float v = ", k) + x + ";\n";
       s += "      for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);\n"
            "      if (rs_l == 0) rs_red[rs_w] = v;\n      __syncthreads();\n"
            "      float t = rs_red[0];\n      for (int w = 1; w < (int)(blockDim.x >> 5); ++w) t += rs_red[w];\n"
@@ -600,8 +617,9 @@ bool fused_rows_jit_launch(const FusedProgram& P, FeedModes modes, const FLayout
   if (n % W != 0) return false;
   for (int k = 0; k < P.n_in; ++k) {
     if (rowsum[k] < 0) continue;
-    if (rowsum[k] >= P.n_in || rowsum[k] == k || rowsum[rowsum[k]] >= 0 ||
-        P.in_dtype[rowsum[k]] != PFB_F32 || L.st[k + 1][ir] != 0)
+    const int j = rowsum[k] & 0xffff;
+    if (j >= P.n_in || j == k || rowsum[j] >= 0 || P.in_dtype[j] != PFB_F32 ||
+        L.st[k + 1][ir] != 0)
       return false;
     for (int d = 0; d < ir; ++d)
       if (L.shape[d] > 1 && L.st[k + 1][d] == 0) return false;

@@ -2001,17 +2001,20 @@ def _fused_launch(ex, arrs, prog, regs, nregs, outs):
 
 
 def _fused_rows(ex, node, arrs, prog, regs, nregs, outs):
-    """A group with row-sum feeds (pass F16, attrs["rowsum"] = ((k, j), ..)):
-    input k is the sum of input j over the row, computed by the group's own
-    kernel (pfb_fused_ew_rows; slot k carries input j's array, described with
-    the sum's broadcast shape [n, 1, .., 1]).  Rows the kernel does not take
-    (not a whole number of warps, > 1024 wide, no NVRTC) get their sums
-    materialised first (reduce_sum as before) and the group runs as usual."""
-    rs = dict(node.attrs["rowsum"])
+    """A group with row-sum feeds (pass F16, attrs["rowsum"] = ((k, j[, op]),
+    ..)): input k is the sum over the row of input j (or of op(input j), a
+    unary program opcode the group also applies to j after loading it),
+    computed by the group's own kernel (pfb_fused_ew_rows; slot k carries
+    input j's array, described with the sum's broadcast shape [n, 1, .., 1];
+    rowsum[k] = j | op << 16).  Rows the kernel does not take (> 32 and not a
+    whole number of warps, > 1024 wide, no NVRTC) get their sums materialised
+    first (reduce_sum as before) and the group runs as usual."""
+    ents = [tuple(e) for e in node.attrs["rowsum"]]
+    rs = {e[0]: (e[1], e[2] if len(e) > 2 else 0) for e in ents}
     shape = outs[0].shape
     bshape = (shape[0],) + (1,) * (len(shape) - 1)
     views = list(arrs)
-    for k, j in rs.items():
+    for k, (j, _) in rs.items():
         x = arrs[j]
         views[k] = DArray(x.buf, x.offset, bshape, (x.strides[0],) + (0,) * (len(shape) - 1),
                           x.dtype)
@@ -2022,7 +2025,8 @@ def _fused_rows(ex, node, arrs, prog, regs, nregs, outs):
         for a in views:
             spec += list(a.parts) if a.parts is not None else [1, 0]
         pa = (ctypes.c_int64 * len(spec))(*spec)
-        rsa = (ctypes.c_int32 * len(views))(*[rs.get(k, -1) for k in range(len(views))])
+        codes = [rs[k][0] | (rs[k][1] << 16) if k in rs else -1 for k in range(len(views))]
+        rsa = (ctypes.c_int32 * len(views))(*codes)
         descs = (N.PfbTensor * len(views))(*[a.desc_part0() for a in views])
         odescs = (N.PfbTensor * len(outs))(*[o.desc() for o in outs])
         nbytes = sum(_abytes(a) * (a.parts[0] if a.parts else 1)
@@ -2037,9 +2041,15 @@ def _fused_rows(ex, node, arrs, prog, regs, nregs, outs):
                  ex._stream, what="fused_ew", work=(nbytes + _abytes(*outs), 0))
         if status[-1] == 0:
             return
-    for k, j in rs.items():
+    for k, (j, op) in rs.items():
+        src = arrs[j]
+        if op:  # the summand op(input j), materialised for the reduction
+            src = ex._reduce_parts(src)
+            t = ex._empty(src.shape, src.dtype)
+            ex._call(ex._lib.pfb_unary, op - 16, src.desc(), t.desc(), ex._stream, what="unary")
+            src = t
         stub = _NodeStub({"axes": tuple(range(1, len(shape)))})
-        (sm,) = _h_reduce_sum(ex, stub, [arrs[j]])
+        (sm,) = _h_reduce_sum(ex, stub, [src])
         views[k] = sm.view(bshape, (sm.strides[0],) + (0,) * (len(shape) - 1))
     if any(a.parts is not None for a in views) or nregs != 1:
         _fused_launch(ex, views, prog, regs, nregs, outs)

@@ -1812,18 +1812,34 @@ def fuse_row_sums(g, keep=()):
             if tuple(sorted(normalize_axes(r.attrs["axes"], len(xsh)))) != tuple(range(1, len(xsh))):
                 continue
             j = ins.index(x)
-            if any(jj == k for _, jj in rs):
+            if any(e[1] == k for e in rs):
                 continue
             if post:
                 prog = _with_post_ops(node, k, post[::-1])
                 if prog is None:
                     continue
                 node.attrs["program"] = prog
-            rs.append((k, j))
+            # the summand's own unary producer (cfg2's exp of the logits),
+            # read nowhere else, moves into the group too: the kernel sums
+            # op(input) and the program applies op after the input's load
+            xn = rw.node(x)
+            pre = None
+            if xn.kind in _UN_CODE and xn.kind != "logical_not" and x[1] == 0 and \
+                    xn.out_dtypes[0] == DType.F64 and \
+                    all(n is node or n is r for n, _ in rw.users().get(x, []) if n.id in live) and \
+                    g.ref_dtype(xn.inputs[0]) == DType.F64 and \
+                    tuple(g.ref_shape(xn.inputs[0]) or ()) == tuple(osh):
+                prog = _with_post_ops(node, j, [("un", 16 + _UN_CODE[xn.kind])])
+                if prog is not None:
+                    node.attrs["program"] = prog
+                    node.inputs[j] = tuple(xn.inputs[0])
+                    ins[j] = tuple(xn.inputs[0])
+                    pre = 16 + _UN_CODE[xn.kind]
+            rs.append((k, j) if pre is None else (k, j, pre))
         if not rs:
             continue
-        for k, j in rs:
-            node.inputs[k] = node.inputs[j]
+        for e in rs:
+            node.inputs[e[0]] = node.inputs[e[1]]
         node.attrs["rowsum"] = tuple(rs)
         rw._users = None
         g._topo_cache = None

@@ -256,3 +256,31 @@ def test_fused_row_sum_feed(env, rows, W, S):
     want = z.sum(axis=2, keepdims=True) * c + z
     np.testing.assert_allclose(out.to_numpy().astype(np.float64), want, rtol=RTOL,
                                atol=ATOL * np.sqrt(W) * 4)
+
+
+@pytest.mark.parametrize("rows,W", [(128, 10), (300, 256), (7, 1)])
+def test_fused_row_sum_of_exp_is_softmax(env, rows, W):
+    """pfb_fused_ew_rows with a summand op: rowsum[1] = 0 | (16 + exp) << 16
+    makes input 1 the row sum of exp(input 0); the program exp(in0) / in1 is
+    the softmax (cfg2's cross-entropy), against f64 numpy."""
+    torch, lib, DArray, DType = env
+    from paper_1903_04243_b200 import _native as N, passes
+    if not lib.pfb_fused_parts_ok():
+        pytest.skip("specialiser unavailable")
+    dev = torch.device("cuda")
+    r = np.random.default_rng(rows * W)
+    z = r.standard_normal((rows, 1, W)).astype(np.float32)
+    Z = DArray.from_numpy(z, DType.F64, dev)
+    rs = Z.view((rows, 1, 1), (Z.strides[0], 0, 0))
+    out = DArray.empty((rows, 1, W), DType.F64, dev)
+    EXP = 16 + passes._UN_CODE["exp"]
+    prog = [(64, 0, 0, 0), (EXP, 0, 0, 0), (64, 1, 1, 0), (passes._BIN_CODE["div"], 2, 0, 1)]
+    flat = (ctypes.c_int32 * 16)(*[v for st in prog for v in st])
+    rsum = (ctypes.c_int32 * 2)(-1, 0 | (EXP << 16))
+    ins = (N.PfbTensor * 2)(Z.desc(), rs.desc())
+    outs = (N.PfbTensor * 1)(out.desc())
+    regs = (ctypes.c_int32 * 1)(2)
+    assert lib.pfb_fused_ew_rows(2, ins, None, rsum, 4, flat, 1, regs, outs, None) == 0
+    torch.cuda.synchronize()
+    e = np.exp(z.astype(np.float64))
+    np.testing.assert_allclose(out.to_numpy(), e / e.sum(axis=2, keepdims=True), rtol=1e-5, atol=1e-7)

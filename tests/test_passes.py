@@ -452,3 +452,18 @@ def test_f18_split_scatter_sum_is_a_concat():
     got = OracleExecutor(g2).run(feeds={"x": xv}, outputs=[g2.out(*mp[keys[0]])])[0].data
     np.testing.assert_array_equal(got, want)
     np.testing.assert_array_equal(want, np.concatenate([xv[2:5], 2 * xv[0:2]]))
+
+
+def test_f16_softmax_exp_and_division_move_into_the_group():
+    """cfg2 (mlp): the softmax's exp producer, row sum and 1/sum all run in
+    the group that reads them (rowsum entry (k, j, exp)); no exp, no division
+    and no row reduction stays live; oracle values unchanged."""
+    from paper_1903_04243_b200 import passes
+    w = WL.cfg2(WL.this_api(), n=4, model="mlp")
+    g, g2, m = _run_both(w)
+    live = passes.live_set(g2, [m[tuple(o)] for o in g.outputs])
+    nodes = [g2.nodes[i] for i in live]
+    kinds = [n.kind for n in nodes]
+    assert "exp" not in kinds and "div" not in kinds, kinds
+    ents = [e for n in nodes if n.attrs.get("rowsum") for e in n.attrs["rowsum"]]
+    assert any(len(e) == 3 and e[2] == 16 + passes._UN_CODE["exp"] for e in ents), ents
