@@ -98,7 +98,9 @@ int pfb_fused_ew_parts(int32_t n_in, const pfb_tensor* ins, const int64_t* parts
 /* pfb_fused_ew_parts with row-sum feeds (pass F16): rowsum[k] >= 0 makes
  * input k the sum of input rowsum[k] over the row (the innermost dim of the
  * outputs' layout) -- ins[k] then only describes the broadcast shape (its
- * data is not read); rowsum[k] < 0 = a normal input.  The sums are computed
+ * data is not read); rowsum[k] < 0 = a normal input.  rowsum[k] = j | op << 16
+ * sums op(input j) instead, op a unary program opcode (16 + PFB_NEG ..
+ * PFB_SQUARE; the softmax's exp).  The sums are computed
  * in the kernel (one row per block: a whole number of warps, <= 1024 wide),
  * so a row reduction feeding an elementwise group costs no launch of its own
  * (cfg5's per-step `reduce_sum(z) < 0` branch mask; reference
