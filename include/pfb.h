@@ -110,6 +110,13 @@ int pfb_fused_ew_parts(int32_t n_in, const pfb_tensor* ins, const int64_t* parts
 int pfb_fused_ew_rows(int32_t n_in, const pfb_tensor* ins, const int64_t* parts,
                       const int32_t* rowsum, int32_t n_steps, const int32_t* program,
                       int32_t n_out, const int32_t* out_regs, pfb_tensor* outs, void* stream);
+/* q <= 8 weighted column sums in one launch (pass F19): outs[k][c] =
+ * sum_r xs[k][r, c] * y[r] (xs[k] [R, C_k] any strides, y [R] or [R, 1]) --
+ * the clipped per-example bias-gradient sums of several parameter blocks
+ * sharing the clip scales (reference reduce_sum of a product, tensor.py:279-283).
+ * outs[k] dense [C_k]. */
+int pfb_col_dots(int32_t q, const pfb_tensor* xs, const pfb_tensor* y, pfb_tensor* outs,
+                 void* stream);
 /* out[i] = sum_s sum_k x_s[i, k], x_s = x + s * part_stride (x: [rows, W] view
  * with unit inner stride): the row sums of a GEMM result still held as
  * split-K partials (pass F15; reference tensor.reduce_sum, tensor.py:279-283). */

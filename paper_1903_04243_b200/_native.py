@@ -51,6 +51,7 @@ _SIGNATURES = {
     "pfb_fused_ew_rows": ([_i32, _P, ctypes.POINTER(ctypes.c_int64), ctypes.POINTER(_i32), _i32,
                            ctypes.POINTER(_i32), _i32, ctypes.POINTER(_i32), _P, _vp], ctypes.c_int),
     "pfb_fused_parts_ok": ([], ctypes.c_int),
+    "pfb_col_dots": ([_i32, _P, _P, _P, _vp], ctypes.c_int),
     "pfb_row_sum_parts": ([_P, _i32, ctypes.c_int64, _P, _vp], ctypes.c_int),
     "pfb_fused_jit_config": ([_i32, ctypes.c_int64], ctypes.c_int),
     "pfb_kernel_launches": ([], ctypes.c_int64),

@@ -619,6 +619,80 @@ __global__ void __launch_bounds__(128) row_sum_parts_kernel(const float* __restr
 }
 }  // namespace pfb
 
+// ---------------------------------------------------------------------------
+// Several weighted column sums in one launch (pass F19): out_q[c] =
+// sum_r x_q[r, c] * y[r] for x_q [R, C_q] (any strides), y [R] -- the
+// per-parameter-block bias-gradient sums of a clipped per-example gradient
+// (sum_i s_i g_i, reference tensor.reduce_sum of a product, tensor.py:279-283)
+// that share the clip scales.  A block = 32 columns x 8 row slices of one
+// operand; the 8 slice sums are combined in slice order (deterministic).
+namespace pfb {
+constexpr int kMaxColDots = 8;
+struct ColDots {
+  const float* x[kMaxColDots];
+  int64_t srow[kMaxColDots], scol[kMaxColDots];
+  float* out[kMaxColDots];
+  int64_t ncol[kMaxColDots];
+  int64_t tile0[kMaxColDots + 1];  // first 32-column tile of operand q
+};
+
+__global__ void __launch_bounds__(256) col_dots_kernel(ColDots D, int q, int64_t R,
+                                                       const float* y, int64_t sy) {
+  pdl_enter();
+  __shared__ float red[8][33];
+  const int64_t tile = blockIdx.x;
+  int o = 0;
+  while (o + 1 < q && tile >= D.tile0[o + 1]) ++o;
+  const int64_t c = (tile - D.tile0[o]) * 32 + (threadIdx.x & 31);
+  const int slice = threadIdx.x >> 5;
+  float acc = 0.f;
+  if (c < D.ncol[o]) {
+    const float* xp = D.x[o] + c * D.scol[o];
+    for (int64_t r = slice; r < R; r += 8) acc = fmaf(__ldg(xp + r * D.srow[o]), __ldg(y + r * sy), acc);
+  }
+  red[slice][threadIdx.x & 31] = acc;
+  __syncthreads();
+  if (threadIdx.x < 32 && c < D.ncol[o]) {
+    float t = red[0][threadIdx.x];
+#pragma unroll
+    for (int k = 1; k < 8; ++k) t += red[k][threadIdx.x];
+    D.out[o][c] = t;
+  }
+}
+}  // namespace pfb
+
+extern "C" int pfb_col_dots(int32_t q, const pfb_tensor* xs, const pfb_tensor* y, pfb_tensor* outs,
+                            void* stream) {
+  using namespace pfb;
+  if (q < 1 || q > kMaxColDots) return PFB_E_ARG;
+  if (y->dtype != PFB_F32) return PFB_E_DTYPE;
+  // y: [R] or [R, 1] (any row stride)
+  if (y->rank < 1 || y->rank > 2 || (y->rank == 2 && y->shape[1] != 1)) return PFB_E_SHAPE;
+  const int64_t R = y->shape[0], sy = y->stride[0];
+  ColDots D = {};
+  int64_t tiles = 0;
+  for (int k = 0; k < q; ++k) {
+    const pfb_tensor& x = xs[k];
+    const pfb_tensor& o = outs[k];
+    if (x.dtype != PFB_F32 || o.dtype != PFB_F32) return PFB_E_DTYPE;
+    if (x.rank != 2 || x.shape[0] != R || o.rank != 1 || o.shape[0] != x.shape[1] ||
+        (o.shape[0] > 1 && o.stride[0] != 1))
+      return PFB_E_SHAPE;
+    D.x[k] = (const float*)x.data;
+    D.srow[k] = x.stride[0];
+    D.scol[k] = x.stride[1];
+    D.out[k] = (float*)o.data;
+    D.ncol[k] = x.shape[1];
+    D.tile0[k] = tiles;
+    tiles += (x.shape[1] + 31) / 32;
+  }
+  D.tile0[q] = tiles;
+  if (tiles == 0) return 0;
+  launch(col_dots_kernel, (unsigned)tiles, 256, 0, as_stream(stream), D, (int)q, R,
+         (const float*)y->data, sy);
+  return launch_status();
+}
+
 extern "C" int pfb_row_sum_parts(const pfb_tensor* x, int32_t parts, int64_t part_stride,
                                  pfb_tensor* out, void* stream) {
   using namespace pfb;

@@ -2187,6 +2187,32 @@ def _h_reduce_dot(ex, node, ins):
     return [out]
 
 
+def _h_reduce_dot_many(ex, node, ins):
+    """reduce_dot_many (pass F19): weighted column sums of several operands
+    sharing the weights in one launch (pfb_col_dots); other layouts run one
+    reduce_dot per operand."""
+    y = ex._dev(ins[0])
+    xs = [ex._dev(v) for v in ins[1:]]
+    outs = [ex._empty((x.shape[1],), x.dtype) for x in xs] \
+        if all(x.rank == 2 for x in xs) else None
+    ok = outs is not None and y.dtype == DType.F64 and all(x.dtype == DType.F64 for x in xs) and \
+        tuple(normalize_axes(node.attrs["axes"], 2)) == (0,) and y.rank in (1, 2)
+    if ok:
+        status = []
+
+        def many(*args):  # PFB_E_SHAPE etc. -> per-operand reduce_dot below
+            rc = ex._lib.pfb_col_dots(*args)
+            status.append(rc)
+            return 0
+        q = len(xs)
+        ex._call(many, q, (N.PfbTensor * q)(*[x.desc() for x in xs]), y.desc(),
+                 (N.PfbTensor * q)(*[o.desc() for o in outs]), ex._stream, what="reduce_dot",
+                 work=(_abytes(*xs, y, *outs), 0))
+        if status[-1] == 0:
+            return outs
+    return [_h_reduce_dot(ex, node, [x, ins[0]])[0] for x in ins[1:]]
+
+
 def _h_select(ex, node, ins):
     m, a, b = (ex._dev(v) for v in ins)
     if m.dtype != DType.BOOL:
@@ -2252,7 +2278,7 @@ _HANDLERS.update({
     "matmul2": _h_matmul2,
     "fused_int": _h_fused_int,
     "gather_rows": _h_gather, "gather_stacked": _h_gather_stacked,
-    "gather_stacked_many": _h_gather_stacked_many, "scatter_rows": _h_scatter_rows,
+    "gather_stacked_many": _h_gather_stacked_many, "reduce_dot_many": _h_reduce_dot_many, "scatter_rows": _h_scatter_rows,
     "scatter_add_rows": _h_scatter_add, "reshape": _h_reshape, "transpose": _h_transpose,
     "slice_leading": _h_slice_leading, "tile_leading": _h_tile_leading,
     "where_true": _h_where_true, "complement": _h_complement, "dim0": _h_dim0,

@@ -989,7 +989,7 @@ def _pipeline(elementwise):
            fuse_reductions, fuse_row_dots, fuse_dual_matmuls, fuse_matmul_epilogues]
     if elementwise:
         seq += [sink_unit_reshapes, fuse_elementwise, place_concats, fuse_row_sums]
-    seq += [merge_sibling_gathers]
+    seq += [merge_sibling_gathers, merge_sibling_reduce_dots]
     return seq
 
 
@@ -2044,3 +2044,45 @@ def _with_post_ops(node, k, post):
     if len(prog) > MAX_STEPS:
         return None
     return tuple(prog)
+
+
+# ----------------------------------------------------------------------------
+# F19: sibling weighted column sums sharing the weights become one launch
+#
+# DP-SGD's clipped bias-gradient sums, sum_i s_i g_i for every parameter block
+# (reduce_dot(g_block, s, axes=(0,)), F4), share the clip scales s: one
+# reduce_dot_many node (pfb_col_dots, one kernel over all blocks' columns).
+
+def merge_sibling_reduce_dots(g, keep=(), max_q=8):
+    """F19 in place on `g` (a private copy).  Returns (count, moved outputs)."""
+    from .tensor import DType, normalize_axes
+    rw = _Rewriter(g, keep)
+    rw.replaced = {}
+    live = live_set(g, keep)
+    groups = {}
+    for node in g.topo_order():
+        if node.id not in live or node.kind != "reduce_dot":
+            continue
+        sx, sy = g.ref_shape(node.inputs[0]), g.ref_shape(node.inputs[1])
+        if sx is None or sy is None or len(sx) != 2 or None in sx or sx[0] < 2:
+            continue
+        if tuple(normalize_axes(node.attrs["axes"], 2)) != (0,) or node.out_dtypes[0] != DType.F64:
+            continue
+        if tuple(sy) not in ((sx[0],), (sx[0], 1)):
+            continue
+        groups.setdefault(tuple(node.inputs[1]), []).append(node)
+    count = 0
+    for y, nodes in groups.items():
+        nodes = nodes[:max_q]
+        if len(nodes) < 2:
+            continue
+        ids = {n.id for n in nodes}
+        if any(_ancestors(g, tuple(n.inputs[0]), m) for n in nodes for m in ids):
+            continue
+        new = g.add_node("reduce_dot_many", [y] + [tuple(n.inputs[0]) for n in nodes],
+                         {"axes": (0,)})
+        for k, n in enumerate(nodes):
+            rw.redirect((n.id, 0), Ref(g, new.id, k))
+        count += 1
+    g._topo_cache = None
+    return count, rw.replaced

@@ -284,3 +284,26 @@ def test_fused_row_sum_of_exp_is_softmax(env, rows, W):
     torch.cuda.synchronize()
     e = np.exp(z.astype(np.float64))
     np.testing.assert_allclose(out.to_numpy(), e / e.sum(axis=2, keepdims=True), rtol=1e-5, atol=1e-7)
+
+
+def test_col_dots_many_operands(env):
+    """pfb_col_dots (pass F19): weighted column sums of several operands with
+    one weight vector (strided and transposed views included), against f64."""
+    torch, lib, DArray, DType = env
+    from paper_1903_04243_b200 import _native as N
+    dev = torch.device("cuda")
+    r = np.random.default_rng(7)
+    R = 128
+    y = r.standard_normal(R).astype(np.float32)
+    xs = [r.standard_normal((R, c)).astype(np.float32) for c in (256, 10, 33)]
+    Y = DArray.from_numpy(y.reshape(R, 1), DType.F64, dev)
+    X = [DArray.from_numpy(x, DType.F64, dev) for x in xs[:2]]
+    xt = DArray.from_numpy(xs[2].T.copy(), DType.F64, dev)  # a transposed view
+    X.append(xt.view((R, 33), (1, R)))
+    O = [DArray.empty((x.shape[1],), DType.F64, dev) for x in xs]
+    assert lib.pfb_col_dots(3, (N.PfbTensor * 3)(*[x.desc() for x in X]), Y.desc(),
+                            (N.PfbTensor * 3)(*[o.desc() for o in O]), None) == 0
+    torch.cuda.synchronize()
+    for x, o in zip(xs, O):
+        np.testing.assert_allclose(o.to_numpy(), (x.astype(np.float64) * y[:, None]).sum(0),
+                                   rtol=RTOL, atol=ATOL)

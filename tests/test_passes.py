@@ -467,3 +467,14 @@ def test_f16_softmax_exp_and_division_move_into_the_group():
     assert "exp" not in kinds and "div" not in kinds, kinds
     ents = [e for n in nodes if n.attrs.get("rowsum") for e in n.attrs["rowsum"]]
     assert any(len(e) == 3 and e[2] == 16 + passes._UN_CODE["exp"] for e in ents), ents
+
+
+def test_f19_clipped_bias_sums_share_one_launch():
+    """cfg2 (mlp): the two clipped bias-gradient sums (reduce_dot with the
+    shared clip scales) become one reduce_dot_many node; values unchanged."""
+    from paper_1903_04243_b200 import passes
+    w = WL.cfg2(WL.this_api(), n=4, model="mlp")
+    g, g2, m = _run_both(w)
+    live = passes.live_set(g2, [m[tuple(o)] for o in g.outputs])
+    kinds = [g2.nodes[i].kind for i in live]
+    assert "reduce_dot" not in kinds and kinds.count("reduce_dot_many") == 1, kinds
