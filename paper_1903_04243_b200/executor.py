@@ -470,6 +470,15 @@ class Executor:
         ptrs = tuple((k, feeds[k].data_ptr()) for k in sorted(feeds) if _direct_feed(feeds[k], self.device))
         if not ptrs or not self.zero_copy_feeds:
             return base
+        # a feed that is (a view of) a result of one of our replays lives in a
+        # capture's memory pool, which a replay rewrites: copy it in instead
+        for cap in self._captures.values():
+            for o in cap.outputs:
+                if isinstance(o, DArray):
+                    lo = o.buf.data_ptr()
+                    hi = lo + o.buf.numel() * o.buf.element_size()
+                    if any(lo <= p < hi for _, p in ptrs):
+                        return base
         psig = base + (ptrs,)
         if psig in self._captures:
             return psig
