@@ -280,7 +280,11 @@ def test_fused_row_sum_of_exp_is_softmax(env, rows, W):
     ins = (N.PfbTensor * 2)(Z.desc(), rs.desc())
     outs = (N.PfbTensor * 1)(out.desc())
     regs = (ctypes.c_int32 * 1)(2)
-    assert lib.pfb_fused_ew_rows(2, ins, None, rsum, 4, flat, 1, regs, outs, None) == 0
+    rc = lib.pfb_fused_ew_rows(2, ins, None, rsum, 4, flat, 1, regs, outs, None)
+    if W == 1:  # a one-element row collapses into the outer dims: declined (the
+        assert rc == N.E_UNSUPPORTED  # executor then materialises the sums)
+        return
+    assert rc == 0
     torch.cuda.synchronize()
     e = np.exp(z.astype(np.float64))
     np.testing.assert_allclose(out.to_numpy(), e / e.sum(axis=2, keepdims=True), rtol=1e-5, atol=1e-7)
